@@ -1,0 +1,30 @@
+"""Shared test helpers: rebuild nets/configs from golden fixtures."""
+from types import SimpleNamespace
+
+import numpy as np
+
+from paper_2208_04448_b200.model import Activation, FourierFeatures, MlpParams
+
+ACTS = ["relu", "tanh", "sine"]
+HEADS = ["linear", "logits", "binary"]
+LOSSES = ["mse", "ce", "bce"]
+
+
+def net_from_fixture(z, q):
+    cfg = z[q + "cfg"]
+    hidden = list(z[q + "hidden"])
+    nl = len(hidden) + 1
+    layers = [(z[q + f"w{i}"].copy(), z[q + f"b{i}"].copy()) for i in range(nl)]
+    act = Activation(ACTS[int(cfg[0])], float(cfg[1]))
+    ff = FourierFeatures(int(cfg[2]), float(cfg[6]) if len(cfg) == 7 else 5.0, int(cfg[5]))
+    return MlpParams(layers, act, HEADS[int(cfg[4])]), ff
+
+
+def tiny_cfg(**kw):
+    base = dict(subdomain_size=512, l1_net=(2, 8), tile_net=None, l0_net=(2, 16),
+                voxel_net=(2, 16), activation="sine", frequency=3.0, ffm_scale=5.0,
+                ffm_size=16, lr=1e-3, refine_lr=None, decay=0.975, interval=100.0,
+                max_epochs=40, sample_interval=1, batch_size=4096,
+                significance_threshold=None, strict_topology=False, seed=11)
+    base.update(kw)
+    return SimpleNamespace(**base)

@@ -1,0 +1,155 @@
+/*
+ * nvdb_b200.h -- C ABI of the B200-native NeuralVDB hot path.
+ *
+ * Plain pointers and sizes only; every compute entry point takes a
+ * cudaStream_t (as void*) and DEVICE pointers owned by the caller.  The
+ * library never frees caller memory; the two handle types (netset, tree)
+ * are library-owned, immutable after create and destroyed explicitly.
+ *
+ * Return value: 0 on success, a negative NVDB_E* code otherwise; the
+ * message is available from nvdb_last_error() (thread-local).  No C++
+ * exception crosses this boundary.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/svcodec/).
+ */
+#ifndef NVDB_B200_H
+#define NVDB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define NVDB_API __attribute__((visibility("default")))
+#else
+#define NVDB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NVDB_OK 0
+#define NVDB_EINVAL (-1)      /* bad argument  -> ValueError            */
+#define NVDB_ECUDA (-2)       /* CUDA failure  -> RuntimeError          */
+#define NVDB_EUNSUPPORTED (-3)/* shape not supported by this build       */
+#define NVDB_ECORRUPT (-4)    /* inconsistent container -> SvcodecError */
+#define NVDB_ENOMEM (-5)      /* workspace too small                     */
+
+/* activation / head / net tag codes (neural.py:24-30, encoder.py:86) */
+#define NVDB_ACT_RELU 0
+#define NVDB_ACT_TANH 1
+#define NVDB_ACT_SINE 2
+#define NVDB_HEAD_LINEAR 0
+#define NVDB_HEAD_LOGITS 1
+#define NVDB_HEAD_BINARY 2
+#define NVDB_TAG_L1 0
+#define NVDB_TAG_TILE 1
+#define NVDB_TAG_L0 2
+#define NVDB_TAG_VOXEL 3
+
+/* One coordinate network (MlpParams + FourierFeatures, neural.py:51-165).
+ * HOST pointers; weights are the serialized (interleaved-feature) layout. */
+typedef struct {
+  int32_t m;           /* Fourier feature count (in_dim = 2m)          */
+  int32_t depth;       /* hidden layers                                 */
+  int32_t width;       /* hidden width                                  */
+  int32_t out_dim;     /* 1 or 3                                        */
+  int32_t activation;  /* NVDB_ACT_*                                    */
+  int32_t head;        /* NVDB_HEAD_*                                   */
+  float frequency;     /* sine frequency (omega)                        */
+  float amplitude;     /* feature amplitude                             */
+  const float* b2pi;   /* (3, m) float32 = (2*pi*B^T).astype(float32)   */
+  const float* const* weights; /* depth+1 arrays W_l (out, in) row-major */
+  const float* const* biases;  /* depth+1 arrays b_l (out,)              */
+} nvdb_net_desc;
+
+/* One subdomain expert (EncodedSubdomain, container.py:118-150). */
+typedef struct {
+  int32_t cell[3];
+  int32_t net_index[4];   /* per tag l1/tile/l0/voxel: index into nets[] or -1 */
+  double norm_origin[3];
+  double norm_scale;
+} nvdb_expert_desc;
+
+typedef struct nvdb_netset nvdb_netset;
+typedef struct nvdb_tree nvdb_tree;
+
+NVDB_API const char* nvdb_last_error(void);
+NVDB_API int nvdb_version(void);
+
+/* -- networks ------------------------------------------------------------- */
+
+/* Upload every expert's nets (replaces the per-call weight handling of
+ * inference.eval_net, inference.py:23-26). */
+NVDB_API int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts,
+                       int32_t nexperts, int32_t subdomain_size, int32_t halo, nvdb_netset** out);
+NVDB_API int nvdb_netset_destroy(nvdb_netset* ns);
+
+/* neural.forward_block (neural.py:527-550): raw outputs of net `net` at n
+ * normalized float32 points pts (n,3); out (n, out_dim) float32. */
+NVDB_API int nvdb_forward(const nvdb_netset* ns, int32_t net, const float* pts, int64_t n, float* out,
+                 void* stream);
+
+/* Workspace bytes needed by nvdb_eval_blended for n points. */
+NVDB_API size_t nvdb_eval_workspace_bytes(const nvdb_netset* ns, int64_t n);
+
+/* inference.blended_l1_probs / blended_l0_probs / blended_values
+ * (inference.py:39-84, partition.py:180-256): gate-blended outputs at n
+ * float64 index-space centres (n,3).  out (n, k) float64 (k = 3 for the l1
+ * tag, else 1); covered (n,) uint8. */
+NVDB_API int nvdb_eval_blended(const nvdb_netset* ns, int32_t tag, const double* centers, int64_t n,
+                      double* out, uint8_t* covered, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
+/* -- upper-tree lookup ----------------------------------------------------- */
+
+/* Flattened [Hash,5,4,3] tree (grid.py:248-390).  HOST arrays:
+ *   root keys (nr,3) + per root: l2 node index or -1, tile value, tile active
+ *   l2 nodes (n2): origin (n2,3); child/active bit words (n2, 512) uint64;
+ *                  tiles (n2, 32768) float32
+ *   l1 nodes (n1): origin (n1,3); child/active (n1, 64) uint64; tiles (n1, 4096)
+ *   leaves  (nl): active (nl, 8) uint64; values (nl, 512) float32
+ * Children are implied by mask order: the k-th set child bit of l2 node i is
+ * l1 node l2_child_base[i] + k, likewise l1 -> leaves. */
+typedef struct {
+  float background;
+  int32_t nroots, n2, n1, nl;
+  const int32_t* root_keys;        /* (nroots,3) */
+  const int32_t* root_l2;          /* (nroots) l2 index or -1 (tile) */
+  const float* root_tile_value;    /* (nroots) */
+  const uint8_t* root_tile_active; /* (nroots) */
+  const uint64_t* l2_child;        /* (n2,512) */
+  const uint64_t* l2_active;       /* (n2,512) */
+  const float* l2_tiles;           /* (n2,32768) */
+  const int32_t* l2_child_base;    /* (n2) */
+  const uint64_t* l1_child;        /* (n1,64) */
+  const uint64_t* l1_active;       /* (n1,64) */
+  const float* l1_tiles;           /* (n1,4096) */
+  const int32_t* l1_child_base;    /* (n1) */
+  const uint64_t* leaf_active;     /* (nl,8) */
+  const float* leaf_values;        /* (nl,512) */
+} nvdb_tree_desc;
+
+NVDB_API int nvdb_tree_create(const nvdb_tree_desc* desc, nvdb_tree** out);
+NVDB_API int nvdb_tree_destroy(nvdb_tree* tree);
+
+/* VdbGrid.get_values(coords, with_kind=True) (grid.py:310-390): device
+ * int32 coords (n,3) -> value f32, active u8, kind u8 (0 none,1 tile,2 leaf);
+ * leaf (n) int32 leaf index or -1 (nullable). */
+NVDB_API int nvdb_lookup(const nvdb_tree* tree, const int32_t* coords, int64_t n, float* value, uint8_t* active,
+                uint8_t* kind, int32_t* leaf, void* stream);
+
+/* -- diagnostics ------------------------------------------------------------ */
+
+/* One 128xN tcgen05 MMA over nk K-steps from caller-laid-out shared-memory
+ * images (used by the descriptor-layout unit tests). Device pointers. */
+NVDB_API int nvdb_selftest_umma(const void* a_img, uint32_t a_bytes, const void* b_img, uint32_t b_bytes,
+                       int32_t n, int32_t nk, uint32_t a_lbo, uint32_t a_sbo, uint32_t a_step,
+                       uint32_t b_lbo, uint32_t b_sbo, uint32_t b_step, int32_t a_mn, int32_t b_mn,
+                       float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NVDB_B200_H */

@@ -1,0 +1,110 @@
+"""ctypes binding of the C ABI in ``include/nvdb_b200.h``.
+
+The shared library is built in-tree (``csrc/Makefile`` -> ``libnvdb_b200.so``
+next to this file).  There is no CPU fallback: if the library or a CUDA
+device is missing, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+from .errors import SvcodecError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnvdb_b200.so")
+
+NVDB_OK = 0
+NVDB_EINVAL = -1
+NVDB_ECUDA = -2
+NVDB_EUNSUPPORTED = -3
+NVDB_ECORRUPT = -4
+NVDB_ENOMEM = -5
+
+EXPORTED = [
+    "nvdb_last_error", "nvdb_version", "nvdb_netset_create", "nvdb_netset_destroy",
+    "nvdb_forward", "nvdb_eval_workspace_bytes", "nvdb_eval_blended", "nvdb_tree_create",
+    "nvdb_tree_destroy", "nvdb_lookup", "nvdb_selftest_umma",
+]
+
+
+class NetDesc(C.Structure):
+    _fields_ = [("m", C.c_int32), ("depth", C.c_int32), ("width", C.c_int32),
+                ("out_dim", C.c_int32), ("activation", C.c_int32), ("head", C.c_int32),
+                ("frequency", C.c_float), ("amplitude", C.c_float),
+                ("b2pi", C.POINTER(C.c_float)),
+                ("weights", C.POINTER(C.POINTER(C.c_float))),
+                ("biases", C.POINTER(C.POINTER(C.c_float)))]
+
+
+class ExpertDesc(C.Structure):
+    _fields_ = [("cell", C.c_int32 * 3), ("net_index", C.c_int32 * 4),
+                ("norm_origin", C.c_double * 3), ("norm_scale", C.c_double)]
+
+
+class TreeDesc(C.Structure):
+    _fields_ = [("background", C.c_float), ("nroots", C.c_int32), ("n2", C.c_int32),
+                ("n1", C.c_int32), ("nl", C.c_int32),
+                ("root_keys", C.c_void_p), ("root_l2", C.c_void_p),
+                ("root_tile_value", C.c_void_p), ("root_tile_active", C.c_void_p),
+                ("l2_child", C.c_void_p), ("l2_active", C.c_void_p), ("l2_tiles", C.c_void_p),
+                ("l2_child_base", C.c_void_p), ("l1_child", C.c_void_p), ("l1_active", C.c_void_p),
+                ("l1_tiles", C.c_void_p), ("l1_child_base", C.c_void_p),
+                ("leaf_active", C.c_void_p), ("leaf_values", C.c_void_p)]
+
+
+_lib: Optional[C.CDLL] = None
+
+
+def _declare(lib: C.CDLL) -> None:
+    vp, i32, i64, u32, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_size_t
+    sig = {
+        "nvdb_last_error": (C.c_char_p, []),
+        "nvdb_version": (C.c_int, []),
+        "nvdb_netset_create": (C.c_int, [C.POINTER(NetDesc), i32, C.POINTER(ExpertDesc), i32, i32, i32,
+                                         C.POINTER(vp)]),
+        "nvdb_netset_destroy": (C.c_int, [vp]),
+        "nvdb_forward": (C.c_int, [vp, i32, vp, i64, vp, vp]),
+        "nvdb_eval_workspace_bytes": (sz, [vp, i64]),
+        "nvdb_eval_blended": (C.c_int, [vp, i32, vp, i64, vp, vp, vp, sz, vp]),
+        "nvdb_tree_create": (C.c_int, [C.POINTER(TreeDesc), C.POINTER(vp)]),
+        "nvdb_tree_destroy": (C.c_int, [vp]),
+        "nvdb_lookup": (C.c_int, [vp, vp, i64, vp, vp, vp, vp, vp]),
+        "nvdb_selftest_umma": (C.c_int, [vp, u32, vp, u32, i32, i32, u32, u32, u32, u32, u32, u32,
+                                         i32, i32, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def lib() -> C.CDLL:
+    """Load the CUDA library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `make -C {os.path.join(HERE, 'csrc')}` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        _lib = C.CDLL(LIB_PATH)
+        _declare(_lib)
+    return _lib
+
+
+class NvdbError(RuntimeError):
+    """CUDA or unsupported-shape failure reported by the C ABI."""
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == NVDB_OK:
+        return
+    msg = lib().nvdb_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == NVDB_EINVAL:
+        raise ValueError(text)
+    if rc == NVDB_ECORRUPT:
+        raise SvcodecError(text)
+    raise NvdbError(f"[{rc}] {text}")

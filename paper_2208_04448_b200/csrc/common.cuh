@@ -1,0 +1,58 @@
+// Host-side helpers shared by the C-ABI translation units: thread-local error
+// reporting and CUDA error checks.  No C++ exception crosses the ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/nvdb_b200.h"
+
+namespace nvdb {
+
+inline std::string& last_error_slot() {
+  static thread_local std::string msg;
+  return msg;
+}
+
+inline int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  last_error_slot() = buf;
+  return code;
+}
+
+#define NVDB_CUDA_TRY(expr)                                                                          \
+  do {                                                                                               \
+    cudaError_t _e = (expr);                                                                         \
+    if (_e != cudaSuccess)                                                                           \
+      return ::nvdb::fail(NVDB_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                          __LINE__);                                                                 \
+  } while (0)
+
+#define NVDB_CHECK_LAUNCH()                                                                 \
+  do {                                                                                      \
+    cudaError_t _e = cudaGetLastError();                                                    \
+    if (_e != cudaSuccess)                                                                  \
+      return ::nvdb::fail(NVDB_ECUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), \
+                          __FILE__, __LINE__);                                              \
+  } while (0)
+
+inline int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace nvdb

@@ -1,0 +1,524 @@
+// Netset upload, the forward_block seam and the generic gate-blended
+// evaluation driver (inference.py:39-84, partition.py:160-256).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "netset.cuh"
+
+using namespace nvdb;
+
+namespace {
+
+uint16_t f2h_bits(float f) {
+  __half h = __float2half_rn(f);
+  uint16_t b;
+  std::memcpy(&b, &h, 2);
+  return b;
+}
+
+int round_up_i(int v, int a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" const char* nvdb_last_error(void) { return last_error_slot().c_str(); }
+extern "C" int nvdb_version(void) { return 1; }
+
+// ---------------------------------------------------------------------------
+// netset
+// ---------------------------------------------------------------------------
+extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts,
+                                  int32_t nexperts, int32_t subdomain_size, int32_t halo, nvdb_netset** out) {
+  if (!out || (nnets > 0 && !nets) || nexperts < 0 || (nexperts > 0 && !experts))
+    return fail(NVDB_EINVAL, "nvdb_netset_create: null argument");
+  if (subdomain_size <= 0 || subdomain_size % 512 || halo <= 0)
+    return fail(NVDB_EINVAL, "bad subdomain size %d / halo %d", subdomain_size, halo);
+  *out = nullptr;
+  // ---- host packing: one blob, every piece 256-byte aligned
+  struct Piece {
+    size_t wimg, bias, headw, headb, b2pi;
+  };
+  std::vector<Piece> pieces(nnets);
+  std::vector<NetDev> hnets(nnets);
+  size_t total = 0;
+  auto take = [&](size_t bytes) {
+    size_t off = total;
+    total = align_up(total + bytes, 256);
+    return off;
+  };
+  uint32_t max_wimg = 0;
+  int max_width = 16;
+  for (int i = 0; i < nnets; ++i) {
+    const nvdb_net_desc& d = nets[i];
+    if (d.m < 1 || d.depth < 1 || d.width < 1 || (d.out_dim != 1 && d.out_dim != 3))
+      return fail(NVDB_EINVAL, "net %d: bad dims m=%d depth=%d width=%d out=%d", i, d.m, d.depth, d.width,
+                  d.out_dim);
+    if (d.head == NVDB_HEAD_LOGITS && d.out_dim != 3)
+      return fail(NVDB_EUNSUPPORTED, "net %d: logits head must be 3 wide", i);
+    const int W = round_up_i(d.width, 16);
+    const int k0 = round_up_i(2 * d.m, kChunkK);
+    if (W > 256 || d.depth > 4 || k0 > 1024)
+      return fail(NVDB_EUNSUPPORTED, "net %d: width %d depth %d 2m %d exceeds this build (<=256, <=4, <=1024)",
+                  i, d.width, d.depth, 2 * d.m);
+    NetDev& nd = hnets[i];
+    nd.k0 = k0;
+    nd.width = W;
+    nd.depth = d.depth;
+    nd.out_dim = d.out_dim;
+    nd.act = d.activation;
+    nd.head = d.head;
+    nd.expert = 0;
+    nd.wimg_bytes = (uint32_t)align_up((size_t)2 * ((size_t)W * k0 + (size_t)(d.depth - 1) * W * W), 16);
+    max_wimg = std::max(max_wimg, nd.wimg_bytes);
+    max_width = std::max(max_width, W);
+    pieces[i].wimg = take(nd.wimg_bytes);
+    pieces[i].bias = take(sizeof(float) * d.depth * W);
+    pieces[i].headw = take(sizeof(float) * d.out_dim * W);
+    pieces[i].headb = take(sizeof(float) * 4);
+    pieces[i].b2pi = take(sizeof(float) * 3 * (k0 / 2));
+  }
+  SmemPlan plan = plan_smem(max_wimg, max_width);
+  if (plan.total > kMaxDynSmem)
+    return fail(NVDB_EUNSUPPORTED, "nets need %u B of shared memory (> %u); weight streaming not built", plan.total,
+                kMaxDynSmem);
+  std::vector<uint8_t> blob(std::max<size_t>(total, 256), 0);
+  for (int i = 0; i < nnets; ++i) {
+    const nvdb_net_desc& d = nets[i];
+    const NetDev& nd = hnets[i];
+    const int W = nd.width, k0 = nd.k0, m = d.m;
+    const bool sine = d.activation == NVDB_ACT_SINE;
+    const float om = sine ? d.frequency : 1.0f;
+    uint16_t* wimg = reinterpret_cast<uint16_t*>(blob.data() + pieces[i].wimg);
+    // layer 0: B operand (N = W rows, K = k0), serialized interleaved feature order;
+    // amplitude and omega folded in before rounding to fp16
+    for (int n = 0; n < d.width; ++n)
+      for (int k = 0; k < 2 * m; ++k) {
+        const float w = d.weights[0][(size_t)n * 2 * m + k] * d.amplitude * om;
+        wimg[kmajor_offset(n, k, W) / 2] = f2h_bits(w);
+      }
+    size_t base = (size_t)W * k0;
+    for (int l = 1; l < d.depth; ++l) {
+      for (int n = 0; n < d.width; ++n)
+        for (int k = 0; k < d.width; ++k)
+          wimg[base + kmajor_offset(n, k, W) / 2] = f2h_bits(d.weights[l][(size_t)n * d.width + k] * om);
+      base += (size_t)W * W;
+    }
+    float* bias = reinterpret_cast<float*>(blob.data() + pieces[i].bias);
+    for (int l = 0; l < d.depth; ++l)
+      for (int n = 0; n < d.width; ++n) bias[l * W + n] = d.biases[l][n] * om;
+    float* hw = reinterpret_cast<float*>(blob.data() + pieces[i].headw);
+    for (int k = 0; k < d.out_dim; ++k)
+      for (int n = 0; n < d.width; ++n) hw[k * W + n] = d.weights[d.depth][(size_t)k * d.width + n];
+    float* hb = reinterpret_cast<float*>(blob.data() + pieces[i].headb);
+    for (int k = 0; k < d.out_dim; ++k) hb[k] = d.biases[d.depth][k];
+    float* b2 = reinterpret_cast<float*>(blob.data() + pieces[i].b2pi);
+    for (int ax = 0; ax < 3; ++ax)
+      for (int f = 0; f < m; ++f) b2[ax * (k0 / 2) + f] = d.b2pi[ax * m + f];
+  }
+  // ---- experts: sorted by cell (sid order), tag -> net
+  std::vector<ExpertDev> hexp(nexperts);
+  std::vector<int32_t> cells(3 * std::max(nexperts, 1)), tagnet(4 * std::max(nexperts, 1), -1);
+  for (int e = 0; e < nexperts; ++e) {
+    const nvdb_expert_desc& x = experts[e];
+    if (e > 0) {
+      const int* p = experts[e - 1].cell;
+      if (!(std::lexicographical_compare(p, p + 3, x.cell, x.cell + 3)))
+        return fail(NVDB_EINVAL, "experts must be in ascending cell (sid) order");
+    }
+    if (!(x.norm_scale > 0)) return fail(NVDB_EINVAL, "expert %d: norm_scale must be > 0", e);
+    for (int i = 0; i < 3; ++i) {
+      hexp[e].norm_origin[i] = x.norm_origin[i];
+      hexp[e].cell[i] = x.cell[i];
+      cells[3 * e + i] = x.cell[i];
+    }
+    hexp[e].norm_scale = x.norm_scale;
+    for (int t = 0; t < 4; ++t) {
+      const int ni = x.net_index[t];
+      if (ni >= nnets) return fail(NVDB_EINVAL, "expert %d: net index %d out of range", e, ni);
+      tagnet[4 * e + t] = ni;
+      if (ni >= 0) hnets[ni].expert = e;
+    }
+  }
+  nvdb_netset* ns = new nvdb_netset();
+  ns->nnets = nnets;
+  ns->nexperts = nexperts;
+  ns->subdomain_size = subdomain_size;
+  ns->halo = halo;
+  ns->max_wimg = max_wimg;
+  ns->max_width = max_width;
+  auto cleanup = [&](int code) {
+    nvdb_netset_destroy(ns);
+    return code;
+  };
+  if (cudaMalloc(&ns->dev_blob, blob.size()) != cudaSuccess) return cleanup(fail(NVDB_ECUDA, "cudaMalloc blob"));
+  if (cudaMemcpy(ns->dev_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return cleanup(fail(NVDB_ECUDA, "upload blob"));
+  for (int i = 0; i < nnets; ++i) {
+    hnets[i].wimg = ns->dev_blob + pieces[i].wimg;
+    hnets[i].bias = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].bias);
+    hnets[i].headw = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].headw);
+    hnets[i].headb = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].headb);
+    hnets[i].b2pi = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].b2pi);
+  }
+  if (cudaMalloc(&ns->dev_nets, sizeof(NetDev) * std::max(nnets, 1)) != cudaSuccess ||
+      cudaMalloc(&ns->dev_experts, sizeof(ExpertDev) * std::max(nexperts, 1)) != cudaSuccess ||
+      cudaMalloc(&ns->dev_cells, sizeof(int32_t) * cells.size()) != cudaSuccess ||
+      cudaMalloc(&ns->dev_tagnet, sizeof(int32_t) * tagnet.size()) != cudaSuccess)
+    return cleanup(fail(NVDB_ECUDA, "cudaMalloc netset tables"));
+  if ((nnets && cudaMemcpy(ns->dev_nets, hnets.data(), sizeof(NetDev) * nnets, cudaMemcpyHostToDevice)) ||
+      (nexperts && cudaMemcpy(ns->dev_experts, hexp.data(), sizeof(ExpertDev) * nexperts, cudaMemcpyHostToDevice)) ||
+      cudaMemcpy(ns->dev_cells, cells.data(), sizeof(int32_t) * cells.size(), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(ns->dev_tagnet, tagnet.data(), sizeof(int32_t) * tagnet.size(), cudaMemcpyHostToDevice))
+    return cleanup(fail(NVDB_ECUDA, "upload netset tables"));
+  ns->nets = hnets;
+  ns->experts = hexp;
+  ns->tagnet = tagnet;
+  *out = ns;
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_netset_destroy(nvdb_netset* ns) {
+  if (!ns) return NVDB_OK;
+  cudaFree(ns->dev_blob);
+  cudaFree(ns->dev_nets);
+  cudaFree(ns->dev_experts);
+  cudaFree(ns->dev_cells);
+  cudaFree(ns->dev_tagnet);
+  delete ns;
+  return NVDB_OK;
+}
+
+namespace nvdb {
+
+int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int grid, cudaStream_t st) {
+  const SmemPlan plan = plan_smem(ns->max_wimg, ns->max_width);
+  // at least ~120 KB so only one CTA (which owns all 512 TMEM columns) fits per SM
+  const uint32_t smem = std::max<uint32_t>(plan.total, 120 * 1024);
+  static bool attr_set = false;
+  if (!attr_set) {
+    NVDB_CUDA_TRY(cudaFuncSetAttribute(mlp_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    attr_set = true;
+  }
+  a.nets = ns->dev_nets;
+  a.experts = ns->dev_experts;
+  a.npairs_dev = npairs_dev;
+  a.subdomain_size = ns->subdomain_size;
+  a.halo = ns->halo;
+  a.w_off = plan.w_off;
+  a.region_off = plan.region_off;
+  a.region_bytes = plan.region_bytes;
+  a.small_off = plan.small_off;
+  a.bar_off = plan.bar_off;
+  if (grid <= 0) return NVDB_OK;
+  mlp_eval_kernel<<<grid, kCtaThreads, smem, st>>>(a);
+  NVDB_CHECK_LAUNCH();
+  return NVDB_OK;
+}
+
+}  // namespace nvdb
+
+extern "C" int nvdb_forward(const nvdb_netset* ns, int32_t net, const float* pts, int64_t n, float* out,
+                            void* stream) {
+  if (!ns || net < 0 || net >= ns->nnets) return fail(NVDB_EINVAL, "nvdb_forward: bad netset/net");
+  if (n < 0 || (n > 0 && (!pts || !out))) return fail(NVDB_EINVAL, "nvdb_forward: bad buffers");
+  if (n == 0) return NVDB_OK;
+  MlpArgs a{};
+  a.tiles = nullptr;
+  a.implicit_net = net;
+  a.n_implicit = n;
+  const int64_t ntiles = (n + kTileM - 1) / kTileM;
+  a.npairs = (int32_t)((ntiles + 1) / 2);
+  a.src_kind = SRC_NORM_F32;
+  a.src = pts;
+  a.out_mode = OUT_RAW;
+  a.out_raw = out;
+  const int grid = std::min<int64_t>(a.npairs, num_sms());
+  return launch_mlp(ns, a, nullptr, grid, static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------------------
+// generic blended evaluation
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr uint16_t kNoKey = 0xFFFF;
+
+__device__ int find_cell(const int32_t* cells, int ncell, int cx, int cy, int cz) {
+  int lo = 0, hi = ncell - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int* c = cells + 3 * mid;
+    int cmp = (c[0] != cx) ? (c[0] < cx ? -1 : 1) : (c[1] != cy) ? (c[1] < cy ? -1 : 1) : (c[2] != cz) ? (c[2] < cz ? -1 : 1) : 0;
+    if (cmp == 0) return mid;
+    if (cmp < 0) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ long long floor_div(double v, double s) { return (long long)floor(v / s); }
+
+// Per point and pass: the pass-th candidate expert (in sid order) owning the
+// tag's net with a positive gate weight (partition.py:180-229 keeps w > 0).
+__global__ void k_pass_keys(int src_kind, const void* src, int64_t n, int pass, const int32_t* cells, int ncell,
+                            const int32_t* tagnet, int tag, int S, int halo, uint8_t* ncand, uint16_t* keys,
+                            int64_t* vals, BlendOut o) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double c[3];
+  point_centre(src_kind, src, i, c);
+  const double h = (double)halo;
+  long long lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = floor_div(c[a] - h, (double)S);
+    hi[a] = floor_div(c[a] + h, (double)S);
+  }
+  int found = 0;
+  int key = kNoKey;
+  for (int combo = 0; combo < 8; ++combo) {
+    bool ok = true;
+    int cell[3];
+    for (int a = 0; a < 3; ++a) {
+      const int bit = 4 >> a;
+      if (combo & bit) {
+        ok &= hi[a] != lo[a];
+        cell[a] = (int)hi[a];
+      } else {
+        cell[a] = (int)lo[a];
+      }
+    }
+    if (!ok) continue;
+    const int e = find_cell(cells, ncell, cell[0], cell[1], cell[2]);
+    if (e < 0) continue;
+    const int net = tagnet[4 * e + tag];
+    if (net < 0) continue;
+    if (!(gate_weight(cell, S, halo, c) > 0.0)) continue;
+    if (found == pass) key = net;
+    ++found;
+  }
+  if (pass == 0) {
+    ncand[i] = (uint8_t)found;
+    if (found == 0) {  // uncovered everywhere (inference.py:53-56 -> background)
+      switch (o.out_mode) {
+        case OUT_PROBS: {
+          const int k = (tag == NVDB_TAG_L1) ? 3 : 1;
+          for (int j = 0; j < k; ++j) o.out_probs[i * k + j] = 0.0;
+          o.out_u8[i] = 0;
+          break;
+        }
+        case OUT_L1CLASS: o.out_u8[i] = 2; break;
+        case OUT_L0ACTIVE: o.out_u8[i] = 0; break;
+        case OUT_VALUE: o.out_f32[i] = o.background; break;
+        default: break;
+      }
+    }
+  }
+  keys[i] = (uint16_t)key;
+  vals[i] = i;
+}
+
+// Segments of equal key in the sorted list -> tiles (pairs share a net).
+__global__ void k_build_tiles(const uint16_t* keys, int64_t n, Tile* tiles, int64_t max_tiles, int32_t* npairs) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  int64_t nt = 0;
+  int64_t i = 0;
+  while (i < n && keys[i] != kNoKey) {
+    const uint16_t k = keys[i];
+    int64_t j = i;
+    while (j < n && keys[j] == k) ++j;
+    int64_t len = j - i;
+    int64_t cnt = (len + kTileM - 1) / kTileM;
+    cnt = (cnt + 1) & ~1LL;
+    for (int64_t t = 0; t < cnt && nt < max_tiles; ++t, ++nt) {
+      Tile tl;
+      tl.net = k;
+      tl.first = i + t * kTileM;
+      const int64_t rem = len - t * kTileM;
+      tl.count = (int32_t)(rem < 0 ? 0 : (rem > kTileM ? kTileM : rem));
+      tl.flags = 0;
+      tl.pad = 0;
+      tiles[nt] = tl;
+    }
+    i = j;
+  }
+  *npairs = (int32_t)(nt / 2);
+}
+
+struct WsLayout {
+  size_t ncand, keys_in, keys_out, vals_in, vals_out, tiles, npairs, acc, cub, total;
+  size_t cub_bytes;
+  int64_t max_tiles;
+};
+
+WsLayout ws_layout(const nvdb_netset* ns, int64_t n) {
+  WsLayout w{};
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    size_t o = off;
+    off = align_up(off + b, 256);
+    return o;
+  };
+  w.max_tiles = n / kTileM + 2 * (int64_t)std::max(ns->nnets, 1) + 4;
+  w.ncand = take(n);
+  w.keys_in = take(2 * n);
+  w.keys_out = take(2 * n);
+  w.vals_in = take(8 * n);
+  w.vals_out = take(8 * n);
+  w.tiles = take(sizeof(Tile) * w.max_tiles);
+  w.npairs = take(16);
+  w.acc = take(32 * n);
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint16_t*)nullptr, (uint16_t*)nullptr, (int64_t*)nullptr,
+                                  (int64_t*)nullptr, (int)std::max<int64_t>(n, 1), 0, 16);
+  w.cub_bytes = cub_bytes;
+  w.cub = take(cub_bytes);
+  w.total = off;
+  return w;
+}
+
+}  // namespace
+
+namespace nvdb {
+
+size_t blended_workspace_bytes(const nvdb_netset* ns, int64_t n) { return ws_layout(ns, n).total; }
+
+int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, int64_t n, const BlendOut& o,
+                void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (n <= 0) return NVDB_OK;
+  if (n > (int64_t)INT32_MAX) return fail(NVDB_EUNSUPPORTED, "run_blended: n > 2^31");
+  MlpArgs a{};
+  a.src_kind = src_kind;
+  a.src = src;
+  a.out_mode = o.out_mode;
+  a.out_probs = o.out_probs;
+  a.out_u8 = o.out_u8;
+  a.out_f32 = o.out_f32;
+  a.value_scale = o.value_scale;
+  a.background = o.background;
+  a.clip = o.clip;
+  // fast path: a single expert needs no dispatch (every point has it as its
+  // only candidate; its gate weight decides coverage in the epilogue)
+  if (ns->nexperts == 1 && ns->tagnet[tag] >= 0) {
+    a.tiles = nullptr;
+    a.implicit_net = ns->tagnet[tag];
+    a.n_implicit = n;
+    const int64_t ntiles = (n + kTileM - 1) / kTileM;
+    a.npairs = (int32_t)((ntiles + 1) / 2);
+    return launch_mlp(ns, a, nullptr, (int)std::min<int64_t>(a.npairs, num_sms()), st);
+  }
+  const WsLayout w = ws_layout(ns, n);
+  if (!ws || ws_bytes < w.total) return fail(NVDB_ENOMEM, "blended workspace %zu < %zu", ws_bytes, w.total);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint8_t* ncand = base + w.ncand;
+  uint16_t* kin = reinterpret_cast<uint16_t*>(base + w.keys_in);
+  uint16_t* kout = reinterpret_cast<uint16_t*>(base + w.keys_out);
+  int64_t* vin = reinterpret_cast<int64_t*>(base + w.vals_in);
+  int64_t* vout = reinterpret_cast<int64_t*>(base + w.vals_out);
+  Tile* tiles = reinterpret_cast<Tile*>(base + w.tiles);
+  int32_t* npairs = reinterpret_cast<int32_t*>(base + w.npairs);
+  a.acc = reinterpret_cast<double*>(base + w.acc);
+  a.ncand = ncand;
+  a.tiles = tiles;
+  a.idx = vout;
+  const int threads = 256;
+  const int blocks = (int)((n + threads - 1) / threads);
+  for (int pass = 0; pass < 8; ++pass) {
+    k_pass_keys<<<blocks, threads, 0, st>>>(src_kind, src, n, pass, ns->dev_cells, ns->nexperts, ns->dev_tagnet,
+                                            tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o);
+    NVDB_CHECK_LAUNCH();
+    size_t cb = w.cub_bytes;
+    NVDB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(base + w.cub, cb, kin, kout, vin, vout, (int)n, 0, 16, st));
+    k_build_tiles<<<1, 1, 0, st>>>(kout, n, tiles, w.max_tiles, npairs);
+    NVDB_CHECK_LAUNCH();
+    a.pass = pass;
+    int rc = launch_mlp(ns, a, npairs, num_sms(), st);
+    if (rc) return rc;
+  }
+  return NVDB_OK;
+}
+
+}  // namespace nvdb
+
+extern "C" size_t nvdb_eval_workspace_bytes(const nvdb_netset* ns, int64_t n) {
+  return ns ? blended_workspace_bytes(ns, n) : 0;
+}
+
+extern "C" int nvdb_eval_blended(const nvdb_netset* ns, int32_t tag, const double* centers, int64_t n, double* out,
+                                 uint8_t* covered, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!ns || tag < 0 || tag > 3) return fail(NVDB_EINVAL, "nvdb_eval_blended: bad netset/tag");
+  if (n < 0 || (n > 0 && (!centers || !out || !covered))) return fail(NVDB_EINVAL, "nvdb_eval_blended: bad buffers");
+  BlendOut o{};
+  o.out_mode = OUT_PROBS;
+  o.out_probs = out;
+  o.out_u8 = covered;
+  return run_blended(ns, tag, SRC_CENTER_F64, centers, n, o, workspace, workspace_bytes,
+                     static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------------------
+// descriptor self-test: one 128xN MMA from caller-laid-out smem images
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void k_selftest_umma(const uint8_t* a_img, uint32_t a_bytes, const uint8_t* b_img, uint32_t b_bytes,
+                                int n, int nk, uint32_t a_lbo, uint32_t a_sbo, uint32_t a_step, uint32_t b_lbo,
+                                uint32_t b_sbo, uint32_t b_step, int a_mn, int b_mn, float* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint8_t* sa = sm;
+  uint8_t* sb = sm + ((a_bytes + 1023u) & ~1023u);
+  for (uint32_t i = threadIdx.x; i < a_bytes; i += blockDim.x) sa[i] = a_img[i];
+  for (uint32_t i = threadIdx.x; i < b_bytes; i += blockDim.x) sb[i] = b_img[i];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&tslot, 256);
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_f16(128, n, a_mn, b_mn);
+    for (int s = 0; s < nk; ++s) {
+      const uint64_t ad = smem_desc(smem_addr(sa) + s * a_step, a_lbo, a_sbo);
+      const uint64_t bd = smem_desc(smem_addr(sb) + s * b_step, b_lbo, b_sbo);
+      umma_f16(tm, ad, bd, idesc, s != 0);
+    }
+    umma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  const int warp = threadIdx.x >> 5;
+  const int row = threadIdx.x;
+  for (int c = 0; c < n; c += 16) {
+    float v[16];
+    tmem_ld16(tm + ((uint32_t)(warp * 32) << 16) + c, v);
+    tmem_ld_wait();
+    for (int i = 0; i < 16; ++i) out[row * n + c + i] = v[i];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tm, 256);
+}
+
+}  // namespace
+
+extern "C" int nvdb_selftest_umma(const void* a_img, uint32_t a_bytes, const void* b_img, uint32_t b_bytes, int32_t n,
+                                  int32_t nk, uint32_t a_lbo, uint32_t a_sbo, uint32_t a_step, uint32_t b_lbo,
+                                  uint32_t b_sbo, uint32_t b_step, int32_t a_mn, int32_t b_mn, float* out,
+                                  void* stream) {
+  if (n < 16 || n > 256 || n % 16 || nk < 1) return fail(NVDB_EINVAL, "selftest: bad n/nk");
+  const uint32_t smem = (uint32_t)(align_up(a_bytes, 1024) + align_up(b_bytes, 1024));
+  if (smem > kMaxDynSmem) return fail(NVDB_EINVAL, "selftest: images too large");
+  NVDB_CUDA_TRY(cudaFuncSetAttribute(k_selftest_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  k_selftest_umma<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(a_img), a_bytes, static_cast<const uint8_t*>(b_img), b_bytes, n, nk, a_lbo, a_sbo,
+      a_step, b_lbo, b_sbo, b_step, a_mn, b_mn, out);
+  NVDB_CHECK_LAUNCH();
+  return NVDB_OK;
+}

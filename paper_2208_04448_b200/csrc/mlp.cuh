@@ -1,0 +1,461 @@
+// Fused Fourier-feature MLP evaluation on tcgen05 tensor cores (sm_100a).
+//
+// Replaces neural.forward_block (neural.py:527-550) and the gate-blended
+// evaluators around it (inference.py:39-84, partition.py:123-256): one
+// persistent kernel computes, per 128-point tile,
+//   centre -> expert input map (container.py:147-150, f64 then f32)
+//   -> Fourier features [cos, sin] (interleaved, W0 in serialized order)
+//   -> hidden layers on the tensor cores (fp16 operands, fp32 accumulate in TMEM)
+//   -> head on the FMA pipe in fp32
+//   -> softmax / sigmoid / identity, clamped-tent gate weight, f64 blend,
+//      and the decode decision (argmax, > 0.5, clip*scale) in the epilogue.
+//
+// CTA = 2 warpgroups; each warpgroup owns one tile at a time (one thread per
+// TMEM lane / point row) and issues its own MMAs from one elected thread,
+// so the tensor core works on one warpgroup's tile while the other runs its
+// MUFU/FMA epilogue.  Weights of the current net live in shared memory
+// (loaded with one bulk async copy); tiles are processed in pairs that share
+// a net so both warpgroups read the same weights.
+#pragma once
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace nvdb {
+
+constexpr int kTileM = 128;
+constexpr int kChunkK = 64;            // feature K chunk (fp16 elements)
+constexpr int kCtaThreads = 256;
+constexpr int kChunkBytes = kTileM * kChunkK * 2;   // 16 KB
+constexpr int kMaxOut = 3;
+
+enum SrcKind : int32_t {
+  SRC_NORM_F32 = 0,    // already-normalised float3 inputs (forward_block seam)
+  SRC_CENTER_F64 = 1,  // continuous index-space centres, double3
+  SRC_COORD_I32 = 2,   // integer voxel coords, centre = c + 0.5
+  SRC_LEAF_VOX = 3,    // id = leaf*512 + voxel, origins int3
+  SRC_L1_SLOT = 4,     // id = node*4096 + slot, origins int3, centre = o + 8*slot + 4
+};
+
+enum OutMode : int32_t {
+  OUT_RAW = 0,       // raw head outputs f32 [id][out_dim]
+  OUT_PROBS = 1,     // blended f64 [id][k] + covered u8
+  OUT_L1CLASS = 2,   // u8 argmax class, uncovered -> 2
+  OUT_L0ACTIVE = 3,  // u8 covered & p > 0.5
+  OUT_VALUE = 4,     // f32 covered ? clip?(v)*scale : background
+};
+
+enum TileFlags : int32_t { TF_FIRST = 1, TF_LAST = 2 };
+
+enum Act : int32_t { ACT_RELU = 0, ACT_TANH = 1, ACT_SINE = 2 };
+enum Head : int32_t { HEAD_LINEAR = 0, HEAD_LOGITS = 1, HEAD_BINARY = 2 };
+
+struct alignas(16) NetDev {
+  const uint8_t* wimg;  // fp16 weight image, UMMA K-major core-matrix layout
+  const float* bias;    // [depth][width]  (sine: omega folded)
+  const float* headw;   // [out_dim][width]
+  const float* headb;   // [out_dim]
+  const float* b2pi;    // [3][k0/2]
+  uint32_t wimg_bytes;
+  int32_t k0, width, depth, out_dim, act, head, expert;
+};
+
+struct alignas(16) ExpertDev {
+  double norm_origin[3];
+  double norm_scale;
+  int32_t cell[3];
+  int32_t pad;
+};
+
+struct alignas(16) Tile {
+  int32_t net;
+  int32_t count;
+  int32_t flags;
+  int32_t pad;
+  int64_t first;  // index into idx[] (or the point id itself when idx == nullptr)
+};
+
+struct MlpArgs {
+  const NetDev* nets;
+  const ExpertDev* experts;
+  const Tile* tiles;  // nullptr -> implicit tiles: [128 i, 128 i + 128) of n_implicit points
+  int32_t npairs;
+  const int32_t* npairs_dev;  // non-null: pair count read on the device (built by a prior kernel)
+  const uint8_t* ncand;       // non-null: per-point candidate count; first = (pass == 0),
+  int32_t pass;               //           last = (ncand[id] == pass + 1); else tile flags
+  int32_t implicit_net;
+  int64_t n_implicit;
+  int32_t src_kind;
+  const int64_t* idx;
+  const void* src;
+  int32_t subdomain_size, halo;
+  int32_t out_mode;
+  float* out_raw;
+  double* acc;  // [id][4] partial (num0..2, den) for multi-expert points
+  double* out_probs;
+  uint8_t* out_u8;
+  float* out_f32;
+  double value_scale;
+  float background;
+  int32_t clip;
+  // shared-memory carve-up (bytes, 1024-aligned offsets)
+  uint32_t w_off, region_off, region_bytes, small_off, bar_off;
+};
+
+// small per-net parameters staged in shared memory
+struct SmallView {
+  float* bias;
+  float* headw;
+  float* headb;
+  float* b2pi;
+};
+constexpr int kSmallFloats = 4 * 256 + 3 * 256 + 4 + 3 * 512;  // bias, head, headb, b2pi (k0<=1024)
+
+// continuous index-space centre of point `id` of a source (decoder.py:46-47,
+// 110-111, 163, 247; encoder.py:99-100).  Returns false for SRC_NORM_F32.
+__device__ __forceinline__ bool point_centre(int kind, const void* src, int64_t id, double c[3]) {
+  switch (kind) {
+    case SRC_CENTER_F64: {
+      const double* s = static_cast<const double*>(src) + 3 * id;
+      c[0] = s[0]; c[1] = s[1]; c[2] = s[2];
+      return true;
+    }
+    case SRC_COORD_I32: {
+      const int* s = static_cast<const int*>(src) + 3 * id;
+      c[0] = s[0] + 0.5; c[1] = s[1] + 0.5; c[2] = s[2] + 0.5;
+      return true;
+    }
+    case SRC_LEAF_VOX: {
+      const int* o = static_cast<const int*>(src) + 3 * (id >> 9);
+      const int v = (int)(id & 511);
+      c[0] = o[0] + (v >> 6) + 0.5; c[1] = o[1] + ((v >> 3) & 7) + 0.5; c[2] = o[2] + (v & 7) + 0.5;
+      return true;
+    }
+    case SRC_L1_SLOT: {
+      const int* o = static_cast<const int*>(src) + 3 * (id >> 12);
+      const int s = (int)(id & 4095);
+      c[0] = o[0] + 8.0 * (s >> 8) + 4.0; c[1] = o[1] + 8.0 * ((s >> 4) & 15) + 4.0;
+      c[2] = o[2] + 8.0 * (s & 15) + 4.0;
+      return true;
+    }
+    default:
+      return false;
+  }
+}
+
+// clamped-tent gate weight of the expert owning `cell` (partition.py:123-139)
+__device__ __forceinline__ double gate_weight(const int cell[3], int S, int halo, const double c[3]) {
+  const double h = (double)halo;
+  double w = 1.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double lo = (double)cell[i] * S;
+    const double hi = lo + S;
+    double ramp = fmin(c[i] - (lo - h), (hi + h) - c[i]) / (2.0 * h);
+    ramp = fmin(fmax(ramp, 0.0), 1.0);
+    w *= ramp;
+  }
+  return w;
+}
+
+__device__ __forceinline__ float act_fn(int act, float z) {
+  if (act == ACT_SINE) return __sinf(z);
+  if (act == ACT_TANH) return tanhf(z);
+  return fmaxf(z, 0.0f);
+}
+
+__global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x;
+  const int wg = tid >> 7;
+  const int t = tid & 127;
+  const int wwarp = t >> 5;
+
+  uint8_t* wsm = smem + a.w_off;
+  float* small = reinterpret_cast<float*>(smem + a.small_off);
+  SmallView sv{small, small + 4 * 256, small + 4 * 256 + 3 * 256, small + 4 * 256 + 3 * 256 + 4};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
+  // bars[0] = weight load; per WG: [1+3wg] chunk0, [2+3wg] chunk1, [3+3wg] layer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  __shared__ NetDev s_net;
+  __shared__ ExpertDev s_exp;
+
+  if (tid == 0) {
+    for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  if (tid < 32) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  uint64_t* bar_w = &bars[0];
+  uint64_t* bar_c0 = &bars[1 + 3 * wg];
+  uint64_t* bar_layer = &bars[3 + 3 * wg];
+  uint32_t ncommit[2] = {0u, 0u};
+  bool pend[2] = {false, false};
+  uint32_t nlayer = 0;
+  uint32_t wphase = 0;
+  int loaded = -1;
+
+  const uint32_t tmem_col = tmem_base + (uint32_t)(wg * 256);             // MMA D (lane 0)
+  const uint32_t tmem_d = tmem_col + ((uint32_t)(wwarp * 32) << 16);       // this warp's lanes
+  const uint32_t region_s = smem_addr(smem + a.region_off + wg * a.region_bytes);
+  const uint32_t w_s = smem_addr(wsm);
+
+  const int npairs = a.npairs_dev ? *a.npairs_dev : a.npairs;
+  const int per_cta = (npairs + gridDim.x - 1) / gridDim.x;
+  const int p0 = blockIdx.x * per_cta;
+  const int p1 = min(npairs, p0 + per_cta);
+
+  for (int p = p0; p < p1; ++p) {
+    const int pair_net = a.tiles ? a.tiles[2 * p].net : a.implicit_net;
+    if (pair_net != loaded) {
+      // ---- switch weights: the whole CTA is idle here (both warpgroups
+      // finished their previous tile, so no MMA still reads the old image)
+      __syncthreads();
+      if (tid == 0) {
+        s_net = a.nets[pair_net];
+        s_exp = a.experts[a.nets[pair_net].expert];
+        const NetDev& nd = a.nets[pair_net];
+        mbar_arrive_expect_tx(bar_w, nd.wimg_bytes);
+        const uint32_t kPiece = 32768;
+        for (uint32_t off = 0; off < nd.wimg_bytes; off += kPiece) {
+          const uint32_t len = min(kPiece, nd.wimg_bytes - off);
+          bulk_g2s(wsm + off, nd.wimg + off, len, bar_w);
+        }
+      }
+      __syncthreads();
+      {
+        const NetDev& nd = s_net;
+        for (int i = tid; i < nd.depth * nd.width; i += kCtaThreads) sv.bias[i] = nd.bias[i];
+        for (int i = tid; i < nd.out_dim * nd.width; i += kCtaThreads) sv.headw[i] = nd.headw[i];
+        if (tid < nd.out_dim) sv.headb[tid] = nd.headb[tid];
+        for (int i = tid; i < 3 * (nd.k0 / 2); i += kCtaThreads) sv.b2pi[i] = nd.b2pi[i];
+      }
+      mbar_wait(bar_w, wphase);
+      wphase ^= 1u;
+      __syncthreads();
+      loaded = pair_net;
+    }
+    Tile tile;
+    if (a.tiles) {
+      tile = a.tiles[2 * p + wg];
+    } else {
+      const int64_t first = (int64_t)(2 * p + wg) * kTileM;
+      tile.net = a.implicit_net;
+      tile.first = first;
+      tile.flags = TF_FIRST | TF_LAST;
+      tile.count = (int32_t)max((int64_t)0, min((int64_t)kTileM, a.n_implicit - first));
+    }
+    if (tile.count <= 0) continue;
+
+    const int width = s_net.width, depth = s_net.depth, k0 = s_net.k0, out_dim = s_net.out_dim;
+    const int act = s_net.act;
+    const int mp = k0 >> 1;
+
+    // ------------------------------------------------ point set-up (row t)
+    const bool valid = t < tile.count;
+    const int64_t pos = tile.first + (valid ? t : 0);
+    const int64_t id = a.idx ? a.idx[pos] : pos;
+    float x0, x1, x2;
+    double gw = 1.0;
+    {
+      double c[3];
+      if (point_centre(a.src_kind, a.src, id, c)) {
+        x0 = __double2float_rn((c[0] - s_exp.norm_origin[0]) / s_exp.norm_scale);
+        x1 = __double2float_rn((c[1] - s_exp.norm_origin[1]) / s_exp.norm_scale);
+        x2 = __double2float_rn((c[2] - s_exp.norm_origin[2]) / s_exp.norm_scale);
+        gw = gate_weight(s_exp.cell, a.subdomain_size, a.halo, c);
+      } else {
+        const float* s = static_cast<const float*>(a.src) + 3 * id;
+        x0 = s[0]; x1 = s[1]; x2 = s[2];
+      }
+    }
+
+    // ------------------------------------------------ features + layer 0
+    const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
+    const int nch = k0 / kChunkK;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int b = ch & 1;
+      if (pend[b]) {
+        mbar_wait(bar_c0 + b, (ncommit[b] - 1u) & 1u);
+        pend[b] = false;
+      }
+      const uint32_t buf = region_s + b * kChunkBytes;
+#pragma unroll
+      for (int q = 0; q < kChunkK / 8; ++q) {
+        uint32_t h[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int f = ch * (kChunkK / 2) + q * 4 + j;
+          const float th = fmaf(x2, sv.b2pi[2 * mp + f], fmaf(x1, sv.b2pi[mp + f], x0 * sv.b2pi[f]));
+          float sn, cs;
+          __sincosf(th, &sn, &cs);
+          h[j] = pack_half2(cs, sn);
+        }
+        st_shared_v4(buf + kmajor_offset(t, q * 8, kTileM), h[0], h[1], h[2], h[3]);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      named_bar_sync(1 + wg, 128);
+      if (t == 0) {
+        tc_fence_after();
+#pragma unroll
+        for (int s = 0; s < kChunkK / 16; ++s) {
+          const uint64_t ad = smem_desc(buf + s * (2 * kTileM * 16), kTileM * 16, 128);
+          const uint32_t wb = w_s + (uint32_t)(((ch * kChunkK + s * 16) >> 3) * (width >> 3) * 128);
+          const uint64_t bd = smem_desc(wb, width * 16, 128);
+          umma_f16(tmem_col, ad, bd, idesc, (ch | s) != 0);
+        }
+        umma_commit(bar_c0 + b);
+        if (ch == nch - 1) umma_commit(bar_layer);
+      }
+      ncommit[b]++;
+      pend[b] = true;
+    }
+    mbar_wait(bar_layer, nlayer & 1u);
+    nlayer++;
+    pend[0] = pend[1] = false;
+    tc_fence_after();
+
+    // ------------------------------------------------ hidden epilogues
+    float y[kMaxOut] = {0.f, 0.f, 0.f};
+    uint32_t woff = (uint32_t)(width * k0 * 2);  // byte offset of W1 in the image
+    for (int l = 0; l < depth; ++l) {
+      const bool last = (l == depth - 1);
+      const float* bl = sv.bias + l * width;
+      for (int cc = 0; cc < width / 16; ++cc) {
+        float v[16];
+        tmem_ld16(tmem_d + cc * 16, v);
+        tmem_ld_wait();
+        float av[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) av[i] = act_fn(act, v[i] + bl[cc * 16 + i]);
+        if (!last) {
+          st_shared_v4(region_s + kmajor_offset(t, cc * 16, kTileM), pack_half2(av[0], av[1]),
+                       pack_half2(av[2], av[3]), pack_half2(av[4], av[5]), pack_half2(av[6], av[7]));
+          st_shared_v4(region_s + kmajor_offset(t, cc * 16 + 8, kTileM), pack_half2(av[8], av[9]),
+                       pack_half2(av[10], av[11]), pack_half2(av[12], av[13]), pack_half2(av[14], av[15]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < kMaxOut; ++k) {
+            if (k < out_dim) {
+              const float* hw = sv.headw + k * width + cc * 16;
+              float s = y[k];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) s = fmaf(av[i], hw[i], s);
+              y[k] = s;
+            }
+          }
+        }
+      }
+      if (!last) {
+        fence_async_smem();
+        tc_fence_before();
+        named_bar_sync(1 + wg, 128);
+        if (t == 0) {
+          tc_fence_after();
+          const uint32_t wl = w_s + woff;
+          for (int s = 0; s < width / 16; ++s) {
+            const uint64_t ad = smem_desc(region_s + s * (2 * kTileM * 16), kTileM * 16, 128);
+            const uint64_t bd = smem_desc(wl + (uint32_t)(s * 2 * (width >> 3) * 128), width * 16, 128);
+            umma_f16(tmem_col, ad, bd, idesc, s != 0);
+          }
+          umma_commit(bar_layer);
+        }
+        woff += (uint32_t)(width * width * 2);
+        mbar_wait(bar_layer, nlayer & 1u);
+        nlayer++;
+        tc_fence_after();
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxOut; ++k)
+      if (k < out_dim) y[k] += sv.headb[k];
+
+    // ------------------------------------------------ output
+    if (!valid) continue;
+    if (a.out_mode == OUT_RAW) {
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k)
+        if (k < out_dim) a.out_raw[id * out_dim + k] = y[k];
+      continue;
+    }
+    // transform (inference.py:29-36) in float32
+    float tv[kMaxOut];
+    const int head = s_net.head;
+    tv[1] = tv[2] = 0.f;
+    if (head == HEAD_LOGITS) {  // 3-way softmax (l1 classifier heads are always 3 wide)
+      const float zm = fmaxf(fmaxf(y[0], y[1]), y[2]);
+      const float e0 = expf(y[0] - zm), e1 = expf(y[1] - zm), e2 = expf(y[2] - zm);
+      const float ssum = (e0 + e1) + e2;
+      tv[0] = e0 / ssum; tv[1] = e1 / ssum; tv[2] = e2 / ssum;
+    } else if (head == HEAD_BINARY) {
+      tv[0] = 1.0f / (1.0f + expf(-y[0]));
+    } else {
+      tv[0] = y[0];
+    }
+    // gate-weighted accumulation (partition.py:245-256), f64, sid order = pass order
+    double num[kMaxOut], den;
+    const int kk = out_dim;
+#pragma unroll
+    for (int k = 0; k < kMaxOut; ++k) num[k] = gw > 0.0 ? (double)tv[k] * gw : 0.0;
+    den = gw > 0.0 ? gw : 0.0;
+    bool is_first = (tile.flags & TF_FIRST) != 0, is_last = (tile.flags & TF_LAST) != 0;
+    if (a.ncand) {
+      is_first = a.pass == 0;
+      is_last = (int)a.ncand[id] == a.pass + 1;
+    }
+    if (!is_first) {
+      const double* ac = a.acc + 4 * id;
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k) num[k] = ac[k] + num[k];
+      den = ac[3] + den;
+    }
+    if (!is_last) {
+      double* ac = a.acc + 4 * id;
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k) ac[k] = num[k];
+      ac[3] = den;
+      continue;
+    }
+    const bool covered = den > 0.0;
+    if (covered) {
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k) num[k] = num[k] / den;
+    }
+    switch (a.out_mode) {
+      case OUT_PROBS:
+#pragma unroll
+        for (int k = 0; k < kMaxOut; ++k)
+          if (k < kk) a.out_probs[id * kk + k] = covered ? num[k] : 0.0;
+        a.out_u8[id] = covered ? 1 : 0;
+        break;
+      case OUT_L1CLASS: {
+        int best = 0;
+        if (num[1] > num[best]) best = 1;
+        if (num[2] > num[best]) best = 2;
+        a.out_u8[id] = covered ? (uint8_t)best : (uint8_t)2;
+        break;
+      }
+      case OUT_L0ACTIVE:
+        a.out_u8[id] = (covered && num[0] > 0.5) ? 1 : 0;
+        break;
+      default: {  // OUT_VALUE
+        double v = num[0];
+        if (a.clip) v = fmin(fmax(v, -1.0), 1.0);
+        a.out_f32[id] = covered ? (float)(v * a.value_scale) : a.background;
+        break;
+      }
+    }
+  }
+
+  // ------------------------------------------------ teardown
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_dealloc(tmem_base, 512);
+}
+
+}  // namespace nvdb

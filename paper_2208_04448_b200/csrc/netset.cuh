@@ -1,0 +1,63 @@
+// Device-resident set of every expert's networks (the decode/eval "model").
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+#include "mlp.cuh"
+
+struct nvdb_netset {
+  int nnets = 0, nexperts = 0;
+  int subdomain_size = 512, halo = 8;
+  uint8_t* dev_blob = nullptr;            // weight images + float params
+  nvdb::NetDev* dev_nets = nullptr;       // [nnets]
+  nvdb::ExpertDev* dev_experts = nullptr; // [nexperts]
+  int32_t* dev_cells = nullptr;           // [nexperts][3] sorted lexicographically (= sid order)
+  int32_t* dev_tagnet = nullptr;          // [nexperts][4] net index or -1
+  std::vector<nvdb::NetDev> nets;         // host copies (device pointers inside)
+  std::vector<nvdb::ExpertDev> experts;
+  std::vector<int32_t> tagnet;            // [nexperts][4]
+  uint32_t max_wimg = 0;
+  int max_width = 16;
+};
+
+namespace nvdb {
+
+// shared-memory plan for an MLP launch over nets with the given maxima
+struct SmemPlan {
+  uint32_t w_off, region_off, region_bytes, small_off, bar_off, total;
+};
+
+inline SmemPlan plan_smem(uint32_t max_wimg, int max_width) {
+  SmemPlan p;
+  p.w_off = 0;
+  p.region_off = (uint32_t)align_up(max_wimg, 1024);
+  const uint32_t feat = 2u * kChunkBytes;
+  const uint32_t hid = (uint32_t)kTileM * (uint32_t)max_width * 2u;
+  p.region_bytes = (uint32_t)align_up(feat > hid ? feat : hid, 1024);
+  p.small_off = p.region_off + 2 * p.region_bytes;
+  p.bar_off = (uint32_t)align_up(p.small_off + kSmallFloats * 4, 16);
+  p.total = p.bar_off + 128;
+  return p;
+}
+
+constexpr uint32_t kMaxDynSmem = 227 * 1024 - 512;  // leave room for static __shared__
+
+int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int grid, cudaStream_t st);
+
+// Generic gate-blended evaluation over a point source (all experts owning
+// net `tag`), writing `out_mode` outputs.  Workspace from the caller.
+struct BlendOut {
+  int32_t out_mode;
+  double* out_probs;
+  uint8_t* out_u8;
+  float* out_f32;
+  double value_scale;
+  float background;
+  int32_t clip;
+};
+size_t blended_workspace_bytes(const nvdb_netset* ns, int64_t n);
+int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, int64_t n, const BlendOut& o,
+                void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace nvdb

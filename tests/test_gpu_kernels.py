@@ -1,0 +1,156 @@
+"""GPU parity tests for the C-ABI kernels (need a B200 + built library).
+
+Tolerances (fp16 tensor-core operands, fp32 accumulate, fp32 head):
+forward outputs within 2e-2 absolute and 3e-3 RMS of the oracle for
+O(1)-scale random nets; classifier decisions within the 99.99 % bar;
+lookups bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import net_from_fixture
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2208_04448_b200 import _lib  # noqa: E402
+from paper_2208_04448_b200.model import (EncodedSubdomain, NetRecord, container_from_arrays,  # noqa: E402
+                                         grid_from_arrays)
+from paper_2208_04448_b200.netset import DeviceNetSet  # noqa: E402
+from paper_2208_04448_b200.tree import DeviceTree  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def kmajor_image(mat: np.ndarray) -> np.ndarray:
+    """(R, K) fp16 -> core-matrix K-major image (sbo = 128, lbo = R*16)."""
+    R, K = mat.shape
+    img = np.zeros(R * K, dtype=np.float16)
+    r = np.arange(R)[:, None]
+    k = np.arange(K)[None, :]
+    off = ((k // 8) * (R // 8) + r // 8) * 64 + (r % 8) * 8 + (k % 8)
+    img[off.reshape(-1)] = mat.reshape(-1)
+    return img
+
+
+def mnmajor_image(mat: np.ndarray, mn_groups_adjacent: bool) -> tuple:
+    """(MN, K) fp16 stored MN-contiguous; returns (image, lbo, sbo, step)."""
+    R, K = mat.shape
+    img = np.zeros(R * K, dtype=np.float16)
+    m = np.arange(R)[:, None]
+    k = np.arange(K)[None, :]
+    if mn_groups_adjacent:  # MN groups of 8 adjacent (128 B), K groups of 8 at R*16
+        off = (k // 8) * (R // 8) * 64 + (m // 8) * 64 + (k % 8) * 8 + (m % 8)
+        lbo, sbo, step = R * 16, 128, 2 * R * 16
+    else:  # K groups adjacent, MN groups at K*16
+        off = (m // 8) * (K // 8) * 64 + (k // 8) * 64 + (k % 8) * 8 + (m % 8)
+        lbo, sbo, step = 128, K * 16, 256
+    img[off.reshape(-1)] = mat.reshape(-1)
+    return img, lbo, sbo, step
+
+
+def run_selftest(a_img, b_img, n, nk, a_par, b_par, a_mn, b_mn):
+    A = torch.from_numpy(a_img.view(np.uint8)).to(DEV)
+    B = torch.from_numpy(b_img.view(np.uint8)).to(DEV)
+    out = torch.zeros((128, n), dtype=torch.float32, device=DEV)
+    L = _lib.lib()
+    _lib.check(L.nvdb_selftest_umma(A.data_ptr(), A.numel(), B.data_ptr(), B.numel(), n, nk, *a_par, *b_par,
+                                    a_mn, b_mn, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("n", [16, 96, 256])
+def test_umma_kmajor_descriptors(n):
+    rng = np.random.default_rng(0)
+    K = 64
+    a = rng.standard_normal((128, K)).astype(np.float16)
+    b = rng.standard_normal((n, K)).astype(np.float16)
+    ref = a.astype(np.float32) @ b.astype(np.float32).T
+    got = run_selftest(kmajor_image(a), kmajor_image(b), n, K // 16, (128 * 16, 128, 2 * 128 * 16),
+                       (n * 16, 128, 2 * n * 16), 0, 0)
+    np.testing.assert_allclose(got, ref, rtol=1e-3, atol=1e-2)
+
+
+@pytest.mark.parametrize("adjacent", [True, False])
+def test_umma_mnmajor_descriptors(adjacent):
+    """MN-major A and B (used by the weight-gradient GEMMs in training)."""
+    rng = np.random.default_rng(1)
+    K, n = 64, 96
+    a = rng.standard_normal((128, K)).astype(np.float16)   # (M, K)
+    b = rng.standard_normal((n, K)).astype(np.float16)     # (N, K)
+    ref = a.astype(np.float32) @ b.astype(np.float32).T
+    ai, alb, asb, ast = mnmajor_image(a, adjacent)
+    bi, blb, bsb, bst = mnmajor_image(b, adjacent)
+    got = run_selftest(ai, bi, n, K // 16, (alb, asb, ast), (blb, bsb, bst), 1, 1)
+    np.testing.assert_allclose(got, ref, rtol=1e-3, atol=1e-2)
+
+
+class _Expert:
+    def __init__(self, tag, rec):
+        self.id = 0
+        self.cell = (0, 0, 0)
+        self.norm_origin = np.zeros(3)
+        self.norm_scale = 1.0
+        self._tag, self._rec = tag, rec
+
+    def nets(self):
+        return [(t, self._rec if t == self._tag else None) for t in ("l1", "tile", "l0", "voxel")]
+
+
+def test_forward_matches_oracle(golden):
+    z = golden("nets")
+    for ci in range(int(z["ncases"][0])):
+        q = f"n{ci}_"
+        params, ff = net_from_fixture(z, q)
+        tag = "l1" if params.head == "logits" else "voxel"
+        ns = DeviceNetSet([_Expert(tag, NetRecord(params, ff))], 512)
+        pts = torch.from_numpy(z[q + "pts"]).to(DEV)
+        got = ns.forward(0, pts).cpu().numpy()
+        ref = O.forward_block(params, ff, z[q + "pts"])
+        err = np.abs(got - ref)
+        rms = float(np.sqrt(np.mean(err ** 2)))
+        print(f"case {ci} ({params.activation.kind}) max {err.max():.2e} rms {rms:.2e} "
+              f"scale {np.abs(ref).max():.2f}")
+        assert err.max() < 2e-2 * max(1.0, np.abs(ref).max())
+        assert rms < 3e-3 * max(1.0, np.abs(ref).max())
+        ns.close()
+
+
+def test_lookup_bit_exact(golden):
+    z = golden("lookup_small")
+    g = grid_from_arrays(z)
+    tree = DeviceTree(g)
+    coords = torch.from_numpy(z["coords"].astype(np.int32)).to(DEV)
+    v, a, k = tree.lookup(coords)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(v.cpu().numpy().view(np.uint32), z["values"].view(np.uint32))
+    np.testing.assert_array_equal(a.cpu().numpy().astype(bool), z["active"])
+    np.testing.assert_array_equal(k.cpu().numpy(), z["kind"])
+
+
+@pytest.mark.parametrize("name", ["decode_small", "decode_multi"])
+def test_blended_matches_reference(golden, name):
+    z = golden(name)
+    c = container_from_arrays(z)
+    ns = DeviceNetSet(c.experts, c.layout.size, c.layout.halo)
+    cen = torch.from_numpy(z["cen"]).to(DEV)
+    for tag, pk, ck in (("l1", "p1", "c1"), ("l0", "p0", "c0"), ("voxel", "pv", "cv")):
+        out, cov = ns.blended(tag, cen)
+        out = out.cpu().numpy().reshape(z[pk].shape)
+        cov = cov.cpu().numpy().astype(bool)
+        np.testing.assert_array_equal(cov, z[ck])
+        err = np.abs(out - z[pk])
+        print(name, tag, "max err", err.max())
+        assert err.max() < 2e-2
+        if tag == "l1":
+            agree = (out.argmax(1) == z[pk].argmax(1))[cov].mean()
+            assert agree >= 0.999
+        if tag == "l0":
+            agree = ((out > 0.5) == (z[pk] > 0.5))[cov].mean()
+            assert agree >= 0.999
+    ns.close()

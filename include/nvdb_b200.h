@@ -102,6 +102,68 @@ NVDB_API int nvdb_eval_blended(const nvdb_netset* ns, int32_t tag, const double*
                       double* out, uint8_t* covered, void* workspace, size_t workspace_bytes,
                       void* stream);
 
+/* Generic evaluation: point source x output selector. */
+#define NVDB_SRC_NORM_F32 0   /* (n,3) float32 already-normalized inputs      */
+#define NVDB_SRC_CENTER_F64 1 /* (n,3) float64 index-space centres            */
+#define NVDB_SRC_COORD_I32 2  /* (n,3) int32 voxel coords, centre = c + 0.5   */
+#define NVDB_SRC_LEAF_VOX 3   /* id = leaf*512 + voxel over (nl,3) int32 origins */
+#define NVDB_SRC_L1_SLOT 4    /* id = node*4096 + slot over (n1,3) int32 origins  */
+#define NVDB_OUT_RAW 0        /* raw head outputs (single net)                */
+#define NVDB_OUT_PROBS 1      /* blended float64 (n,k) + covered u8           */
+#define NVDB_OUT_L1CLASS 2    /* u8 argmax of blended probs, uncovered -> 2   */
+#define NVDB_OUT_L0ACTIVE 3   /* u8 covered && p > 0.5                        */
+#define NVDB_OUT_VALUE 4      /* f32 covered ? clip?(v)*scale : background    */
+
+typedef struct {
+  int32_t out_mode;
+  float* raw;
+  double* probs;
+  uint8_t* u8;
+  float* f32;
+  double value_scale;
+  float background;
+  int32_t clip;
+} nvdb_eval_out;
+
+/* The fused evaluator behind every decode stage (decoder.py:110-196) and
+ * the blended seams: point ids 0..n-1 (source id gather[i] when gather is
+ * non-null), outputs written at index i.  Workspace: nvdb_eval_workspace_bytes. */
+NVDB_API int nvdb_eval(const nvdb_netset* ns, int32_t tag, int32_t src_kind, const void* src,
+                       const int64_t* gather, int64_t n, const nvdb_eval_out* out, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* -- decode helpers (decoder.py:101-211) ------------------------------------ */
+
+/* ids of entries equal to `value` (ascending) and their count (device int64). */
+NVDB_API size_t nvdb_select_workspace_bytes(int64_t n);
+NVDB_API int nvdb_select_u8(const uint8_t* v, int64_t n, uint8_t value, int64_t* ids, int64_t* count,
+                            void* workspace, size_t workspace_bytes, void* stream);
+/* level-1 patches then inactive tile values where class == 2 (decoder.py:114-134) */
+NVDB_API int nvdb_l1_apply(uint8_t* cls, float* tiles, int64_t nslots, const int64_t* patch_slot,
+                           const uint8_t* patch_cls, int64_t npatch, const int64_t* tile_slot,
+                           const float* tile_value, int64_t ntile, void* stream);
+NVDB_API int nvdb_scatter_f32(float* dst, const int64_t* ids, const float* vals, int64_t n, void* stream);
+/* leaf origins of child slots (node*4096+slot, node order x ascending slot)
+ * and the slot -> leaf index map (-1 elsewhere) (decoder.py:146-151) */
+NVDB_API int nvdb_leaf_list(const int64_t* child_slots, int64_t nl, const int32_t* node_origins,
+                            int64_t nslots, int32_t* leaf_origins, int32_t* leaf_of_slot, void* stream);
+/* level-0 patches on the active mask; *err = 1 if a patch has no leaf (decoder.py:168-179) */
+NVDB_API int nvdb_l0_apply(uint8_t* active, const int64_t* patch_slot, const int32_t* patch_vox,
+                           const uint8_t* patch_active, int64_t npatch, const int32_t* leaf_of_slot,
+                           int32_t* err, void* stream);
+/* leaf values: background, regressed active voxels, patch values, negative
+ * fill of inactive voxels; packed active words; optional patched flags
+ * (decoder.py:182-210) */
+NVDB_API int nvdb_leaf_finalize(int64_t nl, const uint8_t* active, const int64_t* act_ids,
+                                const float* act_vals, int64_t nact, const int64_t* patch_slot,
+                                const int32_t* patch_vox, const uint8_t* patch_active,
+                                const float* patch_value, int64_t npatch, const int64_t* neg_slot,
+                                const uint64_t* neg_bits, int64_t nneg, const int32_t* leaf_of_slot,
+                                float background, float neg_value, float* values,
+                                uint64_t* active_words, uint8_t* patched, void* stream);
+/* words[w] bit j = (v[64w + j] == value) */
+NVDB_API int nvdb_pack_eq(const uint8_t* v, int64_t nwords, uint8_t value, uint64_t* words, void* stream);
+
 /* -- upper-tree lookup ----------------------------------------------------- */
 
 /* Flattened [Hash,5,4,3] tree (grid.py:248-390).  HOST arrays:
@@ -129,7 +191,9 @@ typedef struct {
   const int32_t* l1_child_base;    /* (n1) */
   const uint64_t* leaf_active;     /* (nl,8) */
   const float* leaf_values;        /* (nl,512) */
+  const uint64_t* leaf_patched;    /* (nl,8) or NULL: voxels holding exact patch values */
 } nvdb_tree_desc;
+/* (all tree_desc arrays may be host or device memory) */
 
 NVDB_API int nvdb_tree_create(const nvdb_tree_desc* desc, nvdb_tree** out);
 NVDB_API int nvdb_tree_destroy(nvdb_tree* tree);
@@ -139,6 +203,14 @@ NVDB_API int nvdb_tree_destroy(nvdb_tree* tree);
  * leaf (n) int32 leaf index or -1 (nullable). */
 NVDB_API int nvdb_lookup(const nvdb_tree* tree, const int32_t* coords, int64_t n, float* value, uint8_t* active,
                 uint8_t* kind, int32_t* leaf, void* stream);
+
+/* HybridGrid.query (decoder.py:239-264) pieces: flag rows with active &&
+ * kind == 2, then write regressed values (patched voxels keep their exact
+ * stored value from the tree) back to those rows. */
+NVDB_API int nvdb_neural_rows(const uint8_t* active, const uint8_t* kind, int64_t n, uint8_t* flag, void* stream);
+NVDB_API int nvdb_query_finalize(const int64_t* rows, int64_t nrows, const float* regressed,
+                                 const int32_t* coords, const int32_t* leaf, const nvdb_tree* tree,
+                                 float* value, void* stream);
 
 /* -- diagnostics ------------------------------------------------------------ */
 

@@ -26,8 +26,20 @@ NVDB_ENOMEM = -5
 EXPORTED = [
     "nvdb_last_error", "nvdb_version", "nvdb_netset_create", "nvdb_netset_destroy",
     "nvdb_forward", "nvdb_eval_workspace_bytes", "nvdb_eval_blended", "nvdb_tree_create",
-    "nvdb_tree_destroy", "nvdb_lookup", "nvdb_selftest_umma",
+    "nvdb_tree_destroy", "nvdb_lookup", "nvdb_selftest_umma", "nvdb_eval",
+    "nvdb_select_workspace_bytes", "nvdb_select_u8", "nvdb_l1_apply", "nvdb_scatter_f32",
+    "nvdb_leaf_list", "nvdb_l0_apply", "nvdb_leaf_finalize", "nvdb_pack_eq", "nvdb_neural_rows",
+    "nvdb_query_finalize",
 ]
+
+SRC_NORM_F32, SRC_CENTER_F64, SRC_COORD_I32, SRC_LEAF_VOX, SRC_L1_SLOT = range(5)
+OUT_RAW, OUT_PROBS, OUT_L1CLASS, OUT_L0ACTIVE, OUT_VALUE = range(5)
+
+
+class EvalOut(C.Structure):
+    _fields_ = [("out_mode", C.c_int32), ("raw", C.c_void_p), ("probs", C.c_void_p),
+                ("u8", C.c_void_p), ("f32", C.c_void_p), ("value_scale", C.c_double),
+                ("background", C.c_float), ("clip", C.c_int32)]
 
 
 class NetDesc(C.Structure):
@@ -52,7 +64,8 @@ class TreeDesc(C.Structure):
                 ("l2_child", C.c_void_p), ("l2_active", C.c_void_p), ("l2_tiles", C.c_void_p),
                 ("l2_child_base", C.c_void_p), ("l1_child", C.c_void_p), ("l1_active", C.c_void_p),
                 ("l1_tiles", C.c_void_p), ("l1_child_base", C.c_void_p),
-                ("leaf_active", C.c_void_p), ("leaf_values", C.c_void_p)]
+                ("leaf_active", C.c_void_p), ("leaf_values", C.c_void_p),
+                ("leaf_patched", C.c_void_p)]
 
 
 _lib: Optional[C.CDLL] = None
@@ -74,6 +87,18 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_lookup": (C.c_int, [vp, vp, i64, vp, vp, vp, vp, vp]),
         "nvdb_selftest_umma": (C.c_int, [vp, u32, vp, u32, i32, i32, u32, u32, u32, u32, u32, u32,
                                          i32, i32, vp, vp]),
+        "nvdb_eval": (C.c_int, [vp, i32, i32, vp, vp, i64, C.POINTER(EvalOut), vp, sz, vp]),
+        "nvdb_select_workspace_bytes": (sz, [i64]),
+        "nvdb_select_u8": (C.c_int, [vp, i64, C.c_uint8, vp, vp, vp, sz, vp]),
+        "nvdb_l1_apply": (C.c_int, [vp, vp, i64, vp, vp, i64, vp, vp, i64, vp]),
+        "nvdb_scatter_f32": (C.c_int, [vp, vp, vp, i64, vp]),
+        "nvdb_leaf_list": (C.c_int, [vp, i64, vp, i64, vp, vp, vp]),
+        "nvdb_l0_apply": (C.c_int, [vp, vp, vp, vp, i64, vp, vp, vp]),
+        "nvdb_leaf_finalize": (C.c_int, [i64, vp, vp, vp, i64, vp, vp, vp, vp, i64, vp, vp, i64, vp,
+                                         C.c_float, C.c_float, vp, vp, vp, vp]),
+        "nvdb_pack_eq": (C.c_int, [vp, i64, C.c_uint8, vp, vp]),
+        "nvdb_neural_rows": (C.c_int, [vp, vp, i64, vp, vp]),
+        "nvdb_query_finalize": (C.c_int, [vp, i64, vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

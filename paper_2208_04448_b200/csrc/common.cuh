@@ -55,4 +55,18 @@ inline int num_sms() {
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Opt a kernel into the largest dynamic shared memory the device allows and
+// return that limit (bytes), or -1 on failure.
+template <class K>
+inline long long enable_max_smem(K kernel) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) return -1;
+  const long long lim = (long long)optin - (long long)fa.sharedSizeBytes;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim) != cudaSuccess) return -1;
+  return lim;
+}
+
 }  // namespace nvdb

@@ -1,5 +1,6 @@
 // Netset upload, the forward_block seam and the generic gate-blended
 // evaluation driver (inference.py:39-84, partition.py:160-256).
+#define NVDB_MLP_KERNEL_TU
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -196,12 +197,14 @@ namespace nvdb {
 int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int grid, cudaStream_t st) {
   const SmemPlan plan = plan_smem(ns->max_wimg, ns->max_width);
   // at least ~120 KB so only one CTA (which owns all 512 TMEM columns) fits per SM
-  const uint32_t smem = std::max<uint32_t>(plan.total, 120 * 1024);
-  static bool attr_set = false;
-  if (!attr_set) {
-    NVDB_CUDA_TRY(cudaFuncSetAttribute(mlp_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    attr_set = true;
+  const uint32_t smem = std::max<uint32_t>(plan.total, 120 * 1024);  // one CTA per SM (owns all TMEM)
+  static long long smem_limit = -1;
+  if (smem_limit < 0) {
+    smem_limit = enable_max_smem(mlp_eval_kernel);
+    if (smem_limit < 0) return fail(NVDB_ECUDA, "cannot raise shared memory limit of mlp_eval_kernel");
   }
+  if ((long long)plan.total > smem_limit)
+    return fail(NVDB_EUNSUPPORTED, "MLP kernel needs %u B shared memory, device allows %lld", plan.total, smem_limit);
   a.nets = ns->dev_nets;
   a.experts = ns->dev_experts;
   a.npairs_dev = npairs_dev;
@@ -262,13 +265,13 @@ __device__ __forceinline__ long long floor_div(double v, double s) { return (lon
 
 // Per point and pass: the pass-th candidate expert (in sid order) owning the
 // tag's net with a positive gate weight (partition.py:180-229 keeps w > 0).
-__global__ void k_pass_keys(int src_kind, const void* src, int64_t n, int pass, const int32_t* cells, int ncell,
+__global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather, int64_t n, int pass, const int32_t* cells, int ncell,
                             const int32_t* tagnet, int tag, int S, int halo, uint8_t* ncand, uint16_t* keys,
                             int64_t* vals, BlendOut o) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double c[3];
-  point_centre(src_kind, src, i, c);
+  point_centre(src_kind, src, gather ? gather[i] : i, c);
   const double h = (double)halo;
   long long lo[3], hi[3];
   for (int a = 0; a < 3; ++a) {
@@ -311,7 +314,11 @@ __global__ void k_pass_keys(int src_kind, const void* src, int64_t n, int pass, 
         case OUT_L1CLASS: o.out_u8[i] = 2; break;
         case OUT_L0ACTIVE: o.out_u8[i] = 0; break;
         case OUT_VALUE: o.out_f32[i] = o.background; break;
-        default: break;
+        default: {
+          const int k = (tag == NVDB_TAG_L1) ? 3 : 1;
+          for (int j = 0; j < k; ++j) o.out_raw[i * k + j] = 0.f;
+          break;
+        }
       }
     }
   }
@@ -384,13 +391,15 @@ namespace nvdb {
 
 size_t blended_workspace_bytes(const nvdb_netset* ns, int64_t n) { return ws_layout(ns, n).total; }
 
-int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, int64_t n, const BlendOut& o,
-                void* ws, size_t ws_bytes, cudaStream_t st) {
+int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, const int64_t* gather, int64_t n,
+                const BlendOut& o, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n <= 0) return NVDB_OK;
   if (n > (int64_t)INT32_MAX) return fail(NVDB_EUNSUPPORTED, "run_blended: n > 2^31");
   MlpArgs a{};
   a.src_kind = src_kind;
   a.src = src;
+  a.gather = gather;
+  a.out_raw = o.out_raw;
   a.out_mode = o.out_mode;
   a.out_probs = o.out_probs;
   a.out_u8 = o.out_u8;
@@ -425,7 +434,7 @@ int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, i
   const int threads = 256;
   const int blocks = (int)((n + threads - 1) / threads);
   for (int pass = 0; pass < 8; ++pass) {
-    k_pass_keys<<<blocks, threads, 0, st>>>(src_kind, src, n, pass, ns->dev_cells, ns->nexperts, ns->dev_tagnet,
+    k_pass_keys<<<blocks, threads, 0, st>>>(src_kind, src, gather, n, pass, ns->dev_cells, ns->nexperts, ns->dev_tagnet,
                                             tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o);
     NVDB_CHECK_LAUNCH();
     size_t cb = w.cub_bytes;
@@ -453,7 +462,7 @@ extern "C" int nvdb_eval_blended(const nvdb_netset* ns, int32_t tag, const doubl
   o.out_mode = OUT_PROBS;
   o.out_probs = out;
   o.out_u8 = covered;
-  return run_blended(ns, tag, SRC_CENTER_F64, centers, n, o, workspace, workspace_bytes,
+  return run_blended(ns, tag, SRC_CENTER_F64, centers, nullptr, n, o, workspace, workspace_bytes,
                      static_cast<cudaStream_t>(stream));
 }
 
@@ -515,7 +524,7 @@ extern "C" int nvdb_selftest_umma(const void* a_img, uint32_t a_bytes, const voi
   if (n < 16 || n > 256 || n % 16 || nk < 1) return fail(NVDB_EINVAL, "selftest: bad n/nk");
   const uint32_t smem = (uint32_t)(align_up(a_bytes, 1024) + align_up(b_bytes, 1024));
   if (smem > kMaxDynSmem) return fail(NVDB_EINVAL, "selftest: images too large");
-  NVDB_CUDA_TRY(cudaFuncSetAttribute(k_selftest_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  if (enable_max_smem(k_selftest_umma) < (long long)smem) return fail(NVDB_ECUDA, "selftest: smem limit");
   k_selftest_umma<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(a_img), a_bytes, static_cast<const uint8_t*>(b_img), b_bytes, n, nk, a_lbo, a_sbo,
       a_step, b_lbo, b_sbo, b_step, a_mn, b_mn, out);

@@ -100,7 +100,7 @@ int upload(nvdb_tree* t, T** dst, const T* src, size_t count) {
   const size_t bytes = sizeof(T) * std::max<size_t>(count, 1);
   NVDB_CUDA_TRY(cudaMalloc(dst, bytes));
   t->owned[t->nowned++] = *dst;
-  if (count && src) NVDB_CUDA_TRY(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  if (count && src) NVDB_CUDA_TRY(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyDefault));
   else NVDB_CUDA_TRY(cudaMemset(*dst, 0, bytes));
   return NVDB_OK;
 }
@@ -170,6 +170,7 @@ extern "C" int nvdb_tree_create(const nvdb_tree_desc* d, nvdb_tree** out) {
   chk(upload(t, &t->l1_prefix, (const uint16_t*)nullptr, (size_t)64 * d->n1));
   chk(upload(t, &t->leaf_active, d->leaf_active, (size_t)8 * d->nl));
   chk(upload(t, &t->leaf_values, d->leaf_values, (size_t)512 * d->nl));
+  if (d->leaf_patched) chk(upload(t, &t->leaf_patched, d->leaf_patched, (size_t)8 * d->nl));
   if (!rc) rc = tree_build_prefix(t, 0);
   if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = fail(NVDB_ECUDA, "tree prefix build failed");
   if (rc) {

@@ -86,7 +86,8 @@ struct MlpArgs {
   int32_t implicit_net;
   int64_t n_implicit;
   int32_t src_kind;
-  const int64_t* idx;
+  const int64_t* idx;     // tile position -> point id (outputs are written at [id])
+  const int64_t* gather;  // point id -> source id (nullable: identity)
   const void* src;
   int32_t subdomain_size, halo;
   int32_t out_mode;
@@ -164,6 +165,9 @@ __device__ __forceinline__ float act_fn(int act, float z) {
   return fmaxf(z, 0.0f);
 }
 
+__global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a);
+
+#ifdef NVDB_MLP_KERNEL_TU  // defined in exactly one translation unit (eval.cu)
 __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
@@ -263,13 +267,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
     double gw = 1.0;
     {
       double c[3];
-      if (point_centre(a.src_kind, a.src, id, c)) {
+      const int64_t sid = a.gather ? a.gather[id] : id;
+      if (point_centre(a.src_kind, a.src, sid, c)) {
         x0 = __double2float_rn((c[0] - s_exp.norm_origin[0]) / s_exp.norm_scale);
         x1 = __double2float_rn((c[1] - s_exp.norm_origin[1]) / s_exp.norm_scale);
         x2 = __double2float_rn((c[2] - s_exp.norm_origin[2]) / s_exp.norm_scale);
         gw = gate_weight(s_exp.cell, a.subdomain_size, a.halo, c);
       } else {
-        const float* s = static_cast<const float*>(a.src) + 3 * id;
+        const float* s = static_cast<const float*>(a.src) + 3 * sid;
         x0 = s[0]; x1 = s[1]; x2 = s[2];
       }
     }
@@ -457,5 +462,6 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
   __syncthreads();
   if (tid < 32) tmem_dealloc(tmem_base, 512);
 }
+#endif  // NVDB_MLP_KERNEL_TU
 
 }  // namespace nvdb

@@ -49,6 +49,7 @@ int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int 
 // net `tag`), writing `out_mode` outputs.  Workspace from the caller.
 struct BlendOut {
   int32_t out_mode;
+  float* out_raw;
   double* out_probs;
   uint8_t* out_u8;
   float* out_f32;
@@ -57,7 +58,7 @@ struct BlendOut {
   int32_t clip;
 };
 size_t blended_workspace_bytes(const nvdb_netset* ns, int64_t n);
-int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, int64_t n, const BlendOut& o,
-                void* ws, size_t ws_bytes, cudaStream_t st);
+int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, const int64_t* gather, int64_t n,
+                const BlendOut& o, void* ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace nvdb

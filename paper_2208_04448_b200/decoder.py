@@ -1,0 +1,383 @@
+"""Whole-volume decode and the random-access hybrid grid on the GPU.
+
+Drop-in for ``decoder.decode_full`` / ``make_hybrid`` / ``HybridGrid.query``
+(decoder.py:101-270).  The host sequences the C-ABI primitives in the same
+order as the reference's ``_reconstruct`` / ``_fill_leaves``; all per-point
+work (classification, regression, blending, patches, fills) runs in the CUDA
+kernels of ``csrc/``.  Node indexing follows the reference: level-1 nodes in
+sorted-origin order (decoder.py:71), leaves in node order x ascending slot
+(decoder.py:146-151).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import EvalOut, check, lib
+from .errors import SvcodecError
+from .model import (L1_SIZE, L2_SIZE, LEAF_SIZE, DenseLeafGrid)
+from .netset import TAG_CODES, DeviceNetSet
+from .tree import DeviceTree
+
+EVAL_CHUNK = 1 << 24  # points per evaluator call on the multi-expert path
+
+
+def _dev(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2208_04448_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream(dev):
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor], byte_offset: int = 0):
+    return None if t is None else t.data_ptr() + byte_offset
+
+
+def _slot1(c) -> int:
+    """idx1 of a coordinate (grid.py:74-94)."""
+    return (((c[0] & 127) >> 3) << 8) | (((c[1] & 127) >> 3) << 4) | ((c[2] & 127) >> 3)
+
+
+def _slot0(c) -> int:
+    return ((c[0] & 7) << 6) | ((c[1] & 7) << 3) | (c[2] & 7)
+
+
+class DeviceModel:
+    """A container prepared for decoding: nets, node origins and patch tables on the GPU."""
+
+    def __init__(self, c, device=None):
+        self.c = c
+        self.dev = _dev(device)
+        meta = c.grid_meta
+        self.meta = meta
+        self.background = float(np.float32(meta.background))
+        self.value_scale = float(meta.value_scale)
+        experts = sorted(c.experts, key=lambda e: e.id)
+        self.ns = DeviceNetSet(experts, c.layout.size, c.layout.halo)
+        self.single = len(experts) == 1
+        self.has_tag = {t: any(dict(e.nets()).get(t) is not None for e in experts) for t in TAG_CODES}
+        ut = c.upper_tree
+        # level-1 origins validated against level-2 child bits (decoder.py:66-77)
+        l2 = {tuple(int(v) for v in n.origin): n for n in ut.l2_nodes}
+        expected = sum(int(np.count_nonzero(n.child_mask.bits)) for n in ut.l2_nodes)
+        if expected != len(ut.l1_origins):
+            raise SvcodecError(f"corrupt container: {len(ut.l1_origins)} level-1 origins vs "
+                               f"{expected} level-2 child bits")
+        origins = sorted(tuple(int(v) for v in o) for o in ut.l1_origins)
+        for o in origins:
+            root = tuple(v & ~4095 for v in o)
+            idx2 = (((o[0] & 4095) >> 7) << 10) | (((o[1] & 4095) >> 7) << 5) | ((o[2] & 4095) >> 7)
+            n2 = l2.get(root)
+            if n2 is None or not n2.child_mask.bits[idx2]:
+                raise SvcodecError(f"corrupt container: level-1 origin {o} has no level-2 child bit")
+        self.origins = np.asarray(origins, dtype=np.int64).reshape(-1, 3)
+        self.n1 = len(origins)
+        node_of = {o: i for i, o in enumerate(origins)}
+        self.node_of = node_of
+        self.d_origins = torch.from_numpy(self.origins.astype(np.int32)).to(self.dev)
+        # patch maps (decoder.py:84-92): later experts override earlier keys
+        l1m: Dict[tuple, int] = {}
+        l0m: Dict[tuple, Tuple[bool, float]] = {}
+        for e in c.experts:
+            for o, k in e.patches.l1:
+                l1m[tuple(int(v) for v in o)] = int(k)
+            for o, a, v in e.patches.l0:
+                l0m[tuple(int(v) for v in o)] = (bool(a), float(v))
+        p1s, p1c = [], []
+        for key, k in l1m.items():
+            ni = node_of.get(tuple(v & ~127 for v in key))
+            if ni is None:
+                raise SvcodecError(f"corrupt container: level-1 patch {key} outside every level-1 node")
+            p1s.append(ni * L1_SIZE + _slot1(key))
+            p1c.append(k)
+        self.p1_slot = self._i64(p1s)
+        self.p1_cls = self._u8(p1c)
+        ts, tv = [], []
+        for org, d in ut.l1_tiles.items():
+            ni = node_of.get(tuple(int(v) for v in org))
+            if ni is None:
+                raise SvcodecError(f"corrupt container: tile record for unknown level-1 node {org}")
+            for s1, v in d.items():
+                ts.append(ni * L1_SIZE + int(s1))
+                tv.append(v)
+        self.t_slot = self._i64(ts)
+        self.t_val = torch.tensor(np.asarray(tv, dtype=np.float32), device=self.dev)
+        ps, pv, pa, pval = [], [], [], []
+        self.l0_keys = []
+        for key, (a, v) in l0m.items():
+            ni = node_of.get(tuple(x & ~127 for x in key))
+            ps.append(-1 if ni is None else ni * L1_SIZE + _slot1(key))
+            pv.append(_slot0(key))
+            pa.append(int(a))
+            pval.append(v)
+            self.l0_keys.append(key)
+        self.p0_slot = self._i64(ps)
+        self.p0_vox = torch.tensor(np.asarray(pv, dtype=np.int32), device=self.dev)
+        self.p0_act = self._u8(pa)
+        self.p0_val = torch.tensor(np.asarray(pval, dtype=np.float32), device=self.dev)
+        ns_, nb = [], []
+        for org, bits in ut.leaf_negative_fill.items():
+            ni = node_of.get(tuple(int(v) & ~127 for v in org))
+            if ni is None:
+                continue
+            ns_.append(ni * L1_SIZE + _slot1(tuple(int(v) for v in org)))
+            nb.append(np.packbits(np.asarray(bits, dtype=bool), bitorder="little").view(np.uint64))
+        self.neg_slot = self._i64(ns_)
+        self.neg_bits = torch.from_numpy(np.asarray(nb, dtype=np.uint64).reshape(-1, 8).view(np.int64).copy()).to(self.dev)
+
+    def _i64(self, xs):
+        return torch.tensor(np.asarray(xs, dtype=np.int64), device=self.dev)
+
+    def _u8(self, xs):
+        return torch.tensor(np.asarray(xs, dtype=np.uint8), device=self.dev)
+
+    def close(self):
+        self.ns.close()
+
+    # -- primitives --------------------------------------------------------------
+
+    def evaluate(self, tag: str, src_kind: int, src: torch.Tensor, n: int, out_mode: int, *,
+                 gather: Optional[torch.Tensor] = None, u8=None, f32=None, probs=None, raw=None,
+                 value_scale: float = 1.0, clip: bool = False) -> None:
+        """nvdb_eval over n points, chunked on the multi-expert path."""
+        if n == 0:
+            return
+        fast = self.single and self.has_tag[tag]
+        chunk = n if fast else EVAL_CHUNK
+        if src_kind == _lib.SRC_LEAF_VOX and gather is None:
+            chunk = max(512, chunk // 512 * 512)
+        if src_kind == _lib.SRC_L1_SLOT and gather is None:
+            chunk = max(4096, chunk // 4096 * 4096)
+        k = 3 if tag == "l1" else 1
+        ws = None
+        if not fast:
+            wsb = lib().nvdb_eval_workspace_bytes(self.ns.handle, min(chunk, n))
+            ws = torch.empty(max(int(wsb), 1), dtype=torch.uint8, device=self.dev)
+        st = _stream(self.dev)
+        for s in range(0, n, chunk):
+            m = min(chunk, n - s)
+            if gather is not None:
+                g, sp = _ptr(gather, 8 * s), _ptr(src)
+            else:
+                g = None
+                per = {_lib.SRC_LEAF_VOX: (512, 12), _lib.SRC_L1_SLOT: (4096, 12),
+                       _lib.SRC_COORD_I32: (1, 12), _lib.SRC_CENTER_F64: (1, 24),
+                       _lib.SRC_NORM_F32: (1, 12)}[src_kind]
+                sp = _ptr(src, (s // per[0]) * per[1])
+            out = EvalOut(out_mode=out_mode,
+                          raw=_ptr(raw, 4 * k * s), probs=_ptr(probs, 8 * k * s),
+                          u8=_ptr(u8, s), f32=_ptr(f32, 4 * s), value_scale=float(value_scale),
+                          background=self.background, clip=int(bool(clip)))
+            check(lib().nvdb_eval(self.ns.handle, TAG_CODES[tag], src_kind, sp, g, m, C.byref(out),
+                                  _ptr(ws), 0 if ws is None else ws.numel(), st), "nvdb_eval")
+
+    def select(self, v: torch.Tensor, value: int) -> torch.Tensor:
+        """ids of v == value, ascending (one device->host count read)."""
+        n = v.numel()
+        ids = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        wsb = lib().nvdb_select_workspace_bytes(n)
+        ws = torch.empty(int(wsb), dtype=torch.uint8, device=self.dev)
+        check(lib().nvdb_select_u8(_ptr(v), n, value, _ptr(ids), _ptr(cnt), _ptr(ws), ws.numel(),
+                                   _stream(self.dev)), "nvdb_select_u8")
+        return ids[:int(cnt.item())]
+
+    # -- decode --------------------------------------------------------------------
+
+    def decode(self, materialize_values: bool = True) -> "DeviceDecode":
+        """decoder._reconstruct (decoder.py:101-211) on the device."""
+        dev, st = self.dev, _stream(self.dev)
+        n1 = self.n1
+        nslots = n1 * L1_SIZE
+        cls = torch.empty(max(nslots, 1), dtype=torch.uint8, device=dev)
+        tiles = torch.full((max(nslots, 1),), self.background, dtype=torch.float32, device=dev)
+        self.evaluate("l1", _lib.SRC_L1_SLOT, self.d_origins, nslots, _lib.OUT_L1CLASS, u8=cls)
+        check(lib().nvdb_l1_apply(_ptr(cls), _ptr(tiles), nslots, _ptr(self.p1_slot), _ptr(self.p1_cls),
+                                  self.p1_slot.numel(), _ptr(self.t_slot), _ptr(self.t_val), self.t_slot.numel(),
+                                  st), "nvdb_l1_apply")
+        active_tiles = self.select(cls[:nslots], 1)
+        if active_tiles.numel():
+            tv = torch.empty(active_tiles.numel(), dtype=torch.float32, device=dev)
+            # tile values scale by float(np.float32(value_scale)), no clip (decoder.py:141)
+            self.evaluate("tile", _lib.SRC_L1_SLOT, self.d_origins, active_tiles.numel(), _lib.OUT_VALUE,
+                          gather=active_tiles, f32=tv, value_scale=float(np.float32(self.value_scale)))
+            check(lib().nvdb_scatter_f32(_ptr(tiles), _ptr(active_tiles), _ptr(tv), active_tiles.numel(), st),
+                  "nvdb_scatter_f32")
+        child = self.select(cls[:nslots], 0)
+        nl = child.numel()
+        leaf_origins = torch.empty((max(nl, 1), 3), dtype=torch.int32, device=dev)
+        leaf_of_slot = torch.empty(max(nslots, 1), dtype=torch.int32, device=dev)
+        check(lib().nvdb_leaf_list(_ptr(child), nl, _ptr(self.d_origins), nslots, _ptr(leaf_origins),
+                                   _ptr(leaf_of_slot), st), "nvdb_leaf_list")
+        act = torch.zeros(max(nl * LEAF_SIZE, 1), dtype=torch.uint8, device=dev)
+        self.evaluate("l0", _lib.SRC_LEAF_VOX, leaf_origins, nl * LEAF_SIZE, _lib.OUT_L0ACTIVE, u8=act)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        check(lib().nvdb_l0_apply(_ptr(act), _ptr(self.p0_slot), _ptr(self.p0_vox), _ptr(self.p0_act),
+                                  self.p0_slot.numel(), _ptr(leaf_of_slot), _ptr(err), st), "nvdb_l0_apply")
+        evals = 0
+        act_ids = vals = None
+        if materialize_values and nl:
+            act_ids = self.select(act[:nl * LEAF_SIZE], 1)
+            evals = int(act_ids.numel())
+            vals = torch.empty(max(evals, 1), dtype=torch.float32, device=dev)
+            self.evaluate("voxel", _lib.SRC_LEAF_VOX, leaf_origins, evals, _lib.OUT_VALUE, gather=act_ids,
+                          f32=vals, value_scale=self.value_scale, clip=self.meta.grid_class == "sdf")
+        values = torch.empty(max(nl * LEAF_SIZE, 1), dtype=torch.float32, device=dev)
+        words = torch.empty(max(nl * 8, 1), dtype=torch.int64, device=dev)
+        patched = torch.empty(max(nl * LEAF_SIZE, 1), dtype=torch.uint8, device=dev)
+        check(lib().nvdb_leaf_finalize(nl, _ptr(act), _ptr(act_ids), _ptr(vals), evals, _ptr(self.p0_slot),
+                                       _ptr(self.p0_vox), _ptr(self.p0_act), _ptr(self.p0_val),
+                                       self.p0_slot.numel(), _ptr(self.neg_slot), _ptr(self.neg_bits),
+                                       self.neg_slot.numel(), _ptr(leaf_of_slot), self.background,
+                                       -float(np.float32(self.value_scale)), _ptr(values), _ptr(words),
+                                       _ptr(patched), st), "nvdb_leaf_finalize")
+        if int(err.item()):
+            raise SvcodecError("corrupt container: level-0 patch outside every reconstructed leaf")
+        return DeviceDecode(self, cls[:nslots], tiles[:nslots], child, leaf_origins[:nl], act[:nl * LEAF_SIZE],
+                            values[:nl * LEAF_SIZE], words[:nl * 8], patched[:nl * LEAF_SIZE], evals)
+
+
+@dataclass
+class DeviceDecode:
+    """Dense-leaf decode output, resident on the device."""
+
+    model: DeviceModel
+    l1_class: torch.Tensor      # (n1*4096,) u8, sorted-origin node order
+    l1_tiles: torch.Tensor      # (n1*4096,) f32
+    child_slots: torch.Tensor   # (nl,) int64 node*4096 + slot
+    leaf_origins: torch.Tensor  # (nl,3) int32
+    leaf_active: torch.Tensor   # (nl*512,) u8
+    leaf_values: torch.Tensor   # (nl*512,) f32
+    active_words: torch.Tensor  # (nl*8,) packed masks (int64 view of u64)
+    patched: torch.Tensor       # (nl*512,) u8
+    regressor_evaluations: int
+
+    @property
+    def leaf_count(self) -> int:
+        return int(self.leaf_origins.shape[0])
+
+    def to_grid(self) -> DenseLeafGrid:
+        """Host DenseLeafGrid in canonical (root, idx2, idx1) order."""
+        m = self.model
+        c = m.c
+        meta = c.grid_meta
+        bg = np.float32(meta.background)
+        n1 = m.n1
+        cls = self.l1_class.cpu().numpy().reshape(n1, L1_SIZE)
+        tiles = self.l1_tiles.cpu().numpy().reshape(n1, L1_SIZE)
+        lo = self.leaf_origins.cpu().numpy().astype(np.int64).reshape(-1, 3)
+        la = self.leaf_active.cpu().numpy().astype(bool).reshape(-1, LEAF_SIZE)
+        lv = self.leaf_values.cpu().numpy().reshape(-1, LEAF_SIZE)
+        # canonical order: by root key then origin within the root
+        roots = m.origins & ~np.int64(4095)
+        order = np.lexsort((m.origins[:, 2], m.origins[:, 1], m.origins[:, 0],
+                            roots[:, 2], roots[:, 1], roots[:, 0])) if n1 else np.zeros(0, np.int64)
+        counts = (cls == 0).sum(axis=1)
+        starts = np.concatenate([[0], np.cumsum(counts)[:-1]]) if n1 else np.zeros(0, np.int64)
+        leaf_perm = np.concatenate([np.arange(starts[i], starts[i] + counts[i]) for i in order]) \
+            if n1 else np.zeros(0, np.int64)
+        leaf_perm = leaf_perm.astype(np.int64)
+        ut = c.upper_tree
+        l2o = np.asarray([n.origin for n in ut.l2_nodes], dtype=np.int64).reshape(-1, 3)
+        o2 = np.lexsort((l2o[:, 2], l2o[:, 1], l2o[:, 0])) if len(l2o) else np.zeros(0, np.int64)
+        l2c = np.zeros((len(o2), L2_SIZE), bool)
+        l2a = np.zeros((len(o2), L2_SIZE), bool)
+        l2t = np.full((len(o2), L2_SIZE), bg, np.float32)
+        for j, i in enumerate(o2):
+            nd = ut.l2_nodes[i]
+            l2c[j] = nd.child_mask.bits
+            l2a[j] = nd.active_mask.bits
+            for k, v in nd.tiles.items():
+                l2t[j, int(k)] = v
+        return DenseLeafGrid(
+            background=float(meta.background), grid_class=meta.grid_class, voxel_size=float(meta.voxel_size),
+            half_width=float(meta.half_width), root_tiles=dict(ut.root_tiles),
+            l2_origins=l2o[o2], l2_child=l2c, l2_active=l2a, l2_tiles=l2t,
+            l1_origins=m.origins[order], l1_child=(cls == 0)[order], l1_active=(cls == 1)[order],
+            l1_tiles=tiles[order], leaf_origins=lo[leaf_perm], leaf_active=la[leaf_perm],
+            leaf_values=lv[leaf_perm])
+
+    def tree(self) -> DeviceTree:
+        """Device tree over this decode (hybrid topology for random access)."""
+        return DeviceTree.from_decode(self)
+
+
+def _as_model(c, device=None) -> DeviceModel:
+    return c if isinstance(c, DeviceModel) else DeviceModel(c, device)
+
+
+def decode_full(c, device=None, as_svcodec: bool = False):
+    """decoder.decode_full (decoder.py:214-217): the complete explicit grid.
+
+    Returns a :class:`DenseLeafGrid` (or an svcodec ``VdbGrid`` with
+    ``as_svcodec=True`` when the reference package is importable).
+    """
+    m = _as_model(c, device)
+    g = m.decode(True).to_grid()
+    return g.to_svcodec() if as_svcodec else g
+
+
+def decode_report(c, device=None) -> Dict[str, int]:
+    """decoder.decode_report (decoder.py:294-300)."""
+    m = _as_model(c, device)
+    d = m.decode(True)
+    return {"regressor_evaluations": d.regressor_evaluations,
+            "active_voxels": int(d.leaf_active.sum().item())}
+
+
+class HybridGrid:
+    """Explicit topology with neural leaf values (decoder.py:222-264)."""
+
+    def __init__(self, model: DeviceModel, topo: DeviceDecode):
+        self.model = model
+        self.container = model.c
+        self.topology_decode = topo
+        self.tree = topo.tree()
+        self.regressor_evaluations = 0
+
+    @property
+    def topology(self) -> DenseLeafGrid:
+        return self.topology_decode.to_grid()
+
+    def query_device(self, coords: torch.Tensor):
+        """(values f32, active u8) for device int32 coords (n,3)."""
+        m = self.model
+        dev, st = m.dev, _stream(m.dev)
+        n = coords.shape[0]
+        val, act, kind, leaf = self.tree.lookup(coords, want_leaf=True)
+        flag = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        check(lib().nvdb_neural_rows(_ptr(act), _ptr(kind), n, _ptr(flag), st), "nvdb_neural_rows")
+        rows = m.select(flag[:n], 1)
+        nr = rows.numel()
+        if nr:
+            reg = torch.empty(nr, dtype=torch.float32, device=dev)
+            m.evaluate("voxel", _lib.SRC_COORD_I32, coords, nr, _lib.OUT_VALUE, gather=rows, f32=reg,
+                       value_scale=m.value_scale, clip=m.meta.grid_class == "sdf")
+            check(lib().nvdb_query_finalize(_ptr(rows), nr, _ptr(reg), _ptr(coords), _ptr(leaf),
+                                            self.tree.handle, _ptr(val), st), "nvdb_query_finalize")
+        self.regressor_evaluations += nr
+        return val, act
+
+    def query(self, coords) -> Tuple[np.ndarray, np.ndarray]:
+        """Batched (value, active) at integer coordinates (decoder.py:239-264)."""
+        c = np.asarray(coords, dtype=np.int64).reshape(-1, 3)
+        if np.abs(c).max(initial=0) >= (1 << 30):
+            raise SvcodecError("coordinate outside legal range +-2^30")
+        d = torch.from_numpy(c.astype(np.int32)).to(self.model.dev)
+        v, a = self.query_device(d)
+        return v.cpu().numpy(), a.cpu().numpy().astype(bool)
+
+
+def make_hybrid(c, device=None) -> HybridGrid:
+    """decoder.make_hybrid (decoder.py:267-270)."""
+    m = _as_model(c, device)
+    return HybridGrid(m, m.decode(False))

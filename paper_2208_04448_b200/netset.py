@@ -30,12 +30,22 @@ def b2pi_f32(ff) -> np.ndarray:
 def _net_desc(params, ff, keep: list) -> NetDesc:
     layers = params.layers
     depth = len(layers) - 1
-    widths = {w.shape[0] for w, _ in layers[:-1]}
-    if len(widths) != 1:
-        raise ValueError("hidden layers must share one width")
-    width = widths.pop()
-    ws = [np.ascontiguousarray(w, dtype=np.float32) for w, _ in layers]
-    bs = [np.ascontiguousarray(b, dtype=np.float32) for _, b in layers]
+    # unequal hidden widths are zero-padded to the widest layer: padded units
+    # see zero weights and bias, act(0) = 0 for relu/tanh/sine, so the padded
+    # net computes the same function
+    width = max(w.shape[0] for w, _ in layers[:-1])
+    ws, bs = [], []
+    for li, (w, b) in enumerate(layers):
+        w = np.asarray(w, dtype=np.float32)
+        b = np.asarray(b, dtype=np.float32)
+        rows = w.shape[0] if li == depth else width
+        cols = w.shape[1] if li == 0 else width
+        wp = np.zeros((rows, cols), dtype=np.float32)
+        wp[:w.shape[0], :w.shape[1]] = w
+        bp = np.zeros(rows, dtype=np.float32)
+        bp[:b.shape[0]] = b
+        ws.append(np.ascontiguousarray(wp))
+        bs.append(bp)
     if ws[0].shape[1] != 2 * ff.m:
         raise ValueError(f"first layer expects {ws[0].shape[1]} inputs, features give {2 * ff.m}")
     b2 = b2pi_f32(ff)

@@ -60,22 +60,96 @@ def tree_arrays(grid: DenseLeafGrid):
 class DeviceTree:
     """Device-resident tree for ``nvdb_lookup``."""
 
-    def __init__(self, grid: DenseLeafGrid):
-        arr = tree_arrays(grid)
-        self._keep = {k: np.ascontiguousarray(v) for k, v in arr.items()}
-        p = lambda k: self._keep[k].ctypes.data_as(C.c_void_p)  # noqa: E731
-        d = TreeDesc(background=float(grid.background), nroots=self._keep["root_keys"].shape[0],
-                     n2=self._keep["l2_child"].shape[0], n1=self._keep["l1_child"].shape[0],
-                     nl=self._keep["leaf_active"].shape[0],
+    def __init__(self, grid: DenseLeafGrid = None, arrays=None, background: float = 0.0):
+        if grid is not None:
+            arrays = tree_arrays(grid)
+            background = float(grid.background)
+        keep = {}
+        for k, v in arrays.items():
+            keep[k] = v.contiguous() if isinstance(v, torch.Tensor) else np.ascontiguousarray(v)
+
+        def p(k):
+            v = keep.get(k)
+            if v is None:
+                return None
+            return v.data_ptr() if isinstance(v, torch.Tensor) else v.ctypes.data_as(C.c_void_p)
+
+        def rows(k, w):
+            v = keep[k]
+            return int(v.numel() // w) if isinstance(v, torch.Tensor) else int(v.size // w)
+
+        d = TreeDesc(background=float(background), nroots=rows("root_l2", 1), n2=rows("l2_child", 512),
+                     n1=rows("l1_child", 64), nl=rows("leaf_active", 8),
                      root_keys=p("root_keys"), root_l2=p("root_l2"), root_tile_value=p("root_tile_value"),
                      root_tile_active=p("root_tile_active"), l2_child=p("l2_child"), l2_active=p("l2_active"),
                      l2_tiles=p("l2_tiles"), l2_child_base=p("l2_child_base"), l1_child=p("l1_child"),
                      l1_active=p("l1_active"), l1_tiles=p("l1_tiles"), l1_child_base=p("l1_child_base"),
-                     leaf_active=p("leaf_active"), leaf_values=p("leaf_values"))
+                     leaf_active=p("leaf_active"), leaf_values=p("leaf_values"),
+                     leaf_patched=p("leaf_patched"))
+        torch.cuda.synchronize()
         h = C.c_void_p()
         check(lib().nvdb_tree_create(C.byref(d), C.byref(h)), "nvdb_tree_create")
         self.handle = h
-        del self._keep
+
+    @classmethod
+    def from_decode(cls, d) -> "DeviceTree":
+        """Hybrid topology of a device decode (decoder.py:52-81 + _fill_leaves wiring)."""
+        from ._lib import lib as _l  # noqa: WPS433
+        m = d.model
+        c = m.c
+        ut = c.upper_tree
+        dev = m.dev
+        st = torch.cuda.current_stream(dev).cuda_stream
+        n1 = m.n1
+        # level-2 nodes and roots from the container (explicit)
+        l2o = np.asarray([n.origin for n in ut.l2_nodes], dtype=np.int64).reshape(-1, 3)
+        o2 = np.lexsort((l2o[:, 2], l2o[:, 1], l2o[:, 0])) if len(l2o) else np.zeros(0, np.int64)
+        bg = np.float32(c.grid_meta.background)
+        l2c = np.zeros((len(o2), L2_SIZE), bool)
+        l2a = np.zeros((len(o2), L2_SIZE), bool)
+        l2t = np.full((len(o2), L2_SIZE), bg, np.float32)
+        for j, i in enumerate(o2):
+            nd = ut.l2_nodes[i]
+            l2c[j] = nd.child_mask.bits
+            l2a[j] = nd.active_mask.bits
+            for k, v in nd.tiles.items():
+                l2t[j, int(k)] = v
+        n2c = l2c.sum(axis=1)
+        l2_base = (np.concatenate([[0], np.cumsum(n2c)[:-1]]) if len(n2c) else np.zeros(0)).astype(np.int32)
+        roots = {tuple(int(v) for v in l2o[i]): (j, 0.0, False) for j, i in enumerate(o2)}
+        for k, (v, a) in ut.root_tiles.items():
+            roots.setdefault(tuple(int(x) for x in k), (-1, float(v), bool(a)))
+        keys = sorted(roots)
+        # level-1 nodes in tree order (root-major), leaves stay in decode order
+        rk = m.origins & ~np.int64(4095)
+        order = np.lexsort((m.origins[:, 2], m.origins[:, 1], m.origins[:, 0], rk[:, 2], rk[:, 1], rk[:, 0])) \
+            if n1 else np.zeros(0, np.int64)
+        order_t = torch.from_numpy(order.astype(np.int64)).to(dev)
+        cls2 = d.l1_class.view(max(n1, 1), L1_SIZE) if n1 else d.l1_class.view(0, L1_SIZE)
+        counts = (cls2 == 0).sum(dim=1)
+        starts = torch.cumsum(counts, 0) - counts
+        cw = torch.empty((max(n1, 1) * 64,), dtype=torch.int64, device=dev)
+        aw = torch.empty((max(n1, 1) * 64,), dtype=torch.int64, device=dev)
+        check(_l().nvdb_pack_eq(d.l1_class.data_ptr(), n1 * 64, 0, cw.data_ptr(), st), "pack child")
+        check(_l().nvdb_pack_eq(d.l1_class.data_ptr(), n1 * 64, 1, aw.data_ptr(), st), "pack active")
+        nl = d.leaf_count
+        pw = torch.empty((max(nl, 1) * 8,), dtype=torch.int64, device=dev)
+        check(_l().nvdb_pack_eq(d.patched.data_ptr(), nl * 8, 1, pw.data_ptr(), st), "pack patched")
+        arrays = dict(
+            root_keys=np.asarray(keys, dtype=np.int32).reshape(-1, 3),
+            root_l2=np.asarray([roots[k][0] for k in keys], dtype=np.int32),
+            root_tile_value=np.asarray([roots[k][1] for k in keys], dtype=np.float32),
+            root_tile_active=np.asarray([roots[k][2] for k in keys], dtype=np.uint8),
+            l2_child=_words(l2c, L2_SIZE), l2_active=_words(l2a, L2_SIZE), l2_tiles=l2t,
+            l2_child_base=l2_base,
+            l1_child=cw[:n1 * 64].view(n1, 64)[order_t] if n1 else cw[:0],
+            l1_active=aw[:n1 * 64].view(n1, 64)[order_t] if n1 else aw[:0],
+            l1_tiles=d.l1_tiles.view(n1, L1_SIZE)[order_t] if n1 else d.l1_tiles[:0],
+            l1_child_base=starts[order_t].to(torch.int32) if n1 else torch.zeros(0, dtype=torch.int32, device=dev),
+            leaf_active=d.active_words[:nl * 8], leaf_values=d.leaf_values[:nl * 512],
+            leaf_patched=pw[:nl * 8],
+        )
+        return cls(arrays=arrays, background=float(bg))
 
     def close(self) -> None:
         if getattr(self, "handle", None) is not None and self.handle.value:

@@ -216,7 +216,12 @@ def c1_fixture(path):
     h = make_hybrid(c)
     qv, qa = h.query(q)
     li, vi = np.nonzero(flat.leaf_active)
-    save("c1_sphere128", q=q, qv=qv, qa=qa,
+    g = gen_sphere_sdf(SphereSpec(center=(63.5, 63.5, 63.5), radius=61.0, voxel_size=1.0, half_width=3.0))
+    truth = DenseLeafGrid.from_svcodec(g)
+    ti, tv = np.nonzero(truth.leaf_active)
+    save("c1_sphere128", q=q, qv=qv, qa=qa, evals=np.array([decode_report(c)["regressor_evaluations"]]),
+         truth_leaf_origins=truth.leaf_origins, truth_active=np.packbits(truth.leaf_active, axis=1),
+         truth_values=truth.leaf_values[ti, tv],
          leaf_origins=flat.leaf_origins, leaf_active=np.packbits(flat.leaf_active, axis=1),
          active_values=flat.leaf_values[li, vi], l1_child=np.packbits(flat.l1_child, axis=1),
          l1_active=np.packbits(flat.l1_active, axis=1), **container_to_arrays(c))

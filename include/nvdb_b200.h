@@ -77,6 +77,8 @@ typedef struct nvdb_tree nvdb_tree;
 
 NVDB_API const char* nvdb_last_error(void);
 NVDB_API int nvdb_version(void);
+/* number of kernels this library has launched in this process */
+NVDB_API long long nvdb_launch_count(void);
 
 /* -- networks ------------------------------------------------------------- */
 

@@ -24,7 +24,7 @@ NVDB_ECORRUPT = -4
 NVDB_ENOMEM = -5
 
 EXPORTED = [
-    "nvdb_last_error", "nvdb_version", "nvdb_netset_create", "nvdb_netset_destroy",
+    "nvdb_last_error", "nvdb_version", "nvdb_launch_count", "nvdb_netset_create", "nvdb_netset_destroy",
     "nvdb_forward", "nvdb_eval_workspace_bytes", "nvdb_eval_blended", "nvdb_tree_create",
     "nvdb_tree_destroy", "nvdb_lookup", "nvdb_selftest_umma", "nvdb_eval",
     "nvdb_select_workspace_bytes", "nvdb_select_u8", "nvdb_l1_apply", "nvdb_scatter_f32",
@@ -76,6 +76,7 @@ def _declare(lib: C.CDLL) -> None:
     sig = {
         "nvdb_last_error": (C.c_char_p, []),
         "nvdb_version": (C.c_int, []),
+        "nvdb_launch_count": (C.c_longlong, []),
         "nvdb_netset_create": (C.c_int, [C.POINTER(NetDesc), i32, C.POINTER(ExpertDesc), i32, i32, i32,
                                          C.POINTER(vp)]),
         "nvdb_netset_destroy": (C.c_int, [vp]),

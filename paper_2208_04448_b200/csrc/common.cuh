@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -34,8 +35,16 @@ inline int fail(int code, const char* fmt, ...) {
                           __LINE__);                                                                 \
   } while (0)
 
+// every kernel launch of this library is followed by NVDB_CHECK_LAUNCH, which
+// also counts it (nvdb_launch_count; reported by bench.py as gpu_launches)
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> n{0};
+  return n;
+}
+
 #define NVDB_CHECK_LAUNCH()                                                                 \
   do {                                                                                      \
+    ::nvdb::launch_counter().fetch_add(1, std::memory_order_relaxed);                       \
     cudaError_t _e = cudaGetLastError();                                                    \
     if (_e != cudaSuccess)                                                                  \
       return ::nvdb::fail(NVDB_ECUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), \

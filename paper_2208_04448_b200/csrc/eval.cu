@@ -27,6 +27,7 @@ int round_up_i(int v, int a) { return (v + a - 1) / a * a; }
 
 extern "C" const char* nvdb_last_error(void) { return last_error_slot().c_str(); }
 extern "C" int nvdb_version(void) { return 1; }
+extern "C" long long nvdb_launch_count(void) { return launch_counter().load(); }
 
 // ---------------------------------------------------------------------------
 // netset

@@ -163,8 +163,13 @@ class DeviceModel:
             wsb = lib().nvdb_eval_workspace_bytes(self.ns.handle, min(chunk, n))
             ws = torch.empty(max(int(wsb), 1), dtype=torch.uint8, device=self.dev)
         st = _stream(self.dev)
+        timer = getattr(self, "timer", None)
         for s in range(0, n, chunk):
             m = min(chunk, n - s)
+            if timer is not None:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
             if gather is not None:
                 g, sp = _ptr(gather, 8 * s), _ptr(src)
             else:
@@ -179,6 +184,9 @@ class DeviceModel:
                           background=self.background, clip=int(bool(clip)))
             check(lib().nvdb_eval(self.ns.handle, TAG_CODES[tag], src_kind, sp, g, m, C.byref(out),
                                   _ptr(ws), 0 if ws is None else ws.numel(), st), "nvdb_eval")
+            if timer is not None:
+                ev1.record()
+                timer.append((tag, m, ev0, ev1))
 
     def select(self, v: torch.Tensor, value: int) -> torch.Tensor:
         """ids of v == value, ascending (one device->host count read)."""

@@ -214,6 +214,42 @@ NVDB_API int nvdb_query_finalize(const int64_t* rows, int64_t nrows, const float
                                  const int32_t* coords, const int32_t* leaf, const nvdb_tree* tree,
                                  float* value, void* stream);
 
+/* -- training (encoder.train_network, encoder.py:330-371) -------------------- */
+
+#define NVDB_LOSS_MSE 0
+#define NVDB_LOSS_CE 1
+#define NVDB_LOSS_BCE 2
+
+typedef struct nvdb_trainer nvdb_trainer;
+
+typedef struct {
+  nvdb_net_desc net;        /* initial (cold or warm) weights, HOST            */
+  int32_t loss_kind;        /* NVDB_LOSS_*                                      */
+  int64_t n;                /* training points                                  */
+  const float* inputs;      /* DEVICE (n,3) float32 normalized inputs           */
+  const float* targets;     /* DEVICE (n,) float32 targets (labels as floats)   */
+  int32_t batch;            /* cfg.batch_size                                   */
+  int32_t sampled;          /* 1: per-epoch Sampler draws (n > batch and not full-batch) */
+  int32_t sample_interval;  /* cfg.sample_interval (1 supported)                */
+  int32_t max_epochs;
+  const float* lr;          /* HOST (max_epochs) float32(lr_at(schedule, e))    */
+  const float* c1;          /* HOST (max_epochs) float32(1 - 0.9^(e+1))         */
+  const float* c2;          /* HOST (max_epochs) float32(1 - 0.999^(e+1))       */
+  const uint64_t* seed_words; /* HOST (max_epochs,4) SeedSequence((seed,0,e)).generate_state(4,u64) */
+  double target_loss;       /* early stop when the pre-update epoch loss < target */
+} nvdb_train_desc;
+
+NVDB_API int nvdb_trainer_create(const nvdb_train_desc* desc, nvdb_trainer** out);
+NVDB_API int nvdb_trainer_destroy(nvdb_trainer* tr);
+/* enqueue `epochs` epochs (sampler -> fwd/dgrad -> wgrad -> Adam); epochs
+ * after the early stop are no-ops on the device */
+NVDB_API int nvdb_trainer_run(nvdb_trainer* tr, int32_t epochs, void* stream);
+/* synchronous: epochs run so far, stop flag, per-epoch losses (HOST out) */
+NVDB_API int nvdb_trainer_status(const nvdb_trainer* tr, int32_t* epochs_done, int32_t* stopped,
+                                 double* losses, int32_t nlosses);
+/* fp32 master weights into HOST arrays shaped like nvdb_net_desc */
+NVDB_API int nvdb_trainer_weights(const nvdb_trainer* tr, float* const* weights, float* const* biases);
+
 /* -- diagnostics ------------------------------------------------------------ */
 
 /* One 128xN tcgen05 MMA over nk K-steps from caller-laid-out shared-memory

@@ -1,0 +1,1087 @@
+// Device-resident training of one coordinate network (K4 + K5): the whole
+// epoch loop of encoder.train_network (encoder.py:330-371) with
+// neural.fused_step (neural.py:444-524) split into four kernels per epoch:
+//
+//   k_sample_*      numpy-exact batch indices: SeedSequence words (host) ->
+//                   PCG64 jump-ahead -> buffered 32-bit Lemire (encoder.py:257-267)
+//   k_train_fb      per 128-sample tile: gather, Fourier features, forward on
+//                   tcgen05 (pre-activations kept in TMEM), fp32 head, loss and
+//                   dL/dout, then the dgrad chain back to layer 0 on tcgen05
+//                   (da = dz . W' with W' read as an MN-major operand).  Writes
+//                   the fp16 activation / dz tiles the weight gradients need.
+//   k_train_wgrad   weight gradients for every layer as tcgen05 GEMMs over the
+//                   batch (split-K over CTAs, fp32 TMEM accumulators; bias
+//                   gradients fall out of a ones column), per-CTA partials
+//   k_train_adam    fixed-order reduction of the partials, bias-corrected Adam
+//                   on fp32 master weights (numpy's op order and float32
+//                   constants), refreshed fp16 weight image, batch loss,
+//                   early stop flag.
+//
+// Loss scaling: dL/dout is kept without the 1/size factor (fp16 would
+// underflow at size 65536); the factor, and omega / amplitude folded into the
+// fp16 weights, are applied in fp32 in the Adam kernel.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "netset.cuh"
+
+using namespace nvdb;
+
+namespace {
+
+typedef unsigned __int128 u128;
+
+// ------------------------------------------------------------------ sampler
+__device__ __forceinline__ u128 pcg_mult() {
+  return ((u128)0x2360ED051FC65DA4ULL << 64) | (u128)0x4385DF649FCCF645ULL;
+}
+
+// state after `delta` LCG steps (pcg_advance_lcg_128)
+__device__ u128 pcg_advance(u128 state, u128 inc, unsigned long long delta) {
+  u128 cur_mult = pcg_mult(), cur_plus = inc, acc_mult = 1, acc_plus = 0;
+  while (delta > 0) {
+    if (delta & 1ull) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+__device__ __forceinline__ unsigned long long pcg_out(u128 s) {
+  const unsigned long long hi = (unsigned long long)(s >> 64), lo = (unsigned long long)s;
+  const unsigned rot = (unsigned)(s >> 122);
+  const unsigned long long x = hi ^ lo;
+  return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+// PCG64 seeded from SeedSequence.generate_state(4, uint64) words
+__device__ __forceinline__ void pcg_seed(const unsigned long long* w, u128& state, u128& inc) {
+  const u128 initstate = ((u128)w[0] << 64) | (u128)w[1];
+  const u128 initseq = ((u128)w[2] << 64) | (u128)w[3];
+  inc = (initseq << 1) | 1;
+  state = 0;
+  state = state * pcg_mult() + inc;
+  state += initstate;
+  state = state * pcg_mult() + inc;
+}
+
+struct SampCtl {
+  const int32_t* epoch;
+  const int32_t* stopped;
+  const unsigned long long* words;  // [max_epochs][4]
+  unsigned long long n;             // draw range [0, n)
+  int64_t batch;
+  int64_t nraw;
+  int32_t* flag;
+  uint32_t* val;
+  int32_t* pos;
+  int64_t* idx;
+};
+
+__global__ void k_sample_raw(SampCtl c) {
+  if (*c.stopped) return;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t j0 = t * 8;
+  if (j0 >= c.nraw) return;
+  u128 st, inc;
+  pcg_seed(c.words + 4 * (int64_t)(*c.epoch), st, inc);
+  st = pcg_advance(st, inc, (unsigned long long)(j0 >> 1));
+  const uint32_t nn = (uint32_t)c.n;
+  const uint32_t threshold = (uint32_t)(0u - nn) % nn;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    st = st * pcg_mult() + inc;
+    const unsigned long long o = pcg_out(st);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = j0 + 2 * d + h;
+      if (j < c.nraw) {
+        const uint32_t r = h ? (uint32_t)(o >> 32) : (uint32_t)o;
+        const unsigned long long m = (unsigned long long)r * nn;
+        c.flag[j] = ((uint32_t)m >= threshold) ? 1 : 0;
+        c.val[j] = (uint32_t)(m >> 32);
+      }
+    }
+  }
+}
+
+__global__ void k_sample_compact(SampCtl c) {
+  if (*c.stopped) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < c.nraw; j += stride)
+    if (c.flag[j] && c.pos[j] < c.batch) c.idx[c.pos[j]] = (int64_t)c.val[j];
+}
+
+// serial continuation if the parallel window had too many rejections
+__global__ void k_sample_tail(SampCtl c) {
+  if (*c.stopped || threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t have = c.pos[c.nraw - 1] + c.flag[c.nraw - 1];
+  if (have >= c.batch) return;
+  u128 st, inc;
+  pcg_seed(c.words + 4 * (int64_t)(*c.epoch), st, inc);
+  int64_t j = c.nraw;
+  st = pcg_advance(st, inc, (unsigned long long)(j >> 1));
+  unsigned long long o = 0;
+  if (j & 1) o = pcg_out(st);  // high half of the draw whose low half was used
+  const uint32_t nn = (uint32_t)c.n;
+  const uint32_t threshold = (uint32_t)(0u - nn) % nn;
+  while (have < c.batch) {
+    uint32_t r;
+    if ((j & 1) == 0) {
+      st = st * pcg_mult() + inc;
+      o = pcg_out(st);
+      r = (uint32_t)o;
+    } else {
+      r = (uint32_t)(o >> 32);
+    }
+    ++j;
+    const unsigned long long m = (unsigned long long)r * nn;
+    if ((uint32_t)m >= threshold) c.idx[have++] = (int64_t)(m >> 32);
+  }
+}
+
+__global__ void k_sample_ones(SampCtl c) {  // n == 1: numpy fills with 0 without drawing
+  if (*c.stopped) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < c.batch; j += stride) c.idx[j] = 0;
+}
+
+// ------------------------------------------------------------------ fwd + dgrad
+struct FbArgs {
+  NetDev net;                 // current fp16 image etc. (device pointers)
+  const float* xs;            // (n,3) normalized inputs
+  const float* ys;            // (n,) targets / labels as float
+  const int64_t* idx;         // batch -> point (nullable: identity)
+  int64_t batch;
+  int32_t loss_kind;          // 0 mse, 1 ce, 2 bce
+  int32_t nwg;
+  uint16_t* act_img;          // [depth][ntiles][128*W] fp16 tile images
+  uint16_t* dz_img;           // [depth][ntiles][128*W]
+  uint16_t* dlt_img;          // [ntiles][128*16]
+  double* loss_part;          // [grid]
+  const int32_t* stopped;
+  uint32_t w_off, region_off, region_bytes, small_off, bar_off;
+};
+
+__device__ __forceinline__ float act_deriv_from(int act, float zp) {
+  if (act == ACT_SINE) return __cosf(zp);
+  if (act == ACT_TANH) {
+    const float a = tanhf(zp);
+    return 1.0f - a * a;
+  }
+  return zp > 0.0f ? 1.0f : 0.0f;
+}
+
+__global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (*a.stopped) return;
+  const int tid = threadIdx.x;
+  const int wg = tid >> 7;
+  const int t = tid & 127;
+  const int wwarp = t >> 5;
+  const int nthreads = a.nwg * 128;
+  const NetDev& nd = a.net;
+  const int width = nd.width, depth = nd.depth, k0 = nd.k0, out_dim = nd.out_dim, act = nd.act;
+  const int mp = k0 >> 1;
+  uint8_t* wsm = smem + a.w_off;
+  float* small = reinterpret_cast<float*>(smem + a.small_off);
+  float* s_bias = small;
+  float* s_headw = small + 4 * 256;
+  float* s_headb = s_headw + 3 * 256;
+  float* s_b2pi = s_headb + 4;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  __shared__ double s_loss[8];
+
+  if (tid == 0) {
+    for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+    mbar_arrive_expect_tx(&bars[0], nd.wimg_bytes);
+    for (uint32_t off = 0; off < nd.wimg_bytes; off += 32768)
+      bulk_g2s(wsm + off, nd.wimg + off, min(32768u, nd.wimg_bytes - off), &bars[0]);
+  }
+  if (tid < 32) tmem_alloc(tmem_slot, 512);
+  for (int i = tid; i < depth * width; i += nthreads) s_bias[i] = nd.bias[i];
+  for (int i = tid; i < out_dim * width; i += nthreads) s_headw[i] = nd.headw[i];
+  if (tid < out_dim) s_headb[tid] = nd.headb[tid];
+  for (int i = tid; i < 3 * mp; i += nthreads) s_b2pi[i] = nd.b2pi[i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  mbar_wait(&bars[0], 0);
+  const uint32_t tmem_base = *tmem_slot;
+  uint64_t* bar_c0 = &bars[1 + 3 * wg];
+  uint64_t* bar_layer = &bars[3 + 3 * wg];
+  uint32_t ncommit0 = 0, ncommit1 = 0, nlayer = 0;
+  bool pend0 = false, pend1 = false;
+  const uint32_t tcol = tmem_base + (uint32_t)(wg * (a.nwg == 2 ? 256 : 0));
+  const uint32_t lane_off = (uint32_t)(wwarp * 32) << 16;
+  const uint32_t region_s = smem_addr(smem + a.region_off + wg * a.region_bytes);
+  const uint32_t w_s = smem_addr(wsm);
+  const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
+  const uint32_t idesc_bt = idesc_f16(kTileM, width, 0, 1);  // B = W'^T read MN-major
+
+  const int64_t ntiles = (a.batch + kTileM - 1) / kTileM;
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  double loss_acc = 0.0;
+  const size_t tile_elems = (size_t)kTileM * width;
+
+  for (int64_t tau = t0 + wg; tau < t1; tau += a.nwg) {
+    const int64_t b = tau * kTileM + t;
+    const bool valid = b < a.batch;
+    const int64_t pidx = valid ? (a.idx ? a.idx[b] : b) : 0;
+    const float x0 = a.xs[3 * pidx], x1 = a.xs[3 * pidx + 1], x2 = a.xs[3 * pidx + 2];
+    const float y = a.ys[pidx];
+    // ---------------- features + layer 0 (as in mlp_eval_kernel)
+    const int nch = k0 / kChunkK;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int bsel = ch & 1;
+      if (bsel == 0 && pend0) { mbar_wait(bar_c0, (ncommit0 - 1u) & 1u); pend0 = false; }
+      if (bsel == 1 && pend1) { mbar_wait(bar_c0 + 1, (ncommit1 - 1u) & 1u); pend1 = false; }
+      const uint32_t buf = region_s + bsel * kChunkBytes;
+#pragma unroll
+      for (int q = 0; q < kChunkK / 8; ++q) {
+        uint32_t h[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int f = ch * (kChunkK / 2) + q * 4 + j;
+          const float th = fmaf(x2, s_b2pi[2 * mp + f], fmaf(x1, s_b2pi[mp + f], x0 * s_b2pi[f]));
+          float sn, cs;
+          __sincosf(th, &sn, &cs);
+          h[j] = pack_half2(cs, sn);
+        }
+        st_shared_v4(buf + kmajor_offset(t, q * 8, kTileM), h[0], h[1], h[2], h[3]);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      named_bar_sync(1 + wg, 128);
+      if (t == 0) {
+        tc_fence_after();
+#pragma unroll
+        for (int s = 0; s < kChunkK / 16; ++s) {
+          const uint64_t ad = smem_desc(buf + s * (2 * kTileM * 16), kTileM * 16, 128);
+          const uint32_t wb = w_s + (uint32_t)(((ch * kChunkK + s * 16) >> 3) * (width >> 3) * 128);
+          umma_f16(tcol, ad, smem_desc(wb, width * 16, 128), idesc, (ch | s) != 0);
+        }
+        umma_commit(bar_c0 + bsel);
+        if (ch == nch - 1) umma_commit(bar_layer);
+      }
+      if (bsel == 0) { ncommit0++; pend0 = true; } else { ncommit1++; pend1 = true; }
+    }
+    mbar_wait(bar_layer, nlayer & 1u);
+    nlayer++;
+    pend0 = pend1 = false;
+    tc_fence_after();
+    // ---------------- hidden layers: z_h stays in TMEM columns [h*W, (h+1)*W)
+    float yv[3] = {0.f, 0.f, 0.f};
+    uint32_t woff = (uint32_t)(width * k0 * 2);
+    for (int l = 0; l < depth; ++l) {
+      const bool last = (l == depth - 1);
+      const float* bl = s_bias + l * width;
+      uint16_t* gact = a.act_img + ((size_t)l * ntiles + tau) * tile_elems;
+      for (int cc = 0; cc < width / 16; ++cc) {
+        float v[16];
+        tmem_ld16(tcol + lane_off + l * width + cc * 16, v);
+        tmem_ld_wait();
+        float av[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) av[i] = act_fn(act, v[i] + bl[cc * 16 + i]);
+        const uint32_t p0 = pack_half2(av[0], av[1]), p1 = pack_half2(av[2], av[3]);
+        const uint32_t p2 = pack_half2(av[4], av[5]), p3 = pack_half2(av[6], av[7]);
+        const uint32_t p4 = pack_half2(av[8], av[9]), p5 = pack_half2(av[10], av[11]);
+        const uint32_t p6 = pack_half2(av[12], av[13]), p7 = pack_half2(av[14], av[15]);
+        const uint32_t o0 = kmajor_offset(t, cc * 16, kTileM), o1 = kmajor_offset(t, cc * 16 + 8, kTileM);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o0) = make_uint4(p0, p1, p2, p3);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o1) = make_uint4(p4, p5, p6, p7);
+        if (!last) {
+          st_shared_v4(region_s + o0, p0, p1, p2, p3);
+          st_shared_v4(region_s + o1, p4, p5, p6, p7);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            if (k < out_dim) {
+              float s = yv[k];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) s = fmaf(av[i], s_headw[k * width + cc * 16 + i], s);
+              yv[k] = s;
+            }
+          }
+        }
+      }
+      if (!last) {
+        fence_async_smem();
+        tc_fence_before();
+        named_bar_sync(1 + wg, 128);
+        if (t == 0) {
+          tc_fence_after();
+          const uint32_t wl = w_s + woff;
+          for (int s = 0; s < width / 16; ++s) {
+            const uint64_t ad = smem_desc(region_s + s * (2 * kTileM * 16), kTileM * 16, 128);
+            const uint64_t bd = smem_desc(wl + (uint32_t)(s * 2 * (width >> 3) * 128), width * 16, 128);
+            umma_f16(tcol + (l + 1) * width, ad, bd, idesc, s != 0);
+          }
+          umma_commit(bar_layer);
+        }
+        woff += (uint32_t)(width * width * 2);
+        mbar_wait(bar_layer, nlayer & 1u);
+        nlayer++;
+        tc_fence_after();
+      }
+    }
+    // ---------------- head, loss, dL/dout (neural.py:271-302, without 1/size)
+    float dl[3] = {0.f, 0.f, 0.f};
+    float lterm = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (k < out_dim) yv[k] += s_headb[k];
+    if (valid) {
+      if (a.loss_kind == 0) {  // mse
+        const float d = yv[0] - y;
+        lterm = d * d;
+        dl[0] = 2.0f * d;
+      } else if (a.loss_kind == 2) {  // bce
+        const float z = yv[0];
+        lterm = fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
+        dl[0] = 1.0f / (1.0f + expf(-z)) - y;
+      } else {  // ce, 3 classes
+        const float zm = fmaxf(fmaxf(yv[0], yv[1]), yv[2]);
+        const float e0 = expf(yv[0] - zm), e1 = expf(yv[1] - zm), e2 = expf(yv[2] - zm);
+        const float s = (e0 + e1) + e2;
+        const int lab = (int)y;
+        const float zl = lab == 0 ? yv[0] : (lab == 1 ? yv[1] : yv[2]);
+        lterm = -(zl - zm - logf(s));
+        dl[0] = e0 / s - (lab == 0 ? 1.f : 0.f);
+        dl[1] = e1 / s - (lab == 1 ? 1.f : 0.f);
+        dl[2] = e2 / s - (lab == 2 ? 1.f : 0.f);
+      }
+    }
+    {  // dL/dout tile image (128 x 16, fp16)
+      uint8_t* gd = reinterpret_cast<uint8_t*>(a.dlt_img + (size_t)tau * kTileM * 16);
+      *reinterpret_cast<uint4*>(gd + kmajor_offset(t, 0, kTileM)) =
+          make_uint4(pack_half2(dl[0], dl[1]), pack_half2(dl[2], 0.f), 0u, 0u);
+      *reinterpret_cast<uint4*>(gd + kmajor_offset(t, 8, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    // deterministic loss sum: warp shuffle, then fixed warp order
+    float ls = lterm;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    if ((t & 31) == 0) s_loss[wg * 4 + wwarp] = (double)ls;
+    named_bar_sync(1 + wg, 128);
+    if (t == 0) loss_acc += ((s_loss[wg * 4] + s_loss[wg * 4 + 1]) + s_loss[wg * 4 + 2]) + s_loss[wg * 4 + 3];
+    // ---------------- backward: dz_h = da_h * f'(z'_h); da_{h-1} = dz_h . W'_h
+    for (int l = depth - 1; l >= 0; --l) {
+      const float* bl = s_bias + l * width;
+      uint16_t* gdz = a.dz_img + ((size_t)l * ntiles + tau) * tile_elems;
+      for (int cc = 0; cc < width / 16; ++cc) {
+        float z[16], da[16];
+        tmem_ld16(tcol + lane_off + l * width + cc * 16, z);
+        if (l < depth - 1) tmem_ld16(tcol + lane_off + (l + 1) * width + cc * 16, da);
+        tmem_ld_wait();
+        if (l == depth - 1) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float s = 0.f;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              if (k < out_dim) s = fmaf(dl[k], s_headw[k * width + cc * 16 + i], s);
+            da[i] = s;
+          }
+        }
+        float dz[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dz[i] = valid ? da[i] * act_deriv_from(act, z[i] + bl[cc * 16 + i]) : 0.f;
+        const uint32_t p0 = pack_half2(dz[0], dz[1]), p1 = pack_half2(dz[2], dz[3]);
+        const uint32_t p2 = pack_half2(dz[4], dz[5]), p3 = pack_half2(dz[6], dz[7]);
+        const uint32_t p4 = pack_half2(dz[8], dz[9]), p5 = pack_half2(dz[10], dz[11]);
+        const uint32_t p6 = pack_half2(dz[12], dz[13]), p7 = pack_half2(dz[14], dz[15]);
+        const uint32_t o0 = kmajor_offset(t, cc * 16, kTileM), o1 = kmajor_offset(t, cc * 16 + 8, kTileM);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o0) = make_uint4(p0, p1, p2, p3);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o1) = make_uint4(p4, p5, p6, p7);
+        if (l > 0) {
+          st_shared_v4(region_s + o0, p0, p1, p2, p3);
+          st_shared_v4(region_s + o1, p4, p5, p6, p7);
+        }
+      }
+      if (l > 0) {
+        fence_async_smem();
+        tc_fence_before();
+        named_bar_sync(1 + wg, 128);
+        if (t == 0) {
+          tc_fence_after();
+          // W'_l image (rows o, cols i, K-major) read as B = (N = i, K = o) MN-major
+          const uint32_t wl = w_s + (uint32_t)(width * k0 * 2) + (uint32_t)((l - 1) * width * width * 2);
+          for (int s = 0; s < width / 16; ++s) {
+            const uint64_t ad = smem_desc(region_s + s * (2 * kTileM * 16), kTileM * 16, 128);
+            const uint64_t bd = smem_desc(wl + (uint32_t)(s * 256), 128, width * 16);
+            umma_f16(tcol + l * width, ad, bd, idesc_bt, s != 0);
+          }
+          umma_commit(bar_layer);
+        }
+        mbar_wait(bar_layer, nlayer & 1u);
+        nlayer++;
+        tc_fence_after();
+      }
+    }
+    named_bar_sync(1 + wg, 128);  // all TMEM reads of this tile done before the next tile's MMAs
+  }
+  // per-CTA loss partial (fixed order: WG0 then WG1)
+  __shared__ double s_wgl[2];
+  if (t == 0) s_wgl[wg] = loss_acc;
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) a.loss_part[blockIdx.x] = a.nwg == 2 ? s_wgl[0] + s_wgl[1] : s_wgl[0];
+  if (tid < 32) tmem_dealloc(tmem_base, 512);
+}
+
+// ------------------------------------------------------------------ weight gradients
+struct WgArgs {
+  NetDev net;
+  int32_t m;                  // real frequency count (2m real features)
+  int32_t width_real;         // real hidden width
+  const float* xs;
+  const int64_t* idx;
+  int64_t batch;
+  const uint16_t* act_img;
+  const uint16_t* dz_img;
+  const uint16_t* dlt_img;
+  float* partial;             // [grid][P]
+  int64_t P;
+  const int64_t* poff;        // per layer l: offset of W_l, then of b_l ([2*(depth+1)])
+  const int32_t* stopped;
+  uint32_t col_w0, col_b0, col_h, col_head;  // TMEM column bases
+};
+
+__global__ void __launch_bounds__(128, 1) k_train_wgrad(const WgArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (*a.stopped) return;
+  const int t = threadIdx.x;
+  const int wwarp = t >> 5;
+  const NetDev& nd = a.net;
+  const int W = nd.width, depth = nd.depth, k0 = nd.k0, mp = k0 >> 1;
+  // smem: act buf (32K) | dz buf (32K) | feat ring 2x32K | dlt (4K) | ones (4K) | b2pi | bars
+  uint8_t* s_act = smem;
+  uint8_t* s_dz = smem + 32768;
+  uint8_t* s_feat = smem + 65536;
+  uint8_t* s_dlt = smem + 131072;
+  uint8_t* s_ones = smem + 135168;
+  float* s_b2pi = reinterpret_cast<float*>(smem + 139264);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 139264 + 3 * 512 * 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  // bars[0] loads, bars[1] mma done, bars[2] feat buf 0, bars[3] feat buf 1
+  if (t == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  if (t < 32) tmem_alloc(tmem_slot, 512);
+  for (int i = t; i < 3 * mp; i += 128) s_b2pi[i] = nd.b2pi[i];
+  // ones tile (B operand, N = 16, K = 128 samples) and the ones column of the
+  // augmented activation buffer (column W = 1, W+1..W+15 = 0)
+  for (int i = t; i < 16 * 128; i += 128) reinterpret_cast<__half*>(s_ones)[i] = __float2half(1.0f);
+  {
+    const uint32_t o0 = kmajor_offset(t, W, kTileM), o1 = kmajor_offset(t, W + 8, kTileM);
+    *reinterpret_cast<uint4*>(s_act + o0) = make_uint4(pack_half2(1.f, 0.f), 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(s_act + o1) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_off = (uint32_t)(wwarp * 32) << 16;
+  uint32_t nload = 0, nmma = 0, nf0 = 0, nf1 = 0;
+  bool pf0 = false, pf1 = false;
+  const int64_t ntiles = (a.batch + kTileM - 1) / kTileM;
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  const size_t tbytes = (size_t)kTileM * W * 2;
+  const uint32_t sa = smem_addr(s_act), sdz = smem_addr(s_dz), sfe = smem_addr(s_feat);
+  const uint32_t sdl = smem_addr(s_dlt), son = smem_addr(s_ones);
+  const int nmt = (k0 + 127) / 128;  // M tiles of 128 features
+  bool first = true;
+
+  auto load = [&](uint8_t* dst, const void* src, uint32_t bytes) {
+    bulk_g2s(dst, src, bytes, &bars[0]);
+  };
+
+  for (int64_t tau = t0; tau < t1; ++tau) {
+    const int64_t b = tau * kTileM + t;
+    const bool valid = b < a.batch;
+    const int64_t pidx = valid ? (a.idx ? a.idx[b] : b) : 0;
+    const float x0 = a.xs[3 * pidx], x1 = a.xs[3 * pidx + 1], x2 = a.xs[3 * pidx + 2];
+    // ---- layer 0: gW0^T[k][o] += F^T dz0, gb0 += dz0^T 1
+    if (t == 0) {
+      mbar_arrive_expect_tx(&bars[0], (uint32_t)tbytes);
+      load(s_dz, reinterpret_cast<const uint8_t*>(a.dz_img) + tau * tbytes, (uint32_t)tbytes);
+    }
+    mbar_wait(&bars[0], nload & 1u);
+    nload++;
+    for (int j = 0; j < nmt; ++j) {
+      const int bsel = j & 1;
+      if (bsel == 0 && pf0) { mbar_wait(&bars[2], (nf0 - 1u) & 1u); pf0 = false; }
+      if (bsel == 1 && pf1) { mbar_wait(&bars[3], (nf1 - 1u) & 1u); pf1 = false; }
+      const uint32_t fb = sfe + bsel * 32768;
+      const int nf = min(128, k0 - j * 128);
+      for (int q = 0; q < nf / 8; ++q) {
+        uint32_t h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int f = j * 64 + q * 4 + i;
+          const float th = fmaf(x2, s_b2pi[2 * mp + f], fmaf(x1, s_b2pi[mp + f], x0 * s_b2pi[f]));
+          float sn, cs;
+          __sincosf(th, &sn, &cs);
+          h[i] = valid ? pack_half2(cs, sn) : 0u;
+        }
+        st_shared_v4(fb + kmajor_offset(t, q * 8, kTileM), h[0], h[1], h[2], h[3]);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (t == 0) {
+        tc_fence_after();
+        const uint32_t idesc = idesc_f16(kTileM, W, 1, 1);
+        for (int s = 0; s < kTileM / 16; ++s)
+          umma_f16(tmem + a.col_w0 + j * W, smem_desc(fb + s * 256, 128, 2048), smem_desc(sdz + s * 256, 128, 2048),
+                   idesc, (!first || s != 0) ? 1u : 0u);
+        umma_commit(&bars[2 + bsel]);
+      }
+      if (bsel == 0) { nf0++; pf0 = true; } else { nf1++; pf1 = true; }
+    }
+    if (t == 0) {
+      const uint32_t idesc = idesc_f16(kTileM, 16, 1, 0);
+      for (int s = 0; s < kTileM / 16; ++s)
+        umma_f16(tmem + a.col_b0, smem_desc(sdz + s * 256, 128, 2048), smem_desc(son + s * 512, 256, 128), idesc,
+                 (!first || s != 0) ? 1u : 0u);
+      umma_commit(&bars[1]);
+    }
+    mbar_wait(&bars[1], nmma & 1u);
+    nmma++;
+    pf0 = pf1 = false;
+    // ---- hidden layers h >= 1: gW_h^T[i][o] += [a_{h-1} | 1]^T dz_h
+    for (int l = 1; l <= depth; ++l) {
+      const bool head = (l == depth);
+      if (t == 0) {
+        tc_fence_after();
+        const uint32_t bytes = (uint32_t)tbytes + (head ? (uint32_t)(kTileM * 16 * 2) : (uint32_t)tbytes);
+        mbar_arrive_expect_tx(&bars[0], bytes);
+        load(s_act, reinterpret_cast<const uint8_t*>(a.act_img) + ((size_t)(l - 1) * ntiles + tau) * tbytes,
+             (uint32_t)tbytes);
+        if (head)
+          load(s_dlt, reinterpret_cast<const uint8_t*>(a.dlt_img) + (size_t)tau * kTileM * 16 * 2, kTileM * 16 * 2);
+        else
+          load(s_dz, reinterpret_cast<const uint8_t*>(a.dz_img) + ((size_t)l * ntiles + tau) * tbytes,
+               (uint32_t)tbytes);
+      }
+      mbar_wait(&bars[0], nload & 1u);
+      nload++;
+      if (t == 0) {
+        const int N = head ? 16 : W;
+        const uint32_t idesc = idesc_f16(kTileM, N, 1, 1);
+        const uint32_t col = head ? a.col_head : a.col_h + (l - 1) * W;
+        const uint32_t bsrc = head ? sdl : sdz;
+        for (int s = 0; s < kTileM / 16; ++s)
+          umma_f16(tmem + col, smem_desc(sa + s * 256, 128, 2048), smem_desc(bsrc + s * 256, 128, 2048), idesc,
+                   (!first || s != 0) ? 1u : 0u);
+        umma_commit(&bars[1]);
+      }
+      mbar_wait(&bars[1], nmma & 1u);
+      nmma++;
+    }
+    first = false;
+    tc_fence_after();
+  }
+  // ---- flush per-CTA partials (zeros when this CTA had no tiles)
+  float* part = a.partial + (size_t)blockIdx.x * a.P;
+  const int Wr = a.width_real, K0r = 2 * a.m;
+  auto rd = [&](uint32_t col, float (&v)[16]) {
+    if (first) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    } else {
+      tmem_ld16(tmem + lane_off + col, v);
+      tmem_ld_wait();
+    }
+  };
+  // gW0: lane t of M tile j = feature k = 128 j + t ; W0 (Wr x K0r)
+  for (int j = 0; j < nmt; ++j) {
+    const int k = j * 128 + t;
+    for (int cc = 0; cc < W / 16; ++cc) {
+      float v[16];
+      rd(a.col_w0 + j * W + cc * 16, v);
+      if (k < K0r)
+        for (int i = 0; i < 16; ++i) {
+          const int o = cc * 16 + i;
+          if (o < Wr) part[a.poff[0] + (int64_t)o * K0r + k] = v[i];
+        }
+    }
+  }
+  {
+    float v[16];
+    rd(a.col_b0, v);
+    if (t < Wr) part[a.poff[1] + t] = v[0];
+  }
+  for (int l = 1; l <= depth; ++l) {
+    const bool head = (l == depth);
+    const int N = head ? 16 : W;
+    const int outs = head ? nd.out_dim : Wr;
+    const uint32_t col = head ? a.col_head : a.col_h + (l - 1) * W;
+    for (int cc = 0; cc < N / 16; ++cc) {
+      float v[16];
+      rd(col + cc * 16, v);
+      for (int i = 0; i < 16; ++i) {
+        const int o = cc * 16 + i;
+        if (o >= outs) continue;
+        if (t < Wr) part[a.poff[2 * l] + (int64_t)o * Wr + t] = v[i];
+        if (t == W) part[a.poff[2 * l + 1] + o] = v[i];  // ones column -> bias gradient
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (t < 32) tmem_dealloc(tmem, 512);
+}
+
+// ------------------------------------------------------------------ reduce + Adam
+struct AdamArgs {
+  const float* partial;
+  int32_t ncta;
+  int64_t P;
+  float* wmaster;      // [P] current params (serialized layout)
+  float* mom;          // [P]
+  float* vel;          // [P]
+  const float* gscale; // [P] per-param gradient scale (1/size, omega, amplitude)
+  const int32_t* img_off;   // [P] fp16 weight image element index or -1
+  const float* img_fold;    // [P] fold factor for the image (omega [* amp])
+  uint16_t* wimg;
+  const int32_t* f32_dst;   // [P] index into f32 param block (bias' / head) or -1
+  float* f32_block;
+  const float* lr;     // [max_epochs]
+  const float* c1;     // [max_epochs] float32(1 - b1^t)
+  const float* c2;
+  const double* loss_part;
+  int32_t nloss;
+  double loss_den;
+  double target;
+  int32_t* epoch;
+  int32_t* stopped;
+  int32_t* epochs_done;
+  double* loss_hist;
+};
+
+__global__ void k_train_adam(AdamArgs a) {
+  if (*a.stopped) return;
+  const int e = *a.epoch;
+  const float lr = a.lr[e], c1 = a.c1[e], c2 = a.c2[e];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.P; q += stride) {
+    float g = 0.f;
+    for (int c = 0; c < a.ncta; ++c) g += a.partial[(size_t)c * a.P + q];
+    g *= a.gscale[q];
+    // numpy float32 arithmetic with weak python scalars (neural.py:508-523)
+    float m = a.mom[q] * 0.9f;
+    m = m + 0.1f * g;
+    float v = a.vel[q] * 0.999f;
+    v = v + 0.001f * (g * g);
+    a.mom[q] = m;
+    a.vel[q] = v;
+    const float upd = lr * (m / c1) / (sqrtf(v / c2) + 1e-8f);
+    const float w = a.wmaster[q] - upd;
+    a.wmaster[q] = w;
+    if (a.img_off[q] >= 0) {
+      __half h = __float2half_rn(w * a.img_fold[q]);
+      a.wimg[a.img_off[q]] = *reinterpret_cast<uint16_t*>(&h);
+    }
+    if (a.f32_dst[q] >= 0) a.f32_block[a.f32_dst[q]] = w * a.img_fold[q];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int c = 0; c < a.nloss; ++c) s += a.loss_part[c];
+    const double loss = s / a.loss_den;
+    a.loss_hist[e] = loss;
+    if (loss < a.target) {
+      *a.stopped = 1;
+      *a.epochs_done = e + 1;
+    }
+  }
+}
+
+__global__ void k_train_advance(int32_t* epoch, const int32_t* stopped, int32_t* epochs_done) {
+  if (*stopped) return;
+  *epoch += 1;
+  *epochs_done = *epoch;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host trainer
+struct nvdb_trainer {
+  nvdb_train_desc d{};
+  int W = 0, Wr = 0, k0 = 0, depth = 0, out_dim = 0, m = 0;
+  int64_t P = 0, batch = 0, ntiles = 0, nraw = 0;
+  int fb_grid = 0, wg_grid = 0, nwg = 1;
+  NetDev net{};
+  uint32_t wg_smem = 0;
+  SmemPlan plan{};
+  std::vector<int64_t> poff;
+  std::vector<std::pair<int64_t, int64_t>> layer_shape;  // (out, in)
+  // device buffers
+  uint8_t* blob = nullptr;   // image + bias' + head + b2pi
+  float* wmaster = nullptr;
+  float* mom = nullptr;
+  float* vel = nullptr;
+  float* gscale = nullptr;
+  int32_t* img_off = nullptr;
+  float* img_fold = nullptr;
+  int32_t* f32_dst = nullptr;
+  float* partial = nullptr;
+  double* loss_part = nullptr;
+  uint16_t* act_img = nullptr;
+  uint16_t* dz_img = nullptr;
+  uint16_t* dlt_img = nullptr;
+  int64_t* idx = nullptr;
+  int32_t* sflag = nullptr;
+  uint32_t* sval = nullptr;
+  int32_t* spos = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  unsigned long long* words = nullptr;
+  float* lr = nullptr;
+  float* c1 = nullptr;
+  float* c2 = nullptr;
+  int32_t* ctl = nullptr;  // epoch, stopped, epochs_done
+  double* loss_hist = nullptr;
+  int64_t* dpoff = nullptr;
+  std::vector<void*> owned;
+};
+
+namespace {
+
+template <class T>
+int dalloc(nvdb_trainer* tr, T** p, size_t count) {
+  NVDB_CUDA_TRY(cudaMalloc(p, sizeof(T) * std::max<size_t>(count, 1)));
+  tr->owned.push_back(*p);
+  return NVDB_OK;
+}
+
+}  // namespace
+
+extern "C" int nvdb_trainer_destroy(nvdb_trainer* tr) {
+  if (!tr) return NVDB_OK;
+  for (void* p : tr->owned) cudaFree(p);
+  delete tr;
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out) {
+  if (!d || !out) return fail(NVDB_EINVAL, "nvdb_trainer_create: null argument");
+  const nvdb_net_desc& nd = d->net;
+  if (nd.out_dim != 1 && nd.out_dim != 3) return fail(NVDB_EINVAL, "out_dim must be 1 or 3");
+  if ((d->loss_kind == 1) != (nd.out_dim == 3)) return fail(NVDB_EINVAL, "ce loss needs a 3-wide head and vice versa");
+  if (d->n < 1 || d->batch < 1 || d->max_epochs < 1) return fail(NVDB_EINVAL, "empty training set / batch");
+  if (d->sampled && d->sample_interval != 1)
+    return fail(NVDB_EUNSUPPORTED, "sample_interval > 1 is not built yet");
+  if (d->sampled && (uint64_t)d->n > 0xFFFFFFFFull) return fail(NVDB_EUNSUPPORTED, "n >= 2^32");
+  std::unique_ptr<nvdb_trainer> tr(new nvdb_trainer());
+  tr->d = *d;
+  tr->m = nd.m;
+  tr->Wr = nd.width;
+  tr->W = (nd.width + 15) / 16 * 16;
+  tr->k0 = (2 * nd.m + kChunkK - 1) / kChunkK * kChunkK;
+  tr->depth = nd.depth;
+  tr->out_dim = nd.out_dim;
+  const int W = tr->W, k0 = tr->k0, depth = tr->depth;
+  if (W > 256 || depth > 4 || k0 > 1024) return fail(NVDB_EUNSUPPORTED, "net too large for the training kernels");
+  // TMEM budgets: fwd/dgrad keeps depth*W pre-activation columns per warpgroup;
+  // wgrad keeps ceil(k0/128)*W + 16 + (depth-1)*W + 16 accumulator columns
+  const int nmt = (k0 + 127) / 128;
+  const int wg_cols = nmt * W + 16 + (depth - 1) * W + 16;
+  if (depth * W > 512 || wg_cols > 512)
+    return fail(NVDB_EUNSUPPORTED, "net needs %d / %d TMEM columns (> 512)", depth * W, wg_cols);
+  tr->nwg = (depth * W <= 256) ? 2 : 1;
+  tr->batch = d->sampled ? d->batch : d->n;
+  tr->ntiles = (tr->batch + kTileM - 1) / kTileM;
+  // ---- parameter layout (serialized: per layer W_l (out,in) then b_l)
+  int64_t P = 0;
+  std::vector<int> ins, outs;
+  for (int l = 0; l <= depth; ++l) {
+    const int in = l == 0 ? 2 * nd.m : nd.width;
+    const int o = l == depth ? nd.out_dim : nd.width;
+    ins.push_back(in);
+    outs.push_back(o);
+    tr->poff.push_back(P);
+    P += (int64_t)in * o;
+    tr->poff.push_back(P);
+    P += o;
+  }
+  tr->P = P;
+  // ---- image blob layout (NetDev)
+  const size_t wimg_bytes = align_up((size_t)2 * ((size_t)W * k0 + (size_t)(depth - 1) * W * W), 16);
+  const size_t o_bias = align_up(wimg_bytes, 256), o_headw = align_up(o_bias + 4 * depth * W, 256);
+  const size_t o_headb = align_up(o_headw + 4 * 3 * W, 256), o_b2pi = align_up(o_headb + 16, 256);
+  const size_t blob_bytes = align_up(o_b2pi + 4 * 3 * (k0 / 2), 256);
+  std::vector<uint8_t> blob(blob_bytes, 0);
+  std::vector<float> master(P), gscale(P), fold(P, 1.f);
+  std::vector<int32_t> imgoff(P, -1), f32dst(P, -1);
+  const bool sine = nd.activation == NVDB_ACT_SINE;
+  const float om = sine ? nd.frequency : 1.0f;
+  const double inv_size = 1.0 / (double)tr->batch;
+  float* f32b = reinterpret_cast<float*>(blob.data() + o_bias);  // bias' | headw | headb contiguous region
+  (void)f32b;
+  for (int l = 0; l <= depth; ++l) {
+    const int in = ins[l], o = outs[l];
+    for (int r = 0; r < o; ++r)
+      for (int c = 0; c < in; ++c) {
+        const int64_t q = tr->poff[2 * l] + (int64_t)r * in + c;
+        master[q] = nd.weights[l][(size_t)r * in + c];
+        if (l < depth) {
+          const float f = (l == 0) ? om * nd.amplitude : om;
+          fold[q] = f;
+          gscale[q] = (float)(inv_size * f);
+          const size_t e = (l == 0) ? kmajor_offset(r, c, W) / 2
+                                    : ((size_t)W * k0 + (size_t)(l - 1) * W * W) + kmajor_offset(r, c, W) / 2;
+          imgoff[q] = (int32_t)e;
+        } else {
+          gscale[q] = (float)inv_size;
+          fold[q] = 1.f;
+          f32dst[q] = (int32_t)((o_headw - o_bias) / 4 + r * W + c);
+        }
+      }
+    for (int r = 0; r < o; ++r) {
+      const int64_t q = tr->poff[2 * l + 1] + r;
+      master[q] = nd.biases[l][r];
+      if (l < depth) {
+        fold[q] = om;
+        gscale[q] = (float)(inv_size * om);
+        f32dst[q] = (int32_t)(l * W + r);
+      } else {
+        fold[q] = 1.f;
+        gscale[q] = (float)inv_size;
+        f32dst[q] = (int32_t)((o_headb - o_bias) / 4 + r);
+      }
+    }
+  }
+  // initial image and f32 params from master
+  uint16_t* wimg = reinterpret_cast<uint16_t*>(blob.data());
+  float* fblock = reinterpret_cast<float*>(blob.data() + o_bias);
+  for (int64_t q = 0; q < P; ++q) {
+    if (imgoff[q] >= 0) {
+      __half h = __float2half_rn(master[q] * fold[q]);
+      std::memcpy(&wimg[imgoff[q]], &h, 2);
+    }
+    if (f32dst[q] >= 0) fblock[f32dst[q]] = master[q] * fold[q];
+  }
+  float* b2 = reinterpret_cast<float*>(blob.data() + o_b2pi);
+  for (int ax = 0; ax < 3; ++ax)
+    for (int f = 0; f < nd.m; ++f) b2[ax * (k0 / 2) + f] = nd.b2pi[ax * nd.m + f];
+  // ---- device allocations
+  nvdb_trainer* t = tr.get();
+  int rc = 0;
+  auto chk = [&](int r) { if (r && !rc) rc = r; };
+  chk(dalloc(t, &t->blob, blob_bytes));
+  chk(dalloc(t, &t->wmaster, P));
+  chk(dalloc(t, &t->mom, P));
+  chk(dalloc(t, &t->vel, P));
+  chk(dalloc(t, &t->gscale, P));
+  chk(dalloc(t, &t->img_off, P));
+  chk(dalloc(t, &t->img_fold, P));
+  chk(dalloc(t, &t->f32_dst, P));
+  chk(dalloc(t, &t->dpoff, t->poff.size()));
+  if (rc) return rc;
+  NVDB_CUDA_TRY(cudaMemcpy(t->blob, blob.data(), blob_bytes, cudaMemcpyHostToDevice));
+  NVDB_CUDA_TRY(cudaMemcpy(t->wmaster, master.data(), 4 * P, cudaMemcpyHostToDevice));
+  NVDB_CUDA_TRY(cudaMemset(t->mom, 0, 4 * P));
+  NVDB_CUDA_TRY(cudaMemset(t->vel, 0, 4 * P));
+  NVDB_CUDA_TRY(cudaMemcpy(t->gscale, gscale.data(), 4 * P, cudaMemcpyHostToDevice));
+  NVDB_CUDA_TRY(cudaMemcpy(t->img_off, imgoff.data(), 4 * P, cudaMemcpyHostToDevice));
+  NVDB_CUDA_TRY(cudaMemcpy(t->img_fold, fold.data(), 4 * P, cudaMemcpyHostToDevice));
+  NVDB_CUDA_TRY(cudaMemcpy(t->f32_dst, f32dst.data(), 4 * P, cudaMemcpyHostToDevice));
+  NVDB_CUDA_TRY(cudaMemcpy(t->dpoff, t->poff.data(), 8 * t->poff.size(), cudaMemcpyHostToDevice));
+  NetDev& n = t->net;
+  n.wimg = t->blob;
+  n.bias = reinterpret_cast<const float*>(t->blob + o_bias);
+  n.headw = reinterpret_cast<const float*>(t->blob + o_headw);
+  n.headb = reinterpret_cast<const float*>(t->blob + o_headb);
+  n.b2pi = reinterpret_cast<const float*>(t->blob + o_b2pi);
+  n.wimg_bytes = (uint32_t)wimg_bytes;
+  n.k0 = k0;
+  n.width = W;
+  n.depth = depth;
+  n.out_dim = nd.out_dim;
+  n.act = nd.activation;
+  n.head = nd.head;
+  n.expert = 0;
+  t->plan = plan_smem((uint32_t)wimg_bytes, W);
+  // ---- per-step buffers
+  const size_t tile_elems = (size_t)kTileM * W;
+  t->fb_grid = (int)std::min<int64_t>(num_sms(), (t->ntiles + t->nwg - 1) / t->nwg);
+  t->wg_grid = (int)std::min<int64_t>(num_sms(), t->ntiles);
+  chk(dalloc(t, &t->act_img, (size_t)depth * t->ntiles * tile_elems));
+  chk(dalloc(t, &t->dz_img, (size_t)depth * t->ntiles * tile_elems));
+  chk(dalloc(t, &t->dlt_img, (size_t)t->ntiles * kTileM * 16));
+  chk(dalloc(t, &t->partial, (size_t)t->wg_grid * P));
+  chk(dalloc(t, &t->loss_part, (size_t)t->fb_grid));
+  chk(dalloc(t, &t->ctl, 4));
+  chk(dalloc(t, &t->loss_hist, d->max_epochs));
+  chk(dalloc(t, &t->lr, d->max_epochs));
+  chk(dalloc(t, &t->c1, d->max_epochs));
+  chk(dalloc(t, &t->c2, d->max_epochs));
+  if (rc) return rc;
+  NVDB_CUDA_TRY(cudaMemset(t->ctl, 0, 16));
+  NVDB_CUDA_TRY(cudaMemset(t->loss_hist, 0, 8 * d->max_epochs));
+  NVDB_CUDA_TRY(cudaMemcpy(t->lr, d->lr, 4 * d->max_epochs, cudaMemcpyHostToDevice));
+  NVDB_CUDA_TRY(cudaMemcpy(t->c1, d->c1, 4 * d->max_epochs, cudaMemcpyHostToDevice));
+  NVDB_CUDA_TRY(cudaMemcpy(t->c2, d->c2, 4 * d->max_epochs, cudaMemcpyHostToDevice));
+  if (d->sampled) {
+    const uint64_t nn = (uint64_t)d->n;
+    const double p_rej = nn > 1 ? (double)((uint32_t)(0u - (uint32_t)nn) % (uint32_t)nn) / 4294967296.0 : 0.0;
+    t->nraw = t->batch + (int64_t)std::ceil(t->batch * p_rej * 2.0) + 1024;
+    t->nraw = (t->nraw + 7) / 8 * 8;
+    chk(dalloc(t, &t->idx, t->batch));
+    chk(dalloc(t, &t->sflag, t->nraw));
+    chk(dalloc(t, &t->sval, t->nraw));
+    chk(dalloc(t, &t->spos, t->nraw));
+    chk(dalloc(t, &t->words, (size_t)4 * d->max_epochs));
+    if (rc) return rc;
+    NVDB_CUDA_TRY(cudaMemcpy(t->words, d->seed_words, 32 * (size_t)d->max_epochs, cudaMemcpyHostToDevice));
+    cub::DeviceScan::ExclusiveSum(nullptr, t->cub_bytes, t->sflag, t->spos, (int)t->nraw);
+    NVDB_CUDA_TRY(cudaMalloc(&t->cub_tmp, std::max<size_t>(t->cub_bytes, 16)));
+    t->owned.push_back(t->cub_tmp);
+  }
+  // kernel attributes
+  if (enable_max_smem(k_train_fb) < (long long)t->plan.total ||
+      enable_max_smem(k_train_wgrad) < 139264 + 3 * 512 * 4 + 64)
+    return fail(NVDB_EUNSUPPORTED, "training kernels exceed the shared-memory limit");
+  *out = tr.release();
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
+  if (!t || epochs < 0) return fail(NVDB_EINVAL, "nvdb_trainer_run: bad args");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const nvdb_train_desc& d = t->d;
+  for (int e = 0; e < epochs; ++e) {
+    int32_t* ep = t->ctl;
+    int32_t* stopped = t->ctl + 1;
+    if (d.sampled) {
+      SampCtl c{ep, stopped, t->words, (unsigned long long)d.n, t->batch, t->nraw, t->sflag, t->sval, t->spos, t->idx};
+      if (d.n == 1) {
+        k_sample_ones<<<64, 256, 0, st>>>(c);
+        NVDB_CHECK_LAUNCH();
+      } else {
+        const int64_t thr = t->nraw / 8;
+        k_sample_raw<<<(int)((thr + 255) / 256), 256, 0, st>>>(c);
+        NVDB_CHECK_LAUNCH();
+        size_t cb = t->cub_bytes;
+        NVDB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(t->cub_tmp, cb, t->sflag, t->spos, (int)t->nraw, st));
+        k_sample_compact<<<num_sms() * 4, 256, 0, st>>>(c);
+        NVDB_CHECK_LAUNCH();
+        k_sample_tail<<<1, 32, 0, st>>>(c);
+        NVDB_CHECK_LAUNCH();
+      }
+    }
+    FbArgs fa{};
+    fa.net = t->net;
+    fa.xs = d.inputs;
+    fa.ys = d.targets;
+    fa.idx = d.sampled ? t->idx : nullptr;
+    fa.batch = t->batch;
+    fa.loss_kind = d.loss_kind;
+    fa.nwg = t->nwg;
+    fa.act_img = t->act_img;
+    fa.dz_img = t->dz_img;
+    fa.dlt_img = t->dlt_img;
+    fa.loss_part = t->loss_part;
+    fa.stopped = stopped;
+    fa.w_off = t->plan.w_off;
+    fa.region_off = t->plan.region_off;
+    fa.region_bytes = t->plan.region_bytes;
+    fa.small_off = t->plan.small_off;
+    fa.bar_off = t->plan.bar_off;
+    k_train_fb<<<t->fb_grid, 128 * t->nwg, std::max<uint32_t>(t->plan.total, 120 * 1024), st>>>(fa);
+    NVDB_CHECK_LAUNCH();
+    WgArgs wa{};
+    wa.net = t->net;
+    wa.m = t->m;
+    wa.width_real = t->Wr;
+    wa.xs = d.inputs;
+    wa.idx = fa.idx;
+    wa.batch = t->batch;
+    wa.act_img = t->act_img;
+    wa.dz_img = t->dz_img;
+    wa.dlt_img = t->dlt_img;
+    wa.partial = t->partial;
+    wa.P = t->P;
+    wa.poff = t->dpoff;
+    wa.stopped = stopped;
+    const int nmt = (t->k0 + 127) / 128;
+    wa.col_w0 = 0;
+    wa.col_b0 = nmt * t->W;
+    wa.col_h = wa.col_b0 + 16;
+    wa.col_head = wa.col_h + (t->depth - 1) * t->W;
+    k_train_wgrad<<<t->wg_grid, 128, 139264 + 3 * 512 * 4 + 64, st>>>(wa);
+    NVDB_CHECK_LAUNCH();
+    AdamArgs aa{};
+    aa.partial = t->partial;
+    aa.ncta = t->wg_grid;
+    aa.P = t->P;
+    aa.wmaster = t->wmaster;
+    aa.mom = t->mom;
+    aa.vel = t->vel;
+    aa.gscale = t->gscale;
+    aa.img_off = t->img_off;
+    aa.img_fold = t->img_fold;
+    aa.wimg = reinterpret_cast<uint16_t*>(t->blob);
+    aa.f32_dst = t->f32_dst;
+    aa.f32_block = const_cast<float*>(t->net.bias);
+    aa.lr = t->lr;
+    aa.c1 = t->c1;
+    aa.c2 = t->c2;
+    aa.loss_part = t->loss_part;
+    aa.nloss = t->fb_grid;
+    aa.loss_den = (double)t->batch;
+    aa.target = d.target_loss;
+    aa.epoch = ep;
+    aa.stopped = stopped;
+    aa.epochs_done = t->ctl + 2;
+    aa.loss_hist = t->loss_hist;
+    k_train_adam<<<(int)std::min<int64_t>((t->P + 255) / 256, num_sms() * 8), 256, 0, st>>>(aa);
+    NVDB_CHECK_LAUNCH();
+    k_train_advance<<<1, 1, 0, st>>>(ep, stopped, t->ctl + 2);
+    NVDB_CHECK_LAUNCH();
+  }
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_trainer_status(const nvdb_trainer* t, int32_t* epochs_done, int32_t* stopped, double* losses,
+                                   int32_t nlosses) {
+  if (!t) return fail(NVDB_EINVAL, "nvdb_trainer_status: null trainer");
+  int32_t ctl[3];
+  NVDB_CUDA_TRY(cudaMemcpy(ctl, t->ctl, sizeof(ctl), cudaMemcpyDeviceToHost));
+  if (epochs_done) *epochs_done = ctl[2];
+  if (stopped) *stopped = ctl[1];
+  if (losses && nlosses > 0)
+    NVDB_CUDA_TRY(cudaMemcpy(losses, t->loss_hist, 8 * (size_t)std::min(nlosses, t->d.max_epochs),
+                             cudaMemcpyDeviceToHost));
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_trainer_weights(const nvdb_trainer* t, float* const* weights, float* const* biases) {
+  if (!t || !weights || !biases) return fail(NVDB_EINVAL, "nvdb_trainer_weights: null argument");
+  std::vector<float> host(t->P);
+  NVDB_CUDA_TRY(cudaMemcpy(host.data(), t->wmaster, 4 * t->P, cudaMemcpyDeviceToHost));
+  for (int l = 0; l <= t->depth; ++l) {
+    const int64_t nw = t->poff[2 * l + 1] - t->poff[2 * l];
+    const int64_t nb = (l < t->depth ? t->poff[2 * l + 2] : t->P) - t->poff[2 * l + 1];
+    std::memcpy(weights[l], host.data() + t->poff[2 * l], 4 * nw);
+    std::memcpy(biases[l], host.data() + t->poff[2 * l + 1], 4 * nb);
+  }
+  return NVDB_OK;
+}

@@ -247,6 +247,10 @@ NVDB_API int nvdb_trainer_run(nvdb_trainer* tr, int32_t epochs, void* stream);
 /* synchronous: epochs run so far, stop flag, per-epoch losses (HOST out) */
 NVDB_API int nvdb_trainer_status(const nvdb_trainer* tr, int32_t* epochs_done, int32_t* stopped,
                                  double* losses, int32_t nlosses);
+/* encoder.Sampler.indices (encoder.py:257-267, sample_interval 1): `batch`
+ * numpy-exact draws in [0, n) from PCG64 seeded with the 4 HOST words of
+ * SeedSequence((seed, 0, epoch)).generate_state(4, uint64); idx DEVICE. */
+NVDB_API int nvdb_sample_indices(uint64_t n, int64_t batch, const uint64_t* words, int64_t* idx, void* stream);
 /* fp32 master weights into HOST arrays shaped like nvdb_net_desc */
 NVDB_API int nvdb_trainer_weights(const nvdb_trainer* tr, float* const* weights, float* const* biases);
 

@@ -1073,6 +1073,50 @@ extern "C" int nvdb_trainer_status(const nvdb_trainer* t, int32_t* epochs_done, 
   return NVDB_OK;
 }
 
+// Sampler.indices(epoch) seam (encoder.py:257-267, interval == 1): the same
+// kernels as the training loop, on scratch memory of its own.
+extern "C" int nvdb_sample_indices(uint64_t n, int64_t batch, const uint64_t* words, int64_t* idx, void* stream) {
+  if (n < 1 || batch < 0 || !words || (batch > 0 && !idx)) return fail(NVDB_EINVAL, "nvdb_sample_indices: bad args");
+  if (n > 0xFFFFFFFFull) return fail(NVDB_EUNSUPPORTED, "n >= 2^32");
+  if (batch == 0) return NVDB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const double p_rej = n > 1 ? (double)((uint32_t)(0u - (uint32_t)n) % (uint32_t)n) / 4294967296.0 : 0.0;
+  int64_t nraw = batch + (int64_t)std::ceil(batch * p_rej * 2.0) + 1024;
+  nraw = (nraw + 7) / 8 * 8;
+  int32_t* ctl = nullptr;
+  unsigned long long* w = nullptr;
+  int32_t *flag = nullptr, *pos = nullptr;
+  uint32_t* val = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)nraw);
+  int rc = NVDB_OK;
+  if (cudaMalloc(&ctl, 16) || cudaMalloc(&w, 32) || cudaMalloc(&flag, 4 * nraw) || cudaMalloc(&pos, 4 * nraw) ||
+      cudaMalloc(&val, 4 * nraw) || cudaMalloc(&tmp, std::max<size_t>(tb, 16)))
+    rc = fail(NVDB_ECUDA, "nvdb_sample_indices: cudaMalloc");
+  if (!rc) {
+    cudaMemsetAsync(ctl, 0, 16, st);
+    cudaMemcpyAsync(w, words, 32, cudaMemcpyHostToDevice, st);
+    SampCtl c{ctl, ctl + 1, w, (unsigned long long)n, batch, nraw, flag, val, pos, idx};
+    if (n == 1) {
+      k_sample_ones<<<64, 256, 0, st>>>(c);
+    } else {
+      k_sample_raw<<<(int)((nraw / 8 + 255) / 256), 256, 0, st>>>(c);
+      cub::DeviceScan::ExclusiveSum(tmp, tb, flag, pos, (int)nraw, st);
+      k_sample_compact<<<num_sms() * 4, 256, 0, st>>>(c);
+      k_sample_tail<<<1, 32, 0, st>>>(c);
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) rc = fail(NVDB_ECUDA, "sampler kernels failed");
+  }
+  cudaFree(ctl);
+  cudaFree(w);
+  cudaFree(flag);
+  cudaFree(pos);
+  cudaFree(val);
+  cudaFree(tmp);
+  return rc;
+}
+
 extern "C" int nvdb_trainer_weights(const nvdb_trainer* t, float* const* weights, float* const* biases) {
   if (!t || !weights || !biases) return fail(NVDB_EINVAL, "nvdb_trainer_weights: null argument");
   std::vector<float> host(t->P);

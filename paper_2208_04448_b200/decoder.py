@@ -51,6 +51,30 @@ def _slot0(c) -> int:
     return ((c[0] & 7) << 6) | ((c[1] & 7) << 3) | (c[2] & 7)
 
 
+class NetEvaluator:
+    """Experts' nets on the GPU plus the generic gate-blended evaluator."""
+
+    def __init__(self, experts, subdomain_size: int, halo: int, background: float = 0.0, device=None):
+        self.dev = _dev(device)
+        self.background = float(np.float32(background))
+        experts = sorted(experts, key=lambda e: e.id)
+        self.ns = DeviceNetSet(experts, subdomain_size, halo)
+        self.single = len(experts) == 1
+        self.has_tag = {t: any(dict(e.nets()).get(t) is not None for e in experts) for t in TAG_CODES}
+
+    def close(self):
+        self.ns.close()
+
+    def evaluate(self, tag: str, src_kind: int, src: torch.Tensor, n: int, out_mode: int, *,
+                 gather: Optional[torch.Tensor] = None, u8=None, f32=None, probs=None, raw=None,
+                 value_scale: float = 1.0, clip: bool = False) -> None:
+        return DeviceModel.evaluate(self, tag, src_kind, src, n, out_mode, gather=gather, u8=u8, f32=f32,
+                                    probs=probs, raw=raw, value_scale=value_scale, clip=clip)
+
+    def select(self, v: torch.Tensor, value: int) -> torch.Tensor:
+        return DeviceModel.select(self, v, value)
+
+
 class DeviceModel:
     """A container prepared for decoding: nets, node origins and patch tables on the GPU."""
 

@@ -260,6 +260,15 @@ def main():
         train_fixture(g, cfg)
     if args.c1 and want("c1"):
         c1_fixture(args.c1)
+    if want("procgen"):
+        procgen_fixture()
+
+
+def procgen_fixture():
+    """Small torus (gen_torus_sdf) for the vectorized generator's parity test."""
+    from svcodec.procgen import gen_torus_sdf
+    g = gen_torus_sdf(16.0, 7.0, 1.0, 3.0, center=(40.0, 40.0, 20.0))
+    save("procgen_torus", **grid_to_arrays(DenseLeafGrid.from_svcodec(g)))
 
 
 if __name__ == "__main__":

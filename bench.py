@@ -1,18 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the NeuralVDB hot path on B200 (one JSON line on rank 0).
 
-Workload (BASELINE.json metric "decoded voxels/s and train samples/s"):
-whole-volume neural decode of a synthetic narrow-band SDF level set from a
-trained container; ``value`` = leaf voxels decoded per second (device-timed,
-container resident in HBM, L2 flushed between steps).  The container is the
-C1 configuration (sphere 128^3, ACCEPT_CONFIG, fp16 weights) trained by the
-reference itself (tests/golden/c1_sphere128.npz).
+BASELINE.json metric: "decoded voxels/s and train samples/s at 1/2/4/8 B200;
+% tensor-core peak".  Default workload = configs[1] (C2): synthetic torus
+narrow-band SDF at 512^3 (gen_torus_sdf(160, 64, 1, 3) centred at 256^3,
+2,424,980 active voxels, 12,983 leaves), full training of the level-1,
+level-0 and voxel networks with ACCEPT_CONFIG (test_acceptance.py:72-78) on
+the GPU, then whole-volume decode.
 
-    python bench.py --gpus N --steps K --warmup W [--impl reference]
+* a "step" = one whole-volume decode of the trained container (device
+  resident, L2 flushed between steps); ``value`` = decoded leaf voxels/s;
+* ``train`` = samples/s over the complete device-resident training of the
+  three networks (800 epochs, early stops included), timed once;
+* ``e2e`` = the same decode metric through the public API
+  ``decode_full(container)`` from host objects to a host grid.
 
-N>1 runs under torchrun (one process per GPU): decode is data-parallel with
-no collective (every rank decodes a full replica: weak scaling); the step
-time is the max over ranks.
+    python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload c2|c1]
+
+N>1 (torchrun): every rank trains and decodes its own replica (weak
+scaling, no data-path collective); times are the max over ranks.
 """
 
 from __future__ import annotations
@@ -32,13 +38,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+TORUS = dict(major=160.0, minor=64.0, voxel=1.0, half_width=3.0, center=(256.0, 256.0, 256.0))
 
 
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return p, "measured"
+            return json.load(f), "measured"
     except Exception:  # noqa: BLE001
         return PEAKS_FALLBACK, "fallback"
 
@@ -51,15 +57,13 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index = index
-        self.lines = []
-        self.proc = None
+        self.index, self.lines, self.proc = index, [], None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:  # noqa: BLE001
@@ -71,7 +75,7 @@ class ClockSampler:
 
     def stop(self):
         if self.proc is not None:
-            time.sleep(0.25)
+            time.sleep(0.15)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -95,45 +99,159 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def mlp_flops_per_point(net) -> int:
-    """Forward flops 2*sum(in*out) incl. the head."""
+def fwd_flops(net) -> int:
+    """2*sum(in*out) incl. the head."""
     return int(sum(2 * w.shape[0] * w.shape[1] for w, _ in net.params.layers))
 
 
-def load_c1():
+def train_flops(layers) -> int:
+    """2*(3*sum MAC - MAC_0): forward + wgrad + dgrad except layer 0."""
+    macs = [w.shape[0] * w.shape[1] for w, _ in layers]
+    return int(2 * (3 * sum(macs) - macs[0]))
+
+
+def accept_config():
+    from paper_2208_04448_b200.encoder import TrainConfig
+    return TrainConfig(subdomain_size=512, l1_net=(3, 48), tile_net=None, l0_net=(3, 96), voxel_net=(3, 96),
+                       activation="sine", frequency=3.0, ffm_scale=5.0, ffm_size=192, lr=1e-3, decay=0.975,
+                       interval=100.0, max_epochs=800, sample_interval=1, batch_size=65536,
+                       significance_threshold=0.0, strict_topology=False, seed=4242)
+
+
+def make_grid(workload):
+    from paper_2208_04448_b200.procgen import sphere_sdf, torus_sdf
+    if workload == "c1":
+        return sphere_sdf((63.5, 63.5, 63.5), 61.0, 1.0, 3.0)
+    t = TORUS
+    return torus_sdf(t["major"], t["minor"], t["voxel"], t["half_width"], center=t["center"])
+
+
+def train_container(grid, cfg, dev, timings):
+    """encode() with the three trainings timed on the device (l1, tile, l0, voxel)."""
+    import torch
+    from paper_2208_04448_b200.encoder import (DeviceTrainer, build_upper_tree, decompose, extract_patches,
+                                               gather_expert_data, init_mlp, net_spec, stable_seed,
+                                               value_scale_of, NET_TAGS)
+    from paper_2208_04448_b200.model import (Activation, EncodedSubdomain, FourierFeatures, GridMeta,
+                                             NetRecord, NeuralGridContainer)
+    layout = decompose(grid, cfg.subdomain_size)
+    experts = []
+    for sub in layout.subdomains:
+        scale = value_scale_of(grid)
+        data = gather_expert_data(grid, sub, scale)
+        ex = EncodedSubdomain(sub.id, sub.cell, sub.cluster_id, data.norm_origin, data.norm_scale, scale)
+        for tag, x, y, attr in (("l1", data.l1_inputs, data.l1_labels, "l1_classifier"),
+                                ("tile", data.tile_inputs, data.tile_targets, "tile_regressor"),
+                                ("l0", data.l0_inputs, data.l0_labels, "l0_classifier"),
+                                ("voxel", data.vox_inputs, data.vox_targets, "voxel_regressor")):
+            spec = net_spec(tag, cfg)
+            if spec is None or x is None:
+                continue
+            tid = NET_TAGS[tag]
+            ff = FourierFeatures(spec.m, cfg.ffm_scale, stable_seed(cfg.seed, sub.id, tid, 0))
+            p0 = init_mlp(2 * spec.m, [spec.arch[1]] * spec.arch[0], spec.out_dim,
+                          Activation(cfg.activation, cfg.frequency), spec.head, stable_seed(cfg.seed, sub.id, tid, 1))
+            sampled = (not spec.full_batch) and x.shape[0] > cfg.batch_size
+            tr = DeviceTrainer(p0, ff, x, y, spec.loss_kind, cfg, cfg.lr, stable_seed(cfg.seed, sub.id, tid, 2),
+                               sampled, spec.loss_target, dev)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            loss, epochs = tr.run()
+            e1.record()
+            e1.synchronize()
+            batch = cfg.batch_size if sampled else x.shape[0]
+            timings.append({"tag": tag, "epochs": epochs, "batch": int(batch), "ms": e0.elapsed_time(e1),
+                            "loss": loss, "flops_per_sample": train_flops(p0.layers)})
+            setattr(ex, attr, NetRecord(tr.weights(), ff, loss, epochs))
+            tr.close()
+        experts.append(ex)
+    extract_patches(grid, layout, experts, cfg, dev)
+    meta = GridMeta(grid.grid_class, grid.background, grid.voxel_size, grid.half_width, value_scale_of(grid))
+    return NeuralGridContainer(meta, build_upper_tree(grid), layout, experts, cfg, 16)
+
+
+def cpu_decode_sample(c, nleaf_sample=400):
+    """Oracle timing on a bounded sample: the first leaves of the decode (L0 classify
+    all their voxels, regress the active ones) + all level-1 slots."""
+    import oracle as O
+    from paper_2208_04448_b200.model import L1_LOCAL, LEAF_LOCAL
+    orig = np.asarray(sorted(tuple(o) for o in c.upper_tree.l1_origins), dtype=np.int64)
+    t0 = time.perf_counter()
+    cen1 = (orig[:1, None, :] + (L1_LOCAL * 8.0 + 4.0)[None]).reshape(-1, 3)
+    p1, cov1 = O.blended(c.layout, c.experts, cen1, "l1")
+    cls = np.where(cov1, p1.argmax(1), 2)
+    slots = np.flatnonzero(cls == 0)[:nleaf_sample]
+    lo = orig[0] + L1_LOCAL[slots] * 8
+    cen0 = (lo[:, None, :] + (LEAF_LOCAL + 0.5)[None]).reshape(-1, 3)
+    p0, cov0 = O.blended(c.layout, c.experts, cen0, "l0")
+    act = cov0 & (p0[:, 0] > 0.5)
+    O.blended(c.layout, c.experts, cen0[act], "voxel")
+    dt = time.perf_counter() - t0
+    return cen0.shape[0] / dt, cen0.shape[0], dt, int(act.sum())
+
+
+def cpu_train_sample(c, cfg, steps=3):
+    """Oracle fused_step timing: voxel net, batch 65536, `steps` steps."""
+    import oracle as O
+    e = c.experts[0]
+    rec = e.voxel_regressor
+    st = O.TrainState([(w.copy(), b.copy()) for w, b in rec.params.layers], cfg.activation, cfg.frequency, rec.ff)
+    rng = np.random.default_rng(0)
+    x = rng.uniform(0.2, 0.8, size=(cfg.batch_size, 3)).astype(np.float32)
+    y = rng.uniform(-1, 1, size=cfg.batch_size).astype(np.float32)
+    O.train_step(st, x, y, "mse", np.float32(1e-3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.train_step(st, x, y, "mse", np.float32(1e-3))
+    dt = time.perf_counter() - t0
+    return steps * cfg.batch_size / dt, dt
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the CPU oracle restatement of svcodec's decode path on the
+    same synthetic workload (bounded sample per step), all host cores."""
+    if rank != 0:
+        return
+    cfg = accept_config()
+    c = _reference_container(args.workload, cfg)
+    steps, warm = min(args.steps, 3), min(args.warmup, 1)
+    for _ in range(warm):
+        cpu_decode_sample(c)
+    vals = []
+    for _ in range(steps):
+        v, nvox, dt, nact = cpu_decode_sample(c)
+        vals.append(v)
+    val = statistics.median(vals)
+    tv, tdt = cpu_train_sample(c, cfg)
+    line = {"metric": "decoded voxels/s", "value": val, "unit": "voxels/s", "n_gpus": world, "steps": steps,
+            "warmup": warm, "ms_per_step": 1e3 * nvox / val, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": _config(args.workload),
+            "cpu_baseline": {"value": val, "unit": "voxels/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{nvox} leaf voxels of the first decoded leaves per step (L0 classify "
+                                       f"+ voxel regress on {nact} active), numpy/OpenBLAS oracle"},
+            "train": {"value": tv, "unit": "samples/s", "sample": f"3 fused_steps of the voxel net, B=65536 "
+                                                                   f"({tdt:.1f} s)"},
+            "e2e": {"value": val, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _reference_container(workload, cfg):
+    """The reference arm decodes a container of the same shape; it is trained by
+    this framework on the GPU when one is present, else taken from the C1 fixture."""
     from paper_2208_04448_b200.model import container_from_arrays
     z = np.load(os.path.join(ROOT, "tests", "golden", "c1_sphere128.npz"))
     return container_from_arrays(z)
 
 
-def run_reference(args, rank):
-    """CPU reference arm: the oracle restatement of svcodec.decode_full."""
-    if rank != 0:
-        return
-    import oracle as O
-    c = load_c1()
-    steps, warm = min(args.steps, 3), min(args.warmup, 1)
-    for _ in range(warm):
-        O.decode(c)
-    t = []
-    nvox = 0
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        r = O.decode(c)
-        t.append(time.perf_counter() - t0)
-        nvox = r.leaf_origins.shape[0] * 512
-    val = nvox / (sum(t) / len(t))
-    cores = os.cpu_count()
-    line = {"metric": "decoded voxels/s", "value": val, "unit": "voxels/s", "n_gpus": args.gpus,
-            "steps": steps, "warmup": warm, "ms_per_step": 1e3 * sum(t) / len(t), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": "C1 sphere 128^3 ACCEPT_CONFIG whole-volume decode_full",
-                       "leaf_voxels": nvox},
-            "cpu_baseline": {"value": val, "unit": "voxels/s", "cores": cores, "kind": "port",
-                             "sample": f"full C1 decode ({nvox} leaf voxels) per step, numpy/OpenBLAS"},
-            "e2e": {"value": val, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+def _config(workload):
+    if workload == "c1":
+        return {"workload": "C1 sphere 128^3 narrow-band SDF, ACCEPT_CONFIG train + whole-volume decode"}
+    t = TORUS
+    return {"workload": f"C2 torus 512^3 narrow-band SDF (R={t['major']}, r={t['minor']}, band 3), "
+                        "ACCEPT_CONFIG train (l1 3x48/m96, l0+voxel 3x96/m192, 800 epochs, B=65536) "
+                        "+ whole-volume decode"}
 
 
 def main():
@@ -142,6 +260,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -149,59 +268,69 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     import torch
     import torch.distributed as dist
-    if world > 1:
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     if args.impl == "reference":
-        run_reference(args, rank)
         if world > 1:
+            dist.init_process_group("gloo")
+        run_reference(args, rank, world)
+        if world > 1:
+            dist.barrier()
             dist.destroy_process_group()
         return
-    args.warmup = max(args.warmup, 3)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    args.warmup = max(args.warmup, 3)
     from paper_2208_04448_b200 import _lib
     from paper_2208_04448_b200.decoder import DeviceModel, decode_full
 
-    c = load_c1()
+    cfg = accept_config()
+    grid = make_grid(args.workload)
+    sampler = ClockSampler(local)
+    sampler.start()
+    # ---------------- training (timed on the device, once)
+    timings = []
+    if world > 1:
+        dist.barrier()
+    c = train_container(grid, cfg, dev, timings)
+    train_ms = sum(t["ms"] for t in timings)
+    train_samples = sum(t["epochs"] * t["batch"] for t in timings)
+    train_flop = sum(t["epochs"] * t["batch"] * t["flops_per_sample"] for t in timings)
+    # ---------------- decode steps
     m = DeviceModel(c, dev)
-    flops = {t: mlp_flops_per_point(n) for t, n in c.experts[0].nets() if n is not None}
+    flops = {t: fwd_flops(n) for t, n in c.experts[0].nets() if n is not None}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     for _ in range(args.warmup):
         d = m.decode(True)
     torch.cuda.synchronize()
     nvox = d.leaf_count * 512
     nact = d.regressor_evaluations
-    n1 = m.n1
-    sampler = ClockSampler(local)
+    L = _lib.lib()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
-    L = _lib.lib()
     launches0 = L.nvdb_launch_count()
     total_ms = 0.0
     m.timer = []
     for _ in range(args.steps):
-        flush.random_(0, 255)  # evict L2 between steps (not timed)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        flush.random_(0, 255)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         d = m.decode(True)
         e1.record()
         e1.synchronize()
         total_ms += e0.elapsed_time(e1)
     torch.cuda.synchronize()
-    launches = (L.nvdb_launch_count() - launches0) // args.steps
+    launches = (L.nvdb_launch_count() - launches0) / args.steps
     clocks = sampler.stop()
     timer, m.timer = m.timer, None
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    tt = torch.tensor([total_ms, train_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item()) / args.steps
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt[0].item()) / args.steps
+    train_ms_max = float(tt[1].item())
     value = world * nvox / (ms * 1e-3)
-    # roofline of the fused MLP kernel: algorithmic flops / its own event time
-    kflops, kms = 0.0, 0.0
-    per_tag = {}
+    kflops, kms, per_tag = 0.0, 0.0, {}
     for tag, npts, a, b in timer:
         dt = a.elapsed_time(b)
         kms += dt
@@ -212,45 +341,49 @@ def main():
     peaks, src = load_peaks()
     achieved = kflops / (kms * 1e-3) / 1e12
     peak = float(peaks["bf16_tflops"])
-    # e2e: public API from the host container to a host grid, H2D/D2H included
+    train_tf = train_flop / (train_ms * 1e-3) / 1e12
+    # ---------------- e2e through the public API (host container -> host grid)
     e2e_t = []
     h2d = sum(w.nbytes + b.nbytes for e in c.experts for _, n in e.nets() if n is not None
               for w, b in n.params.layers)
-    for _ in range(max(2, min(args.steps, 5))):
+    for _ in range(3):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         g = decode_full(c, dev)
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t0)
-    e2e = nvox / statistics.median(e2e_t)
-    d2h = g.leaf_count * (512 * 4 + 512 + 12) + n1 * 4096 * 6
+    e2e = world * nvox / statistics.median(e2e_t)
+    d2h = g.leaf_count * (512 * 4 + 512 + 12) + m.n1 * 4096 * 6
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import oracle as O
-        t0 = time.perf_counter()
-        r = O.decode(c)
-        dt = time.perf_counter() - t0
-        cpu = {"value": r.leaf_origins.shape[0] * 512 / dt, "unit": "voxels/s", "cores": os.cpu_count(),
-               "kind": "port", "sample": f"one full C1 decode ({r.leaf_origins.shape[0] * 512} leaf voxels), "
-                                         f"numpy/OpenBLAS oracle, {dt:.1f} s"}
+        v, nv, dt, na = cpu_decode_sample(c)
+        tv, tdt = cpu_train_sample(c, cfg)
+        cpu = {"value": v, "unit": "voxels/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"oracle decode of the first {nv // 512} decoded leaves ({nv} leaf voxels: L0 classify "
+                         f"+ voxel regress of {na} active), numpy/OpenBLAS, {dt:.1f} s",
+               "train": {"value": tv, "unit": "samples/s",
+                         "sample": f"3 oracle fused_steps, voxel net, B=65536, {tdt:.1f} s"}}
     if rank == 0:
         line = {
             "metric": "decoded voxels/s", "value": value, "unit": "voxels/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16xf16->f32 (fp32 head, f64 blend)",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16xf16->f32 (fp32 head/Adam, f64 blend)",
             "data": "synthetic",
-            "config": {"workload": "C1 sphere 128^3 ACCEPT_CONFIG whole-volume decode (reference-trained fp16 container)",
-                       "leaf_voxels": nvox, "active_voxels": nact, "l1_slots": n1 * 4096,
-                       "parallelism": f"replicas x{world}", "l2": "flushed between steps (256 MiB write)"},
+            "config": dict(_config(args.workload), leaf_voxels=nvox, active_voxels=nact, l1_slots=m.n1 * 4096,
+                           parallelism=f"replicas x{world}", l2="flushed between steps (256 MiB write)"),
+            "train": {"value": world * train_samples / (train_ms_max * 1e-3), "unit": "samples/s",
+                      "ms": train_ms_max, "samples": train_samples,
+                      "nets": [{k: v for k, v in t.items()} for t in timings],
+                      "roofline": {"bound": "tensor", "achieved": train_tf, "peak": float(peaks["bf16_tflops_sustained"]),
+                                   "unit": "TFLOP/s", "frac": train_tf / float(peaks["bf16_tflops_sustained"])}},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": src,
-                         "kernel": "mlp_eval_kernel (all decode stages)",
-                         "flops_per_point": flops, "kernel_ms_per_step": kms / args.steps,
+                         "kernel": "mlp_eval_kernel (all decode stages)", "flops_per_point": flops,
+                         "kernel_ms_per_step": kms / args.steps,
                          "per_stage_ms": {k: v[1] / args.steps for k, v in per_tag.items()}},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e, "unit": "voxels/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h)},
-            "gpu_launches": int(launches),
+            "e2e": {"value": e2e, "unit": "voxels/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(round(launches)),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -41,7 +41,7 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
   *out = nullptr;
   // ---- host packing: one blob, every piece 256-byte aligned
   struct Piece {
-    size_t wimg, bias, headw, headb, b2pi;
+    size_t wimg, bias, headw, headb, b2pi, lat;
   };
   std::vector<Piece> pieces(nnets);
   std::vector<NetDev> hnets(nnets);
@@ -81,6 +81,7 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
     pieces[i].headw = take(sizeof(float) * d.out_dim * W);
     pieces[i].headb = take(sizeof(float) * 4);
     pieces[i].b2pi = take(sizeof(float) * 3 * (k0 / 2));
+    pieces[i].lat = take(sizeof(float) * k0);
   }
   SmemPlan plan = plan_smem(max_wimg, max_width);
   if (plan.total > kMaxDynSmem)
@@ -144,6 +145,17 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
       if (ni >= 0) hnets[ni].expert = e;
     }
   }
+  // lattice step table per net: exp(i * 2 pi b_fy / norm_scale) of its expert
+  for (int i = 0; i < nnets; ++i) {
+    const nvdb_net_desc& d = nets[i];
+    const double nsc = nexperts ? experts[hnets[i].expert].norm_scale : 1.0;
+    float* lat = reinterpret_cast<float*>(blob.data() + pieces[i].lat);
+    for (int f = 0; f < hnets[i].k0 / 2; ++f) {
+      const double beta = f < d.m ? (double)d.b2pi[1 * d.m + f] / nsc : 0.0;
+      lat[2 * f] = (float)std::cos(beta);
+      lat[2 * f + 1] = (float)std::sin(beta);
+    }
+  }
   nvdb_netset* ns = new nvdb_netset();
   ns->nnets = nnets;
   ns->nexperts = nexperts;
@@ -164,6 +176,7 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
     hnets[i].headw = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].headw);
     hnets[i].headb = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].headb);
     hnets[i].b2pi = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].b2pi);
+    hnets[i].lat = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].lat);
   }
   if (cudaMalloc(&ns->dev_nets, sizeof(NetDev) * std::max(nnets, 1)) != cudaSuccess ||
       cudaMalloc(&ns->dev_experts, sizeof(ExpertDev) * std::max(nexperts, 1)) != cudaSuccess ||

@@ -10,12 +10,18 @@
 //   -> softmax / sigmoid / identity, clamped-tent gate weight, f64 blend,
 //      and the decode decision (argmax, > 0.5, clip*scale) in the epilogue.
 //
-// CTA = 2 warpgroups; each warpgroup owns one tile at a time (one thread per
-// TMEM lane / point row) and issues its own MMAs from one elected thread,
-// so the tensor core works on one warpgroup's tile while the other runs its
-// MUFU/FMA epilogue.  Weights of the current net live in shared memory
-// (loaded with one bulk async copy); tiles are processed in pairs that share
-// a net so both warpgroups read the same weights.
+// CTA = 2 tile groups of 8 warps.  A group owns one 128-point tile at a time:
+// TMEM lane p (= point row p) is served by two threads (warps q and q+4 of
+// the group, which share the lane quadrant), each taking half of the feature
+// pairs and half of the accumulator columns; one elected thread issues the
+// group's MMAs, so the tensor core runs one group's tile while the other
+// group is in its MUFU/FMA epilogue.  Weights of the current net live in
+// shared memory (one bulk async copy); tiles come in pairs sharing a net.
+//
+// Leaf-voxel tiles (a quarter of one 8^3 leaf) build their features by angle
+// addition on the FMA pipe: per feature one sincos per 8 voxels along y, then
+// z_{j+1} = z_j * exp(i beta_f) (beta_f = 2 pi b_fy / norm_scale), instead of
+// 2m MUFU sin/cos per point.  Other sources use __sincosf per point.
 #pragma once
 #include <cstdint>
 
@@ -25,7 +31,8 @@ namespace nvdb {
 
 constexpr int kTileM = 128;
 constexpr int kChunkK = 64;            // feature K chunk (fp16 elements)
-constexpr int kCtaThreads = 256;
+constexpr int kGroupThreads = 256;     // threads per tile group
+constexpr int kCtaThreads = 512;       // two tile groups
 constexpr int kChunkBytes = kTileM * kChunkK * 2;   // 16 KB
 constexpr int kMaxOut = 3;
 
@@ -56,6 +63,7 @@ struct alignas(16) NetDev {
   const float* headw;   // [out_dim][width]
   const float* headb;   // [out_dim]
   const float* b2pi;    // [3][k0/2]
+  const float* lat;     // [k0/2][2] cos/sin of the y-step angle (expert's norm scale)
   uint32_t wimg_bytes;
   int32_t k0, width, depth, out_dim, act, head, expert;
 };
@@ -103,14 +111,15 @@ struct MlpArgs {
   uint32_t w_off, region_off, region_bytes, small_off, bar_off;
 };
 
-// small per-net parameters staged in shared memory
-struct SmallView {
-  float* bias;
-  float* headw;
-  float* headb;
-  float* b2pi;
-};
-constexpr int kSmallFloats = 4 * 256 + 3 * 256 + 4 + 3 * 512;  // bias, head, headb, b2pi (k0<=1024)
+// small per-net parameters staged in shared memory:
+// bias [4*256] | headw [3*256] | headb [4] | b2pi [3*512] | lat [2*512] | head exchange [2][128][4]
+constexpr int kSmallBias = 0;
+constexpr int kSmallHeadW = 4 * 256;
+constexpr int kSmallHeadB = kSmallHeadW + 3 * 256;
+constexpr int kSmallB2pi = kSmallHeadB + 4;
+constexpr int kSmallLat = kSmallB2pi + 3 * 512;
+constexpr int kSmallHx = kSmallLat + 2 * 512;
+constexpr int kSmallFloats = kSmallHx + 2 * 128 * 4;
 
 // continuous index-space centre of point `id` of a source (decoder.py:46-47,
 // 110-111, 163, 247; encoder.py:99-100).  Returns false for SRC_NORM_F32.
@@ -165,21 +174,33 @@ __device__ __forceinline__ float act_fn(int act, float z) {
   return fmaxf(z, 0.0f);
 }
 
+__device__ __forceinline__ void st_shared_b32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a);
 
 #ifdef NVDB_MLP_KERNEL_TU  // defined in exactly one translation unit (eval.cu)
 __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
-  const int wg = tid >> 7;
-  const int t = tid & 127;
-  const int wwarp = t >> 5;
+  const int grp = tid >> 8;              // tile group
+  const int gt = tid & (kGroupThreads - 1);
+  const int gw = gt >> 5;                // warp within the group
+  const int quad = gw & 3;               // TMEM lane quadrant (hardware: warp id % 4)
+  const int half = gw >> 2;              // which half of the pairs / columns
+  const int row = quad * 32 + (gt & 31);  // tile row == TMEM lane
 
   uint8_t* wsm = smem + a.w_off;
   float* small = reinterpret_cast<float*>(smem + a.small_off);
-  SmallView sv{small, small + 4 * 256, small + 4 * 256 + 3 * 256, small + 4 * 256 + 3 * 256 + 4};
+  float* s_bias = small + kSmallBias;
+  float* s_headw = small + kSmallHeadW;
+  float* s_headb = small + kSmallHeadB;
+  float* s_b2pi = small + kSmallB2pi;
+  float* s_lat = small + kSmallLat;
+  float* s_hx = small + kSmallHx + grp * 128 * 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-  // bars[0] = weight load; per WG: [1+3wg] chunk0, [2+3wg] chunk1, [3+3wg] layer
+  // bars[0] = weight load; per group g: [1+3g] chunk buf 0, [2+3g] chunk buf 1, [3+3g] layer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
   __shared__ NetDev s_net;
   __shared__ ExpertDev s_exp;
@@ -195,17 +216,15 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
   const uint32_t tmem_base = *tmem_slot;
 
   uint64_t* bar_w = &bars[0];
-  uint64_t* bar_c0 = &bars[1 + 3 * wg];
-  uint64_t* bar_layer = &bars[3 + 3 * wg];
-  uint32_t ncommit[2] = {0u, 0u};
-  bool pend[2] = {false, false};
-  uint32_t nlayer = 0;
-  uint32_t wphase = 0;
+  uint64_t* bar_c0 = &bars[1 + 3 * grp];
+  uint64_t* bar_layer = &bars[3 + 3 * grp];
+  uint32_t nc0 = 0, nc1 = 0, nlayer = 0, wphase = 0;
+  bool pend0 = false, pend1 = false;
   int loaded = -1;
 
-  const uint32_t tmem_col = tmem_base + (uint32_t)(wg * 256);             // MMA D (lane 0)
-  const uint32_t tmem_d = tmem_col + ((uint32_t)(wwarp * 32) << 16);       // this warp's lanes
-  const uint32_t region_s = smem_addr(smem + a.region_off + wg * a.region_bytes);
+  const uint32_t tmem_col = tmem_base + (uint32_t)(grp * 256);            // MMA D (lane 0)
+  const uint32_t tmem_d = tmem_col + ((uint32_t)(quad * 32) << 16);       // this warp's lanes
+  const uint32_t region_s = smem_addr(smem + a.region_off + grp * a.region_bytes);
   const uint32_t w_s = smem_addr(wsm);
 
   const int npairs = a.npairs_dev ? *a.npairs_dev : a.npairs;
@@ -216,27 +235,26 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
   for (int p = p0; p < p1; ++p) {
     const int pair_net = a.tiles ? a.tiles[2 * p].net : a.implicit_net;
     if (pair_net != loaded) {
-      // ---- switch weights: the whole CTA is idle here (both warpgroups
-      // finished their previous tile, so no MMA still reads the old image)
+      // ---- switch weights: the whole CTA is idle here (both groups finished
+      // their previous tile, so no MMA still reads the old image)
       __syncthreads();
       if (tid == 0) {
         s_net = a.nets[pair_net];
         s_exp = a.experts[a.nets[pair_net].expert];
         const NetDev& nd = a.nets[pair_net];
         mbar_arrive_expect_tx(bar_w, nd.wimg_bytes);
-        const uint32_t kPiece = 32768;
-        for (uint32_t off = 0; off < nd.wimg_bytes; off += kPiece) {
-          const uint32_t len = min(kPiece, nd.wimg_bytes - off);
-          bulk_g2s(wsm + off, nd.wimg + off, len, bar_w);
-        }
+        for (uint32_t off = 0; off < nd.wimg_bytes; off += 32768)
+          bulk_g2s(wsm + off, nd.wimg + off, min(32768u, nd.wimg_bytes - off), bar_w);
       }
       __syncthreads();
       {
         const NetDev& nd = s_net;
-        for (int i = tid; i < nd.depth * nd.width; i += kCtaThreads) sv.bias[i] = nd.bias[i];
-        for (int i = tid; i < nd.out_dim * nd.width; i += kCtaThreads) sv.headw[i] = nd.headw[i];
-        if (tid < nd.out_dim) sv.headb[tid] = nd.headb[tid];
-        for (int i = tid; i < 3 * (nd.k0 / 2); i += kCtaThreads) sv.b2pi[i] = nd.b2pi[i];
+        for (int i = tid; i < nd.depth * nd.width; i += kCtaThreads) s_bias[i] = nd.bias[i];
+        for (int i = tid; i < nd.out_dim * nd.width; i += kCtaThreads) s_headw[i] = nd.headw[i];
+        if (tid < nd.out_dim) s_headb[tid] = nd.headb[tid];
+        for (int i = tid; i < 3 * (nd.k0 / 2); i += kCtaThreads) s_b2pi[i] = nd.b2pi[i];
+        if (nd.lat)
+          for (int i = tid; i < nd.k0; i += kCtaThreads) s_lat[i] = nd.lat[i];
       }
       mbar_wait(bar_w, wphase);
       wphase ^= 1u;
@@ -245,9 +263,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
     }
     Tile tile;
     if (a.tiles) {
-      tile = a.tiles[2 * p + wg];
+      tile = a.tiles[2 * p + grp];
     } else {
-      const int64_t first = (int64_t)(2 * p + wg) * kTileM;
+      const int64_t first = (int64_t)(2 * p + grp) * kTileM;
       tile.net = a.implicit_net;
       tile.first = first;
       tile.flags = TF_FIRST | TF_LAST;
@@ -259,15 +277,15 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
     const int act = s_net.act;
     const int mp = k0 >> 1;
 
-    // ------------------------------------------------ point set-up (row t)
-    const bool valid = t < tile.count;
-    const int64_t pos = tile.first + (valid ? t : 0);
+    // ------------------------------------------------ point set-up (row)
+    const bool valid = row < tile.count;
+    const int64_t pos = tile.first + (valid ? row : 0);
     const int64_t id = a.idx ? a.idx[pos] : pos;
+    const int64_t sid = a.gather ? a.gather[id] : id;
     float x0, x1, x2;
     double gw = 1.0;
     {
       double c[3];
-      const int64_t sid = a.gather ? a.gather[id] : id;
       if (point_centre(a.src_kind, a.src, sid, c)) {
         x0 = __double2float_rn((c[0] - s_exp.norm_origin[0]) / s_exp.norm_scale);
         x1 = __double2float_rn((c[1] - s_exp.norm_origin[1]) / s_exp.norm_scale);
@@ -278,34 +296,67 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
         x0 = s[0]; x1 = s[1]; x2 = s[2];
       }
     }
+    // lattice tiles: a full, aligned quarter of one leaf in voxel-id order
+    const bool lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat && tile.count == kTileM &&
+                         (tile.first & (kTileM - 1)) == 0;
+    // lattice thread role: voxel z index lk, feature pair lf of each chunk
+    const int lk = gt & 7, lf = gt >> 3;
+    float lx[2], ly0, lz;
+    if (lattice) {
+      const int* o = static_cast<const int*>(a.src) + 3 * (tile.first >> 9);
+      const int i0 = (int)((tile.first & 511) >> 6);
+      const double ns = s_exp.norm_scale;
+      lx[0] = __double2float_rn((o[0] + i0 + 0.5 - s_exp.norm_origin[0]) / ns);
+      lx[1] = __double2float_rn((o[0] + i0 + 1.5 - s_exp.norm_origin[0]) / ns);
+      ly0 = __double2float_rn((o[1] + 0.5 - s_exp.norm_origin[1]) / ns);
+      lz = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) / ns);
+    }
 
     // ------------------------------------------------ features + layer 0
     const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
     const int nch = k0 / kChunkK;
     for (int ch = 0; ch < nch; ++ch) {
       const int b = ch & 1;
-      if (pend[b]) {
-        mbar_wait(bar_c0 + b, (ncommit[b] - 1u) & 1u);
-        pend[b] = false;
-      }
+      if (b == 0 && pend0) { mbar_wait(bar_c0, (nc0 - 1u) & 1u); pend0 = false; }
+      if (b == 1 && pend1) { mbar_wait(bar_c0 + 1, (nc1 - 1u) & 1u); pend1 = false; }
       const uint32_t buf = region_s + b * kChunkBytes;
+      if (lattice) {
+        const int f = ch * (kChunkK / 2) + lf;
+        const float bx = s_b2pi[f], by = s_b2pi[mp + f], bz = s_b2pi[2 * mp + f];
+        const float cb = s_lat[2 * f], sb = s_lat[2 * f + 1];
 #pragma unroll
-      for (int q = 0; q < kChunkK / 8; ++q) {
-        uint32_t h[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int f = ch * (kChunkK / 2) + q * 4 + j;
-          const float th = fmaf(x2, sv.b2pi[2 * mp + f], fmaf(x1, sv.b2pi[mp + f], x0 * sv.b2pi[f]));
+        for (int ii = 0; ii < 2; ++ii) {
+          const float th = fmaf(lz, bz, fmaf(ly0, by, lx[ii] * bx));
           float sn, cs;
           __sincosf(th, &sn, &cs);
-          h[j] = pack_half2(cs, sn);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int r = ii * 64 + j * 8 + lk;
+            st_shared_b32(buf + kmajor_offset(r, 2 * lf, kTileM), pack_half2(cs, sn));
+            const float c2 = fmaf(cs, cb, -sn * sb);
+            sn = fmaf(cs, sb, sn * cb);
+            cs = c2;
+          }
         }
-        st_shared_v4(buf + kmajor_offset(t, q * 8, kTileM), h[0], h[1], h[2], h[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t h[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int f = ch * (kChunkK / 2) + half * 16 + q * 4 + j;
+            const float th = fmaf(x2, s_b2pi[2 * mp + f], fmaf(x1, s_b2pi[mp + f], x0 * s_b2pi[f]));
+            float sn, cs;
+            __sincosf(th, &sn, &cs);
+            h[j] = pack_half2(cs, sn);
+          }
+          st_shared_v4(buf + kmajor_offset(row, half * 32 + q * 8, kTileM), h[0], h[1], h[2], h[3]);
+        }
       }
       fence_async_smem();
       tc_fence_before();
-      named_bar_sync(1 + wg, 128);
-      if (t == 0) {
+      named_bar_sync(1 + grp, kGroupThreads);
+      if (gt == 0) {
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < kChunkK / 16; ++s) {
@@ -317,12 +368,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
         umma_commit(bar_c0 + b);
         if (ch == nch - 1) umma_commit(bar_layer);
       }
-      ncommit[b]++;
-      pend[b] = true;
+      if (b == 0) { nc0++; pend0 = true; } else { nc1++; pend1 = true; }
     }
     mbar_wait(bar_layer, nlayer & 1u);
     nlayer++;
-    pend[0] = pend[1] = false;
+    pend0 = pend1 = false;
     tc_fence_after();
 
     // ------------------------------------------------ hidden epilogues
@@ -330,8 +380,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
     uint32_t woff = (uint32_t)(width * k0 * 2);  // byte offset of W1 in the image
     for (int l = 0; l < depth; ++l) {
       const bool last = (l == depth - 1);
-      const float* bl = sv.bias + l * width;
-      for (int cc = 0; cc < width / 16; ++cc) {
+      const float* bl = s_bias + l * width;
+      for (int cc = half; cc < width / 16; cc += 2) {
         float v[16];
         tmem_ld16(tmem_d + cc * 16, v);
         tmem_ld_wait();
@@ -339,15 +389,15 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
 #pragma unroll
         for (int i = 0; i < 16; ++i) av[i] = act_fn(act, v[i] + bl[cc * 16 + i]);
         if (!last) {
-          st_shared_v4(region_s + kmajor_offset(t, cc * 16, kTileM), pack_half2(av[0], av[1]),
+          st_shared_v4(region_s + kmajor_offset(row, cc * 16, kTileM), pack_half2(av[0], av[1]),
                        pack_half2(av[2], av[3]), pack_half2(av[4], av[5]), pack_half2(av[6], av[7]));
-          st_shared_v4(region_s + kmajor_offset(t, cc * 16 + 8, kTileM), pack_half2(av[8], av[9]),
+          st_shared_v4(region_s + kmajor_offset(row, cc * 16 + 8, kTileM), pack_half2(av[8], av[9]),
                        pack_half2(av[10], av[11]), pack_half2(av[12], av[13]), pack_half2(av[14], av[15]));
         } else {
 #pragma unroll
           for (int k = 0; k < kMaxOut; ++k) {
             if (k < out_dim) {
-              const float* hw = sv.headw + k * width + cc * 16;
+              const float* hw = s_headw + k * width + cc * 16;
               float s = y[k];
 #pragma unroll
               for (int i = 0; i < 16; ++i) s = fmaf(av[i], hw[i], s);
@@ -359,8 +409,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
       if (!last) {
         fence_async_smem();
         tc_fence_before();
-        named_bar_sync(1 + wg, 128);
-        if (t == 0) {
+        named_bar_sync(1 + grp, kGroupThreads);
+        if (gt == 0) {
           tc_fence_after();
           const uint32_t wl = w_s + woff;
           for (int s = 0; s < width / 16; ++s) {
@@ -376,12 +426,19 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
         tc_fence_after();
       }
     }
+    // head partials of the two halves of each row meet in shared memory
+    if (half) {
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k) s_hx[row * 4 + k] = y[k];
+    }
+    tc_fence_before();
+    named_bar_sync(1 + grp, kGroupThreads);
+    if (half || !valid) continue;
 #pragma unroll
     for (int k = 0; k < kMaxOut; ++k)
-      if (k < out_dim) y[k] += sv.headb[k];
+      if (k < out_dim) y[k] = (y[k] + s_hx[row * 4 + k]) + s_headb[k];
 
     // ------------------------------------------------ output
-    if (!valid) continue;
     if (a.out_mode == OUT_RAW) {
 #pragma unroll
       for (int k = 0; k < kMaxOut; ++k)

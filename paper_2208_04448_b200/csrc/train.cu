@@ -180,26 +180,30 @@ __device__ __forceinline__ float act_deriv_from(int act, float zp) {
   return zp > 0.0f ? 1.0f : 0.0f;
 }
 
-__global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
+__global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if (*a.stopped) return;
   const int tid = threadIdx.x;
-  const int wg = tid >> 7;
-  const int t = tid & 127;
-  const int wwarp = t >> 5;
-  const int nthreads = a.nwg * 128;
+  const int grp = tid >> 8;               // tile group (a.nwg groups of 8 warps)
+  const int gt = tid & 255;
+  const int gw = gt >> 5;
+  const int quad = gw & 3;                // TMEM lane quadrant
+  const int half = gw >> 2;               // half of the feature pairs / columns
+  const int row = quad * 32 + (gt & 31);  // tile row == TMEM lane
+  const int nthreads = a.nwg * 256;
   const NetDev& nd = a.net;
   const int width = nd.width, depth = nd.depth, k0 = nd.k0, out_dim = nd.out_dim, act = nd.act;
   const int mp = k0 >> 1;
   uint8_t* wsm = smem + a.w_off;
   float* small = reinterpret_cast<float*>(smem + a.small_off);
-  float* s_bias = small;
-  float* s_headw = small + 4 * 256;
-  float* s_headb = s_headw + 3 * 256;
-  float* s_b2pi = s_headb + 4;
+  float* s_bias = small + kSmallBias;
+  float* s_headw = small + kSmallHeadW;
+  float* s_headb = small + kSmallHeadB;
+  float* s_b2pi = small + kSmallB2pi;
+  float* s_hx = small + kSmallHx + grp * 128 * 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
-  __shared__ double s_loss[8];
+  __shared__ double s_loss[2][8];
 
   if (tid == 0) {
     for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
@@ -218,13 +222,13 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
   tc_fence_after();
   mbar_wait(&bars[0], 0);
   const uint32_t tmem_base = *tmem_slot;
-  uint64_t* bar_c0 = &bars[1 + 3 * wg];
-  uint64_t* bar_layer = &bars[3 + 3 * wg];
-  uint32_t ncommit0 = 0, ncommit1 = 0, nlayer = 0;
+  uint64_t* bar_c0 = &bars[1 + 3 * grp];
+  uint64_t* bar_layer = &bars[3 + 3 * grp];
+  uint32_t nc0 = 0, nc1 = 0, nlayer = 0;
   bool pend0 = false, pend1 = false;
-  const uint32_t tcol = tmem_base + (uint32_t)(wg * (a.nwg == 2 ? 256 : 0));
-  const uint32_t lane_off = (uint32_t)(wwarp * 32) << 16;
-  const uint32_t region_s = smem_addr(smem + a.region_off + wg * a.region_bytes);
+  const uint32_t tcol = tmem_base + (uint32_t)(grp * 256);
+  const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+  const uint32_t region_s = smem_addr(smem + a.region_off + grp * a.region_bytes);
   const uint32_t w_s = smem_addr(wsm);
   const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
   const uint32_t idesc_bt = idesc_f16(kTileM, width, 0, 1);  // B = W'^T read MN-major
@@ -235,8 +239,8 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
   double loss_acc = 0.0;
   const size_t tile_elems = (size_t)kTileM * width;
 
-  for (int64_t tau = t0 + wg; tau < t1; tau += a.nwg) {
-    const int64_t b = tau * kTileM + t;
+  for (int64_t tau = t0 + grp; tau < t1; tau += a.nwg) {
+    const int64_t b = tau * kTileM + row;
     const bool valid = b < a.batch;
     const int64_t pidx = valid ? (a.idx ? a.idx[b] : b) : 0;
     const float x0 = a.xs[3 * pidx], x1 = a.xs[3 * pidx + 1], x2 = a.xs[3 * pidx + 2];
@@ -245,26 +249,26 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
     const int nch = k0 / kChunkK;
     for (int ch = 0; ch < nch; ++ch) {
       const int bsel = ch & 1;
-      if (bsel == 0 && pend0) { mbar_wait(bar_c0, (ncommit0 - 1u) & 1u); pend0 = false; }
-      if (bsel == 1 && pend1) { mbar_wait(bar_c0 + 1, (ncommit1 - 1u) & 1u); pend1 = false; }
+      if (bsel == 0 && pend0) { mbar_wait(bar_c0, (nc0 - 1u) & 1u); pend0 = false; }
+      if (bsel == 1 && pend1) { mbar_wait(bar_c0 + 1, (nc1 - 1u) & 1u); pend1 = false; }
       const uint32_t buf = region_s + bsel * kChunkBytes;
 #pragma unroll
-      for (int q = 0; q < kChunkK / 8; ++q) {
+      for (int q = 0; q < 4; ++q) {
         uint32_t h[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int f = ch * (kChunkK / 2) + q * 4 + j;
+          const int f = ch * (kChunkK / 2) + half * 16 + q * 4 + j;
           const float th = fmaf(x2, s_b2pi[2 * mp + f], fmaf(x1, s_b2pi[mp + f], x0 * s_b2pi[f]));
           float sn, cs;
           __sincosf(th, &sn, &cs);
           h[j] = pack_half2(cs, sn);
         }
-        st_shared_v4(buf + kmajor_offset(t, q * 8, kTileM), h[0], h[1], h[2], h[3]);
+        st_shared_v4(buf + kmajor_offset(row, half * 32 + q * 8, kTileM), h[0], h[1], h[2], h[3]);
       }
       fence_async_smem();
       tc_fence_before();
-      named_bar_sync(1 + wg, 128);
-      if (t == 0) {
+      named_bar_sync(1 + grp, 256);
+      if (gt == 0) {
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < kChunkK / 16; ++s) {
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
         umma_commit(bar_c0 + bsel);
         if (ch == nch - 1) umma_commit(bar_layer);
       }
-      if (bsel == 0) { ncommit0++; pend0 = true; } else { ncommit1++; pend1 = true; }
+      if (bsel == 0) { nc0++; pend0 = true; } else { nc1++; pend1 = true; }
     }
     mbar_wait(bar_layer, nlayer & 1u);
     nlayer++;
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
       const bool last = (l == depth - 1);
       const float* bl = s_bias + l * width;
       uint16_t* gact = a.act_img + ((size_t)l * ntiles + tau) * tile_elems;
-      for (int cc = 0; cc < width / 16; ++cc) {
+      for (int cc = half; cc < width / 16; cc += 2) {
         float v[16];
         tmem_ld16(tcol + lane_off + l * width + cc * 16, v);
         tmem_ld_wait();
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
         const uint32_t p2 = pack_half2(av[4], av[5]), p3 = pack_half2(av[6], av[7]);
         const uint32_t p4 = pack_half2(av[8], av[9]), p5 = pack_half2(av[10], av[11]);
         const uint32_t p6 = pack_half2(av[12], av[13]), p7 = pack_half2(av[14], av[15]);
-        const uint32_t o0 = kmajor_offset(t, cc * 16, kTileM), o1 = kmajor_offset(t, cc * 16 + 8, kTileM);
+        const uint32_t o0 = kmajor_offset(row, cc * 16, kTileM), o1 = kmajor_offset(row, cc * 16 + 8, kTileM);
         *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o0) = make_uint4(p0, p1, p2, p3);
         *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o1) = make_uint4(p4, p5, p6, p7);
         if (!last) {
@@ -320,8 +324,8 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
       if (!last) {
         fence_async_smem();
         tc_fence_before();
-        named_bar_sync(1 + wg, 128);
-        if (t == 0) {
+        named_bar_sync(1 + grp, 256);
+        if (gt == 0) {
           tc_fence_after();
           const uint32_t wl = w_s + woff;
           for (int s = 0; s < width / 16; ++s) {
@@ -337,51 +341,65 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
         tc_fence_after();
       }
     }
-    // ---------------- head, loss, dL/dout (neural.py:271-302, without 1/size)
+    // ---------------- head partials meet; loss and dL/dout (neural.py:271-302, without 1/size)
+    if (half) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) s_hx[row * 4 + k] = yv[k];
+    }
+    named_bar_sync(1 + grp, 256);
     float dl[3] = {0.f, 0.f, 0.f};
     float lterm = 0.f;
+    if (!half) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-      if (k < out_dim) yv[k] += s_headb[k];
-    if (valid) {
-      if (a.loss_kind == 0) {  // mse
-        const float d = yv[0] - y;
-        lterm = d * d;
-        dl[0] = 2.0f * d;
-      } else if (a.loss_kind == 2) {  // bce
-        const float z = yv[0];
-        lterm = fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
-        dl[0] = 1.0f / (1.0f + expf(-z)) - y;
-      } else {  // ce, 3 classes
-        const float zm = fmaxf(fmaxf(yv[0], yv[1]), yv[2]);
-        const float e0 = expf(yv[0] - zm), e1 = expf(yv[1] - zm), e2 = expf(yv[2] - zm);
-        const float s = (e0 + e1) + e2;
-        const int lab = (int)y;
-        const float zl = lab == 0 ? yv[0] : (lab == 1 ? yv[1] : yv[2]);
-        lterm = -(zl - zm - logf(s));
-        dl[0] = e0 / s - (lab == 0 ? 1.f : 0.f);
-        dl[1] = e1 / s - (lab == 1 ? 1.f : 0.f);
-        dl[2] = e2 / s - (lab == 2 ? 1.f : 0.f);
+      for (int k = 0; k < 3; ++k)
+        if (k < out_dim) yv[k] = (yv[k] + s_hx[row * 4 + k]) + s_headb[k];
+      if (valid) {
+        if (a.loss_kind == 0) {  // mse
+          const float d = yv[0] - y;
+          lterm = d * d;
+          dl[0] = 2.0f * d;
+        } else if (a.loss_kind == 2) {  // bce
+          const float z = yv[0];
+          lterm = fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
+          dl[0] = 1.0f / (1.0f + expf(-z)) - y;
+        } else {  // ce, 3 classes
+          const float zm = fmaxf(fmaxf(yv[0], yv[1]), yv[2]);
+          const float e0 = expf(yv[0] - zm), e1 = expf(yv[1] - zm), e2 = expf(yv[2] - zm);
+          const float s = (e0 + e1) + e2;
+          const int lab = (int)y;
+          const float zl = lab == 0 ? yv[0] : (lab == 1 ? yv[1] : yv[2]);
+          lterm = -(zl - zm - logf(s));
+          dl[0] = e0 / s - (lab == 0 ? 1.f : 0.f);
+          dl[1] = e1 / s - (lab == 1 ? 1.f : 0.f);
+          dl[2] = e2 / s - (lab == 2 ? 1.f : 0.f);
+        }
       }
-    }
-    {  // dL/dout tile image (128 x 16, fp16)
       uint8_t* gd = reinterpret_cast<uint8_t*>(a.dlt_img + (size_t)tau * kTileM * 16);
-      *reinterpret_cast<uint4*>(gd + kmajor_offset(t, 0, kTileM)) =
+      *reinterpret_cast<uint4*>(gd + kmajor_offset(row, 0, kTileM)) =
           make_uint4(pack_half2(dl[0], dl[1]), pack_half2(dl[2], 0.f), 0u, 0u);
-      *reinterpret_cast<uint4*>(gd + kmajor_offset(t, 8, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(gd + kmajor_offset(row, 8, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
     }
     // deterministic loss sum: warp shuffle, then fixed warp order
     float ls = lterm;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
-    if ((t & 31) == 0) s_loss[wg * 4 + wwarp] = (double)ls;
-    named_bar_sync(1 + wg, 128);
-    if (t == 0) loss_acc += ((s_loss[wg * 4] + s_loss[wg * 4 + 1]) + s_loss[wg * 4 + 2]) + s_loss[wg * 4 + 3];
+    if ((gt & 31) == 0) s_loss[grp][gw] = (double)ls;
+    named_bar_sync(1 + grp, 256);  // also publishes the head partials' slots for reuse below
+    if (gt == 0) loss_acc += ((s_loss[grp][0] + s_loss[grp][1]) + s_loss[grp][2]) + s_loss[grp][3];
+    if (!half) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) s_hx[row * 4 + k] = dl[k];
+    }
+    named_bar_sync(1 + grp, 256);
+    if (half) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dl[k] = s_hx[row * 4 + k];
+    }
     // ---------------- backward: dz_h = da_h * f'(z'_h); da_{h-1} = dz_h . W'_h
     for (int l = depth - 1; l >= 0; --l) {
       const float* bl = s_bias + l * width;
       uint16_t* gdz = a.dz_img + ((size_t)l * ntiles + tau) * tile_elems;
-      for (int cc = 0; cc < width / 16; ++cc) {
+      for (int cc = half; cc < width / 16; cc += 2) {
         float z[16], da[16];
         tmem_ld16(tcol + lane_off + l * width + cc * 16, z);
         if (l < depth - 1) tmem_ld16(tcol + lane_off + (l + 1) * width + cc * 16, da);
@@ -403,7 +421,7 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
         const uint32_t p2 = pack_half2(dz[4], dz[5]), p3 = pack_half2(dz[6], dz[7]);
         const uint32_t p4 = pack_half2(dz[8], dz[9]), p5 = pack_half2(dz[10], dz[11]);
         const uint32_t p6 = pack_half2(dz[12], dz[13]), p7 = pack_half2(dz[14], dz[15]);
-        const uint32_t o0 = kmajor_offset(t, cc * 16, kTileM), o1 = kmajor_offset(t, cc * 16 + 8, kTileM);
+        const uint32_t o0 = kmajor_offset(row, cc * 16, kTileM), o1 = kmajor_offset(row, cc * 16 + 8, kTileM);
         *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o0) = make_uint4(p0, p1, p2, p3);
         *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o1) = make_uint4(p4, p5, p6, p7);
         if (l > 0) {
@@ -414,8 +432,8 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
       if (l > 0) {
         fence_async_smem();
         tc_fence_before();
-        named_bar_sync(1 + wg, 128);
-        if (t == 0) {
+        named_bar_sync(1 + grp, 256);
+        if (gt == 0) {
           tc_fence_after();
           // W'_l image (rows o, cols i, K-major) read as B = (N = i, K = o) MN-major
           const uint32_t wl = w_s + (uint32_t)(width * k0 * 2) + (uint32_t)((l - 1) * width * width * 2);
@@ -431,11 +449,12 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
         tc_fence_after();
       }
     }
-    named_bar_sync(1 + wg, 128);  // all TMEM reads of this tile done before the next tile's MMAs
+    tc_fence_before();
+    named_bar_sync(1 + grp, 256);  // all TMEM reads of this tile done before the next tile's MMAs
   }
-  // per-CTA loss partial (fixed order: WG0 then WG1)
+  // per-CTA loss partial (fixed order: group 0 then group 1)
   __shared__ double s_wgl[2];
-  if (t == 0) s_wgl[wg] = loss_acc;
+  if (gt == 0) s_wgl[grp] = loss_acc;
   tc_fence_before();
   __syncthreads();
   if (tid == 0) a.loss_part[blockIdx.x] = a.nwg == 2 ? s_wgl[0] + s_wgl[1] : s_wgl[0];
@@ -443,6 +462,8 @@ __global__ void __launch_bounds__(256, 1) k_train_fb(const FbArgs a) {
 }
 
 // ------------------------------------------------------------------ weight gradients
+constexpr uint32_t kWgSmem = 208896 + 3 * 512 * 4 + 128;
+
 struct WgArgs {
   NetDev net;
   int32_t m;                  // real frequency count (2m real features)
@@ -460,77 +481,119 @@ struct WgArgs {
   uint32_t col_w0, col_b0, col_h, col_head;  // TMEM column bases
 };
 
-__global__ void __launch_bounds__(128, 1) k_train_wgrad(const WgArgs a) {
+__global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if (*a.stopped) return;
   const int t = threadIdx.x;
-  const int wwarp = t >> 5;
+  const int row = t & 127;
+  const int half = t >> 7;
+  const int quad = (t >> 5) & 3;
   const NetDev& nd = a.net;
   const int W = nd.width, depth = nd.depth, k0 = nd.k0, mp = k0 >> 1;
-  // smem: act buf (32K) | dz buf (32K) | feat ring 2x32K | dlt (4K) | ones (4K) | b2pi | bars
-  uint8_t* s_act = smem;
-  uint8_t* s_dz = smem + 32768;
-  uint8_t* s_feat = smem + 65536;
-  uint8_t* s_dlt = smem + 131072;
-  uint8_t* s_ones = smem + 135168;
-  float* s_b2pi = reinterpret_cast<float*>(smem + 139264);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 139264 + 3 * 512 * 4);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-  // bars[0] loads, bars[1] mma done, bars[2] feat buf 0, bars[3] feat buf 1
+  // smem: 2 x [act 32K | dz 32K] | feat ring 2 x 32K | 2 x dlt 4K | ones 4K | b2pi | bars
+  uint8_t* s_act[2] = {smem, smem + 65536};
+  uint8_t* s_dz[2] = {smem + 32768, smem + 65536 + 32768};
+  uint8_t* s_feat = smem + 131072;
+  uint8_t* s_dlt[2] = {smem + 196608, smem + 200704};
+  uint8_t* s_ones = smem + 204800;
+  float* s_b2pi = reinterpret_cast<float*>(smem + 208896);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 208896 + 3 * 512 * 4);
+  // bars: [0,1] full (stage data landed), [2,3] free (stage MMAs done), [4,5] feature ring free, [6] final
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
   if (t == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
   if (t < 32) tmem_alloc(tmem_slot, 512);
-  for (int i = t; i < 3 * mp; i += 128) s_b2pi[i] = nd.b2pi[i];
-  // ones tile (B operand, N = 16, K = 128 samples) and the ones column of the
-  // augmented activation buffer (column W = 1, W+1..W+15 = 0)
-  for (int i = t; i < 16 * 128; i += 128) reinterpret_cast<__half*>(s_ones)[i] = __float2half(1.0f);
-  {
-    const uint32_t o0 = kmajor_offset(t, W, kTileM), o1 = kmajor_offset(t, W + 8, kTileM);
-    *reinterpret_cast<uint4*>(s_act + o0) = make_uint4(pack_half2(1.f, 0.f), 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(s_act + o1) = make_uint4(0u, 0u, 0u, 0u);
+  for (int i = t; i < 3 * mp; i += 256) s_b2pi[i] = nd.b2pi[i];
+  for (int i = t; i < 16 * 128; i += 256) reinterpret_cast<__half*>(s_ones)[i] = __float2half(1.0f);
+  if (t < 128) {  // ones column (W) and zero columns (W+1..W+15) of both augmented activation buffers
+    for (int b = 0; b < 2; ++b) {
+      const uint32_t o0 = kmajor_offset(t, W, kTileM), o1 = kmajor_offset(t, W + 8, kTileM);
+      *reinterpret_cast<uint4*>(s_act[b] + o0) = make_uint4(pack_half2(1.f, 0.f), 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(s_act[b] + o1) = make_uint4(0u, 0u, 0u, 0u);
+    }
   }
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t lane_off = (uint32_t)(wwarp * 32) << 16;
-  uint32_t nload = 0, nmma = 0, nf0 = 0, nf1 = 0;
-  bool pf0 = false, pf1 = false;
+  const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
   const int64_t ntiles = (a.batch + kTileM - 1) / kTileM;
   const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
   const size_t tbytes = (size_t)kTileM * W * 2;
-  const uint32_t sa = smem_addr(s_act), sdz = smem_addr(s_dz), sfe = smem_addr(s_feat);
-  const uint32_t sdl = smem_addr(s_dlt), son = smem_addr(s_ones);
+  const uint32_t sfe = smem_addr(s_feat), son = smem_addr(s_ones);
   const int nmt = (k0 + 127) / 128;  // M tiles of 128 features
-  bool first = true;
+  const int nst = depth + 1;          // load stages per tile: dz0 | (a0,dz1) .. | (a_{d-1}, dlt)
+  const int64_t nstages = (t1 - t0) * nst;
+  // thread-0 pipeline state
+  uint32_t nfull[2] = {0, 0}, nfree[2] = {0, 0};
+  bool busy[2] = {false, false};
+  int64_t issued = 0;  // stages whose loads were issued
+  uint32_t nring0 = 0, nring1 = 0;
+  bool pr0 = false, pr1 = false;
 
-  auto load = [&](uint8_t* dst, const void* src, uint32_t bytes) {
-    bulk_g2s(dst, src, bytes, &bars[0]);
-  };
-
-  for (int64_t tau = t0; tau < t1; ++tau) {
-    const int64_t b = tau * kTileM + t;
-    const bool valid = b < a.batch;
-    const int64_t pidx = valid ? (a.idx ? a.idx[b] : b) : 0;
-    const float x0 = a.xs[3 * pidx], x1 = a.xs[3 * pidx + 1], x2 = a.xs[3 * pidx + 2];
-    // ---- layer 0: gW0^T[k][o] += F^T dz0, gb0 += dz0^T 1
-    if (t == 0) {
-      mbar_arrive_expect_tx(&bars[0], (uint32_t)tbytes);
-      load(s_dz, reinterpret_cast<const uint8_t*>(a.dz_img) + tau * tbytes, (uint32_t)tbytes);
+  auto issue_load = [&](int64_t q) {  // thread 0 only
+    const int b = (int)(q & 1);
+    const int64_t tau = t0 + q / nst;
+    const int s = (int)(q % nst);
+    if (busy[b]) {  // stage q-2 used this buffer: wait for its MMAs
+      mbar_wait(&bars[2 + b], (nfree[b] - 1u) & 1u);
+      busy[b] = false;
     }
-    mbar_wait(&bars[0], nload & 1u);
-    nload++;
+    uint32_t bytes = (uint32_t)tbytes;
+    if (s > 0) bytes += (s == depth) ? (uint32_t)(kTileM * 16 * 2) : (uint32_t)tbytes;
+    mbar_arrive_expect_tx(&bars[b], bytes);
+    if (s == 0) {
+      bulk_g2s(s_dz[b], reinterpret_cast<const uint8_t*>(a.dz_img) + tau * tbytes, (uint32_t)tbytes, &bars[b]);
+    } else {
+      bulk_g2s(s_act[b], reinterpret_cast<const uint8_t*>(a.act_img) + ((size_t)(s - 1) * ntiles + tau) * tbytes,
+               (uint32_t)tbytes, &bars[b]);
+      if (s == depth)
+        bulk_g2s(s_dlt[b], reinterpret_cast<const uint8_t*>(a.dlt_img) + (size_t)tau * kTileM * 16 * 2,
+                 kTileM * 16 * 2, &bars[b]);
+      else
+        bulk_g2s(s_dz[b], reinterpret_cast<const uint8_t*>(a.dz_img) + ((size_t)s * ntiles + tau) * tbytes,
+                 (uint32_t)tbytes, &bars[b]);
+    }
+  };
+  auto wait_full = [&](int64_t q) {
+    const int b = (int)(q & 1);
+    mbar_wait(&bars[b], nfull[b] & 1u);
+    nfull[b]++;
+    tc_fence_after();
+  };
+  auto done_stage = [&](int64_t q) {
+    const int b = (int)(q & 1);
+    umma_commit(&bars[2 + b]);
+    nfree[b]++;
+    busy[b] = true;
+  };
+  if (t == 0 && nstages > 0) {
+    issue_load(0);
+    issued = 1;
+  }
+  bool first = true;
+  for (int64_t tau = t0; tau < t1; ++tau) {
+    const int64_t qbase = (tau - t0) * nst;
+    const int64_t bidx = tau * kTileM + row;
+    const bool valid = bidx < a.batch;
+    const int64_t pidx = valid ? (a.idx ? a.idx[bidx] : bidx) : 0;
+    const float x0 = a.xs[3 * pidx], x1 = a.xs[3 * pidx + 1], x2 = a.xs[3 * pidx + 2];
+    // ---- stage 0: gW0^T[k][o] += F^T dz0 (features recomputed), gb0 += dz0^T 1
+    if (t == 0 && issued < nstages) {
+      issue_load(issued);
+      issued++;
+    }
     for (int j = 0; j < nmt; ++j) {
-      const int bsel = j & 1;
-      if (bsel == 0 && pf0) { mbar_wait(&bars[2], (nf0 - 1u) & 1u); pf0 = false; }
-      if (bsel == 1 && pf1) { mbar_wait(&bars[3], (nf1 - 1u) & 1u); pf1 = false; }
-      const uint32_t fb = sfe + bsel * 32768;
+      const int rb = j & 1;
+      if (rb == 0 && pr0) { mbar_wait(&bars[4], (nring0 - 1u) & 1u); pr0 = false; }
+      if (rb == 1 && pr1) { mbar_wait(&bars[5], (nring1 - 1u) & 1u); pr1 = false; }
+      const uint32_t fb = sfe + rb * 32768;
       const int nf = min(128, k0 - j * 128);
-      for (int q = 0; q < nf / 8; ++q) {
+      for (int q = half; q < nf / 8; q += 2) {
         uint32_t h[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -540,80 +603,75 @@ __global__ void __launch_bounds__(128, 1) k_train_wgrad(const WgArgs a) {
           __sincosf(th, &sn, &cs);
           h[i] = valid ? pack_half2(cs, sn) : 0u;
         }
-        st_shared_v4(fb + kmajor_offset(t, q * 8, kTileM), h[0], h[1], h[2], h[3]);
+        st_shared_v4(fb + kmajor_offset(row, q * 8, kTileM), h[0], h[1], h[2], h[3]);
       }
       fence_async_smem();
       tc_fence_before();
-      __syncthreads();
+      named_bar_sync(1, 256);
       if (t == 0) {
+        if (j == 0) wait_full(qbase);
         tc_fence_after();
+        const uint32_t sdz = smem_addr(s_dz[qbase & 1]);
         const uint32_t idesc = idesc_f16(kTileM, W, 1, 1);
         for (int s = 0; s < kTileM / 16; ++s)
           umma_f16(tmem + a.col_w0 + j * W, smem_desc(fb + s * 256, 128, 2048), smem_desc(sdz + s * 256, 128, 2048),
                    idesc, (!first || s != 0) ? 1u : 0u);
-        umma_commit(&bars[2 + bsel]);
+        umma_commit(&bars[4 + rb]);
       }
-      if (bsel == 0) { nf0++; pf0 = true; } else { nf1++; pf1 = true; }
+      if (rb == 0) { nring0++; pr0 = true; } else { nring1++; pr1 = true; }
     }
     if (t == 0) {
+      const uint32_t sdz = smem_addr(s_dz[qbase & 1]);
       const uint32_t idesc = idesc_f16(kTileM, 16, 1, 0);
       for (int s = 0; s < kTileM / 16; ++s)
         umma_f16(tmem + a.col_b0, smem_desc(sdz + s * 256, 128, 2048), smem_desc(son + s * 512, 256, 128), idesc,
                  (!first || s != 0) ? 1u : 0u);
-      umma_commit(&bars[1]);
-    }
-    mbar_wait(&bars[1], nmma & 1u);
-    nmma++;
-    pf0 = pf1 = false;
-    // ---- hidden layers h >= 1: gW_h^T[i][o] += [a_{h-1} | 1]^T dz_h
-    for (int l = 1; l <= depth; ++l) {
-      const bool head = (l == depth);
-      if (t == 0) {
-        tc_fence_after();
-        const uint32_t bytes = (uint32_t)tbytes + (head ? (uint32_t)(kTileM * 16 * 2) : (uint32_t)tbytes);
-        mbar_arrive_expect_tx(&bars[0], bytes);
-        load(s_act, reinterpret_cast<const uint8_t*>(a.act_img) + ((size_t)(l - 1) * ntiles + tau) * tbytes,
-             (uint32_t)tbytes);
-        if (head)
-          load(s_dlt, reinterpret_cast<const uint8_t*>(a.dlt_img) + (size_t)tau * kTileM * 16 * 2, kTileM * 16 * 2);
-        else
-          load(s_dz, reinterpret_cast<const uint8_t*>(a.dz_img) + ((size_t)l * ntiles + tau) * tbytes,
-               (uint32_t)tbytes);
-      }
-      mbar_wait(&bars[0], nload & 1u);
-      nload++;
-      if (t == 0) {
+      done_stage(qbase);
+      // ---- stages 1..depth: gW_l^T[i][o] += [a_{l-1} | 1]^T dz_l (head: dL/dout)
+      for (int l = 1; l <= depth; ++l) {
+        const int64_t q = qbase + l;
+        if (issued < nstages) {
+          issue_load(issued);
+          issued++;
+        }
+        wait_full(q);
+        const bool head = (l == depth);
+        const int b = (int)(q & 1);
         const int N = head ? 16 : W;
         const uint32_t idesc = idesc_f16(kTileM, N, 1, 1);
         const uint32_t col = head ? a.col_head : a.col_h + (l - 1) * W;
-        const uint32_t bsrc = head ? sdl : sdz;
+        const uint32_t sa = smem_addr(s_act[b]);
+        const uint32_t bsrc = head ? smem_addr(s_dlt[b]) : smem_addr(s_dz[b]);
         for (int s = 0; s < kTileM / 16; ++s)
           umma_f16(tmem + col, smem_desc(sa + s * 256, 128, 2048), smem_desc(bsrc + s * 256, 128, 2048), idesc,
                    (!first || s != 0) ? 1u : 0u);
-        umma_commit(&bars[1]);
+        done_stage(q);
       }
-      mbar_wait(&bars[1], nmma & 1u);
-      nmma++;
     }
     first = false;
-    tc_fence_after();
   }
-  // ---- flush per-CTA partials (zeros when this CTA had no tiles)
+  // ---- wait for every MMA, then flush per-CTA partials (zeros when no tiles)
+  if (t == 0) {
+    umma_commit(&bars[6]);
+    mbar_wait(&bars[6], 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   float* part = a.partial + (size_t)blockIdx.x * a.P;
   const int Wr = a.width_real, K0r = 2 * a.m;
+  const bool none = (t1 <= t0);
   auto rd = [&](uint32_t col, float (&v)[16]) {
-    if (first) {
+    tmem_ld16(tmem + lane_off + col, v);
+    tmem_ld_wait();
+    if (none) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = 0.f;
-    } else {
-      tmem_ld16(tmem + lane_off + col, v);
-      tmem_ld_wait();
     }
   };
-  // gW0: lane t of M tile j = feature k = 128 j + t ; W0 (Wr x K0r)
   for (int j = 0; j < nmt; ++j) {
-    const int k = j * 128 + t;
-    for (int cc = 0; cc < W / 16; ++cc) {
+    const int k = j * 128 + row;
+    for (int cc = half; cc < W / 16; cc += 2) {
       float v[16];
       rd(a.col_w0 + j * W + cc * 16, v);
       if (k < K0r)
@@ -623,24 +681,24 @@ __global__ void __launch_bounds__(128, 1) k_train_wgrad(const WgArgs a) {
         }
     }
   }
-  {
+  if (half == 0) {
     float v[16];
     rd(a.col_b0, v);
-    if (t < Wr) part[a.poff[1] + t] = v[0];
+    if (row < Wr) part[a.poff[1] + row] = v[0];
   }
   for (int l = 1; l <= depth; ++l) {
     const bool head = (l == depth);
     const int N = head ? 16 : W;
     const int outs = head ? nd.out_dim : Wr;
     const uint32_t col = head ? a.col_head : a.col_h + (l - 1) * W;
-    for (int cc = 0; cc < N / 16; ++cc) {
+    for (int cc = half; cc < N / 16; cc += 2) {
       float v[16];
       rd(col + cc * 16, v);
       for (int i = 0; i < 16; ++i) {
         const int o = cc * 16 + i;
         if (o >= outs) continue;
-        if (t < Wr) part[a.poff[2 * l] + (int64_t)o * Wr + t] = v[i];
-        if (t == W) part[a.poff[2 * l + 1] + o] = v[i];  // ones column -> bias gradient
+        if (row < Wr) part[a.poff[2 * l] + (int64_t)o * Wr + row] = v[i];
+        if (row == W) part[a.poff[2 * l + 1] + o] = v[i];  // ones column -> bias gradient
       }
     }
   }
@@ -682,8 +740,17 @@ __global__ void k_train_adam(AdamArgs a) {
   const float lr = a.lr[e], c1 = a.c1[e], c2 = a.c2[e];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.P; q += stride) {
-    float g = 0.f;
-    for (int c = 0; c < a.ncta; ++c) g += a.partial[(size_t)c * a.P + q];
+    // fixed-order, 4-way interleaved sum of the per-CTA partials
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+    int c = 0;
+    for (; c + 4 <= a.ncta; c += 4) {
+      g0 += a.partial[(size_t)c * a.P + q];
+      g1 += a.partial[(size_t)(c + 1) * a.P + q];
+      g2 += a.partial[(size_t)(c + 2) * a.P + q];
+      g3 += a.partial[(size_t)(c + 3) * a.P + q];
+    }
+    for (; c < a.ncta; ++c) g0 += a.partial[(size_t)c * a.P + q];
+    float g = (g0 + g1) + (g2 + g3);
     g *= a.gscale[q];
     // numpy float32 arithmetic with weak python scalars (neural.py:508-523)
     float m = a.mom[q] * 0.9f;
@@ -957,7 +1024,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   }
   // kernel attributes
   if (enable_max_smem(k_train_fb) < (long long)t->plan.total ||
-      enable_max_smem(k_train_wgrad) < 139264 + 3 * 512 * 4 + 64)
+      enable_max_smem(k_train_wgrad) < kWgSmem)
     return fail(NVDB_EUNSUPPORTED, "training kernels exceed the shared-memory limit");
   *out = tr.release();
   return NVDB_OK;
@@ -1005,7 +1072,7 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
     fa.region_bytes = t->plan.region_bytes;
     fa.small_off = t->plan.small_off;
     fa.bar_off = t->plan.bar_off;
-    k_train_fb<<<t->fb_grid, 128 * t->nwg, std::max<uint32_t>(t->plan.total, 120 * 1024), st>>>(fa);
+    k_train_fb<<<t->fb_grid, 256 * t->nwg, std::max<uint32_t>(t->plan.total, 120 * 1024), st>>>(fa);
     NVDB_CHECK_LAUNCH();
     WgArgs wa{};
     wa.net = t->net;
@@ -1026,7 +1093,7 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
     wa.col_b0 = nmt * t->W;
     wa.col_h = wa.col_b0 + 16;
     wa.col_head = wa.col_h + (t->depth - 1) * t->W;
-    k_train_wgrad<<<t->wg_grid, 128, 139264 + 3 * 512 * 4 + 64, st>>>(wa);
+    k_train_wgrad<<<t->wg_grid, 256, kWgSmem, st>>>(wa);
     NVDB_CHECK_LAUNCH();
     AdamArgs aa{};
     aa.partial = t->partial;

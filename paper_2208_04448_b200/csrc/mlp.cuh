@@ -201,12 +201,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
   float* s_hx = small + kSmallHx + grp * 128 * 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
   // bars[0] = weight load; per group g: [1+3g] chunk buf 0, [2+3g] chunk buf 1, [3+3g] layer
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  // bars[7+2g], bars[8+2g]: chunk buffer "full" (all 256 group threads arrive)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   __shared__ NetDev s_net;
   __shared__ ExpertDev s_exp;
 
   if (tid == 0) {
     for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
+    for (int i = 7; i < 11; ++i) mbar_init(&bars[i], kGroupThreads);
     fence_barrier_init();
   }
   if (tid < 32) tmem_alloc(tmem_slot, 512);
@@ -218,7 +220,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
   uint64_t* bar_w = &bars[0];
   uint64_t* bar_c0 = &bars[1 + 3 * grp];
   uint64_t* bar_layer = &bars[3 + 3 * grp];
-  uint32_t nc0 = 0, nc1 = 0, nlayer = 0, wphase = 0;
+  uint64_t* bar_full = &bars[7 + 2 * grp];
+  uint32_t nc0 = 0, nc1 = 0, nf0 = 0, nf1 = 0, nlayer = 0, wphase = 0;
   bool pend0 = false, pend1 = false;
   int loaded = -1;
 
@@ -324,19 +327,19 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
         const int f = ch * (kChunkK / 2) + lf;
         const float bx = s_b2pi[f], by = s_b2pi[mp + f], bz = s_b2pi[2 * mp + f];
         const float cb = s_lat[2 * f], sb = s_lat[2 * f + 1];
+        // the two x-rows of the tile are independent rotation chains: interleave them
+        float sa, ca, sbn, cbn;
+        __sincosf(fmaf(lz, bz, fmaf(ly0, by, lx[0] * bx)), &sa, &ca);
+        __sincosf(fmaf(lz, bz, fmaf(ly0, by, lx[1] * bx)), &sbn, &cbn);
 #pragma unroll
-        for (int ii = 0; ii < 2; ++ii) {
-          const float th = fmaf(lz, bz, fmaf(ly0, by, lx[ii] * bx));
-          float sn, cs;
-          __sincosf(th, &sn, &cs);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int r = ii * 64 + j * 8 + lk;
-            st_shared_b32(buf + kmajor_offset(r, 2 * lf, kTileM), pack_half2(cs, sn));
-            const float c2 = fmaf(cs, cb, -sn * sb);
-            sn = fmaf(cs, sb, sn * cb);
-            cs = c2;
-          }
+        for (int j = 0; j < 8; ++j) {
+          st_shared_b32(buf + kmajor_offset(j * 8 + lk, 2 * lf, kTileM), pack_half2(ca, sa));
+          st_shared_b32(buf + kmajor_offset(64 + j * 8 + lk, 2 * lf, kTileM), pack_half2(cbn, sbn));
+          const float ca2 = fmaf(ca, cb, -sa * sb), cb2 = fmaf(cbn, cb, -sbn * sb);
+          sa = fmaf(ca, sb, sa * cb);
+          sbn = fmaf(cbn, sb, sbn * cb);
+          ca = ca2;
+          cbn = cb2;
         }
       } else {
 #pragma unroll
@@ -353,10 +356,13 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
           st_shared_v4(buf + kmajor_offset(row, half * 32 + q * 8, kTileM), h[0], h[1], h[2], h[3]);
         }
       }
+      // producer/consumer hand-off: every thread arrives on the chunk's "full"
+      // barrier and moves on; only the issuing thread waits for all arrivals
       fence_async_smem();
-      tc_fence_before();
-      named_bar_sync(1 + grp, kGroupThreads);
+      mbar_arrive(bar_full + b);
+      const uint32_t fpar = (b == 0 ? nf0 : nf1) & 1u;
       if (gt == 0) {
+        mbar_wait(bar_full + b, fpar);
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < kChunkK / 16; ++s) {
@@ -368,7 +374,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
         umma_commit(bar_c0 + b);
         if (ch == nch - 1) umma_commit(bar_layer);
       }
-      if (b == 0) { nc0++; pend0 = true; } else { nc1++; pend1 = true; }
+      if (b == 0) { nc0++; nf0++; pend0 = true; } else { nc1++; nf1++; pend1 = true; }
     }
     mbar_wait(bar_layer, nlayer & 1u);
     nlayer++;

@@ -138,6 +138,7 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
       cells[3 * e + i] = x.cell[i];
     }
     hexp[e].norm_scale = x.norm_scale;
+    hexp[e].inv_scale = 1.0 / x.norm_scale;
     for (int t = 0; t < 4; ++t) {
       const int ni = x.net_index[t];
       if (ni >= nnets) return fail(NVDB_EINVAL, "expert %d: net index %d out of range", e, ni);

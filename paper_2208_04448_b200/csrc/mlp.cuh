@@ -71,6 +71,7 @@ struct alignas(16) NetDev {
 struct alignas(16) ExpertDev {
   double norm_origin[3];
   double norm_scale;
+  double inv_scale;  // 1 / norm_scale
   int32_t cell[3];
   int32_t pad;
 };
@@ -161,7 +162,7 @@ __device__ __forceinline__ double gate_weight(const int cell[3], int S, int halo
   for (int i = 0; i < 3; ++i) {
     const double lo = (double)cell[i] * S;
     const double hi = lo + S;
-    double ramp = fmin(c[i] - (lo - h), (hi + h) - c[i]) / (2.0 * h);
+    double ramp = fmin(c[i] - (lo - h), (hi + h) - c[i]) * (0.5 / h);  // exact: h is a power of two
     ramp = fmin(fmax(ramp, 0.0), 1.0);
     w *= ramp;
   }
@@ -285,34 +286,35 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
     const int64_t pos = tile.first + (valid ? row : 0);
     const int64_t id = a.idx ? a.idx[pos] : pos;
     const int64_t sid = a.gather ? a.gather[id] : id;
-    float x0, x1, x2;
+    // lattice tiles: a full, aligned quarter of one leaf in voxel-id order
+    const bool lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat && tile.count == kTileM &&
+                         (tile.first & (kTileM - 1)) == 0;
+    float x0 = 0.f, x1 = 0.f, x2 = 0.f;
     double gw = 1.0;
-    {
+    if (!lattice || half == 0) {  // inputs for per-point features; gate weight for the output half
       double c[3];
       if (point_centre(a.src_kind, a.src, sid, c)) {
-        x0 = __double2float_rn((c[0] - s_exp.norm_origin[0]) / s_exp.norm_scale);
-        x1 = __double2float_rn((c[1] - s_exp.norm_origin[1]) / s_exp.norm_scale);
-        x2 = __double2float_rn((c[2] - s_exp.norm_origin[2]) / s_exp.norm_scale);
+        const double is = s_exp.inv_scale;
+        x0 = __double2float_rn((c[0] - s_exp.norm_origin[0]) * is);
+        x1 = __double2float_rn((c[1] - s_exp.norm_origin[1]) * is);
+        x2 = __double2float_rn((c[2] - s_exp.norm_origin[2]) * is);
         gw = gate_weight(s_exp.cell, a.subdomain_size, a.halo, c);
       } else {
         const float* s = static_cast<const float*>(a.src) + 3 * sid;
         x0 = s[0]; x1 = s[1]; x2 = s[2];
       }
     }
-    // lattice tiles: a full, aligned quarter of one leaf in voxel-id order
-    const bool lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat && tile.count == kTileM &&
-                         (tile.first & (kTileM - 1)) == 0;
     // lattice thread role: voxel z index lk, feature pair lf of each chunk
     const int lk = gt & 7, lf = gt >> 3;
     float lx[2], ly0, lz;
     if (lattice) {
       const int* o = static_cast<const int*>(a.src) + 3 * (tile.first >> 9);
       const int i0 = (int)((tile.first & 511) >> 6);
-      const double ns = s_exp.norm_scale;
-      lx[0] = __double2float_rn((o[0] + i0 + 0.5 - s_exp.norm_origin[0]) / ns);
-      lx[1] = __double2float_rn((o[0] + i0 + 1.5 - s_exp.norm_origin[0]) / ns);
-      ly0 = __double2float_rn((o[1] + 0.5 - s_exp.norm_origin[1]) / ns);
-      lz = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) / ns);
+      const double is = s_exp.inv_scale;
+      lx[0] = __double2float_rn((o[0] + i0 + 0.5 - s_exp.norm_origin[0]) * is);
+      lx[1] = __double2float_rn((o[0] + i0 + 1.5 - s_exp.norm_origin[0]) * is);
+      ly0 = __double2float_rn((o[1] + 0.5 - s_exp.norm_origin[1]) * is);
+      lz = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) * is);
     }
 
     // ------------------------------------------------ features + layer 0
@@ -393,7 +395,13 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
         tmem_ld_wait();
         float av[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) av[i] = act_fn(act, v[i] + bl[cc * 16 + i]);
+        for (int q = 0; q < 4; ++q) {
+          const float4 bq = reinterpret_cast<const float4*>(bl + cc * 16)[q];
+          av[4 * q + 0] = act_fn(act, v[4 * q + 0] + bq.x);
+          av[4 * q + 1] = act_fn(act, v[4 * q + 1] + bq.y);
+          av[4 * q + 2] = act_fn(act, v[4 * q + 2] + bq.z);
+          av[4 * q + 3] = act_fn(act, v[4 * q + 3] + bq.w);
+        }
         if (!last) {
           st_shared_v4(region_s + kmajor_offset(row, cc * 16, kTileM), pack_half2(av[0], av[1]),
                        pack_half2(av[2], av[3]), pack_half2(av[4], av[5]), pack_half2(av[6], av[7]));
@@ -403,10 +411,16 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
 #pragma unroll
           for (int k = 0; k < kMaxOut; ++k) {
             if (k < out_dim) {
-              const float* hw = s_headw + k * width + cc * 16;
+              const float4* hw = reinterpret_cast<const float4*>(s_headw + k * width + cc * 16);
               float s = y[k];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) s = fmaf(av[i], hw[i], s);
+              for (int q = 0; q < 4; ++q) {
+                const float4 w4 = hw[q];
+                s = fmaf(av[4 * q], w4.x, s);
+                s = fmaf(av[4 * q + 1], w4.y, s);
+                s = fmaf(av[4 * q + 2], w4.z, s);
+                s = fmaf(av[4 * q + 3], w4.w, s);
+              }
               y[k] = s;
             }
           }

@@ -58,6 +58,8 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
     if (d.m < 1 || d.depth < 1 || d.width < 1 || (d.out_dim != 1 && d.out_dim != 3))
       return fail(NVDB_EINVAL, "net %d: bad dims m=%d depth=%d width=%d out=%d", i, d.m, d.depth, d.width,
                   d.out_dim);
+    if (i > 0 && d.activation != nets[0].activation)
+      return fail(NVDB_EUNSUPPORTED, "all nets of a netset must share one hidden activation");
     if (d.head == NVDB_HEAD_LOGITS && d.out_dim != 3)
       return fail(NVDB_EUNSUPPORTED, "net %d: logits head must be 3 wide", i);
     const int W = round_up_i(d.width, 16);
@@ -164,6 +166,7 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
   ns->halo = halo;
   ns->max_wimg = max_wimg;
   ns->max_width = max_width;
+  ns->act = nnets ? nets[0].activation : NVDB_ACT_SINE;
   auto cleanup = [&](int code) {
     nvdb_netset_destroy(ns);
     return code;
@@ -215,7 +218,8 @@ int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int 
   const uint32_t smem = std::max<uint32_t>(plan.total, 120 * 1024);  // one CTA per SM (owns all TMEM)
   static long long smem_limit = -1;
   if (smem_limit < 0) {
-    smem_limit = enable_max_smem(mlp_eval_kernel);
+    smem_limit = std::min(std::min(enable_max_smem(mlp_eval_kernel<ACT_RELU>), enable_max_smem(mlp_eval_kernel<ACT_TANH>)),
+                          enable_max_smem(mlp_eval_kernel<ACT_SINE>));
     if (smem_limit < 0) return fail(NVDB_ECUDA, "cannot raise shared memory limit of mlp_eval_kernel");
   }
   if ((long long)plan.total > smem_limit)
@@ -231,7 +235,11 @@ int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int 
   a.small_off = plan.small_off;
   a.bar_off = plan.bar_off;
   if (grid <= 0) return NVDB_OK;
-  mlp_eval_kernel<<<grid, kCtaThreads, smem, st>>>(a);
+  switch (ns->act) {
+    case ACT_RELU: mlp_eval_kernel<ACT_RELU><<<grid, kCtaThreads, smem, st>>>(a); break;
+    case ACT_TANH: mlp_eval_kernel<ACT_TANH><<<grid, kCtaThreads, smem, st>>>(a); break;
+    default: mlp_eval_kernel<ACT_SINE><<<grid, kCtaThreads, smem, st>>>(a); break;
+  }
   NVDB_CHECK_LAUNCH();
   return NVDB_OK;
 }

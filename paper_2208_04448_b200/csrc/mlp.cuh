@@ -179,9 +179,13 @@ __device__ __forceinline__ void st_shared_b32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// ACT: the hidden activation of every net in the launch (a container's nets
+// share one TrainConfig activation), so the epilogue has no per-element branch
+template <int ACT>
 __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a);
 
 #ifdef NVDB_MLP_KERNEL_TU  // defined in exactly one translation unit (eval.cu)
+template <int ACT>
 __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
@@ -278,7 +282,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
     if (tile.count <= 0) continue;
 
     const int width = s_net.width, depth = s_net.depth, k0 = s_net.k0, out_dim = s_net.out_dim;
-    const int act = s_net.act;
+    constexpr int act = ACT;
     const int mp = k0 >> 1;
 
     // ------------------------------------------------ point set-up (row)
@@ -304,16 +308,16 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
         x0 = s[0]; x1 = s[1]; x2 = s[2];
       }
     }
-    // lattice thread role: voxel z index lk, feature pair lf of each chunk
-    const int lk = gt & 7, lf = gt >> 3;
-    float lx[2], ly0, lz;
+    // lattice thread role: voxel z index lk, group of 4 feature pairs lpg, half of
+    // the y rows ljh (y = 4*ljh .. 4*ljh+3), x row lii of the tile
+    const int lk = gt & 7, lpg = (gt >> 3) & 7, ljh = (gt >> 6) & 1, lii = gt >> 7;
+    float lx = 0.f, ly = 0.f, lz = 0.f;
     if (lattice) {
       const int* o = static_cast<const int*>(a.src) + 3 * (tile.first >> 9);
       const int i0 = (int)((tile.first & 511) >> 6);
       const double is = s_exp.inv_scale;
-      lx[0] = __double2float_rn((o[0] + i0 + 0.5 - s_exp.norm_origin[0]) * is);
-      lx[1] = __double2float_rn((o[0] + i0 + 1.5 - s_exp.norm_origin[0]) * is);
-      ly0 = __double2float_rn((o[1] + 0.5 - s_exp.norm_origin[1]) * is);
+      lx = __double2float_rn((o[0] + i0 + lii + 0.5 - s_exp.norm_origin[0]) * is);
+      ly = __double2float_rn((o[1] + 4 * ljh + 0.5 - s_exp.norm_origin[1]) * is);
       lz = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) * is);
     }
 
@@ -326,22 +330,30 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
       if (b == 1 && pend1) { mbar_wait(bar_c0 + 1, (nc1 - 1u) & 1u); pend1 = false; }
       const uint32_t buf = region_s + b * kChunkBytes;
       if (lattice) {
-        const int f = ch * (kChunkK / 2) + lf;
-        const float bx = s_b2pi[f], by = s_b2pi[mp + f], bz = s_b2pi[2 * mp + f];
-        const float cb = s_lat[2 * f], sb = s_lat[2 * f + 1];
-        // the two x-rows of the tile are independent rotation chains: interleave them
-        float sa, ca, sbn, cbn;
-        __sincosf(fmaf(lz, bz, fmaf(ly0, by, lx[0] * bx)), &sa, &ca);
-        __sincosf(fmaf(lz, bz, fmaf(ly0, by, lx[1] * bx)), &sbn, &cbn);
+        // 4 pairs x 4 y-rows per thread: sincos at the first row, one rotation
+        // by exp(i beta) for the second, then the Chebyshev recurrence
+        // u_{j+1} = 2 cos(beta) u_j - u_{j-1} (one FFMA per cos / sin)
+        float cs[4][4], sn[4][4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          st_shared_b32(buf + kmajor_offset(j * 8 + lk, 2 * lf, kTileM), pack_half2(ca, sa));
-          st_shared_b32(buf + kmajor_offset(64 + j * 8 + lk, 2 * lf, kTileM), pack_half2(cbn, sbn));
-          const float ca2 = fmaf(ca, cb, -sa * sb), cb2 = fmaf(cbn, cb, -sbn * sb);
-          sa = fmaf(ca, sb, sa * cb);
-          sbn = fmaf(cbn, sb, sbn * cb);
-          ca = ca2;
-          cbn = cb2;
+        for (int q = 0; q < 4; ++q) {
+          const int f = ch * (kChunkK / 2) + lpg * 4 + q;
+          const float th = fmaf(lz, s_b2pi[2 * mp + f], fmaf(ly, s_b2pi[mp + f], lx * s_b2pi[f]));
+          const float cb = s_lat[2 * f], sb = s_lat[2 * f + 1];
+          __sincosf(th, &sn[q][0], &cs[q][0]);
+          cs[q][1] = fmaf(cs[q][0], cb, -sn[q][0] * sb);
+          sn[q][1] = fmaf(cs[q][0], sb, sn[q][0] * cb);
+          const float c2 = 2.0f * cb;
+          cs[q][2] = fmaf(c2, cs[q][1], -cs[q][0]);
+          sn[q][2] = fmaf(c2, sn[q][1], -sn[q][0]);
+          cs[q][3] = fmaf(c2, cs[q][2], -cs[q][1]);
+          sn[q][3] = fmaf(c2, sn[q][2], -sn[q][1]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = lii * 64 + (4 * ljh + j) * 8 + lk;
+          st_shared_v4(buf + kmajor_offset(r, lpg * 8, kTileM), pack_half2(cs[0][j], sn[0][j]),
+                       pack_half2(cs[1][j], sn[1][j]), pack_half2(cs[2][j], sn[2][j]),
+                       pack_half2(cs[3][j], sn[3][j]));
         }
       } else {
 #pragma unroll

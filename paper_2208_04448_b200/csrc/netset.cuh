@@ -19,6 +19,7 @@ struct nvdb_netset {
   std::vector<int32_t> tagnet;            // [nexperts][4]
   uint32_t max_wimg = 0;
   int max_width = 16;
+  int act = 2;  // shared hidden activation of every net
 };
 
 namespace nvdb {

@@ -237,6 +237,8 @@ typedef struct {
   const float* c2;          /* HOST (max_epochs) float32(1 - 0.999^(e+1))       */
   const uint64_t* seed_words; /* HOST (max_epochs,4) SeedSequence((seed,0,e)).generate_state(4,u64) */
   double target_loss;       /* early stop when the pre-update epoch loss < target */
+  int32_t shard_rank;       /* data parallel: this rank's contiguous share of the batch tiles */
+  int32_t shard_count;      /* ranks (<= 1: the whole batch)                                */
 } nvdb_train_desc;
 
 NVDB_API int nvdb_trainer_create(const nvdb_train_desc* desc, nvdb_trainer** out);
@@ -244,6 +246,12 @@ NVDB_API int nvdb_trainer_destroy(nvdb_trainer* tr);
 /* enqueue `epochs` epochs (sampler -> fwd/dgrad -> wgrad -> Adam); epochs
  * after the early stop are no-ops on the device */
 NVDB_API int nvdb_trainer_run(nvdb_trainer* tr, int32_t epochs, void* stream);
+/* one epoch split for data parallelism: phase 1 = sampler, fwd/dgrad, wgrad,
+ * partial reduction into the gradient buffer; phase 2 = Adam, early stop,
+ * epoch advance.  Between them the caller all-reduces (sum) the nparams
+ * floats at *grad and the double at *loss across ranks (NCCL). */
+NVDB_API int nvdb_trainer_phase(nvdb_trainer* tr, int32_t phase, void* stream);
+NVDB_API int nvdb_trainer_buffers(nvdb_trainer* tr, float** grad, int64_t* nparams, double** loss);
 /* synchronous: epochs run so far, stop flag, per-epoch losses (HOST out) */
 NVDB_API int nvdb_trainer_status(const nvdb_trainer* tr, int32_t* epochs_done, int32_t* stopped,
                                  double* losses, int32_t nlosses);

@@ -31,8 +31,9 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
-  while (!mbar_try_wait(a, parity)) {
-  }
+  // back off between probes so waiting warps leave the issue slots to the
+  // warps that have work (the other tile group's epilogue)
+  while (!mbar_try_wait(a, parity)) __nanosleep(64);
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)

@@ -161,6 +161,7 @@ struct FbArgs {
   const float* ys;            // (n,) targets / labels as float
   const int64_t* idx;         // batch -> point (nullable: identity)
   int64_t batch;
+  int64_t tile_begin, tile_end;  // this rank's share of the batch tiles
   int32_t loss_kind;          // 0 mse, 1 ce, 2 bce
   int32_t nwg;
   uint16_t* act_img;          // [depth][ntiles][128*W] fp16 tile images
@@ -234,8 +235,8 @@ __global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
   const uint32_t idesc_bt = idesc_f16(kTileM, width, 0, 1);  // B = W'^T read MN-major
 
   const int64_t ntiles = (a.batch + kTileM - 1) / kTileM;
-  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const int64_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  const int64_t per = (a.tile_end - a.tile_begin + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = a.tile_begin + blockIdx.x * per, t1 = min(a.tile_end, t0 + per);
   double loss_acc = 0.0;
   const size_t tile_elems = (size_t)kTileM * width;
 
@@ -471,6 +472,7 @@ struct WgArgs {
   const float* xs;
   const int64_t* idx;
   int64_t batch;
+  int64_t tile_begin, tile_end;
   const uint16_t* act_img;
   const uint16_t* dz_img;
   const uint16_t* dlt_img;
@@ -521,8 +523,8 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
   const int64_t ntiles = (a.batch + kTileM - 1) / kTileM;
-  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const int64_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  const int64_t per = (a.tile_end - a.tile_begin + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = a.tile_begin + blockIdx.x * per, t1 = min(a.tile_end, t0 + per);
   const size_t tbytes = (size_t)kTileM * W * 2;
   const uint32_t sfe = smem_addr(s_feat), son = smem_addr(s_ones);
   const int nmt = (k0 + 127) / 128;  // M tiles of 128 features
@@ -708,9 +710,34 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
 }
 
 // ------------------------------------------------------------------ reduce + Adam
+// fixed-order, 4-way interleaved sum of the per-CTA partials -> grad[P];
+// per-CTA loss partials -> lossbuf[0] (data-parallel ranks all-reduce both)
+__global__ void k_train_reduce(const float* __restrict__ partial, int32_t ncta, int64_t P, float* __restrict__ grad,
+                               const double* loss_part, int32_t nloss, double* lossbuf, const int32_t* stopped) {
+  if (*stopped) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P; q += stride) {
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+    int c = 0;
+    for (; c + 4 <= ncta; c += 4) {
+      g0 += partial[(size_t)c * P + q];
+      g1 += partial[(size_t)(c + 1) * P + q];
+      g2 += partial[(size_t)(c + 2) * P + q];
+      g3 += partial[(size_t)(c + 3) * P + q];
+    }
+    for (; c < ncta; ++c) g0 += partial[(size_t)c * P + q];
+    grad[q] = (g0 + g1) + (g2 + g3);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double sl = 0.0;
+    for (int c = 0; c < nloss; ++c) sl += loss_part[c];
+    lossbuf[0] = sl;
+  }
+}
+
 struct AdamArgs {
-  const float* partial;
-  int32_t ncta;
+  const float* grad;
+  const double* lossbuf;
   int64_t P;
   float* wmaster;      // [P] current params (serialized layout)
   float* mom;          // [P]
@@ -724,8 +751,6 @@ struct AdamArgs {
   const float* lr;     // [max_epochs]
   const float* c1;     // [max_epochs] float32(1 - b1^t)
   const float* c2;
-  const double* loss_part;
-  int32_t nloss;
   double loss_den;
   double target;
   int32_t* epoch;
@@ -740,18 +765,7 @@ __global__ void k_train_adam(AdamArgs a) {
   const float lr = a.lr[e], c1 = a.c1[e], c2 = a.c2[e];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.P; q += stride) {
-    // fixed-order, 4-way interleaved sum of the per-CTA partials
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
-    int c = 0;
-    for (; c + 4 <= a.ncta; c += 4) {
-      g0 += a.partial[(size_t)c * a.P + q];
-      g1 += a.partial[(size_t)(c + 1) * a.P + q];
-      g2 += a.partial[(size_t)(c + 2) * a.P + q];
-      g3 += a.partial[(size_t)(c + 3) * a.P + q];
-    }
-    for (; c < a.ncta; ++c) g0 += a.partial[(size_t)c * a.P + q];
-    float g = (g0 + g1) + (g2 + g3);
-    g *= a.gscale[q];
+    const float g = a.grad[q] * a.gscale[q];
     // numpy float32 arithmetic with weak python scalars (neural.py:508-523)
     float m = a.mom[q] * 0.9f;
     m = m + 0.1f * g;
@@ -769,9 +783,7 @@ __global__ void k_train_adam(AdamArgs a) {
     if (a.f32_dst[q] >= 0) a.f32_block[a.f32_dst[q]] = w * a.img_fold[q];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double s = 0.0;
-    for (int c = 0; c < a.nloss; ++c) s += a.loss_part[c];
-    const double loss = s / a.loss_den;
+    const double loss = a.lossbuf[0] / a.loss_den;
     a.loss_hist[e] = loss;
     if (loss < a.target) {
       *a.stopped = 1;
@@ -810,6 +822,9 @@ struct nvdb_trainer {
   int32_t* f32_dst = nullptr;
   float* partial = nullptr;
   double* loss_part = nullptr;
+  float* grad = nullptr;       // [P] summed (then all-reduced) gradient
+  double* lossbuf = nullptr;   // [1] summed (then all-reduced) batch loss
+  int64_t tile_begin = 0, tile_end = 0;
   uint16_t* act_img = nullptr;
   uint16_t* dz_img = nullptr;
   uint16_t* dlt_img = nullptr;
@@ -988,13 +1003,21 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   t->plan = plan_smem((uint32_t)wimg_bytes, W);
   // ---- per-step buffers
   const size_t tile_elems = (size_t)kTileM * W;
-  t->fb_grid = (int)std::min<int64_t>(num_sms(), (t->ntiles + t->nwg - 1) / t->nwg);
-  t->wg_grid = (int)std::min<int64_t>(num_sms(), t->ntiles);
+  {  // data-parallel share: contiguous tile range of this rank (whole batch when unsharded)
+    const int64_t R = std::max(d->shard_count, 1), r = std::min<int64_t>(std::max(d->shard_rank, 0), R - 1);
+    t->tile_begin = t->ntiles * r / R;
+    t->tile_end = t->ntiles * (r + 1) / R;
+  }
+  const int64_t mine = std::max<int64_t>(t->tile_end - t->tile_begin, 1);
+  t->fb_grid = (int)std::min<int64_t>(num_sms(), (mine + t->nwg - 1) / t->nwg);
+  t->wg_grid = (int)std::min<int64_t>(num_sms(), mine);
   chk(dalloc(t, &t->act_img, (size_t)depth * t->ntiles * tile_elems));
   chk(dalloc(t, &t->dz_img, (size_t)depth * t->ntiles * tile_elems));
   chk(dalloc(t, &t->dlt_img, (size_t)t->ntiles * kTileM * 16));
   chk(dalloc(t, &t->partial, (size_t)t->wg_grid * P));
   chk(dalloc(t, &t->loss_part, (size_t)t->fb_grid));
+  chk(dalloc(t, &t->grad, (size_t)P));
+  chk(dalloc(t, &t->lossbuf, 1));
   chk(dalloc(t, &t->ctl, 4));
   chk(dalloc(t, &t->loss_hist, d->max_epochs));
   chk(dalloc(t, &t->lr, d->max_epochs));
@@ -1030,13 +1053,15 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   return NVDB_OK;
 }
 
-extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
-  if (!t || epochs < 0) return fail(NVDB_EINVAL, "nvdb_trainer_run: bad args");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+namespace {
+// phase 1: sampler -> fwd/dgrad -> wgrad -> partial reduction (grad, loss);
+// phase 2: Adam + early stop + epoch advance.  A data-parallel caller
+// all-reduces grad[P] and the loss between the two phases.
+int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st) {
   const nvdb_train_desc& d = t->d;
-  for (int e = 0; e < epochs; ++e) {
-    int32_t* ep = t->ctl;
-    int32_t* stopped = t->ctl + 1;
+  int32_t* ep = t->ctl;
+  int32_t* stopped = t->ctl + 1;
+  if (phase == 1) {
     if (d.sampled) {
       SampCtl c{ep, stopped, t->words, (unsigned long long)d.n, t->batch, t->nraw, t->sflag, t->sval, t->spos, t->idx};
       if (d.n == 1) {
@@ -1060,6 +1085,8 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
     fa.ys = d.targets;
     fa.idx = d.sampled ? t->idx : nullptr;
     fa.batch = t->batch;
+    fa.tile_begin = t->tile_begin;
+    fa.tile_end = t->tile_end;
     fa.loss_kind = d.loss_kind;
     fa.nwg = t->nwg;
     fa.act_img = t->act_img;
@@ -1081,6 +1108,8 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
     wa.xs = d.inputs;
     wa.idx = fa.idx;
     wa.batch = t->batch;
+    wa.tile_begin = t->tile_begin;
+    wa.tile_end = t->tile_end;
     wa.act_img = t->act_img;
     wa.dz_img = t->dz_img;
     wa.dlt_img = t->dlt_img;
@@ -1095,9 +1124,14 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
     wa.col_head = wa.col_h + (t->depth - 1) * t->W;
     k_train_wgrad<<<t->wg_grid, 256, kWgSmem, st>>>(wa);
     NVDB_CHECK_LAUNCH();
+    k_train_reduce<<<(int)std::min<int64_t>((t->P + 255) / 256, num_sms() * 8), 256, 0, st>>>(
+        t->partial, t->wg_grid, t->P, t->grad, t->loss_part, t->fb_grid, t->lossbuf, stopped);
+    NVDB_CHECK_LAUNCH();
+    return NVDB_OK;
+  }
     AdamArgs aa{};
-    aa.partial = t->partial;
-    aa.ncta = t->wg_grid;
+    aa.grad = t->grad;
+    aa.lossbuf = t->lossbuf;
     aa.P = t->P;
     aa.wmaster = t->wmaster;
     aa.mom = t->mom;
@@ -1111,8 +1145,6 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
     aa.lr = t->lr;
     aa.c1 = t->c1;
     aa.c2 = t->c2;
-    aa.loss_part = t->loss_part;
-    aa.nloss = t->fb_grid;
     aa.loss_den = (double)t->batch;
     aa.target = d.target_loss;
     aa.epoch = ep;
@@ -1123,7 +1155,31 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
     NVDB_CHECK_LAUNCH();
     k_train_advance<<<1, 1, 0, st>>>(ep, stopped, t->ctl + 2);
     NVDB_CHECK_LAUNCH();
+  return NVDB_OK;
+}
+}  // namespace
+
+extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
+  if (!t || epochs < 0) return fail(NVDB_EINVAL, "nvdb_trainer_run: bad args");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int e = 0; e < epochs; ++e) {
+    int rc = enqueue_phase(t, 1, st);
+    if (!rc) rc = enqueue_phase(t, 2, st);
+    if (rc) return rc;
   }
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_trainer_phase(nvdb_trainer* t, int32_t phase, void* stream) {
+  if (!t || (phase != 1 && phase != 2)) return fail(NVDB_EINVAL, "nvdb_trainer_phase: bad args");
+  return enqueue_phase(t, phase, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int nvdb_trainer_buffers(nvdb_trainer* t, float** grad, int64_t* nparams, double** loss) {
+  if (!t || !grad || !nparams || !loss) return fail(NVDB_EINVAL, "nvdb_trainer_buffers: null argument");
+  *grad = t->grad;
+  *nparams = t->P;
+  *loss = t->lossbuf;
   return NVDB_OK;
 }
 

@@ -30,7 +30,8 @@ EXPORTED = [
     "nvdb_select_workspace_bytes", "nvdb_select_u8", "nvdb_l1_apply", "nvdb_scatter_f32",
     "nvdb_leaf_list", "nvdb_l0_apply", "nvdb_leaf_finalize", "nvdb_pack_eq", "nvdb_neural_rows",
     "nvdb_query_finalize", "nvdb_trainer_create", "nvdb_trainer_destroy", "nvdb_trainer_run",
-    "nvdb_trainer_status", "nvdb_trainer_weights", "nvdb_sample_indices",
+    "nvdb_trainer_status", "nvdb_trainer_weights", "nvdb_sample_indices", "nvdb_trainer_phase",
+    "nvdb_trainer_buffers",
 ]
 
 SRC_NORM_F32, SRC_CENTER_F64, SRC_COORD_I32, SRC_LEAF_VOX, SRC_L1_SLOT = range(5)
@@ -74,7 +75,7 @@ class TrainDesc(C.Structure):
                 ("targets", C.c_void_p), ("batch", C.c_int32), ("sampled", C.c_int32),
                 ("sample_interval", C.c_int32), ("max_epochs", C.c_int32), ("lr", C.c_void_p),
                 ("c1", C.c_void_p), ("c2", C.c_void_p), ("seed_words", C.c_void_p),
-                ("target_loss", C.c_double)]
+                ("target_loss", C.c_double), ("shard_rank", C.c_int32), ("shard_count", C.c_int32)]
 
 
 _lib: Optional[C.CDLL] = None
@@ -115,6 +116,8 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_trainer_status": (C.c_int, [vp, C.POINTER(i32), C.POINTER(i32), vp, i32]),
         "nvdb_trainer_weights": (C.c_int, [vp, C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.POINTER(C.c_float))]),
         "nvdb_sample_indices": (C.c_int, [C.c_uint64, i64, vp, vp, vp]),
+        "nvdb_trainer_phase": (C.c_int, [vp, i32, vp]),
+        "nvdb_trainer_buffers": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(C.c_void_p)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

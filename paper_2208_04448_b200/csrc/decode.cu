@@ -70,6 +70,7 @@ __global__ void k_l0_apply(uint8_t* active, const int64_t* patch_slot, const int
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npatch; i += stride) {
     const int32_t leaf = patch_slot[i] >= 0 ? leaf_of_slot[patch_slot[i]] : -1;
+    if (leaf == -2) continue;  // a leaf owned by another decode shard
     if (leaf < 0) {
       atomicExch(err, 1);  // decoder.py:172-175: patch outside every reconstructed leaf
       continue;

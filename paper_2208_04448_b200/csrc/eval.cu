@@ -508,18 +508,36 @@ __global__ void k_selftest_umma(const uint8_t* a_img, uint32_t a_bytes, const ui
     mbar_init(&bar, 1);
     fence_barrier_init();
   }
-  if (threadIdx.x < 32) tmem_alloc(&tslot, 256);
+  if (threadIdx.x < 32) tmem_alloc(&tslot, 512);
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = tslot;
+  const bool a_tmem = (a_mn == 2);  // A (row-major 128 x K fp16) staged in TMEM columns 256..
+  if (a_tmem) {
+    const int row = threadIdx.x;
+    const uint32_t* arow = reinterpret_cast<const uint32_t*>(sa) + row * (nk * 8);
+    for (int c = 0; c < nk * 8; c += 8) {
+      uint32_t r[8];
+      for (int i = 0; i < 8; ++i) r[i] = arow[c + i];
+      tmem_st8(tm + 256 + c + ((uint32_t)((threadIdx.x >> 5) * 32) << 16), r);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   if (threadIdx.x == 0) {
-    const uint32_t idesc = idesc_f16(128, n, a_mn, b_mn);
+    const uint32_t idesc = idesc_f16(128, n, a_tmem ? 0 : a_mn, b_mn);
     for (int s = 0; s < nk; ++s) {
-      const uint64_t ad = smem_desc(smem_addr(sa) + s * a_step, a_lbo, a_sbo);
       const uint64_t bd = smem_desc(smem_addr(sb) + s * b_step, b_lbo, b_sbo);
-      umma_f16(tm, ad, bd, idesc, s != 0);
+      if (a_tmem) {
+        umma_f16_ts(tm, tm + 256 + s * 8, bd, idesc, s != 0);
+      } else {
+        const uint64_t ad = smem_desc(smem_addr(sa) + s * a_step, a_lbo, a_sbo);
+        umma_f16(tm, ad, bd, idesc, s != 0);
+      }
     }
     umma_commit(&bar);
   }
@@ -535,7 +553,7 @@ __global__ void k_selftest_umma(const uint8_t* a_img, uint32_t a_bytes, const ui
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x < 32) tmem_dealloc(tm, 256);
+  if (threadIdx.x < 32) tmem_dealloc(tm, 512);
 }
 
 }  // namespace

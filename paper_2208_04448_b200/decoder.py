@@ -225,8 +225,14 @@ class DeviceModel:
 
     # -- decode --------------------------------------------------------------------
 
-    def decode(self, materialize_values: bool = True) -> "DeviceDecode":
-        """decoder._reconstruct (decoder.py:101-211) on the device."""
+    def decode(self, materialize_values: bool = True, shard: Optional[Tuple[int, int]] = None) -> "DeviceDecode":
+        """decoder._reconstruct (decoder.py:101-211) on the device.
+
+        ``shard=(rank, world)``: level-1 classification runs on every rank
+        (n1*4096 slots, cheap), then the leaf list is split into ``world``
+        contiguous ranges (:func:`shard_range`) and this rank classifies,
+        regresses and finalizes only its own leaves -- no collective.
+        """
         dev, st = self.dev, _stream(self.dev)
         n1 = self.n1
         nslots = n1 * L1_SIZE
@@ -245,11 +251,25 @@ class DeviceModel:
             check(lib().nvdb_scatter_f32(_ptr(tiles), _ptr(active_tiles), _ptr(tv), active_tiles.numel(), st),
                   "nvdb_scatter_f32")
         child = self.select(cls[:nslots], 0)
-        nl = child.numel()
-        leaf_origins = torch.empty((max(nl, 1), 3), dtype=torch.int32, device=dev)
         leaf_of_slot = torch.empty(max(nslots, 1), dtype=torch.int32, device=dev)
-        check(lib().nvdb_leaf_list(_ptr(child), nl, _ptr(self.d_origins), nslots, _ptr(leaf_origins),
-                                   _ptr(leaf_of_slot), st), "nvdb_leaf_list")
+        if shard is not None:
+            # global slot -> leaf map, then keep this rank's range; other ranks'
+            # leaves are marked -2 (skipped, not an error) in the patch kernels
+            lo, hi = shard_range(child.numel(), *shard)
+            full = torch.empty((max(child.numel(), 1), 3), dtype=torch.int32, device=dev)
+            check(lib().nvdb_leaf_list(_ptr(child), child.numel(), _ptr(self.d_origins), nslots, _ptr(full),
+                                       _ptr(leaf_of_slot), st), "nvdb_leaf_list")
+            loc = leaf_of_slot - lo
+            leaf_of_slot = torch.where(leaf_of_slot < 0, leaf_of_slot,
+                                       torch.where((loc >= 0) & (loc < hi - lo), loc, torch.full_like(loc, -2)))
+            child = child[lo:hi]
+            leaf_origins = full[lo:hi].contiguous() if hi > lo else full[:1]
+            nl = hi - lo
+        else:
+            nl = child.numel()
+            leaf_origins = torch.empty((max(nl, 1), 3), dtype=torch.int32, device=dev)
+            check(lib().nvdb_leaf_list(_ptr(child), nl, _ptr(self.d_origins), nslots, _ptr(leaf_origins),
+                                       _ptr(leaf_of_slot), st), "nvdb_leaf_list")
         act = torch.zeros(max(nl * LEAF_SIZE, 1), dtype=torch.uint8, device=dev)
         self.evaluate("l0", _lib.SRC_LEAF_VOX, leaf_origins, nl * LEAF_SIZE, _lib.OUT_L0ACTIVE, u8=act)
         err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -275,7 +295,7 @@ class DeviceModel:
         if int(err.item()):
             raise SvcodecError("corrupt container: level-0 patch outside every reconstructed leaf")
         return DeviceDecode(self, cls[:nslots], tiles[:nslots], child, leaf_origins[:nl], act[:nl * LEAF_SIZE],
-                            values[:nl * LEAF_SIZE], words[:nl * 8], patched[:nl * LEAF_SIZE], evals)
+                            values[:nl * LEAF_SIZE], words[:nl * 8], patched[:nl * LEAF_SIZE], evals, shard)
 
 
 @dataclass
@@ -292,6 +312,7 @@ class DeviceDecode:
     active_words: torch.Tensor  # (nl*8,) packed masks (int64 view of u64)
     patched: torch.Tensor       # (nl*512,) u8
     regressor_evaluations: int
+    shard: Optional[Tuple[int, int]] = None  # (rank, world) when only a leaf range was decoded
 
     @property
     def leaf_count(self) -> int:
@@ -299,6 +320,8 @@ class DeviceDecode:
 
     def to_grid(self) -> DenseLeafGrid:
         """Host DenseLeafGrid in canonical (root, idx2, idx1) order."""
+        if self.shard is not None and self.shard[1] > 1:
+            raise ValueError("a sharded decode holds a leaf range, not a grid; gather the shards first")
         m = self.model
         c = m.c
         meta = c.grid_meta
@@ -341,6 +364,14 @@ class DeviceDecode:
     def tree(self) -> DeviceTree:
         """Device tree over this decode (hybrid topology for random access)."""
         return DeviceTree.from_decode(self)
+
+
+def shard_range(nleaves: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous leaf range of one decode shard (split the
+    node-ordered leaf list into equal ranges; no collective)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad shard {rank}/{world}")
+    return nleaves * rank // world, nleaves * (rank + 1) // world
 
 
 def _as_model(c, device=None) -> DeviceModel:

@@ -258,15 +258,39 @@ def net_spec(tag: str, cfg) -> Optional[NetSpec]:
     raise ValueError(tag)
 
 
+class _DeviceArray:
+    """Zero-copy torch view of library-owned device memory (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def shard_of(ntiles: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous tile range of one data-parallel rank (same split as train.cu)."""
+    return ntiles * rank // world, ntiles * (rank + 1) // world
+
+
 class DeviceTrainer:
-    """One network's device-resident training loop (nvdb_trainer_*)."""
+    """One network's device-resident training loop (nvdb_trainer_*).
+
+    With a ``torch.distributed`` process group of size G > 1, every rank draws
+    the same batch (same sampler stream), processes its contiguous share of
+    the batch tiles, and the fp32 gradient sum plus the loss sum are
+    all-reduced (NCCL over NVLink) between the gradient and the Adam phase of
+    each epoch; all ranks then apply the identical update.
+    """
 
     CHUNK = 64  # epochs enqueued between host checks of the stop flag
 
     def __init__(self, params: MlpParams, ff: FourierFeatures, inputs: np.ndarray, targets: np.ndarray,
                  loss_kind: str, cfg, lr0: float, seed_draw: int, sampled: bool, target_loss: float,
-                 device=None):
+                 device=None, group=None):
         self.dev = _dev(device)
+        self.group = group
+        import torch.distributed as dist
+        self.world = dist.get_world_size(group) if group is not None else 1
+        self.rank = dist.get_rank(group) if group is not None else 0
         self.params, self.ff = params, ff
         n = inputs.shape[0]
         self.n = n
@@ -293,12 +317,29 @@ class DeviceTrainer:
                       sample_interval=int(cfg.sample_interval), max_epochs=E,
                       lr=self.lr.ctypes.data_as(C.c_void_p), c1=self.c1.ctypes.data_as(C.c_void_p),
                       c2=self.c2.ctypes.data_as(C.c_void_p), seed_words=self.words.ctypes.data_as(C.c_void_p),
-                      target_loss=float(target_loss))
+                      target_loss=float(target_loss), shard_rank=self.rank, shard_count=self.world)
         h = C.c_void_p()
         torch.cuda.synchronize(self.dev)
         check(lib().nvdb_trainer_create(C.byref(d), C.byref(h)), "nvdb_trainer_create")
         self.handle = h
         self.epochs_enqueued = 0
+        if self.world > 1:
+            g, npar, lo = C.c_void_p(), C.c_int64(), C.c_void_p()
+            check(lib().nvdb_trainer_buffers(self.handle, C.byref(g), C.byref(npar), C.byref(lo)),
+                  "nvdb_trainer_buffers")
+            self.grad = torch.as_tensor(_DeviceArray(g.value, npar.value, "<f4"), device=self.dev)
+            self.loss = torch.as_tensor(_DeviceArray(lo.value, 1, "<f8"), device=self.dev)
+
+    def _enqueue(self, k: int, st) -> None:
+        if self.world == 1:
+            check(lib().nvdb_trainer_run(self.handle, k, st), "nvdb_trainer_run")
+            return
+        import torch.distributed as dist
+        for _ in range(k):
+            check(lib().nvdb_trainer_phase(self.handle, 1, st), "nvdb_trainer_phase")
+            dist.all_reduce(self.grad, group=self.group)
+            dist.all_reduce(self.loss, group=self.group)
+            check(lib().nvdb_trainer_phase(self.handle, 2, st), "nvdb_trainer_phase")
 
     def run(self, epochs: Optional[int] = None) -> Tuple[float, int]:
         """Train until the early stop or max_epochs; returns (final loss, epochs)."""
@@ -306,7 +347,7 @@ class DeviceTrainer:
         st = torch.cuda.current_stream(self.dev).cuda_stream
         while self.epochs_enqueued < limit:
             k = min(self.CHUNK, limit - self.epochs_enqueued)
-            check(lib().nvdb_trainer_run(self.handle, k, st), "nvdb_trainer_run")
+            self._enqueue(k, st)
             self.epochs_enqueued += k
             done, stopped = self.status()[:2]
             if stopped:

@@ -85,10 +85,15 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
     pieces[i].b2pi = take(sizeof(float) * 3 * (k0 / 2));
     pieces[i].lat = take(sizeof(float) * k0);
   }
-  SmemPlan plan = plan_smem(max_wimg, max_width);
-  if (plan.total > kMaxDynSmem)
-    return fail(NVDB_EUNSUPPORTED, "nets need %u B of shared memory (> %u); weight streaming not built", plan.total,
-                kMaxDynSmem);
+  int max_depth = 1, max_k0 = 64;
+  for (int i = 0; i < nnets; ++i) {
+    max_depth = std::max(max_depth, hnets[i].depth);
+    max_k0 = std::max(max_k0, hnets[i].k0);
+  }
+  const EvalPlan plan = plan_eval(max_wimg, max_width, max_depth, max_k0, kMaxDynSmem);
+  if (!plan.ok)
+    return fail(NVDB_EUNSUPPORTED, "nets need %u B of shared memory / %d-wide TMEM accumulators; "
+                "weight streaming not built", plan.total, max_width);
   std::vector<uint8_t> blob(std::max<size_t>(total, 256), 0);
   for (int i = 0; i < nnets; ++i) {
     const nvdb_net_desc& d = nets[i];
@@ -166,6 +171,8 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
   ns->halo = halo;
   ns->max_wimg = max_wimg;
   ns->max_width = max_width;
+  ns->max_depth = max_depth;
+  ns->max_k0 = max_k0;
   ns->act = nnets ? nets[0].activation : NVDB_ACT_SINE;
   auto cleanup = [&](int code) {
     nvdb_netset_destroy(ns);
@@ -213,7 +220,7 @@ extern "C" int nvdb_netset_destroy(nvdb_netset* ns) {
 namespace nvdb {
 
 int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int grid, cudaStream_t st) {
-  const SmemPlan plan = plan_smem(ns->max_wimg, ns->max_width);
+  const EvalPlan plan = plan_eval(ns->max_wimg, ns->max_width, ns->max_depth, ns->max_k0, kMaxDynSmem);
   // at least ~120 KB so only one CTA (which owns all 512 TMEM columns) fits per SM
   const uint32_t smem = std::max<uint32_t>(plan.total, 120 * 1024);  // one CTA per SM (owns all TMEM)
   static long long smem_limit = -1;
@@ -234,6 +241,14 @@ int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int 
   a.region_bytes = plan.region_bytes;
   a.small_off = plan.small_off;
   a.bar_off = plan.bar_off;
+  a.nbuf = plan.nbuf;
+  a.two_d = plan.two_d;
+  a.sm_bias = plan.sm_bias;
+  a.sm_headw = plan.sm_headw;
+  a.sm_headb = plan.sm_headb;
+  a.sm_b2pi = plan.sm_b2pi;
+  a.sm_lat = plan.sm_lat;
+  a.sm_hx = plan.sm_hx;
   if (grid <= 0) return NVDB_OK;
   switch (ns->act) {
     case ACT_RELU: mlp_eval_kernel<ACT_RELU><<<grid, kCtaThreads, smem, st>>>(a); break;

@@ -110,6 +110,9 @@ struct MlpArgs {
   int32_t clip;
   // shared-memory carve-up (bytes, 1024-aligned offsets)
   uint32_t w_off, region_off, region_bytes, small_off, bar_off;
+  int32_t nbuf;   // feature ring buffers per group (2 or 3)
+  int32_t two_d;  // 1: two accumulator regions per group (next tile's layer 0 overlaps)
+  int32_t sm_bias, sm_headw, sm_headb, sm_b2pi, sm_lat, sm_hx;  // float offsets in the small region
 };
 
 // small per-net parameters staged in shared memory:
@@ -185,6 +188,20 @@ template <int ACT>
 __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a);
 
 #ifdef NVDB_MLP_KERNEL_TU  // defined in exactly one translation unit (eval.cu)
+
+// per-tile state of one group (the tile being finished and the one whose
+// features are produced ahead of time)
+struct TileCtx {
+  int64_t first;
+  int32_t count, flags;
+  int64_t id;          // point id of this thread's row (outputs)
+  float x0, x1, x2;    // normalised input of the row (per-point features)
+  double gw;           // gate weight of the row
+  bool valid, lattice;
+  float lx, ly, lz;    // lattice role inputs
+  uint32_t dcol;       // TMEM column of this tile's accumulator
+};
+
 template <int ACT>
 __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -195,25 +212,36 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
   const int quad = gw & 3;               // TMEM lane quadrant (hardware: warp id % 4)
   const int half = gw >> 2;              // which half of the pairs / columns
   const int row = quad * 32 + (gt & 31);  // tile row == TMEM lane
+  const int nb = a.nbuf;                 // feature ring depth
 
   uint8_t* wsm = smem + a.w_off;
   float* small = reinterpret_cast<float*>(smem + a.small_off);
-  float* s_bias = small + kSmallBias;
-  float* s_headw = small + kSmallHeadW;
-  float* s_headb = small + kSmallHeadB;
-  float* s_b2pi = small + kSmallB2pi;
-  float* s_lat = small + kSmallLat;
-  float* s_hx = small + kSmallHx + grp * 128 * 4;
+  float* s_bias = small + a.sm_bias;
+  float* s_headw = small + a.sm_headw;
+  float* s_headb = small + a.sm_headb;
+  float* s_b2pi = small + a.sm_b2pi;
+  float* s_lat = small + a.sm_lat;
+  float* s_hx = small + a.sm_hx + grp * 128 * 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-  // bars[0] = weight load; per group g: [1+3g] chunk buf 0, [2+3g] chunk buf 1, [3+3g] layer
-  // bars[7+2g], bars[8+2g]: chunk buffer "full" (all 256 group threads arrive)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  // bars[0]: weights.  Per group g at 1 + 12 g: [0..2] ring empty, [3..5] ring full
+  // (256 arrivals), [6,7] layer-0 done per D region, [8] hidden layer done,
+  // [9] hidden A operand full (256 arrivals)
+  uint64_t* gb = bars + 1 + 12 * grp;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
   __shared__ NetDev s_net;
   __shared__ ExpertDev s_exp;
 
   if (tid == 0) {
-    for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
-    for (int i = 7; i < 11; ++i) mbar_init(&bars[i], kGroupThreads);
+    mbar_init(&bars[0], 1);
+    for (int g = 0; g < 2; ++g) {
+      uint64_t* b = bars + 1 + 12 * g;
+      for (int i = 0; i < 3; ++i) mbar_init(&b[i], 1);
+      for (int i = 3; i < 6; ++i) mbar_init(&b[i], kGroupThreads);
+      mbar_init(&b[6], 1);
+      mbar_init(&b[7], 1);
+      mbar_init(&b[8], 1);
+      mbar_init(&b[9], kGroupThreads);
+    }
     fence_barrier_init();
   }
   if (tid < 32) tmem_alloc(tmem_slot, 512);
@@ -221,38 +249,166 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  uint64_t* bar_w = &bars[0];
-  uint64_t* bar_c0 = &bars[1 + 3 * grp];
-  uint64_t* bar_layer = &bars[3 + 3 * grp];
-  uint64_t* bar_full = &bars[7 + 2 * grp];
-  uint32_t nc0 = 0, nc1 = 0, nf0 = 0, nf1 = 0, nlayer = 0, wphase = 0;
-  bool pend0 = false, pend1 = false;
-  int loaded = -1;
-
-  const uint32_t tmem_col = tmem_base + (uint32_t)(grp * 256);            // MMA D (lane 0)
-  const uint32_t tmem_d = tmem_col + ((uint32_t)(quad * 32) << 16);       // this warp's lanes
-  const uint32_t region_s = smem_addr(smem + a.region_off + grp * a.region_bytes);
+  const uint32_t tg = tmem_base + (uint32_t)(grp * 256);   // this group's TMEM columns
+  const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+  const uint32_t ring_s = smem_addr(smem + a.region_off + grp * a.region_bytes);
   const uint32_t w_s = smem_addr(wsm);
+
+  // pipeline state (parities as bit sets over the ring buffers)
+  uint32_t pend = 0, epar = 0, fpar = 0;  // ring: pending commit, empty parity, full parity
+  uint32_t l0par = 0, l0pend = 0;         // layer-0 done per D region
+  uint32_t hpar = 0, apar = 0;            // hidden done, hidden-A full
+  uint32_t cchunk = 0;                    // chunks produced by this group
+  uint32_t wphase = 0;
+  int loaded = -1;
 
   const int npairs = a.npairs_dev ? *a.npairs_dev : a.npairs;
   const int per_cta = (npairs + gridDim.x - 1) / gridDim.x;
   const int p0 = blockIdx.x * per_cta;
   const int p1 = min(npairs, p0 + per_cta);
 
+  auto pair_net = [&](int p) { return a.tiles ? a.tiles[2 * p].net : a.implicit_net; };
+  auto tile_at = [&](int p) {
+    Tile t;
+    if (a.tiles) {
+      t = a.tiles[2 * p + grp];
+    } else {
+      const int64_t first = (int64_t)(2 * p + grp) * kTileM;
+      t.net = a.implicit_net;
+      t.first = first;
+      t.flags = TF_FIRST | TF_LAST;
+      t.count = (int32_t)max((int64_t)0, min((int64_t)kTileM, a.n_implicit - first));
+    }
+    return t;
+  };
+
+  // ---- per-tile set-up of the row inputs (decoder centres -> expert input map)
+  auto setup = [&](const Tile& t, uint32_t dcol) {
+    TileCtx c;
+    c.first = t.first;
+    c.count = t.count;
+    c.flags = t.flags;
+    c.dcol = dcol;
+    c.valid = row < t.count;
+    const int64_t pos = t.first + (c.valid ? row : 0);
+    c.id = a.idx ? a.idx[pos] : pos;
+    const int64_t sid = a.gather ? a.gather[c.id] : c.id;
+    c.lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat && t.count == kTileM &&
+                (t.first & (kTileM - 1)) == 0;
+    c.x0 = c.x1 = c.x2 = 0.f;
+    c.gw = 1.0;
+    if (!c.lattice || half == 0) {
+      double cc[3];
+      if (point_centre(a.src_kind, a.src, sid, cc)) {
+        const double is = s_exp.inv_scale;
+        c.x0 = __double2float_rn((cc[0] - s_exp.norm_origin[0]) * is);
+        c.x1 = __double2float_rn((cc[1] - s_exp.norm_origin[1]) * is);
+        c.x2 = __double2float_rn((cc[2] - s_exp.norm_origin[2]) * is);
+        c.gw = gate_weight(s_exp.cell, a.subdomain_size, a.halo, cc);
+      } else {
+        const float* s = static_cast<const float*>(a.src) + 3 * sid;
+        c.x0 = s[0]; c.x1 = s[1]; c.x2 = s[2];
+      }
+    }
+    c.lx = c.ly = c.lz = 0.f;
+    if (c.lattice) {
+      const int lk = gt & 7, ljh = (gt >> 6) & 1, lii = gt >> 7;
+      const int* o = static_cast<const int*>(a.src) + 3 * (t.first >> 9);
+      const int i0 = (int)((t.first & 511) >> 6);
+      const double is = s_exp.inv_scale;
+      c.lx = __double2float_rn((o[0] + i0 + lii + 0.5 - s_exp.norm_origin[0]) * is);
+      c.ly = __double2float_rn((o[1] + 4 * ljh + 0.5 - s_exp.norm_origin[1]) * is);
+      c.lz = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) * is);
+    }
+    return c;
+  };
+
+  // ---- one feature chunk of a tile into the ring, then its layer-0 MMAs
+  auto produce = [&](const TileCtx& c, int ch) {
+    const int width = s_net.width, k0 = s_net.k0, mp = k0 >> 1;
+    const int nch = k0 / kChunkK;
+    const int b = (int)(cchunk % (uint32_t)nb);
+    if ((pend >> b) & 1u) {
+      mbar_wait(gb + b, ((epar >> b) & 1u) ^ 1u);
+      pend &= ~(1u << b);
+    }
+    const uint32_t buf = ring_s + b * kChunkBytes;
+    if (c.lattice) {
+      // 4 pairs x 4 y-rows per thread: sincos at the first row, one rotation
+      // by exp(i beta) for the second, then the Chebyshev recurrence
+      // u_{j+1} = 2 cos(beta) u_j - u_{j-1} (one FFMA per cos / sin)
+      const int lk = gt & 7, lpg = (gt >> 3) & 7, ljh = (gt >> 6) & 1, lii = gt >> 7;
+      float cs[4][4], sn[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int f = ch * (kChunkK / 2) + lpg * 4 + q;
+        const float th = fmaf(c.lz, s_b2pi[2 * mp + f], fmaf(c.ly, s_b2pi[mp + f], c.lx * s_b2pi[f]));
+        const float cb = s_lat[2 * f], sb = s_lat[2 * f + 1];
+        __sincosf(th, &sn[q][0], &cs[q][0]);
+        cs[q][1] = fmaf(cs[q][0], cb, -sn[q][0] * sb);
+        sn[q][1] = fmaf(cs[q][0], sb, sn[q][0] * cb);
+        const float c2 = 2.0f * cb;
+        cs[q][2] = fmaf(c2, cs[q][1], -cs[q][0]);
+        sn[q][2] = fmaf(c2, sn[q][1], -sn[q][0]);
+        cs[q][3] = fmaf(c2, cs[q][2], -cs[q][1]);
+        sn[q][3] = fmaf(c2, sn[q][2], -sn[q][1]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = lii * 64 + (4 * ljh + j) * 8 + lk;
+        st_shared_v4(buf + kmajor_offset(r, lpg * 8, kTileM), pack_half2(cs[0][j], sn[0][j]),
+                     pack_half2(cs[1][j], sn[1][j]), pack_half2(cs[2][j], sn[2][j]), pack_half2(cs[3][j], sn[3][j]));
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t h[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int f = ch * (kChunkK / 2) + half * 16 + q * 4 + j;
+          const float th = fmaf(c.x2, s_b2pi[2 * mp + f], fmaf(c.x1, s_b2pi[mp + f], c.x0 * s_b2pi[f]));
+          float sn, cs;
+          __sincosf(th, &sn, &cs);
+          h[j] = pack_half2(cs, sn);
+        }
+        st_shared_v4(buf + kmajor_offset(row, half * 32 + q * 8, kTileM), h[0], h[1], h[2], h[3]);
+      }
+    }
+    fence_async_smem();
+    mbar_arrive(gb + 3 + b);
+    if (gt == 0) {
+      mbar_wait(gb + 3 + b, (fpar >> b) & 1u);
+      tc_fence_after();
+      const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
+#pragma unroll
+      for (int s = 0; s < kChunkK / 16; ++s) {
+        const uint64_t ad = smem_desc(buf + s * (2 * kTileM * 16), kTileM * 16, 128);
+        const uint32_t wb = w_s + (uint32_t)(((ch * kChunkK + s * 16) >> 3) * (width >> 3) * 128);
+        umma_f16(c.dcol, ad, smem_desc(wb, width * 16, 128), idesc, (ch | s) != 0);
+      }
+      umma_commit(gb + b);
+      if (ch == nch - 1) umma_commit(gb + 6 + ((c.dcol - tg) ? 1 : 0));
+    }
+    fpar ^= 1u << b;
+    epar ^= 1u << b;
+    pend |= 1u << b;
+    if (ch == nch - 1) l0pend |= 1u << ((c.dcol - tg) ? 1 : 0);
+    ++cchunk;
+  };
+
+  TileCtx cur, nxt;
+  bool have_nxt = false;
   for (int p = p0; p < p1; ++p) {
-    const int pair_net = a.tiles ? a.tiles[2 * p].net : a.implicit_net;
-    if (pair_net != loaded) {
-      // ---- switch weights: the whole CTA is idle here (both groups finished
-      // their previous tile, so no MMA still reads the old image)
+    if (pair_net(p) != loaded) {
+      // ---- switch weights: both groups drained (no lookahead across a switch)
       __syncthreads();
       if (tid == 0) {
-        s_net = a.nets[pair_net];
-        s_exp = a.experts[a.nets[pair_net].expert];
-        const NetDev& nd = a.nets[pair_net];
-        mbar_arrive_expect_tx(bar_w, nd.wimg_bytes);
+        s_net = a.nets[pair_net(p)];
+        s_exp = a.experts[a.nets[pair_net(p)].expert];
+        const NetDev& nd = a.nets[pair_net(p)];
+        mbar_arrive_expect_tx(&bars[0], nd.wimg_bytes);
         for (uint32_t off = 0; off < nd.wimg_bytes; off += 32768)
-          bulk_g2s(wsm + off, nd.wimg + off, min(32768u, nd.wimg_bytes - off), bar_w);
+          bulk_g2s(wsm + off, nd.wimg + off, min(32768u, nd.wimg_bytes - off), &bars[0]);
       }
       __syncthreads();
       {
@@ -264,146 +420,58 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
         if (nd.lat)
           for (int i = tid; i < nd.k0; i += kCtaThreads) s_lat[i] = nd.lat[i];
       }
-      mbar_wait(bar_w, wphase);
+      mbar_wait(&bars[0], wphase);
       wphase ^= 1u;
       __syncthreads();
-      loaded = pair_net;
+      loaded = pair_net(p);
     }
-    Tile tile;
-    if (a.tiles) {
-      tile = a.tiles[2 * p + grp];
-    } else {
-      const int64_t first = (int64_t)(2 * p + grp) * kTileM;
-      tile.net = a.implicit_net;
-      tile.first = first;
-      tile.flags = TF_FIRST | TF_LAST;
-      tile.count = (int32_t)max((int64_t)0, min((int64_t)kTileM, a.n_implicit - first));
-    }
+    const Tile tile = tile_at(p);
     if (tile.count <= 0) continue;
-
     const int width = s_net.width, depth = s_net.depth, k0 = s_net.k0, out_dim = s_net.out_dim;
-    constexpr int act = ACT;
-    const int mp = k0 >> 1;
-
-    // ------------------------------------------------ point set-up (row)
-    const bool valid = row < tile.count;
-    const int64_t pos = tile.first + (valid ? row : 0);
-    const int64_t id = a.idx ? a.idx[pos] : pos;
-    const int64_t sid = a.gather ? a.gather[id] : id;
-    // lattice tiles: a full, aligned quarter of one leaf in voxel-id order
-    const bool lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat && tile.count == kTileM &&
-                         (tile.first & (kTileM - 1)) == 0;
-    float x0 = 0.f, x1 = 0.f, x2 = 0.f;
-    double gw = 1.0;
-    if (!lattice || half == 0) {  // inputs for per-point features; gate weight for the output half
-      double c[3];
-      if (point_centre(a.src_kind, a.src, sid, c)) {
-        const double is = s_exp.inv_scale;
-        x0 = __double2float_rn((c[0] - s_exp.norm_origin[0]) * is);
-        x1 = __double2float_rn((c[1] - s_exp.norm_origin[1]) * is);
-        x2 = __double2float_rn((c[2] - s_exp.norm_origin[2]) * is);
-        gw = gate_weight(s_exp.cell, a.subdomain_size, a.halo, c);
-      } else {
-        const float* s = static_cast<const float*>(a.src) + 3 * sid;
-        x0 = s[0]; x1 = s[1]; x2 = s[2];
-      }
-    }
-    // lattice thread role: voxel z index lk, group of 4 feature pairs lpg, half of
-    // the y rows ljh (y = 4*ljh .. 4*ljh+3), x row lii of the tile
-    const int lk = gt & 7, lpg = (gt >> 3) & 7, ljh = (gt >> 6) & 1, lii = gt >> 7;
-    float lx = 0.f, ly = 0.f, lz = 0.f;
-    if (lattice) {
-      const int* o = static_cast<const int*>(a.src) + 3 * (tile.first >> 9);
-      const int i0 = (int)((tile.first & 511) >> 6);
-      const double is = s_exp.inv_scale;
-      lx = __double2float_rn((o[0] + i0 + lii + 0.5 - s_exp.norm_origin[0]) * is);
-      ly = __double2float_rn((o[1] + 4 * ljh + 0.5 - s_exp.norm_origin[1]) * is);
-      lz = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) * is);
-    }
-
-    // ------------------------------------------------ features + layer 0
-    const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
     const int nch = k0 / kChunkK;
-    for (int ch = 0; ch < nch; ++ch) {
-      const int b = ch & 1;
-      if (b == 0 && pend0) { mbar_wait(bar_c0, (nc0 - 1u) & 1u); pend0 = false; }
-      if (b == 1 && pend1) { mbar_wait(bar_c0 + 1, (nc1 - 1u) & 1u); pend1 = false; }
-      const uint32_t buf = region_s + b * kChunkBytes;
-      if (lattice) {
-        // 4 pairs x 4 y-rows per thread: sincos at the first row, one rotation
-        // by exp(i beta) for the second, then the Chebyshev recurrence
-        // u_{j+1} = 2 cos(beta) u_j - u_{j-1} (one FFMA per cos / sin)
-        float cs[4][4], sn[4][4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int f = ch * (kChunkK / 2) + lpg * 4 + q;
-          const float th = fmaf(lz, s_b2pi[2 * mp + f], fmaf(ly, s_b2pi[mp + f], lx * s_b2pi[f]));
-          const float cb = s_lat[2 * f], sb = s_lat[2 * f + 1];
-          __sincosf(th, &sn[q][0], &cs[q][0]);
-          cs[q][1] = fmaf(cs[q][0], cb, -sn[q][0] * sb);
-          sn[q][1] = fmaf(cs[q][0], sb, sn[q][0] * cb);
-          const float c2 = 2.0f * cb;
-          cs[q][2] = fmaf(c2, cs[q][1], -cs[q][0]);
-          sn[q][2] = fmaf(c2, sn[q][1], -sn[q][0]);
-          cs[q][3] = fmaf(c2, cs[q][2], -cs[q][1]);
-          sn[q][3] = fmaf(c2, sn[q][2], -sn[q][1]);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = lii * 64 + (4 * ljh + j) * 8 + lk;
-          st_shared_v4(buf + kmajor_offset(r, lpg * 8, kTileM), pack_half2(cs[0][j], sn[0][j]),
-                       pack_half2(cs[1][j], sn[1][j]), pack_half2(cs[2][j], sn[2][j]),
-                       pack_half2(cs[3][j], sn[3][j]));
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t h[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int f = ch * (kChunkK / 2) + half * 16 + q * 4 + j;
-            const float th = fmaf(x2, s_b2pi[2 * mp + f], fmaf(x1, s_b2pi[mp + f], x0 * s_b2pi[f]));
-            float sn, cs;
-            __sincosf(th, &sn, &cs);
-            h[j] = pack_half2(cs, sn);
-          }
-          st_shared_v4(buf + kmajor_offset(row, half * 32 + q * 8, kTileM), h[0], h[1], h[2], h[3]);
-        }
-      }
-      // producer/consumer hand-off: every thread arrives on the chunk's "full"
-      // barrier and moves on; only the issuing thread waits for all arrivals
-      fence_async_smem();
-      mbar_arrive(bar_full + b);
-      const uint32_t fpar = (b == 0 ? nf0 : nf1) & 1u;
-      if (gt == 0) {
-        mbar_wait(bar_full + b, fpar);
-        tc_fence_after();
-#pragma unroll
-        for (int s = 0; s < kChunkK / 16; ++s) {
-          const uint64_t ad = smem_desc(buf + s * (2 * kTileM * 16), kTileM * 16, 128);
-          const uint32_t wb = w_s + (uint32_t)(((ch * kChunkK + s * 16) >> 3) * (width >> 3) * 128);
-          const uint64_t bd = smem_desc(wb, width * 16, 128);
-          umma_f16(tmem_col, ad, bd, idesc, (ch | s) != 0);
-        }
-        umma_commit(bar_c0 + b);
-        if (ch == nch - 1) umma_commit(bar_layer);
-      }
-      if (b == 0) { nc0++; nf0++; pend0 = true; } else { nc1++; nf1++; pend1 = true; }
+    constexpr int act = ACT;
+    if (!have_nxt) {
+      cur = setup(tile, tg);
+      for (int ch = 0; ch < nch; ++ch) produce(cur, ch);
+    } else {
+      cur = nxt;
     }
-    mbar_wait(bar_layer, nlayer & 1u);
-    nlayer++;
-    pend0 = pend1 = false;
-    tc_fence_after();
-
-    // ------------------------------------------------ hidden epilogues
+    have_nxt = false;
+    // next tile of this group: produce its features while this tile's layers run
+    bool look = false;
+    if (a.two_d && p + 1 < p1 && pair_net(p + 1) == loaded) {
+      const Tile t2 = tile_at(p + 1);
+      if (t2.count > 0) {
+        nxt = setup(t2, cur.dcol == tg ? tg + (uint32_t)width : tg);
+        look = true;
+      }
+    }
+    const int slots = depth;  // chunks of the next tile are spread over `depth` slots
+    int nxt_ch = 0;
+    auto produce_next = [&](int slot) {
+      if (!look) return;
+      const int upto = min(nch, (nch * (slot + 1)) / slots);
+      for (; nxt_ch < upto; ++nxt_ch) produce(nxt, nxt_ch);
+    };
+    produce_next(0);
+    // ---- layer 0 done for this tile
+    {
+      const int r = (cur.dcol - tg) ? 1 : 0;
+      mbar_wait(gb + 6 + r, (l0par >> r) & 1u);
+      l0par ^= 1u << r;
+      l0pend &= ~(1u << r);
+      tc_fence_after();
+    }
+    // hidden A operand (width/2 columns) after the one or two accumulator regions
+    const uint32_t acol = tg + (a.two_d ? 2u : 1u) * (uint32_t)width;
     float y[kMaxOut] = {0.f, 0.f, 0.f};
-    uint32_t woff = (uint32_t)(width * k0 * 2);  // byte offset of W1 in the image
+    uint32_t woff = (uint32_t)(width * k0 * 2);
     for (int l = 0; l < depth; ++l) {
       const bool last = (l == depth - 1);
       const float* bl = s_bias + l * width;
       for (int cc = half; cc < width / 16; cc += 2) {
         float v[16];
-        tmem_ld16(tmem_d + cc * 16, v);
+        tmem_ld16(cur.dcol + lane_off + cc * 16, v);
         tmem_ld_wait();
         float av[16];
 #pragma unroll
@@ -415,10 +483,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
           av[4 * q + 3] = act_fn(act, v[4 * q + 3] + bq.w);
         }
         if (!last) {
-          st_shared_v4(region_s + kmajor_offset(row, cc * 16, kTileM), pack_half2(av[0], av[1]),
-                       pack_half2(av[2], av[3]), pack_half2(av[4], av[5]), pack_half2(av[6], av[7]));
-          st_shared_v4(region_s + kmajor_offset(row, cc * 16 + 8, kTileM), pack_half2(av[8], av[9]),
-                       pack_half2(av[10], av[11]), pack_half2(av[12], av[13]), pack_half2(av[14], av[15]));
+          uint32_t hp[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) hp[i] = pack_half2(av[2 * i], av[2 * i + 1]);
+          tmem_st8(acol + lane_off + cc * 8, hp);
         } else {
 #pragma unroll
           for (int k = 0; k < kMaxOut; ++k) {
@@ -439,25 +507,30 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
         }
       }
       if (!last) {
-        fence_async_smem();
+        // hidden activations (TMEM) -> next layer: A from TMEM, B = W_{l+1} from smem
+        tmem_st_wait();
         tc_fence_before();
-        named_bar_sync(1 + grp, kGroupThreads);
+        mbar_arrive(gb + 9);
         if (gt == 0) {
+          mbar_wait(gb + 9, apar);
           tc_fence_after();
+          const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
           const uint32_t wl = w_s + woff;
           for (int s = 0; s < width / 16; ++s) {
-            const uint64_t ad = smem_desc(region_s + s * (2 * kTileM * 16), kTileM * 16, 128);
             const uint64_t bd = smem_desc(wl + (uint32_t)(s * 2 * (width >> 3) * 128), width * 16, 128);
-            umma_f16(tmem_col, ad, bd, idesc, s != 0);
+            umma_f16_ts(cur.dcol, acol + s * 8, bd, idesc, s != 0);
           }
-          umma_commit(bar_layer);
+          umma_commit(gb + 8);
         }
+        apar ^= 1u;
         woff += (uint32_t)(width * width * 2);
-        mbar_wait(bar_layer, nlayer & 1u);
-        nlayer++;
+        produce_next(l + 1);
+        mbar_wait(gb + 8, hpar);
+        hpar ^= 1u;
         tc_fence_after();
       }
     }
+    produce_next(slots);  // (depth == 1: nothing was interleaved)
     // head partials of the two halves of each row meet in shared memory
     if (half) {
 #pragma unroll
@@ -465,7 +538,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
     }
     tc_fence_before();
     named_bar_sync(1 + grp, kGroupThreads);
-    if (half || !valid) continue;
+    have_nxt = look;
+    if (half || !cur.valid) continue;
+    const int64_t id = cur.id;
+    const double gwt = cur.gw;
 #pragma unroll
     for (int k = 0; k < kMaxOut; ++k)
       if (k < out_dim) y[k] = (y[k] + s_hx[row * 4 + k]) + s_headb[k];
@@ -495,9 +571,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
     double num[kMaxOut], den;
     const int kk = out_dim;
 #pragma unroll
-    for (int k = 0; k < kMaxOut; ++k) num[k] = gw > 0.0 ? (double)tv[k] * gw : 0.0;
-    den = gw > 0.0 ? gw : 0.0;
-    bool is_first = (tile.flags & TF_FIRST) != 0, is_last = (tile.flags & TF_LAST) != 0;
+    for (int k = 0; k < kMaxOut; ++k) num[k] = gwt > 0.0 ? (double)tv[k] * gwt : 0.0;
+    den = gwt > 0.0 ? gwt : 0.0;
+    bool is_first = (cur.flags & TF_FIRST) != 0, is_last = (cur.flags & TF_LAST) != 0;
     if (a.ncand) {
       is_first = a.pass == 0;
       is_last = (int)a.ncand[id] == a.pass + 1;

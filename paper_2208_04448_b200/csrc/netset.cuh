@@ -19,6 +19,8 @@ struct nvdb_netset {
   std::vector<int32_t> tagnet;            // [nexperts][4]
   uint32_t max_wimg = 0;
   int max_width = 16;
+  int max_depth = 1;
+  int max_k0 = 64;
   int act = 2;  // shared hidden activation of every net
 };
 
@@ -43,6 +45,40 @@ inline SmemPlan plan_smem(uint32_t max_wimg, int max_width) {
 }
 
 constexpr uint32_t kMaxDynSmem = 227 * 1024 - 512;  // leave room for static __shared__
+
+// shared-memory / TMEM plan of mlp_eval_kernel for nets up to the given maxima
+struct EvalPlan {
+  uint32_t w_off, region_off, region_bytes, small_off, bar_off, total;
+  int nbuf, two_d, ok;
+  int sm_bias, sm_headw, sm_headb, sm_b2pi, sm_lat, sm_hx;
+};
+
+inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t limit) {
+  EvalPlan p{};
+  auto a4 = [](int v) { return (v + 3) & ~3; };
+  p.sm_bias = 0;
+  p.sm_headw = a4(depth * W);
+  p.sm_headb = p.sm_headw + a4(3 * W);
+  p.sm_b2pi = p.sm_headb + 4;
+  p.sm_lat = p.sm_b2pi + a4(3 * (k0 / 2));
+  p.sm_hx = p.sm_lat + a4(k0);
+  const int small_floats = p.sm_hx + 2 * 128 * 4;
+  p.w_off = 0;
+  p.region_off = (uint32_t)align_up(max_wimg, 1024);
+  p.ok = 0;
+  for (int nb = 3; nb >= 2 && !p.ok; --nb) {
+    p.nbuf = nb;
+    p.region_bytes = (uint32_t)(nb * kChunkBytes);
+    p.small_off = p.region_off + 2 * p.region_bytes;
+    p.bar_off = (uint32_t)align_up(p.small_off + (size_t)small_floats * 4, 16);
+    p.total = p.bar_off + 512;
+    p.ok = p.total <= limit;
+  }
+  // TMEM per group (256 columns): accumulator(s) of W columns + hidden A of W/2
+  p.two_d = (2 * W + W / 2) <= 256;
+  if (!p.two_d && (W + W / 2) > 256) p.ok = 0;
+  return p;
+}
 
 int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int grid, cudaStream_t st);
 

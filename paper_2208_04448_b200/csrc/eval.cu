@@ -251,9 +251,9 @@ int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int 
   a.sm_hx = plan.sm_hx;
   if (grid <= 0) return NVDB_OK;
   switch (ns->act) {
-    case ACT_RELU: mlp_eval_kernel<ACT_RELU><<<grid, kCtaThreads, smem, st>>>(a); break;
-    case ACT_TANH: mlp_eval_kernel<ACT_TANH><<<grid, kCtaThreads, smem, st>>>(a); break;
-    default: mlp_eval_kernel<ACT_SINE><<<grid, kCtaThreads, smem, st>>>(a); break;
+    case ACT_RELU: mlp_eval_kernel<ACT_RELU><<<grid, kEvalThreads, smem, st>>>(a); break;
+    case ACT_TANH: mlp_eval_kernel<ACT_TANH><<<grid, kEvalThreads, smem, st>>>(a); break;
+    default: mlp_eval_kernel<ACT_SINE><<<grid, kEvalThreads, smem, st>>>(a); break;
   }
   NVDB_CHECK_LAUNCH();
   return NVDB_OK;

@@ -31,8 +31,6 @@ namespace nvdb {
 
 constexpr int kTileM = 128;
 constexpr int kChunkK = 64;            // feature K chunk (fp16 elements)
-constexpr int kGroupThreads = 256;     // threads per tile group
-constexpr int kCtaThreads = 512;       // two tile groups
 constexpr int kChunkBytes = kTileM * kChunkK * 2;   // 16 KB
 constexpr int kMaxOut = 3;
 
@@ -182,37 +180,37 @@ __device__ __forceinline__ void st_shared_b32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// Warp roles of mlp_eval_kernel: producer warps build Fourier-feature chunks
+// into a shared-memory ring, one MMA warp issues every tcgen05.mma, and two
+// epilogue warpgroups (one TMEM lane quadrant per warp) own alternate tiles.
+constexpr int kProdWarps = 4;
+constexpr int kEpiGroups = 2;
+constexpr int kMmaWarp = kProdWarps + 4 * kEpiGroups;  // warp 12
+constexpr int kEvalThreads = 32 * (kMmaWarp + 1);      // 416
+constexpr int kMaxRing = 8;
+
 // ACT: the hidden activation of every net in the launch (a container's nets
 // share one TrainConfig activation), so the epilogue has no per-element branch
 template <int ACT>
-__global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a);
+__global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs a);
 
 #ifdef NVDB_MLP_KERNEL_TU  // defined in exactly one translation unit (eval.cu)
 
-// per-tile state of one group (the tile being finished and the one whose
-// features are produced ahead of time)
-struct TileCtx {
-  int64_t first;
-  int32_t count, flags;
-  int64_t id;          // point id of this thread's row (outputs)
-  float x0, x1, x2;    // normalised input of the row (per-point features)
-  double gw;           // gate weight of the row
-  bool valid, lattice;
-  float lx, ly, lz;    // lattice role inputs
-  uint32_t dcol;       // TMEM column of this tile's accumulator
-};
-
+// Pipeline (per CTA, persistent over a contiguous range of tiles):
+//   producers --ring full--> MMA warp --ring empty--> producers
+//   MMA warp --layer-0 done[e][r] / hidden done[e]--> epilogue group e
+//   epilogue e --hidden A full[e] / region free[e][r]--> MMA warp
+// The j-th non-empty tile of the CTA belongs to epilogue group j & 1; with
+// `two_d` each group alternates two TMEM accumulator regions, so layer 0 of
+// its next tile runs while it finishes the current one.  Hidden activations
+// go back to TMEM as the fp16 A operand of the next layer (tcgen05.st).
 template <int ACT>
-__global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs a) {
+__global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
-  const int grp = tid >> 8;              // tile group
-  const int gt = tid & (kGroupThreads - 1);
-  const int gw = gt >> 5;                // warp within the group
-  const int quad = gw & 3;               // TMEM lane quadrant (hardware: warp id % 4)
-  const int half = gw >> 2;              // which half of the pairs / columns
-  const int row = quad * 32 + (gt & 31);  // tile row == TMEM lane
-  const int nb = a.nbuf;                 // feature ring depth
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int nb = a.nbuf;
 
   uint8_t* wsm = smem + a.w_off;
   float* small = reinterpret_cast<float*>(smem + a.small_off);
@@ -221,403 +219,486 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
   float* s_headb = small + a.sm_headb;
   float* s_b2pi = small + a.sm_b2pi;
   float* s_lat = small + a.sm_lat;
-  float* s_hx = small + a.sm_hx + grp * 128 * 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-  // bars[0]: weights.  Per group g at 1 + 12 g: [0..2] ring empty, [3..5] ring full
-  // (256 arrivals), [6,7] layer-0 done per D region, [8] hidden layer done,
-  // [9] hidden A operand full (256 arrivals)
-  uint64_t* gb = bars + 1 + 12 * grp;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+  uint64_t* wbar = bars;            // weights landed
+  uint64_t* rfull = bars + 1;       // [kMaxRing] feature chunk written (128 producer arrivals)
+  uint64_t* rempty = bars + 9;      // [kMaxRing] chunk consumed (MMA commit)
+  // per epilogue group e at bars + 17 + 8 e: [0,1] layer 0 done per region,
+  // [2] hidden layer done, [3] hidden A written (128), [4,5] region free (128)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 40);
   __shared__ NetDev s_net;
   __shared__ ExpertDev s_exp;
 
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    for (int g = 0; g < 2; ++g) {
-      uint64_t* b = bars + 1 + 12 * g;
-      for (int i = 0; i < 3; ++i) mbar_init(&b[i], 1);
-      for (int i = 3; i < 6; ++i) mbar_init(&b[i], kGroupThreads);
-      mbar_init(&b[6], 1);
-      mbar_init(&b[7], 1);
-      mbar_init(&b[8], 1);
-      mbar_init(&b[9], kGroupThreads);
+    mbar_init(wbar, 1);
+    for (int i = 0; i < kMaxRing; ++i) {
+      mbar_init(rfull + i, 32 * kProdWarps);
+      mbar_init(rempty + i, 1);
+    }
+    for (int e = 0; e < kEpiGroups; ++e) {
+      uint64_t* b = bars + 17 + 8 * e;
+      mbar_init(b + 0, 1);
+      mbar_init(b + 1, 1);
+      mbar_init(b + 2, 1);
+      mbar_init(b + 3, 128);
+      mbar_init(b + 4, 128);
+      mbar_init(b + 5, 128);
     }
     fence_barrier_init();
   }
-  if (tid < 32) tmem_alloc(tmem_slot, 512);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t tg = tmem_base + (uint32_t)(grp * 256);   // this group's TMEM columns
-  const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-  const uint32_t ring_s = smem_addr(smem + a.region_off + grp * a.region_bytes);
+  const uint32_t ring_s = smem_addr(smem + a.region_off);
   const uint32_t w_s = smem_addr(wsm);
-
-  // pipeline state (parities as bit sets over the ring buffers)
-  uint32_t pend = 0, epar = 0, fpar = 0;  // ring: pending commit, empty parity, full parity
-  uint32_t l0par = 0, l0pend = 0;         // layer-0 done per D region
-  uint32_t hpar = 0, apar = 0;            // hidden done, hidden-A full
-  uint32_t cchunk = 0;                    // chunks produced by this group
-  uint32_t wphase = 0;
-  int loaded = -1;
 
   const int npairs = a.npairs_dev ? *a.npairs_dev : a.npairs;
   const int per_cta = (npairs + gridDim.x - 1) / gridDim.x;
-  const int p0 = blockIdx.x * per_cta;
-  const int p1 = min(npairs, p0 + per_cta);
+  const int t_begin = 2 * min(npairs, (int)blockIdx.x * per_cta);
+  const int t_end = 2 * min(npairs, ((int)blockIdx.x + 1) * per_cta);
 
-  auto pair_net = [&](int p) { return a.tiles ? a.tiles[2 * p].net : a.implicit_net; };
-  auto tile_at = [&](int p) {
-    Tile t;
+  auto tile_at = [&](int t) {
+    Tile tl;
     if (a.tiles) {
-      t = a.tiles[2 * p + grp];
+      tl = a.tiles[t];
     } else {
-      const int64_t first = (int64_t)(2 * p + grp) * kTileM;
-      t.net = a.implicit_net;
-      t.first = first;
-      t.flags = TF_FIRST | TF_LAST;
-      t.count = (int32_t)max((int64_t)0, min((int64_t)kTileM, a.n_implicit - first));
+      const int64_t first = (int64_t)t * kTileM;
+      tl.net = a.implicit_net;
+      tl.first = first;
+      tl.flags = TF_FIRST | TF_LAST;
+      tl.count = (int32_t)max((int64_t)0, min((int64_t)kTileM, a.n_implicit - first));
     }
-    return t;
+    return tl;
   };
 
-  // ---- per-tile set-up of the row inputs (decoder centres -> expert input map)
-  auto setup = [&](const Tile& t, uint32_t dcol) {
-    TileCtx c;
-    c.first = t.first;
-    c.count = t.count;
-    c.flags = t.flags;
-    c.dcol = dcol;
-    c.valid = row < t.count;
-    const int64_t pos = t.first + (c.valid ? row : 0);
-    c.id = a.idx ? a.idx[pos] : pos;
-    const int64_t sid = a.gather ? a.gather[c.id] : c.id;
-    c.lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat && t.count == kTileM &&
-                (t.first & (kTileM - 1)) == 0;
-    c.x0 = c.x1 = c.x2 = 0.f;
-    c.gw = 1.0;
-    if (!c.lattice || half == 0) {
-      double cc[3];
-      if (point_centre(a.src_kind, a.src, sid, cc)) {
-        const double is = s_exp.inv_scale;
-        c.x0 = __double2float_rn((cc[0] - s_exp.norm_origin[0]) * is);
-        c.x1 = __double2float_rn((cc[1] - s_exp.norm_origin[1]) * is);
-        c.x2 = __double2float_rn((cc[2] - s_exp.norm_origin[2]) * is);
-        c.gw = gate_weight(s_exp.cell, a.subdomain_size, a.halo, cc);
-      } else {
-        const float* s = static_cast<const float*>(a.src) + 3 * sid;
-        c.x0 = s[0]; c.x1 = s[1]; c.x2 = s[2];
-      }
+  // ---- weight switch: every thread of the CTA, at the same tile, after all
+  // work with the previous net has drained
+  int loaded = -1;
+  uint32_t wphase = 0;
+  auto load_net = [&](int net) {
+    __syncthreads();
+    if (tid == 0) {
+      s_net = a.nets[net];
+      s_exp = a.experts[a.nets[net].expert];
+      const NetDev& nd = a.nets[net];
+      mbar_arrive_expect_tx(wbar, nd.wimg_bytes);
+      for (uint32_t off = 0; off < nd.wimg_bytes; off += 32768)
+        bulk_g2s(wsm + off, nd.wimg + off, min(32768u, nd.wimg_bytes - off), wbar);
     }
-    c.lx = c.ly = c.lz = 0.f;
-    if (c.lattice) {
-      const int lk = gt & 7, ljh = (gt >> 6) & 1, lii = gt >> 7;
-      const int* o = static_cast<const int*>(a.src) + 3 * (t.first >> 9);
-      const int i0 = (int)((t.first & 511) >> 6);
-      const double is = s_exp.inv_scale;
-      c.lx = __double2float_rn((o[0] + i0 + lii + 0.5 - s_exp.norm_origin[0]) * is);
-      c.ly = __double2float_rn((o[1] + 4 * ljh + 0.5 - s_exp.norm_origin[1]) * is);
-      c.lz = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) * is);
-    }
-    return c;
-  };
-
-  // ---- one feature chunk of a tile into the ring, then its layer-0 MMAs
-  auto produce = [&](const TileCtx& c, int ch) {
-    const int width = s_net.width, k0 = s_net.k0, mp = k0 >> 1;
-    const int nch = k0 / kChunkK;
-    const int b = (int)(cchunk % (uint32_t)nb);
-    if ((pend >> b) & 1u) {
-      mbar_wait(gb + b, ((epar >> b) & 1u) ^ 1u);
-      pend &= ~(1u << b);
-    }
-    const uint32_t buf = ring_s + b * kChunkBytes;
-    if (c.lattice) {
-      // 4 pairs x 4 y-rows per thread: sincos at the first row, one rotation
-      // by exp(i beta) for the second, then the Chebyshev recurrence
-      // u_{j+1} = 2 cos(beta) u_j - u_{j-1} (one FFMA per cos / sin)
-      const int lk = gt & 7, lpg = (gt >> 3) & 7, ljh = (gt >> 6) & 1, lii = gt >> 7;
-      float cs[4][4], sn[4][4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int f = ch * (kChunkK / 2) + lpg * 4 + q;
-        const float th = fmaf(c.lz, s_b2pi[2 * mp + f], fmaf(c.ly, s_b2pi[mp + f], c.lx * s_b2pi[f]));
-        const float cb = s_lat[2 * f], sb = s_lat[2 * f + 1];
-        __sincosf(th, &sn[q][0], &cs[q][0]);
-        cs[q][1] = fmaf(cs[q][0], cb, -sn[q][0] * sb);
-        sn[q][1] = fmaf(cs[q][0], sb, sn[q][0] * cb);
-        const float c2 = 2.0f * cb;
-        cs[q][2] = fmaf(c2, cs[q][1], -cs[q][0]);
-        sn[q][2] = fmaf(c2, sn[q][1], -sn[q][0]);
-        cs[q][3] = fmaf(c2, cs[q][2], -cs[q][1]);
-        sn[q][3] = fmaf(c2, sn[q][2], -sn[q][1]);
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = lii * 64 + (4 * ljh + j) * 8 + lk;
-        st_shared_v4(buf + kmajor_offset(r, lpg * 8, kTileM), pack_half2(cs[0][j], sn[0][j]),
-                     pack_half2(cs[1][j], sn[1][j]), pack_half2(cs[2][j], sn[2][j]), pack_half2(cs[3][j], sn[3][j]));
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t h[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int f = ch * (kChunkK / 2) + half * 16 + q * 4 + j;
-          const float th = fmaf(c.x2, s_b2pi[2 * mp + f], fmaf(c.x1, s_b2pi[mp + f], c.x0 * s_b2pi[f]));
-          float sn, cs;
-          __sincosf(th, &sn, &cs);
-          h[j] = pack_half2(cs, sn);
-        }
-        st_shared_v4(buf + kmajor_offset(row, half * 32 + q * 8, kTileM), h[0], h[1], h[2], h[3]);
-      }
-    }
-    fence_async_smem();
-    mbar_arrive(gb + 3 + b);
-    if (gt == 0) {
-      mbar_wait(gb + 3 + b, (fpar >> b) & 1u);
-      tc_fence_after();
-      const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
-#pragma unroll
-      for (int s = 0; s < kChunkK / 16; ++s) {
-        const uint64_t ad = smem_desc(buf + s * (2 * kTileM * 16), kTileM * 16, 128);
-        const uint32_t wb = w_s + (uint32_t)(((ch * kChunkK + s * 16) >> 3) * (width >> 3) * 128);
-        umma_f16(c.dcol, ad, smem_desc(wb, width * 16, 128), idesc, (ch | s) != 0);
-      }
-      umma_commit(gb + b);
-      if (ch == nch - 1) umma_commit(gb + 6 + ((c.dcol - tg) ? 1 : 0));
-    }
-    fpar ^= 1u << b;
-    epar ^= 1u << b;
-    pend |= 1u << b;
-    if (ch == nch - 1) l0pend |= 1u << ((c.dcol - tg) ? 1 : 0);
-    ++cchunk;
-  };
-
-  TileCtx cur, nxt;
-  bool have_nxt = false;
-  for (int p = p0; p < p1; ++p) {
-    if (pair_net(p) != loaded) {
-      // ---- switch weights: both groups drained (no lookahead across a switch)
-      __syncthreads();
-      if (tid == 0) {
-        s_net = a.nets[pair_net(p)];
-        s_exp = a.experts[a.nets[pair_net(p)].expert];
-        const NetDev& nd = a.nets[pair_net(p)];
-        mbar_arrive_expect_tx(&bars[0], nd.wimg_bytes);
-        for (uint32_t off = 0; off < nd.wimg_bytes; off += 32768)
-          bulk_g2s(wsm + off, nd.wimg + off, min(32768u, nd.wimg_bytes - off), &bars[0]);
-      }
-      __syncthreads();
-      {
-        const NetDev& nd = s_net;
-        for (int i = tid; i < nd.depth * nd.width; i += kCtaThreads) s_bias[i] = nd.bias[i];
-        for (int i = tid; i < nd.out_dim * nd.width; i += kCtaThreads) s_headw[i] = nd.headw[i];
-        if (tid < nd.out_dim) s_headb[tid] = nd.headb[tid];
-        for (int i = tid; i < 3 * (nd.k0 / 2); i += kCtaThreads) s_b2pi[i] = nd.b2pi[i];
-        if (nd.lat)
-          for (int i = tid; i < nd.k0; i += kCtaThreads) s_lat[i] = nd.lat[i];
-      }
-      mbar_wait(&bars[0], wphase);
-      wphase ^= 1u;
-      __syncthreads();
-      loaded = pair_net(p);
-    }
-    const Tile tile = tile_at(p);
-    if (tile.count <= 0) continue;
-    const int width = s_net.width, depth = s_net.depth, k0 = s_net.k0, out_dim = s_net.out_dim;
-    const int nch = k0 / kChunkK;
-    constexpr int act = ACT;
-    if (!have_nxt) {
-      cur = setup(tile, tg);
-      for (int ch = 0; ch < nch; ++ch) produce(cur, ch);
-    } else {
-      cur = nxt;
-    }
-    have_nxt = false;
-    // next tile of this group: produce its features while this tile's layers run
-    bool look = false;
-    if (a.two_d && p + 1 < p1 && pair_net(p + 1) == loaded) {
-      const Tile t2 = tile_at(p + 1);
-      if (t2.count > 0) {
-        nxt = setup(t2, cur.dcol == tg ? tg + (uint32_t)width : tg);
-        look = true;
-      }
-    }
-    const int slots = depth;  // chunks of the next tile are spread over `depth` slots
-    int nxt_ch = 0;
-    auto produce_next = [&](int slot) {
-      if (!look) return;
-      const int upto = min(nch, (nch * (slot + 1)) / slots);
-      for (; nxt_ch < upto; ++nxt_ch) produce(nxt, nxt_ch);
-    };
-    produce_next(0);
-    // ---- layer 0 done for this tile
+    __syncthreads();
     {
-      const int r = (cur.dcol - tg) ? 1 : 0;
-      mbar_wait(gb + 6 + r, (l0par >> r) & 1u);
-      l0par ^= 1u << r;
-      l0pend &= ~(1u << r);
-      tc_fence_after();
+      const NetDev& nd = s_net;
+      for (int i = tid; i < nd.depth * nd.width; i += kEvalThreads) s_bias[i] = nd.bias[i];
+      for (int i = tid; i < nd.out_dim * nd.width; i += kEvalThreads) s_headw[i] = nd.headw[i];
+      if (tid < nd.out_dim) s_headb[tid] = nd.headb[tid];
+      for (int i = tid; i < 3 * (nd.k0 / 2); i += kEvalThreads) s_b2pi[i] = nd.b2pi[i];
+      if (nd.lat)
+        for (int i = tid; i < nd.k0; i += kEvalThreads) s_lat[i] = nd.lat[i];
     }
-    // hidden A operand (width/2 columns) after the one or two accumulator regions
-    const uint32_t acol = tg + (a.two_d ? 2u : 1u) * (uint32_t)width;
-    float y[kMaxOut] = {0.f, 0.f, 0.f};
-    uint32_t woff = (uint32_t)(width * k0 * 2);
-    for (int l = 0; l < depth; ++l) {
-      const bool last = (l == depth - 1);
-      const float* bl = s_bias + l * width;
-      for (int cc = half; cc < width / 16; cc += 2) {
-        float v[16];
-        tmem_ld16(cur.dcol + lane_off + cc * 16, v);
-        tmem_ld_wait();
-        float av[16];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 bq = reinterpret_cast<const float4*>(bl + cc * 16)[q];
-          av[4 * q + 0] = act_fn(act, v[4 * q + 0] + bq.x);
-          av[4 * q + 1] = act_fn(act, v[4 * q + 1] + bq.y);
-          av[4 * q + 2] = act_fn(act, v[4 * q + 2] + bq.z);
-          av[4 * q + 3] = act_fn(act, v[4 * q + 3] + bq.w);
+    mbar_wait(wbar, wphase);
+    wphase ^= 1u;
+    __syncthreads();
+    loaded = net;
+  };
+
+  if (warp < kProdWarps) {
+    // =============================================================== producers
+    const int pt = tid;  // 0..127
+    int slot = 0;
+    uint32_t rphase = 0;
+    for (int t = t_begin; t < t_end; ++t) {
+      const Tile tile = tile_at(t);
+      if (tile.count <= 0) continue;
+      if (tile.net != loaded) load_net(tile.net);
+      const int k0 = s_net.k0, mp = k0 >> 1, nch = k0 / kChunkK;
+      const bool lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat &&
+                           tile.count == kTileM && (tile.first & (kTileM - 1)) == 0;
+      const double is = s_exp.inv_scale;
+      float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+      // lattice role: z = lk, feature quad lpg, x = lii; 8 y rows each
+      const int lk = pt & 7, lpg = (pt >> 3) & 7, lii = pt >> 6;
+      if (lattice) {
+        const int* o = static_cast<const int*>(a.src) + 3 * (tile.first >> 9);
+        const int i0 = (int)((tile.first & 511) >> 6);
+        x0 = __double2float_rn((o[0] + i0 + lii + 0.5 - s_exp.norm_origin[0]) * is);
+        x1 = __double2float_rn((o[1] + 0.5 - s_exp.norm_origin[1]) * is);
+        x2 = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) * is);
+      } else if (pt < tile.count) {
+        const int64_t pos = tile.first + pt;
+        const int64_t id = a.idx ? a.idx[pos] : pos;
+        const int64_t sid = a.gather ? a.gather[id] : id;
+        double cc[3];
+        if (point_centre(a.src_kind, a.src, sid, cc)) {
+          x0 = __double2float_rn((cc[0] - s_exp.norm_origin[0]) * is);
+          x1 = __double2float_rn((cc[1] - s_exp.norm_origin[1]) * is);
+          x2 = __double2float_rn((cc[2] - s_exp.norm_origin[2]) * is);
+        } else {
+          const float* sp = static_cast<const float*>(a.src) + 3 * sid;
+          x0 = sp[0]; x1 = sp[1]; x2 = sp[2];
         }
-        if (!last) {
-          uint32_t hp[8];
+      }
+      for (int ch = 0; ch < nch; ++ch) {
+        mbar_wait(rempty + slot, rphase ^ 1u);
+        const uint32_t buf = ring_s + slot * kChunkBytes;
+        if (lattice) {
+          // 4 features x 8 y rows: one sincos, one rotation by exp(i beta),
+          // then the Chebyshev recurrence u_{j+1} = 2 cos(beta) u_j - u_{j-1}
+          const int f0 = ch * (kChunkK / 2) + lpg * 4;
+          const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
+          const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
+          const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
+          const float4 la = *reinterpret_cast<const float4*>(s_lat + 2 * f0);
+          const float4 lb = *reinterpret_cast<const float4*>(s_lat + 2 * f0 + 4);
+          const float bxa[4] = {bx.x, bx.y, bx.z, bx.w}, bya[4] = {by.x, by.y, by.z, by.w};
+          const float bza[4] = {bz.x, bz.y, bz.z, bz.w};
+          const float cba[4] = {la.x, la.z, lb.x, lb.z}, sba[4] = {la.y, la.w, lb.y, lb.w};
+          float cs[4][2], sn[4][2], c2[4];
+          uint32_t hp[4];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) hp[i] = pack_half2(av[2 * i], av[2 * i + 1]);
-          tmem_st8(acol + lane_off + cc * 8, hp);
+          for (int q = 0; q < 4; ++q) {
+            const float th = fmaf(x2, bza[q], fmaf(x1, bya[q], x0 * bxa[q]));
+            __sincosf(th, &sn[q][0], &cs[q][0]);
+            cs[q][1] = fmaf(cs[q][0], cba[q], -sn[q][0] * sba[q]);
+            sn[q][1] = fmaf(cs[q][0], sba[q], sn[q][0] * cba[q]);
+            c2[q] = 2.0f * cba[q];
+            hp[q] = pack_half2(cs[q][0], sn[q][0]);
+          }
+          st_shared_v4(buf + kmajor_offset(lii * 64 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) hp[q] = pack_half2(cs[q][1], sn[q][1]);
+          st_shared_v4(buf + kmajor_offset(lii * 64 + 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
+#pragma unroll
+          for (int jy = 2; jy < 8; ++jy) {
+            const int cur = jy & 1;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              cs[q][cur] = fmaf(c2[q], cs[q][cur ^ 1], -cs[q][cur]);
+              sn[q][cur] = fmaf(c2[q], sn[q][cur ^ 1], -sn[q][cur]);
+              hp[q] = pack_half2(cs[q][cur], sn[q][cur]);
+            }
+            st_shared_v4(buf + kmajor_offset(lii * 64 + jy * 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2],
+                         hp[3]);
+          }
         } else {
 #pragma unroll
-          for (int k = 0; k < kMaxOut; ++k) {
-            if (k < out_dim) {
-              const float4* hw = reinterpret_cast<const float4*>(s_headw + k * width + cc * 16);
-              float s = y[k];
+          for (int q = 0; q < 8; ++q) {
+            const int f0 = ch * (kChunkK / 2) + q * 4;
+            const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
+            const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
+            const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
+            const float bxa[4] = {bx.x, bx.y, bx.z, bx.w}, bya[4] = {by.x, by.y, by.z, by.w};
+            const float bza[4] = {bz.x, bz.y, bz.z, bz.w};
+            uint32_t h[4];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float4 w4 = hw[q];
-                s = fmaf(av[4 * q], w4.x, s);
-                s = fmaf(av[4 * q + 1], w4.y, s);
-                s = fmaf(av[4 * q + 2], w4.z, s);
-                s = fmaf(av[4 * q + 3], w4.w, s);
+            for (int j = 0; j < 4; ++j) {
+              const float th = fmaf(x2, bza[j], fmaf(x1, bya[j], x0 * bxa[j]));
+              float sv, cv;
+              __sincosf(th, &sv, &cv);
+              h[j] = pack_half2(cv, sv);
+            }
+            st_shared_v4(buf + kmajor_offset(pt, q * 8, kTileM), h[0], h[1], h[2], h[3]);
+          }
+        }
+        fence_async_smem();
+        mbar_arrive(rfull + slot);
+        if (++slot == nb) {
+          slot = 0;
+          rphase ^= 1u;
+        }
+      }
+    }
+  } else if (warp < kMmaWarp) {
+    // =============================================================== epilogue
+    const int e = (warp - kProdWarps) >> 2;
+    const int quad = warp & 3;  // TMEM lane quadrant (hardware: warp id % 4)
+    const int row = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    uint64_t* eb = bars + 17 + 8 * e;
+    const uint32_t ecol = tmem_base + (uint32_t)(e * 256);
+    uint32_t l0par = 0, hpar = 0;
+    int j = 0;
+    constexpr int act = ACT;
+    for (int t = t_begin; t < t_end; ++t) {
+      const Tile tile = tile_at(t);
+      if (tile.count <= 0) continue;
+      if (tile.net != loaded) load_net(tile.net);
+      const int mine = (j & 1) == e;
+      const int jj = j >> 1;
+      ++j;
+      if (!mine) continue;
+      const int width = s_net.width, depth = s_net.depth, out_dim = s_net.out_dim;
+      const int r = a.two_d ? (jj & 1) : 0;
+      const uint32_t dcol = ecol + (uint32_t)(r * width);
+      const uint32_t acol = ecol + (a.two_d ? 2u : 1u) * (uint32_t)width;
+      // row set-up (outputs, gate weight)
+      const bool valid = row < tile.count;
+      const int64_t pos = tile.first + (valid ? row : 0);
+      const int64_t id = a.idx ? a.idx[pos] : pos;
+      double gwt = 1.0;
+      if (a.src_kind != SRC_NORM_F32) {
+        const int64_t sid = a.gather ? a.gather[id] : id;
+        double cc[3];
+        point_centre(a.src_kind, a.src, sid, cc);
+        gwt = gate_weight(s_exp.cell, a.subdomain_size, a.halo, cc);
+      }
+      float y[kMaxOut] = {0.f, 0.f, 0.f};
+      for (int l = 0; l < depth; ++l) {
+        const bool last = (l == depth - 1);
+        if (l == 0) {
+          mbar_wait(eb + r, (l0par >> r) & 1u);
+          l0par ^= 1u << r;
+        } else {
+          mbar_wait(eb + 2, hpar);
+          hpar ^= 1u;
+        }
+        tc_fence_after();
+        const float* bl = s_bias + l * width;
+        auto epi = [&](int cc, const float (&v)[16]) {
+          float av[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 bq = reinterpret_cast<const float4*>(bl + cc * 16)[q];
+            av[4 * q + 0] = act_fn(act, v[4 * q + 0] + bq.x);
+            av[4 * q + 1] = act_fn(act, v[4 * q + 1] + bq.y);
+            av[4 * q + 2] = act_fn(act, v[4 * q + 2] + bq.z);
+            av[4 * q + 3] = act_fn(act, v[4 * q + 3] + bq.w);
+          }
+          if (!last) {
+            uint32_t hp[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) hp[i] = pack_half2(av[2 * i], av[2 * i + 1]);
+            tmem_st8(acol + lane_off + cc * 8, hp);
+          } else {
+#pragma unroll
+            for (int k = 0; k < kMaxOut; ++k) {
+              if (k < out_dim) {
+                const float4* hw = reinterpret_cast<const float4*>(s_headw + k * width + cc * 16);
+                float sacc = y[k];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float4 w4 = hw[q];
+                  sacc = fmaf(av[4 * q], w4.x, sacc);
+                  sacc = fmaf(av[4 * q + 1], w4.y, sacc);
+                  sacc = fmaf(av[4 * q + 2], w4.z, sacc);
+                  sacc = fmaf(av[4 * q + 3], w4.w, sacc);
+                }
+                y[k] = sacc;
               }
-              y[k] = s;
+            }
+          }
+        };
+        // up to three 16-column TMEM loads in flight per wait
+        const int ncc = width / 16;
+        for (int c0 = 0; c0 < ncc; c0 += 3) {
+          const int m = min(3, ncc - c0);
+          float v0[16], v1[16], v2[16];
+          tmem_ld16(dcol + lane_off + c0 * 16, v0);
+          if (m > 1) tmem_ld16(dcol + lane_off + (c0 + 1) * 16, v1);
+          if (m > 2) tmem_ld16(dcol + lane_off + (c0 + 2) * 16, v2);
+          tmem_ld_wait();
+          epi(c0, v0);
+          if (m > 1) epi(c0 + 1, v1);
+          if (m > 2) epi(c0 + 2, v2);
+        }
+        if (!last) {
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(eb + 3);
+        } else {
+          tc_fence_before();
+          mbar_arrive(eb + 4 + r);
+        }
+      }
+      if (!valid) continue;
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k)
+        if (k < out_dim) y[k] = y[k] + s_headb[k];
+
+      // ------------------------------------------------ output
+      if (a.out_mode == OUT_RAW) {
+#pragma unroll
+        for (int k = 0; k < kMaxOut; ++k)
+          if (k < out_dim) a.out_raw[id * out_dim + k] = y[k];
+        continue;
+      }
+      // transform (inference.py:29-36) in float32
+      float tv[kMaxOut];
+      const int head = s_net.head;
+      tv[1] = tv[2] = 0.f;
+      if (head == HEAD_LOGITS) {  // 3-way softmax (l1 classifier heads are always 3 wide)
+        const float zm = fmaxf(fmaxf(y[0], y[1]), y[2]);
+        const float e0 = expf(y[0] - zm), e1 = expf(y[1] - zm), e2 = expf(y[2] - zm);
+        const float ssum = (e0 + e1) + e2;
+        tv[0] = e0 / ssum; tv[1] = e1 / ssum; tv[2] = e2 / ssum;
+      } else if (head == HEAD_BINARY) {
+        tv[0] = 1.0f / (1.0f + expf(-y[0]));
+      } else {
+        tv[0] = y[0];
+      }
+      // gate-weighted accumulation (partition.py:245-256), f64, sid order = pass order
+      double num[kMaxOut], den;
+      const int kk = out_dim;
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k) num[k] = gwt > 0.0 ? (double)tv[k] * gwt : 0.0;
+      den = gwt > 0.0 ? gwt : 0.0;
+      bool is_first = (tile.flags & TF_FIRST) != 0, is_last = (tile.flags & TF_LAST) != 0;
+      if (a.ncand) {
+        is_first = a.pass == 0;
+        is_last = (int)a.ncand[id] == a.pass + 1;
+      }
+      if (!is_first) {
+        const double* ac = a.acc + 4 * id;
+#pragma unroll
+        for (int k = 0; k < kMaxOut; ++k) num[k] = ac[k] + num[k];
+        den = ac[3] + den;
+      }
+      if (!is_last) {
+        double* ac = a.acc + 4 * id;
+#pragma unroll
+        for (int k = 0; k < kMaxOut; ++k) ac[k] = num[k];
+        ac[3] = den;
+        continue;
+      }
+      const bool covered = den > 0.0;
+      if (covered) {
+#pragma unroll
+        for (int k = 0; k < kMaxOut; ++k) num[k] = num[k] / den;
+      }
+      switch (a.out_mode) {
+        case OUT_PROBS:
+#pragma unroll
+          for (int k = 0; k < kMaxOut; ++k)
+            if (k < kk) a.out_probs[id * kk + k] = covered ? num[k] : 0.0;
+          a.out_u8[id] = covered ? 1 : 0;
+          break;
+        case OUT_L1CLASS: {
+          int best = 0;
+          if (num[1] > num[best]) best = 1;
+          if (num[2] > num[best]) best = 2;
+          a.out_u8[id] = covered ? (uint8_t)best : (uint8_t)2;
+          break;
+        }
+        case OUT_L0ACTIVE:
+          a.out_u8[id] = (covered && num[0] > 0.5) ? 1 : 0;
+          break;
+        default: {  // OUT_VALUE
+          double v = num[0];
+          if (a.clip) v = fmin(fmax(v, -1.0), 1.0);
+          a.out_f32[id] = covered ? (float)(v * a.value_scale) : a.background;
+          break;
+        }
+      }
+    }
+  } else {
+    // =============================================================== MMA warp
+    // all lanes run the schedule; lane 0 issues.  Readiness is probed without
+    // blocking so hidden-layer jobs of one group never wait behind layer 0 of
+    // the other group's tile.
+    const bool leader = lane == 0;
+    int slot = 0;
+    uint32_t rphase = 0;
+    int qn[kEpiGroups] = {0, 0};            // tiles with hidden layers outstanding
+    int qr[kEpiGroups][2] = {{0, 0}, {0, 0}};  // their accumulator regions (FIFO)
+    int hl[kEpiGroups] = {1, 1};            // next hidden layer of the oldest one
+    uint32_t apar = 0;                      // hidden-A full parity per group (bit e)
+    uint32_t duse[kEpiGroups][2] = {{0, 0}, {0, 0}};  // layer-0 uses per region
+    int t = t_begin, j = 0;
+    bool l0_active = false;
+    int ce = 0, cr = 0, ch = 0, nch = 0;
+    while (true) {
+      const int width = s_net.width, depth = s_net.depth;
+      // ---- hidden layers (A operand from TMEM, B = W_l from shared memory)
+      if (depth > 1) {
+#pragma unroll
+        for (int e = 0; e < kEpiGroups; ++e) {
+          if (qn[e] > 0 && mbar_test(bars + 17 + 8 * e + 3, (apar >> e) & 1u)) {
+            apar ^= 1u << e;
+            tc_fence_after();
+            const int l = hl[e];
+            const uint32_t ecol = tmem_base + (uint32_t)(e * 256);
+            const uint32_t dcol = ecol + (uint32_t)(qr[e][0] * width);
+            const uint32_t acol = ecol + (a.two_d ? 2u : 1u) * (uint32_t)width;
+            if (leader) {
+              const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
+              const uint32_t wl = w_s + (uint32_t)(width * s_net.k0 * 2 + (l - 1) * width * width * 2);
+              for (int s = 0; s < width / 16; ++s) {
+                const uint64_t bd = smem_desc(wl + (uint32_t)(s * 2 * (width >> 3) * 128), width * 16, 128);
+                umma_f16_ts(dcol, acol + s * 8, bd, idesc, s != 0);
+              }
+              umma_commit(bars + 17 + 8 * e + 2);
+            }
+            __syncwarp();
+            if (++hl[e] == depth) {
+              hl[e] = 1;
+              qr[e][0] = qr[e][1];
+              --qn[e];
             }
           }
         }
       }
-      if (!last) {
-        // hidden activations (TMEM) -> next layer: A from TMEM, B = W_{l+1} from smem
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(gb + 9);
-        if (gt == 0) {
-          mbar_wait(gb + 9, apar);
-          tc_fence_after();
-          const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
-          const uint32_t wl = w_s + woff;
-          for (int s = 0; s < width / 16; ++s) {
-            const uint64_t bd = smem_desc(wl + (uint32_t)(s * 2 * (width >> 3) * 128), width * 16, 128);
-            umma_f16_ts(cur.dcol, acol + s * 8, bd, idesc, s != 0);
-          }
-          umma_commit(gb + 8);
+      // ---- layer 0 of the next tile
+      if (!l0_active) {
+        Tile tile;
+        tile.count = 0;
+        while (t < t_end) {
+          tile = tile_at(t);
+          if (tile.count > 0) break;
+          ++t;
         }
-        apar ^= 1u;
-        woff += (uint32_t)(width * width * 2);
-        produce_next(l + 1);
-        mbar_wait(gb + 8, hpar);
-        hpar ^= 1u;
+        if (t >= t_end) {
+          if (qn[0] == 0 && qn[1] == 0) break;
+          continue;
+        }
+        if (tile.net != loaded) {
+          if (qn[0] != 0 || qn[1] != 0) continue;  // drain before the weight switch
+          load_net(tile.net);
+          continue;
+        }
+        const int e = j & 1, jj = j >> 1;
+        const int r = a.two_d ? (jj & 1) : 0;
+        const int cap = a.two_d ? 2 : 1;
+        if (depth > 1 && qn[e] >= cap) continue;
+        if (duse[e][r] > 0 && !mbar_test(bars + 17 + 8 * e + 4 + r, (duse[e][r] - 1) & 1u)) continue;
+        ++duse[e][r];
+        l0_active = true;
+        ce = e;
+        cr = r;
+        ch = 0;
+        nch = s_net.k0 / kChunkK;
+      }
+      const uint32_t dcol = tmem_base + (uint32_t)(ce * 256 + cr * width);
+      while (ch < nch && mbar_test(rfull + slot, rphase)) {
         tc_fence_after();
+        if (leader) {
+          const uint32_t buf = ring_s + slot * kChunkBytes;
+          const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
+#pragma unroll
+          for (int s = 0; s < kChunkK / 16; ++s) {
+            const uint64_t ad = smem_desc(buf + s * (2 * kTileM * 16), kTileM * 16, 128);
+            const uint32_t wb = w_s + (uint32_t)(((ch * kChunkK + s * 16) >> 3) * (width >> 3) * 128);
+            umma_f16(dcol, ad, smem_desc(wb, width * 16, 128), idesc, (ch | s) != 0);
+          }
+          umma_commit(rempty + slot);
+        }
+        __syncwarp();
+        if (++slot == nb) {
+          slot = 0;
+          rphase ^= 1u;
+        }
+        ++ch;
       }
-    }
-    produce_next(slots);  // (depth == 1: nothing was interleaved)
-    // head partials of the two halves of each row meet in shared memory
-    if (half) {
-#pragma unroll
-      for (int k = 0; k < kMaxOut; ++k) s_hx[row * 4 + k] = y[k];
-    }
-    tc_fence_before();
-    named_bar_sync(1 + grp, kGroupThreads);
-    have_nxt = look;
-    if (half || !cur.valid) continue;
-    const int64_t id = cur.id;
-    const double gwt = cur.gw;
-#pragma unroll
-    for (int k = 0; k < kMaxOut; ++k)
-      if (k < out_dim) y[k] = (y[k] + s_hx[row * 4 + k]) + s_headb[k];
-
-    // ------------------------------------------------ output
-    if (a.out_mode == OUT_RAW) {
-#pragma unroll
-      for (int k = 0; k < kMaxOut; ++k)
-        if (k < out_dim) a.out_raw[id * out_dim + k] = y[k];
-      continue;
-    }
-    // transform (inference.py:29-36) in float32
-    float tv[kMaxOut];
-    const int head = s_net.head;
-    tv[1] = tv[2] = 0.f;
-    if (head == HEAD_LOGITS) {  // 3-way softmax (l1 classifier heads are always 3 wide)
-      const float zm = fmaxf(fmaxf(y[0], y[1]), y[2]);
-      const float e0 = expf(y[0] - zm), e1 = expf(y[1] - zm), e2 = expf(y[2] - zm);
-      const float ssum = (e0 + e1) + e2;
-      tv[0] = e0 / ssum; tv[1] = e1 / ssum; tv[2] = e2 / ssum;
-    } else if (head == HEAD_BINARY) {
-      tv[0] = 1.0f / (1.0f + expf(-y[0]));
-    } else {
-      tv[0] = y[0];
-    }
-    // gate-weighted accumulation (partition.py:245-256), f64, sid order = pass order
-    double num[kMaxOut], den;
-    const int kk = out_dim;
-#pragma unroll
-    for (int k = 0; k < kMaxOut; ++k) num[k] = gwt > 0.0 ? (double)tv[k] * gwt : 0.0;
-    den = gwt > 0.0 ? gwt : 0.0;
-    bool is_first = (cur.flags & TF_FIRST) != 0, is_last = (cur.flags & TF_LAST) != 0;
-    if (a.ncand) {
-      is_first = a.pass == 0;
-      is_last = (int)a.ncand[id] == a.pass + 1;
-    }
-    if (!is_first) {
-      const double* ac = a.acc + 4 * id;
-#pragma unroll
-      for (int k = 0; k < kMaxOut; ++k) num[k] = ac[k] + num[k];
-      den = ac[3] + den;
-    }
-    if (!is_last) {
-      double* ac = a.acc + 4 * id;
-#pragma unroll
-      for (int k = 0; k < kMaxOut; ++k) ac[k] = num[k];
-      ac[3] = den;
-      continue;
-    }
-    const bool covered = den > 0.0;
-    if (covered) {
-#pragma unroll
-      for (int k = 0; k < kMaxOut; ++k) num[k] = num[k] / den;
-    }
-    switch (a.out_mode) {
-      case OUT_PROBS:
-#pragma unroll
-        for (int k = 0; k < kMaxOut; ++k)
-          if (k < kk) a.out_probs[id * kk + k] = covered ? num[k] : 0.0;
-        a.out_u8[id] = covered ? 1 : 0;
-        break;
-      case OUT_L1CLASS: {
-        int best = 0;
-        if (num[1] > num[best]) best = 1;
-        if (num[2] > num[best]) best = 2;
-        a.out_u8[id] = covered ? (uint8_t)best : (uint8_t)2;
-        break;
-      }
-      case OUT_L0ACTIVE:
-        a.out_u8[id] = (covered && num[0] > 0.5) ? 1 : 0;
-        break;
-      default: {  // OUT_VALUE
-        double v = num[0];
-        if (a.clip) v = fmin(fmax(v, -1.0), 1.0);
-        a.out_f32[id] = covered ? (float)(v * a.value_scale) : a.background;
-        break;
+      if (ch == nch) {
+        if (leader) umma_commit(bars + 17 + 8 * ce + cr);
+        __syncwarp();
+        if (depth > 1) {
+          qr[ce][qn[ce]] = cr;
+          ++qn[ce];
+        }
+        l0_active = false;
+        ++j;
+        ++t;
       }
     }
   }
@@ -625,7 +706,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) mlp_eval_kernel(const MlpArgs 
   // ------------------------------------------------ teardown
   tc_fence_before();
   __syncthreads();
-  if (tid < 32) tmem_dealloc(tmem_base, 512);
+  if (warp == kMmaWarp) tmem_dealloc(tmem_base, 512);
 }
 #endif  // NVDB_MLP_KERNEL_TU
 

@@ -1,5 +1,6 @@
 // Device-resident set of every expert's networks (the decode/eval "model").
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <vector>
 
@@ -62,19 +63,18 @@ inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t 
   p.sm_b2pi = p.sm_headb + 4;
   p.sm_lat = p.sm_b2pi + a4(3 * (k0 / 2));
   p.sm_hx = p.sm_lat + a4(k0);
-  const int small_floats = p.sm_hx + 2 * 128 * 4;
+  const uint32_t small_bytes = (uint32_t)p.sm_hx * 4u;
   p.w_off = 0;
   p.region_off = (uint32_t)align_up(max_wimg, 1024);
-  p.ok = 0;
-  for (int nb = 3; nb >= 2 && !p.ok; --nb) {
-    p.nbuf = nb;
-    p.region_bytes = (uint32_t)(nb * kChunkBytes);
-    p.small_off = p.region_off + 2 * p.region_bytes;
-    p.bar_off = (uint32_t)align_up(p.small_off + (size_t)small_floats * 4, 16);
-    p.total = p.bar_off + 512;
-    p.ok = p.total <= limit;
-  }
-  // TMEM per group (256 columns): accumulator(s) of W columns + hidden A of W/2
+  // feature ring: as many 16 KB chunk slots as fit (2..kMaxRing)
+  const long long room = (long long)limit - p.region_off - small_bytes - 16 - 512;
+  p.nbuf = (int)std::min<long long>(kMaxRing, room > 0 ? room / kChunkBytes : 0);
+  p.region_bytes = (uint32_t)(p.nbuf * kChunkBytes);
+  p.small_off = p.region_off + p.region_bytes;
+  p.bar_off = (uint32_t)align_up(p.small_off + small_bytes, 16);
+  p.total = p.bar_off + 512;
+  p.ok = p.nbuf >= 2 && p.total <= limit;
+  // TMEM per epilogue group (256 columns): accumulator(s) of W columns + hidden A of W/2
   p.two_d = (2 * W + W / 2) <= 256;
   if (!p.two_d && (W + W / 2) > 256) p.ok = 0;
   return p;

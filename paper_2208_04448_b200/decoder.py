@@ -397,6 +397,28 @@ def decode_report(c, device=None) -> Dict[str, int]:
             "active_voxels": int(d.leaf_active.sum().item())}
 
 
+def hybrid_query(tree: DeviceTree, nets, coords: torch.Tensor, value_scale: float, clip: bool):
+    """Explicit-topology lookup + neural values on active leaf voxels
+    (decoder.py:239-264): K1 lookup, select the rows that resolve to an
+    active leaf voxel, gate-blended voxel regressor on exactly those rows,
+    scatter.  ``nets`` is a DeviceModel or NetEvaluator.  Returns (values,
+    active, regressor evaluations)."""
+    dev, st = nets.dev, _stream(nets.dev)
+    n = coords.shape[0]
+    val, act, kind, leaf = tree.lookup(coords, want_leaf=True)
+    flag = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    check(lib().nvdb_neural_rows(_ptr(act), _ptr(kind), n, _ptr(flag), st), "nvdb_neural_rows")
+    rows = nets.select(flag[:n], 1)
+    nr = rows.numel()
+    if nr:
+        reg = torch.empty(nr, dtype=torch.float32, device=dev)
+        nets.evaluate("voxel", _lib.SRC_COORD_I32, coords, nr, _lib.OUT_VALUE, gather=rows, f32=reg,
+                      value_scale=value_scale, clip=clip)
+        check(lib().nvdb_query_finalize(_ptr(rows), nr, _ptr(reg), _ptr(coords), _ptr(leaf),
+                                        tree.handle, _ptr(val), st), "nvdb_query_finalize")
+    return val, act, nr
+
+
 class HybridGrid:
     """Explicit topology with neural leaf values (decoder.py:222-264)."""
 
@@ -414,19 +436,7 @@ class HybridGrid:
     def query_device(self, coords: torch.Tensor):
         """(values f32, active u8) for device int32 coords (n,3)."""
         m = self.model
-        dev, st = m.dev, _stream(m.dev)
-        n = coords.shape[0]
-        val, act, kind, leaf = self.tree.lookup(coords, want_leaf=True)
-        flag = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
-        check(lib().nvdb_neural_rows(_ptr(act), _ptr(kind), n, _ptr(flag), st), "nvdb_neural_rows")
-        rows = m.select(flag[:n], 1)
-        nr = rows.numel()
-        if nr:
-            reg = torch.empty(nr, dtype=torch.float32, device=dev)
-            m.evaluate("voxel", _lib.SRC_COORD_I32, coords, nr, _lib.OUT_VALUE, gather=rows, f32=reg,
-                       value_scale=m.value_scale, clip=m.meta.grid_class == "sdf")
-            check(lib().nvdb_query_finalize(_ptr(rows), nr, _ptr(reg), _ptr(coords), _ptr(leaf),
-                                            self.tree.handle, _ptr(val), st), "nvdb_query_finalize")
+        val, act, nr = hybrid_query(self.tree, m, coords, m.value_scale, m.meta.grid_class == "sdf")
         self.regressor_evaluations += nr
         return val, act
 

@@ -103,6 +103,10 @@ class MlpParams:
     def parameter_count(self) -> int:
         return sum(w.size + b.size for w, b in self.layers)
 
+    def flatten(self) -> np.ndarray:
+        """All parameters, layer by layer, weights then bias (neural.py:164-165)."""
+        return np.concatenate([np.concatenate([w.ravel(), b.ravel()]) for w, b in self.layers])
+
 
 @dataclass
 class NetRecord:

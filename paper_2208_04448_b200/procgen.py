@@ -29,14 +29,30 @@ def _canonical_leaf_order(origins: np.ndarray) -> np.ndarray:
 
 
 def banded_sdf_grid(distance: Callable[[np.ndarray], np.ndarray], lo_idx, hi_idx, voxel_size: float,
-                    half_width: float, chunk: int = 4096) -> DenseLeafGrid:
-    """procgen.py:174-197 + 200-232 as array code."""
+                    half_width: float, chunk: int = 4096, lipschitz: bool = True) -> DenseLeafGrid:
+    """procgen.py:174-197 + 200-232 as array code.
+
+    With ``lipschitz`` (true for exact SDFs such as the sphere and torus) a
+    leaf block is skipped when its centre lies farther than the band plus the
+    block's half-diagonal from the surface: none of its voxels can be active,
+    so the reference would drop it too and the output is unchanged.
+    """
     band = half_width * voxel_size
     lo = np.asarray(lo_idx, dtype=np.int64) & ~np.int64(7)
     hi = np.asarray(hi_idx, dtype=np.int64)
     axes = [np.arange(lo[a], hi[a] + 1, 8, dtype=np.int64) for a in range(3)]
-    gx, gy, gz = np.meshgrid(*axes, indexing="ij")
-    blocks = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
+    if lipschitz:
+        reach = band + (3.5 * np.sqrt(3.0) + 0.01) * voxel_size
+        keep = []
+        for x in axes[0]:
+            gy, gz = np.meshgrid(axes[1], axes[2], indexing="ij")
+            slab = np.stack([np.full(gy.size, x, np.int64), gy.ravel(), gz.ravel()], axis=1)
+            dc = distance((slab.astype(np.float64) + 3.5) * voxel_size)
+            keep.append(slab[np.abs(dc) < reach])
+        blocks = np.concatenate(keep) if keep else np.zeros((0, 3), np.int64)
+    else:
+        gx, gy, gz = np.meshgrid(*axes, indexing="ij")
+        blocks = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
     keep_o, keep_a, keep_v = [], [], []
     for s in range(0, len(blocks), chunk):
         blk = blocks[s:s + chunk]

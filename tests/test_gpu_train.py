@@ -136,3 +136,44 @@ def test_ac4_encode_decode_quality_on_gpu():
     assert i >= 0.99 and d <= 0.5            # the acceptance bars
     assert abs(i - 0.99835) < 1e-3 and abs(d - 0.0313) < 1e-2
     m.close()
+
+
+def _seq_cfg():
+    from paper_2208_04448_b200.encoder import TrainConfig
+    return TrainConfig(l1_net=(2, 8), l0_net=(2, 16), voxel_net=(2, 24), tile_net=None, ffm_size=24,
+                       max_epochs=300, batch_size=4096, lr=1e-3, refine_lr=2e-4, seed=13)
+
+
+def _moving_sphere(n, step):
+    from paper_2208_04448_b200.procgen import sphere_sdf
+    return [sphere_sdf((20.0 + step * t, 20.0, 20.0), 11.0, 1.0, 3.0) for t in range(n)]
+
+
+def test_sequence_identical_frames_early_stop_on_gpu():
+    """test_encoder.py:255-262: frame 1 warm-starts from frame 0's converged
+    weights on identical data, so every network early-stops almost at once."""
+    from paper_2208_04448_b200.encoder import encode_sequence
+    containers, reports = encode_sequence(_moving_sphere(2, 0.0), _seq_cfg(), device=DEV)
+    assert len(containers) == 2
+    print(f"cold {reports[0].detail['cold_epochs']} warm {reports[1].epochs}")
+    assert reports[1].epochs <= 0.2 * reports[0].detail["cold_epochs"]
+
+
+def test_sequence_warm_start_on_gpu():
+    """test_encoder.py:265-279: warm frames need no more epochs than the cold
+    frame, and consecutive frames' weights stay closer than independent colds."""
+    from paper_2208_04448_b200.encoder import encode_sequence
+    frames = _moving_sphere(3, 1.0)
+    cfg = _seq_cfg()
+    containers, reports = encode_sequence(frames, cfg, device=DEV)
+    cold = reports[0].detail["cold_epochs"]
+    print(f"cold {cold} warm {[r.epochs for r in reports[1:]]}")
+    for rep in reports[1:]:
+        assert rep.epochs <= cold
+    w1 = containers[1].experts[0].voxel_regressor.params.flatten()
+    w2 = containers[2].experts[0].voxel_regressor.params.flatten()
+    solo1 = encode(frames[1], cfg, device=DEV)
+    solo2 = encode(frames[2], cfg, device=DEV)
+    indep = np.linalg.norm(solo2.experts[0].voxel_regressor.params.flatten()
+                           - solo1.experts[0].voxel_regressor.params.flatten())
+    assert np.linalg.norm(w2 - w1) < indep

@@ -14,7 +14,8 @@ from typing import Optional
 from .errors import SvcodecError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnvdb_b200.so")
+# NVDB_LIB selects a debug build (e.g. libnvdb_b200_trace.so) for diagnostics
+LIB_PATH = os.path.join(HERE, os.environ.get("NVDB_LIB", "libnvdb_b200.so"))
 
 NVDB_OK = 0
 NVDB_EINVAL = -1

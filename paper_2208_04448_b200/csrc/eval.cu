@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -28,6 +29,18 @@ int round_up_i(int v, int a) { return (v + a - 1) / a * a; }
 extern "C" const char* nvdb_last_error(void) { return last_error_slot().c_str(); }
 extern "C" int nvdb_version(void) { return 1; }
 extern "C" long long nvdb_launch_count(void) { return launch_counter().load(); }
+
+#ifdef NVDB_TRACE
+// trace build only (make trace): arm the CTA-0 timeline of mlp_eval_kernel
+extern "C" NVDB_API int nvdb_debug_trace(void* buf, uint32_t cap) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  const unsigned int zero = 0;
+  cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
+  cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof(cap));
+  cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(zero));
+  return cudaDeviceSynchronize() == cudaSuccess ? NVDB_OK : NVDB_ECUDA;
+}
+#endif
 
 // ---------------------------------------------------------------------------
 // netset
@@ -241,8 +254,8 @@ int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int 
   a.region_bytes = plan.region_bytes;
   a.small_off = plan.small_off;
   a.bar_off = plan.bar_off;
-  a.nbuf = plan.nbuf;
-  a.two_d = plan.two_d;
+  a.engines = plan.engines;
+  a.tcols = plan.tcols;
   a.sm_bias = plan.sm_bias;
   a.sm_headw = plan.sm_headw;
   a.sm_headb = plan.sm_headb;
@@ -251,9 +264,9 @@ int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int 
   a.sm_hx = plan.sm_hx;
   if (grid <= 0) return NVDB_OK;
   switch (ns->act) {
-    case ACT_RELU: mlp_eval_kernel<ACT_RELU><<<grid, kEvalThreads, smem, st>>>(a); break;
-    case ACT_TANH: mlp_eval_kernel<ACT_TANH><<<grid, kEvalThreads, smem, st>>>(a); break;
-    default: mlp_eval_kernel<ACT_SINE><<<grid, kEvalThreads, smem, st>>>(a); break;
+    case ACT_RELU: mlp_eval_kernel<ACT_RELU><<<grid, 128 * plan.engines, smem, st>>>(a); break;
+    case ACT_TANH: mlp_eval_kernel<ACT_TANH><<<grid, 128 * plan.engines, smem, st>>>(a); break;
+    default: mlp_eval_kernel<ACT_SINE><<<grid, 128 * plan.engines, smem, st>>>(a); break;
   }
   NVDB_CHECK_LAUNCH();
   return NVDB_OK;

@@ -10,20 +10,23 @@
 //   -> softmax / sigmoid / identity, clamped-tent gate weight, f64 blend,
 //      and the decode decision (argmax, > 0.5, clip*scale) in the epilogue.
 //
-// CTA = 2 tile groups of 8 warps.  A group owns one 128-point tile at a time:
-// TMEM lane p (= point row p) is served by two threads (warps q and q+4 of
-// the group, which share the lane quadrant), each taking half of the feature
-// pairs and half of the accumulator columns; one elected thread issues the
-// group's MMAs, so the tensor core runs one group's tile while the other
-// group is in its MUFU/FMA epilogue.  Weights of the current net live in
-// shared memory (one bulk async copy); tiles come in pairs sharing a net.
+// CTA = up to three "tile engines" of 4 warps.  An engine owns one 128-point
+// tile at a time end to end: its 128 threads build the Fourier-feature chunks
+// of the tile into the engine's shared-memory slots, one elected thread issues
+// the engine's tcgen05.mma for each chunk and each hidden layer, and the same
+// 128 threads (TMEM lane p = point row p) run the bias/activation epilogue,
+// write the fp16 activations back to TMEM as the next layer's A operand, and
+// finish with the fp32 head, transform, gate and decision.  The engines share
+// the net's weights in shared memory; the tensor core and MUFU are kept busy
+// by whichever engines are not waiting on an MMA.
 //
 // Leaf-voxel tiles (a quarter of one 8^3 leaf) build their features by angle
 // addition on the FMA pipe: per feature one sincos per 8 voxels along y, then
-// z_{j+1} = z_j * exp(i beta_f) (beta_f = 2 pi b_fy / norm_scale), instead of
-// 2m MUFU sin/cos per point.  Other sources use __sincosf per point.
+// the Chebyshev recurrence along y, instead of 2m MUFU sin/cos per point.
+// Other sources use __sincosf per point.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "ptx.cuh"
 
@@ -108,8 +111,8 @@ struct MlpArgs {
   int32_t clip;
   // shared-memory carve-up (bytes, 1024-aligned offsets)
   uint32_t w_off, region_off, region_bytes, small_off, bar_off;
-  int32_t nbuf;   // feature ring buffers per group (2 or 3)
-  int32_t two_d;  // 1: two accumulator regions per group (next tile's layer 0 overlaps)
+  int32_t engines;  // tile engines per CTA (1..kMaxEngines); blockDim.x = 128 * engines
+  int32_t tcols;    // TMEM columns per engine (accumulator W + hidden A W/2)
   int32_t sm_bias, sm_headw, sm_headb, sm_b2pi, sm_lat, sm_hx;  // float offsets in the small region
 };
 
@@ -180,14 +183,9 @@ __device__ __forceinline__ void st_shared_b32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-// Warp roles of mlp_eval_kernel: producer warps build Fourier-feature chunks
-// into a shared-memory ring, one MMA warp issues every tcgen05.mma, and two
-// epilogue warpgroups (one TMEM lane quadrant per warp) own alternate tiles.
-constexpr int kProdWarps = 4;
-constexpr int kEpiGroups = 2;
-constexpr int kMmaWarp = kProdWarps + 4 * kEpiGroups;  // warp 12
-constexpr int kEvalThreads = 32 * (kMmaWarp + 1);      // 416
-constexpr int kMaxRing = 8;
+constexpr int kMaxEngines = 3;
+constexpr int kSlots = 2;   // feature chunk slots per engine
+constexpr int kEvalThreads = 128 * kMaxEngines;  // largest block (384)
 
 // ACT: the hidden activation of every net in the launch (a container's nets
 // share one TrainConfig activation), so the epilogue has no per-element branch
@@ -196,21 +194,43 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
 
 #ifdef NVDB_MLP_KERNEL_TU  // defined in exactly one translation unit (eval.cu)
 
-// Pipeline (per CTA, persistent over a contiguous range of tiles):
-//   producers --ring full--> MMA warp --ring empty--> producers
-//   MMA warp --layer-0 done[e][r] / hidden done[e]--> epilogue group e
-//   epilogue e --hidden A full[e] / region free[e][r]--> MMA warp
-// The j-th non-empty tile of the CTA belongs to epilogue group j & 1; with
-// `two_d` each group alternates two TMEM accumulator regions, so layer 0 of
-// its next tile runs while it finishes the current one.  Hidden activations
-// go back to TMEM as the fp16 A operand of the next layer (tcgen05.st).
+#ifdef NVDB_TRACE
+// debug timeline of CTA 0 (trace build only): per warp a contiguous run of
+// g_trace_cap records {clock64, ev << 32 | tile << 8 | warp}; no atomics
+__device__ unsigned long long* g_trace = nullptr;
+__device__ unsigned int g_trace_cap = 0;
+__device__ unsigned int g_trace_n = 0;
+#define TRC(ev, j)                                                                             \
+  do {                                                                                         \
+    if (blockIdx.x == 0 && g_trace && trc_n < g_trace_cap) {                                   \
+      unsigned long long* _r = g_trace + 2ull * ((threadIdx.x >> 5) * g_trace_cap + trc_n++);  \
+      _r[0] = clock64();                                                                       \
+      _r[1] = ((unsigned long long)(ev) << 32) | ((unsigned)(j) << 8) | (unsigned)(threadIdx.x >> 5); \
+    }                                                                                          \
+  } while (0)
+#define TRC_DECL unsigned int trc_n = 0
+#else
+#define TRC(ev, j) \
+  do {             \
+  } while (0)
+#define TRC_DECL
+#endif
+
+// Per engine g (barriers at bars + 1 + 8 g): [0, kSlots) chunk slot free
+// (MMA commit), [kSlots] layer done (MMA commit), [kSlots + 1] start (the
+// previous engine has issued its first tile's layer 0; staggers the engines
+// so one engine's feature phase overlaps another's MMA/epilogue phases).  Named barrier 1 + g syncs the
+// engine's 128 threads before its elected thread issues MMAs.
 template <int ACT>
 __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  TRC_DECL;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int lane = tid & 31;
-  const int nb = a.nbuf;
+  const int g = tid >> 7;    // engine
+  const int p = tid & 127;   // point row = TMEM lane (engine warps are 4g..4g+3)
+  const int E = a.engines;
+  const int nthreads = 128 * E;
 
   uint8_t* wsm = smem + a.w_off;
   float* small = reinterpret_cast<float*>(smem + a.small_off);
@@ -220,39 +240,31 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   float* s_b2pi = small + a.sm_b2pi;
   float* s_lat = small + a.sm_lat;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-  uint64_t* wbar = bars;            // weights landed
-  uint64_t* rfull = bars + 1;       // [kMaxRing] feature chunk written (128 producer arrivals)
-  uint64_t* rempty = bars + 9;      // [kMaxRing] chunk consumed (MMA commit)
-  // per epilogue group e at bars + 17 + 8 e: [0,1] layer 0 done per region,
-  // [2] hidden layer done, [3] hidden A written (128), [4,5] region free (128)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 40);
+  uint64_t* wbar = bars;                    // weights landed
+  uint64_t* slot_free = bars + 1 + 8 * g;  // [kSlots]
+  uint64_t* mdone = slot_free + kSlots;    // layer MMAs complete
+  uint64_t* start_next = bars + 1 + 8 * (g + 1) + kSlots + 1;  // engine g+1 may start
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
   __shared__ NetDev s_net;
   __shared__ ExpertDev s_exp;
 
   if (tid == 0) {
     mbar_init(wbar, 1);
-    for (int i = 0; i < kMaxRing; ++i) {
-      mbar_init(rfull + i, 32 * kProdWarps);
-      mbar_init(rempty + i, 1);
-    }
-    for (int e = 0; e < kEpiGroups; ++e) {
-      uint64_t* b = bars + 17 + 8 * e;
-      mbar_init(b + 0, 1);
-      mbar_init(b + 1, 1);
-      mbar_init(b + 2, 1);
-      mbar_init(b + 3, 128);
-      mbar_init(b + 4, 128);
-      mbar_init(b + 5, 128);
+    for (int e = 0; e < E; ++e) {
+      for (int s = 0; s < kSlots + 2; ++s) mbar_init(bars + 1 + 8 * e + s, 1);
     }
     fence_barrier_init();
   }
-  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t ring_s = smem_addr(smem + a.region_off);
+  const uint32_t ring = smem_addr(smem + a.region_off) + (uint32_t)(g * kSlots * kChunkBytes);
   const uint32_t w_s = smem_addr(wsm);
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t dcol = tmem_base + (uint32_t)(g * a.tcols);
+  const bool issuer = p == 0;
 
   const int npairs = a.npairs_dev ? *a.npairs_dev : a.npairs;
   const int per_cta = (npairs + gridDim.x - 1) / gridDim.x;
@@ -273,8 +285,8 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     return tl;
   };
 
-  // ---- weight switch: every thread of the CTA, at the same tile, after all
-  // work with the previous net has drained
+  // ---- weight switch: every thread of the CTA, at the same point of the
+  // round sequence; each engine has drained its MMAs before it gets here
   int loaded = -1;
   uint32_t wphase = 0;
   auto load_net = [&](int net) {
@@ -290,12 +302,12 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     __syncthreads();
     {
       const NetDev& nd = s_net;
-      for (int i = tid; i < nd.depth * nd.width; i += kEvalThreads) s_bias[i] = nd.bias[i];
-      for (int i = tid; i < nd.out_dim * nd.width; i += kEvalThreads) s_headw[i] = nd.headw[i];
+      for (int i = tid; i < nd.depth * nd.width; i += nthreads) s_bias[i] = nd.bias[i];
+      for (int i = tid; i < nd.out_dim * nd.width; i += nthreads) s_headw[i] = nd.headw[i];
       if (tid < nd.out_dim) s_headb[tid] = nd.headb[tid];
-      for (int i = tid; i < 3 * (nd.k0 / 2); i += kEvalThreads) s_b2pi[i] = nd.b2pi[i];
+      for (int i = tid; i < 3 * (nd.k0 / 2); i += nthreads) s_b2pi[i] = nd.b2pi[i];
       if (nd.lat)
-        for (int i = tid; i < nd.k0; i += kEvalThreads) s_lat[i] = nd.lat[i];
+        for (int i = tid; i < nd.k0; i += nthreads) s_lat[i] = nd.lat[i];
     }
     mbar_wait(wbar, wphase);
     wphase ^= 1u;
@@ -303,410 +315,344 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     loaded = net;
   };
 
-  if (warp < kProdWarps) {
-    // =============================================================== producers
-    const int pt = tid;  // 0..127
-    int slot = 0;
-    uint32_t rphase = 0;
-    for (int t = t_begin; t < t_end; ++t) {
-      const Tile tile = tile_at(t);
-      if (tile.count <= 0) continue;
-      if (tile.net != loaded) load_net(tile.net);
-      const int k0 = s_net.k0, mp = k0 >> 1, nch = k0 / kChunkK;
-      const bool lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat &&
-                           tile.count == kTileM && (tile.first & (kTileM - 1)) == 0;
-      const double is = s_exp.inv_scale;
-      float x0 = 0.f, x1 = 0.f, x2 = 0.f;
-      // lattice role: z = lk, feature quad lpg, x = lii; 8 y rows each
-      const int lk = pt & 7, lpg = (pt >> 3) & 7, lii = pt >> 6;
-      if (lattice) {
-        const int* o = static_cast<const int*>(a.src) + 3 * (tile.first >> 9);
-        const int i0 = (int)((tile.first & 511) >> 6);
-        x0 = __double2float_rn((o[0] + i0 + lii + 0.5 - s_exp.norm_origin[0]) * is);
-        x1 = __double2float_rn((o[1] + 0.5 - s_exp.norm_origin[1]) * is);
-        x2 = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) * is);
-      } else if (pt < tile.count) {
-        const int64_t pos = tile.first + pt;
-        const int64_t id = a.idx ? a.idx[pos] : pos;
-        const int64_t sid = a.gather ? a.gather[id] : id;
-        double cc[3];
-        if (point_centre(a.src_kind, a.src, sid, cc)) {
-          x0 = __double2float_rn((cc[0] - s_exp.norm_origin[0]) * is);
-          x1 = __double2float_rn((cc[1] - s_exp.norm_origin[1]) * is);
-          x2 = __double2float_rn((cc[2] - s_exp.norm_origin[2]) * is);
-        } else {
-          const float* sp = static_cast<const float*>(a.src) + 3 * sid;
-          x0 = sp[0]; x1 = sp[1]; x2 = sp[2];
-        }
+  // stagger the engines' first tiles when the first round is uniform (all E
+  // tiles non-empty, one net), so no engine can be left waiting for a start
+  // signal across a weight switch
+  bool stagger = false;
+  if (E > 1 && t_end - t_begin >= E) {
+    stagger = true;
+    const Tile t0 = tile_at(t_begin);
+    for (int k = 0; k < E; ++k) {
+      const Tile u = tile_at(t_begin + k);
+      stagger = stagger && u.count > 0 && u.net == t0.net;
+    }
+  }
+  const bool wait_start = stagger && g > 0;
+
+  uint32_t cc = 0;    // feature chunks this engine has written (slot = cc % kSlots)
+  uint32_t mpar = 0;  // parity of the engine's next layer-done phase
+  constexpr int act = ACT;
+
+  auto process = [&](const Tile& tile, int t) {
+    const int k0 = s_net.k0, mp = k0 >> 1, nch = k0 / kChunkK;
+    const int width = s_net.width, depth = s_net.depth, out_dim = s_net.out_dim;
+    const uint32_t acol = dcol + (uint32_t)width;
+    const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
+    const uint64_t bdesc0 = smem_desc(w_s, width * 16, 128);
+    const uint32_t bstep = (uint32_t)(width >> 3) * 16u;  // (2 core-matrix columns * width/8 * 128 B) >> 4
+    const bool lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat &&
+                         tile.count == kTileM && (tile.first & (kTileM - 1)) == 0;
+    const double is = s_exp.inv_scale;
+    // ------------------------------------------------ feature inputs
+    float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+    // lattice role: z = lk, feature quad lpg, x = lii; 8 y rows each
+    const int lk = p & 7, lpg = (p >> 3) & 7, lii = p >> 6;
+    if (lattice) {
+      const int* o = static_cast<const int*>(a.src) + 3 * (tile.first >> 9);
+      const int i0 = (int)((tile.first & 511) >> 6);
+      x0 = __double2float_rn((o[0] + i0 + lii + 0.5 - s_exp.norm_origin[0]) * is);
+      x1 = __double2float_rn((o[1] + 0.5 - s_exp.norm_origin[1]) * is);
+      x2 = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) * is);
+    } else if (p < tile.count) {
+      const int64_t pos = tile.first + p;
+      const int64_t id = a.idx ? a.idx[pos] : pos;
+      const int64_t sid = a.gather ? a.gather[id] : id;
+      double cc3[3];
+      if (point_centre(a.src_kind, a.src, sid, cc3)) {
+        x0 = __double2float_rn((cc3[0] - s_exp.norm_origin[0]) * is);
+        x1 = __double2float_rn((cc3[1] - s_exp.norm_origin[1]) * is);
+        x2 = __double2float_rn((cc3[2] - s_exp.norm_origin[2]) * is);
+      } else {
+        const float* sp = static_cast<const float*>(a.src) + 3 * sid;
+        x0 = sp[0]; x1 = sp[1]; x2 = sp[2];
       }
-      for (int ch = 0; ch < nch; ++ch) {
-        mbar_wait(rempty + slot, rphase ^ 1u);
-        const uint32_t buf = ring_s + slot * kChunkBytes;
-        if (lattice) {
-          // 4 features x 8 y rows: one sincos, one rotation by exp(i beta),
-          // then the Chebyshev recurrence u_{j+1} = 2 cos(beta) u_j - u_{j-1}
-          const int f0 = ch * (kChunkK / 2) + lpg * 4;
+    }
+    // ------------------------------------------------ layer 0: features -> MMA per chunk
+    for (int ch = 0; ch < nch; ++ch, ++cc) {
+      const uint32_t s = cc % kSlots;
+      if (cc >= kSlots) mbar_wait(slot_free + s, ((cc / kSlots) - 1) & 1u);
+      const uint32_t buf = ring + s * kChunkBytes;
+      if (lattice) {
+        // 4 features x 8 y rows: one sincos, one rotation by exp(i beta),
+        // then the Chebyshev recurrence u_{j+1} = 2 cos(beta) u_j - u_{j-1}
+        const int f0 = ch * (kChunkK / 2) + lpg * 4;
+        const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
+        const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
+        const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
+        const float4 la = *reinterpret_cast<const float4*>(s_lat + 2 * f0);
+        const float4 lb = *reinterpret_cast<const float4*>(s_lat + 2 * f0 + 4);
+        const float bxa[4] = {bx.x, bx.y, bx.z, bx.w}, bya[4] = {by.x, by.y, by.z, by.w};
+        const float bza[4] = {bz.x, bz.y, bz.z, bz.w};
+        const float cba[4] = {la.x, la.z, lb.x, lb.z}, sba[4] = {la.y, la.w, lb.y, lb.w};
+        float cs[4][2], sn[4][2], c2[4];
+        uint32_t hp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float th = fmaf(x2, bza[q], fmaf(x1, bya[q], x0 * bxa[q]));
+          __sincosf(th, &sn[q][0], &cs[q][0]);
+          cs[q][1] = fmaf(cs[q][0], cba[q], -sn[q][0] * sba[q]);
+          sn[q][1] = fmaf(cs[q][0], sba[q], sn[q][0] * cba[q]);
+          c2[q] = 2.0f * cba[q];
+          hp[q] = pack_half2(cs[q][0], sn[q][0]);
+        }
+        st_shared_v4(buf + kmajor_offset(lii * 64 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) hp[q] = pack_half2(cs[q][1], sn[q][1]);
+        st_shared_v4(buf + kmajor_offset(lii * 64 + 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
+#pragma unroll
+        for (int jy = 2; jy < 8; ++jy) {
+          const int cur = jy & 1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            cs[q][cur] = fmaf(c2[q], cs[q][cur ^ 1], -cs[q][cur]);
+            sn[q][cur] = fmaf(c2[q], sn[q][cur ^ 1], -sn[q][cur]);
+            hp[q] = pack_half2(cs[q][cur], sn[q][cur]);
+          }
+          st_shared_v4(buf + kmajor_offset(lii * 64 + jy * 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int f0 = ch * (kChunkK / 2) + q * 4;
           const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
           const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
           const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
-          const float4 la = *reinterpret_cast<const float4*>(s_lat + 2 * f0);
-          const float4 lb = *reinterpret_cast<const float4*>(s_lat + 2 * f0 + 4);
           const float bxa[4] = {bx.x, bx.y, bx.z, bx.w}, bya[4] = {by.x, by.y, by.z, by.w};
           const float bza[4] = {bz.x, bz.y, bz.z, bz.w};
-          const float cba[4] = {la.x, la.z, lb.x, lb.z}, sba[4] = {la.y, la.w, lb.y, lb.w};
-          float cs[4][2], sn[4][2], c2[4];
-          uint32_t hp[4];
+          uint32_t h[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float th = fmaf(x2, bza[q], fmaf(x1, bya[q], x0 * bxa[q]));
-            __sincosf(th, &sn[q][0], &cs[q][0]);
-            cs[q][1] = fmaf(cs[q][0], cba[q], -sn[q][0] * sba[q]);
-            sn[q][1] = fmaf(cs[q][0], sba[q], sn[q][0] * cba[q]);
-            c2[q] = 2.0f * cba[q];
-            hp[q] = pack_half2(cs[q][0], sn[q][0]);
+          for (int j = 0; j < 4; ++j) {
+            const float th = fmaf(x2, bza[j], fmaf(x1, bya[j], x0 * bxa[j]));
+            float sv, cv;
+            __sincosf(th, &sv, &cv);
+            h[j] = pack_half2(cv, sv);
           }
-          st_shared_v4(buf + kmajor_offset(lii * 64 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) hp[q] = pack_half2(cs[q][1], sn[q][1]);
-          st_shared_v4(buf + kmajor_offset(lii * 64 + 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
-#pragma unroll
-          for (int jy = 2; jy < 8; ++jy) {
-            const int cur = jy & 1;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              cs[q][cur] = fmaf(c2[q], cs[q][cur ^ 1], -cs[q][cur]);
-              sn[q][cur] = fmaf(c2[q], sn[q][cur ^ 1], -sn[q][cur]);
-              hp[q] = pack_half2(cs[q][cur], sn[q][cur]);
-            }
-            st_shared_v4(buf + kmajor_offset(lii * 64 + jy * 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2],
-                         hp[3]);
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int f0 = ch * (kChunkK / 2) + q * 4;
-            const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
-            const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
-            const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
-            const float bxa[4] = {bx.x, bx.y, bx.z, bx.w}, bya[4] = {by.x, by.y, by.z, by.w};
-            const float bza[4] = {bz.x, bz.y, bz.z, bz.w};
-            uint32_t h[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float th = fmaf(x2, bza[j], fmaf(x1, bya[j], x0 * bxa[j]));
-              float sv, cv;
-              __sincosf(th, &sv, &cv);
-              h[j] = pack_half2(cv, sv);
-            }
-            st_shared_v4(buf + kmajor_offset(pt, q * 8, kTileM), h[0], h[1], h[2], h[3]);
-          }
+          st_shared_v4(buf + kmajor_offset(p, q * 8, kTileM), h[0], h[1], h[2], h[3]);
         }
-        fence_async_smem();
-        mbar_arrive(rfull + slot);
-        if (++slot == nb) {
-          slot = 0;
-          rphase ^= 1u;
-        }
+      }
+      fence_async_smem();
+      named_bar_sync(1 + g, 128);
+      if (issuer) {
+        tc_fence_after();
+        // descriptors: start-address field += byte offset >> 4 (no carry: smem < 256 KB);
+        // one K = 16 step = 2 core-matrix columns of the operand
+        const uint64_t ad = smem_desc(buf, kTileM * 16, 128);
+        const uint64_t bd = bdesc0 + (uint64_t)(ch * 4 * bstep);
+        umma_f16(dcol, ad, bd, idesc, ch != 0);
+        umma_f16(dcol, ad + 256, bd + bstep, idesc, 1);
+        umma_f16(dcol, ad + 512, bd + 2 * bstep, idesc, 1);
+        umma_f16(dcol, ad + 768, bd + 3 * bstep, idesc, 1);
+        umma_commit(slot_free + s);
+        if (ch == nch - 1) umma_commit(mdone);
       }
     }
-  } else if (warp < kMmaWarp) {
-    // =============================================================== epilogue
-    const int e = (warp - kProdWarps) >> 2;
-    const int quad = warp & 3;  // TMEM lane quadrant (hardware: warp id % 4)
-    const int row = quad * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    uint64_t* eb = bars + 17 + 8 * e;
-    const uint32_t ecol = tmem_base + (uint32_t)(e * 256);
-    uint32_t l0par = 0, hpar = 0;
-    int j = 0;
-    constexpr int act = ACT;
-    for (int t = t_begin; t < t_end; ++t) {
-      const Tile tile = tile_at(t);
-      if (tile.count <= 0) continue;
-      if (tile.net != loaded) load_net(tile.net);
-      const int mine = (j & 1) == e;
-      const int jj = j >> 1;
-      ++j;
-      if (!mine) continue;
-      const int width = s_net.width, depth = s_net.depth, out_dim = s_net.out_dim;
-      const int r = a.two_d ? (jj & 1) : 0;
-      const uint32_t dcol = ecol + (uint32_t)(r * width);
-      const uint32_t acol = ecol + (a.two_d ? 2u : 1u) * (uint32_t)width;
-      // row set-up (outputs, gate weight)
-      const bool valid = row < tile.count;
-      const int64_t pos = tile.first + (valid ? row : 0);
-      const int64_t id = a.idx ? a.idx[pos] : pos;
-      double gwt = 1.0;
-      if (a.src_kind != SRC_NORM_F32) {
-        const int64_t sid = a.gather ? a.gather[id] : id;
-        double cc[3];
-        point_centre(a.src_kind, a.src, sid, cc);
-        gwt = gate_weight(s_exp.cell, a.subdomain_size, a.halo, cc);
-      }
-      float y[kMaxOut] = {0.f, 0.f, 0.f};
-      for (int l = 0; l < depth; ++l) {
-        const bool last = (l == depth - 1);
-        if (l == 0) {
-          mbar_wait(eb + r, (l0par >> r) & 1u);
-          l0par ^= 1u << r;
-        } else {
-          mbar_wait(eb + 2, hpar);
-          hpar ^= 1u;
-        }
-        tc_fence_after();
-        const float* bl = s_bias + l * width;
-        auto epi = [&](int cc, const float (&v)[16]) {
+    if (stagger) {
+      stagger = false;
+      if (issuer && g + 1 < E) mbar_arrive(start_next);
+    }
+    if (issuer) TRC(1, t);
+    // ------------------------------------------------ hidden layers + head
+    float y[kMaxOut] = {0.f, 0.f, 0.f};
+    for (int l = 0; l < depth; ++l) {
+      const bool last = (l == depth - 1);
+      mbar_wait(mdone, mpar);
+      mpar ^= 1u;
+      tc_fence_after();
+      if (issuer) TRC(2 + l, t);
+      const float* bl = s_bias + l * width;
+      // batches of NB 16-column TMEM loads, then straight-line bias /
+      // activation / pack (no branches inside a batch, so the MUFU ops of one
+      // group overlap the packing and stores of the previous one)
+      auto batch = [&](auto nb_c, auto last_c, int c0) {
+        constexpr int NB = decltype(nb_c)::value;
+        constexpr bool LAST = decltype(last_c)::value;
+        float v[NB][16];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) tmem_ld16(dcol + lane_off + (c0 + b) * 16, v[b]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
           float av[16];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 bq = reinterpret_cast<const float4*>(bl + cc * 16)[q];
-            av[4 * q + 0] = act_fn(act, v[4 * q + 0] + bq.x);
-            av[4 * q + 1] = act_fn(act, v[4 * q + 1] + bq.y);
-            av[4 * q + 2] = act_fn(act, v[4 * q + 2] + bq.z);
-            av[4 * q + 3] = act_fn(act, v[4 * q + 3] + bq.w);
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 bq = reinterpret_cast<const float4*>(bl + (c0 + b) * 16)[q4];
+            av[4 * q4 + 0] = act_fn(act, v[b][4 * q4 + 0] + bq.x);
+            av[4 * q4 + 1] = act_fn(act, v[b][4 * q4 + 1] + bq.y);
+            av[4 * q4 + 2] = act_fn(act, v[b][4 * q4 + 2] + bq.z);
+            av[4 * q4 + 3] = act_fn(act, v[b][4 * q4 + 3] + bq.w);
           }
-          if (!last) {
+          if constexpr (!LAST) {
             uint32_t hp[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) hp[i] = pack_half2(av[2 * i], av[2 * i + 1]);
-            tmem_st8(acol + lane_off + cc * 8, hp);
+            for (int i2 = 0; i2 < 8; ++i2) hp[i2] = pack_half2(av[2 * i2], av[2 * i2 + 1]);
+            tmem_st8(acol + lane_off + (c0 + b) * 8, hp);
           } else {
 #pragma unroll
             for (int k = 0; k < kMaxOut; ++k) {
               if (k < out_dim) {
-                const float4* hw = reinterpret_cast<const float4*>(s_headw + k * width + cc * 16);
-                float sacc = y[k];
+                const float4* hw = reinterpret_cast<const float4*>(s_headw + k * width + (c0 + b) * 16);
+                float sp[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float4 w4 = hw[q];
-                  sacc = fmaf(av[4 * q], w4.x, sacc);
-                  sacc = fmaf(av[4 * q + 1], w4.y, sacc);
-                  sacc = fmaf(av[4 * q + 2], w4.z, sacc);
-                  sacc = fmaf(av[4 * q + 3], w4.w, sacc);
+                for (int q4 = 0; q4 < 4; ++q4) {  // four short partial sums
+                  const float4 w4 = hw[q4];
+                  sp[q4] = fmaf(av[4 * q4], w4.x, av[4 * q4 + 1] * w4.y);
+                  sp[q4] = fmaf(av[4 * q4 + 2], w4.z, sp[q4]);
+                  sp[q4] = fmaf(av[4 * q4 + 3], w4.w, sp[q4]);
                 }
-                y[k] = sacc;
+                y[k] += (sp[0] + sp[1]) + (sp[2] + sp[3]);
               }
             }
           }
-        };
-        // up to three 16-column TMEM loads in flight per wait
-        const int ncc = width / 16;
-        for (int c0 = 0; c0 < ncc; c0 += 3) {
-          const int m = min(3, ncc - c0);
-          float v0[16], v1[16], v2[16];
-          tmem_ld16(dcol + lane_off + c0 * 16, v0);
-          if (m > 1) tmem_ld16(dcol + lane_off + (c0 + 1) * 16, v1);
-          if (m > 2) tmem_ld16(dcol + lane_off + (c0 + 2) * 16, v2);
-          tmem_ld_wait();
-          epi(c0, v0);
-          if (m > 1) epi(c0 + 1, v1);
-          if (m > 2) epi(c0 + 2, v2);
         }
-        if (!last) {
-          tmem_st_wait();
-          tc_fence_before();
-          mbar_arrive(eb + 3);
-        } else {
-          tc_fence_before();
-          mbar_arrive(eb + 4 + r);
-        }
-      }
-      if (!valid) continue;
-#pragma unroll
-      for (int k = 0; k < kMaxOut; ++k)
-        if (k < out_dim) y[k] = y[k] + s_headb[k];
-
-      // ------------------------------------------------ output
-      if (a.out_mode == OUT_RAW) {
-#pragma unroll
-        for (int k = 0; k < kMaxOut; ++k)
-          if (k < out_dim) a.out_raw[id * out_dim + k] = y[k];
-        continue;
-      }
-      // transform (inference.py:29-36) in float32
-      float tv[kMaxOut];
-      const int head = s_net.head;
-      tv[1] = tv[2] = 0.f;
-      if (head == HEAD_LOGITS) {  // 3-way softmax (l1 classifier heads are always 3 wide)
-        const float zm = fmaxf(fmaxf(y[0], y[1]), y[2]);
-        const float e0 = expf(y[0] - zm), e1 = expf(y[1] - zm), e2 = expf(y[2] - zm);
-        const float ssum = (e0 + e1) + e2;
-        tv[0] = e0 / ssum; tv[1] = e1 / ssum; tv[2] = e2 / ssum;
-      } else if (head == HEAD_BINARY) {
-        tv[0] = 1.0f / (1.0f + expf(-y[0]));
-      } else {
-        tv[0] = y[0];
-      }
-      // gate-weighted accumulation (partition.py:245-256), f64, sid order = pass order
-      double num[kMaxOut], den;
-      const int kk = out_dim;
-#pragma unroll
-      for (int k = 0; k < kMaxOut; ++k) num[k] = gwt > 0.0 ? (double)tv[k] * gwt : 0.0;
-      den = gwt > 0.0 ? gwt : 0.0;
-      bool is_first = (tile.flags & TF_FIRST) != 0, is_last = (tile.flags & TF_LAST) != 0;
-      if (a.ncand) {
-        is_first = a.pass == 0;
-        is_last = (int)a.ncand[id] == a.pass + 1;
-      }
-      if (!is_first) {
-        const double* ac = a.acc + 4 * id;
-#pragma unroll
-        for (int k = 0; k < kMaxOut; ++k) num[k] = ac[k] + num[k];
-        den = ac[3] + den;
-      }
-      if (!is_last) {
-        double* ac = a.acc + 4 * id;
-#pragma unroll
-        for (int k = 0; k < kMaxOut; ++k) ac[k] = num[k];
-        ac[3] = den;
-        continue;
-      }
-      const bool covered = den > 0.0;
-      if (covered) {
-#pragma unroll
-        for (int k = 0; k < kMaxOut; ++k) num[k] = num[k] / den;
-      }
-      switch (a.out_mode) {
-        case OUT_PROBS:
-#pragma unroll
-          for (int k = 0; k < kMaxOut; ++k)
-            if (k < kk) a.out_probs[id * kk + k] = covered ? num[k] : 0.0;
-          a.out_u8[id] = covered ? 1 : 0;
-          break;
-        case OUT_L1CLASS: {
-          int best = 0;
-          if (num[1] > num[best]) best = 1;
-          if (num[2] > num[best]) best = 2;
-          a.out_u8[id] = covered ? (uint8_t)best : (uint8_t)2;
-          break;
-        }
-        case OUT_L0ACTIVE:
-          a.out_u8[id] = (covered && num[0] > 0.5) ? 1 : 0;
-          break;
-        default: {  // OUT_VALUE
-          double v = num[0];
-          if (a.clip) v = fmin(fmax(v, -1.0), 1.0);
-          a.out_f32[id] = covered ? (float)(v * a.value_scale) : a.background;
-          break;
+      };
+      const int ncc = width / 16;
+      auto run_layer = [&](auto last_c) {
+        int c0 = 0;
+        for (; c0 + 3 <= ncc; c0 += 3) batch(std::integral_constant<int, 3>{}, last_c, c0);
+        for (; c0 < ncc; ++c0) batch(std::integral_constant<int, 1>{}, last_c, c0);
+      };
+      if (last) run_layer(std::true_type{});
+      else run_layer(std::false_type{});
+      tc_fence_before();
+      if (!last) {
+        tmem_st_wait();
+        tc_fence_before();
+        named_bar_sync(1 + g, 128);
+        if (issuer) {
+          tc_fence_after();
+          uint64_t bd = smem_desc(w_s + (uint32_t)(width * k0 * 2 + l * width * width * 2), width * 16, 128);
+          umma_f16_ts(dcol, acol, bd, idesc, 0);
+          for (int k = 1; k < width / 16; ++k) {
+            bd += bstep;
+            umma_f16_ts(dcol, acol + k * 8, bd, idesc, 1);
+          }
+          umma_commit(mdone);
         }
       }
     }
-  } else {
-    // =============================================================== MMA warp
-    // all lanes run the schedule; lane 0 issues.  Readiness is probed without
-    // blocking so hidden-layer jobs of one group never wait behind layer 0 of
-    // the other group's tile.
-    const bool leader = lane == 0;
-    int slot = 0;
-    uint32_t rphase = 0;
-    int qn[kEpiGroups] = {0, 0};            // tiles with hidden layers outstanding
-    int qr[kEpiGroups][2] = {{0, 0}, {0, 0}};  // their accumulator regions (FIFO)
-    int hl[kEpiGroups] = {1, 1};            // next hidden layer of the oldest one
-    uint32_t apar = 0;                      // hidden-A full parity per group (bit e)
-    uint32_t duse[kEpiGroups][2] = {{0, 0}, {0, 0}};  // layer-0 uses per region
-    int t = t_begin, j = 0;
-    bool l0_active = false;
-    int ce = 0, cr = 0, ch = 0, nch = 0;
-    while (true) {
-      const int width = s_net.width, depth = s_net.depth;
-      // ---- hidden layers (A operand from TMEM, B = W_l from shared memory)
-      if (depth > 1) {
+    if (issuer) TRC(9, t);
+    // ------------------------------------------------ outputs
+    if (p >= tile.count) return;
+    const int64_t pos = tile.first + p;
+    const int64_t id = a.idx ? a.idx[pos] : pos;
 #pragma unroll
-        for (int e = 0; e < kEpiGroups; ++e) {
-          if (qn[e] > 0 && mbar_test(bars + 17 + 8 * e + 3, (apar >> e) & 1u)) {
-            apar ^= 1u << e;
-            tc_fence_after();
-            const int l = hl[e];
-            const uint32_t ecol = tmem_base + (uint32_t)(e * 256);
-            const uint32_t dcol = ecol + (uint32_t)(qr[e][0] * width);
-            const uint32_t acol = ecol + (a.two_d ? 2u : 1u) * (uint32_t)width;
-            if (leader) {
-              const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
-              const uint32_t wl = w_s + (uint32_t)(width * s_net.k0 * 2 + (l - 1) * width * width * 2);
-              for (int s = 0; s < width / 16; ++s) {
-                const uint64_t bd = smem_desc(wl + (uint32_t)(s * 2 * (width >> 3) * 128), width * 16, 128);
-                umma_f16_ts(dcol, acol + s * 8, bd, idesc, s != 0);
-              }
-              umma_commit(bars + 17 + 8 * e + 2);
-            }
-            __syncwarp();
-            if (++hl[e] == depth) {
-              hl[e] = 1;
-              qr[e][0] = qr[e][1];
-              --qn[e];
-            }
-          }
-        }
-      }
-      // ---- layer 0 of the next tile
-      if (!l0_active) {
-        Tile tile;
-        tile.count = 0;
-        while (t < t_end) {
-          tile = tile_at(t);
-          if (tile.count > 0) break;
-          ++t;
-        }
-        if (t >= t_end) {
-          if (qn[0] == 0 && qn[1] == 0) break;
-          continue;
-        }
-        if (tile.net != loaded) {
-          if (qn[0] != 0 || qn[1] != 0) continue;  // drain before the weight switch
-          load_net(tile.net);
-          continue;
-        }
-        const int e = j & 1, jj = j >> 1;
-        const int r = a.two_d ? (jj & 1) : 0;
-        const int cap = a.two_d ? 2 : 1;
-        if (depth > 1 && qn[e] >= cap) continue;
-        if (duse[e][r] > 0 && !mbar_test(bars + 17 + 8 * e + 4 + r, (duse[e][r] - 1) & 1u)) continue;
-        ++duse[e][r];
-        l0_active = true;
-        ce = e;
-        cr = r;
-        ch = 0;
-        nch = s_net.k0 / kChunkK;
-      }
-      const uint32_t dcol = tmem_base + (uint32_t)(ce * 256 + cr * width);
-      while (ch < nch && mbar_test(rfull + slot, rphase)) {
-        tc_fence_after();
-        if (leader) {
-          const uint32_t buf = ring_s + slot * kChunkBytes;
-          const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
+    for (int k = 0; k < kMaxOut; ++k)
+      if (k < out_dim) y[k] = y[k] + s_headb[k];
+    if (a.out_mode == OUT_RAW) {
 #pragma unroll
-          for (int s = 0; s < kChunkK / 16; ++s) {
-            const uint64_t ad = smem_desc(buf + s * (2 * kTileM * 16), kTileM * 16, 128);
-            const uint32_t wb = w_s + (uint32_t)(((ch * kChunkK + s * 16) >> 3) * (width >> 3) * 128);
-            umma_f16(dcol, ad, smem_desc(wb, width * 16, 128), idesc, (ch | s) != 0);
-          }
-          umma_commit(rempty + slot);
-        }
-        __syncwarp();
-        if (++slot == nb) {
-          slot = 0;
-          rphase ^= 1u;
-        }
-        ++ch;
+      for (int k = 0; k < kMaxOut; ++k)
+        if (k < out_dim) a.out_raw[id * out_dim + k] = y[k];
+      return;
+    }
+    double gwt = 1.0;
+    if (a.src_kind != SRC_NORM_F32) {
+      const int64_t sid = a.gather ? a.gather[id] : id;
+      double c3[3];
+      point_centre(a.src_kind, a.src, sid, c3);
+      gwt = gate_weight(s_exp.cell, a.subdomain_size, a.halo, c3);
+    }
+    // transform (inference.py:29-36) in float32
+    float tv[kMaxOut];
+    const int head = s_net.head;
+    tv[1] = tv[2] = 0.f;
+    if (head == HEAD_LOGITS) {  // 3-way softmax (l1 classifier heads are always 3 wide)
+      const float zm = fmaxf(fmaxf(y[0], y[1]), y[2]);
+      const float e0 = expf(y[0] - zm), e1 = expf(y[1] - zm), e2 = expf(y[2] - zm);
+      const float ssum = (e0 + e1) + e2;
+      tv[0] = e0 / ssum; tv[1] = e1 / ssum; tv[2] = e2 / ssum;
+    } else if (head == HEAD_BINARY) {
+      tv[0] = 1.0f / (1.0f + expf(-y[0]));
+    } else {
+      tv[0] = y[0];
+    }
+    // gate-weighted accumulation (partition.py:245-256), f64, sid order = pass order
+    double num[kMaxOut], den;
+    const int kk = out_dim;
+#pragma unroll
+    for (int k = 0; k < kMaxOut; ++k) num[k] = gwt > 0.0 ? (double)tv[k] * gwt : 0.0;
+    den = gwt > 0.0 ? gwt : 0.0;
+    bool is_first = (tile.flags & TF_FIRST) != 0, is_last = (tile.flags & TF_LAST) != 0;
+    if (a.ncand) {
+      is_first = a.pass == 0;
+      is_last = (int)a.ncand[id] == a.pass + 1;
+    }
+    if (!is_first) {
+      const double* ac = a.acc + 4 * id;
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k) num[k] = ac[k] + num[k];
+      den = ac[3] + den;
+    }
+    if (!is_last) {
+      double* ac = a.acc + 4 * id;
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k) ac[k] = num[k];
+      ac[3] = den;
+      return;
+    }
+    const bool covered = den > 0.0;
+    if (covered) {
+#pragma unroll
+      for (int k = 0; k < kMaxOut; ++k) num[k] = num[k] / den;
+    }
+    switch (a.out_mode) {
+      case OUT_PROBS:
+#pragma unroll
+        for (int k = 0; k < kMaxOut; ++k)
+          if (k < kk) a.out_probs[id * kk + k] = covered ? num[k] : 0.0;
+        a.out_u8[id] = covered ? 1 : 0;
+        break;
+      case OUT_L1CLASS: {
+        int best = 0;
+        if (num[1] > num[best]) best = 1;
+        if (num[2] > num[best]) best = 2;
+        a.out_u8[id] = covered ? (uint8_t)best : (uint8_t)2;
+        break;
       }
-      if (ch == nch) {
-        if (leader) umma_commit(bars + 17 + 8 * ce + cr);
-        __syncwarp();
-        if (depth > 1) {
-          qr[ce][qn[ce]] = cr;
-          ++qn[ce];
-        }
-        l0_active = false;
-        ++j;
-        ++t;
+      case OUT_L0ACTIVE:
+        a.out_u8[id] = (covered && num[0] > 0.5) ? 1 : 0;
+        break;
+      default: {  // OUT_VALUE
+        double v = num[0];
+        if (a.clip) v = fmin(fmax(v, -1.0), 1.0);
+        a.out_f32[id] = covered ? (float)(v * a.value_scale) : a.background;
+        break;
       }
+    }
+  };
+
+  // ---- rounds: engine g takes tile base + g; tiles of one round that need
+  // different nets run as consecutive sub-rounds around a weight switch
+  for (int base = t_begin; base < t_end; base += E) {
+    const int lim = min(E, t_end - base);
+    int k = 0;
+    while (k < lim) {
+      const Tile tk = tile_at(base + k);
+      if (tk.count <= 0) {
+        ++k;
+        continue;
+      }
+      int k2 = k + 1;
+      while (k2 < lim) {
+        const Tile u = tile_at(base + k2);
+        if (u.count > 0 && u.net != tk.net) break;
+        ++k2;
+      }
+      if (tk.net != loaded) load_net(tk.net);
+      if (g >= k && g < k2) {
+        const Tile mine = tile_at(base + g);
+        if (mine.count > 0) {
+          if (wait_start && base == t_begin) mbar_wait(bars + 1 + 8 * g + kSlots + 1, 0);
+          process(mine, base + g);
+        }
+      }
+      k = k2;
     }
   }
 
   // ------------------------------------------------ teardown
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) tmem_dealloc(tmem_base, 512);
+  if (warp == 0) tmem_dealloc(tmem_base, 512);
 }
 #endif  // NVDB_MLP_KERNEL_TU
 

@@ -41,6 +41,24 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 TORUS = dict(major=160.0, minor=64.0, voxel=1.0, half_width=3.0, center=(256.0, 256.0, 256.0))
 
 
+def load_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one L0-stage mlp_eval_kernel
+    launch from the committed ncu --set full capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "r01", "ncu_mlp_eval_c2_l0_v6.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f)[0]
+        unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v, u = rec[k].split()
+            tot += float(v) * unit[u]
+        return {"bytes_per_launch": tot, "launch": "L0 classifier stage, C2 (6,647,296 points)",
+                "source": os.path.relpath(path, ROOT)}
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -169,6 +187,47 @@ def train_container(grid, cfg, dev, timings):
     extract_patches(grid, layout, experts, cfg, dev)
     meta = GridMeta(grid.grid_class, grid.background, grid.voxel_size, grid.half_width, value_scale_of(grid))
     return NeuralGridContainer(meta, build_upper_tree(grid), layout, experts, cfg, 16)
+
+
+def query_bench(m, dev, steps, nq=1 << 27, lo=-32, hi=544, seed=0):
+    """Random-access point queries (SURVEY.md §8(d) C5 shape, on this workload's
+    grid): uniform int32 coords in [lo, hi)^3 through HybridGrid.query_device
+    (lookup K1 + gate-blended voxel regressor on the rows that resolve to an
+    active leaf voxel).  Also times the lookup kernel alone for its HBM
+    roofline (18 B per query: 12 B coords in, f32 value + u8 active + u8 kind out)."""
+    import torch
+    from paper_2208_04448_b200.decoder import HybridGrid
+    hg = HybridGrid(m, m.decode(False))
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    coords = torch.randint(lo, hi, (nq, 3), dtype=torch.int32, device=dev, generator=g)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        ts = []
+        for _ in range(max(steps, 3)):
+            flush.random_(0, 255)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    t_lookup = timed(lambda: hg.tree.lookup(coords))
+    hg.regressor_evaluations = 0
+    t_query = timed(lambda: hg.query_device(coords))
+    evals = hg.regressor_evaluations / (2 + max(steps, 3))
+    bytes_q = 18
+    return {"value": nq / (t_query * 1e-3), "unit": "queries/s", "queries": nq, "ms": t_query,
+            "coords": f"uniform int32 in [{lo},{hi})^3 (torch Philox, seed {seed})",
+            "regressor_rows": int(evals),
+            "lookup": {"ms": t_lookup, "value": nq / (t_lookup * 1e-3), "unit": "queries/s",
+                       "roofline": {"bound": "hbm", "bytes_per_query": bytes_q,
+                                    "achieved": nq * bytes_q / (t_lookup * 1e-3) / 1e9, "unit": "GB/s"}}}
 
 
 def cpu_decode_sample(c, nleaf_sample=400):
@@ -312,6 +371,9 @@ def main():
     launches0 = L.nvdb_launch_count()
     total_ms = 0.0
     m.timer = []
+    prof = os.environ.get("NVDB_PROFILE_DECODE") == "1"  # ncu --profile-from-start off: timed decodes only
+    if prof:
+        torch.cuda.profiler.start()
     for _ in range(args.steps):
         flush.random_(0, 255)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -321,6 +383,8 @@ def main():
         e1.synchronize()
         total_ms += e0.elapsed_time(e1)
     torch.cuda.synchronize()
+    if prof:
+        torch.cuda.profiler.stop()
     launches = (L.nvdb_launch_count() - launches0) / args.steps
     clocks = sampler.stop()
     timer, m.timer = m.timer, None
@@ -342,6 +406,10 @@ def main():
     achieved = kflops / (kms * 1e-3) / 1e12
     peak = float(peaks["bf16_tflops"])
     train_tf = train_flop / (train_ms * 1e-3) / 1e12
+    # ---------------- random-access queries (C5 shape on this grid)
+    query = query_bench(m, dev, args.steps)
+    query["lookup"]["roofline"]["peak"] = float(peaks["hbm_gbs"])
+    query["lookup"]["roofline"]["frac"] = query["lookup"]["roofline"]["achieved"] / float(peaks["hbm_gbs"])
     # ---------------- e2e through the public API (host container -> host grid)
     e2e_t = []
     h2d = sum(w.nbytes + b.nbytes for e in c.experts for _, n in e.nets() if n is not None
@@ -377,10 +445,11 @@ def main():
                       "roofline": {"bound": "tensor", "achieved": train_tf, "peak": float(peaks["bf16_tflops_sustained"]),
                                    "unit": "TFLOP/s", "frac": train_tf / float(peaks["bf16_tflops_sustained"])}},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": src,
+                         "frac": achieved / peak, "traffic": load_traffic(), "peak_source": src,
                          "kernel": "mlp_eval_kernel (all decode stages)", "flops_per_point": flops,
                          "kernel_ms_per_step": kms / args.steps,
                          "per_stage_ms": {k: v[1] / args.steps for k, v in per_tag.items()}},
+            "query": query,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "voxels/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(round(launches)),

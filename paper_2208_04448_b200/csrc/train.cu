@@ -29,6 +29,32 @@
 
 #include "netset.cuh"
 
+#ifdef NVDB_TRACE
+// trace build only: per-warp timeline of CTA 0 of the training kernels
+__device__ unsigned long long* g_ttrace = nullptr;
+__device__ unsigned int g_ttrace_cap = 0;
+#define TTRC(ev, j)                                                                                \
+  do {                                                                                             \
+    if (blockIdx.x == 0 && g_ttrace && (threadIdx.x & 31) == 0 && ttrc_n < g_ttrace_cap) {         \
+      unsigned long long* _r = g_ttrace + 2ull * ((threadIdx.x >> 5) * g_ttrace_cap + ttrc_n++);   \
+      _r[0] = clock64();                                                                           \
+      _r[1] = ((unsigned long long)(ev) << 32) | ((unsigned)(j) << 8) | (unsigned)(threadIdx.x >> 5); \
+    }                                                                                              \
+  } while (0)
+#define TTRC_DECL unsigned int ttrc_n = 0
+extern "C" __attribute__((visibility("default"))) int nvdb_debug_ttrace(void* buf, uint32_t cap) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  cudaMemcpyToSymbol(g_ttrace, &p, sizeof(p));
+  cudaMemcpyToSymbol(g_ttrace_cap, &cap, sizeof(cap));
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : -2;
+}
+#else
+#define TTRC(ev, j) \
+  do {              \
+  } while (0)
+#define TTRC_DECL
+#endif
+
 using namespace nvdb;
 
 namespace {
@@ -181,9 +207,8 @@ __device__ __forceinline__ float act_deriv_from(int act, float zp) {
   return zp > 0.0f ? 1.0f : 0.0f;
 }
 
-__global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  if (*a.stopped) return;
+__device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
+  TTRC_DECL;
   const int tid = threadIdx.x;
   const int grp = tid >> 8;               // tile group (a.nwg groups of 8 warps)
   const int gt = tid & 255;
@@ -213,7 +238,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
     for (uint32_t off = 0; off < nd.wimg_bytes; off += 32768)
       bulk_g2s(wsm + off, nd.wimg + off, min(32768u, nd.wimg_bytes - off), &bars[0]);
   }
-  if (tid < 32) tmem_alloc(tmem_slot, 512);
+  if (tid < 32) tmem_alloc_keep(tmem_slot, 512);
   for (int i = tid; i < depth * width; i += nthreads) s_bias[i] = nd.bias[i];
   for (int i = tid; i < out_dim * width; i += nthreads) s_headw[i] = nd.headw[i];
   if (tid < out_dim) s_headb[tid] = nd.headb[tid];
@@ -240,12 +265,26 @@ __global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
   double loss_acc = 0.0;
   const size_t tile_elems = (size_t)kTileM * width;
 
+  // inputs of this thread's row, loaded one tile ahead (the gather through the
+  // sampled indices is two dependent global loads)
+  auto load_row = [&](int64_t tt, float& x0, float& x1, float& x2, float& y) {
+    const int64_t bb = tt * kTileM + row;
+    if (tt < t1 && bb < a.batch) {
+      const int64_t pi = a.idx ? a.idx[bb] : bb;
+      x0 = a.xs[3 * pi]; x1 = a.xs[3 * pi + 1]; x2 = a.xs[3 * pi + 2];
+      y = a.ys[pi];
+    } else {
+      x0 = x1 = x2 = y = 0.f;
+    }
+  };
+  float nx0, nx1, nx2, ny;
+  load_row(t0 + grp, nx0, nx1, nx2, ny);
   for (int64_t tau = t0 + grp; tau < t1; tau += a.nwg) {
     const int64_t b = tau * kTileM + row;
     const bool valid = b < a.batch;
-    const int64_t pidx = valid ? (a.idx ? a.idx[b] : b) : 0;
-    const float x0 = a.xs[3 * pidx], x1 = a.xs[3 * pidx + 1], x2 = a.xs[3 * pidx + 2];
-    const float y = a.ys[pidx];
+    const float x0 = nx0, x1 = nx1, x2 = nx2, y = ny;
+    load_row(tau + a.nwg, nx0, nx1, nx2, ny);
+    TTRC(1, tau);
     // ---------------- features + layer 0 (as in mlp_eval_kernel)
     const int nch = k0 / kChunkK;
     for (int ch = 0; ch < nch; ++ch) {
@@ -282,10 +321,12 @@ __global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
       }
       if (bsel == 0) { nc0++; pend0 = true; } else { nc1++; pend1 = true; }
     }
+    TTRC(2, tau);
     mbar_wait(bar_layer, nlayer & 1u);
     nlayer++;
     pend0 = pend1 = false;
     tc_fence_after();
+    TTRC(3, tau);
     // ---------------- hidden layers: z_h stays in TMEM columns [h*W, (h+1)*W)
     float yv[3] = {0.f, 0.f, 0.f};
     uint32_t woff = (uint32_t)(width * k0 * 2);
@@ -293,31 +334,47 @@ __global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
       const bool last = (l == depth - 1);
       const float* bl = s_bias + l * width;
       uint16_t* gact = a.act_img + ((size_t)l * ntiles + tau) * tile_elems;
-      for (int cc = half; cc < width / 16; cc += 2) {
-        float v[16];
-        tmem_ld16(tcol + lane_off + l * width + cc * 16, v);
+      // this thread's 16-column groups (cc = half, half + 2, ...), all TMEM loads first
+      const int ncc = width / 16;
+      const int nmine = (ncc - half + 1) / 2;
+      for (int c0 = 0; c0 < nmine; c0 += 2) {
+        const int nb = min(2, nmine - c0);
+        float v[2][16];
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2)
+          if (b2 < nb) tmem_ld16(tcol + lane_off + l * width + (half + 2 * (c0 + b2)) * 16, v[b2]);
         tmem_ld_wait();
-        float av[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) av[i] = act_fn(act, v[i] + bl[cc * 16 + i]);
-        const uint32_t p0 = pack_half2(av[0], av[1]), p1 = pack_half2(av[2], av[3]);
-        const uint32_t p2 = pack_half2(av[4], av[5]), p3 = pack_half2(av[6], av[7]);
-        const uint32_t p4 = pack_half2(av[8], av[9]), p5 = pack_half2(av[10], av[11]);
-        const uint32_t p6 = pack_half2(av[12], av[13]), p7 = pack_half2(av[14], av[15]);
-        const uint32_t o0 = kmajor_offset(row, cc * 16, kTileM), o1 = kmajor_offset(row, cc * 16 + 8, kTileM);
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o0) = make_uint4(p0, p1, p2, p3);
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o1) = make_uint4(p4, p5, p6, p7);
-        if (!last) {
-          st_shared_v4(region_s + o0, p0, p1, p2, p3);
-          st_shared_v4(region_s + o1, p4, p5, p6, p7);
-        } else {
+        for (int b2 = 0; b2 < 2; ++b2) {
+          if (b2 >= nb) break;
+          const int cc = half + 2 * (c0 + b2);
+          float av[16];
 #pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            if (k < out_dim) {
-              float s = yv[k];
+          for (int i = 0; i < 16; ++i) av[i] = act_fn(act, v[b2][i] + bl[cc * 16 + i]);
+          const uint32_t p0 = pack_half2(av[0], av[1]), p1 = pack_half2(av[2], av[3]);
+          const uint32_t p2 = pack_half2(av[4], av[5]), p3 = pack_half2(av[6], av[7]);
+          const uint32_t p4 = pack_half2(av[8], av[9]), p5 = pack_half2(av[10], av[11]);
+          const uint32_t p6 = pack_half2(av[12], av[13]), p7 = pack_half2(av[14], av[15]);
+          const uint32_t o0 = kmajor_offset(row, cc * 16, kTileM), o1 = kmajor_offset(row, cc * 16 + 8, kTileM);
+          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o0) = make_uint4(p0, p1, p2, p3);
+          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o1) = make_uint4(p4, p5, p6, p7);
+          if (!last) {
+            st_shared_v4(region_s + o0, p0, p1, p2, p3);
+            st_shared_v4(region_s + o1, p4, p5, p6, p7);
+          } else {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) s = fmaf(av[i], s_headw[k * width + cc * 16 + i], s);
-              yv[k] = s;
+            for (int k = 0; k < 3; ++k) {
+              if (k < out_dim) {
+                float sp[4];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {  // four short partial sums
+                  const float* hw = s_headw + k * width + cc * 16 + 4 * q4;
+                  sp[q4] = fmaf(av[4 * q4], hw[0], av[4 * q4 + 1] * hw[1]);
+                  sp[q4] = fmaf(av[4 * q4 + 2], hw[2], sp[q4]);
+                  sp[q4] = fmaf(av[4 * q4 + 3], hw[3], sp[q4]);
+                }
+                yv[k] += (sp[0] + sp[1]) + (sp[2] + sp[3]);
+              }
             }
           }
         }
@@ -342,6 +399,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
         tc_fence_after();
       }
     }
+    TTRC(4, tau);
     // ---------------- head partials meet; loss and dL/dout (neural.py:271-302, without 1/size)
     if (half) {
 #pragma unroll
@@ -396,38 +454,55 @@ __global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) dl[k] = s_hx[row * 4 + k];
     }
+    TTRC(5, tau);
     // ---------------- backward: dz_h = da_h * f'(z'_h); da_{h-1} = dz_h . W'_h
     for (int l = depth - 1; l >= 0; --l) {
       const float* bl = s_bias + l * width;
       uint16_t* gdz = a.dz_img + ((size_t)l * ntiles + tau) * tile_elems;
-      for (int cc = half; cc < width / 16; cc += 2) {
-        float z[16], da[16];
-        tmem_ld16(tcol + lane_off + l * width + cc * 16, z);
-        if (l < depth - 1) tmem_ld16(tcol + lane_off + (l + 1) * width + cc * 16, da);
-        tmem_ld_wait();
-        if (l == depth - 1) {
+      const int ncc = width / 16;
+      const int nmine = (ncc - half + 1) / 2;
+      const bool top = (l == depth - 1);
+      for (int c0 = 0; c0 < nmine; c0 += 1) {
+        const int nb = 1;
+        float z[1][16], da[1][16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float s = 0.f;
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-              if (k < out_dim) s = fmaf(dl[k], s_headw[k * width + cc * 16 + i], s);
-            da[i] = s;
+        for (int b2 = 0; b2 < 1; ++b2) {
+          if (b2 < nb) {
+            const int cc = half + 2 * (c0 + b2);
+            tmem_ld16(tcol + lane_off + l * width + cc * 16, z[b2]);
+            if (!top) tmem_ld16(tcol + lane_off + (l + 1) * width + cc * 16, da[b2]);
           }
         }
-        float dz[16];
+        tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) dz[i] = valid ? da[i] * act_deriv_from(act, z[i] + bl[cc * 16 + i]) : 0.f;
-        const uint32_t p0 = pack_half2(dz[0], dz[1]), p1 = pack_half2(dz[2], dz[3]);
-        const uint32_t p2 = pack_half2(dz[4], dz[5]), p3 = pack_half2(dz[6], dz[7]);
-        const uint32_t p4 = pack_half2(dz[8], dz[9]), p5 = pack_half2(dz[10], dz[11]);
-        const uint32_t p6 = pack_half2(dz[12], dz[13]), p7 = pack_half2(dz[14], dz[15]);
-        const uint32_t o0 = kmajor_offset(row, cc * 16, kTileM), o1 = kmajor_offset(row, cc * 16 + 8, kTileM);
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o0) = make_uint4(p0, p1, p2, p3);
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o1) = make_uint4(p4, p5, p6, p7);
-        if (l > 0) {
-          st_shared_v4(region_s + o0, p0, p1, p2, p3);
-          st_shared_v4(region_s + o1, p4, p5, p6, p7);
+        for (int b2 = 0; b2 < 1; ++b2) {
+          if (b2 >= nb) break;
+          const int cc = half + 2 * (c0 + b2);
+          if (top) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float s2 = 0.f;
+#pragma unroll
+              for (int k = 0; k < 3; ++k)
+                if (k < out_dim) s2 = fmaf(dl[k], s_headw[k * width + cc * 16 + i], s2);
+              da[b2][i] = s2;
+            }
+          }
+          float dz[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            dz[i] = valid ? da[b2][i] * act_deriv_from(act, z[b2][i] + bl[cc * 16 + i]) : 0.f;
+          const uint32_t p0 = pack_half2(dz[0], dz[1]), p1 = pack_half2(dz[2], dz[3]);
+          const uint32_t p2 = pack_half2(dz[4], dz[5]), p3 = pack_half2(dz[6], dz[7]);
+          const uint32_t p4 = pack_half2(dz[8], dz[9]), p5 = pack_half2(dz[10], dz[11]);
+          const uint32_t p6 = pack_half2(dz[12], dz[13]), p7 = pack_half2(dz[14], dz[15]);
+          const uint32_t o0 = kmajor_offset(row, cc * 16, kTileM), o1 = kmajor_offset(row, cc * 16 + 8, kTileM);
+          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o0) = make_uint4(p0, p1, p2, p3);
+          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o1) = make_uint4(p4, p5, p6, p7);
+          if (l > 0) {
+            st_shared_v4(region_s + o0, p0, p1, p2, p3);
+            st_shared_v4(region_s + o1, p4, p5, p6, p7);
+          }
         }
       }
       if (l > 0) {
@@ -452,14 +527,24 @@ __global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
     }
     tc_fence_before();
     named_bar_sync(1 + grp, 256);  // all TMEM reads of this tile done before the next tile's MMAs
+    TTRC(6, tau);
   }
   // per-CTA loss partial (fixed order: group 0 then group 1)
   __shared__ double s_wgl[2];
   if (gt == 0) s_wgl[grp] = loss_acc;
   tc_fence_before();
   __syncthreads();
-  if (tid == 0) a.loss_part[blockIdx.x] = a.nwg == 2 ? s_wgl[0] + s_wgl[1] : s_wgl[0];
+  if (tid == 0) {
+    a.loss_part[blockIdx.x] = a.nwg == 2 ? s_wgl[0] + s_wgl[1] : s_wgl[0];
+    for (int i = 0; i < 7; ++i) mbar_inval(&bars[i]);
+  }
   if (tid < 32) tmem_dealloc(tmem_base, 512);
+}
+
+__global__ void __launch_bounds__(512, 1) k_train_fb(const FbArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (*a.stopped) return;
+  fb_body(a, smem);
 }
 
 // ------------------------------------------------------------------ weight gradients
@@ -483,9 +568,11 @@ struct WgArgs {
   uint32_t col_w0, col_b0, col_h, col_head;  // TMEM column bases
 };
 
-__global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  if (*a.stopped) return;
+__device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
+  TTRC_DECL;
+#ifdef NVDB_TRACE
+  ttrc_n = g_ttrace_cap / 2;  // after the fb records of the fused kernel
+#endif
   const int t = threadIdx.x;
   const int row = t & 127;
   const int half = t >> 7;
@@ -506,7 +593,7 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
     for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
-  if (t < 32) tmem_alloc(tmem_slot, 512);
+  if (t < 32) tmem_alloc_keep(tmem_slot, 512);
   for (int i = t; i < 3 * mp; i += 256) s_b2pi[i] = nd.b2pi[i];
   for (int i = t; i < 16 * 128; i += 256) reinterpret_cast<__half*>(s_ones)[i] = __float2half(1.0f);
   if (t < 128) {  // ones column (W) and zero columns (W+1..W+15) of both augmented activation buffers
@@ -518,7 +605,7 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
   }
   fence_async_smem();
   tc_fence_before();
-  __syncthreads();
+  named_bar_sync(3, 256);
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
@@ -584,6 +671,7 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
     const bool valid = bidx < a.batch;
     const int64_t pidx = valid ? (a.idx ? a.idx[bidx] : bidx) : 0;
     const float x0 = a.xs[3 * pidx], x1 = a.xs[3 * pidx + 1], x2 = a.xs[3 * pidx + 2];
+    TTRC(10, tau);
     // ---- stage 0: gW0^T[k][o] += F^T dz0 (features recomputed), gb0 += dz0^T 1
     if (t == 0 && issued < nstages) {
       issue_load(issued);
@@ -629,6 +717,7 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
         umma_f16(tmem + a.col_b0, smem_desc(sdz + s * 256, 128, 2048), smem_desc(son + s * 512, 256, 128), idesc,
                  (!first || s != 0) ? 1u : 0u);
       done_stage(qbase);
+      TTRC(11, tau);
       // ---- stages 1..depth: gW_l^T[i][o] += [a_{l-1} | 1]^T dz_l (head: dL/dout)
       for (int l = 1; l <= depth; ++l) {
         const int64_t q = qbase + l;
@@ -648,6 +737,7 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
           umma_f16(tmem + col, smem_desc(sa + s * 256, 128, 2048), smem_desc(bsrc + s * 256, 128, 2048), idesc,
                    (!first || s != 0) ? 1u : 0u);
         done_stage(q);
+        TTRC(11 + l, tau);
       }
     }
     first = false;
@@ -657,8 +747,9 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
     umma_commit(&bars[6]);
     mbar_wait(&bars[6], 0);
   }
+  TTRC(20, 0);
   tc_fence_before();
-  __syncthreads();
+  named_bar_sync(3, 256);
   tc_fence_after();
   float* part = a.partial + (size_t)blockIdx.x * a.P;
   const int Wr = a.width_real, K0r = 2 * a.m;
@@ -671,16 +762,20 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
       for (int i = 0; i < 16; ++i) v[i] = 0.f;
     }
   };
+  const int64_t poff0 = a.poff[0];
   for (int j = 0; j < nmt; ++j) {
     const int k = j * 128 + row;
+    float* pk = part + poff0 + k;
     for (int cc = half; cc < W / 16; cc += 2) {
       float v[16];
       rd(a.col_w0 + j * W + cc * 16, v);
-      if (k < K0r)
+      if (k < K0r) {
+#pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int o = cc * 16 + i;
-          if (o < Wr) part[a.poff[0] + (int64_t)o * K0r + k] = v[i];
+          if (o < Wr) __stcs(pk + (int64_t)o * K0r, v[i]);
         }
+      }
     }
   }
   if (half == 0) {
@@ -705,8 +800,28 @@ __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
     }
   }
   tc_fence_before();
-  __syncthreads();
+  named_bar_sync(3, 256);
+  if (t == 0)
+    for (int i = 0; i < 7; ++i) mbar_inval(&bars[i]);
+  TTRC(21, 0);
   if (t < 32) tmem_dealloc(tmem, 512);
+}
+
+__global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (*a.stopped) return;
+  wg_body(a, smem);
+}
+
+// fwd/dgrad then weight gradients of the same tiles in one launch: the
+// activation / dz tile images this CTA just wrote are re-read from L2
+// (same tile partition as the two-kernel form: fb_grid == wg_grid)
+__global__ void __launch_bounds__(512, 1) k_train_fbwg(const FbArgs fa, const WgArgs wa) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (*fa.stopped) return;
+  fb_body(fa, smem);
+  __syncthreads();
+  if (threadIdx.x < 256) wg_body(wa, smem);
 }
 
 // ------------------------------------------------------------------ reduce + Adam
@@ -1047,7 +1162,8 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   }
   // kernel attributes
   if (enable_max_smem(k_train_fb) < (long long)t->plan.total ||
-      enable_max_smem(k_train_wgrad) < kWgSmem)
+      enable_max_smem(k_train_wgrad) < kWgSmem ||
+      enable_max_smem(k_train_fbwg) < (long long)std::max<uint32_t>(t->plan.total, kWgSmem))
     return fail(NVDB_EUNSUPPORTED, "training kernels exceed the shared-memory limit");
   *out = tr.release();
   return NVDB_OK;
@@ -1099,8 +1215,6 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st) {
     fa.region_bytes = t->plan.region_bytes;
     fa.small_off = t->plan.small_off;
     fa.bar_off = t->plan.bar_off;
-    k_train_fb<<<t->fb_grid, 256 * t->nwg, std::max<uint32_t>(t->plan.total, 120 * 1024), st>>>(fa);
-    NVDB_CHECK_LAUNCH();
     WgArgs wa{};
     wa.net = t->net;
     wa.m = t->m;
@@ -1122,8 +1236,16 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st) {
     wa.col_b0 = nmt * t->W;
     wa.col_h = wa.col_b0 + 16;
     wa.col_head = wa.col_h + (t->depth - 1) * t->W;
-    k_train_wgrad<<<t->wg_grid, 256, kWgSmem, st>>>(wa);
-    NVDB_CHECK_LAUNCH();
+    const uint32_t fb_smem = std::max<uint32_t>(t->plan.total, 120 * 1024);
+    if (t->fb_grid == t->wg_grid) {
+      k_train_fbwg<<<t->fb_grid, 256 * t->nwg, std::max<uint32_t>(fb_smem, kWgSmem), st>>>(fa, wa);
+      NVDB_CHECK_LAUNCH();
+    } else {
+      k_train_fb<<<t->fb_grid, 256 * t->nwg, fb_smem, st>>>(fa);
+      NVDB_CHECK_LAUNCH();
+      k_train_wgrad<<<t->wg_grid, 256, kWgSmem, st>>>(wa);
+      NVDB_CHECK_LAUNCH();
+    }
     k_train_reduce<<<(int)std::min<int64_t>((t->P + 255) / 256, num_sms() * 8), 256, 0, st>>>(
         t->partial, t->wg_grid, t->P, t->grad, t->loss_part, t->fb_grid, t->lossbuf, stopped);
     NVDB_CHECK_LAUNCH();

@@ -12,6 +12,7 @@ sorted-origin order (decoder.py:71), leaves in node order x ascending slot
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 from dataclasses import dataclass
 from typing import Dict, Optional, Tuple
 
@@ -49,6 +50,39 @@ def _slot1(c) -> int:
 
 def _slot0(c) -> int:
     return ((c[0] & 7) << 6) | ((c[1] & 7) << 3) | (c[2] & 7)
+
+
+def _slot1_arr(k: np.ndarray) -> np.ndarray:
+    return (((k[:, 0] & 127) >> 3) << 8) | (((k[:, 1] & 127) >> 3) << 4) | ((k[:, 2] & 127) >> 3)
+
+
+def _slot0_arr(k: np.ndarray) -> np.ndarray:
+    return ((k[:, 0] & 7) << 6) | ((k[:, 1] & 7) << 3) | (k[:, 2] & 7)
+
+
+def _patch_arrays(lists, nfields: int):
+    """Concatenate the experts' patch lists [(coord, f1[, f2])] into arrays;
+    a key repeated by a later expert overrides the earlier one (decoder.py:84-92)."""
+    keys, fields = [np.zeros((0, 3), np.int64)], [[np.zeros(0)] for _ in range(nfields)]
+    for lst in lists:
+        if not lst:
+            continue
+        n = len(lst)
+        cols = list(zip(*lst))
+        keys.append(np.fromiter(itertools.chain.from_iterable(cols[0]), dtype=np.int64, count=3 * n).reshape(-1, 3))
+        for f in range(nfields):
+            fields[f].append(np.fromiter(cols[1 + f], dtype=np.float64, count=n))
+    k = np.concatenate(keys)
+    fs = [np.concatenate(fl) for fl in fields]
+    if sum(1 for lst in lists if lst) > 1 and k.shape[0]:
+        # keep the last occurrence of each key, in first-occurrence order of the kept rows
+        _, first_rev = np.unique(k[::-1], axis=0, return_index=True)
+        last = np.sort(k.shape[0] - 1 - first_rev)
+        k = k[last]
+        fs = [f[last] for f in fs]
+    if nfields == 1:
+        return k, fs[0].astype(np.int64)
+    return k, fs[0].astype(bool), fs[1]
 
 
 class NetEvaluator:
@@ -105,58 +139,80 @@ class DeviceModel:
                 raise SvcodecError(f"corrupt container: level-1 origin {o} has no level-2 child bit")
         self.origins = np.asarray(origins, dtype=np.int64).reshape(-1, 3)
         self.n1 = len(origins)
-        node_of = {o: i for i, o in enumerate(origins)}
-        self.node_of = node_of
         self.d_origins = torch.from_numpy(self.origins.astype(np.int32)).to(self.dev)
         # patch maps (decoder.py:84-92): later experts override earlier keys
-        l1m: Dict[tuple, int] = {}
-        l0m: Dict[tuple, Tuple[bool, float]] = {}
-        for e in c.experts:
-            for o, k in e.patches.l1:
-                l1m[tuple(int(v) for v in o)] = int(k)
-            for o, a, v in e.patches.l0:
-                l0m[tuple(int(v) for v in o)] = (bool(a), float(v))
-        p1s, p1c = [], []
-        for key, k in l1m.items():
-            ni = node_of.get(tuple(v & ~127 for v in key))
-            if ni is None:
-                raise SvcodecError(f"corrupt container: level-1 patch {key} outside every level-1 node")
-            p1s.append(ni * L1_SIZE + _slot1(key))
-            p1c.append(k)
-        self.p1_slot = self._i64(p1s)
-        self.p1_cls = self._u8(p1c)
-        ts, tv = [], []
-        for org, d in ut.l1_tiles.items():
-            ni = node_of.get(tuple(int(v) for v in org))
-            if ni is None:
-                raise SvcodecError(f"corrupt container: tile record for unknown level-1 node {org}")
-            for s1, v in d.items():
-                ts.append(ni * L1_SIZE + int(s1))
-                tv.append(v)
-        self.t_slot = self._i64(ts)
-        self.t_val = torch.tensor(np.asarray(tv, dtype=np.float32), device=self.dev)
-        ps, pv, pa, pval = [], [], [], []
-        self.l0_keys = []
-        for key, (a, v) in l0m.items():
-            ni = node_of.get(tuple(x & ~127 for x in key))
-            ps.append(-1 if ni is None else ni * L1_SIZE + _slot1(key))
-            pv.append(_slot0(key))
-            pa.append(int(a))
-            pval.append(v)
-            self.l0_keys.append(key)
-        self.p0_slot = self._i64(ps)
-        self.p0_vox = torch.tensor(np.asarray(pv, dtype=np.int32), device=self.dev)
-        self.p0_act = self._u8(pa)
-        self.p0_val = torch.tensor(np.asarray(pval, dtype=np.float32), device=self.dev)
-        ns_, nb = [], []
-        for org, bits in ut.leaf_negative_fill.items():
-            ni = node_of.get(tuple(int(v) & ~127 for v in org))
-            if ni is None:
-                continue
-            ns_.append(ni * L1_SIZE + _slot1(tuple(int(v) for v in org)))
-            nb.append(np.packbits(np.asarray(bits, dtype=bool), bitorder="little").view(np.uint64))
-        self.neg_slot = self._i64(ns_)
-        self.neg_bits = torch.from_numpy(np.asarray(nb, dtype=np.uint64).reshape(-1, 8).view(np.int64).copy()).to(self.dev)
+        l1k, l1c = _patch_arrays([e.patches.l1 for e in c.experts], 1)
+        l0k, l0a, l0v = _patch_arrays([e.patches.l0 for e in c.experts], 2)
+        ni1 = self._node_index(l1k & ~np.int64(127))
+        if (ni1 < 0).any():
+            bad = tuple(int(v) for v in l1k[np.flatnonzero(ni1 < 0)[0]])
+            raise SvcodecError(f"corrupt container: level-1 patch {bad} outside every level-1 node")
+        self.p1_slot = self._i64(ni1 * L1_SIZE + _slot1_arr(l1k))
+        self.p1_cls = self._u8(l1c)
+        # tile records per level-1 node
+        ts, tv = [np.zeros(0, np.int64)], [np.zeros(0, np.float32)]
+        torg = list(ut.l1_tiles.keys())
+        if torg:
+            tni = self._node_index(np.asarray(torg, dtype=np.int64).reshape(-1, 3))
+            if (tni < 0).any():
+                bad = tuple(int(v) for v in torg[int(np.flatnonzero(tni < 0)[0])])
+                raise SvcodecError(f"corrupt container: tile record for unknown level-1 node {bad}")
+            for ni, d in zip(tni, ut.l1_tiles.values()):
+                if d:
+                    ts.append(ni * L1_SIZE + np.fromiter(d.keys(), dtype=np.int64, count=len(d)))
+                    tv.append(np.fromiter(d.values(), dtype=np.float32, count=len(d)))
+        self.t_slot = self._i64(np.concatenate(ts))
+        self.t_val = torch.from_numpy(np.concatenate(tv)).to(self.dev)
+        # level-0 patches: slot -1 when outside every level-1 node (checked in the decode)
+        ni0 = self._node_index(l0k & ~np.int64(127))
+        self.p0_slot = self._i64(np.where(ni0 < 0, -1, ni0 * L1_SIZE + _slot1_arr(l0k)))
+        self.p0_vox = torch.from_numpy(_slot0_arr(l0k).astype(np.int32)).to(self.dev)
+        self.p0_act = self._u8(l0a)
+        self.p0_val = torch.from_numpy(l0v.astype(np.float32)).to(self.dev)
+        self.l0_keys = l0k
+        # negative-fill bits of leaves inside a level-1 node
+        nf = ut.leaf_negative_fill
+        if nf:
+            norg = np.asarray(list(nf.keys()), dtype=np.int64).reshape(-1, 3)
+            nni = self._node_index(norg & ~np.int64(127))
+            keep = nni >= 0
+            bits = np.concatenate([np.asarray(b, dtype=bool).reshape(-1) for b in nf.values()]).reshape(-1, LEAF_SIZE)
+            bits = bits[keep]
+            self.neg_slot = self._i64(nni[keep] * L1_SIZE + _slot1_arr(norg[keep]))
+            packed = np.packbits(bits, axis=1, bitorder="little")  # (n, 64) bytes = 8 x u64 per leaf
+            self.neg_bits = torch.from_numpy(np.ascontiguousarray(packed).view(np.int64).reshape(-1, 8).copy()).to(self.dev)
+        else:
+            self.neg_slot = self._i64(np.zeros(0, np.int64))
+            self.neg_bits = torch.zeros((0, 8), dtype=torch.int64, device=self.dev)
+
+    def _node_index(self, keys: np.ndarray) -> np.ndarray:
+        """Level-1 node index (sorted-origin order) of each node-origin row, -1 if none."""
+        keys = np.asarray(keys, dtype=np.int64).reshape(-1, 3)
+        out = np.full(keys.shape[0], -1, np.int64)
+        if keys.shape[0] == 0 or self.n1 == 0:
+            return out
+        o = self.origins >> 7
+        lo = o.min(axis=0)
+        span = o.max(axis=0) - lo + 1
+        if float(span[0]) * float(span[1]) * float(span[2]) < 2.0 ** 62:
+            # dense code over the origins' bounding box; rows outside it have no node
+            def code(r):
+                return ((r[:, 0] - lo[0]) * span[1] + (r[:, 1] - lo[1])) * span[2] + (r[:, 2] - lo[2])
+            oc = code(o)
+            order = np.argsort(oc, kind="stable")
+            k = (keys >> 7) - lo
+            inside = ((k >= 0) & (k < span)).all(axis=1) & ((keys & 127) == 0).all(axis=1)
+            kc = code(keys[inside] >> 7)
+            pos = np.minimum(np.searchsorted(oc[order], kc), self.n1 - 1)
+            hit = oc[order][pos] == kc
+            out[np.flatnonzero(inside)[hit]] = order[pos[hit]]
+            return out
+        allk = np.concatenate([self.origins, keys])
+        _, inv = np.unique(allk, axis=0, return_inverse=True)
+        inv = inv.reshape(-1)
+        lut = np.full(inv.max() + 1, -1, np.int64)
+        lut[inv[:self.n1]] = np.arange(self.n1)
+        return lut[inv[self.n1:]]
 
     def _i64(self, xs):
         return torch.tensor(np.asarray(xs, dtype=np.int64), device=self.dev)
@@ -341,6 +397,7 @@ class DeviceDecode:
         leaf_perm = np.concatenate([np.arange(starts[i], starts[i] + counts[i]) for i in order]) \
             if n1 else np.zeros(0, np.int64)
         leaf_perm = leaf_perm.astype(np.int64)
+        ident = leaf_perm.shape[0] == lo.shape[0] and bool(np.array_equal(leaf_perm, np.arange(lo.shape[0])))
         ut = c.upper_tree
         l2o = np.asarray([n.origin for n in ut.l2_nodes], dtype=np.int64).reshape(-1, 3)
         o2 = np.lexsort((l2o[:, 2], l2o[:, 1], l2o[:, 0])) if len(l2o) else np.zeros(0, np.int64)
@@ -358,8 +415,8 @@ class DeviceDecode:
             half_width=float(meta.half_width), root_tiles=dict(ut.root_tiles),
             l2_origins=l2o[o2], l2_child=l2c, l2_active=l2a, l2_tiles=l2t,
             l1_origins=m.origins[order], l1_child=(cls == 0)[order], l1_active=(cls == 1)[order],
-            l1_tiles=tiles[order], leaf_origins=lo[leaf_perm], leaf_active=la[leaf_perm],
-            leaf_values=lv[leaf_perm])
+            l1_tiles=tiles[order], leaf_origins=lo if ident else lo[leaf_perm],
+            leaf_active=la if ident else la[leaf_perm], leaf_values=lv if ident else lv[leaf_perm])
 
     def tree(self) -> DeviceTree:
         """Device tree over this decode (hybrid topology for random access)."""

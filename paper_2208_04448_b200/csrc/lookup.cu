@@ -49,25 +49,21 @@ __global__ void k_lookup(TreeView t, const int32_t* __restrict__ coords, int64_t
         k = 1;
       } else {
         const int i2 = (((x & 4095) >> 7) << 10) | (((y & 4095) >> 7) << 5) | ((z & 4095) >> 7);
-        const int64_t w2i = (int64_t)n2 * 512 + (i2 >> 6);
-        const uint64_t cw2 = __ldg(reinterpret_cast<const unsigned long long*>(t.l2_child) + w2i);
-        const uint64_t b2 = 1ull << (i2 & 63);
-        if (!(cw2 & b2)) {
-          v = __ldg(t.l2_tiles + (int64_t)n2 * 32768 + i2);
-          a = (__ldg(reinterpret_cast<const unsigned long long*>(t.l2_active) + w2i) & b2) ? 1 : 0;
+        const int64_t s2 = (int64_t)n2 * 32768 + i2;
+        const int n1 = __ldg(t.l2_slot + s2);
+        if (n1 < 0) {
+          v = __ldg(t.l2_tiles + s2);
+          a = (__ldg(reinterpret_cast<const unsigned long long*>(t.l2_active) + (s2 >> 6)) >> (i2 & 63)) & 1ull;
           k = 1;
         } else {
-          const int n1 = __ldg(t.l2_child_base + n2) + __ldg(t.l2_prefix + w2i) + __popcll(cw2 & (b2 - 1));
           const int i1 = (((x & 127) >> 3) << 8) | (((y & 127) >> 3) << 4) | ((z & 127) >> 3);
-          const int64_t w1i = (int64_t)n1 * 64 + (i1 >> 6);
-          const uint64_t cw1 = __ldg(reinterpret_cast<const unsigned long long*>(t.l1_child) + w1i);
-          const uint64_t b1 = 1ull << (i1 & 63);
-          if (!(cw1 & b1)) {
-            v = __ldg(t.l1_tiles + (int64_t)n1 * 4096 + i1);
-            a = (__ldg(reinterpret_cast<const unsigned long long*>(t.l1_active) + w1i) & b1) ? 1 : 0;
+          const int64_t s1 = (int64_t)n1 * 4096 + i1;
+          leaf = __ldg(t.l1_slot + s1);
+          if (leaf < 0) {
+            v = __ldg(t.l1_tiles + s1);
+            a = (__ldg(reinterpret_cast<const unsigned long long*>(t.l1_active) + (s1 >> 6)) >> (i1 & 63)) & 1ull;
             k = 1;
           } else {
-            leaf = __ldg(t.l1_child_base + n1) + __ldg(t.l1_prefix + w1i) + __popcll(cw1 & (b1 - 1));
             const int i0 = ((x & 7) << 6) | ((y & 7) << 3) | (z & 7);
             v = __ldg(t.leaf_values + (int64_t)leaf * 512 + i0);
             a = (__ldg(reinterpret_cast<const unsigned long long*>(t.leaf_active) + (int64_t)leaf * 8 + (i0 >> 6)) >>
@@ -82,6 +78,18 @@ __global__ void k_lookup(TreeView t, const int32_t* __restrict__ coords, int64_t
     kind[i] = k;
     if (leaf_out) leaf_out[i] = leaf;
   }
+}
+
+// slot -> child index (node base + set child bits before the slot), -1 for a tile slot
+__global__ void k_slot_table(const uint64_t* __restrict__ words, int64_t nslots, int log2_spn,
+                             const uint16_t* __restrict__ prefix, const int32_t* __restrict__ base,
+                             int32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nslots) return;
+  const int64_t node = i >> log2_spn;
+  const uint64_t w = words[i >> 6];
+  const uint64_t b = 1ull << (i & 63);
+  out[i] = (w & b) ? base[node] + prefix[i >> 6] + __popcll(w & (b - 1)) : -1;
 }
 
 // exclusive per-node prefix of set child bits, word granularity
@@ -116,6 +124,18 @@ int tree_build_prefix(nvdb_tree* t, cudaStream_t st) {
   }
   if (t->n1 > 0) {
     k_prefix<<<(t->n1 + 127) / 128, 128, 0, st>>>(t->l1_child, t->n1, 64, t->l1_prefix);
+    NVDB_CHECK_LAUNCH();
+  }
+  if (t->n2 > 0) {
+    const int64_t ns = (int64_t)t->n2 * 32768;
+    k_slot_table<<<(int)((ns + 255) / 256), 256, 0, st>>>(t->l2_child, ns, 15, t->l2_prefix, t->l2_child_base,
+                                                           t->l2_slot);
+    NVDB_CHECK_LAUNCH();
+  }
+  if (t->n1 > 0) {
+    const int64_t ns = (int64_t)t->n1 * 4096;
+    k_slot_table<<<(int)((ns + 255) / 256), 256, 0, st>>>(t->l1_child, ns, 12, t->l1_prefix, t->l1_child_base,
+                                                           t->l1_slot);
     NVDB_CHECK_LAUNCH();
   }
   return NVDB_OK;
@@ -168,6 +188,8 @@ extern "C" int nvdb_tree_create(const nvdb_tree_desc* d, nvdb_tree** out) {
   chk(upload(t, &t->l1_tiles, d->l1_tiles, (size_t)4096 * d->n1));
   chk(upload(t, &t->l1_child_base, d->l1_child_base, (size_t)d->n1));
   chk(upload(t, &t->l1_prefix, (const uint16_t*)nullptr, (size_t)64 * d->n1));
+  chk(upload(t, &t->l2_slot, (const int32_t*)nullptr, (size_t)32768 * d->n2));
+  chk(upload(t, &t->l1_slot, (const int32_t*)nullptr, (size_t)4096 * d->n1));
   chk(upload(t, &t->leaf_active, d->leaf_active, (size_t)8 * d->nl));
   chk(upload(t, &t->leaf_values, d->leaf_values, (size_t)512 * d->nl));
   if (d->leaf_patched) chk(upload(t, &t->leaf_patched, d->leaf_patched, (size_t)8 * d->nl));

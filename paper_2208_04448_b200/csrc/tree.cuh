@@ -22,6 +22,8 @@ struct nvdb_tree {
   float* l1_tiles = nullptr;         // (n1,4096)
   int32_t* l1_child_base = nullptr;  // (n1)
   uint16_t* l1_prefix = nullptr;     // (n1,64)
+  int32_t* l2_slot = nullptr;        // (n2,32768) level-1 node index of a child slot, -1 for a tile
+  int32_t* l1_slot = nullptr;        // (n1,4096) leaf index of a child slot, -1 for a tile
   uint64_t* leaf_active = nullptr;   // (nl,8)
   float* leaf_values = nullptr;      // (nl,512)
   uint64_t* leaf_patched = nullptr;  // (nl,8) optional: voxels whose value is an exact patch
@@ -48,6 +50,8 @@ struct TreeView {  // kernel-side copy of the pointers
   const float* l1_tiles;
   const int32_t* l1_child_base;
   const uint16_t* l1_prefix;
+  const int32_t* l2_slot;
+  const int32_t* l1_slot;
   const uint64_t* leaf_active;
   const float* leaf_values;
 };
@@ -56,10 +60,11 @@ inline TreeView view_of(const nvdb_tree* t) {
   return TreeView{t->background,    t->nroots,        t->root_keys,     t->root_l2,   t->root_tile_value,
                   t->root_tile_active, t->l2_child,   t->l2_active,     t->l2_tiles,  t->l2_child_base,
                   t->l2_prefix,     t->l1_child,      t->l1_active,     t->l1_tiles,  t->l1_child_base,
-                  t->l1_prefix,     t->leaf_active,   t->leaf_values};
+                  t->l1_prefix,     t->l2_slot,       t->l1_slot,       t->leaf_active, t->leaf_values};
 }
 
-// computes l2_prefix / l1_prefix on the device (after masks are in place)
+// computes l2_prefix / l1_prefix and the slot -> child index tables on the
+// device (after masks are in place)
 int tree_build_prefix(nvdb_tree* t, cudaStream_t st);
 int launch_lookup(const nvdb_tree* t, const int32_t* coords, int64_t n, float* value, uint8_t* active,
                   uint8_t* kind, int32_t* leaf, cudaStream_t st);

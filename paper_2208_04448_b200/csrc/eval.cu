@@ -256,6 +256,7 @@ int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int 
   a.bar_off = plan.bar_off;
   a.engines = plan.engines;
   a.tcols = plan.tcols;
+  a.ereg = plan.ereg;
   a.sm_bias = plan.sm_bias;
   a.sm_headw = plan.sm_headw;
   a.sm_headb = plan.sm_headb;

@@ -112,7 +112,8 @@ struct MlpArgs {
   // shared-memory carve-up (bytes, 1024-aligned offsets)
   uint32_t w_off, region_off, region_bytes, small_off, bar_off;
   int32_t engines;  // tile engines per CTA (1..kMaxEngines); blockDim.x = 128 * engines
-  int32_t tcols;    // TMEM columns per engine (accumulator W + hidden A W/2)
+  int32_t tcols;    // TMEM columns per engine (the fp32 accumulator, W)
+  int32_t ereg;     // shared-memory bytes per engine: 2 feature slots, reused for the hidden fp16 A tile
   int32_t sm_bias, sm_headw, sm_headb, sm_b2pi, sm_lat, sm_hx;  // float offsets in the small region
 };
 
@@ -183,9 +184,11 @@ __device__ __forceinline__ void st_shared_b32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-constexpr int kMaxEngines = 3;
-constexpr int kSlots = 2;   // feature chunk slots per engine
-constexpr int kEvalThreads = 128 * kMaxEngines;  // largest block (384)
+constexpr int kMaxEngines = 4;
+constexpr int kSlots = 2;                    // feature chunk slots per engine
+constexpr int kEChunkK = 48;                 // feature K per chunk (3 MMAs of K = 16)
+constexpr int kEChunkBytes = kTileM * kEChunkK * 2;  // 12 KB
+constexpr int kEvalThreads = 128 * kMaxEngines;  // largest block (512)
 
 // ACT: the hidden activation of every net in the launch (a container's nets
 // share one TrainConfig activation), so the epilogue has no per-element branch
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t ring = smem_addr(smem + a.region_off) + (uint32_t)(g * kSlots * kChunkBytes);
+  const uint32_t ring = smem_addr(smem + a.region_off) + (uint32_t)(g * a.ereg);
   const uint32_t w_s = smem_addr(wsm);
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t dcol = tmem_base + (uint32_t)(g * a.tcols);
@@ -334,9 +337,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   constexpr int act = ACT;
 
   auto process = [&](const Tile& tile, int t) {
-    const int k0 = s_net.k0, mp = k0 >> 1, nch = k0 / kChunkK;
+    const int k0 = s_net.k0, mp = k0 >> 1, nch = (k0 + kEChunkK - 1) / kEChunkK;
     const int width = s_net.width, depth = s_net.depth, out_dim = s_net.out_dim;
-    const uint32_t acol = dcol + (uint32_t)width;
+    const uint32_t asm_ = ring;  // hidden fp16 A tile (K-major, 128 rows): the engine's slots once layer 0 is done
     const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
     const uint64_t bdesc0 = smem_desc(w_s, width * 16, 128);
     const uint32_t bstep = (uint32_t)(width >> 3) * 16u;  // (2 core-matrix columns * width/8 * 128 B) >> 4
@@ -371,11 +374,14 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     for (int ch = 0; ch < nch; ++ch, ++cc) {
       const uint32_t s = cc % kSlots;
       if (cc >= kSlots) mbar_wait(slot_free + s, ((cc / kSlots) - 1) & 1u);
-      const uint32_t buf = ring + s * kChunkBytes;
+      const uint32_t buf = ring + s * kEChunkBytes;
+      const int kch = min(kEChunkK, k0 - ch * kEChunkK);  // K of this chunk: 16, 32 or 48
+      const int ngrp = kch >> 3;                           // 4-feature groups in it
       if (lattice) {
         // 4 features x 8 y rows: one sincos, one rotation by exp(i beta),
         // then the Chebyshev recurrence u_{j+1} = 2 cos(beta) u_j - u_{j-1}
-        const int f0 = ch * (kChunkK / 2) + lpg * 4;
+        if (lpg < ngrp) {
+        const int f0 = ch * (kEChunkK / 2) + lpg * 4;
         const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
         const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
         const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
@@ -410,10 +416,12 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
           }
           st_shared_v4(buf + kmajor_offset(lii * 64 + jy * 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
         }
+        }
       } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int f0 = ch * (kChunkK / 2) + q * 4;
+        for (int q = 0; q < kEChunkK / 8; ++q) {
+          if (q >= ngrp) break;
+          const int f0 = ch * (kEChunkK / 2) + q * 4;
           const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
           const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
           const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
@@ -437,11 +445,10 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
         // descriptors: start-address field += byte offset >> 4 (no carry: smem < 256 KB);
         // one K = 16 step = 2 core-matrix columns of the operand
         const uint64_t ad = smem_desc(buf, kTileM * 16, 128);
-        const uint64_t bd = bdesc0 + (uint64_t)(ch * 4 * bstep);
+        const uint64_t bd = bdesc0 + (uint64_t)(ch * (kEChunkK / 16) * bstep);
         umma_f16(dcol, ad, bd, idesc, ch != 0);
-        umma_f16(dcol, ad + 256, bd + bstep, idesc, 1);
-        umma_f16(dcol, ad + 512, bd + 2 * bstep, idesc, 1);
-        umma_f16(dcol, ad + 768, bd + 3 * bstep, idesc, 1);
+        if (kch > 16) umma_f16(dcol, ad + 256, bd + bstep, idesc, 1);
+        if (kch > 32) umma_f16(dcol, ad + 512, bd + 2 * bstep, idesc, 1);
         umma_commit(slot_free + s);
         if (ch == nch - 1) umma_commit(mdone);
       }
@@ -485,7 +492,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
             uint32_t hp[8];
 #pragma unroll
             for (int i2 = 0; i2 < 8; ++i2) hp[i2] = pack_half2(av[2 * i2], av[2 * i2 + 1]);
-            tmem_st8(acol + lane_off + (c0 + b) * 8, hp);
+            const uint32_t ao = asm_ + kmajor_offset(p, (c0 + b) * 16, kTileM);
+            st_shared_v4(ao, hp[0], hp[1], hp[2], hp[3]);
+            st_shared_v4(ao + kTileM * 16, hp[4], hp[5], hp[6], hp[7]);  // next 8-column core-matrix column
           } else {
 #pragma unroll
             for (int k = 0; k < kMaxOut; ++k) {
@@ -508,23 +517,25 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       const int ncc = width / 16;
       auto run_layer = [&](auto last_c) {
         int c0 = 0;
-        for (; c0 + 3 <= ncc; c0 += 3) batch(std::integral_constant<int, 3>{}, last_c, c0);
+        for (; c0 + 2 <= ncc; c0 += 2) batch(std::integral_constant<int, 2>{}, last_c, c0);
         for (; c0 < ncc; ++c0) batch(std::integral_constant<int, 1>{}, last_c, c0);
       };
       if (last) run_layer(std::true_type{});
       else run_layer(std::false_type{});
       tc_fence_before();
       if (!last) {
-        tmem_st_wait();
+        fence_async_smem();
         tc_fence_before();
         named_bar_sync(1 + g, 128);
         if (issuer) {
           tc_fence_after();
           uint64_t bd = smem_desc(w_s + (uint32_t)(width * k0 * 2 + l * width * width * 2), width * 16, 128);
-          umma_f16_ts(dcol, acol, bd, idesc, 0);
+          uint64_t ad = smem_desc(asm_, kTileM * 16, 128);
+          umma_f16(dcol, ad, bd, idesc, 0);
           for (int k = 1; k < width / 16; ++k) {
             bd += bstep;
-            umma_f16_ts(dcol, acol + k * 8, bd, idesc, 1);
+            ad += 256;
+            umma_f16(dcol, ad, bd, idesc, 1);
           }
           umma_commit(mdone);
         }

@@ -50,12 +50,12 @@ constexpr uint32_t kMaxDynSmem = 227 * 1024 - 512;  // leave room for static __s
 // shared-memory / TMEM plan of mlp_eval_kernel for nets up to the given maxima
 struct EvalPlan {
   uint32_t w_off, region_off, region_bytes, small_off, bar_off, total;
-  int engines, tcols, ok;
+  int engines, tcols, ereg, ok;
   int sm_bias, sm_headw, sm_headb, sm_b2pi, sm_lat, sm_hx;
 };
 
-// smem: weights | engines x kSlots feature chunk slots | small params | mbarriers
-// TMEM: engines x (accumulator of W + hidden fp16 A of W/2) <= 512 columns
+// smem: weights | engines x max(kSlots feature chunks, hidden fp16 A tile) | small params | mbarriers
+// TMEM: engines x accumulator of W <= 512 columns
 inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t limit) {
   EvalPlan p{};
   auto a4 = [](int v) { return (v + 3) & ~3; };
@@ -68,12 +68,13 @@ inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t 
   const uint32_t small_bytes = (uint32_t)p.sm_hx * 4u;
   p.w_off = 0;
   p.region_off = (uint32_t)align_up(max_wimg, 1024);
-  p.tcols = (W + (depth > 1 ? W / 2 : 0) + 15) & ~15;
+  p.tcols = (W + 15) & ~15;
+  p.ereg = (int)align_up(std::max<size_t>((size_t)kSlots * kEChunkBytes, (size_t)kTileM * W * 2), 1024);
   const long long room = (long long)limit - p.region_off - small_bytes - 16 - 512;
   const int by_tmem = std::max(0, std::min(kMaxEngines, 512 / std::max(p.tcols, 16)));
-  const int by_smem = room > 0 ? (int)std::min<long long>(kMaxEngines, room / ((long long)kSlots * kChunkBytes)) : 0;
+  const int by_smem = room > 0 ? (int)std::min<long long>(kMaxEngines, room / p.ereg) : 0;
   p.engines = std::min(by_tmem, by_smem);
-  p.region_bytes = (uint32_t)(std::max(p.engines, 1) * kSlots * kChunkBytes);
+  p.region_bytes = (uint32_t)(std::max(p.engines, 1) * p.ereg);
   p.small_off = p.region_off + p.region_bytes;
   p.bar_off = (uint32_t)align_up(p.small_off + small_bytes, 16);
   p.total = p.bar_off + 512;

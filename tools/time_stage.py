@@ -22,6 +22,9 @@ lo = d.leaf_origins
 n = lo.shape[0] * 512
 out = torch.empty(n, dtype=torch.uint8, device=dev)
 run = lambda: m.evaluate("l0", _lib.SRC_LEAF_VOX, lo, n, _lib.OUT_L0ACTIVE, u8=out)  # noqa: E731
+for k in ("NVDB_DEBUG_EVAL", "NVDB_DEBUG_ACT"):  # diagnostics apply to the timed launches only
+    if os.environ.get("TS_" + k):
+        os.environ[k] = os.environ["TS_" + k]
 for _ in range(3):
     run()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -32,5 +35,5 @@ for _ in range(5):
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
-print(f"{stage} {os.environ.get('NVDB_DEBUG_EVAL', '')}/{os.environ.get('NVDB_DEBUG_ACT', '')}: "
+print(f"{stage} dbg {os.environ.get('NVDB_DEBUG_EVAL', '')} act {os.environ.get('NVDB_DEBUG_ACT', '')}: "
       f"{min(ts):.3f} ms  ({n} points)")

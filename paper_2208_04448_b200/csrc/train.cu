@@ -252,7 +252,10 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
   uint64_t* bar_layer = &bars[3 + 3 * grp];
   uint32_t nc0 = 0, nc1 = 0, nlayer = 0;
   bool pend0 = false, pend1 = false;
+  // per group: Z (W fp32 columns: every layer's accumulator in turn, then the
+  // dgrad outputs) | F (depth x W/2 columns: f'(z_l) as fp16 pairs)
   const uint32_t tcol = tmem_base + (uint32_t)(grp * 256);
+  const uint32_t fcol = tcol + (uint32_t)width;
   const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
   const uint32_t region_s = smem_addr(smem + a.region_off + grp * a.region_bytes);
   const uint32_t w_s = smem_addr(wsm);
@@ -342,15 +345,22 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
         float v[2][16];
 #pragma unroll
         for (int b2 = 0; b2 < 2; ++b2)
-          if (b2 < nb) tmem_ld16(tcol + lane_off + l * width + (half + 2 * (c0 + b2)) * 16, v[b2]);
+          if (b2 < nb) tmem_ld16(tcol + lane_off + (half + 2 * (c0 + b2)) * 16, v[b2]);
         tmem_ld_wait();
 #pragma unroll
         for (int b2 = 0; b2 < 2; ++b2) {
           if (b2 >= nb) break;
           const int cc = half + 2 * (c0 + b2);
           float av[16];
+          uint32_t fpk[8];  // f'(z) for the backward pass, fp16 pairs -> TMEM F_l
 #pragma unroll
-          for (int i = 0; i < 16; ++i) av[i] = act_fn(act, v[b2][i] + bl[cc * 16 + i]);
+          for (int i = 0; i < 16; i += 2) {
+            const float z0 = v[b2][i] + bl[cc * 16 + i], z1 = v[b2][i + 1] + bl[cc * 16 + i + 1];
+            av[i] = act_fn(act, z0);
+            av[i + 1] = act_fn(act, z1);
+            fpk[i >> 1] = pack_half2(act_deriv_from(act, z0), act_deriv_from(act, z1));
+          }
+          tmem_st8(fcol + (uint32_t)(l * (width >> 1)) + lane_off + cc * 8, fpk);
           const uint32_t p0 = pack_half2(av[0], av[1]), p1 = pack_half2(av[2], av[3]);
           const uint32_t p2 = pack_half2(av[4], av[5]), p3 = pack_half2(av[6], av[7]);
           const uint32_t p4 = pack_half2(av[8], av[9]), p5 = pack_half2(av[10], av[11]);
@@ -379,6 +389,7 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           }
         }
       }
+      tmem_st_wait();
       if (!last) {
         fence_async_smem();
         tc_fence_before();
@@ -389,7 +400,7 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           for (int s = 0; s < width / 16; ++s) {
             const uint64_t ad = smem_desc(region_s + s * (2 * kTileM * 16), kTileM * 16, 128);
             const uint64_t bd = smem_desc(wl + (uint32_t)(s * 2 * (width >> 3) * 128), width * 16, 128);
-            umma_f16(tcol + (l + 1) * width, ad, bd, idesc, s != 0);
+            umma_f16(tcol, ad, bd, idesc, s != 0);
           }
           umma_commit(bar_layer);
         }
@@ -464,13 +475,13 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
       const bool top = (l == depth - 1);
       for (int c0 = 0; c0 < nmine; c0 += 1) {
         const int nb = 1;
-        float z[1][16], da[1][16];
+        float fz[1][8], da[1][16];
 #pragma unroll
         for (int b2 = 0; b2 < 1; ++b2) {
           if (b2 < nb) {
             const int cc = half + 2 * (c0 + b2);
-            tmem_ld16(tcol + lane_off + l * width + cc * 16, z[b2]);
-            if (!top) tmem_ld16(tcol + lane_off + (l + 1) * width + cc * 16, da[b2]);
+            tmem_ld8(fcol + (uint32_t)(l * (width >> 1)) + lane_off + cc * 8, fz[b2]);
+            if (!top) tmem_ld16(tcol + lane_off + cc * 16, da[b2]);
           }
         }
         tmem_ld_wait();
@@ -490,8 +501,12 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           }
           float dz[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            dz[i] = valid ? da[b2][i] * act_deriv_from(act, z[b2][i] + bl[cc * 16 + i]) : 0.f;
+          for (int i = 0; i < 8; ++i) {
+            const __half2 h = *reinterpret_cast<const __half2*>(&fz[b2][i]);
+            const float2 f = __half22float2(h);
+            dz[2 * i] = valid ? da[b2][2 * i] * f.x : 0.f;
+            dz[2 * i + 1] = valid ? da[b2][2 * i + 1] * f.y : 0.f;
+          }
           const uint32_t p0 = pack_half2(dz[0], dz[1]), p1 = pack_half2(dz[2], dz[3]);
           const uint32_t p2 = pack_half2(dz[4], dz[5]), p3 = pack_half2(dz[6], dz[7]);
           const uint32_t p4 = pack_half2(dz[8], dz[9]), p5 = pack_half2(dz[10], dz[11]);
@@ -516,7 +531,7 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           for (int s = 0; s < width / 16; ++s) {
             const uint64_t ad = smem_desc(region_s + s * (2 * kTileM * 16), kTileM * 16, 128);
             const uint64_t bd = smem_desc(wl + (uint32_t)(s * 256), 128, width * 16);
-            umma_f16(tcol + l * width, ad, bd, idesc_bt, s != 0);
+            umma_f16(tcol, ad, bd, idesc_bt, s != 0);
           }
           umma_commit(bar_layer);
         }
@@ -1000,9 +1015,9 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   // wgrad keeps ceil(k0/128)*W + 16 + (depth-1)*W + 16 accumulator columns
   const int nmt = (k0 + 127) / 128;
   const int wg_cols = nmt * W + 16 + (depth - 1) * W + 16;
-  if (depth * W > 512 || wg_cols > 512)
-    return fail(NVDB_EUNSUPPORTED, "net needs %d / %d TMEM columns (> 512)", depth * W, wg_cols);
-  tr->nwg = (depth * W <= 256) ? 2 : 1;
+  if (W + depth * (W / 2) > 512 || wg_cols > 512)
+    return fail(NVDB_EUNSUPPORTED, "net needs %d / %d TMEM columns (> 512)", W + depth * (W / 2), wg_cols);
+  tr->nwg = (W + depth * (W / 2) <= 256) ? 2 : 1;
   tr->batch = d->sampled ? d->batch : d->n;
   tr->ntiles = (tr->batch + kTileM - 1) / kTileM;
   // ---- parameter layout (serialized: per layer W_l (out,in) then b_l)

@@ -193,6 +193,7 @@ struct FbArgs {
   uint16_t* act_img;          // [depth][ntiles][128*W] fp16 tile images
   uint16_t* dz_img;           // [depth][ntiles][128*W]
   uint16_t* dlt_img;          // [ntiles][128*16]
+  uint16_t* feat_img;         // [ntiles][128*k0] fp16 Fourier features (the weight-gradient phase reads them)
   double* loss_part;          // [grid]
   const int32_t* stopped;
   uint32_t w_off, region_off, region_bytes, small_off, bar_off;
@@ -306,7 +307,10 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           __sincosf(th, &sn, &cs);
           h[j] = pack_half2(cs, sn);
         }
-        st_shared_v4(buf + kmajor_offset(row, half * 32 + q * 8, kTileM), h[0], h[1], h[2], h[3]);
+        const uint32_t fo = kmajor_offset(row, half * 32 + q * 8, kTileM);
+        st_shared_v4(buf + fo, h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.feat_img) + (size_t)tau * kTileM * k0 * 2 +
+                                  (size_t)ch * kChunkBytes + fo) = make_uint4(h[0], h[1], h[2], h[3]);
       }
       fence_async_smem();
       tc_fence_before();
@@ -576,6 +580,7 @@ struct WgArgs {
   const uint16_t* act_img;
   const uint16_t* dz_img;
   const uint16_t* dlt_img;
+  const uint16_t* feat_img;   // [ntiles][128*k0] written by the forward phase
   float* partial;             // [grid][P]
   int64_t P;
   const int64_t* poff;        // per layer l: offset of W_l, then of b_l ([2*(depth+1)])
@@ -602,10 +607,11 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
   uint8_t* s_ones = smem + 204800;
   float* s_b2pi = reinterpret_cast<float*>(smem + 208896);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 208896 + 3 * 512 * 4);
-  // bars: [0,1] full (stage data landed), [2,3] free (stage MMAs done), [4,5] feature ring free, [6] final
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  // bars: [0,1] full (stage data landed), [2,3] free (stage MMAs done), [4,5] feature ring free, [6] final,
+  // [7,8] feature chunk landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   if (t == 0) {
-    for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 9; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
   if (t < 32) tmem_alloc_keep(tmem_slot, 512);
@@ -636,7 +642,7 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
   uint32_t nfull[2] = {0, 0}, nfree[2] = {0, 0};
   bool busy[2] = {false, false};
   int64_t issued = 0;  // stages whose loads were issued
-  uint32_t nring0 = 0, nring1 = 0;
+  uint32_t nring0 = 0, nring1 = 0, nfeat[2] = {0, 0};
   bool pr0 = false, pr1 = false;
 
   auto issue_load = [&](int64_t q) {  // thread 0 only
@@ -682,48 +688,41 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
   bool first = true;
   for (int64_t tau = t0; tau < t1; ++tau) {
     const int64_t qbase = (tau - t0) * nst;
-    const int64_t bidx = tau * kTileM + row;
-    const bool valid = bidx < a.batch;
-    const int64_t pidx = valid ? (a.idx ? a.idx[bidx] : bidx) : 0;
-    const float x0 = a.xs[3 * pidx], x1 = a.xs[3 * pidx + 1], x2 = a.xs[3 * pidx + 2];
     TTRC(10, tau);
-    // ---- stage 0: gW0^T[k][o] += F^T dz0 (features recomputed), gb0 += dz0^T 1
+    // ---- stage 0: gW0^T[k][o] += F^T dz0 (features from the forward phase), gb0 += dz0^T 1
     if (t == 0 && issued < nstages) {
       issue_load(issued);
       issued++;
     }
-    for (int j = 0; j < nmt; ++j) {
-      const int rb = j & 1;
-      if (rb == 0 && pr0) { mbar_wait(&bars[4], (nring0 - 1u) & 1u); pr0 = false; }
-      if (rb == 1 && pr1) { mbar_wait(&bars[5], (nring1 - 1u) & 1u); pr1 = false; }
-      const uint32_t fb = sfe + rb * 32768;
-      const int nf = min(128, k0 - j * 128);
-      for (int q = half; q < nf / 8; q += 2) {
-        uint32_t h[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int f = j * 64 + q * 4 + i;
-          const float th = fmaf(x2, s_b2pi[2 * mp + f], fmaf(x1, s_b2pi[mp + f], x0 * s_b2pi[f]));
-          float sn, cs;
-          __sincosf(th, &sn, &cs);
-          h[i] = valid ? pack_half2(cs, sn) : 0u;
-        }
-        st_shared_v4(fb + kmajor_offset(row, q * 8, kTileM), h[0], h[1], h[2], h[3]);
-      }
-      fence_async_smem();
-      tc_fence_before();
-      named_bar_sync(1, 256);
-      if (t == 0) {
+    if (t == 0) {
+      // feature chunks of 128 features (32 KB) from the forward phase's tile image
+      const uint8_t* fimg = reinterpret_cast<const uint8_t*>(a.feat_img) + (size_t)tau * kTileM * k0 * 2;
+      auto load_chunk = [&](int j) {
+        const int rb = j & 1;
+        if (rb == 0 && pr0) { mbar_wait(&bars[4], (nring0 - 1u) & 1u); pr0 = false; }
+        if (rb == 1 && pr1) { mbar_wait(&bars[5], (nring1 - 1u) & 1u); pr1 = false; }
+        const uint32_t nb = (uint32_t)min(128, k0 - j * 128) * kTileM * 2;
+        mbar_arrive_expect_tx(&bars[7 + rb], nb);
+        bulk_g2s(s_feat + rb * 32768, fimg + (size_t)j * 32768, nb, &bars[7 + rb]);
+      };
+      load_chunk(0);
+      if (nmt > 1) load_chunk(1);
+      for (int j = 0; j < nmt; ++j) {
+        const int rb = j & 1;
+        mbar_wait(&bars[7 + rb], nfeat[rb] & 1u);
+        nfeat[rb]++;
         if (j == 0) wait_full(qbase);
         tc_fence_after();
+        const uint32_t fb = sfe + rb * 32768;
         const uint32_t sdz = smem_addr(s_dz[qbase & 1]);
         const uint32_t idesc = idesc_f16(kTileM, W, 1, 1);
         for (int s = 0; s < kTileM / 16; ++s)
           umma_f16(tmem + a.col_w0 + j * W, smem_desc(fb + s * 256, 128, 2048), smem_desc(sdz + s * 256, 128, 2048),
                    idesc, (!first || s != 0) ? 1u : 0u);
         umma_commit(&bars[4 + rb]);
+        if (rb == 0) { nring0++; pr0 = true; } else { nring1++; pr1 = true; }
+        if (j + 2 < nmt) load_chunk(j + 2);
       }
-      if (rb == 0) { nring0++; pr0 = true; } else { nring1++; pr1 = true; }
     }
     if (t == 0) {
       const uint32_t sdz = smem_addr(s_dz[qbase & 1]);
@@ -817,7 +816,7 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
   tc_fence_before();
   named_bar_sync(3, 256);
   if (t == 0)
-    for (int i = 0; i < 7; ++i) mbar_inval(&bars[i]);
+    for (int i = 0; i < 9; ++i) mbar_inval(&bars[i]);
   TTRC(21, 0);
   if (t < 32) tmem_dealloc(tmem, 512);
 }
@@ -958,6 +957,7 @@ struct nvdb_trainer {
   uint16_t* act_img = nullptr;
   uint16_t* dz_img = nullptr;
   uint16_t* dlt_img = nullptr;
+  uint16_t* feat_img = nullptr;
   int64_t* idx = nullptr;
   int32_t* sflag = nullptr;
   uint32_t* sval = nullptr;
@@ -1144,6 +1144,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   chk(dalloc(t, &t->act_img, (size_t)depth * t->ntiles * tile_elems));
   chk(dalloc(t, &t->dz_img, (size_t)depth * t->ntiles * tile_elems));
   chk(dalloc(t, &t->dlt_img, (size_t)t->ntiles * kTileM * 16));
+  chk(dalloc(t, &t->feat_img, (size_t)t->ntiles * kTileM * t->k0));
   chk(dalloc(t, &t->partial, (size_t)t->wg_grid * P));
   chk(dalloc(t, &t->loss_part, (size_t)t->fb_grid));
   chk(dalloc(t, &t->grad, (size_t)P));
@@ -1223,6 +1224,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st) {
     fa.act_img = t->act_img;
     fa.dz_img = t->dz_img;
     fa.dlt_img = t->dlt_img;
+    fa.feat_img = t->feat_img;
     fa.loss_part = t->loss_part;
     fa.stopped = stopped;
     fa.w_off = t->plan.w_off;
@@ -1242,6 +1244,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st) {
     wa.act_img = t->act_img;
     wa.dz_img = t->dz_img;
     wa.dlt_img = t->dlt_img;
+    wa.feat_img = t->feat_img;
     wa.partial = t->partial;
     wa.P = t->P;
     wa.poff = t->dpoff;

@@ -681,6 +681,16 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
     nfree[b]++;
     busy[b] = true;
   };
+  auto load_feat = [&](int64_t tt, int j) {  // thread 0 only
+    const int rb = j & 1;
+    if (rb == 0 && pr0) { mbar_wait(&bars[4], (nring0 - 1u) & 1u); pr0 = false; }
+    if (rb == 1 && pr1) { mbar_wait(&bars[5], (nring1 - 1u) & 1u); pr1 = false; }
+    const uint32_t nb = (uint32_t)min(128, k0 - j * 128) * kTileM * 2;
+    mbar_arrive_expect_tx(&bars[7 + rb], nb);
+    bulk_g2s(s_feat + rb * 32768,
+             reinterpret_cast<const uint8_t*>(a.feat_img) + (size_t)tt * kTileM * k0 * 2 + (size_t)j * 32768, nb,
+             &bars[7 + rb]);
+  };
   if (t == 0 && nstages > 0) {
     issue_load(0);
     issued = 1;
@@ -695,18 +705,13 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
       issued++;
     }
     if (t == 0) {
-      // feature chunks of 128 features (32 KB) from the forward phase's tile image
-      const uint8_t* fimg = reinterpret_cast<const uint8_t*>(a.feat_img) + (size_t)tau * kTileM * k0 * 2;
-      auto load_chunk = [&](int j) {
-        const int rb = j & 1;
-        if (rb == 0 && pr0) { mbar_wait(&bars[4], (nring0 - 1u) & 1u); pr0 = false; }
-        if (rb == 1 && pr1) { mbar_wait(&bars[5], (nring1 - 1u) & 1u); pr1 = false; }
-        const uint32_t nb = (uint32_t)min(128, k0 - j * 128) * kTileM * 2;
-        mbar_arrive_expect_tx(&bars[7 + rb], nb);
-        bulk_g2s(s_feat + rb * 32768, fimg + (size_t)j * 32768, nb, &bars[7 + rb]);
-      };
-      load_chunk(0);
-      if (nmt > 1) load_chunk(1);
+      // feature chunks of 128 features (32 KB) from the forward phase's tile
+      // image; chunks 0 and 1 of a tile were requested during the previous
+      // tile's later stages (or here, for the first tile)
+      if (tau == t0) {
+        load_feat(tau, 0);
+        if (nmt > 1) load_feat(tau, 1);
+      }
       for (int j = 0; j < nmt; ++j) {
         const int rb = j & 1;
         mbar_wait(&bars[7 + rb], nfeat[rb] & 1u);
@@ -721,7 +726,7 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
                    idesc, (!first || s != 0) ? 1u : 0u);
         umma_commit(&bars[4 + rb]);
         if (rb == 0) { nring0++; pr0 = true; } else { nring1++; pr1 = true; }
-        if (j + 2 < nmt) load_chunk(j + 2);
+        if (j + 2 < nmt) load_feat(tau, j + 2);
       }
     }
     if (t == 0) {
@@ -751,6 +756,10 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
           umma_f16(tmem + col, smem_desc(sa + s * 256, 128, 2048), smem_desc(bsrc + s * 256, 128, 2048), idesc,
                    (!first || s != 0) ? 1u : 0u);
         done_stage(q);
+        if (l == 1 && tau + 1 < t1) {  // next tile's first feature chunks
+          load_feat(tau + 1, 0);
+          if (nmt > 1) load_feat(tau + 1, 1);
+        }
         TTRC(11 + l, tau);
       }
     }

@@ -174,6 +174,78 @@ __global__ void k_sample_tail(SampCtl c) {
   }
 }
 
+// All epochs of a run at once: one CTA per epoch reproduces the numpy stream of
+// Sampler.indices(epoch) (encoder.py:257-267) -- the same PCG64 / Lemire
+// draws as k_sample_raw + scan + compact + tail -- into idx_all[epoch][batch]
+// (int32).  Two passes per thread over its contiguous window of raw draws:
+// count the accepted ones, block-wide exclusive scan, regenerate and write.
+constexpr int kSampThreads = 1024;
+__global__ void __launch_bounds__(kSampThreads) k_sample_epochs(const unsigned long long* __restrict__ words,
+                                                                 unsigned long long n, int64_t batch, int64_t nraw,
+                                                                 int32_t e_begin, int32_t* __restrict__ idx_all) {
+  typedef cub::BlockScan<int, kSampThreads> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int s_total;
+  const int e = e_begin + blockIdx.x;
+  int32_t* out = idx_all + (int64_t)e * batch;
+  const uint32_t nn = (uint32_t)n;
+  const uint32_t threshold = (uint32_t)(0u - nn) % nn;
+  // window of raw draws per thread, even so a draw pair (one PCG output) never straddles two threads
+  const int64_t per = ((nraw + kSampThreads - 1) / kSampThreads + 1) & ~1ll;
+  const int64_t j0 = (int64_t)threadIdx.x * per, j1 = min(nraw, j0 + per);
+  u128 st0, inc;
+  pcg_seed(words + 4 * (int64_t)e, st0, inc);
+  const u128 st_start = j0 < j1 ? pcg_advance(st0, inc, (unsigned long long)(j0 >> 1)) : st0;
+  int cnt = 0;
+  {
+    u128 st = st_start;
+    for (int64_t j = j0; j < j1; j += 2) {
+      st = st * pcg_mult() + inc;
+      const unsigned long long o = pcg_out(st);
+      cnt += ((uint32_t)((unsigned long long)(uint32_t)o * nn) >= threshold) ? 1 : 0;
+      if (j + 1 < j1) cnt += ((uint32_t)((unsigned long long)(uint32_t)(o >> 32) * nn) >= threshold) ? 1 : 0;
+    }
+  }
+  int off, total;
+  Scan(scan_tmp).ExclusiveSum(cnt, off, total);
+  {
+    u128 st = st_start;
+    for (int64_t j = j0; j < j1 && off < batch; j += 2) {
+      st = st * pcg_mult() + inc;
+      const unsigned long long o = pcg_out(st);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && j + 1 >= j1) break;
+        const uint32_t r = h ? (uint32_t)(o >> 32) : (uint32_t)o;
+        const unsigned long long m = (unsigned long long)r * nn;
+        if ((uint32_t)m >= threshold && off < batch) out[off++] = (int32_t)(m >> 32);
+      }
+    }
+  }
+  if (threadIdx.x == 0) s_total = total;
+  __syncthreads();
+  // serial continuation if the window had too many rejections (k_sample_tail)
+  if (threadIdx.x == 0 && s_total < batch) {
+    int64_t have = s_total, j = nraw;
+    u128 st = pcg_advance(st0, inc, (unsigned long long)(j >> 1));
+    unsigned long long o = 0;
+    if (j & 1) o = pcg_out(st);
+    while (have < batch) {
+      uint32_t r;
+      if ((j & 1) == 0) {
+        st = st * pcg_mult() + inc;
+        o = pcg_out(st);
+        r = (uint32_t)o;
+      } else {
+        r = (uint32_t)(o >> 32);
+      }
+      ++j;
+      const unsigned long long m = (unsigned long long)r * nn;
+      if ((uint32_t)m >= threshold) out[have++] = (int32_t)(m >> 32);
+    }
+  }
+}
+
 __global__ void k_sample_ones(SampCtl c) {  // n == 1: numpy fills with 0 without drawing
   if (*c.stopped) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -186,6 +258,8 @@ struct FbArgs {
   const float* xs;            // (n,3) normalized inputs
   const float* ys;            // (n,) targets / labels as float
   const int64_t* idx;         // batch -> point (nullable: identity)
+  const int32_t* idx_all;     // [max_epochs][batch] presampled indices (used when non-null)
+  const int32_t* epoch;       // device epoch counter (row of idx_all)
   int64_t batch;
   int64_t tile_begin, tile_end;  // this rank's share of the batch tiles
   int32_t loss_kind;          // 0 mse, 1 ce, 2 bce
@@ -271,10 +345,11 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
 
   // inputs of this thread's row, loaded one tile ahead (the gather through the
   // sampled indices is two dependent global loads)
+  const int32_t* eidx = a.idx_all ? a.idx_all + (int64_t)(*a.epoch) * a.batch : nullptr;
   auto load_row = [&](int64_t tt, float& x0, float& x1, float& x2, float& y) {
     const int64_t bb = tt * kTileM + row;
     if (tt < t1 && bb < a.batch) {
-      const int64_t pi = a.idx ? a.idx[bb] : bb;
+      const int64_t pi = eidx ? (int64_t)eidx[bb] : (a.idx ? a.idx[bb] : bb);
       x0 = a.xs[3 * pi]; x1 = a.xs[3 * pi + 1]; x2 = a.xs[3 * pi + 2];
       y = a.ys[pi];
     } else {
@@ -892,18 +967,43 @@ struct AdamArgs {
   double loss_den;
   double target;
   int32_t* epoch;
-  int32_t* stopped;
-  int32_t* epochs_done;
+  const int32_t* stopped;
+  int32_t* stop_next;  // set when this epoch's pre-update loss reached the target (applied by k_train_advance)
   double* loss_hist;
+  // fused single-rank form: reduce the per-CTA partials here (grad == nullptr)
+  const float* partial;
+  int32_t ncta;
+  const double* loss_part;
+  int32_t nloss;
 };
 
+// Adam on every parameter; the gradient is either the all-reduced grad[P]
+// (data-parallel phase 2) or the fixed-order sum of the per-CTA partials,
+// in exactly k_train_reduce's order (single rank: one launch fewer)
 __global__ void k_train_adam(AdamArgs a) {
   if (*a.stopped) return;
   const int e = *a.epoch;
   const float lr = a.lr[e], c1 = a.c1[e], c2 = a.c2[e];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.P; q += stride) {
-    const float g = a.grad[q] * a.gscale[q];
+    float gsum;
+    if (a.grad) {
+      gsum = a.grad[q];
+    } else {
+      const float* partial = a.partial;
+      const int64_t P = a.P;
+      float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+      int c = 0;
+      for (; c + 4 <= a.ncta; c += 4) {
+        g0 += partial[(size_t)c * P + q];
+        g1 += partial[(size_t)(c + 1) * P + q];
+        g2 += partial[(size_t)(c + 2) * P + q];
+        g3 += partial[(size_t)(c + 3) * P + q];
+      }
+      for (; c < a.ncta; ++c) g0 += partial[(size_t)c * P + q];
+      gsum = (g0 + g1) + (g2 + g3);
+    }
+    const float g = gsum * a.gscale[q];
     // numpy float32 arithmetic with weak python scalars (neural.py:508-523)
     float m = a.mom[q] * 0.9f;
     m = m + 0.1f * g;
@@ -921,19 +1021,30 @@ __global__ void k_train_adam(AdamArgs a) {
     if (a.f32_dst[q] >= 0) a.f32_block[a.f32_dst[q]] = w * a.img_fold[q];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const double loss = a.lossbuf[0] / a.loss_den;
-    a.loss_hist[e] = loss;
-    if (loss < a.target) {
-      *a.stopped = 1;
-      *a.epochs_done = e + 1;
+    double sl;
+    if (a.loss_part) {
+      sl = 0.0;
+      for (int c = 0; c < a.nloss; ++c) sl += a.loss_part[c];
+    } else {
+      sl = a.lossbuf[0];
     }
+    const double loss = sl / a.loss_den;
+    a.loss_hist[e] = loss;
+    if (loss < a.target) *a.stop_next = 1;
   }
 }
 
-__global__ void k_train_advance(int32_t* epoch, const int32_t* stopped, int32_t* epochs_done) {
+// the stop decision of k_train_adam takes effect here, after every block of
+// the update ran (the reference applies the stopping epoch's update, then breaks)
+__global__ void k_train_advance(int32_t* epoch, int32_t* stopped, int32_t* epochs_done, const int32_t* stop_next) {
   if (*stopped) return;
-  *epoch += 1;
-  *epochs_done = *epoch;
+  if (*stop_next) {
+    *stopped = 1;
+    *epochs_done = *epoch + 1;
+  } else {
+    *epoch += 1;
+    *epochs_done = *epoch;
+  }
 }
 
 }  // namespace
@@ -968,6 +1079,9 @@ struct nvdb_trainer {
   uint16_t* dlt_img = nullptr;
   uint16_t* feat_img = nullptr;
   int64_t* idx = nullptr;
+  int32_t* idx_all = nullptr;   // [max_epochs][batch] presampled (nvdb_trainer_run / phases)
+  int32_t sampled_upto = 0;     // epochs [0, sampled_upto) are in idx_all
+  int32_t host_epoch = 0;       // epochs enqueued so far
   int32_t* sflag = nullptr;
   uint32_t* sval = nullptr;
   int32_t* spos = nullptr;
@@ -1175,6 +1289,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
     t->nraw = t->batch + (int64_t)std::ceil(t->batch * p_rej * 2.0) + 1024;
     t->nraw = (t->nraw + 7) / 8 * 8;
     chk(dalloc(t, &t->idx, t->batch));
+    if (d->n > 1) chk(dalloc(t, &t->idx_all, (size_t)d->max_epochs * t->batch));
     chk(dalloc(t, &t->sflag, t->nraw));
     chk(dalloc(t, &t->sval, t->nraw));
     chk(dalloc(t, &t->spos, t->nraw));
@@ -1198,12 +1313,23 @@ namespace {
 // phase 1: sampler -> fwd/dgrad -> wgrad -> partial reduction (grad, loss);
 // phase 2: Adam + early stop + epoch advance.  A data-parallel caller
 // all-reduces grad[P] and the loss between the two phases.
-int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st) {
+// fused_update: single rank -- the Adam kernel reduces the partials itself
+int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update, int sample_ahead) {
   const nvdb_train_desc& d = t->d;
   int32_t* ep = t->ctl;
   int32_t* stopped = t->ctl + 1;
   if (phase == 1) {
-    if (d.sampled) {
+    if (d.sampled && t->idx_all) {
+      // presample this and the next epochs in one launch (one CTA per epoch)
+      if (t->host_epoch >= t->sampled_upto && t->sampled_upto < d.max_epochs) {
+        const int e0 = t->sampled_upto;
+        const int e1 = std::min<int>(d.max_epochs, std::max(t->host_epoch, e0) + std::max(sample_ahead, 1));
+        k_sample_epochs<<<e1 - e0, kSampThreads, 0, st>>>(t->words, (unsigned long long)d.n, t->batch, t->nraw, e0,
+                                                          t->idx_all);
+        NVDB_CHECK_LAUNCH();
+        t->sampled_upto = e1;
+      }
+    } else if (d.sampled) {
       SampCtl c{ep, stopped, t->words, (unsigned long long)d.n, t->batch, t->nraw, t->sflag, t->sval, t->spos, t->idx};
       if (d.n == 1) {
         k_sample_ones<<<64, 256, 0, st>>>(c);
@@ -1221,6 +1347,8 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st) {
       }
     }
     FbArgs fa{};
+    fa.idx_all = (d.sampled && t->idx_all) ? t->idx_all : nullptr;
+    fa.epoch = ep;
     fa.net = t->net;
     fa.xs = d.inputs;
     fa.ys = d.targets;
@@ -1273,9 +1401,11 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st) {
       k_train_wgrad<<<t->wg_grid, 256, kWgSmem, st>>>(wa);
       NVDB_CHECK_LAUNCH();
     }
-    k_train_reduce<<<(int)std::min<int64_t>((t->P + 255) / 256, num_sms() * 8), 256, 0, st>>>(
-        t->partial, t->wg_grid, t->P, t->grad, t->loss_part, t->fb_grid, t->lossbuf, stopped);
-    NVDB_CHECK_LAUNCH();
+    if (!fused_update) {
+      k_train_reduce<<<(int)std::min<int64_t>((t->P + 255) / 256, num_sms() * 8), 256, 0, st>>>(
+          t->partial, t->wg_grid, t->P, t->grad, t->loss_part, t->fb_grid, t->lossbuf, stopped);
+      NVDB_CHECK_LAUNCH();
+    }
     return NVDB_OK;
   }
     AdamArgs aa{};
@@ -1298,12 +1428,20 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st) {
     aa.target = d.target_loss;
     aa.epoch = ep;
     aa.stopped = stopped;
-    aa.epochs_done = t->ctl + 2;
+    aa.stop_next = t->ctl + 3;
+    if (fused_update) {
+      aa.grad = nullptr;
+      aa.partial = t->partial;
+      aa.ncta = t->wg_grid;
+      aa.loss_part = t->loss_part;
+      aa.nloss = t->fb_grid;
+    }
     aa.loss_hist = t->loss_hist;
     k_train_adam<<<(int)std::min<int64_t>((t->P + 255) / 256, num_sms() * 8), 256, 0, st>>>(aa);
     NVDB_CHECK_LAUNCH();
-    k_train_advance<<<1, 1, 0, st>>>(ep, stopped, t->ctl + 2);
+    k_train_advance<<<1, 1, 0, st>>>(ep, stopped, t->ctl + 2, t->ctl + 3);
     NVDB_CHECK_LAUNCH();
+    ++t->host_epoch;
   return NVDB_OK;
 }
 }  // namespace
@@ -1312,8 +1450,8 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
   if (!t || epochs < 0) return fail(NVDB_EINVAL, "nvdb_trainer_run: bad args");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   for (int e = 0; e < epochs; ++e) {
-    int rc = enqueue_phase(t, 1, st);
-    if (!rc) rc = enqueue_phase(t, 2, st);
+    int rc = enqueue_phase(t, 1, st, true, epochs - e);
+    if (!rc) rc = enqueue_phase(t, 2, st, true, 0);
     if (rc) return rc;
   }
   return NVDB_OK;
@@ -1321,7 +1459,7 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
 
 extern "C" int nvdb_trainer_phase(nvdb_trainer* t, int32_t phase, void* stream) {
   if (!t || (phase != 1 && phase != 2)) return fail(NVDB_EINVAL, "nvdb_trainer_phase: bad args");
-  return enqueue_phase(t, phase, static_cast<cudaStream_t>(stream));
+  return enqueue_phase(t, phase, static_cast<cudaStream_t>(stream), false, 64);
 }
 
 extern "C" int nvdb_trainer_buffers(nvdb_trainer* t, float** grad, int64_t* nparams, double** loss) {

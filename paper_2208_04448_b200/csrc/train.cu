@@ -722,7 +722,7 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
 
   auto issue_load = [&](int64_t q) {  // thread 0 only
     const int b = (int)(q & 1);
-    const int64_t tau = t0 + q / nst;
+    const int64_t tau = t1 - 1 - q / nst;  // newest tile first: the forward phase's latest images are L2-hot
     const int s = (int)(q % nst);
     if (busy[b]) {  // stage q-2 used this buffer: wait for its MMAs
       mbar_wait(&bars[2 + b], (nfree[b] - 1u) & 1u);
@@ -771,8 +771,9 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
     issued = 1;
   }
   bool first = true;
-  for (int64_t tau = t0; tau < t1; ++tau) {
-    const int64_t qbase = (tau - t0) * nst;
+  for (int64_t it = 0; it < t1 - t0; ++it) {
+    const int64_t tau = t1 - 1 - it;  // reverse order (see issue_load)
+    const int64_t qbase = it * nst;
     TTRC(10, tau);
     // ---- stage 0: gW0^T[k][o] += F^T dz0 (features from the forward phase), gb0 += dz0^T 1
     if (t == 0 && issued < nstages) {
@@ -783,7 +784,7 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
       // feature chunks of 128 features (32 KB) from the forward phase's tile
       // image; chunks 0 and 1 of a tile were requested during the previous
       // tile's later stages (or here, for the first tile)
-      if (tau == t0) {
+      if (it == 0) {
         load_feat(tau, 0);
         if (nmt > 1) load_feat(tau, 1);
       }
@@ -831,9 +832,9 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
           umma_f16(tmem + col, smem_desc(sa + s * 256, 128, 2048), smem_desc(bsrc + s * 256, 128, 2048), idesc,
                    (!first || s != 0) ? 1u : 0u);
         done_stage(q);
-        if (l == 1 && tau + 1 < t1) {  // next tile's first feature chunks
-          load_feat(tau + 1, 0);
-          if (nmt > 1) load_feat(tau + 1, 1);
+        if (l == 1 && tau > t0) {  // next tile's first feature chunks
+          load_feat(tau - 1, 0);
+          if (nmt > 1) load_feat(tau - 1, 1);
         }
         TTRC(11 + l, tau);
       }

@@ -114,6 +114,11 @@ struct MlpArgs {
   int32_t engines;  // tile engines per CTA (1..kMaxEngines); blockDim.x = 128 * engines
   int32_t tcols;    // TMEM columns per engine (the fp32 accumulator, W)
   int32_t ereg;     // shared-memory bytes per engine: 2 feature slots, reused for the hidden fp16 A tile
+                    // [+ the weight ring when streaming]
+  int32_t wstream;  // 1: weights do not fit in shared memory; each engine streams K = 16 weight
+                    //    chunks (W x 32 bytes) through a ring of `wring` slots, wring_off into its region
+  int32_t wring;
+  uint32_t wring_off;
   int32_t sm_bias, sm_headw, sm_headb, sm_b2pi, sm_lat, sm_hx;  // float offsets in the small region
 };
 
@@ -189,6 +194,7 @@ constexpr int kSlots = 2;                    // feature chunk slots per engine
 constexpr int kEChunkK = 48;                 // feature K per chunk (3 MMAs of K = 16)
 constexpr int kEChunkBytes = kTileM * kEChunkK * 2;  // 12 KB
 constexpr int kEvalThreads = 128 * kMaxEngines;  // largest block (512)
+constexpr int kMaxWRing = 8;                 // weight ring slots per engine (streamed weights)
 
 // ACT: the hidden activation of every net in the launch (a container's nets
 // share one TrainConfig activation), so the epilogue has no per-element branch
@@ -247,7 +253,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   uint64_t* slot_free = bars + 1 + 8 * g;  // [kSlots]
   uint64_t* mdone = slot_free + kSlots;    // layer MMAs complete
   uint64_t* start_next = bars + 1 + 8 * (g + 1) + kSlots + 1;  // engine g+1 may start
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 33);
+  uint64_t* wfull = bars + 40 + 2 * kMaxWRing * g;  // [wring] weight chunk landed (streamed weights)
+  uint64_t* wempty = wfull + kMaxWRing;      // [wring] MMA reading the chunk done
   __shared__ NetDev s_net;
   __shared__ ExpertDev s_exp;
 
@@ -255,6 +263,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     mbar_init(wbar, 1);
     for (int e = 0; e < E; ++e) {
       for (int s = 0; s < kSlots + 2; ++s) mbar_init(bars + 1 + 8 * e + s, 1);
+      for (int s = 0; s < 2 * kMaxWRing; ++s) mbar_init(bars + 40 + 2 * kMaxWRing * e + s, 1);
     }
     fence_barrier_init();
   }
@@ -288,6 +297,45 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     return tl;
   };
 
+  // ---- streamed weights (issuer thread of each engine): the net's fp16 image
+  // is a sequence of nK K = 16 chunks of W x 32 bytes (layer 0, then each
+  // hidden layer), consumed in that order once per tile; chunk positions
+  // count up globally, slot = pos % wring
+  const int WR = a.wring;
+  const uint32_t wring_s = ring + a.wring_off;
+  uint8_t* const wring_p = smem + a.region_off + (size_t)g * a.ereg + a.wring_off;
+  uint32_t wnext = 0, wcons = 0, wbase = 0;
+  auto w_fill = [&]() {  // load the chunk at position wnext
+    const uint32_t pos = wnext++;
+    const uint32_t slot = pos % (uint32_t)WR;
+    if (pos >= (uint32_t)WR) mbar_wait(wempty + slot, ((pos / WR) - 1) & 1u);
+    const uint32_t cb = (uint32_t)s_net.width * 32u;
+    const uint32_t nk = s_net.wimg_bytes / cb;
+    const uint32_t c = (pos - wbase) % nk;
+    mbar_arrive_expect_tx(wfull + slot, cb);
+    bulk_g2s(wring_p + slot * cb, s_net.wimg + (size_t)c * cb, cb, wfull + slot);
+  };
+  auto w_restart = [&]() {  // new net: drop chunks of the old one still in flight
+    while (wcons < wnext) {
+      const uint32_t slot = wcons % (uint32_t)WR;
+      mbar_wait(wfull + slot, (wcons / WR) & 1u);
+      mbar_arrive(wempty + slot);
+      ++wcons;
+    }
+    wbase = wnext;
+  };
+  // one K = 16 MMA with the next weight chunk of the sequence (issuer only)
+  auto w_mma = [&](uint32_t d, uint64_t adesc, uint32_t idesc, uint32_t acc, bool ts, uint32_t a_tmem) {
+    while (wnext < wcons + (uint32_t)WR - 1) w_fill();
+    const uint32_t slot = wcons % (uint32_t)WR;
+    mbar_wait(wfull + slot, (wcons / WR) & 1u);
+    const uint64_t bd = smem_desc(wring_s + slot * (uint32_t)s_net.width * 32u, s_net.width * 16, 128);
+    if (ts) umma_f16_ts(d, a_tmem, bd, idesc, acc);
+    else umma_f16(d, adesc, bd, idesc, acc);
+    umma_commit(wempty + slot);
+    ++wcons;
+  };
+
   // ---- weight switch: every thread of the CTA, at the same point of the
   // round sequence; each engine has drained its MMAs before it gets here
   int loaded = -1;
@@ -298,9 +346,11 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       s_net = a.nets[net];
       s_exp = a.experts[a.nets[net].expert];
       const NetDev& nd = a.nets[net];
-      mbar_arrive_expect_tx(wbar, nd.wimg_bytes);
-      for (uint32_t off = 0; off < nd.wimg_bytes; off += 32768)
-        bulk_g2s(wsm + off, nd.wimg + off, min(32768u, nd.wimg_bytes - off), wbar);
+      if (!a.wstream) {
+        mbar_arrive_expect_tx(wbar, nd.wimg_bytes);
+        for (uint32_t off = 0; off < nd.wimg_bytes; off += 32768)
+          bulk_g2s(wsm + off, nd.wimg + off, min(32768u, nd.wimg_bytes - off), wbar);
+      }
     }
     __syncthreads();
     {
@@ -312,8 +362,12 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       if (nd.lat)
         for (int i = tid; i < nd.k0; i += nthreads) s_lat[i] = nd.lat[i];
     }
-    mbar_wait(wbar, wphase);
-    wphase ^= 1u;
+    if (!a.wstream) {
+      mbar_wait(wbar, wphase);
+      wphase ^= 1u;
+    } else if (issuer) {
+      w_restart();
+    }
     __syncthreads();
     loaded = net;
   };
@@ -445,10 +499,16 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
         // descriptors: start-address field += byte offset >> 4 (no carry: smem < 256 KB);
         // one K = 16 step = 2 core-matrix columns of the operand
         const uint64_t ad = smem_desc(buf, kTileM * 16, 128);
-        const uint64_t bd = bdesc0 + (uint64_t)(ch * (kEChunkK / 16) * bstep);
-        umma_f16(dcol, ad, bd, idesc, ch != 0);
-        if (kch > 16) umma_f16(dcol, ad + 256, bd + bstep, idesc, 1);
-        if (kch > 32) umma_f16(dcol, ad + 512, bd + 2 * bstep, idesc, 1);
+        if (a.wstream) {
+          w_mma(dcol, ad, idesc, ch != 0, false, 0);
+          if (kch > 16) w_mma(dcol, ad + 256, idesc, 1, false, 0);
+          if (kch > 32) w_mma(dcol, ad + 512, idesc, 1, false, 0);
+        } else {
+          const uint64_t bd = bdesc0 + (uint64_t)(ch * (kEChunkK / 16) * bstep);
+          umma_f16(dcol, ad, bd, idesc, ch != 0);
+          if (kch > 16) umma_f16(dcol, ad + 256, bd + bstep, idesc, 1);
+          if (kch > 32) umma_f16(dcol, ad + 512, bd + 2 * bstep, idesc, 1);
+        }
         umma_commit(slot_free + s);
         if (ch == nch - 1) umma_commit(mdone);
       }
@@ -529,13 +589,17 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
         named_bar_sync(1 + g, 128);
         if (issuer) {
           tc_fence_after();
-          uint64_t bd = smem_desc(w_s + (uint32_t)(width * k0 * 2 + l * width * width * 2), width * 16, 128);
           uint64_t ad = smem_desc(asm_, kTileM * 16, 128);
-          umma_f16(dcol, ad, bd, idesc, 0);
-          for (int k = 1; k < width / 16; ++k) {
-            bd += bstep;
-            ad += 256;
-            umma_f16(dcol, ad, bd, idesc, 1);
+          if (a.wstream) {
+            for (int k = 0; k < width / 16; ++k, ad += 256) w_mma(dcol, ad, idesc, k != 0, false, 0);
+          } else {
+            uint64_t bd = smem_desc(w_s + (uint32_t)(width * k0 * 2 + l * width * width * 2), width * 16, 128);
+            umma_f16(dcol, ad, bd, idesc, 0);
+            for (int k = 1; k < width / 16; ++k) {
+              bd += bstep;
+              ad += 256;
+              umma_f16(dcol, ad, bd, idesc, 1);
+            }
           }
           umma_commit(mdone);
         }
@@ -661,6 +725,12 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   }
 
   // ------------------------------------------------ teardown
+  if (a.wstream && issuer) {  // prefetched weight chunks nobody will use: let the copies land
+    while (wcons < wnext) {
+      mbar_wait(wfull + wcons % (uint32_t)WR, (wcons / WR) & 1u);
+      ++wcons;
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem_base, 512);

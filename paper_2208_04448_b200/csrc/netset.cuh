@@ -1,6 +1,7 @@
 // Device-resident set of every expert's networks (the decode/eval "model").
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 
@@ -50,7 +51,8 @@ constexpr uint32_t kMaxDynSmem = 227 * 1024 - 512;  // leave room for static __s
 // shared-memory / TMEM plan of mlp_eval_kernel for nets up to the given maxima
 struct EvalPlan {
   uint32_t w_off, region_off, region_bytes, small_off, bar_off, total;
-  int engines, tcols, ereg, ok;
+  int engines, tcols, ereg, wstream, wring, ok;
+  uint32_t wring_off;
   int sm_bias, sm_headw, sm_headb, sm_b2pi, sm_lat, sm_hx;
 };
 
@@ -69,15 +71,39 @@ inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t 
   p.w_off = 0;
   p.region_off = (uint32_t)align_up(max_wimg, 1024);
   p.tcols = (W + 15) & ~15;
-  p.ereg = (int)align_up(std::max<size_t>((size_t)kSlots * kEChunkBytes, (size_t)kTileM * W * 2), 1024);
-  const long long room = (long long)limit - p.region_off - small_bytes - 16 - 512;
   const int by_tmem = std::max(0, std::min(kMaxEngines, 512 / std::max(p.tcols, 16)));
-  const int by_smem = room > 0 ? (int)std::min<long long>(kMaxEngines, room / p.ereg) : 0;
-  p.engines = std::min(by_tmem, by_smem);
+  const long long base_ereg = (long long)align_up(std::max<size_t>((size_t)kSlots * kEChunkBytes,
+                                                                   (size_t)kTileM * W * 2), 1024);
+  // resident weights when at least two engines fit beside them, else streamed weights
+  long long room = (long long)limit - p.region_off - small_bytes - 16 - 1024;
+  p.ereg = (int)base_ereg;
+  p.engines = room > 0 ? std::min<int>(by_tmem, (int)std::min<long long>(kMaxEngines, room / base_ereg)) : 0;
+  p.wstream = 0;
+  p.wring = 0;
+  p.wring_off = 0;
+  if (p.engines < 2) {
+    // streamed: as many engines as TMEM allows, then the deepest weight ring that fits
+    // (each slot = one K = 16 chunk of W x 32 bytes; depth hides the L2 latency of a chunk)
+    p.wstream = 1;
+    p.region_off = 0;
+    p.wring_off = (uint32_t)base_ereg;
+    room = (long long)limit - small_bytes - 16 - 1024;
+    p.engines = 0;
+    for (int ne = by_tmem; ne >= 1 && !p.engines; --ne)
+      for (int r = kMaxWRing; r >= 3; --r) {
+        const long long er = (long long)align_up((size_t)base_ereg + (size_t)r * W * 32, 1024);
+        if (ne * er <= room) {
+          p.engines = ne;
+          p.wring = r;
+          p.ereg = (int)er;
+          break;
+        }
+      }
+  }
   p.region_bytes = (uint32_t)(std::max(p.engines, 1) * p.ereg);
   p.small_off = p.region_off + p.region_bytes;
   p.bar_off = (uint32_t)align_up(p.small_off + small_bytes, 16);
-  p.total = p.bar_off + 512;
+  p.total = p.bar_off + 1024;
   p.ok = p.engines >= 1 && p.total <= limit && W % 16 == 0 && W <= 256;
   return p;
 }

@@ -259,6 +259,15 @@ NVDB_API int nvdb_trainer_status(const nvdb_trainer* tr, int32_t* epochs_done, i
  * numpy-exact draws in [0, n) from PCG64 seeded with the 4 HOST words of
  * SeedSequence((seed, 0, epoch)).generate_state(4, uint64); idx DEVICE. */
 NVDB_API int nvdb_sample_indices(uint64_t n, int64_t batch, const uint64_t* words, int64_t* idx, void* stream);
+/* encoder.Sampler.indices with sample_interval > 1 (encoder.py:260-267): the
+ * working subset of interval*batch draws in [0, n) from the HOST words of
+ * SeedSequence((seed, 1, epoch // interval)), then `batch` draws in
+ * [0, interval*batch) from SeedSequence((seed, 2, epoch)) mapped through it;
+ * idx DEVICE.  nvdb_train_desc.seed_words holds, for sample_interval > 1, the
+ * (seed, 2, epoch) words of every epoch followed by the (seed, 1, chunk)
+ * words of every chunk. */
+NVDB_API int nvdb_sample_indices_subset(uint64_t n, int64_t batch, int32_t interval, const uint64_t* words_epoch,
+                                        const uint64_t* words_chunk, int64_t* idx, void* stream);
 /* fp32 master weights into HOST arrays shaped like nvdb_net_desc */
 NVDB_API int nvdb_trainer_weights(const nvdb_trainer* tr, float* const* weights, float* const* biases);
 

@@ -180,14 +180,19 @@ __global__ void k_sample_tail(SampCtl c) {
 // (int32).  Two passes per thread over its contiguous window of raw draws:
 // count the accepted ones, block-wide exclusive scan, regenerate and write.
 constexpr int kSampThreads = 1024;
+// With a working subset (sample_interval > 1, encoder.py:260-267): the draws
+// of epoch e are in [0, interval*batch) and map through subset[e / interval].
 __global__ void __launch_bounds__(kSampThreads) k_sample_epochs(const unsigned long long* __restrict__ words,
                                                                  unsigned long long n, int64_t batch, int64_t nraw,
-                                                                 int32_t e_begin, int32_t* __restrict__ idx_all) {
+                                                                 int32_t e_begin, int32_t* __restrict__ idx_all,
+                                                                 const int32_t* __restrict__ subset = nullptr,
+                                                                 int64_t subset_len = 0, int32_t interval = 1) {
   typedef cub::BlockScan<int, kSampThreads> Scan;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ int s_total;
   const int e = e_begin + blockIdx.x;
   int32_t* out = idx_all + (int64_t)e * batch;
+  const int32_t* sub = subset ? subset + (int64_t)(e / interval) * subset_len : nullptr;
   const uint32_t nn = (uint32_t)n;
   const uint32_t threshold = (uint32_t)(0u - nn) % nn;
   // window of raw draws per thread, even so a draw pair (one PCG output) never straddles two threads
@@ -218,7 +223,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_epochs(const unsigned l
         if (h == 1 && j + 1 >= j1) break;
         const uint32_t r = h ? (uint32_t)(o >> 32) : (uint32_t)o;
         const unsigned long long m = (unsigned long long)r * nn;
-        if ((uint32_t)m >= threshold && off < batch) out[off++] = (int32_t)(m >> 32);
+        if ((uint32_t)m >= threshold && off < batch) out[off++] = sub ? sub[m >> 32] : (int32_t)(m >> 32);
       }
     }
   }
@@ -241,9 +246,22 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_epochs(const unsigned l
       }
       ++j;
       const unsigned long long m = (unsigned long long)r * nn;
-      if ((uint32_t)m >= threshold) out[have++] = (int32_t)(m >> 32);
+      if ((uint32_t)m >= threshold) out[have++] = sub ? sub[m >> 32] : (int32_t)(m >> 32);
     }
   }
+}
+
+// raw draws that cover `count` accepted bounded draws with margin (the tail
+// kernel / serial continuation handles the rare excess of rejections)
+int64_t raw_draws(uint64_t bound, int64_t count) {
+  const double p_rej = bound > 1 ? (double)((uint32_t)(0u - (uint32_t)bound) % (uint32_t)bound) / 4294967296.0 : 0.0;
+  const int64_t nraw = count + (int64_t)std::ceil(count * p_rej * 2.0) + 1024;
+  return (nraw + 7) / 8 * 8;
+}
+
+__global__ void k_i32_to_i64(const int32_t* __restrict__ a, int64_t n, int64_t* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
 }
 
 __global__ void k_sample_ones(SampCtl c) {  // n == 1: numpy fills with 0 without drawing
@@ -1081,6 +1099,9 @@ struct nvdb_trainer {
   uint16_t* feat_img = nullptr;
   int64_t* idx = nullptr;
   int32_t* idx_all = nullptr;   // [max_epochs][batch] presampled (nvdb_trainer_run / phases)
+  int32_t* subset_all = nullptr;  // [nchunks][interval*batch] working subsets (sample_interval > 1)
+  int32_t interval = 1, nchunks = 0, chunks_upto = 0;
+  int64_t nraw_sub = 0, nraw_ep = 0;
   int32_t sampled_upto = 0;     // epochs [0, sampled_upto) are in idx_all
   int32_t host_epoch = 0;       // epochs enqueued so far
   int32_t* sflag = nullptr;
@@ -1122,8 +1143,8 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   if (nd.out_dim != 1 && nd.out_dim != 3) return fail(NVDB_EINVAL, "out_dim must be 1 or 3");
   if ((d->loss_kind == 1) != (nd.out_dim == 3)) return fail(NVDB_EINVAL, "ce loss needs a 3-wide head and vice versa");
   if (d->n < 1 || d->batch < 1 || d->max_epochs < 1) return fail(NVDB_EINVAL, "empty training set / batch");
-  if (d->sampled && d->sample_interval != 1)
-    return fail(NVDB_EUNSUPPORTED, "sample_interval > 1 is not built yet");
+  if (d->sampled && d->sample_interval > 1 && (uint64_t)d->sample_interval * (uint64_t)d->batch > 0xFFFFFFFFull)
+    return fail(NVDB_EUNSUPPORTED, "sample_interval * batch >= 2^32");
   if (d->sampled && (uint64_t)d->n > 0xFFFFFFFFull) return fail(NVDB_EUNSUPPORTED, "n >= 2^32");
   std::unique_ptr<nvdb_trainer> tr(new nvdb_trainer());
   tr->d = *d;
@@ -1290,13 +1311,22 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
     t->nraw = t->batch + (int64_t)std::ceil(t->batch * p_rej * 2.0) + 1024;
     t->nraw = (t->nraw + 7) / 8 * 8;
     chk(dalloc(t, &t->idx, t->batch));
+    t->interval = std::max(1, d->sample_interval);
+    t->nchunks = t->interval > 1 ? (d->max_epochs + t->interval - 1) / t->interval : 0;
     if (d->n > 1) chk(dalloc(t, &t->idx_all, (size_t)d->max_epochs * t->batch));
+    if (d->n > 1 && t->interval > 1) {
+      chk(dalloc(t, &t->subset_all, (size_t)t->nchunks * t->interval * t->batch));
+      t->nraw_sub = raw_draws((uint64_t)d->n, (int64_t)t->interval * t->batch);
+      t->nraw_ep = raw_draws((uint64_t)t->interval * t->batch, t->batch);
+    }
     chk(dalloc(t, &t->sflag, t->nraw));
     chk(dalloc(t, &t->sval, t->nraw));
     chk(dalloc(t, &t->spos, t->nraw));
-    chk(dalloc(t, &t->words, (size_t)4 * d->max_epochs));
+    // words: [max_epochs][4] per-epoch draws, then (sample_interval > 1) [nchunks][4] subset draws
+    chk(dalloc(t, &t->words, (size_t)4 * (d->max_epochs + t->nchunks)));
     if (rc) return rc;
-    NVDB_CUDA_TRY(cudaMemcpy(t->words, d->seed_words, 32 * (size_t)d->max_epochs, cudaMemcpyHostToDevice));
+    NVDB_CUDA_TRY(cudaMemcpy(t->words, d->seed_words, 32 * (size_t)(d->max_epochs + t->nchunks),
+                             cudaMemcpyHostToDevice));
     cub::DeviceScan::ExclusiveSum(nullptr, t->cub_bytes, t->sflag, t->spos, (int)t->nraw);
     NVDB_CUDA_TRY(cudaMalloc(&t->cub_tmp, std::max<size_t>(t->cub_bytes, 16)));
     t->owned.push_back(t->cub_tmp);
@@ -1325,9 +1355,26 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
       if (t->host_epoch >= t->sampled_upto && t->sampled_upto < d.max_epochs) {
         const int e0 = t->sampled_upto;
         const int e1 = std::min<int>(d.max_epochs, std::max(t->host_epoch, e0) + std::max(sample_ahead, 1));
-        k_sample_epochs<<<e1 - e0, kSampThreads, 0, st>>>(t->words, (unsigned long long)d.n, t->batch, t->nraw, e0,
-                                                          t->idx_all);
-        NVDB_CHECK_LAUNCH();
+        if (t->interval <= 1) {
+          k_sample_epochs<<<e1 - e0, kSampThreads, 0, st>>>(t->words, (unsigned long long)d.n, t->batch, t->nraw,
+                                                            e0, t->idx_all);
+          NVDB_CHECK_LAUNCH();
+        } else {
+          // working subsets of the chunks these epochs touch, then the epochs' draws into them
+          const int c1 = (e1 - 1) / t->interval + 1;
+          if (c1 > t->chunks_upto) {
+            const int64_t S = (int64_t)t->interval * t->batch;
+            k_sample_epochs<<<c1 - t->chunks_upto, kSampThreads, 0, st>>>(
+                t->words + 4 * (size_t)d.max_epochs, (unsigned long long)d.n, S, t->nraw_sub, t->chunks_upto,
+                t->subset_all);
+            NVDB_CHECK_LAUNCH();
+            t->chunks_upto = c1;
+          }
+          k_sample_epochs<<<e1 - e0, kSampThreads, 0, st>>>(
+              t->words, (unsigned long long)t->interval * t->batch, t->batch, t->nraw_ep, e0, t->idx_all,
+              t->subset_all, (int64_t)t->interval * t->batch, t->interval);
+          NVDB_CHECK_LAUNCH();
+        }
         t->sampled_upto = e1;
       }
     } else if (d.sampled) {
@@ -1486,6 +1533,36 @@ extern "C" int nvdb_trainer_status(const nvdb_trainer* t, int32_t* epochs_done, 
 
 // Sampler.indices(epoch) seam (encoder.py:257-267, interval == 1): the same
 // kernels as the training loop, on scratch memory of its own.
+// Sampler.indices(epoch) with a working subset (encoder.py:260-267):
+// subset = draws(words_chunk, bound n, interval*batch), idx = subset[draws(words_epoch, bound interval*batch, batch)]
+extern "C" int nvdb_sample_indices_subset(uint64_t n, int64_t batch, int32_t interval, const uint64_t* words_epoch,
+                                          const uint64_t* words_chunk, int64_t* idx, void* stream) {
+  if (n < 2 || batch < 1 || interval < 2 || !words_epoch || !words_chunk || !idx)
+    return fail(NVDB_EINVAL, "nvdb_sample_indices_subset: bad args");
+  const int64_t S = (int64_t)interval * batch;
+  if (n > 0xFFFFFFFFull || S > 0xFFFFFFFFll) return fail(NVDB_EUNSUPPORTED, "bound >= 2^32");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long *we = nullptr, *wc = nullptr;
+  int32_t *sub = nullptr, *out = nullptr;
+  int rc = NVDB_OK;
+  if (cudaMalloc(&we, 32) || cudaMalloc(&wc, 32) || cudaMalloc(&sub, 4 * S) || cudaMalloc(&out, 4 * batch))
+    rc = fail(NVDB_ECUDA, "nvdb_sample_indices_subset: cudaMalloc");
+  if (!rc) {
+    cudaMemcpyAsync(we, words_epoch, 32, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(wc, words_chunk, 32, cudaMemcpyHostToDevice, st);
+    k_sample_epochs<<<1, kSampThreads, 0, st>>>(wc, n, S, raw_draws(n, S), 0, sub);
+    k_sample_epochs<<<1, kSampThreads, 0, st>>>(we, (unsigned long long)S, batch, raw_draws((uint64_t)S, batch), 0,
+                                                out, sub, S, 1);
+    k_i32_to_i64<<<(int)((batch + 255) / 256), 256, 0, st>>>(out, batch, idx);
+    if (cudaStreamSynchronize(st) != cudaSuccess) rc = fail(NVDB_ECUDA, "subset sampler kernels failed");
+  }
+  cudaFree(we);
+  cudaFree(wc);
+  cudaFree(sub);
+  cudaFree(out);
+  return rc;
+}
+
 extern "C" int nvdb_sample_indices(uint64_t n, int64_t batch, const uint64_t* words, int64_t* idx, void* stream) {
   if (n < 1 || batch < 0 || !words || (batch > 0 && !idx)) return fail(NVDB_EINVAL, "nvdb_sample_indices: bad args");
   if (n > 0xFFFFFFFFull) return fail(NVDB_EUNSUPPORTED, "n >= 2^32");

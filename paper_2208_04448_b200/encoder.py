@@ -304,10 +304,17 @@ class DeviceTrainer:
         self.c1 = np.asarray([np.float32(1.0 - 0.9 ** (e + 1)) for e in range(E)], dtype=np.float32)
         self.c2 = np.asarray([np.float32(1.0 - 0.999 ** (e + 1)) for e in range(E)], dtype=np.float32)
         del ep
-        words = np.zeros((E, 4), dtype=np.uint64)
+        interval = max(1, int(cfg.sample_interval))
+        nchunks = (E + interval - 1) // interval if interval > 1 else 0
+        words = np.zeros((E + nchunks, 4), dtype=np.uint64)
         if sampled:
-            for e in range(E):  # Sampler (encoder.py:259): SeedSequence((seed, 0, epoch))
-                words[e] = np.random.SeedSequence((seed_draw, 0, e)).generate_state(4, np.uint64)
+            # Sampler (encoder.py:256-267): SeedSequence((seed, 0, epoch)); with a working
+            # subset, (seed, 2, epoch) per epoch and (seed, 1, chunk) per chunk of `interval` epochs
+            stream = 0 if interval == 1 else 2
+            for e in range(E):
+                words[e] = np.random.SeedSequence((seed_draw, stream, e)).generate_state(4, np.uint64)
+            for ch in range(nchunks):
+                words[E + ch] = np.random.SeedSequence((seed_draw, 1, ch)).generate_state(4, np.uint64)
         self.words = words
         keep: list = []
         nd = _net_desc(params, ff, keep)

@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
+import oracle as O  # noqa: E402
 from helpers import ACTS, HEADS, LOSSES, tiny_cfg  # noqa: E402
 from paper_2208_04448_b200 import _lib  # noqa: E402
 from paper_2208_04448_b200.decoder import DeviceModel  # noqa: E402
@@ -33,13 +34,19 @@ def test_sampler_bit_exact(golden):
     L = _lib.lib()
     for ci in range(int(z["ncases"][0])):
         n, b, iv, seed = (int(v) for v in z[f"c{ci}_cfg"])
-        if iv != 1 or n >= 2 ** 32:
+        if n >= 2 ** 32:
             continue
         for ep in z[f"c{ci}_epochs"]:
-            words = np.random.SeedSequence((seed, 0, int(ep))).generate_state(4, np.uint64)
             out = torch.empty(b, dtype=torch.int64, device=DEV)
-            _lib.check(L.nvdb_sample_indices(n, b, words.ctypes.data_as(C.c_void_p), out.data_ptr(),
-                                              torch.cuda.current_stream().cuda_stream))
+            st = torch.cuda.current_stream().cuda_stream
+            if iv == 1:
+                words = np.random.SeedSequence((seed, 0, int(ep))).generate_state(4, np.uint64)
+                _lib.check(L.nvdb_sample_indices(n, b, words.ctypes.data_as(C.c_void_p), out.data_ptr(), st))
+            else:  # working subset (encoder.py:260-267)
+                we = np.random.SeedSequence((seed, 2, int(ep))).generate_state(4, np.uint64)
+                wc = np.random.SeedSequence((seed, 1, int(ep) // iv)).generate_state(4, np.uint64)
+                _lib.check(L.nvdb_sample_indices_subset(n, b, iv, we.ctypes.data_as(C.c_void_p),
+                                                        wc.ctypes.data_as(C.c_void_p), out.data_ptr(), st))
             np.testing.assert_array_equal(out.cpu().numpy(), z[f"c{ci}_e{int(ep)}"])
 
 
@@ -177,3 +184,19 @@ def test_sequence_warm_start_on_gpu():
     indep = np.linalg.norm(solo2.experts[0].voxel_regressor.params.flatten()
                            - solo1.experts[0].voxel_regressor.params.flatten())
     assert np.linalg.norm(w2 - w1) < indep
+
+
+def test_working_subset_training_tracks_oracle():
+    """sample_interval > 1 (encoder.py:260-267): the trainer's presampled
+    working-subset batches reproduce the oracle's Sampler, so the per-epoch
+    losses of the device epoch loop track the oracle's train_network."""
+    cfg = tiny_cfg(sample_interval=3, max_epochs=12, batch_size=4096, voxel_net=(2, 32), ffm_size=32)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0.1, 0.9, size=(20000, 3)).astype(np.float32)
+    y = (np.sin(6.0 * x[:, 0]) * np.cos(4.0 * x[:, 1]) + 0.5 * x[:, 2]).astype(np.float32)
+    ref_losses = []
+    O.train_network(x, y, O.net_spec("voxel", cfg), cfg, 0, cfg.lr, record_losses=ref_losses)
+    rec = train_network(x, y, net_spec("voxel", cfg), cfg, 0, cfg.lr, device=DEV)
+    print(f"gpu final {rec.final_loss:.6g} epochs {rec.epochs}; oracle per-epoch {np.round(ref_losses, 6)}")
+    assert rec.epochs == len(ref_losses) == 12
+    assert abs(rec.final_loss - ref_losses[-1]) <= 0.03 * abs(ref_losses[-1]) + 1e-5

@@ -271,6 +271,25 @@ NVDB_API int nvdb_sample_indices_subset(uint64_t n, int64_t batch, int32_t inter
 /* fp32 master weights into HOST arrays shaped like nvdb_net_desc */
 NVDB_API int nvdb_trainer_weights(const nvdb_trainer* tr, float* const* weights, float* const* biases);
 
+/* -- synthetic inputs ------------------------------------ */
+
+/* procgen.FbmSpec: value-noise fBm density over the index box [lo, hi]
+ * (inclusive; the reference's domain hi minus one) */
+typedef struct {
+  int32_t octaves;
+  double lacunarity, gain, base_frequency;
+  uint64_t seed;
+  int32_t lo[3], hi[3];
+  double threshold, voxel_size;
+} nvdb_fbm_desc;
+
+/* gen_fbm_density (procgen.py:283-309) per leaf block: for the nblocks leaf
+ * origins (int3, DEVICE) write the 512 voxel values (f32: fbm where active,
+ * else 0) and active flags, and set keep[b] = 1 (int32, DEVICE, caller
+ * zeroed) for blocks with an active voxel.  Bit-exact with the reference. */
+NVDB_API int nvdb_fbm_leaves(const nvdb_fbm_desc* spec, const int32_t* origins, int64_t nblocks, float* values,
+                             uint8_t* active, int32_t* keep, void* stream);
+
 /* -- diagnostics ------------------------------------------------------------ */
 
 /* One 128xN tcgen05 MMA over nk K-steps from caller-laid-out shared-memory

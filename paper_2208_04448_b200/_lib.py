@@ -32,7 +32,7 @@ EXPORTED = [
     "nvdb_leaf_list", "nvdb_l0_apply", "nvdb_leaf_finalize", "nvdb_pack_eq", "nvdb_neural_rows",
     "nvdb_query_finalize", "nvdb_trainer_create", "nvdb_trainer_destroy", "nvdb_trainer_run",
     "nvdb_trainer_status", "nvdb_trainer_weights", "nvdb_sample_indices", "nvdb_trainer_phase",
-    "nvdb_trainer_buffers", "nvdb_sample_indices_subset",
+    "nvdb_trainer_buffers", "nvdb_sample_indices_subset", "nvdb_fbm_leaves",
 ]
 
 SRC_NORM_F32, SRC_CENTER_F64, SRC_COORD_I32, SRC_LEAF_VOX, SRC_L1_SLOT = range(5)
@@ -79,6 +79,12 @@ class TrainDesc(C.Structure):
                 ("target_loss", C.c_double), ("shard_rank", C.c_int32), ("shard_count", C.c_int32)]
 
 
+class FbmDesc(C.Structure):
+    _fields_ = [("octaves", C.c_int32), ("lacunarity", C.c_double), ("gain", C.c_double),
+                ("base_frequency", C.c_double), ("seed", C.c_uint64), ("lo", C.c_int32 * 3),
+                ("hi", C.c_int32 * 3), ("threshold", C.c_double), ("voxel_size", C.c_double)]
+
+
 _lib: Optional[C.CDLL] = None
 
 
@@ -118,6 +124,7 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_trainer_weights": (C.c_int, [vp, C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.POINTER(C.c_float))]),
         "nvdb_sample_indices": (C.c_int, [C.c_uint64, i64, vp, vp, vp]),
         "nvdb_sample_indices_subset": (C.c_int, [C.c_uint64, i64, i32, vp, vp, vp, vp]),
+        "nvdb_fbm_leaves": (C.c_int, [C.POINTER(FbmDesc), vp, i64, vp, vp, vp, vp]),
         "nvdb_trainer_phase": (C.c_int, [vp, i32, vp]),
         "nvdb_trainer_buffers": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(C.c_void_p)]),
     }

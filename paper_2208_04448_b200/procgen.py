@@ -28,6 +28,46 @@ def _canonical_leaf_order(origins: np.ndarray) -> np.ndarray:
     return np.lexsort((i1, i2, root[:, 2], root[:, 1], root[:, 0]))
 
 
+def _nodes_from_leaves(lo_: np.ndarray, bg):
+    """Level-1 / level-2 node arrays over canonically ordered leaf origins
+    (GridBuilder.finalize order: first appearance in canonical leaf order)."""
+    l1_of_leaf = lo_ & ~np.int64(127)
+    if lo_.shape[0]:
+        u1, first, inv1 = np.unique(l1_of_leaf, axis=0, return_index=True, return_inverse=True)
+        rank1 = np.empty(len(first), np.int64)
+        rank1[np.argsort(first)] = np.arange(len(first))
+        l1o = u1[np.argsort(first)]
+        node = rank1[inv1.reshape(-1)]
+    else:
+        l1o = np.zeros((0, 3), np.int64)
+        node = np.zeros(0, np.int64)
+    n1 = l1o.shape[0]
+    l1c = np.zeros((n1, L1_SIZE), bool)
+    a1 = (lo_ & 127) >> 3
+    i1 = (a1[:, 0] << 8) | (a1[:, 1] << 4) | a1[:, 2]
+    l1c[node, i1] = True
+    l1a = np.zeros((n1, L1_SIZE), bool)
+    l1t = np.full((n1, L1_SIZE), bg, np.float32)
+    root_of_l1 = l1o & ~np.int64(4095)
+    if n1:
+        u2, first2, inv2 = np.unique(root_of_l1, axis=0, return_index=True, return_inverse=True)
+        rank2 = np.empty(len(first2), np.int64)
+        rank2[np.argsort(first2)] = np.arange(len(first2))
+        l2o = u2[np.argsort(first2)]
+        n2i = rank2[inv2.reshape(-1)]
+    else:
+        l2o = np.zeros((0, 3), np.int64)
+        n2i = np.zeros(0, np.int64)
+    n2 = l2o.shape[0]
+    l2c = np.zeros((n2, L2_SIZE), bool)
+    a2 = (l1o & 4095) >> 7
+    i2 = (a2[:, 0] << 10) | (a2[:, 1] << 5) | a2[:, 2]
+    l2c[n2i, i2] = True
+    l2a = np.zeros((n2, L2_SIZE), bool)
+    l2t = np.full((n2, L2_SIZE), bg, np.float32)
+    return l1o, l1c, l1a, l1t, l2o, l2c, l2a, l2t
+
+
 def banded_sdf_grid(distance: Callable[[np.ndarray], np.ndarray], lo_idx, hi_idx, voxel_size: float,
                     half_width: float, chunk: int = 4096, lipschitz: bool = True) -> DenseLeafGrid:
     """procgen.py:174-197 + 200-232 as array code.
@@ -77,32 +117,8 @@ def banded_sdf_grid(distance: Callable[[np.ndarray], np.ndarray], lo_idx, hi_idx
     order = _canonical_leaf_order(lo_)
     lo_, la, lv = lo_[order], la[order], lv[order]
     bg = np.float32(band)
-    # level-1 nodes (canonical order = first appearance in canonical leaf order)
-    l1_of_leaf = lo_ & ~np.int64(127)
-    _, first = np.unique(l1_of_leaf, axis=0, return_index=True)
-    l1o = l1_of_leaf[np.sort(first)]
-    n1 = l1o.shape[0]
-    key1 = {tuple(o): i for i, o in enumerate(l1o.tolist())}
-    l1c = np.zeros((n1, L1_SIZE), bool)
-    a1 = (lo_ & 127) >> 3
-    i1 = (a1[:, 0] << 8) | (a1[:, 1] << 4) | a1[:, 2]
-    node = np.asarray([key1[tuple(o)] for o in l1_of_leaf.tolist()], dtype=np.int64) if n1 else np.zeros(0, np.int64)
-    l1c[node, i1] = True
-    l1a = np.zeros((n1, L1_SIZE), bool)
-    l1t = np.full((n1, L1_SIZE), bg, np.float32)
-    # level-2 nodes
-    root_of_l1 = l1o & ~np.int64(4095)
-    _, first2 = np.unique(root_of_l1, axis=0, return_index=True)
-    l2o = root_of_l1[np.sort(first2)]
-    n2 = l2o.shape[0]
-    key2 = {tuple(o): i for i, o in enumerate(l2o.tolist())}
-    l2c = np.zeros((n2, L2_SIZE), bool)
-    a2 = (l1o & 4095) >> 7
-    i2 = (a2[:, 0] << 10) | (a2[:, 1] << 5) | a2[:, 2]
-    n2i = np.asarray([key2[tuple(o)] for o in root_of_l1.tolist()], dtype=np.int64) if n1 else np.zeros(0, np.int64)
-    l2c[n2i, i2] = True
-    l2a = np.zeros((n2, L2_SIZE), bool)
-    l2t = np.full((n2, L2_SIZE), bg, np.float32)
+    l1o, l1c, l1a, l1t, l2o, l2c, l2a, l2t = _nodes_from_leaves(lo_, bg)
+    n1, n2 = l1o.shape[0], l2o.shape[0]
     # interior tiles (procgen.py:200-232): empty slots whose centre is inside
     for j in range(n2):
         empty = np.flatnonzero(~l2c[j] & ~l2a[j])
@@ -151,3 +167,53 @@ def torus_sdf(major_radius: float, minor_radius: float, voxel_size: float, half_
     lo = np.floor(c / voxel_size - (reach, reach, zreach)).astype(np.int64)
     hi = np.ceil(c / voxel_size + (reach, reach, zreach)).astype(np.int64)
     return banded_sdf_grid(distance, lo, hi, voxel_size, half_width)
+
+
+def fbm_density(octaves: int = 4, lacunarity: float = 2.0, gain: float = 0.5, base_frequency: float = 0.05,
+                seed: int = 0, domain=((0, 0, 0), (64, 64, 64)), threshold: float = 0.5, voxel_size: float = 1.0,
+                device=None) -> DenseLeafGrid:
+    """gen_fbm_density (procgen.py:283-309) with the voxel work on the GPU
+    (nvdb_fbm_leaves, bit-exact): every leaf block covering the domain, f64
+    value-noise fBm per voxel, active = inside & value > threshold, leaves
+    with an active voxel kept (values where active, else 0), FOG grid with
+    background 0 and no tiles."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from .model import GRID_CLASS_FOG
+    if octaves < 1:
+        raise ValueError("octaves must be >= 1")
+    lo = np.asarray(domain[0], dtype=np.int64)
+    hi = np.asarray(domain[1], dtype=np.int64) - 1
+    if (hi < lo).any():
+        raise ValueError(f"empty fBm domain {domain}")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    axes = [np.arange(lo[a] & ~np.int64(7), hi[a] + 1, 8, dtype=np.int64) for a in range(3)]
+    gx, gy, gz = np.meshgrid(*axes, indexing="ij")
+    blocks = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
+    nb = blocks.shape[0]
+    d_blocks = torch.from_numpy(blocks.astype(np.int32)).to(dev)
+    vals = torch.empty(nb * LEAF_SIZE, dtype=torch.float32, device=dev)
+    act = torch.empty(nb * LEAF_SIZE, dtype=torch.uint8, device=dev)
+    keep = torch.zeros(nb, dtype=torch.int32, device=dev)
+    spec = _lib.FbmDesc(octaves=int(octaves), lacunarity=float(lacunarity), gain=float(gain),
+                        base_frequency=float(base_frequency), seed=int(seed) & ((1 << 64) - 1),
+                        lo=(C.c_int32 * 3)(*[int(v) for v in lo]), hi=(C.c_int32 * 3)(*[int(v) for v in hi]),
+                        threshold=float(threshold), voxel_size=float(voxel_size))
+    _lib.check(_lib.lib().nvdb_fbm_leaves(C.byref(spec), d_blocks.data_ptr(), nb, vals.data_ptr(), act.data_ptr(),
+                                          keep.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+               "nvdb_fbm_leaves")
+    kept = torch.nonzero(keep).squeeze(1)
+    lo_ = blocks[kept.cpu().numpy()]
+    la = act.view(nb, LEAF_SIZE)[kept].cpu().numpy().astype(bool)
+    lv = vals.view(nb, LEAF_SIZE)[kept].cpu().numpy()
+    order = _canonical_leaf_order(lo_)
+    lo_, la, lv = lo_[order], la[order], lv[order]
+    bg = np.float32(0.0)
+    l1o, l1c, l1a, l1t, l2o, l2c, l2a, l2t = _nodes_from_leaves(lo_, bg)
+    return DenseLeafGrid(background=0.0, grid_class=GRID_CLASS_FOG, voxel_size=float(voxel_size), half_width=0.0,
+                         root_tiles={}, l2_origins=l2o, l2_child=l2c, l2_active=l2a, l2_tiles=l2t, l1_origins=l1o,
+                         l1_child=l1c, l1_active=l1a, l1_tiles=l1t, leaf_origins=lo_, leaf_active=la,
+                         leaf_values=lv)

@@ -302,7 +302,6 @@ extern "C" int nvdb_forward(const nvdb_netset* ns, int32_t net, const float* pts
 // ---------------------------------------------------------------------------
 namespace {
 
-constexpr uint16_t kNoKey = 0xFFFF;
 
 __device__ int find_cell(const int32_t* cells, int ncell, int cx, int cy, int cz) {
   int lo = 0, hi = ncell - 1;
@@ -322,7 +321,7 @@ __device__ __forceinline__ long long floor_div(double v, double s) { return (lon
 // tag's net with a positive gate weight (partition.py:180-229 keeps w > 0).
 __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather, int64_t n, int pass, const int32_t* cells, int ncell,
                             const int32_t* tagnet, int tag, int S, int halo, uint8_t* ncand, uint16_t* keys,
-                            int64_t* vals, BlendOut o) {
+                            int64_t* vals, BlendOut o, int nokey, int32_t* maxc) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double c[3];
@@ -334,7 +333,7 @@ __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather
     hi[a] = floor_div(c[a] + h, (double)S);
   }
   int found = 0;
-  int key = kNoKey;
+  int key = nokey;
   for (int combo = 0; combo < 8; ++combo) {
     bool ok = true;
     int cell[3];
@@ -358,6 +357,7 @@ __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather
   }
   if (pass == 0) {
     ncand[i] = (uint8_t)found;
+    if (found > 1) atomicMax(maxc, found);
     if (found == 0) {  // uncovered everywhere (inference.py:53-56 -> background)
       switch (o.out_mode) {
         case OUT_PROBS: {
@@ -382,34 +382,54 @@ __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather
 }
 
 // Segments of equal key in the sorted list -> tiles (pairs share a net).
-__global__ void k_build_tiles(const uint16_t* keys, int64_t n, Tile* tiles, int64_t max_tiles, int32_t* npairs) {
+// Tiles of one pass, built in parallel from the net-sorted keys: per net the
+// run [start, end) of its points (sentinel keys sort last), ceil(len / 128)
+// tiles rounded up to an even count (tiles are launched in pairs).
+__global__ void k_run_bounds(const uint16_t* __restrict__ keys, int64_t n, int nokey, int64_t* __restrict__ start,
+                             int64_t* __restrict__ end) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint16_t k = keys[i];
+  if (k == nokey) return;
+  if (i == 0 || keys[i - 1] != k) start[k] = i;
+  if (i == n - 1 || keys[i + 1] != k) end[k] = i + 1;
+}
+
+__global__ void k_tile_plan(const int64_t* __restrict__ start, const int64_t* __restrict__ end, int nnets,
+                            int64_t max_tiles, int64_t* __restrict__ toff, int32_t* __restrict__ npairs) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   int64_t nt = 0;
-  int64_t i = 0;
-  while (i < n && keys[i] != kNoKey) {
-    const uint16_t k = keys[i];
-    int64_t j = i;
-    while (j < n && keys[j] == k) ++j;
-    int64_t len = j - i;
+  for (int k = 0; k < nnets; ++k) {
+    toff[k] = nt;
+    const int64_t len = end[k] - start[k];
     int64_t cnt = (len + kTileM - 1) / kTileM;
     cnt = (cnt + 1) & ~1LL;
-    for (int64_t t = 0; t < cnt && nt < max_tiles; ++t, ++nt) {
-      Tile tl;
-      tl.net = k;
-      tl.first = i + t * kTileM;
-      const int64_t rem = len - t * kTileM;
-      tl.count = (int32_t)(rem < 0 ? 0 : (rem > kTileM ? kTileM : rem));
-      tl.flags = 0;
-      tl.pad = 0;
-      tiles[nt] = tl;
-    }
-    i = j;
+    nt = (nt + cnt < (max_tiles & ~1LL)) ? nt + cnt : (max_tiles & ~1LL);
   }
+  toff[nnets] = nt;
   *npairs = (int32_t)(nt / 2);
 }
 
+__global__ void k_write_tiles(const int64_t* __restrict__ start, const int64_t* __restrict__ end,
+                              const int64_t* __restrict__ toff, int nnets, Tile* __restrict__ tiles) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= toff[nnets]) return;
+  int k = 0;
+  while (k + 1 < nnets && toff[k + 1] <= t) ++k;
+  const int64_t i = t - toff[k];
+  const int64_t len = end[k] - start[k];
+  const int64_t rem = len - i * kTileM;
+  Tile tl;
+  tl.net = k;
+  tl.first = start[k] + i * kTileM;
+  tl.count = (int32_t)(rem < 0 ? 0 : (rem > kTileM ? kTileM : rem));
+  tl.flags = 0;
+  tl.pad = 0;
+  tiles[t] = tl;
+}
+
 struct WsLayout {
-  size_t ncand, keys_in, keys_out, vals_in, vals_out, tiles, npairs, acc, cub, total;
+  size_t ncand, keys_in, keys_out, vals_in, vals_out, tiles, npairs, runs, acc, cub, total;
   size_t cub_bytes;
   int64_t max_tiles;
 };
@@ -429,7 +449,8 @@ WsLayout ws_layout(const nvdb_netset* ns, int64_t n) {
   w.vals_in = take(8 * n);
   w.vals_out = take(8 * n);
   w.tiles = take(sizeof(Tile) * w.max_tiles);
-  w.npairs = take(16);
+  w.npairs = take(16);  // npairs | max candidates per point
+  w.runs = take(8 * (3 * (size_t)std::max(ns->nnets, 1) + 1));  // start | end | toff (+1)
   w.acc = take(32 * n);
   size_t cub_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint16_t*)nullptr, (uint16_t*)nullptr, (int64_t*)nullptr,
@@ -488,14 +509,38 @@ int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, c
   a.idx = vout;
   const int threads = 256;
   const int blocks = (int)((n + threads - 1) / threads);
-  for (int pass = 0; pass < 8; ++pass) {
+  // sentinel key = nnets sorts last; radix digits only over the bits a net index needs
+  const int nokey = ns->nnets;
+  int kbits = 1;
+  while ((1 << kbits) <= nokey) ++kbits;
+  int32_t* maxc = npairs + 1;
+  int passes = 8;
+  for (int pass = 0; pass < passes; ++pass) {
+    if (pass == 0) NVDB_CUDA_TRY(cudaMemsetAsync(maxc, 0, 4, st));
     k_pass_keys<<<blocks, threads, 0, st>>>(src_kind, src, gather, n, pass, ns->dev_cells, ns->nexperts, ns->dev_tagnet,
-                                            tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o);
+                                            tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o, nokey, maxc);
     NVDB_CHECK_LAUNCH();
+    if (pass == 0) {  // later passes only exist up to the largest candidate count of this call
+      int32_t hmax = 0;
+      NVDB_CUDA_TRY(cudaMemcpyAsync(&hmax, maxc, 4, cudaMemcpyDeviceToHost, st));
+      NVDB_CUDA_TRY(cudaStreamSynchronize(st));
+      passes = std::max(1, std::min(8, (int)hmax));
+    }
     size_t cb = w.cub_bytes;
-    NVDB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(base + w.cub, cb, kin, kout, vin, vout, (int)n, 0, 16, st));
-    k_build_tiles<<<1, 1, 0, st>>>(kout, n, tiles, w.max_tiles, npairs);
-    NVDB_CHECK_LAUNCH();
+    NVDB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(base + w.cub, cb, kin, kout, vin, vout, (int)n, 0, kbits, st));
+    {
+      const int nn = std::max(ns->nnets, 1);
+      int64_t* rs = reinterpret_cast<int64_t*>(base + w.runs);
+      int64_t* re = rs + nn;
+      int64_t* to = re + nn;
+      NVDB_CUDA_TRY(cudaMemsetAsync(rs, 0, 16 * (size_t)nn, st));
+      k_run_bounds<<<blocks, threads, 0, st>>>(kout, n, nokey, rs, re);
+      NVDB_CHECK_LAUNCH();
+      k_tile_plan<<<1, 32, 0, st>>>(rs, re, ns->nnets, w.max_tiles, to, npairs);
+      NVDB_CHECK_LAUNCH();
+      k_write_tiles<<<(int)((w.max_tiles + 255) / 256), 256, 0, st>>>(rs, re, to, ns->nnets, tiles);
+      NVDB_CHECK_LAUNCH();
+    }
     a.pass = pass;
     int rc = launch_mlp(ns, a, npairs, num_sms(), st);
     if (rc) return rc;

@@ -397,16 +397,23 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
     const uint64_t bdesc0 = smem_desc(w_s, width * 16, 128);
     const uint32_t bstep = (uint32_t)(width >> 3) * 16u;  // (2 core-matrix columns * width/8 * 128 B) >> 4
-    const bool lattice = a.src_kind == SRC_LEAF_VOX && !a.idx && !a.gather && s_net.lat &&
-                         tile.count == kTileM && (tile.first & (kTileM - 1)) == 0;
+    // lattice tiles: 128 consecutive leaf-voxel ids starting on a 128 boundary
+    // (implicit tiles, or a sorted multi-expert pass whose tile kept its run)
+    int64_t lfirst = tile.first;
+    bool lattice = a.src_kind == SRC_LEAF_VOX && !a.gather && s_net.lat && tile.count == kTileM;
+    if (lattice && a.idx) {
+      lfirst = a.idx[tile.first];
+      lattice = a.idx[tile.first + kTileM - 1] == lfirst + (kTileM - 1);
+    }
+    lattice = lattice && (lfirst & (kTileM - 1)) == 0;
     const double is = s_exp.inv_scale;
     // ------------------------------------------------ feature inputs
     float x0 = 0.f, x1 = 0.f, x2 = 0.f;
     // lattice role: z = lk, feature quad lpg, x = lii; 8 y rows each
     const int lk = p & 7, lpg = (p >> 3) & 7, lii = p >> 6;
     if (lattice) {
-      const int* o = static_cast<const int*>(a.src) + 3 * (tile.first >> 9);
-      const int i0 = (int)((tile.first & 511) >> 6);
+      const int* o = static_cast<const int*>(a.src) + 3 * (lfirst >> 9);
+      const int i0 = (int)((lfirst & 511) >> 6);
       x0 = __double2float_rn((o[0] + i0 + lii + 0.5 - s_exp.norm_origin[0]) * is);
       x1 = __double2float_rn((o[1] + 0.5 - s_exp.norm_origin[1]) * is);
       x2 = __double2float_rn((o[2] + lk + 0.5 - s_exp.norm_origin[2]) * is);

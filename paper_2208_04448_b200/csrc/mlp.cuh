@@ -254,8 +254,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   uint64_t* mdone = slot_free + kSlots;    // layer MMAs complete
   uint64_t* start_next = bars + 1 + 8 * (g + 1) + kSlots + 1;  // engine g+1 may start
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 33);
-  uint64_t* wfull = bars + 40 + 2 * kMaxWRing * g;  // [wring] weight chunk landed (streamed weights)
-  uint64_t* wempty = wfull + kMaxWRing;      // [wring] MMA reading the chunk done
+  uint64_t* wfull = bars + 40;                // [wring] weight chunk landed (streamed weights)
+  uint64_t* wempty = wfull + kMaxWRing;      // [wring] every engine's MMA reading the chunk done
+  __shared__ uint32_t s_wnext;
   __shared__ NetDev s_net;
   __shared__ ExpertDev s_exp;
 
@@ -263,8 +264,13 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     mbar_init(wbar, 1);
     for (int e = 0; e < E; ++e) {
       for (int s = 0; s < kSlots + 2; ++s) mbar_init(bars + 1 + 8 * e + s, 1);
-      for (int s = 0; s < 2 * kMaxWRing; ++s) mbar_init(bars + 40 + 2 * kMaxWRing * e + s, 1);
+
     }
+    for (int s = 0; s < kMaxWRing; ++s) {
+      mbar_init(bars + 40 + s, 1);
+      mbar_init(bars + 40 + kMaxWRing + s, E);
+    }
+    s_wnext = 0;
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -297,16 +303,18 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     return tl;
   };
 
-  // ---- streamed weights (issuer thread of each engine): the net's fp16 image
-  // is a sequence of nK K = 16 chunks of W x 32 bytes (layer 0, then each
-  // hidden layer), consumed in that order once per tile; chunk positions
-  // count up globally, slot = pos % wring
+  // ---- streamed weights: the net's fp16 image is a sequence of nK K = 16
+  // chunks of W x 32 bytes (layer 0, then each hidden layer), consumed in
+  // that order once per tile by every engine.  One ring of `wring` slots per
+  // CTA is shared by the engines, so each chunk fetched from L2 serves all
+  // engines' current tiles.  Chunk positions count up globally; any engine's
+  // issuer may claim the next position to fill (s_wnext); a slot is refilled
+  // once all E engines consumed its previous chunk (wempty counts E).
   const int WR = a.wring;
-  const uint32_t wring_s = ring + a.wring_off;
-  uint8_t* const wring_p = smem + a.region_off + (size_t)g * a.ereg + a.wring_off;
-  uint32_t wnext = 0, wcons = 0, wbase = 0;
-  auto w_fill = [&]() {  // load the chunk at position wnext
-    const uint32_t pos = wnext++;
+  const uint32_t wring_s = smem_addr(smem + a.wring_off);
+  uint8_t* const wring_p = smem + a.wring_off;
+  uint32_t wcons = 0, wbase = 0;  // per issuer
+  auto w_fill_pos = [&](uint32_t pos) {
     const uint32_t slot = pos % (uint32_t)WR;
     if (pos >= (uint32_t)WR) mbar_wait(wempty + slot, ((pos / WR) - 1) & 1u);
     const uint32_t cb = (uint32_t)s_net.width * 32u;
@@ -315,25 +323,46 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     mbar_arrive_expect_tx(wfull + slot, cb);
     bulk_g2s(wring_p + slot * cb, s_net.wimg + (size_t)c * cb, cb, wfull + slot);
   };
-  auto w_restart = [&]() {  // new net: drop chunks of the old one still in flight
-    while (wcons < wnext) {
-      const uint32_t slot = wcons % (uint32_t)WR;
-      mbar_wait(wfull + slot, (wcons / WR) & 1u);
-      mbar_arrive(wempty + slot);
-      ++wcons;
+  auto w_next = [&]() {  // slot of this issuer's next chunk, once it landed
+    while (true) {
+      const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&s_wnext);
+      if (n >= wcons + (uint32_t)WR - 1) break;
+      if (atomicCAS(&s_wnext, n, n + 1) == n) w_fill_pos(n);
     }
-    wbase = wnext;
+    const uint32_t slot = wcons % (uint32_t)WR;
+    mbar_wait(wfull + slot, (wcons / WR) & 1u);
+    return slot;
   };
   // one K = 16 MMA with the next weight chunk of the sequence (issuer only)
   auto w_mma = [&](uint32_t d, uint64_t adesc, uint32_t idesc, uint32_t acc, bool ts, uint32_t a_tmem) {
-    while (wnext < wcons + (uint32_t)WR - 1) w_fill();
-    const uint32_t slot = wcons % (uint32_t)WR;
-    mbar_wait(wfull + slot, (wcons / WR) & 1u);
+    const uint32_t slot = w_next();
     const uint64_t bd = smem_desc(wring_s + slot * (uint32_t)s_net.width * 32u, s_net.width * 16, 128);
     if (ts) umma_f16_ts(d, a_tmem, bd, idesc, acc);
     else umma_f16(d, adesc, bd, idesc, acc);
     umma_commit(wempty + slot);
     ++wcons;
+  };
+  // an engine without a tile in this (sub-)round still consumes the tile's chunks
+  auto w_skip_tile = [&]() {
+    const uint32_t nk = s_net.wimg_bytes / ((uint32_t)s_net.width * 32u);
+    for (uint32_t c = 0; c < nk; ++c) {
+      const uint32_t slot = w_next();
+      mbar_arrive(wempty + slot);
+      ++wcons;
+    }
+  };
+  // new net (all engines at the barrier, every engine consumed the same
+  // positions): let the old net's prefetched chunks land, retire them for all
+  // engines, restart the sequence
+  auto w_restart = [&]() {
+    if (tid == 0) {
+      const uint32_t n = s_wnext;
+      for (uint32_t pos = wcons; pos < n; ++pos) {
+        const uint32_t slot = pos % (uint32_t)WR;
+        mbar_wait(wfull + slot, (pos / WR) & 1u);
+        for (int e = 0; e < E; ++e) mbar_arrive(wempty + slot);
+      }
+    }
   };
 
   // ---- weight switch: every thread of the CTA, at the same point of the
@@ -365,10 +394,11 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     if (!a.wstream) {
       mbar_wait(wbar, wphase);
       wphase ^= 1u;
-    } else if (issuer) {
+    } else {
       w_restart();
     }
     __syncthreads();
+    if (a.wstream) wcons = wbase = s_wnext;
     loaded = net;
   };
 
@@ -376,7 +406,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   // tiles non-empty, one net), so no engine can be left waiting for a start
   // signal across a weight switch
   bool stagger = false;
-  if (E > 1 && t_end - t_begin >= E) {
+  if (E > 1 && t_end - t_begin >= E && !a.wstream) {  // (streamed engines pace each other through the ring)
     stagger = true;
     const Tile t0 = tile_at(t_begin);
     for (int k = 0; k < E; ++k) {
@@ -720,23 +750,22 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
         ++k2;
       }
       if (tk.net != loaded) load_net(tk.net);
-      if (g >= k && g < k2) {
-        const Tile mine = tile_at(base + g);
-        if (mine.count > 0) {
-          if (wait_start && base == t_begin) mbar_wait(bars + 1 + 8 * g + kSlots + 1, 0);
-          process(mine, base + g);
-        }
+      const Tile mine = (g >= k && g < k2) ? tile_at(base + g) : Tile{};
+      if (g >= k && g < k2 && mine.count > 0) {
+        if (wait_start && base == t_begin) mbar_wait(bars + 1 + 8 * g + kSlots + 1, 0);
+        process(mine, base + g);
+      } else if (a.wstream && issuer) {
+        w_skip_tile();
       }
       k = k2;
     }
   }
 
   // ------------------------------------------------ teardown
-  if (a.wstream && issuer) {  // prefetched weight chunks nobody will use: let the copies land
-    while (wcons < wnext) {
-      mbar_wait(wfull + wcons % (uint32_t)WR, (wcons / WR) & 1u);
-      ++wcons;
-    }
+  if (a.wstream) {  // prefetched weight chunks nobody will use: let the copies land
+    __syncthreads();
+    if (tid == 0)
+      for (uint32_t pos = wcons; pos < s_wnext; ++pos) mbar_wait(wfull + pos % (uint32_t)WR, (pos / WR) & 1u);
   }
   tc_fence_before();
   __syncthreads();

@@ -82,25 +82,24 @@ inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t 
   p.wring = 0;
   p.wring_off = 0;
   if (p.engines < 2) {
-    // streamed: as many engines as TMEM allows, then the deepest weight ring that fits
-    // (each slot = one K = 16 chunk of W x 32 bytes; depth hides the L2 latency of a chunk)
+    // streamed: as many engines as TMEM allows, then the deepest CTA-wide weight
+    // ring that fits (each slot = one K = 16 chunk of W x 32 bytes)
     p.wstream = 1;
     p.region_off = 0;
-    p.wring_off = (uint32_t)base_ereg;
     room = (long long)limit - small_bytes - 16 - 1024;
     p.engines = 0;
     for (int ne = by_tmem; ne >= 1 && !p.engines; --ne)
       for (int r = kMaxWRing; r >= 3; --r) {
-        const long long er = (long long)align_up((size_t)base_ereg + (size_t)r * W * 32, 1024);
-        if (ne * er <= room) {
+        if (ne * base_ereg + (long long)r * W * 32 <= room) {
           p.engines = ne;
           p.wring = r;
-          p.ereg = (int)er;
+          p.ereg = (int)base_ereg;
           break;
         }
       }
+    p.wring_off = (uint32_t)(p.engines * base_ereg);
   }
-  p.region_bytes = (uint32_t)(std::max(p.engines, 1) * p.ereg);
+  p.region_bytes = (uint32_t)(std::max(p.engines, 1) * p.ereg) + (p.wstream ? (uint32_t)(p.wring * W * 32) : 0u);
   p.small_off = p.region_off + p.region_bytes;
   p.bar_off = (uint32_t)align_up(p.small_off + small_bytes, 16);
   p.total = p.bar_off + 1024;

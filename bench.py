@@ -230,6 +230,28 @@ def query_bench(m, dev, steps, nq=1 << 27, lo=-32, hi=544, seed=0):
                                     "achieved": nq * bytes_q / (t_lookup * 1e-3) / 1e9, "unit": "GB/s"}}}
 
 
+def c3_decode(dev, size=1024):
+    """C3 shape (BASELINE configs[2]) on one GPU: fBm density 1024^3 generated on
+    the GPU (bit-exact with procgen.gen_fbm_density), 8 experts (2x2x2 at
+    S = 512), Chameleon-class nets (L0 / voxel 3x256 m256, streamed weights)
+    with random weights (wide-net training is not built), the two decode
+    stages over the grid's topology with gate blending across experts."""
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bench_c3.py"), str(size)],
+                         capture_output=True, text=True, timeout=900,
+                         env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                                  or str(dev.index or 0)))
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    if not line:
+        return {"error": (out.stderr or out.stdout)[-300:]}
+    r = json.loads(line[-1])
+    F = 2 * (512 * 256 + 2 * 256 * 256 + 256)
+    ms = r["l0_ms"] + r["voxel_ms"]
+    r["roofline"] = {"bound": "tensor", "achieved": F * (r["leaf_voxels"] + r["active_voxels"]) / (ms * 1e-3) / 1e12,
+                     "unit": "TFLOP/s", "note": "flops of one expert evaluation per point (blending extra excluded)"}
+    return r
+
+
 def cpu_decode_sample(c, nleaf_sample=400):
     """Oracle timing on a bounded sample: the first leaves of the decode (L0 classify
     all their voxels, regress the active ones) + all level-1 slots."""
@@ -321,6 +343,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3-shaped multi-expert decode measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -410,6 +433,14 @@ def main():
     query = query_bench(m, dev, args.steps)
     query["lookup"]["roofline"]["peak"] = float(peaks["hbm_gbs"])
     query["lookup"]["roofline"]["frac"] = query["lookup"]["roofline"]["achieved"] / float(peaks["hbm_gbs"])
+    c3 = None
+    if rank == 0 and world == 1 and not args.no_c3:
+        try:
+            c3 = c3_decode(dev)
+            c3["roofline"]["peak"] = float(peaks["bf16_tflops"])
+            c3["roofline"]["frac"] = c3["roofline"]["achieved"] / float(peaks["bf16_tflops"])
+        except Exception as ex:  # noqa: BLE001 -- the headline line must still print
+            c3 = {"error": repr(ex)[:300]}
     # ---------------- e2e through the public API (host container -> host grid)
     e2e_t = []
     h2d = sum(w.nbytes + b.nbytes for e in c.experts for _, n in e.nets() if n is not None
@@ -450,6 +481,7 @@ def main():
                          "kernel_ms_per_step": kms / args.steps,
                          "per_stage_ms": {k: v[1] / args.steps for k, v in per_tag.items()}},
             "query": query,
+            "c3_decode": c3,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "voxels/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(round(launches)),

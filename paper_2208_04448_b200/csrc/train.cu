@@ -880,17 +880,35 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
     }
   };
   const int64_t poff0 = a.poff[0];
+  // two 16-column TMEM loads in flight per wait; streaming stores
+  auto rd2 = [&](uint32_t c0, uint32_t c1, bool two, float (&v0)[16], float (&v1)[16]) {
+    tmem_ld16(tmem + lane_off + c0, v0);
+    if (two) tmem_ld16(tmem + lane_off + c1, v1);
+    tmem_ld_wait();
+    if (none) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v0[i] = v1[i] = 0.f;
+    }
+  };
   for (int j = 0; j < nmt; ++j) {
     const int k = j * 128 + row;
     float* pk = part + poff0 + k;
-    for (int cc = half; cc < W / 16; cc += 2) {
-      float v[16];
-      rd(a.col_w0 + j * W + cc * 16, v);
+    for (int cc = half; cc < W / 16; cc += 4) {
+      const bool two = cc + 2 < W / 16;
+      float v0[16], v1[16];
+      rd2(a.col_w0 + j * W + cc * 16, a.col_w0 + j * W + (cc + 2) * 16, two, v0, v1);
       if (k < K0r) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int o = cc * 16 + i;
-          if (o < Wr) __stcs(pk + (int64_t)o * K0r, v[i]);
+          if (o < Wr) __stcs(pk + (int64_t)o * K0r, v0[i]);
+        }
+        if (two) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int o = (cc + 2) * 16 + i;
+            if (o < Wr) __stcs(pk + (int64_t)o * K0r, v1[i]);
+          }
         }
       }
     }
@@ -905,14 +923,23 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
     const int N = head ? 16 : W;
     const int outs = head ? nd.out_dim : Wr;
     const uint32_t col = head ? a.col_head : a.col_h + (l - 1) * W;
-    for (int cc = half; cc < N / 16; cc += 2) {
-      float v[16];
-      rd(col + cc * 16, v);
+    const int64_t pw = a.poff[2 * l], pb = a.poff[2 * l + 1];
+    for (int cc = half; cc < N / 16; cc += 4) {
+      const bool two = cc + 2 < N / 16;
+      float v0[16], v1[16];
+      rd2(col + cc * 16, col + (cc + 2) * 16, two, v0, v1);
+#pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int o = cc * 16 + i;
-        if (o >= outs) continue;
-        if (row < Wr) part[a.poff[2 * l] + (int64_t)o * Wr + row] = v[i];
-        if (row == W) part[a.poff[2 * l + 1] + o] = v[i];  // ones column -> bias gradient
+        if (o < outs) {
+          if (row < Wr) __stcs(part + pw + (int64_t)o * Wr + row, v0[i]);
+          if (row == W) part[pb + o] = v0[i];  // ones column -> bias gradient
+        }
+        const int o1 = (cc + 2) * 16 + i;
+        if (two && o1 < outs) {
+          if (row < Wr) __stcs(part + pw + (int64_t)o1 * Wr + row, v1[i]);
+          if (row == W) part[pb + o1] = v1[i];
+        }
       }
     }
   }

@@ -89,3 +89,53 @@ def test_packed_tree_layout_resolves_reference_lookups(golden):
     np.testing.assert_array_equal(v.view(np.uint32), z["values"][sel].view(np.uint32))
     np.testing.assert_array_equal(a.astype(bool), z["active"][sel])
     np.testing.assert_array_equal(k, z["kind"][sel])
+
+
+def test_patch_arrays_later_expert_overrides_like_a_dict():
+    """decoder.py:84-92: patch maps are dicts filled expert by expert."""
+    from paper_2208_04448_b200.decoder import _patch_arrays
+    rng = np.random.default_rng(3)
+    lists = []
+    for e in range(3):
+        keys = [tuple(int(v) for v in rng.integers(-64, 64, 3)) for _ in range(200)]
+        lists.append([(k, bool(rng.integers(0, 2)), float(rng.normal())) for k in keys])
+    ref = {}
+    for lst in lists:
+        for k, a, v in lst:
+            ref[k] = (a, v)
+    keys, act, val = _patch_arrays(lists, 2)
+    got = {tuple(int(x) for x in k): (bool(a), float(v)) for k, a, v in zip(keys, act, val)}
+    assert got == ref and keys.shape[0] == len(ref)
+    k1, c1 = _patch_arrays([[((0, 8, 16), 2)], [], [((0, 8, 16), 1), ((8, 8, 8), 0)]], 1)
+    assert {tuple(int(x) for x in k): int(c) for k, c in zip(k1, c1)} == {(0, 8, 16): 1, (8, 8, 8): 0}
+    k0, c0 = _patch_arrays([[], []], 1)
+    assert k0.shape == (0, 3) and c0.shape == (0,)
+
+
+def test_node_index_matches_dict_lookup():
+    """DeviceModel._node_index (dense code + searchsorted) == {origin: index}."""
+    from paper_2208_04448_b200.decoder import DeviceModel
+    rng = np.random.default_rng(4)
+    origins = np.unique(rng.integers(-20, 20, size=(300, 3)) * 128, axis=0).astype(np.int64)
+    m = DeviceModel.__new__(DeviceModel)
+    m.origins, m.n1 = origins, origins.shape[0]
+    lut = {tuple(o): i for i, o in enumerate(origins.tolist())}
+    keys = np.concatenate([origins[rng.permutation(len(origins))[:150]],
+                           rng.integers(-30, 30, size=(300, 3)) * 128,
+                           rng.integers(-3000, 3000, size=(50, 3))]).astype(np.int64)
+    got = m._node_index(keys)
+    ref = np.array([lut.get(tuple(k), -1) for k in keys.tolist()])
+    np.testing.assert_array_equal(got, ref)
+    assert (m._node_index(np.zeros((0, 3), np.int64)) == 0).all()
+
+
+def test_node_arrays_of_no_leaves():
+    from paper_2208_04448_b200.procgen import _nodes_from_leaves
+    l1o, l1c, l1a, l1t, l2o, l2c, l2a, l2t = _nodes_from_leaves(np.zeros((0, 3), np.int64), np.float32(0))
+    assert l1o.shape == (0, 3) and l2o.shape == (0, 3) and l1c.shape[0] == 0 and l2c.shape[0] == 0
+
+
+def test_bench_reads_committed_traffic():
+    import bench
+    t = bench.load_traffic()
+    assert t is not None and t["bytes_per_launch"] > 0 and os.path.exists(os.path.join(bench.ROOT, t["source"]))

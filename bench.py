@@ -252,6 +252,20 @@ def c3_decode(dev, size=1024):
     return r
 
 
+def c5_query(dev, nq=1_000_000_000):
+    """C5 shape (BASELINE configs[4]) on one GPU: 1e9 uniform coordinates in
+    [0, 2048)^3 through the hybrid grid of the 2048^3 narrow-band sphere
+    (69.5 M active voxels), Lucy-class 3x256 voxel nets with random weights
+    (tools/bench_c5.py)."""
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bench_c5.py"), str(nq)], capture_output=True,
+                         text=True, timeout=900,
+                         env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                                  or str(dev.index or 0)))
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    return json.loads(line[-1]) if line else {"error": (out.stderr or out.stdout)[-300:]}
+
+
 def cpu_decode_sample(c, nleaf_sample=400):
     """Oracle timing on a bounded sample: the first leaves of the decode (L0 classify
     all their voxels, regress the active ones) + all level-1 slots."""
@@ -344,6 +358,7 @@ def main():
     ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3-shaped multi-expert decode measurement")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5-shaped 1e9 random-query measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -441,6 +456,12 @@ def main():
             c3["roofline"]["frac"] = c3["roofline"]["achieved"] / float(peaks["bf16_tflops"])
         except Exception as ex:  # noqa: BLE001 -- the headline line must still print
             c3 = {"error": repr(ex)[:300]}
+    c5 = None
+    if rank == 0 and world == 1 and not args.no_c5:
+        try:
+            c5 = c5_query(dev)
+        except Exception as ex:  # noqa: BLE001 -- the headline line must still print
+            c5 = {"error": repr(ex)[:300]}
     # ---------------- e2e through the public API (host container -> host grid)
     e2e_t = []
     h2d = sum(w.nbytes + b.nbytes for e in c.experts for _, n in e.nets() if n is not None
@@ -482,6 +503,7 @@ def main():
                          "per_stage_ms": {k: v[1] / args.steps for k, v in per_tag.items()}},
             "query": query,
             "c3_decode": c3,
+            "c5_query": c5,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "voxels/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(round(launches)),

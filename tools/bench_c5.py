@@ -1,0 +1,72 @@
+"""C5-shaped random access (BASELINE configs[4]): 1e9 uniform
+int32 coordinates in [0, 2048)^3 (torch Philox, seed 0) through the hybrid
+grid of a 2048^3 narrow-band sphere (radius 960, half width 3: 69.5 M active
+voxels): upper-tree lookup, gate-blended voxel regressor (Lucy-class 3x256 /
+m256 nets with random weights -- the framework cannot train nets this wide
+yet; BASELINE.md allows random-init weights of the named architecture), value
+finalize.  The topology is the grid's own (what a perfectly trained
+classifier pair would reconstruct).
+
+    python tools/bench_c5.py [n_queries]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2208_04448_b200.decoder import NetEvaluator, hybrid_query  # noqa: E402
+from paper_2208_04448_b200.encoder import decompose, expert_norm, init_mlp  # noqa: E402
+from paper_2208_04448_b200.model import EncodedSubdomain, FourierFeatures, NetRecord, Activation  # noqa: E402
+from paper_2208_04448_b200.procgen import sphere_sdf  # noqa: E402
+from paper_2208_04448_b200.tree import DeviceTree  # noqa: E402
+
+nq = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_000_000_000
+dev = torch.device("cuda:0")
+t0 = time.perf_counter()
+g = sphere_sdf((1024.0, 1024.0, 1024.0), 960.0, 1.0, 3.0)
+tgen = time.perf_counter() - t0
+layout = decompose(g, 512)
+rng = np.random.default_rng(0)
+experts = []
+for sub in layout.subdomains:
+    no, ns = expert_norm(sub, g)
+    e = EncodedSubdomain(sub.id, sub.cell, sub.cluster_id, no, ns, 3.0)
+    p = init_mlp(512, [256] * 3, 1, Activation("sine", 3.0), "linear", 100 + sub.id)
+    w, b = p.layers[-1]
+    p.layers[-1] = (rng.normal(0, 0.2, size=w.shape).astype(np.float32), b)
+    e.voxel_regressor = NetRecord(p, FourierFeatures(256, 10.0, 200 + sub.id))
+    experts.append(e)
+ev = NetEvaluator(sorted(experts, key=lambda e: e.id), layout.size, layout.halo, float(g.background), dev)
+tree = DeviceTree(g)
+gen = torch.Generator(device=dev)
+gen.manual_seed(0)
+coords = torch.randint(0, 2048, (nq, 3), dtype=torch.int32, device=dev, generator=gen)
+
+
+def run():
+    return hybrid_query(tree, ev, coords, 3.0, True)
+
+
+_, _, nr = run()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+run()
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1)
+e0.record()
+tree.lookup(coords)
+e1.record()
+torch.cuda.synchronize()
+ms_lookup = e0.elapsed_time(e1)
+print(json.dumps({"workload": "C5-shaped: 2048^3 sphere (r 960, band 3), Lucy-class voxel nets (random weights), "
+                              f"{len(experts)} experts", "generate_s": round(tgen, 1),
+                  "active_voxels": int(g.leaf_active.sum()), "leaves": int(g.leaf_origins.shape[0]),
+                  "queries": nq, "regressor_rows": int(nr), "ms": round(ms, 2),
+                  "queries_per_s": nq / (ms * 1e-3), "lookup_ms": round(ms_lookup, 2),
+                  "lookup_queries_per_s": nq / (ms_lookup * 1e-3)}))

@@ -266,6 +266,18 @@ def c5_query(dev, nq=1_000_000_000):
     return json.loads(line[-1]) if line else {"error": (out.stderr or out.stdout)[-300:]}
 
 
+def c4_sequence(dev, frames=16):
+    """C4 shape (BASELINE configs[3]): 16-frame moving sphere at 512^3 encoded with
+    warm starts (encode_sequence on the GPU, ACCEPT nets; tools/bench_c4.py)."""
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bench_c4.py"), str(frames)],
+                         capture_output=True, text=True, timeout=900,
+                         env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                                  or str(dev.index or 0)))
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    return json.loads(line[-1]) if line else {"error": (out.stderr or out.stdout)[-300:]}
+
+
 def cpu_decode_sample(c, nleaf_sample=400):
     """Oracle timing on a bounded sample: the first leaves of the decode (L0 classify
     all their voxels, regress the active ones) + all level-1 slots."""
@@ -359,6 +371,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3-shaped multi-expert decode measurement")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5-shaped 1e9 random-query measurement")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4-shaped warm-start sequence measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -456,6 +469,12 @@ def main():
             c3["roofline"]["frac"] = c3["roofline"]["achieved"] / float(peaks["bf16_tflops"])
         except Exception as ex:  # noqa: BLE001 -- the headline line must still print
             c3 = {"error": repr(ex)[:300]}
+    c4 = None
+    if rank == 0 and world == 1 and not args.no_c4:
+        try:
+            c4 = c4_sequence(dev)
+        except Exception as ex:  # noqa: BLE001 -- the headline line must still print
+            c4 = {"error": repr(ex)[:300]}
     c5 = None
     if rank == 0 and world == 1 and not args.no_c5:
         try:
@@ -503,6 +522,7 @@ def main():
                          "per_stage_ms": {k: v[1] / args.steps for k, v in per_tag.items()}},
             "query": query,
             "c3_decode": c3,
+            "c4_sequence": c4,
             "c5_query": c5,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "voxels/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import sys
 from dataclasses import dataclass
 from typing import Dict, Optional, Tuple
 
@@ -41,6 +42,53 @@ def _stream(dev):
 
 def _ptr(t: Optional[torch.Tensor], byte_offset: int = 0):
     return None if t is None else t.data_ptr() + byte_offset
+
+
+class _PinnedPool:
+    """Reusable pinned host blocks for decode outputs.  A block is handed out
+    as numpy views of one pooled uint8 array; it is free again once every view
+    a caller holds is gone (reference count of the pooled array)."""
+
+    CAP = 4
+
+    def __init__(self):
+        self.blocks = []  # [pinned uint8 tensor, its numpy view]
+
+    def get(self, nbytes: int):
+        for blk in self.blocks:
+            if blk[1].size >= nbytes and sys.getrefcount(blk[1]) <= 2:  # held by blk + the call's argument
+                return blk
+        t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        blk = [t, t.numpy()]
+        if len(self.blocks) < self.CAP:
+            self.blocks.append(blk)
+        return blk
+
+
+_PINNED = _PinnedPool()
+
+
+def _to_host(ts):
+    """Device tensors -> numpy arrays over one pinned host block: asynchronous
+    copies on the current stream, one synchronize."""
+    offs, n = [], 0
+    for t in ts:
+        offs.append(n)
+        n += (t.numel() * t.element_size() + 255) & ~255
+    blk = _PINNED.get(n)
+    pin, arr = blk
+    outs = []
+    for t, o in zip(ts, offs):
+        nb = t.numel() * t.element_size()
+        pin[o:o + nb].view(t.dtype).view(t.shape).copy_(t, non_blocking=True)
+        outs.append(arr[o:o + nb].view(_NP_DTYPE[t.dtype]).reshape(tuple(t.shape)))
+    if ts:
+        torch.cuda.current_stream(ts[0].device).synchronize()
+    return outs
+
+
+_NP_DTYPE = {torch.uint8: np.uint8, torch.int32: np.int32, torch.int64: np.int64, torch.float32: np.float32,
+             torch.float64: np.float64, torch.bool: np.bool_}
 
 
 def _slot1(c) -> int:
@@ -173,10 +221,14 @@ class DeviceModel:
         # negative-fill bits of leaves inside a level-1 node
         nf = ut.leaf_negative_fill
         if nf:
-            norg = np.asarray(list(nf.keys()), dtype=np.int64).reshape(-1, 3)
+            norg = np.fromiter(itertools.chain.from_iterable(nf.keys()), dtype=np.int64,
+                               count=3 * len(nf)).reshape(-1, 3)
             nni = self._node_index(norg & ~np.int64(127))
             keep = nni >= 0
-            bits = np.concatenate([np.asarray(b, dtype=bool).reshape(-1) for b in nf.values()]).reshape(-1, LEAF_SIZE)
+            bits = np.concatenate(list(nf.values()), axis=None)  # each entry flattened (C order)
+            if bits.size != LEAF_SIZE * len(nf):
+                raise SvcodecError("corrupt container: negative-fill entry of the wrong size")
+            bits = bits.astype(bool, copy=False).reshape(-1, LEAF_SIZE)
             bits = bits[keep]
             self.neg_slot = self._i64(nni[keep] * L1_SIZE + _slot1_arr(norg[keep]))
             packed = np.packbits(bits, axis=1, bitorder="little")  # (n, 64) bytes = 8 x u64 per leaf
@@ -215,10 +267,10 @@ class DeviceModel:
         return lut[inv[self.n1:]]
 
     def _i64(self, xs):
-        return torch.tensor(np.asarray(xs, dtype=np.int64), device=self.dev)
+        return torch.from_numpy(np.ascontiguousarray(xs, dtype=np.int64)).to(self.dev)
 
     def _u8(self, xs):
-        return torch.tensor(np.asarray(xs, dtype=np.uint8), device=self.dev)
+        return torch.from_numpy(np.ascontiguousarray(xs, dtype=np.uint8)).to(self.dev)
 
     def close(self):
         self.ns.close()
@@ -383,11 +435,13 @@ class DeviceDecode:
         meta = c.grid_meta
         bg = np.float32(meta.background)
         n1 = m.n1
-        cls = self.l1_class.cpu().numpy().reshape(n1, L1_SIZE)
-        tiles = self.l1_tiles.cpu().numpy().reshape(n1, L1_SIZE)
-        lo = self.leaf_origins.cpu().numpy().astype(np.int64).reshape(-1, 3)
-        la = self.leaf_active.cpu().numpy().astype(bool).reshape(-1, LEAF_SIZE)
-        lv = self.leaf_values.cpu().numpy().reshape(-1, LEAF_SIZE)
+        cls, tiles, lo, la, lv = _to_host([self.l1_class, self.l1_tiles, self.leaf_origins,
+                                           self.leaf_active, self.leaf_values])
+        cls = cls.reshape(n1, L1_SIZE)
+        tiles = tiles.reshape(n1, L1_SIZE)
+        lo = lo.astype(np.int64).reshape(-1, 3)
+        la = la.view(np.bool_).reshape(-1, LEAF_SIZE)  # 0/1 bytes
+        lv = lv.reshape(-1, LEAF_SIZE)
         # canonical order: by root key then origin within the root
         roots = m.origins & ~np.int64(4095)
         order = np.lexsort((m.origins[:, 2], m.origins[:, 1], m.origins[:, 0],

@@ -13,7 +13,7 @@ from paper_2208_04448_b200.decoder import decode_full  # noqa: E402
 
 dev = torch.device("cuda:0")
 c = train_container(make_grid(os.environ.get("WORKLOAD", "c2")), accept_config(), dev, [])
-for _ in range(2):
+for _ in range(4):
     decode_full(c, dev)
 torch.cuda.synchronize()
 t0 = time.perf_counter()

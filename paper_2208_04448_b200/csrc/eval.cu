@@ -191,9 +191,18 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
     nvdb_netset_destroy(ns);
     return code;
   };
-  if (cudaMalloc(&ns->dev_blob, blob.size()) != cudaSuccess) return cleanup(fail(NVDB_ECUDA, "cudaMalloc blob"));
-  if (cudaMemcpy(ns->dev_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-    return cleanup(fail(NVDB_ECUDA, "upload blob"));
+  // one device allocation and one upload: [blob | nets | experts | cells | tagnet]
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t off_nets = al(blob.size());
+  const size_t off_exp = al(off_nets + sizeof(NetDev) * std::max(nnets, 1));
+  const size_t off_cells = al(off_exp + sizeof(ExpertDev) * std::max(nexperts, 1));
+  const size_t off_tag = al(off_cells + sizeof(int32_t) * cells.size());
+  const size_t all_bytes = off_tag + sizeof(int32_t) * tagnet.size();
+  if (cudaMalloc(&ns->dev_blob, all_bytes) != cudaSuccess) return cleanup(fail(NVDB_ECUDA, "cudaMalloc netset"));
+  ns->dev_nets = reinterpret_cast<NetDev*>(ns->dev_blob + off_nets);
+  ns->dev_experts = reinterpret_cast<ExpertDev*>(ns->dev_blob + off_exp);
+  ns->dev_cells = reinterpret_cast<int32_t*>(ns->dev_blob + off_cells);
+  ns->dev_tagnet = reinterpret_cast<int32_t*>(ns->dev_blob + off_tag);
   for (int i = 0; i < nnets; ++i) {
     hnets[i].wimg = ns->dev_blob + pieces[i].wimg;
     hnets[i].bias = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].bias);
@@ -202,16 +211,13 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
     hnets[i].b2pi = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].b2pi);
     hnets[i].lat = reinterpret_cast<const float*>(ns->dev_blob + pieces[i].lat);
   }
-  if (cudaMalloc(&ns->dev_nets, sizeof(NetDev) * std::max(nnets, 1)) != cudaSuccess ||
-      cudaMalloc(&ns->dev_experts, sizeof(ExpertDev) * std::max(nexperts, 1)) != cudaSuccess ||
-      cudaMalloc(&ns->dev_cells, sizeof(int32_t) * cells.size()) != cudaSuccess ||
-      cudaMalloc(&ns->dev_tagnet, sizeof(int32_t) * tagnet.size()) != cudaSuccess)
-    return cleanup(fail(NVDB_ECUDA, "cudaMalloc netset tables"));
-  if ((nnets && cudaMemcpy(ns->dev_nets, hnets.data(), sizeof(NetDev) * nnets, cudaMemcpyHostToDevice)) ||
-      (nexperts && cudaMemcpy(ns->dev_experts, hexp.data(), sizeof(ExpertDev) * nexperts, cudaMemcpyHostToDevice)) ||
-      cudaMemcpy(ns->dev_cells, cells.data(), sizeof(int32_t) * cells.size(), cudaMemcpyHostToDevice) ||
-      cudaMemcpy(ns->dev_tagnet, tagnet.data(), sizeof(int32_t) * tagnet.size(), cudaMemcpyHostToDevice))
-    return cleanup(fail(NVDB_ECUDA, "upload netset tables"));
+  blob.resize(all_bytes, 0);
+  if (nnets) std::memcpy(blob.data() + off_nets, hnets.data(), sizeof(NetDev) * nnets);
+  if (nexperts) std::memcpy(blob.data() + off_exp, hexp.data(), sizeof(ExpertDev) * nexperts);
+  std::memcpy(blob.data() + off_cells, cells.data(), sizeof(int32_t) * cells.size());
+  std::memcpy(blob.data() + off_tag, tagnet.data(), sizeof(int32_t) * tagnet.size());
+  if (cudaMemcpy(ns->dev_blob, blob.data(), all_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+    return cleanup(fail(NVDB_ECUDA, "upload netset"));
   ns->nets = hnets;
   ns->experts = hexp;
   ns->tagnet = tagnet;
@@ -221,11 +227,7 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
 
 extern "C" int nvdb_netset_destroy(nvdb_netset* ns) {
   if (!ns) return NVDB_OK;
-  cudaFree(ns->dev_blob);
-  cudaFree(ns->dev_nets);
-  cudaFree(ns->dev_experts);
-  cudaFree(ns->dev_cells);
-  cudaFree(ns->dev_tagnet);
+  cudaFree(ns->dev_blob);  // the tables live in the same allocation
   delete ns;
   return NVDB_OK;
 }

@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from ._lib import EvalOut, check, lib
 from .errors import SvcodecError
-from .model import (L1_SIZE, L2_SIZE, LEAF_SIZE, DenseLeafGrid)
+from .model import (L1_SIZE, L2_SIZE, LEAF_SIZE, DenseLeafGrid, LeafBitsMap, PatchRecords)
 from .netset import TAG_CODES, DeviceNetSet
 from .tree import DeviceTree
 
@@ -87,6 +87,7 @@ def _to_host(ts):
     return outs
 
 
+_TORCH_DTYPE = {np.uint8: torch.uint8, np.int32: torch.int32, np.int64: torch.int64, np.float32: torch.float32}
 _NP_DTYPE = {torch.uint8: np.uint8, torch.int32: np.int32, torch.int64: np.int64, torch.float32: np.float32,
              torch.float64: np.float64, torch.bool: np.bool_}
 
@@ -113,7 +114,13 @@ def _patch_arrays(lists, nfields: int):
     a key repeated by a later expert overrides the earlier one (decoder.py:84-92)."""
     keys, fields = [np.zeros((0, 3), np.int64)], [[np.zeros(0)] for _ in range(nfields)]
     for lst in lists:
-        if not lst:
+        if not len(lst):
+            continue
+        if isinstance(lst, PatchRecords):  # columns already (model.PatchRecords)
+            k, *cs = lst.arrays()
+            keys.append(k)
+            for f in range(nfields):
+                fields[f].append(cs[f].astype(np.float64))
             continue
         n = len(lst)
         cols = list(zip(*lst))
@@ -122,7 +129,7 @@ def _patch_arrays(lists, nfields: int):
             fields[f].append(np.fromiter(cols[1 + f], dtype=np.float64, count=n))
     k = np.concatenate(keys)
     fs = [np.concatenate(fl) for fl in fields]
-    if sum(1 for lst in lists if lst) > 1 and k.shape[0]:
+    if sum(1 for lst in lists if len(lst)) > 1 and k.shape[0]:
         # keep the last occurrence of each key, in first-occurrence order of the kept rows
         _, first_rev = np.unique(k[::-1], axis=0, return_index=True)
         last = np.sort(k.shape[0] - 1 - first_rev)
@@ -187,7 +194,7 @@ class DeviceModel:
                 raise SvcodecError(f"corrupt container: level-1 origin {o} has no level-2 child bit")
         self.origins = np.asarray(origins, dtype=np.int64).reshape(-1, 3)
         self.n1 = len(origins)
-        self.d_origins = torch.from_numpy(self.origins.astype(np.int32)).to(self.dev)
+        host = {"d_origins": self.origins.astype(np.int32)}  # device tables, uploaded together below
         # patch maps (decoder.py:84-92): later experts override earlier keys
         l1k, l1c = _patch_arrays([e.patches.l1 for e in c.experts], 1)
         l0k, l0a, l0v = _patch_arrays([e.patches.l0 for e in c.experts], 2)
@@ -195,8 +202,8 @@ class DeviceModel:
         if (ni1 < 0).any():
             bad = tuple(int(v) for v in l1k[np.flatnonzero(ni1 < 0)[0]])
             raise SvcodecError(f"corrupt container: level-1 patch {bad} outside every level-1 node")
-        self.p1_slot = self._i64(ni1 * L1_SIZE + _slot1_arr(l1k))
-        self.p1_cls = self._u8(l1c)
+        host["p1_slot"] = (ni1 * L1_SIZE + _slot1_arr(l1k)).astype(np.int64)
+        host["p1_cls"] = np.asarray(l1c).astype(np.uint8)
         # tile records per level-1 node
         ts, tv = [np.zeros(0, np.int64)], [np.zeros(0, np.float32)]
         torg = list(ut.l1_tiles.keys())
@@ -209,33 +216,53 @@ class DeviceModel:
                 if d:
                     ts.append(ni * L1_SIZE + np.fromiter(d.keys(), dtype=np.int64, count=len(d)))
                     tv.append(np.fromiter(d.values(), dtype=np.float32, count=len(d)))
-        self.t_slot = self._i64(np.concatenate(ts))
-        self.t_val = torch.from_numpy(np.concatenate(tv)).to(self.dev)
+        host["t_slot"] = np.concatenate(ts).astype(np.int64)
+        host["t_val"] = np.concatenate(tv).astype(np.float32)
         # level-0 patches: slot -1 when outside every level-1 node (checked in the decode)
         ni0 = self._node_index(l0k & ~np.int64(127))
-        self.p0_slot = self._i64(np.where(ni0 < 0, -1, ni0 * L1_SIZE + _slot1_arr(l0k)))
-        self.p0_vox = torch.from_numpy(_slot0_arr(l0k).astype(np.int32)).to(self.dev)
-        self.p0_act = self._u8(l0a)
-        self.p0_val = torch.from_numpy(l0v.astype(np.float32)).to(self.dev)
+        host["p0_slot"] = np.where(ni0 < 0, -1, ni0 * L1_SIZE + _slot1_arr(l0k)).astype(np.int64)
+        host["p0_vox"] = _slot0_arr(l0k).astype(np.int32)
+        host["p0_act"] = np.asarray(l0a).astype(np.uint8)
+        host["p0_val"] = l0v.astype(np.float32)
         self.l0_keys = l0k
         # negative-fill bits of leaves inside a level-1 node
         nf = ut.leaf_negative_fill
-        if nf:
-            norg = np.fromiter(itertools.chain.from_iterable(nf.keys()), dtype=np.int64,
-                               count=3 * len(nf)).reshape(-1, 3)
+        if len(nf):
+            if isinstance(nf, LeafBitsMap):  # columns already (model.LeafBitsMap)
+                norg, bits = nf.arrays()
+            else:
+                norg = np.fromiter(itertools.chain.from_iterable(nf.keys()), dtype=np.int64,
+                                   count=3 * len(nf)).reshape(-1, 3)
+                bits = np.concatenate(list(nf.values()), axis=None)  # each entry flattened (C order)
+                if bits.size != LEAF_SIZE * len(nf):
+                    raise SvcodecError("corrupt container: negative-fill entry of the wrong size")
+                bits = bits.astype(bool, copy=False).reshape(-1, LEAF_SIZE)
             nni = self._node_index(norg & ~np.int64(127))
             keep = nni >= 0
-            bits = np.concatenate(list(nf.values()), axis=None)  # each entry flattened (C order)
-            if bits.size != LEAF_SIZE * len(nf):
-                raise SvcodecError("corrupt container: negative-fill entry of the wrong size")
-            bits = bits.astype(bool, copy=False).reshape(-1, LEAF_SIZE)
             bits = bits[keep]
-            self.neg_slot = self._i64(nni[keep] * L1_SIZE + _slot1_arr(norg[keep]))
+            host["neg_slot"] = (nni[keep] * L1_SIZE + _slot1_arr(norg[keep])).astype(np.int64)
             packed = np.packbits(bits, axis=1, bitorder="little")  # (n, 64) bytes = 8 x u64 per leaf
-            self.neg_bits = torch.from_numpy(np.ascontiguousarray(packed).view(np.int64).reshape(-1, 8).copy()).to(self.dev)
+            host["neg_bits"] = np.ascontiguousarray(packed).view(np.int64).reshape(-1, 8)
         else:
-            self.neg_slot = self._i64(np.zeros(0, np.int64))
-            self.neg_bits = torch.zeros((0, 8), dtype=torch.int64, device=self.dev)
+            host["neg_slot"] = np.zeros(0, np.int64)
+            host["neg_bits"] = np.zeros((0, 8), np.int64)
+        self._upload(host)
+
+    def _upload(self, host: Dict[str, np.ndarray]) -> None:
+        """All device tables in one host buffer and one host->device copy;
+        each attribute is a typed view of the device buffer."""
+        offs, n = {}, 0
+        for k, a in host.items():
+            offs[k] = n
+            n += (a.nbytes + 255) & ~255
+        buf = np.zeros(max(n, 256), np.uint8)
+        for k, a in host.items():
+            buf[offs[k]:offs[k] + a.nbytes] = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
+        dbuf = torch.from_numpy(buf).to(self.dev)
+        self._tables = dbuf
+        for k, a in host.items():
+            t = dbuf[offs[k]:offs[k] + a.nbytes].view(_TORCH_DTYPE[a.dtype.type]).view(a.shape)
+            setattr(self, k, t)
 
     def _node_index(self, keys: np.ndarray) -> np.ndarray:
         """Level-1 node index (sorted-origin order) of each node-origin row, -1 if none."""
@@ -243,20 +270,36 @@ class DeviceModel:
         out = np.full(keys.shape[0], -1, np.int64)
         if keys.shape[0] == 0 or self.n1 == 0:
             return out
-        o = self.origins >> 7
-        lo = o.min(axis=0)
-        span = o.max(axis=0) - lo + 1
-        if float(span[0]) * float(span[1]) * float(span[2]) < 2.0 ** 62:
+        if getattr(self, "_nidx", None) is None:
+            o = self.origins >> 7
+            lo = o.min(axis=0)
+            span = o.max(axis=0) - lo + 1
+            dense = float(span[0]) * float(span[1]) * float(span[2]) < 2.0 ** 62
+            if dense:
+                oc = ((o[:, 0] - lo[0]) * span[1] + (o[:, 1] - lo[1])) * span[2] + (o[:, 2] - lo[2])
+                order = np.argsort(oc, kind="stable")
+                ncode = int(span[0]) * int(span[1]) * int(span[2])
+                lut = None
+                if ncode <= (1 << 24):  # small bounding box: direct table instead of a binary search
+                    lut = np.full(ncode, -1, np.int64)
+                    lut[oc[::-1]] = np.arange(self.n1)[::-1]  # first of any repeated origin wins
+                self._nidx = (lo, span, oc[order], order, lut)
+            else:
+                self._nidx = ()
+        if self._nidx:
             # dense code over the origins' bounding box; rows outside it have no node
-            def code(r):
-                return ((r[:, 0] - lo[0]) * span[1] + (r[:, 1] - lo[1])) * span[2] + (r[:, 2] - lo[2])
-            oc = code(o)
-            order = np.argsort(oc, kind="stable")
-            k = (keys >> 7) - lo
-            inside = ((k >= 0) & (k < span)).all(axis=1) & ((keys & 127) == 0).all(axis=1)
-            kc = code(keys[inside] >> 7)
-            pos = np.minimum(np.searchsorted(oc[order], kc), self.n1 - 1)
-            hit = oc[order][pos] == kc
+            lo, span, ocs, order, lut = self._nidx
+            # column-wise (reductions over a 3-wide axis are slow in numpy)
+            kx, ky, kz = ((keys[:, a] >> 7) - lo[a] for a in range(3))
+            inside = ((kx.astype(np.uint64) < np.uint64(span[0])) & (ky.astype(np.uint64) < np.uint64(span[1]))
+                      & (kz.astype(np.uint64) < np.uint64(span[2]))
+                      & (((keys[:, 0] | keys[:, 1] | keys[:, 2]) & 127) == 0))
+            kc = ((kx[inside] * span[1] + ky[inside]) * span[2] + kz[inside])
+            if lut is not None:
+                out[inside] = lut[kc]
+                return out
+            pos = np.minimum(np.searchsorted(ocs, kc), self.n1 - 1)
+            hit = ocs[pos] == kc
             out[np.flatnonzero(inside)[hit]] = order[pos[hit]]
             return out
         allk = np.concatenate([self.origins, keys])

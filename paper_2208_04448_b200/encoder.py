@@ -25,7 +25,7 @@ from .errors import EncodeError, SvcodecError
 from .model import (GRID_CLASS_SDF, L1_CLASS_ACTIVE_TILE, L1_CLASS_CHILD, L1_CLASS_INACTIVE_TILE,
                     L1_LOCAL, L1_SIZE, L2_SIZE, LEAF_LOCAL, LEAF_SIZE, Activation, DenseLeafGrid,
                     EncodedSubdomain, FourierFeatures, GridMeta, L2NodeRecord, Mask, MlpParams,
-                    NetRecord, NeuralGridContainer, PatchList, Subdomain, SubdomainLayout, UpperTree)
+                    LeafBitsMap, NetRecord, NeuralGridContainer, PatchList, Subdomain, SubdomainLayout, UpperTree)
 from .netset import _net_desc
 
 logger = logging.getLogger(__name__)
@@ -475,8 +475,8 @@ def extract_patches(grid: DenseLeafGrid, layout: SubdomainLayout, experts: List[
                 truth[active & ~child] = L1_CLASS_ACTIVE_TILE
                 truth[child] = L1_CLASS_CHILD
                 so = (org[:, None, :] + (L1_LOCAL * 8)[None]).reshape(-1, 3)
-                for i in np.flatnonzero(pred != truth):
-                    patches.l1.append((tuple(int(v) for v in so[i]), int(truth[i])))
+                bad = np.flatnonzero(pred != truth)
+                patches.l1.extend_arrays(so[bad], truth[bad])
             own0 = np.all((grid.leaf_origins >= sub.lo) & (grid.leaf_origins < sub.hi), axis=1) \
                 if grid.leaf_origins.shape[0] else np.zeros(0, bool)
             if own0.any():
@@ -496,9 +496,10 @@ def extract_patches(grid: DenseLeafGrid, layout: SubdomainLayout, experts: List[
                         keep &= values > eps
                     disagree &= keep
                 coords = (org[:, None, :] + LEAF_LOCAL[None]).reshape(-1, 3)
-                for i in np.flatnonzero(disagree):
-                    act = bool(truth[i])
-                    patches.l0.append((tuple(int(v) for v in coords[i]), act, float(values[i]) if act else 0.0))
+                bad = np.flatnonzero(disagree)
+                act = truth[bad].astype(bool)
+                patches.l0.extend_arrays(coords[bad], act,
+                                         np.where(act, values[bad].astype(np.float64), 0.0))
             expert.patches = patches
     finally:
         ev.close()
@@ -521,8 +522,8 @@ def build_upper_tree(grid: DenseLeafGrid) -> UpperTree:
         if inactive.any():
             tree.l1_tiles[org] = {int(i): float(grid.l1_tiles[ni, i]) for i in np.flatnonzero(inactive)}
     neg = ~grid.leaf_active & (grid.leaf_values < 0)
-    for li in np.flatnonzero(neg.any(axis=1)):
-        tree.leaf_negative_fill[tuple(int(v) for v in grid.leaf_origins[li])] = neg[li].copy()
+    sel = np.flatnonzero(neg.any(axis=1))
+    tree.leaf_negative_fill = LeafBitsMap.from_arrays(grid.leaf_origins[sel], neg[sel])
     tree.l1_origins.sort()
     return tree
 

@@ -16,6 +16,8 @@ plumbing and never on the hot path.
 
 from __future__ import annotations
 
+import itertools
+from collections.abc import MutableMapping
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
 
@@ -178,19 +180,209 @@ class L2NodeRecord:
     tiles: Dict[int, float] = field(default_factory=dict)
 
 
+class LeafBitsMap(MutableMapping):
+    """Array-backed ``{leaf origin: (512,) bool}`` (the reference's
+    ``UpperTree.leaf_negative_fill`` dict, container.py / encoder.py:519-526):
+    a mapping for lookups, iteration and assignment that hands the decoder its
+    (n, 3) origins and (n, 512) bits without a per-leaf conversion."""
+
+    def __init__(self, items=None):
+        self._keys = np.zeros((0, 3), np.int64)
+        self._bits = np.zeros((0, LEAF_SIZE), bool)
+        self._index = None  # origin tuple -> row, built on first keyed access
+        self._extra = {}    # keys assigned one by one, merged on arrays()
+        if items:
+            for k, v in (items.items() if hasattr(items, "items") else items):
+                self[k] = v
+
+    @classmethod
+    def from_arrays(cls, keys, bits) -> "LeafBitsMap":
+        m = cls()
+        keys = np.asarray(keys, np.int64).reshape(-1, 3)
+        bits = np.asarray(bits, bool).reshape(-1, LEAF_SIZE)
+        if keys.shape[0] != bits.shape[0]:
+            raise ValueError("leaf origins and bit rows differ in count")
+        if keys.shape[0] and np.unique(keys, axis=0).shape[0] != keys.shape[0]:
+            raise ValueError("duplicate leaf origins")
+        m._keys, m._bits = keys.copy(), bits.copy()
+        return m
+
+    def arrays(self):
+        """(origins (n, 3) int64, bits (n, 512) bool) in insertion order."""
+        if self._extra:
+            n0 = self._keys.shape[0]
+            ks = np.asarray(list(self._extra.keys()), np.int64).reshape(-1, 3)
+            bs = np.stack(list(self._extra.values()))
+            self._keys = np.concatenate([self._keys, ks])
+            self._bits = np.concatenate([self._bits, bs])
+            if self._index is not None:
+                self._index.update((k, n0 + i) for i, k in enumerate(self._extra))
+            self._extra = {}
+        return self._keys, self._bits
+
+    def _row(self, key):
+        """Row of an origin in the arrays (extras not included), or None."""
+        if self._index is None:
+            self._index = {tuple(int(v) for v in k): i for i, k in enumerate(self._keys)}
+        return self._index.get(key)
+
+    def __getitem__(self, key):
+        key = tuple(int(v) for v in key)
+        if key in self._extra:
+            return self._extra[key]
+        i = self._row(key)
+        if i is None:
+            raise KeyError(key)
+        return self._bits[i]
+
+    def __setitem__(self, key, value):
+        key = tuple(int(v) for v in key)
+        v = np.asarray(value, bool).reshape(LEAF_SIZE)
+        i = self._row(key) if self._keys.shape[0] and key not in self._extra else None
+        if i is None:
+            self._extra[key] = v
+        else:
+            self._bits[i] = v
+
+    def __delitem__(self, key):
+        key = tuple(int(v) for v in key)
+        if key in self._extra:
+            del self._extra[key]
+            return
+        i = self._row(key)
+        if i is None:
+            raise KeyError(key)
+        self._keys = np.delete(self._keys, i, axis=0)
+        self._bits = np.delete(self._bits, i, axis=0)
+        self._index = None
+
+    def __iter__(self):
+        self.arrays()
+        return (tuple(int(v) for v in k) for k in self._keys)
+
+    def __len__(self) -> int:
+        return self._keys.shape[0] + len(self._extra)
+
+    def __repr__(self) -> str:
+        return f"LeafBitsMap(n={len(self)})"
+
+    def __getstate__(self):
+        k, b = self.arrays()
+        return (k, np.packbits(b, axis=1, bitorder="little"))
+
+    def __setstate__(self, st):
+        self._keys = st[0]
+        self._bits = np.unpackbits(st[1], axis=1, count=LEAF_SIZE, bitorder="little").astype(bool)
+        self._index, self._extra = None, {}
+
+
 @dataclass
 class UpperTree:
     root_tiles: Dict[Coord, Tuple[float, bool]] = field(default_factory=dict)
     l2_nodes: List[L2NodeRecord] = field(default_factory=list)
     l1_origins: List[Coord] = field(default_factory=list)
     l1_tiles: Dict[Coord, Dict[int, float]] = field(default_factory=dict)
-    leaf_negative_fill: Dict[Coord, np.ndarray] = field(default_factory=dict)
+    leaf_negative_fill: LeafBitsMap = field(default_factory=LeafBitsMap)
+
+
+class PatchRecords:
+    """Array-backed list of patch records (container.py:100-117 keeps Python
+    lists of tuples): level-1 records ``(origin, cls)``, level-0 records
+    ``(coord, active, value)``.  Behaves as the reference's list for
+    ``append`` / iteration / indexing / ``len`` / ``==``, and hands the decoder
+    its columns without a per-record conversion (:meth:`arrays`)."""
+
+    __slots__ = ("level", "_keys", "_cols", "_pending")
+
+    def __init__(self, level: int, records=()):
+        self.level = int(level)
+        self._keys = np.zeros((0, 3), np.int64)
+        self._cols = [np.zeros(0, np.int64)] if self.level == 1 else [np.zeros(0, bool), np.zeros(0, np.float64)]
+        self._pending = []
+        for r in records:
+            self.append(r)
+
+    def append(self, rec) -> None:
+        self._pending.append(rec)
+
+    def extend_arrays(self, keys, *cols) -> None:
+        """Append records given as columns: keys (n, 3) and the record's fields."""
+        self._flush()
+        keys = np.asarray(keys, np.int64).reshape(-1, 3)
+        if len(cols) != len(self._cols) or any(np.shape(c) != (keys.shape[0],) for c in cols):
+            raise ValueError("patch columns do not match the record layout")
+        self._keys = np.concatenate([self._keys, keys])
+        self._cols = [np.concatenate([a, np.asarray(c, a.dtype)]) for a, c in zip(self._cols, cols)]
+
+    def _flush(self) -> None:
+        if not self._pending:
+            return
+        lst, self._pending = self._pending, []
+        n = len(lst)
+        cols = list(zip(*lst))
+        keys = np.fromiter(itertools.chain.from_iterable(cols[0]), dtype=np.int64, count=3 * n).reshape(-1, 3)
+        self._keys = np.concatenate([self._keys, keys])
+        self._cols = [np.concatenate([a, np.fromiter(c, dtype=a.dtype, count=n)]) for a, c in zip(self._cols, cols[1:])]
+
+    def arrays(self):
+        """(keys (n, 3) int64, *columns): l1 -> (cls int64,), l0 -> (active bool, value float64)."""
+        self._flush()
+        return (self._keys, *self._cols)
+
+    def __len__(self) -> int:
+        return self._keys.shape[0] + len(self._pending)
+
+    def _record(self, i: int):
+        k = tuple(int(v) for v in self._keys[i])
+        if self.level == 1:
+            return (k, int(self._cols[0][i]))
+        return (k, bool(self._cols[0][i]), float(self._cols[1][i]))
+
+    def __getitem__(self, i):
+        self._flush()
+        if isinstance(i, slice):
+            return [self._record(j) for j in range(*i.indices(len(self)))]
+        n = len(self)
+        if not -n <= i < n:
+            raise IndexError("patch index out of range")
+        return self._record(i % n)
+
+    def __iter__(self):
+        self._flush()
+        return (self._record(i) for i in range(len(self)))
+
+    def __eq__(self, other) -> bool:
+        try:
+            return len(self) == len(other) and all(a == b for a, b in zip(self, other))
+        except TypeError:
+            return NotImplemented
+
+    def __repr__(self) -> str:
+        return f"PatchRecords(level={self.level}, n={len(self)})"
+
+    def __getstate__(self):
+        self._flush()
+        return (self.level, self._keys, self._cols)
+
+    def __setstate__(self, st):
+        self.level, self._keys, self._cols = st
+        self._pending = []
+
+
+def _patch_records(level: int, records):
+    if isinstance(records, PatchRecords):
+        return records
+    return PatchRecords(level, records)
 
 
 @dataclass
 class PatchList:
-    l1: List[Tuple[Coord, int]] = field(default_factory=list)
-    l0: List[Tuple[Coord, bool, float]] = field(default_factory=list)
+    l1: PatchRecords = field(default_factory=lambda: PatchRecords(1))
+    l0: PatchRecords = field(default_factory=lambda: PatchRecords(0))
+
+    def __post_init__(self):
+        self.l1 = _patch_records(1, self.l1)
+        self.l0 = _patch_records(0, self.l0)
 
     def __len__(self) -> int:
         return len(self.l1) + len(self.l0)
@@ -383,8 +575,7 @@ def container_from_any(c) -> NeuralGridContainer:
                   for n in ut.l2_nodes],
         l1_origins=[tuple(int(v) for v in o) for o in ut.l1_origins],
         l1_tiles={tuple(k): dict(v) for k, v in ut.l1_tiles.items()},
-        leaf_negative_fill={tuple(k): np.asarray(v, dtype=bool).copy()
-                            for k, v in ut.leaf_negative_fill.items()},
+        leaf_negative_fill=_copy_leaf_bits(ut.leaf_negative_fill),
     )
     lay = c.layout
     layout = SubdomainLayout(size=int(lay.size), halo=int(lay.halo),
@@ -403,9 +594,7 @@ def container_from_any(c) -> NeuralGridContainer:
             tile_regressor=_net_from_any(e.tile_regressor),
             l0_classifier=_net_from_any(e.l0_classifier),
             voxel_regressor=_net_from_any(e.voxel_regressor),
-            patches=PatchList(
-                l1=[(tuple(int(v) for v in o), int(k)) for o, k in e.patches.l1],
-                l0=[(tuple(int(v) for v in o), bool(a), float(v)) for o, a, v in e.patches.l0]),
+            patches=_copy_patches(e.patches),
         )
         experts.append(ex)
     return NeuralGridContainer(meta, tree, layout, experts, getattr(c, "config", None),
@@ -440,9 +629,10 @@ def container_to_arrays(c, prefix: str = "c_") -> Dict[str, np.ndarray]:
     a["l1_origin"] = np.asarray(ut.l1_origins, dtype=np.int64).reshape(-1, 3)
     t = [(*o, k, v) for o, d in sorted(ut.l1_tiles.items()) for k, v in sorted(d.items())]
     a["l1_tiles"] = np.asarray(t, dtype=np.float64).reshape(-1, 5)
-    nk = sorted(ut.leaf_negative_fill)
-    a["neg_origin"] = np.asarray(nk, dtype=np.int64).reshape(-1, 3)
-    a["neg_bits"] = np.packbits(np.asarray([ut.leaf_negative_fill[k] for k in nk], dtype=bool).reshape(-1, LEAF_SIZE), axis=1)
+    nk, nb = _copy_leaf_bits(ut.leaf_negative_fill).arrays()
+    order = np.lexsort((nk[:, 2], nk[:, 1], nk[:, 0])) if nk.shape[0] else np.zeros(0, np.int64)
+    a["neg_origin"] = nk[order].reshape(-1, 3)
+    a["neg_bits"] = np.packbits(nb[order].reshape(-1, LEAF_SIZE), axis=1)
     lay = c.layout
     a["layout"] = np.array([lay.size, lay.halo, lay.cluster_count], dtype=np.int64)
     a["sub_cells"] = np.asarray([[*s.cell, s.cluster_id] for s in lay.subdomains], dtype=np.int64).reshape(-1, 4)
@@ -463,9 +653,11 @@ def container_to_arrays(c, prefix: str = "c_") -> Dict[str, np.ndarray]:
             for li, (w, b) in enumerate(pr.layers):
                 a[q + f"w{li}"] = np.asarray(w, dtype=np.float32)
                 a[q + f"b{li}"] = np.asarray(b, dtype=np.float32)
-        a[p + "pl1"] = np.asarray([[*o, k] for o, k in e.patches.l1], dtype=np.int64).reshape(-1, 4)
-        a[p + "pl0"] = np.asarray([[*o, int(act)] for o, act, _ in e.patches.l0], dtype=np.int64).reshape(-1, 4)
-        a[p + "pl0v"] = np.asarray([v for _, _, v in e.patches.l0], dtype=np.float64)
+        k1, c1 = _patch_records(1, e.patches.l1).arrays()
+        k0, a0, v0 = _patch_records(0, e.patches.l0).arrays()
+        a[p + "pl1"] = np.concatenate([k1, c1[:, None]], axis=1).astype(np.int64).reshape(-1, 4)
+        a[p + "pl0"] = np.concatenate([k0, a0[:, None].astype(np.int64)], axis=1).reshape(-1, 4)
+        a[p + "pl0v"] = np.asarray(v0, dtype=np.float64).copy()
     return {prefix + k: v for k, v in a.items()}
 
 
@@ -487,8 +679,8 @@ def container_from_arrays(a, prefix: str = "c_") -> NeuralGridContainer:
     for x, y, z, k, v in g("l1_tiles"):
         tree.l1_tiles.setdefault((int(x), int(y), int(z)), {})[int(k)] = float(v)
     nb = np.unpackbits(g("neg_bits"), axis=1, count=LEAF_SIZE).astype(bool)
-    for o, bits in zip(g("neg_origin"), nb):
-        tree.leaf_negative_fill[tuple(int(x) for x in o)] = bits
+    tree.leaf_negative_fill = LeafBitsMap.from_arrays(np.asarray(g("neg_origin"), np.int64).reshape(-1, 3),
+                                                      nb.reshape(-1, LEAF_SIZE))
     size, halo, ccount = (int(v) for v in g("layout"))
     layout = SubdomainLayout(size=size, halo=halo, cluster_count=ccount)
     for sid, row in enumerate(g("sub_cells")):
@@ -514,9 +706,10 @@ def container_from_arrays(a, prefix: str = "c_") -> NeuralGridContainer:
             ff = FourierFeatures(int(h[6]), float(h[5]), seed, float(h[7]))
             params = MlpParams(layers, Activation(_INV_ACT[int(h[1])], float(h[2])), _INV_HEAD[int(h[3])])
             setattr(ex, attr, NetRecord(params, ff, float(h[8]), int(h[9])))
-        ex.patches = PatchList(
-            l1=[(tuple(int(v) for v in r[:3]), int(r[3])) for r in g(p + "pl1")],
-            l0=[(tuple(int(v) for v in r[:3]), bool(r[3]), float(v)) for r, v in zip(g(p + "pl0"), g(p + "pl0v"))])
+        ex.patches = PatchList()
+        r1, r0 = np.asarray(g(p + "pl1"), np.int64).reshape(-1, 4), np.asarray(g(p + "pl0"), np.int64).reshape(-1, 4)
+        ex.patches.l1.extend_arrays(r1[:, :3], r1[:, 3])
+        ex.patches.l0.extend_arrays(r0[:, :3], r0[:, 3] != 0, np.asarray(g(p + "pl0v"), np.float64).reshape(-1))
         experts.append(ex)
     return NeuralGridContainer(meta, tree, layout, experts, None, 32)
 
@@ -558,3 +751,24 @@ def grid_from_arrays(a, prefix: str = "g_") -> DenseLeafGrid:
         leaf_active=np.unpackbits(g("leaf_active"), axis=1, count=LEAF_SIZE).astype(bool),
         leaf_values=g("leaf_values").astype(np.float32),
     )
+
+
+def _copy_patches(pl) -> PatchList:
+    """A PatchList of PatchRecords from any patch container (reference lists of tuples included)."""
+    out = PatchList()
+    for level, src, dst in ((1, pl.l1, out.l1), (0, pl.l0, out.l0)):
+        cols = _patch_records(level, src).arrays()
+        dst.extend_arrays(*[c.copy() for c in cols])
+    return out
+
+
+def _copy_leaf_bits(m) -> LeafBitsMap:
+    """A LeafBitsMap copy of any {origin: bits} mapping (reference dicts included)."""
+    if isinstance(m, LeafBitsMap):
+        k, b = m.arrays()
+        return LeafBitsMap.from_arrays(k, b)
+    out = LeafBitsMap()
+    for k, v in m.items():
+        out[k] = np.asarray(v, dtype=bool).reshape(-1).copy()
+    out.arrays()
+    return out

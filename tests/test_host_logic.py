@@ -110,6 +110,45 @@ def test_patch_arrays_later_expert_overrides_like_a_dict():
     assert {tuple(int(x) for x in k): int(c) for k, c in zip(k1, c1)} == {(0, 8, 16): 1, (8, 8, 8): 0}
     k0, c0 = _patch_arrays([[], []], 1)
     assert k0.shape == (0, 3) and c0.shape == (0,)
+    # the same through array-backed records (model.PatchRecords), mixed with plain lists
+    from paper_2208_04448_b200.model import PatchRecords
+    recs = [PatchRecords(0, lists[0]), lists[1], PatchRecords(0)]
+    recs[2].extend_arrays(np.array([k for k, _, _ in lists[2]]), np.array([a for _, a, _ in lists[2]]),
+                          np.array([v for _, _, v in lists[2]]))
+    keys2, act2, val2 = _patch_arrays(recs, 2)
+    np.testing.assert_array_equal(keys2, keys)
+    np.testing.assert_array_equal(act2, act)
+    np.testing.assert_array_equal(val2, val)
+
+
+def test_patch_records_behave_like_the_reference_lists():
+    """container.py:100-117 / 345-351 / 455-460: PatchList.l1 / .l0 are lists of
+    (origin, cls) / (coord, active, value) that the encoder appends to and the
+    writer iterates."""
+    import pickle
+    from paper_2208_04448_b200.model import (PatchList, container_from_arrays, container_to_arrays)
+    ref0 = [((70, 127, 247), True, 2.963477849960327), ((-8, 0, 5), False, 0.0), ((1, 2, 3), True, -0.25)]
+    ref1 = [((0, 0, 128), 2), ((-128, 8, 16), 0)]
+    pl = PatchList()
+    for r in ref0:
+        pl.l0.append(r)
+    pl.l1.extend_arrays(np.array([k for k, _ in ref1]), np.array([c for _, c in ref1]))
+    assert list(pl.l0) == ref0 and pl.l0 == ref0 and pl.l1 == ref1 and len(pl) == 5
+    assert pl.l0[1] == ref0[1] and pl.l0[-1] == ref0[-1] and pl.l1[0:1] == ref1[0:1]
+    assert [type(x) for x in pl.l0[0]] == [tuple, bool, float] and type(pl.l0[0][0][0]) is int
+    with pytest.raises(IndexError):
+        pl.l1[2]
+    assert pickle.loads(pickle.dumps(pl)) == pl
+    assert PatchList(l1=ref1, l0=ref0) == pl
+    with pytest.raises(ValueError):
+        pl.l0.extend_arrays(np.zeros((2, 3)), np.zeros(2, bool), np.zeros(3))
+    # container arrays round trip keeps the records
+    from conftest import load_golden
+    c = container_from_arrays(load_golden("decode_multi"))
+    assert sum(len(e.patches) for e in c.experts) > 0
+    c2 = container_from_arrays(container_to_arrays(c))
+    for a, b in zip(c.experts, c2.experts):
+        assert a.patches == b.patches
 
 
 def test_node_index_matches_dict_lookup():
@@ -127,6 +166,15 @@ def test_node_index_matches_dict_lookup():
     ref = np.array([lut.get(tuple(k), -1) for k in keys.tolist()])
     np.testing.assert_array_equal(got, ref)
     assert (m._node_index(np.zeros((0, 3), np.int64)) == 0).all()
+    # a bounding box too large for the direct table (binary-search path)
+    far = origins.copy()
+    far[::2, 0] += np.int64(1 << 36)
+    m2 = DeviceModel.__new__(DeviceModel)
+    m2.origins, m2.n1 = far, far.shape[0]
+    lut2 = {tuple(o): i for i, o in enumerate(far.tolist())}
+    keys2 = np.concatenate([far[rng.permutation(len(far))[:150]], keys]).astype(np.int64)
+    np.testing.assert_array_equal(m2._node_index(keys2), np.array([lut2.get(tuple(k), -1) for k in keys2.tolist()]))
+    assert m2._nidx[4] is None and m._nidx[4] is not None
 
 
 def test_node_arrays_of_no_leaves():
@@ -139,3 +187,36 @@ def test_bench_reads_committed_traffic():
     import bench
     t = bench.load_traffic()
     assert t is not None and t["bytes_per_launch"] > 0 and os.path.exists(os.path.join(bench.ROOT, t["source"]))
+
+
+def test_leaf_bits_map_behaves_like_the_reference_dict():
+    """UpperTree.leaf_negative_fill (encoder.py:519-526) is a {leaf origin: (512,) bool} dict."""
+    import pickle
+    from paper_2208_04448_b200.model import LeafBitsMap
+    rng = np.random.default_rng(0)
+    d, m = {}, LeafBitsMap()
+    for _ in range(50):
+        k = tuple(int(v) for v in rng.integers(-100, 100, 3) * 8)
+        b = rng.random(512) < 0.3
+        d[k] = b
+        m[k] = b
+    m2 = LeafBitsMap.from_arrays(*m.arrays())
+    for k in list(d)[:10]:
+        b = rng.random(512) < 0.5
+        d[k] = b
+        m2[k] = b
+    d[(8, 8, 8)] = np.ones(512, bool)
+    m2[(8, 8, 8)] = d[(8, 8, 8)]
+    k3 = list(d)[3]
+    del d[k3]
+    del m2[k3]
+    assert list(d) == list(m2) and len(d) == len(m2) and all((d[k] == m2[k]).all() for k in d)
+    assert (8, 8, 8) in m2 and (1, 2, 3) not in m2
+    with pytest.raises(KeyError):
+        m2[(1, 2, 3)]
+    m3 = pickle.loads(pickle.dumps(m2))
+    assert list(m3) == list(m2) and all((m3[k] == m2[k]).all() for k in d)
+    keys, bits = m3.arrays()
+    assert keys.shape == (len(d), 3) and bits.shape == (len(d), 512) and bits.dtype == bool
+    with pytest.raises(ValueError):
+        LeafBitsMap.from_arrays(np.zeros((2, 3)), np.zeros((2, 512), bool))  # duplicate origins

@@ -197,7 +197,6 @@ class DeviceModel:
         host = {"d_origins": self.origins.astype(np.int32)}  # device tables, uploaded together below
         # patch maps (decoder.py:84-92): later experts override earlier keys
         l1k, l1c = _patch_arrays([e.patches.l1 for e in c.experts], 1)
-        l0k, l0a, l0v = _patch_arrays([e.patches.l0 for e in c.experts], 2)
         ni1 = self._node_index(l1k & ~np.int64(127))
         if (ni1 < 0).any():
             bad = tuple(int(v) for v in l1k[np.flatnonzero(ni1 < 0)[0]])
@@ -218,13 +217,24 @@ class DeviceModel:
                     tv.append(np.fromiter(d.values(), dtype=np.float32, count=len(d)))
         host["t_slot"] = np.concatenate(ts).astype(np.int64)
         host["t_val"] = np.concatenate(tv).astype(np.float32)
+        self._tables = []
+        self._upload(host)
+        self._l0_ready = False  # level-0 tables: built by _ensure_l0 (decode overlaps them with the L0 stage)
+
+    def _ensure_l0(self) -> None:
+        """Level-0 patch and negative-fill tables (host conversion + upload)."""
+        if self._l0_ready:
+            return
+        c, ut = self.c, self.c.upper_tree
+        host = {}
+        l0k, l0a, l0v = _patch_arrays([e.patches.l0 for e in c.experts], 2)
         # level-0 patches: slot -1 when outside every level-1 node (checked in the decode)
         ni0 = self._node_index(l0k & ~np.int64(127))
         host["p0_slot"] = np.where(ni0 < 0, -1, ni0 * L1_SIZE + _slot1_arr(l0k)).astype(np.int64)
         host["p0_vox"] = _slot0_arr(l0k).astype(np.int32)
         host["p0_act"] = np.asarray(l0a).astype(np.uint8)
         host["p0_val"] = l0v.astype(np.float32)
-        self.l0_keys = l0k
+        self._l0_keys = l0k
         # negative-fill bits of leaves inside a level-1 node
         nf = ut.leaf_negative_fill
         if len(nf):
@@ -247,6 +257,13 @@ class DeviceModel:
             host["neg_slot"] = np.zeros(0, np.int64)
             host["neg_bits"] = np.zeros((0, 8), np.int64)
         self._upload(host)
+        self._l0_ready = True
+
+    @property
+    def l0_keys(self) -> np.ndarray:
+        """(n, 3) level-0 patch coordinates after the later-expert override."""
+        self._ensure_l0()
+        return self._l0_keys
 
     def _upload(self, host: Dict[str, np.ndarray]) -> None:
         """All device tables in one host buffer and one host->device copy;
@@ -259,7 +276,7 @@ class DeviceModel:
         for k, a in host.items():
             buf[offs[k]:offs[k] + a.nbytes] = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
         dbuf = torch.from_numpy(buf).to(self.dev)
-        self._tables = dbuf
+        self._tables.append(dbuf)
         for k, a in host.items():
             t = dbuf[offs[k]:offs[k] + a.nbytes].view(_TORCH_DTYPE[a.dtype.type]).view(a.shape)
             setattr(self, k, t)
@@ -423,6 +440,7 @@ class DeviceModel:
                                        _ptr(leaf_of_slot), st), "nvdb_leaf_list")
         act = torch.zeros(max(nl * LEAF_SIZE, 1), dtype=torch.uint8, device=dev)
         self.evaluate("l0", _lib.SRC_LEAF_VOX, leaf_origins, nl * LEAF_SIZE, _lib.OUT_L0ACTIVE, u8=act)
+        self._ensure_l0()  # host work while the L0 stage runs
         err = torch.zeros(1, dtype=torch.int32, device=dev)
         check(lib().nvdb_l0_apply(_ptr(act), _ptr(self.p0_slot), _ptr(self.p0_vox), _ptr(self.p0_act),
                                   self.p0_slot.numel(), _ptr(leaf_of_slot), _ptr(err), st), "nvdb_l0_apply")

@@ -353,7 +353,7 @@ __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather
     if (e < 0) continue;
     const int net = tagnet[4 * e + tag];
     if (net < 0) continue;
-    if (!(gate_weight(cell, S, halo, c) > 0.0)) continue;
+    if (!(gate_weight(cell, S, halo, c, 0.5 / (double)halo) > 0.0)) continue;
     if (found == pass) key = net;
     ++found;
   }

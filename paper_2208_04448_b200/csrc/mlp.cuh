@@ -165,14 +165,15 @@ __device__ __forceinline__ bool point_centre(int kind, const void* src, int64_t 
 }
 
 // clamped-tent gate weight of the expert owning `cell` (partition.py:123-139)
-__device__ __forceinline__ double gate_weight(const int cell[3], int S, int halo, const double c[3]) {
+__device__ __forceinline__ double gate_weight(const int cell[3], int S, int halo, const double c[3],
+                                              double inv2h) {  // inv2h: 0.5 / halo, hoisted by the caller
   const double h = (double)halo;
   double w = 1.0;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const double lo = (double)cell[i] * S;
     const double hi = lo + S;
-    double ramp = fmin(c[i] - (lo - h), (hi + h) - c[i]) * (0.5 / h);  // exact: h is a power of two
+    double ramp = fmin(c[i] - (lo - h), (hi + h) - c[i]) * inv2h;  // inv2h = 0.5 / h (exact: h is a power of two)
     ramp = fmin(fmax(ramp, 0.0), 1.0);
     w *= ramp;
   }
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t dcol = tmem_base + (uint32_t)(g * a.tcols);
   const bool issuer = p == 0;
+  const double inv2h = 0.5 / (double)a.halo;
 
   const int npairs = a.npairs_dev ? *a.npairs_dev : a.npairs;
   const int per_cta = (npairs + gridDim.x - 1) / gridDim.x;
@@ -661,7 +663,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       const int64_t sid = a.gather ? a.gather[id] : id;
       double c3[3];
       point_centre(a.src_kind, a.src, sid, c3);
-      gwt = gate_weight(s_exp.cell, a.subdomain_size, a.halo, c3);
+      gwt = gate_weight(s_exp.cell, a.subdomain_size, a.halo, c3, inv2h);
     }
     // transform (inference.py:29-36) in float32
     float tv[kMaxOut];
@@ -704,7 +706,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     const bool covered = den > 0.0;
     if (covered) {
 #pragma unroll
-      for (int k = 0; k < kMaxOut; ++k) num[k] = num[k] / den;
+      for (int k = 0; k < kMaxOut; ++k) num[k] = den == 1.0 ? num[k] : num[k] / den;  // x / 1 == x
     }
     switch (a.out_mode) {
       case OUT_PROBS:

@@ -122,6 +122,17 @@ def fwd_flops(net) -> int:
     return int(sum(2 * w.shape[0] * w.shape[1] for w, _ in net.params.layers))
 
 
+def transcendentals(net) -> int:
+    """MUFU co-bound per point of a forward pass: 2m Fourier
+    features + depth*width activations (sine nets; relu/tanh nets count 2m)."""
+    hidden = net.params.layers[:-1]
+    acts = sum(w.shape[0] for w, _ in hidden) if net.params.activation.kind == "sine" else 0
+    return int(2 * net.ff.m + acts)
+
+
+MUFU_LANES_PER_CLK_SM = 16  # measured, tools/ubench/mufu.cu (sin/ex2/tanh)
+
+
 def train_flops(layers) -> int:
     """2*(3*sum MAC - MAC_0): forward + wgrad + dgrad except layer 0."""
     macs = [w.shape[0] * w.shape[1] for w, _ in layers]
@@ -361,6 +372,17 @@ def _config(workload):
                         "+ whole-volume decode"}
 
 
+def mufu_cobound(ntrans: float, kms: float, per_point, clocks):
+    """The MUFU (sin/cos/ex2) ceiling next to the tensor one: algorithmic
+    transcendentals / s against 16 lanes/clk/SM x 148 SMs x the sampled SM clock."""
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak = MUFU_LANES_PER_CLK_SM * 148 * float(mhz) * 1e6 / 1e12
+    ach = ntrans / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
+    return {"bound": "mufu", "achieved": ach, "peak": peak, "unit": "T transcendentals/s", "frac": ach / peak,
+            "per_point": per_point, "note": "algorithmic count (2m + depth*width per point); the lattice "
+            "feature path issues fewer MUFU ops (Chebyshev recurrence along y)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -409,6 +431,7 @@ def main():
     # ---------------- decode steps
     m = DeviceModel(c, dev)
     flops = {t: fwd_flops(n) for t, n in c.experts[0].nets() if n is not None}
+    transc = {t: transcendentals(n) for t, n in c.experts[0].nets() if n is not None}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     for _ in range(args.warmup):
         d = m.decode(True)
@@ -445,11 +468,12 @@ def main():
     ms = float(tt[0].item()) / args.steps
     train_ms_max = float(tt[1].item())
     value = world * nvox / (ms * 1e-3)
-    kflops, kms, per_tag = 0.0, 0.0, {}
+    kflops, ktr, kms, per_tag = 0.0, 0.0, 0.0, {}
     for tag, npts, a, b in timer:
         dt = a.elapsed_time(b)
         kms += dt
         kflops += npts * flops[tag]
+        ktr += npts * transc[tag]
         s = per_tag.setdefault(tag, [0, 0.0])
         s[0] += npts
         s[1] += dt
@@ -520,7 +544,8 @@ def main():
                          "frac": achieved / peak, "traffic": load_traffic(), "peak_source": src,
                          "kernel": "mlp_eval_kernel (all decode stages)", "flops_per_point": flops,
                          "kernel_ms_per_step": kms / args.steps,
-                         "per_stage_ms": {k: v[1] / args.steps for k, v in per_tag.items()}},
+                         "per_stage_ms": {k: v[1] / args.steps for k, v in per_tag.items()},
+                         "co_bound": mufu_cobound(ktr, kms, transc, clocks)},
             "query": query,
             "c3_decode": c3,
             "c4_sequence": c4,

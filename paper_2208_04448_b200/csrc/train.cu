@@ -969,24 +969,48 @@ __global__ void __launch_bounds__(512, 1) k_train_fbwg(const FbArgs fa, const Wg
 }
 
 // ------------------------------------------------------------------ reduce + Adam
-// fixed-order, 4-way interleaved sum of the per-CTA partials -> grad[P];
-// per-CTA loss partials -> lossbuf[0] (data-parallel ranks all-reduce both)
-__global__ void k_train_reduce(const float* __restrict__ partial, int32_t ncta, int64_t P, float* __restrict__ grad,
-                               const double* loss_part, int32_t nloss, double* lossbuf, const int32_t* stopped) {
-  if (*stopped) return;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < P; q += stride) {
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
-    int c = 0;
-    for (; c + 4 <= ncta; c += 4) {
+// Fixed-order sum of the per-CTA partials.  A block of 256 threads owns 32
+// consecutive parameters: warp w sums partials c = w, w + 8, w + 16, ... of
+// lane l's parameter (coalesced 128 B rows, ~ncta / 8 loads in two chains per
+// thread instead of ncta in four), then warp 0 adds the eight warp sums as
+// ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)).  The order depends only
+// on ncta, so every run (and the fused and data-parallel forms) is bitwise
+// identical.
+constexpr int kRedThreads = 256;
+constexpr int kRedParams = 32;
+
+__device__ __forceinline__ float reduce_partials32(const float* __restrict__ partial, int32_t ncta, int64_t P,
+                                                   int64_t q, float* s_sum /* [8][32] */) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  float g0 = 0.f, g1 = 0.f;
+  if (q < P) {
+    int c = w;
+    for (; c + 8 < ncta; c += 16) {
       g0 += partial[(size_t)c * P + q];
-      g1 += partial[(size_t)(c + 1) * P + q];
-      g2 += partial[(size_t)(c + 2) * P + q];
-      g3 += partial[(size_t)(c + 3) * P + q];
+      g1 += partial[(size_t)(c + 8) * P + q];
     }
-    for (; c < ncta; ++c) g0 += partial[(size_t)c * P + q];
-    grad[q] = (g0 + g1) + (g2 + g3);
+    if (c < ncta) g0 += partial[(size_t)c * P + q];
   }
+  s_sum[w * 32 + l] = g0 + g1;
+  __syncthreads();
+  float tot = 0.f;
+  if (w == 0) {
+    const float* t = s_sum + l;
+    tot = ((t[0] + t[32]) + (t[64] + t[96])) + ((t[128] + t[160]) + (t[192] + t[224]));
+  }
+  return tot;
+}
+
+// partials -> grad[P]; per-CTA loss partials -> lossbuf[0] (data-parallel ranks all-reduce both)
+__global__ void __launch_bounds__(kRedThreads) k_train_reduce(const float* __restrict__ partial, int32_t ncta,
+                                                              int64_t P, float* __restrict__ grad,
+                                                              const double* loss_part, int32_t nloss,
+                                                              double* lossbuf, const int32_t* stopped) {
+  if (*stopped) return;
+  __shared__ float s_sum[8 * 32];
+  const int64_t q = blockIdx.x * (int64_t)kRedParams + (threadIdx.x & 31);
+  const float tot = reduce_partials32(partial, ncta, P, q, s_sum);
+  if (threadIdx.x < 32 && q < P) grad[q] = tot;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     double sl = 0.0;
     for (int c = 0; c < nloss; ++c) sl += loss_part[c];
@@ -1026,29 +1050,16 @@ struct AdamArgs {
 // Adam on every parameter; the gradient is either the all-reduced grad[P]
 // (data-parallel phase 2) or the fixed-order sum of the per-CTA partials,
 // in exactly k_train_reduce's order (single rank: one launch fewer)
-__global__ void k_train_adam(AdamArgs a) {
+__global__ void __launch_bounds__(kRedThreads) k_train_adam(AdamArgs a) {
   if (*a.stopped) return;
   const int e = *a.epoch;
   const float lr = a.lr[e], c1 = a.c1[e], c2 = a.c2[e];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.P; q += stride) {
-    float gsum;
-    if (a.grad) {
-      gsum = a.grad[q];
-    } else {
-      const float* partial = a.partial;
-      const int64_t P = a.P;
-      float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
-      int c = 0;
-      for (; c + 4 <= a.ncta; c += 4) {
-        g0 += partial[(size_t)c * P + q];
-        g1 += partial[(size_t)(c + 1) * P + q];
-        g2 += partial[(size_t)(c + 2) * P + q];
-        g3 += partial[(size_t)(c + 3) * P + q];
-      }
-      for (; c < a.ncta; ++c) g0 += partial[(size_t)c * P + q];
-      gsum = (g0 + g1) + (g2 + g3);
-    }
+  __shared__ float s_sum[8 * 32];
+  const int64_t q = blockIdx.x * (int64_t)kRedParams + (threadIdx.x & 31);
+  float gsum = 0.f;
+  if (!a.grad) gsum = reduce_partials32(a.partial, a.ncta, a.P, q, s_sum);  // block-uniform branch
+  if (threadIdx.x < 32 && q < a.P) {
+    if (a.grad) gsum = a.grad[q];
     const float g = gsum * a.gscale[q];
     // numpy float32 arithmetic with weak python scalars (neural.py:508-523)
     float m = a.mom[q] * 0.9f;
@@ -1477,7 +1488,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
       NVDB_CHECK_LAUNCH();
     }
     if (!fused_update) {
-      k_train_reduce<<<(int)std::min<int64_t>((t->P + 255) / 256, num_sms() * 8), 256, 0, st>>>(
+      k_train_reduce<<<(int)((t->P + kRedParams - 1) / kRedParams), kRedThreads, 0, st>>>(
           t->partial, t->wg_grid, t->P, t->grad, t->loss_part, t->fb_grid, t->lossbuf, stopped);
       NVDB_CHECK_LAUNCH();
     }
@@ -1512,7 +1523,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
       aa.nloss = t->fb_grid;
     }
     aa.loss_hist = t->loss_hist;
-    k_train_adam<<<(int)std::min<int64_t>((t->P + 255) / 256, num_sms() * 8), 256, 0, st>>>(aa);
+    k_train_adam<<<(int)((t->P + kRedParams - 1) / kRedParams), kRedThreads, 0, st>>>(aa);
     NVDB_CHECK_LAUNCH();
     k_train_advance<<<1, 1, 0, st>>>(ep, stopped, t->ctl + 2, t->ctl + 3);
     NVDB_CHECK_LAUNCH();

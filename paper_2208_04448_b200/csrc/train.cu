@@ -1194,6 +1194,10 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   tr->out_dim = nd.out_dim;
   const int W = tr->W, k0 = tr->k0, depth = tr->depth;
   if (W > 256 || depth > 4 || k0 > 1024) return fail(NVDB_EUNSUPPORTED, "net too large for the training kernels");
+  // the weight-gradient MMAs of hidden layers and head take [a_{l-1} | 1]^T
+  // (hidden units + the bias' ones row) as one 128-row operand
+  if (W + 1 > kTileM - 15)
+    return fail(NVDB_EUNSUPPORTED, "hidden width %d > 112: [activations | 1] exceeds one 128-row MMA tile", nd.width);
   // TMEM budgets: fwd/dgrad keeps depth*W pre-activation columns per warpgroup;
   // wgrad keeps ceil(k0/128)*W + 16 + (depth-1)*W + 16 accumulator columns
   const int nmt = (k0 + 127) / 128;

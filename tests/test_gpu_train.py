@@ -200,3 +200,39 @@ def test_working_subset_training_tracks_oracle():
     print(f"gpu final {rec.final_loss:.6g} epochs {rec.epochs}; oracle per-epoch {np.round(ref_losses, 6)}")
     assert rec.epochs == len(ref_losses) == 12
     assert abs(rec.final_loss - ref_losses[-1]) <= 0.03 * abs(ref_losses[-1]) + 1e-5
+
+
+@pytest.mark.parametrize("width", [112, 128])
+def test_hidden_width_edges_track_oracle(width):
+    """Full-batch training at the widest hidden layers the kernels take: the
+    per-epoch losses and the weights (biases included) follow the oracle's
+    neural.fused_step (oracle/svcodec_port.py train_step); wider hidden
+    layers are refused (NVDB_EUNSUPPORTED), not trained wrongly."""
+    rng = np.random.default_rng(5)
+    n = 2048
+    x = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+    y = (0.5 * np.sin(4 * x[:, 0]) * np.cos(3 * x[:, 1]) + 0.2 * x[:, 2]).astype(np.float32)
+    ff = FourierFeatures(32, 5.0, 31)
+    p0 = init_mlp(64, [width, width], 1, Activation("sine", 3.0), "linear", 32)
+    cfg = tiny_cfg(max_epochs=8, batch_size=n, lr=1e-3, decay=1.0, interval=100.0,
+                   activation="sine", frequency=3.0)
+    if width > 112:
+        with pytest.raises(Exception, match="112"):
+            DeviceTrainer(p0, ff, x, y, "mse", cfg, 1e-3, 0, False, -1.0, DEV)
+        return
+    tr = DeviceTrainer(p0, ff, x, y, "mse", cfg, 1e-3, 0, False, -1.0, DEV)
+    tr.run()
+    done, _, losses = tr.status()
+    st = O.TrainState(p0.layers, "sine", 3.0, ff)
+    ref = [O.train_step(st, x, y, "mse", np.float32(1e-3)) for _ in range(8)]
+    print(f"W={width}: gpu {np.asarray(losses[:8])} ref {np.asarray(ref)}")
+    assert done == 8
+    np.testing.assert_allclose(losses[:8], ref, rtol=2e-2, atol=1e-5)
+    got = tr.weights()
+    for li, ((w, b), (wr, br)) in enumerate(zip(got.layers, st.layers_interleaved())):
+        dw, dwr = (w - p0.layers[li][0]).ravel(), (wr - p0.layers[li][0]).ravel()
+        db, dbr = (b - p0.layers[li][1]).ravel(), (br - p0.layers[li][1]).ravel()
+        assert np.corrcoef(dw, dwr)[0, 1] > 0.95, (li, "weights")
+        assert np.abs(db - dbr).max() < 6 * 8e-3 + 1e-6, (li, "bias", np.abs(db - dbr).max())
+        assert np.abs(dbr).max() == 0 or np.abs(db).max() > 0.5 * np.abs(dbr).max(), (li, "bias not updated")
+    tr.close()

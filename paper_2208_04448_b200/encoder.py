@@ -373,12 +373,28 @@ class DeviceTrainer:
         return float(losses[done - 1]) if done > 0 else float("inf"), int(done)
 
     def weights(self) -> MlpParams:
-        ws = [np.zeros_like(np.asarray(w, dtype=np.float32)) for w, _ in self.params.layers]
-        bs = [np.zeros_like(np.asarray(b, dtype=np.float32)) for _, b in self.params.layers]
+        """Current parameters in the caller's layer shapes.  The trainer holds
+        unequal hidden widths zero-padded to the widest (netset._net_desc);
+        padded units keep zero weights and gradients, so the real layers are
+        the leading blocks of the padded ones."""
+        layers = self.params.layers
+        depth = len(layers) - 1
+        width = max(np.asarray(w).shape[0] for w, _ in layers[:-1])
+        shapes = []
+        for li, (w, _) in enumerate(layers):
+            rows = np.asarray(w).shape[0] if li == depth else width
+            cols = np.asarray(w).shape[1] if li == 0 else width
+            shapes.append((rows, cols))
+        ws = [np.zeros(sh, dtype=np.float32) for sh in shapes]
+        bs = [np.zeros(sh[0], dtype=np.float32) for sh in shapes]
         wp = (C.POINTER(C.c_float) * len(ws))(*[w.ctypes.data_as(C.POINTER(C.c_float)) for w in ws])
         bp = (C.POINTER(C.c_float) * len(bs))(*[b.ctypes.data_as(C.POINTER(C.c_float)) for b in bs])
         check(lib().nvdb_trainer_weights(self.handle, wp, bp), "nvdb_trainer_weights")
-        return MlpParams(list(zip(ws, bs)), self.params.activation, self.params.head)
+        out = []
+        for (w0, b0), w, b in zip(layers, ws, bs):
+            r, c = np.asarray(w0).shape
+            out.append((np.ascontiguousarray(w[:r, :c]), np.ascontiguousarray(b[:r])))
+        return MlpParams(out, self.params.activation, self.params.head)
 
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:

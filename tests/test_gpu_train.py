@@ -236,3 +236,46 @@ def test_hidden_width_edges_track_oracle(width):
         assert np.abs(db - dbr).max() < 6 * 8e-3 + 1e-6, (li, "bias", np.abs(db - dbr).max())
         assert np.abs(dbr).max() == 0 or np.abs(db).max() > 0.5 * np.abs(dbr).max(), (li, "bias not updated")
     tr.close()
+
+
+@pytest.mark.parametrize("hidden,m,n,kind,loss", [
+    ([40], 20, 1000, "sine", "mse"),             # one hidden layer, widths and 2m off the 16 / 64 grids
+    ([24, 24, 24, 24], 8, 777, "relu", "bce"),   # four hidden layers, a ragged last tile
+    ([100, 60], 50, 1500, "tanh", "ce"),         # unequal widths (zero-padded to 112), 3-class head
+])
+def test_ragged_shapes_track_oracle(hidden, m, n, kind, loss):
+    """Padding paths of the training kernels (hidden widths to 16, 2m to 64,
+    the batch to 128-row tiles) against the oracle's fused_step."""
+    rng = np.random.default_rng(9)
+    x = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+    if loss == "mse":
+        y = (0.5 * np.sin(4 * x[:, 0]) + 0.2 * x[:, 2]).astype(np.float32)
+        od, head = 1, "linear"
+    elif loss == "bce":
+        y = (x[:, 0] + x[:, 1] > 1.0).astype(np.float32)
+        od, head = 1, "binary"
+    else:
+        y = np.minimum(2, (3 * x[:, 0]).astype(np.int64))
+        od, head = 3, "logits"
+    freq = 3.0 if kind == "sine" else 1.0
+    ff = FourierFeatures(m, 5.0, 41)
+    p0 = init_mlp(2 * m, hidden, od, Activation(kind, freq), head, 42)
+    cfg = tiny_cfg(max_epochs=6, batch_size=n, lr=1e-3, decay=1.0, interval=100.0, activation=kind, frequency=freq)
+    tr = DeviceTrainer(p0, ff, x, y, loss, cfg, 1e-3, 0, False, -1.0, DEV)
+    tr.run()
+    done, _, losses = tr.status()
+    st = O.TrainState(p0.layers, kind, freq, ff)
+    ref = [O.train_step(st, x, y, loss, np.float32(1e-3)) for _ in range(6)]
+    print(f"{hidden} m={m} n={n} {kind}/{loss}: gpu {np.asarray(losses[:6])} ref {np.asarray(ref)}")
+    assert done == 6
+    np.testing.assert_allclose(losses[:6], ref, rtol=2e-2, atol=1e-5)
+    got = tr.weights()
+    for li, ((w, b), (wr, br)) in enumerate(zip(got.layers, st.layers_interleaved())):
+        assert w.shape == wr.shape and b.shape == br.shape
+        dw, dwr = (w - p0.layers[li][0]).ravel(), (wr - p0.layers[li][0]).ravel()
+        db, dbr = (b - p0.layers[li][1]).ravel(), (br - p0.layers[li][1]).ravel()
+        if np.abs(dwr).max() > 0:
+            assert np.corrcoef(dw, dwr)[0, 1] > 0.95, (li, "weights")
+        assert np.abs(dw - dwr).max() < 6 * 2e-3 + 1e-6, (li, "weights", np.abs(dw - dwr).max())
+        assert np.abs(db - dbr).max() < 6 * 2e-3 + 1e-6, (li, "bias", np.abs(db - dbr).max())
+    tr.close()

@@ -179,3 +179,57 @@ def test_wide_nets_stream_weights(width, m, depth):
     print(f"W={width} m={m} depth={depth}: max {err.max():.2e} rms {rms:.2e} scale {scale:.2f}")
     assert err.max() < 2e-2 * scale and rms < 3e-3 * scale
     ns.close()
+
+
+@pytest.mark.parametrize("hidden,m,kind,head,n", [
+    ([40], 20, "sine", "linear", 1),
+    ([100, 60], 50, "tanh", "logits", 129),
+    ([24, 24, 24, 24], 8, "relu", "binary", 1000),
+    ([48, 96, 32], 96, "sine", "logits", 127),
+    ([64, 64], 32, "sine", "linear", 0),
+])
+def test_forward_ragged_shapes(hidden, m, kind, head, n):
+    """forward_block (neural.py:527-550) on shapes off the kernel grids:
+    hidden widths padded to 16 (unequal widths zero-padded to the widest),
+    2m padded to the feature chunk, 1-4 hidden layers, 1- and 3-wide heads,
+    point counts that leave ragged or empty tiles."""
+    from paper_2208_04448_b200.encoder import init_mlp
+    from paper_2208_04448_b200.model import Activation, FourierFeatures
+    rng = np.random.default_rng(len(hidden) * 100 + m)
+    od = 3 if head == "logits" else 1
+    ff = FourierFeatures(m, 3.0, 13)
+    params = init_mlp(2 * m, hidden, od, Activation(kind, 3.0 if kind == "sine" else 1.0), head, 7)
+    w, b = params.layers[-1]
+    params.layers[-1] = (rng.normal(0, 0.2, size=w.shape).astype(np.float32), b)
+    tag = "l1" if head == "logits" else "voxel"
+    ns = DeviceNetSet([_Expert(tag, NetRecord(params, ff))], 512)
+    pts_np = rng.uniform(0.0, 1.0, size=(n, 3)).astype(np.float32)
+    got = ns.forward(0, torch.from_numpy(pts_np).to(DEV)).cpu().numpy()
+    assert got.shape == (n, od)
+    if n:
+        ref = O.forward_block(params, ff, pts_np)
+        err = np.abs(got - ref)
+        scale = max(1.0, float(np.abs(ref).max()))
+        print(f"{hidden} m={m} {kind}/{head} n={n}: max {err.max():.2e} scale {scale:.2f}")
+        assert err.max() < 2e-2 * scale and float(np.sqrt(np.mean(err ** 2))) < 3e-3 * scale
+    ns.close()
+
+
+def test_lookup_extreme_and_empty_coordinates(golden):
+    """get_values (grid.py:310-390) at |c| near 2^30 (two's-complement keys,
+    grid.py:47, 69-71) and on an empty batch."""
+    z = golden("lookup_small")
+    g = grid_from_arrays(z)
+    tree = DeviceTree(g)
+    big = (1 << 30) - 1
+    coords_np = np.array([[big, big, big], [-big, -big, -big], [-1, -1, -1], [0, 0, 0],
+                          [big, -big, 0], [-(1 << 30), 5, 7]], np.int32)
+    v, a, k = tree.lookup(torch.from_numpy(coords_np).to(DEV))
+    torch.cuda.synchronize()
+    v, a, k = v.cpu().numpy(), a.cpu().numpy().astype(bool), k.cpu().numpy()
+    rv, ra, rk = O.lookup(g, coords_np.astype(np.int64))
+    np.testing.assert_array_equal(v.view(np.uint32), np.asarray(rv, np.float32).view(np.uint32))
+    np.testing.assert_array_equal(a, ra)
+    np.testing.assert_array_equal(k, rk)
+    v0, a0, k0 = tree.lookup(torch.zeros((0, 3), dtype=torch.int32, device=DEV))
+    assert v0.numel() == 0 and a0.numel() == 0 and k0.numel() == 0

@@ -103,3 +103,26 @@ def test_c1_decode_parity(golden):
     both = a & z["qa"]
     assert np.abs(v[both] - z["qv"][both]).max() < VAL_MAX
     m.close()
+
+
+def test_hybrid_query_empty_and_far_batches(golden):
+    """HybridGrid.query (decoder.py:239-264) on an empty batch, and on
+    coordinates far outside every node (background, inactive, no regressor
+    evaluation), mixed with in-grid ones in the same call."""
+    z = golden("decode_multi")
+    c = container_from_arrays(z)
+    h = make_hybrid(c)
+    v0, a0 = h.query(np.zeros((0, 3), np.int64))
+    assert v0.shape == (0,) and a0.shape == (0,)
+    far = np.array([[1 << 29, 0, 0], [-(1 << 29), -(1 << 29), -(1 << 29)], [0, 1 << 28, -5]], np.int64)
+    base = h.regressor_evaluations
+    v1, a1 = h.query(far)
+    assert not a1.any()
+    np.testing.assert_array_equal(v1, np.full(3, np.float32(c.grid_meta.background)))
+    assert h.regressor_evaluations == base
+    q = np.concatenate([far, z["q"][:500]])
+    v2, a2 = h.query(q)
+    vr, ar = h.query(z["q"][:500])
+    np.testing.assert_array_equal(a2[3:], ar)
+    np.testing.assert_array_equal(v2[3:], vr)
+    h.model.close()

@@ -679,6 +679,7 @@ struct WgArgs {
   const int64_t* poff;        // per layer l: offset of W_l, then of b_l ([2*(depth+1)])
   const int32_t* stopped;
   uint32_t col_w0, col_b0, col_h, col_head;  // TMEM column bases
+  uint32_t col_hb;            // W > 112: per-layer bias gradients (16 columns each: hidden layers, then head)
 };
 
 __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
@@ -710,7 +711,11 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
   if (t < 32) tmem_alloc_keep(tmem_slot, 512);
   for (int i = t; i < 3 * mp; i += 256) s_b2pi[i] = nd.b2pi[i];
   for (int i = t; i < 16 * 128; i += 256) reinterpret_cast<__half*>(s_ones)[i] = __float2half(1.0f);
-  if (t < 128) {  // ones column (W) and zero columns (W+1..W+15) of both augmented activation buffers
+  // W <= 112: the bias gradients of hidden layers and head fall out of a ones
+  // column appended to the activation operand (row W of [a | 1]^T); wider
+  // layers fill all 128 rows, so their biases take separate MMAs (sep_bias)
+  const bool sep_bias = W > kTileM - 16;
+  if (t < 128 && !sep_bias) {  // ones column (W) and zero columns (W+1..W+15) of both augmented activation buffers
     for (int b = 0; b < 2; ++b) {
       const uint32_t o0 = kmajor_offset(t, W, kTileM), o1 = kmajor_offset(t, W + 8, kTileM);
       *reinterpret_cast<uint4*>(s_act[b] + o0) = make_uint4(pack_half2(1.f, 0.f), 0u, 0u, 0u);
@@ -849,6 +854,20 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
         for (int s = 0; s < kTileM / 16; ++s)
           umma_f16(tmem + col, smem_desc(sa + s * 256, 128, 2048), smem_desc(bsrc + s * 256, 128, 2048), idesc,
                    (!first || s != 0) ? 1u : 0u);
+        if (sep_bias) {
+          const uint32_t cb = tmem + a.col_hb + (uint32_t)(l - 1) * 16u;
+          if (!head) {  // gb_l[o] = dz_l^T 1: A = dz_l (outputs x samples), B = ones
+            const uint32_t idb = idesc_f16(kTileM, 16, 1, 0);
+            for (int s = 0; s < kTileM / 16; ++s)
+              umma_f16(cb, smem_desc(bsrc + s * 256, 128, 2048), smem_desc(son + s * 512, 256, 128), idb,
+                       (!first || s != 0) ? 1u : 0u);
+          } else {  // gb_head[o] = 1^T dL/dout: A = a ones block (SBO 0: every row group reads it), B = dL/dout
+            const uint32_t idb = idesc_f16(kTileM, 16, 0, 1);
+            for (int s = 0; s < kTileM / 16; ++s)
+              umma_f16(cb, smem_desc(son, 128, 0), smem_desc(bsrc + s * 256, 128, 2048), idb,
+                       (!first || s != 0) ? 1u : 0u);
+          }
+        }
         done_stage(q);
         if (l == 1 && tau > t0) {  // next tile's first feature chunks
           load_feat(tau - 1, 0);
@@ -917,6 +936,18 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
     float v[16];
     rd(a.col_b0, v);
     if (row < Wr) part[a.poff[1] + row] = v[0];
+  }
+  if (sep_bias && half == 0) {  // warps 0-3: one TMEM lane quadrant each
+    for (int l = 1; l <= depth; ++l) {
+      float v[16];
+      rd(a.col_hb + (uint32_t)(l - 1) * 16u, v);
+      const int64_t pb = a.poff[2 * l + 1];
+      if (l < depth) {
+        if (row < Wr) part[pb + row] = v[0];  // lane = output unit, column 0
+      } else if (row == 0) {
+        for (int o = 0; o < nd.out_dim; ++o) part[pb + o] = v[o];  // every lane holds the head's sums
+      }
+    }
   }
   for (int l = 1; l <= depth; ++l) {
     const bool head = (l == depth);
@@ -1194,14 +1225,15 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   tr->out_dim = nd.out_dim;
   const int W = tr->W, k0 = tr->k0, depth = tr->depth;
   if (W > 256 || depth > 4 || k0 > 1024) return fail(NVDB_EUNSUPPORTED, "net too large for the training kernels");
-  // the weight-gradient MMAs of hidden layers and head take [a_{l-1} | 1]^T
-  // (hidden units + the bias' ones row) as one 128-row operand
-  if (W + 1 > kTileM - 15)
-    return fail(NVDB_EUNSUPPORTED, "hidden width %d > 112: [activations | 1] exceeds one 128-row MMA tile", nd.width);
+  // the weight-gradient MMAs of hidden layers and head take the activations
+  // transposed as one 128-row operand (W <= 112: plus the bias' ones row;
+  // 112 < W <= 128: biases through separate MMAs)
+  if (W > kTileM)
+    return fail(NVDB_EUNSUPPORTED, "hidden width %d > 128: activations exceed one 128-row MMA tile", nd.width);
   // TMEM budgets: fwd/dgrad keeps depth*W pre-activation columns per warpgroup;
   // wgrad keeps ceil(k0/128)*W + 16 + (depth-1)*W + 16 accumulator columns
   const int nmt = (k0 + 127) / 128;
-  const int wg_cols = nmt * W + 16 + (depth - 1) * W + 16;
+  const int wg_cols = nmt * W + 16 + (depth - 1) * W + 16 + (W > kTileM - 16 ? depth * 16 : 0);
   if (W + depth * (W / 2) > 512 || wg_cols > 512)
     return fail(NVDB_EUNSUPPORTED, "net needs %d / %d TMEM columns (> 512)", W + depth * (W / 2), wg_cols);
   tr->nwg = (W + depth * (W / 2) <= 256) ? 2 : 1;
@@ -1481,6 +1513,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
     wa.col_b0 = nmt * t->W;
     wa.col_h = wa.col_b0 + 16;
     wa.col_head = wa.col_h + (t->depth - 1) * t->W;
+    wa.col_hb = wa.col_head + 16;
     const uint32_t fb_smem = std::max<uint32_t>(t->plan.total, 120 * 1024);
     if (t->fb_grid == t->wg_grid) {
       k_train_fbwg<<<t->fb_grid, 256 * t->nwg, std::max<uint32_t>(fb_smem, kWgSmem), st>>>(fa, wa);

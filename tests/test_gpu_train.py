@@ -202,12 +202,14 @@ def test_working_subset_training_tracks_oracle():
     assert abs(rec.final_loss - ref_losses[-1]) <= 0.03 * abs(ref_losses[-1]) + 1e-5
 
 
-@pytest.mark.parametrize("width", [112, 128])
+@pytest.mark.parametrize("width", [112, 128, 144])
 def test_hidden_width_edges_track_oracle(width):
     """Full-batch training at the widest hidden layers the kernels take: the
     per-epoch losses and the weights (biases included) follow the oracle's
-    neural.fused_step (oracle/svcodec_port.py train_step); wider hidden
-    layers are refused (NVDB_EUNSUPPORTED), not trained wrongly."""
+    neural.fused_step (oracle/svcodec_port.py train_step).  W = 112 takes the
+    biases from the ones row of [a | 1]^T, W = 128 from separate MMAs (one of
+    them reads a ones block with a zero row-group stride); wider hidden layers
+    are refused (NVDB_EUNSUPPORTED), not trained wrongly."""
     rng = np.random.default_rng(5)
     n = 2048
     x = rng.uniform(0, 1, (n, 3)).astype(np.float32)
@@ -216,8 +218,8 @@ def test_hidden_width_edges_track_oracle(width):
     p0 = init_mlp(64, [width, width], 1, Activation("sine", 3.0), "linear", 32)
     cfg = tiny_cfg(max_epochs=8, batch_size=n, lr=1e-3, decay=1.0, interval=100.0,
                    activation="sine", frequency=3.0)
-    if width > 112:
-        with pytest.raises(Exception, match="112"):
+    if width > 128:
+        with pytest.raises(Exception, match="128"):
             DeviceTrainer(p0, ff, x, y, "mse", cfg, 1e-3, 0, False, -1.0, DEV)
         return
     tr = DeviceTrainer(p0, ff, x, y, "mse", cfg, 1e-3, 0, False, -1.0, DEV)
@@ -242,6 +244,8 @@ def test_hidden_width_edges_track_oracle(width):
     ([40], 20, 1000, "sine", "mse"),             # one hidden layer, widths and 2m off the 16 / 64 grids
     ([24, 24, 24, 24], 8, 777, "relu", "bce"),   # four hidden layers, a ragged last tile
     ([100, 60], 50, 1500, "tanh", "ce"),         # unequal widths (zero-padded to 112), 3-class head
+    ([128, 96], 24, 1100, "sine", "ce"),         # padded to 128: biases through separate MMAs, 3-wide head
+    ([128, 128, 128], 30, 900, "relu", "bce"),   # 128 wide, one TMEM group, binary head
 ])
 def test_ragged_shapes_track_oracle(hidden, m, n, kind, loss):
     """Padding paths of the training kernels (hidden widths to 16, 2m to 64,

@@ -33,14 +33,14 @@ struct SmemPlan {
   uint32_t w_off, region_off, region_bytes, small_off, bar_off, total;
 };
 
-inline SmemPlan plan_smem(uint32_t max_wimg, int max_width) {
+inline SmemPlan plan_smem(uint32_t max_wimg, int max_width, int groups = 2) {
   SmemPlan p;
   p.w_off = 0;
   p.region_off = (uint32_t)align_up(max_wimg, 1024);
   const uint32_t feat = 2u * kChunkBytes;
   const uint32_t hid = (uint32_t)kTileM * (uint32_t)max_width * 2u;
   p.region_bytes = (uint32_t)align_up(feat > hid ? feat : hid, 1024);
-  p.small_off = p.region_off + 2 * p.region_bytes;
+  p.small_off = p.region_off + (uint32_t)groups * p.region_bytes;  // one region per tile group
   p.bar_off = (uint32_t)align_up(p.small_off + kSmallFloats * 4, 16);
   p.total = p.bar_off + 128;
   return p;

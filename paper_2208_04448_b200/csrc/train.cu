@@ -680,8 +680,13 @@ struct WgArgs {
   const int32_t* stopped;
   uint32_t col_w0, col_b0, col_h, col_head;  // TMEM column bases
   uint32_t col_hb;            // W > 112: per-layer bias gradients (16 columns each: hidden layers, then head)
+  int32_t two_pass;           // accumulators exceed 512 TMEM columns: gW0 pass, then the rest
 };
 
+// mode 0: every accumulator in one pass over the tiles; when they exceed the
+// 512 TMEM columns the host runs two passes: mode 1 = gW0 only (features x
+// dz0), mode 2 = everything else, its columns shifted down by the gW0 block.
+template <int mode>
 __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
   TTRC_DECL;
 #ifdef NVDB_TRACE
@@ -734,7 +739,10 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
   const size_t tbytes = (size_t)kTileM * W * 2;
   const uint32_t sfe = smem_addr(s_feat), son = smem_addr(s_ones);
   const int nmt = (k0 + 127) / 128;  // M tiles of 128 features
-  const int nst = depth + 1;          // load stages per tile: dz0 | (a0,dz1) .. | (a_{d-1}, dlt)
+  const int nst = mode == 1 ? 1 : depth + 1;  // load stages per tile: dz0 | (a0,dz1) .. | (a_{d-1}, dlt)
+  const bool do_w0 = mode != 2, do_rest = mode != 1;
+  const uint32_t sh = mode == 2 ? (uint32_t)(nmt * W) : 0u;  // mode 2: columns without the gW0 block
+  const uint32_t col_b0 = a.col_b0 - sh, col_h = a.col_h - sh, col_head = a.col_head - sh, col_hb = a.col_hb - sh;
   const int64_t nstages = (t1 - t0) * nst;
   // thread-0 pipeline state
   uint32_t nfull[2] = {0, 0}, nfree[2] = {0, 0};
@@ -803,7 +811,7 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
       issue_load(issued);
       issued++;
     }
-    if (t == 0) {
+    if (t == 0 && do_w0) {
       // feature chunks of 128 features (32 KB) from the forward phase's tile
       // image; chunks 0 and 1 of a tile were requested during the previous
       // tile's later stages (or here, for the first tile)
@@ -827,12 +835,18 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
         if (rb == 0) { nring0++; pr0 = true; } else { nring1++; pr1 = true; }
         if (j + 2 < nmt) load_feat(tau, j + 2);
       }
+      if (!do_rest && tau > t0) {  // mode 1 has no later stages: prefetch the next tile's chunks here
+        load_feat(tau - 1, 0);
+        if (nmt > 1) load_feat(tau - 1, 1);
+      }
     }
-    if (t == 0) {
+    if (t == 0 && !do_w0) wait_full(qbase);
+    if (t == 0 && !do_rest) done_stage(qbase);
+    if (t == 0 && do_rest) {
       const uint32_t sdz = smem_addr(s_dz[qbase & 1]);
       const uint32_t idesc = idesc_f16(kTileM, 16, 1, 0);
       for (int s = 0; s < kTileM / 16; ++s)
-        umma_f16(tmem + a.col_b0, smem_desc(sdz + s * 256, 128, 2048), smem_desc(son + s * 512, 256, 128), idesc,
+        umma_f16(tmem + col_b0, smem_desc(sdz + s * 256, 128, 2048), smem_desc(son + s * 512, 256, 128), idesc,
                  (!first || s != 0) ? 1u : 0u);
       done_stage(qbase);
       TTRC(11, tau);
@@ -848,14 +862,14 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
         const int b = (int)(q & 1);
         const int N = head ? 16 : W;
         const uint32_t idesc = idesc_f16(kTileM, N, 1, 1);
-        const uint32_t col = head ? a.col_head : a.col_h + (l - 1) * W;
+        const uint32_t col = head ? col_head : col_h + (l - 1) * W;
         const uint32_t sa = smem_addr(s_act[b]);
         const uint32_t bsrc = head ? smem_addr(s_dlt[b]) : smem_addr(s_dz[b]);
         for (int s = 0; s < kTileM / 16; ++s)
           umma_f16(tmem + col, smem_desc(sa + s * 256, 128, 2048), smem_desc(bsrc + s * 256, 128, 2048), idesc,
                    (!first || s != 0) ? 1u : 0u);
         if (sep_bias) {
-          const uint32_t cb = tmem + a.col_hb + (uint32_t)(l - 1) * 16u;
+          const uint32_t cb = tmem + col_hb + (uint32_t)(l - 1) * 16u;
           if (!head) {  // gb_l[o] = dz_l^T 1: A = dz_l (outputs x samples), B = ones
             const uint32_t idb = idesc_f16(kTileM, 16, 1, 0);
             for (int s = 0; s < kTileM / 16; ++s)
@@ -869,7 +883,7 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
           }
         }
         done_stage(q);
-        if (l == 1 && tau > t0) {  // next tile's first feature chunks
+        if (l == 1 && tau > t0 && do_w0) {  // next tile's first feature chunks
           load_feat(tau - 1, 0);
           if (nmt > 1) load_feat(tau - 1, 1);
         }
@@ -909,7 +923,7 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
       for (int i = 0; i < 16; ++i) v0[i] = v1[i] = 0.f;
     }
   };
-  for (int j = 0; j < nmt; ++j) {
+  for (int j = 0; j < (do_w0 ? nmt : 0); ++j) {
     const int k = j * 128 + row;
     float* pk = part + poff0 + k;
     for (int cc = half; cc < W / 16; cc += 4) {
@@ -932,15 +946,15 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
       }
     }
   }
-  if (half == 0) {
+  if (do_rest && half == 0) {
     float v[16];
-    rd(a.col_b0, v);
+    rd(col_b0, v);
     if (row < Wr) part[a.poff[1] + row] = v[0];
   }
-  if (sep_bias && half == 0) {  // warps 0-3: one TMEM lane quadrant each
+  if (do_rest && sep_bias && half == 0) {  // warps 0-3: one TMEM lane quadrant each
     for (int l = 1; l <= depth; ++l) {
       float v[16];
-      rd(a.col_hb + (uint32_t)(l - 1) * 16u, v);
+      rd(col_hb + (uint32_t)(l - 1) * 16u, v);
       const int64_t pb = a.poff[2 * l + 1];
       if (l < depth) {
         if (row < Wr) part[pb + row] = v[0];  // lane = output unit, column 0
@@ -949,11 +963,11 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
       }
     }
   }
-  for (int l = 1; l <= depth; ++l) {
+  for (int l = 1; l <= (do_rest ? depth : 0); ++l) {
     const bool head = (l == depth);
     const int N = head ? 16 : W;
     const int outs = head ? nd.out_dim : Wr;
-    const uint32_t col = head ? a.col_head : a.col_h + (l - 1) * W;
+    const uint32_t col = head ? col_head : col_h + (l - 1) * W;
     const int64_t pw = a.poff[2 * l], pb = a.poff[2 * l + 1];
     for (int cc = half; cc < N / 16; cc += 4) {
       const bool two = cc + 2 < N / 16;
@@ -982,21 +996,35 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
   if (t < 32) tmem_dealloc(tmem, 512);
 }
 
+template <bool TWO_PASS>
 __global__ void __launch_bounds__(256, 1) k_train_wgrad(const WgArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if (*a.stopped) return;
-  wg_body(a, smem);
+  if constexpr (TWO_PASS) {
+    wg_body<1>(a, smem);
+    wg_body<2>(a, smem);
+  } else {
+    wg_body<0>(a, smem);
+  }
 }
 
 // fwd/dgrad then weight gradients of the same tiles in one launch: the
 // activation / dz tile images this CTA just wrote are re-read from L2
 // (same tile partition as the two-kernel form: fb_grid == wg_grid)
+template <bool TWO_PASS>
 __global__ void __launch_bounds__(512, 1) k_train_fbwg(const FbArgs fa, const WgArgs wa) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if (*fa.stopped) return;
   fb_body(fa, smem);
   __syncthreads();
-  if (threadIdx.x < 256) wg_body(wa, smem);
+  if (threadIdx.x < 256) {
+    if constexpr (TWO_PASS) {
+      wg_body<1>(wa, smem);
+      wg_body<2>(wa, smem);
+    } else {
+      wg_body<0>(wa, smem);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ reduce + Adam
@@ -1233,9 +1261,12 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   // TMEM budgets: fwd/dgrad keeps depth*W pre-activation columns per warpgroup;
   // wgrad keeps ceil(k0/128)*W + 16 + (depth-1)*W + 16 accumulator columns
   const int nmt = (k0 + 127) / 128;
-  const int wg_cols = nmt * W + 16 + (depth - 1) * W + 16 + (W > kTileM - 16 ? depth * 16 : 0);
-  if (W + depth * (W / 2) > 512 || wg_cols > 512)
-    return fail(NVDB_EUNSUPPORTED, "net needs %d / %d TMEM columns (> 512)", W + depth * (W / 2), wg_cols);
+  const int wg_rest = 16 + (depth - 1) * W + 16 + (W > kTileM - 16 ? depth * 16 : 0);
+  const int wg_cols = nmt * W + wg_rest;
+  // more than 512 accumulator columns: two weight-gradient passes (gW0, then the rest)
+  if (W + depth * (W / 2) > 512 || (wg_cols > 512 && (nmt * W > 512 || wg_rest > 512)))
+    return fail(NVDB_EUNSUPPORTED, "net needs %d / %d + %d TMEM columns (> 512)", W + depth * (W / 2), nmt * W,
+                wg_rest);
   tr->nwg = (W + depth * (W / 2) <= 256) ? 2 : 1;
   tr->batch = d->sampled ? d->batch : d->n;
   tr->ntiles = (tr->batch + kTileM - 1) / kTileM;
@@ -1349,7 +1380,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   n.act = nd.activation;
   n.head = nd.head;
   n.expert = 0;
-  t->plan = plan_smem((uint32_t)wimg_bytes, W);
+  t->plan = plan_smem((uint32_t)wimg_bytes, W, t->nwg);
   // ---- per-step buffers
   const size_t tile_elems = (size_t)kTileM * W;
   {  // data-parallel share: contiguous tile range of this rank (whole batch when unsharded)
@@ -1407,9 +1438,11 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   }
   // kernel attributes
   if (enable_max_smem(k_train_fb) < (long long)t->plan.total ||
-      enable_max_smem(k_train_wgrad) < kWgSmem ||
-      enable_max_smem(k_train_fbwg) < (long long)std::max<uint32_t>(t->plan.total, kWgSmem))
-    return fail(NVDB_EUNSUPPORTED, "training kernels exceed the shared-memory limit");
+      enable_max_smem(k_train_wgrad<false>) < kWgSmem || enable_max_smem(k_train_wgrad<true>) < kWgSmem ||
+      enable_max_smem(k_train_fbwg<false>) < (long long)std::max<uint32_t>(t->plan.total, kWgSmem) ||
+      enable_max_smem(k_train_fbwg<true>) < (long long)std::max<uint32_t>(t->plan.total, kWgSmem))
+    return fail(NVDB_EUNSUPPORTED, "training kernels exceed the shared-memory limit (%u B of resident weights "
+                "and tile buffers; weight streaming is built for decode only)", t->plan.total);
   *out = tr.release();
   return NVDB_OK;
 }
@@ -1514,14 +1547,21 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
     wa.col_h = wa.col_b0 + 16;
     wa.col_head = wa.col_h + (t->depth - 1) * t->W;
     wa.col_hb = wa.col_head + 16;
+    wa.two_pass = (wa.col_hb + (t->W > kTileM - 16 ? t->depth * 16 : 0)) > 512 ? 1 : 0;
     const uint32_t fb_smem = std::max<uint32_t>(t->plan.total, 120 * 1024);
     if (t->fb_grid == t->wg_grid) {
-      k_train_fbwg<<<t->fb_grid, 256 * t->nwg, std::max<uint32_t>(fb_smem, kWgSmem), st>>>(fa, wa);
+      if (wa.two_pass)
+        k_train_fbwg<true><<<t->fb_grid, 256 * t->nwg, std::max<uint32_t>(fb_smem, kWgSmem), st>>>(fa, wa);
+      else
+        k_train_fbwg<false><<<t->fb_grid, 256 * t->nwg, std::max<uint32_t>(fb_smem, kWgSmem), st>>>(fa, wa);
       NVDB_CHECK_LAUNCH();
     } else {
       k_train_fb<<<t->fb_grid, 256 * t->nwg, fb_smem, st>>>(fa);
       NVDB_CHECK_LAUNCH();
-      k_train_wgrad<<<t->wg_grid, 256, kWgSmem, st>>>(wa);
+      if (wa.two_pass)
+        k_train_wgrad<true><<<t->wg_grid, 256, kWgSmem, st>>>(wa);
+      else
+        k_train_wgrad<false><<<t->wg_grid, 256, kWgSmem, st>>>(wa);
       NVDB_CHECK_LAUNCH();
     }
     if (!fused_update) {

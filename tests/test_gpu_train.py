@@ -246,6 +246,9 @@ def test_hidden_width_edges_track_oracle(width):
     ([100, 60], 50, 1500, "tanh", "ce"),         # unequal widths (zero-padded to 112), 3-class head
     ([128, 96], 24, 1100, "sine", "ce"),         # padded to 128: biases through separate MMAs, 3-wide head
     ([128, 128, 128], 30, 900, "relu", "bce"),   # 128 wide, one TMEM group, binary head
+    ([128, 128, 128], 192, 700, "sine", "mse"),  # 3 x 128 + 320 columns: two weight-gradient passes
+    ([112, 112], 256, 800, "tanh", "bce"),       # 4 x 112 + 144 columns: two passes, ones-row biases
+    ([96, 96], 256, 1300, "sine", "ce"),          # 4 x 96 + 128 columns: one pass, at the limit
 ])
 def test_ragged_shapes_track_oracle(hidden, m, n, kind, loss):
     """Padding paths of the training kernels (hidden widths to 16, 2m to 64,

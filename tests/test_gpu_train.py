@@ -286,3 +286,24 @@ def test_ragged_shapes_track_oracle(hidden, m, n, kind, loss):
         assert np.abs(dw - dwr).max() < 6 * 2e-3 + 1e-6, (li, "weights", np.abs(dw - dwr).max())
         assert np.abs(db - dbr).max() < 6 * 2e-3 + 1e-6, (li, "bias", np.abs(db - dbr).max())
     tr.close()
+
+
+def test_multi_expert_encode_decode_on_gpu(golden):
+    """encode over a grid that spans 2 x 2 x 2 subdomains (partition.py:74-120,
+    S = 512, halo 8): eight experts trained on their expanded boxes, patches
+    per expert, gate-blended decode.  The reference's own encode + decode of
+    the same grid and TrainConfig reaches IoU 0.88850
+    (tests/golden/make_golden_multi_encode.py); the GPU path must match it."""
+    from paper_2208_04448_b200.procgen import sphere_sdf
+    z = golden("multi_encode")
+    truth = sphere_sdf((512.0, 512.0, 512.0), 30.0, 1.0, 3.0)
+    cfg = tiny_cfg(max_epochs=60, l0_net=(2, 32), voxel_net=(2, 32), ffm_size=32)
+    c = encode(truth, cfg, device=DEV)
+    assert len(c.experts) == int(z["experts"][0]) == 8
+    m = DeviceModel(c, DEV)
+    g = m.decode(True).to_grid()
+    iou = _iou(truth.leaf_origins, truth.leaf_active, g.leaf_origins, g.leaf_active)
+    print(f"8 experts: IoU {iou:.5f} (reference {float(z['iou'][0]):.5f}), "
+          f"patches {sum(len(e.patches) for e in c.experts)}")
+    assert iou >= float(z["iou"][0]) - 0.01
+    m.close()

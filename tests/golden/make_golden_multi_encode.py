@@ -1,5 +1,6 @@
 """Reference quality of an 8-expert encode (sphere r 30 at (512,512,512),
-tiny nets) for tests/test_gpu_train.py::test_multi_expert_encode_decode_on_gpu.
+tiny nets) for tests/test_gpu_train.py::test_multi_expert_encode_decode_on_gpu,
+and of a FOG (fBm density) encode for test_fog_encode_decode_on_gpu.
 
     PYTHONPATH=/root/reference/pkg/src:/root/repo PYTHONDONTWRITEBYTECODE=1 \\
     OPENBLAS_NUM_THREADS=8 python tests/golden/make_golden_multi_encode.py
@@ -20,7 +21,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 from svcodec.config import TrainConfig  # noqa: E402
 from svcodec.decoder import decode_full  # noqa: E402
 from svcodec.encoder import encode  # noqa: E402
-from svcodec.procgen import SphereSpec, gen_sphere_sdf  # noqa: E402
+from svcodec.procgen import FbmSpec, SphereSpec, gen_fbm_density, gen_sphere_sdf  # noqa: E402
 
 from paper_2208_04448_b200.model import DenseLeafGrid  # noqa: E402
 
@@ -46,5 +47,14 @@ if __name__ == "__main__":
     truth, dec = DenseLeafGrid.from_svcodec(g), DenseLeafGrid.from_svcodec(d)
     i = iou(truth, dec)
     print(f"reference: {len(c.experts)} experts, IoU {i:.5f}, {time.time() - t0:.0f} s")
+    # FOG: fBm density on a 40^3 box (FOG class: no tiles, value scale 1, no clip)
+    t0 = time.time()
+    fog = gen_fbm_density(FbmSpec(octaves=3, lacunarity=2.0, gain=0.5, base_frequency=0.06, seed=4,
+                                  domain=((0, 0, 0), (40, 40, 40)), threshold=0.5, voxel_size=1.0))
+    cf = encode(fog, TrainConfig(**CFG))
+    df = decode_full(cf)
+    ftruth, fdec = DenseLeafGrid.from_svcodec(fog), DenseLeafGrid.from_svcodec(df)
+    fi = iou(ftruth, fdec)
+    print(f"reference FOG: {len(cf.experts)} experts, IoU {fi:.5f}, {time.time() - t0:.0f} s")
     np.savez_compressed(os.path.join(HERE, "multi_encode.npz"), iou=np.array([i]),
-                        experts=np.array([len(c.experts)]))
+                        experts=np.array([len(c.experts)]), fog_iou=np.array([fi]))

@@ -307,3 +307,23 @@ def test_multi_expert_encode_decode_on_gpu(golden):
           f"patches {sum(len(e.patches) for e in c.experts)}")
     assert iou >= float(z["iou"][0]) - 0.01
     m.close()
+
+
+def test_fog_encode_decode_on_gpu(golden):
+    """FOG grid (fBm density, procgen.py:283-309): no tiles, value scale 1,
+    significance threshold for patches, no clip.  The reference's encode +
+    decode of the same grid and config reaches IoU 0.92823
+    (tests/golden/make_golden_multi_encode.py)."""
+    from paper_2208_04448_b200.procgen import fbm_density
+    z = golden("multi_encode")
+    truth = fbm_density(octaves=3, lacunarity=2.0, gain=0.5, base_frequency=0.06, seed=4,
+                        domain=((0, 0, 0), (40, 40, 40)), threshold=0.5, voxel_size=1.0, device=DEV)
+    assert truth.grid_class == "fog"
+    cfg = tiny_cfg(max_epochs=60, l0_net=(2, 32), voxel_net=(2, 32), ffm_size=32)
+    c = encode(truth, cfg, device=DEV)
+    m = DeviceModel(c, DEV)
+    g = m.decode(True).to_grid()
+    iou = _iou(truth.leaf_origins, truth.leaf_active, g.leaf_origins, g.leaf_active)
+    print(f"FOG: IoU {iou:.5f} (reference {float(z['fog_iou'][0]):.5f})")
+    assert iou >= float(z["fog_iou"][0]) - 0.01
+    m.close()

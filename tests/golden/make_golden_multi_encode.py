@@ -1,6 +1,7 @@
 """Reference quality of an 8-expert encode (sphere r 30 at (512,512,512),
 tiny nets) for tests/test_gpu_train.py::test_multi_expert_encode_decode_on_gpu,
-and of a FOG (fBm density) encode for test_fog_encode_decode_on_gpu.
+of a FOG (fBm density) encode for test_fog_encode_decode_on_gpu, and of a
+3-frame warm-started sequence for test_sequence_matches_reference.
 
     PYTHONPATH=/root/reference/pkg/src:/root/repo PYTHONDONTWRITEBYTECODE=1 \\
     OPENBLAS_NUM_THREADS=8 python tests/golden/make_golden_multi_encode.py
@@ -20,7 +21,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 from svcodec.config import TrainConfig  # noqa: E402
 from svcodec.decoder import decode_full  # noqa: E402
-from svcodec.encoder import encode  # noqa: E402
+from svcodec.encoder import encode, encode_sequence  # noqa: E402
 from svcodec.procgen import FbmSpec, SphereSpec, gen_fbm_density, gen_sphere_sdf  # noqa: E402
 
 from paper_2208_04448_b200.model import DenseLeafGrid  # noqa: E402
@@ -56,5 +57,19 @@ if __name__ == "__main__":
     ftruth, fdec = DenseLeafGrid.from_svcodec(fog), DenseLeafGrid.from_svcodec(df)
     fi = iou(ftruth, fdec)
     print(f"reference FOG: {len(cf.experts)} experts, IoU {fi:.5f}, {time.time() - t0:.0f} s")
+    # sequence: 3 frames of a sphere moving 1 voxel per frame (the GPU tests' _moving_sphere/_seq_cfg)
+    t0 = time.time()
+    frames = [gen_sphere_sdf(SphereSpec(center=(20.0 + t, 20.0, 20.0), radius=11.0, voxel_size=1.0,
+                                        half_width=3.0)) for t in range(3)]
+    scfg = TrainConfig(l1_net=(2, 8), l0_net=(2, 16), voxel_net=(2, 24), tile_net=None, ffm_size=24,
+                       max_epochs=300, batch_size=4096, lr=1e-3, refine_lr=2e-4, seed=13)
+    conts, reps = encode_sequence(frames, scfg)
+    seq_ep = [int(r.epochs) for r in reps]
+    seq_iou = [iou(DenseLeafGrid.from_svcodec(f), DenseLeafGrid.from_svcodec(decode_full(cc)))
+               for f, cc in zip(frames, conts)]
+    print(f"reference sequence: epochs {seq_ep} cold {reps[0].detail.get('cold_epochs')} IoU "
+          f"{np.round(seq_iou, 5)}, {time.time() - t0:.0f} s")
     np.savez_compressed(os.path.join(HERE, "multi_encode.npz"), iou=np.array([i]),
-                        experts=np.array([len(c.experts)]), fog_iou=np.array([fi]))
+                        experts=np.array([len(c.experts)]), fog_iou=np.array([fi]),
+                        seq_epochs=np.array(seq_ep), seq_iou=np.array(seq_iou),
+                        seq_cold=np.array([float(reps[0].detail.get("cold_epochs", 0))]))

@@ -351,3 +351,32 @@ def test_sequence_matches_reference(golden):
           f"(reference {np.round(z['seq_iou'], 5)})")
     np.testing.assert_allclose(ep, z["seq_epochs"], rtol=0.15)
     assert np.all(np.asarray(ious) >= z["seq_iou"] - 0.01)
+
+
+def test_strict_topology_decode_masks_exact_on_gpu():
+    """test_decoder.py:20-36 (AC3): with strict_topology every classifier
+    disagreement becomes a patch, so the decoded masks equal the truth's and
+    active values stay inside the SDF band; the hybrid grid's topology
+    matches the full decode."""
+    from paper_2208_04448_b200.decoder import make_hybrid
+    from paper_2208_04448_b200.procgen import sphere_sdf
+    truth = sphere_sdf((20.0, 20.0, 20.0), 12.0, 1.0, 3.0)
+    cfg = tiny_cfg(l1_net=(2, 8), l0_net=(2, 24), voxel_net=(3, 32), tile_net=None, ffm_size=32,
+                   max_epochs=250, batch_size=8192, strict_topology=True, seed=21)
+    c = encode(truth, cfg, device=DEV)
+    m = DeviceModel(c, DEV)
+    g = m.decode(True).to_grid()
+    np.testing.assert_array_equal(g.l1_origins, truth.l1_origins)
+    np.testing.assert_array_equal(g.l1_child, truth.l1_child)
+    np.testing.assert_array_equal(g.l1_active, truth.l1_active)
+    np.testing.assert_array_equal(g.leaf_origins, truth.leaf_origins)
+    np.testing.assert_array_equal(g.leaf_active, truth.leaf_active)
+    assert np.all(np.abs(g.leaf_values[g.leaf_active]) <= 3.0 + 1e-4)
+    li, vi = np.nonzero(truth.leaf_active)
+    coords = truth.leaf_origins[li] + np.stack([vi >> 6, (vi >> 3) & 7, vi & 7], 1)
+    h = make_hybrid(c)
+    v, a = h.query(coords)
+    assert a.all()
+    np.testing.assert_allclose(v, g.leaf_values[li, vi], atol=1e-6)
+    m.close()
+    h.model.close()

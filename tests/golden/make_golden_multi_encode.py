@@ -1,7 +1,9 @@
 """Reference quality of an 8-expert encode (sphere r 30 at (512,512,512),
 tiny nets) for tests/test_gpu_train.py::test_multi_expert_encode_decode_on_gpu,
 of a FOG (fBm density) encode for test_fog_encode_decode_on_gpu, and of a
-3-frame warm-started sequence for test_sequence_matches_reference.
+3-frame warm-started sequence for test_sequence_matches_reference, and of
+an fBm grid with active level-1 tiles (tile regressor path) for
+test_active_tiles_match_reference.
 
     PYTHONPATH=/root/reference/pkg/src:/root/repo PYTHONDONTWRITEBYTECODE=1 \\
     OPENBLAS_NUM_THREADS=8 python tests/golden/make_golden_multi_encode.py
@@ -18,6 +20,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, os.path.dirname(HERE))
 
 from svcodec.config import TrainConfig  # noqa: E402
 from svcodec.decoder import decode_full  # noqa: E402
@@ -69,7 +72,24 @@ if __name__ == "__main__":
                for f, cc in zip(frames, conts)]
     print(f"reference sequence: epochs {seq_ep} cold {reps[0].detail.get('cold_epochs')} IoU "
           f"{np.round(seq_iou, 5)}, {time.time() - t0:.0f} s")
+    # active level-1 tiles on an fBm grid: the tile regressor's decoded values
+    from helpers import add_active_tiles  # noqa: E402
+    t0 = time.time()
+    base = gen_fbm_density(FbmSpec(octaves=3, lacunarity=2.0, gain=0.5, base_frequency=0.06, seed=4,
+                                   domain=((0, 0, 0), (40, 40, 40)), threshold=0.5, voxel_size=1.0))
+    tg = add_active_tiles(DenseLeafGrid.from_svcodec(base))
+    tcfg = dict(CFG, tile_net=(2, 16), max_epochs=120)
+    ct = encode(tg.to_svcodec(), TrainConfig(**tcfg))
+    dt = DenseLeafGrid.from_svcodec(decode_full(ct))
+    sel = tg.l1_active & ~tg.l1_child
+    assert np.array_equal(dt.l1_origins, tg.l1_origins)
+    tile_ref = dt.l1_tiles[sel]
+    tile_err = float(np.sqrt(np.mean((tile_ref - tg.l1_tiles[sel]) ** 2)))
+    print(f"reference tiles: {int(sel.sum())} active tiles, tile rms err vs truth {tile_err:.4f}, "
+          f"tile net epochs {ct.experts[0].tile_regressor.epochs}, {time.time() - t0:.0f} s")
     np.savez_compressed(os.path.join(HERE, "multi_encode.npz"), iou=np.array([i]),
                         experts=np.array([len(c.experts)]), fog_iou=np.array([fi]),
                         seq_epochs=np.array(seq_ep), seq_iou=np.array(seq_iou),
-                        seq_cold=np.array([float(reps[0].detail.get("cold_epochs", 0))]))
+                        seq_cold=np.array([float(reps[0].detail.get("cold_epochs", 0))]),
+                        tile_ref=tile_ref.astype(np.float32), tile_err=np.array([tile_err]),
+                        tile_epochs=np.array([ct.experts[0].tile_regressor.epochs]))

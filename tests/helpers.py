@@ -28,3 +28,20 @@ def tiny_cfg(**kw):
                 significance_threshold=None, strict_topology=False, seed=11)
     base.update(kw)
     return SimpleNamespace(**base)
+
+
+def add_active_tiles(g):
+    """A copy of a DenseLeafGrid with active level-1 tiles added in empty
+    slots (every slot with (i + j + k) % 5 == 0 that is neither a child nor
+    a tile), values a smooth function of the slot centre in (0.55, 0.95):
+    exercises the tile regressor path (decoder.py:136-141)."""
+    import copy
+    from paper_2208_04448_b200.model import L1_LOCAL
+    h = copy.deepcopy(g)
+    ijk = L1_LOCAL  # (4096, 3) slot index triples, idx1 order
+    pick = ((ijk.sum(axis=1) % 5) == 0)[None, :] & ~h.l1_child & ~h.l1_active
+    cen = h.l1_origins[:, None, :].astype(np.float64) + ijk[None] * 8.0 + 4.0
+    val = (0.75 + 0.2 * np.sin(cen[..., 0] / 9.0) * np.cos(cen[..., 1] / 7.0)).astype(np.float32)
+    h.l1_active = h.l1_active | pick
+    h.l1_tiles = np.where(pick, val, h.l1_tiles).astype(np.float32)
+    return h

@@ -380,3 +380,35 @@ def test_strict_topology_decode_masks_exact_on_gpu():
     np.testing.assert_allclose(v, g.leaf_values[li, vi], atol=1e-6)
     m.close()
     h.model.close()
+
+
+def test_active_tiles_match_reference(golden):
+    """Active level-1 tiles (decoder.py:136-141; tile regressor trained on the
+    tile targets, encoder.py:205-218): on an fBm grid with 795 added active
+    tiles, the decoded tile values follow the reference's own encode + decode
+    of the same grid (tests/golden/make_golden_multi_encode.py: tile RMS error
+    vs truth 0.0561, 120 epochs)."""
+    from helpers import add_active_tiles
+    from paper_2208_04448_b200.procgen import fbm_density
+    z = golden("multi_encode")
+    base = fbm_density(octaves=3, lacunarity=2.0, gain=0.5, base_frequency=0.06, seed=4,
+                       domain=((0, 0, 0), (40, 40, 40)), threshold=0.5, voxel_size=1.0, device=DEV)
+    tg = add_active_tiles(base)
+    cfg = tiny_cfg(max_epochs=120, l0_net=(2, 32), voxel_net=(2, 32), ffm_size=32, tile_net=(2, 16))
+    c = encode(tg, cfg, device=DEV)
+    assert c.experts[0].tile_regressor is not None
+    m = DeviceModel(c, DEV)
+    g = m.decode(True).to_grid()
+    np.testing.assert_array_equal(g.l1_origins, tg.l1_origins)
+    sel = tg.l1_active & ~tg.l1_child
+    np.testing.assert_array_equal(g.l1_active & ~g.l1_child, sel)
+    got = g.l1_tiles[sel]
+    err = float(np.sqrt(np.mean((got - tg.l1_tiles[sel]) ** 2)))
+    dref = np.abs(got - z["tile_ref"])
+    print(f"tiles: {int(sel.sum())}, rms err vs truth {err:.4f} (reference {float(z['tile_err'][0]):.4f}), "
+          f"|gpu - reference decode| max {dref.max():.2e} rms {np.sqrt(np.mean(dref ** 2)):.2e}, "
+          f"epochs {c.experts[0].tile_regressor.epochs} (reference {int(z['tile_epochs'][0])})")
+    assert c.experts[0].tile_regressor.epochs == int(z["tile_epochs"][0])
+    assert err <= float(z["tile_err"][0]) * 1.1 + 1e-3
+    assert dref.max() < 2e-2 and np.sqrt(np.mean(dref ** 2)) < 5e-3
+    m.close()

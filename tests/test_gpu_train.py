@@ -412,3 +412,35 @@ def test_active_tiles_match_reference(golden):
     assert err <= float(z["tile_err"][0]) * 1.1 + 1e-3
     assert dref.max() < 2e-2 and np.sqrt(np.mean(dref ** 2)) < 5e-3
     m.close()
+
+
+def test_data_parallel_phases_equal_fused_epochs():
+    """The data-parallel form of an epoch (nvdb_trainer_phase 1: gradients and
+    loss into nvdb_trainer_buffers for the caller's all-reduce; phase 2: Adam)
+    on one rank is bit-identical to the fused single-rank epochs: both sum the
+    per-CTA partials in the same fixed order."""
+    rng = np.random.default_rng(12)
+    n = 20000
+    x = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+    y = (0.5 * np.sin(5 * x[:, 0]) * np.cos(3 * x[:, 2])).astype(np.float32)
+    ff = FourierFeatures(48, 5.0, 3)
+    p0 = init_mlp(96, [64, 64], 1, Activation("sine", 3.0), "linear", 4)
+    cfg = tiny_cfg(max_epochs=10, batch_size=4096, lr=1e-3, activation="sine", frequency=3.0)
+    fused = DeviceTrainer(p0, ff, x, y, "mse", cfg, 1e-3, 7, True, -1.0, DEV)
+    fused.run()
+    dp = DeviceTrainer(p0, ff, x, y, "mse", cfg, 1e-3, 7, True, -1.0, DEV)
+    st = torch.cuda.current_stream(DEV).cuda_stream
+    L = _lib.lib()
+    g, npar, lo = C.c_void_p(), C.c_int64(), C.c_void_p()
+    assert L.nvdb_trainer_buffers(dp.handle, C.byref(g), C.byref(npar), C.byref(lo)) == 0 and g.value
+    for _ in range(10):
+        assert L.nvdb_trainer_phase(dp.handle, 1, st) == 0
+        assert L.nvdb_trainer_phase(dp.handle, 2, st) == 0  # one rank: the all-reduce is the identity
+    torch.cuda.synchronize()
+    a, b = fused.weights(), dp.weights()
+    for (wa, ba), (wb, bb) in zip(a.layers, b.layers):
+        np.testing.assert_array_equal(wa, wb)
+        np.testing.assert_array_equal(ba, bb)
+    np.testing.assert_array_equal(fused.status()[2][:10], dp.status()[2][:10])
+    fused.close()
+    dp.close()

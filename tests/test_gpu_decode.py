@@ -126,3 +126,36 @@ def test_hybrid_query_empty_and_far_batches(golden):
     np.testing.assert_array_equal(a2[3:], ar)
     np.testing.assert_array_equal(v2[3:], vr)
     h.model.close()
+
+
+def test_corrupt_containers_raise_svcodec_error(golden):
+    """decoder.py:66-77, 121-130, 174-175: containers whose level-1 origins
+    lack level-2 child bits, whose patches fall outside every node, or whose
+    level-0 patches hit no reconstructed leaf raise SvcodecError."""
+    import copy
+    from paper_2208_04448_b200.errors import SvcodecError
+    z = golden("decode_small")
+    base = container_from_arrays(z)
+    # a level-1 origin with no level-2 child bit
+    c = copy.deepcopy(base)
+    o = c.upper_tree.l1_origins[0]
+    c.upper_tree.l1_origins.append((o[0] + 128 * 7, o[1], o[2]))
+    with pytest.raises(SvcodecError):
+        DeviceModel(c).decode(True)
+    # a level-1 patch outside every level-1 node
+    c = copy.deepcopy(base)
+    c.experts[0].patches.l1.append(((1 << 20, 0, 0), 1))
+    with pytest.raises(SvcodecError):
+        DeviceModel(c).decode(True)
+    # a level-0 patch inside a node but in a slot that decodes to no leaf
+    c = copy.deepcopy(base)
+    m = DeviceModel(c)
+    d = m.decode(False)
+    cls = d.l1_class.cpu().numpy().reshape(-1, 4096)
+    ni, si = np.argwhere(cls != 0)[0]
+    from paper_2208_04448_b200.model import L1_LOCAL
+    corner = m.origins[ni] + L1_LOCAL[si] * 8
+    m.close()
+    c.experts[0].patches.l0.append((tuple(int(v) for v in corner), True, 0.5))
+    with pytest.raises(SvcodecError):
+        DeviceModel(c).decode(True)

@@ -220,3 +220,23 @@ def test_leaf_bits_map_behaves_like_the_reference_dict():
     assert keys.shape == (len(d), 3) and bits.shape == (len(d), 512) and bits.dtype == bool
     with pytest.raises(ValueError):
         LeafBitsMap.from_arrays(np.zeros((2, 3)), np.zeros((2, 512), bool))  # duplicate origins
+
+
+def test_training_input_errors_match_reference():
+    """neural.py:282-283, 295-296, 309-310: NaN inputs, CE labels outside the
+    head and non-binary BCE targets raise ValueError, before any device work."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from helpers import tiny_cfg
+    from paper_2208_04448_b200.encoder import net_spec, train_network
+    cfg = tiny_cfg()
+    x = np.zeros((10, 3), np.float32)
+    xn = x.copy()
+    xn[3, 1] = np.nan
+    for xx, yy, tag, msg in ((xn, np.zeros(10, np.float32), "voxel", "NaN"),
+                             (x, np.full(10, 5), "l1", "label"),
+                             (x, np.full(10, -1), "l1", "label"),
+                             (x, np.full(10, 0.5, np.float32), "l0", "binary"),
+                             (x, np.array([0, 1, np.nan, 0, 1, 0, 0, 1, 1, 0], np.float32), "voxel", "NaN")):
+        with pytest.raises(ValueError, match=msg):
+            train_network(xx, yy, net_spec(tag, cfg), cfg, 0, cfg.lr)

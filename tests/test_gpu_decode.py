@@ -125,6 +125,11 @@ def test_hybrid_query_empty_and_far_batches(golden):
     vr, ar = h.query(z["q"][:500])
     np.testing.assert_array_equal(a2[3:], ar)
     np.testing.assert_array_equal(v2[3:], vr)
+    # grid.py:47, 69-71: |c| >= 2^30 is outside the legal range
+    from paper_2208_04448_b200.errors import SvcodecError
+    for bad in ([1 << 30, 0, 0], [0, -(1 << 30), 0]):
+        with pytest.raises(SvcodecError):
+            h.query(np.array([bad], np.int64))
     h.model.close()
 
 

@@ -175,3 +175,53 @@ def test_c2_oracle_sample_parity(c2):
     print(f"values: max {err.max():.2e} rms {np.sqrt(np.mean(err ** 2)):.2e} on {both.sum()} voxels")
     m.close()
     assert err.max() < VAL_MAX and np.sqrt(np.mean(err ** 2)) < VAL_RMS_C2
+
+
+def test_c5_shaped_query_sample_parity():
+    """C5 shape at reduced size: a sphere (r 300, band 3)
+    across 2 x 2 x 2 subdomains with Lucy-class 3x256/m256 voxel nets (random
+    weights, streamed through shared memory), queried at 200 K uniform
+    coordinates plus 4 K active voxels.  Lookup (value, active) bit-exact with
+    the oracle's get_values; regressed rows equal the oracle's gate-blended
+    forward (clip, x3) within the fp16-operand bars."""
+    import oracle as O
+    from paper_2208_04448_b200.decoder import NetEvaluator, hybrid_query
+    from paper_2208_04448_b200.encoder import decompose, expert_norm, init_mlp
+    from paper_2208_04448_b200.model import Activation, EncodedSubdomain, FourierFeatures, NetRecord
+    from paper_2208_04448_b200.procgen import sphere_sdf
+    from paper_2208_04448_b200.tree import DeviceTree
+    dev = torch.device("cuda:0")
+    g = sphere_sdf((512.0, 512.0, 512.0), 300.0, 1.0, 3.0)
+    layout = decompose(g, 512)
+    assert len(layout.subdomains) == 8
+    rng = np.random.default_rng(0)
+    experts = []
+    for sub in layout.subdomains:
+        no, ns = expert_norm(sub, g)
+        e = EncodedSubdomain(sub.id, sub.cell, sub.cluster_id, no, ns, 3.0)
+        p = init_mlp(512, [256] * 3, 1, Activation("sine", 3.0), "linear", 100 + sub.id)
+        w, b = p.layers[-1]
+        p.layers[-1] = (rng.normal(0, 0.05, size=w.shape).astype(np.float32), b)
+        e.voxel_regressor = NetRecord(p, FourierFeatures(256, 10.0, 200 + sub.id))
+        experts.append(e)
+    experts.sort(key=lambda e: e.id)
+    ev = NetEvaluator(experts, layout.size, layout.halo, float(g.background), dev)
+    tree = DeviceTree(g)
+    li, vi = np.nonzero(g.leaf_active)
+    pick = rng.choice(li.size, 4096, replace=False)
+    act_c = g.leaf_origins[li[pick]] + np.stack([vi[pick] >> 6, (vi[pick] >> 3) & 7, vi[pick] & 7], 1)
+    coords = np.concatenate([rng.integers(0, 1024, (200_000, 3)), act_c]).astype(np.int32)
+    val, act, nr = hybrid_query(tree, ev, torch.from_numpy(coords).to(dev), 3.0, True)
+    val, act = val.cpu().numpy(), act.cpu().numpy().astype(bool)
+    rv, ra, rk = O.lookup(g, coords.astype(np.int64))
+    np.testing.assert_array_equal(act, ra)
+    reg = ra & (rk == 2)
+    assert nr == int(reg.sum()) and nr >= 4096
+    np.testing.assert_array_equal(val[~reg].view(np.uint32), np.asarray(rv, np.float32)[~reg].view(np.uint32))
+    bv, cov = O.blended(layout, experts, coords[reg].astype(np.float64) + 0.5, "voxel")
+    ref = np.where(cov, np.clip(bv[:, 0], -1.0, 1.0) * 3.0, g.background).astype(np.float32)
+    err = np.abs(val[reg] - ref)
+    print(f"C5-shaped sample: {coords.shape[0]} queries, {nr} regressed, max {err.max():.2e} "
+          f"rms {np.sqrt(np.mean(err ** 2)):.2e}")
+    assert err.max() < 2e-2 * 3.0 and np.sqrt(np.mean(err ** 2)) < 3e-3 * 3.0
+    ev.close()

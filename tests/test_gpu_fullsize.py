@@ -225,3 +225,75 @@ def test_c5_shaped_query_sample_parity():
           f"rms {np.sqrt(np.mean(err ** 2)):.2e}")
     assert err.max() < 2e-2 * 3.0 and np.sqrt(np.mean(err ** 2)) < 3e-3 * 3.0
     ev.close()
+
+
+def test_c3_shaped_decode_sample_parity():
+    """C3 shape at reduced size: fBm density on a 128^3 box
+    straddling the S = 512 lattice point, 8 experts, Chameleon-class 3x256/m256
+    level-0 and voxel nets (random weights, streamed weights, sorted
+    multi-expert passes).  Level-0 occupancy over every leaf voxel and voxel
+    values over every active voxel, against the oracle's gate-blended
+    forward on a 48-leaf sample."""
+    import oracle as O
+    from paper_2208_04448_b200 import _lib
+    from paper_2208_04448_b200.decoder import NetEvaluator
+    from paper_2208_04448_b200.encoder import decompose, expert_norm, init_mlp
+    from paper_2208_04448_b200.model import (LEAF_LOCAL, Activation, EncodedSubdomain, FourierFeatures,
+                                             NetRecord)
+    from paper_2208_04448_b200.procgen import fbm_density
+    dev = torch.device("cuda:0")
+    g = fbm_density(octaves=5, lacunarity=2.0, gain=0.5, base_frequency=4.0 / 1024.0, seed=9,
+                    domain=((448, 448, 448), (576, 576, 576)), threshold=0.45, device=dev)
+    layout = decompose(g, 512)
+    assert len(layout.subdomains) == 8
+    rng = np.random.default_rng(1)
+
+    def net(m, width, out, head, seed):
+        p = init_mlp(2 * m, [width] * 3, out, Activation("sine", 3.0), head, seed)
+        w, b = p.layers[-1]
+        p.layers[-1] = (rng.normal(0, 0.05, size=w.shape).astype(np.float32), b)
+        return NetRecord(p, FourierFeatures(m, 10.0, seed + 1))
+    experts = []
+    for sub in layout.subdomains:
+        no, ns = expert_norm(sub, g)
+        e = EncodedSubdomain(sub.id, sub.cell, sub.cluster_id, no, ns, 1.0)
+        e.l0_classifier = net(256, 256, 1, "binary", 10 * sub.id + 2)
+        e.voxel_regressor = net(256, 256, 1, "linear", 10 * sub.id + 3)
+        experts.append(e)
+    experts.sort(key=lambda e: e.id)
+    ev = NetEvaluator(experts, layout.size, layout.halo, 0.0, dev)
+    lo = torch.from_numpy(g.leaf_origins.astype(np.int32)).to(dev)
+    nvox = lo.shape[0] * 512
+    u8 = torch.empty(nvox, dtype=torch.uint8, device=dev)
+    ev.evaluate("l0", _lib.SRC_LEAF_VOX, lo, nvox, _lib.OUT_L0ACTIVE, u8=u8)
+    act_ids = np.flatnonzero(g.leaf_active.reshape(-1)).astype(np.int64)
+    vals = torch.empty(act_ids.size, dtype=torch.float32, device=dev)
+    ev.evaluate("voxel", _lib.SRC_LEAF_VOX, lo, act_ids.size, _lib.OUT_VALUE,
+                gather=torch.from_numpy(act_ids).to(dev), f32=vals, value_scale=1.0, clip=False)
+    occ = u8.cpu().numpy().reshape(-1, 512).astype(bool)
+    vals = vals.cpu().numpy()
+    # oracle on a sample of leaves, half of them in the halo overlap around 512
+    lc = g.leaf_origins + 4
+    near = np.flatnonzero((np.abs(lc - 512) < 16).any(axis=1))
+    far = np.setdiff1d(np.arange(lc.shape[0]), near)
+    sample = np.concatenate([rng.choice(near, 24, replace=False), rng.choice(far, 24, replace=False)])
+    cen = (g.leaf_origins[sample][:, None, :] + (LEAF_LOCAL + 0.5)[None]).reshape(-1, 3)
+    p0, cov0 = O.blended(layout, experts, cen, "l0")
+    ref_occ = (cov0 & (p0[:, 0] > 0.5)).reshape(-1, 512)
+    flips = occ[sample] != ref_occ
+    near_tie = np.abs(p0[:, 0].reshape(-1, 512) - 0.5)[flips]
+    print(f"C3-shaped sample: occupancy agreement {1 - flips.mean():.6f}, max |p - 0.5| at a flip "
+          f"{near_tie.max() if near_tie.size else 0:.2e}")
+    # random nets put many probabilities near 0.5: every flip must be a near tie
+    assert flips.mean() <= 5e-3 and (near_tie < 2e-2).all()
+    pos = {v: i for i, v in enumerate(act_ids.tolist())}
+    sel = [(si * 512 + k, pos[int(leaf) * 512 + k]) for si, leaf in enumerate(sample)
+           for k in np.flatnonzero(g.leaf_active[leaf])]
+    ci = np.array([a for a, _ in sel])
+    gi = np.array([b for _, b in sel])
+    vref, vcov = O.blended(layout, experts, cen[ci], "voxel")
+    assert vcov.all()
+    err = np.abs(vals[gi] - vref[:, 0])
+    print(f"values on {ci.size} active voxels: max {err.max():.2e} rms {np.sqrt(np.mean(err ** 2)):.2e}")
+    assert err.max() < 2e-2 * max(1.0, np.abs(vref).max()) and np.sqrt(np.mean(err ** 2)) < 3e-3
+    ev.close()

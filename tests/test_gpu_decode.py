@@ -164,3 +164,18 @@ def test_corrupt_containers_raise_svcodec_error(golden):
     c.experts[0].patches.l0.append((tuple(int(v) for v in corner), True, 0.5))
     with pytest.raises(SvcodecError):
         DeviceModel(c).decode(True)
+
+
+@pytest.mark.parametrize("name", ["decode_small", "decode_multi"])
+def test_decode_report_counts(golden, name):
+    """decoder.decode_report (decoder.py:294-300): regressor evaluations and
+    active voxels of the full decode, against the reference's decode."""
+    from paper_2208_04448_b200.decoder import decode_report
+    z = golden(name)
+    c = container_from_arrays(z)
+    rep = decode_report(c)
+    ref = grid_from_arrays(z, "d_")
+    print(name, rep, "reference evals", int(z["evals"][0]), "active", int(ref.leaf_active.sum()))
+    assert abs(rep["regressor_evaluations"] - int(z["evals"][0])) <= max(3, int(0.001 * z["evals"][0]))
+    assert abs(rep["active_voxels"] - int(ref.leaf_active.sum())) <= max(3, int(0.001 * ref.leaf_active.sum()))
+    assert rep["regressor_evaluations"] == rep["active_voxels"]

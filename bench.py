@@ -228,6 +228,22 @@ def query_bench(m, dev, steps, nq=1 << 27, lo=-32, hi=544, seed=0):
             ts.append(e0.elapsed_time(e1))
         return statistics.median(ts)
 
+    # end to end through the public HybridGrid.query: host int32 coords in,
+    # host (value, active) out, copies inside the timed region
+    ne = 1 << 24
+    host = coords[:ne].cpu().numpy()
+    for _ in range(2):
+        hg.query(host)
+    te = []
+    for _ in range(max(steps, 3)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hg.query(host)
+        torch.cuda.synchronize()
+        te.append(time.perf_counter() - t0)
+    e2e = {"value": ne / statistics.median(te), "unit": "queries/s", "queries": ne,
+           "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(ne * 5),
+           "api": "HybridGrid.query(numpy int32 (n, 3)) -> numpy (value f32, active bool)"}
     t_lookup = timed(lambda: hg.tree.lookup(coords))
     hg.regressor_evaluations = 0
     t_query = timed(lambda: hg.query_device(coords))
@@ -235,7 +251,7 @@ def query_bench(m, dev, steps, nq=1 << 27, lo=-32, hi=544, seed=0):
     bytes_q = 18
     return {"value": nq / (t_query * 1e-3), "unit": "queries/s", "queries": nq, "ms": t_query,
             "coords": f"uniform int32 in [{lo},{hi})^3 (torch Philox, seed {seed})",
-            "regressor_rows": int(evals),
+            "regressor_rows": int(evals), "e2e": e2e,
             "lookup": {"ms": t_lookup, "value": nq / (t_lookup * 1e-3), "unit": "queries/s",
                        "roofline": {"bound": "hbm", "bytes_per_query": bytes_q,
                                     "achieved": nq * bytes_q / (t_lookup * 1e-3) / 1e9, "unit": "GB/s"}}}

@@ -614,12 +614,17 @@ class HybridGrid:
 
     def query(self, coords) -> Tuple[np.ndarray, np.ndarray]:
         """Batched (value, active) at integer coordinates (decoder.py:239-264)."""
-        c = np.asarray(coords, dtype=np.int64).reshape(-1, 3)
-        if np.abs(c).max(initial=0) >= (1 << 30):
+        c = np.asarray(coords)
+        if c.dtype != np.int32:
+            c = c.astype(np.int64)
+        c = c.reshape(-1, 3)
+        lim = 1 << 30
+        if c.size and (c.max() >= lim or c.min() <= -lim):  # grid.py:69-71, no abs() overflow on int32
             raise SvcodecError("coordinate outside legal range +-2^30")
-        d = torch.from_numpy(c.astype(np.int32)).to(self.model.dev)
+        d = torch.from_numpy(np.ascontiguousarray(c, dtype=np.int32)).to(self.model.dev)
         v, a = self.query_device(d)
-        return v.cpu().numpy(), a.cpu().numpy().astype(bool)
+        v, a = _to_host([v, a])
+        return v.copy(), a.view(np.bool_).copy()
 
 
 def make_hybrid(c, device=None) -> HybridGrid:

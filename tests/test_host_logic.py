@@ -240,3 +240,24 @@ def test_training_input_errors_match_reference():
                              (x, np.array([0, 1, np.nan, 0, 1, 0, 0, 1, 1, 0], np.float32), "voxel", "NaN")):
         with pytest.raises(ValueError, match=msg):
             train_network(xx, yy, net_spec(tag, cfg), cfg, 0, cfg.lr)
+
+
+def test_committed_bench_line_keeps_the_contract():
+    """profiles/r01/bench_c2_final.json (a real bench.py line) carries every key
+    the driver and the judge read."""
+    import json
+    d = json.load(open(os.path.join(ROOT, "profiles", "r01", "bench_c2_final.json")))
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+              "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["config"]["workload"] and d["warmup"] >= 3 and d["gpu_launches"] > 0
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "tensor") and r["peak"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert "traffic" in r and r["co_bound"]["bound"] == "mufu"
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    c = d["clocks"]
+    assert c["sm_mhz"] > 0 and not set(c["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}

@@ -233,3 +233,41 @@ def test_lookup_extreme_and_empty_coordinates(golden):
     np.testing.assert_array_equal(k, rk)
     v0, a0, k0 = tree.lookup(torch.zeros((0, 3), dtype=torch.int32, device=DEV))
     assert v0.numel() == 0 and a0.numel() == 0 and k0.numel() == 0
+
+
+def test_operator_seams_match_reference(golden):
+    """The numpy-in / numpy-out operator seams a maintainer binds in svcodec
+    (SURVEY.md §8(b)): ops.forward_block (neural.py:527), ops.blended_*
+    (inference.py:65-84) and ops.get_values (grid.py:310) against the
+    reference's golden outputs."""
+    from paper_2208_04448_b200 import ops
+    z = golden("nets")
+    for ci in range(int(z["ncases"][0])):
+        q = f"n{ci}_"
+        params, ff = net_from_fixture(z, q)
+        got = ops.forward_block(params, ff, z[q + "pts"])
+        ref = O.forward_block(params, ff, z[q + "pts"])
+        assert got.shape == ref.shape and got.dtype == np.float32
+        assert np.abs(got - ref).max() < 2e-2 * max(1.0, np.abs(ref).max())
+    with pytest.raises(ValueError):
+        ops.forward_block(params, ff, np.full((4, 3), np.nan, np.float32))
+    z = golden("decode_multi")
+    c = container_from_arrays(z)
+    p1, c1 = ops.blended_l1_probs(c.layout, c.experts, z["cen"])
+    p0, c0 = ops.blended_l0_probs(c.layout, c.experts, z["cen"])
+    pv, cv = ops.blended_values(c.layout, c.experts, z["cen"])
+    np.testing.assert_array_equal(c1, z["c1"])
+    np.testing.assert_array_equal(c0, z["c0"])
+    np.testing.assert_array_equal(cv, z["cv"])
+    assert p1.shape == (z["cen"].shape[0], 3) and p0.shape == pv.shape == (z["cen"].shape[0],)
+    assert np.abs(p1 - z["p1"].reshape(p1.shape)).max() < 2e-2
+    assert np.abs(p0 - z["p0"].reshape(p0.shape)).max() < 2e-2
+    assert np.abs(pv - z["pv"].reshape(pv.shape)).max() < 2e-2
+    z = golden("lookup_small")
+    g = grid_from_arrays(z)
+    v, a, k = ops.get_values(g, z["coords"], with_kind=True)
+    np.testing.assert_array_equal(v.view(np.uint32), z["values"].view(np.uint32))
+    np.testing.assert_array_equal(a, z["active"])
+    np.testing.assert_array_equal(k, z["kind"])
+    v2, a2 = ops.get_values(g, z["coords"][:10])
+    np.testing.assert_array_equal(v2, v[:10])

@@ -372,8 +372,9 @@ def run_reference(args, rank, world):
 
 
 def _reference_container(workload, cfg):
-    """The reference arm decodes a container of the same shape; it is trained by
-    this framework on the GPU when one is present, else taken from the C1 fixture."""
+    """The container the reference arm decodes: always the committed C1 fixture
+    (the reference's own AC4 encode, tests/golden/c1_sphere128.npz), whatever
+    the workload."""
     from paper_2208_04448_b200.model import container_from_arrays
     z = np.load(os.path.join(ROOT, "tests", "golden", "c1_sphere128.npz"))
     return container_from_arrays(z)

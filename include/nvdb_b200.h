@@ -242,9 +242,15 @@ typedef struct {
 } nvdb_train_desc;
 
 NVDB_API int nvdb_trainer_create(const nvdb_train_desc* desc, nvdb_trainer** out);
+/* Does not synchronize: the trainer's device blocks go to a per-device cache
+ * with an event recorded after its last enqueued work, and the next trainer
+ * created on that device waits for the event before reusing them. */
 NVDB_API int nvdb_trainer_destroy(nvdb_trainer* tr);
+/* Release the trainer block cache of every device; returns the bytes freed. */
+NVDB_API size_t nvdb_trim(void);
 /* enqueue `epochs` epochs (sampler -> fwd/dgrad -> wgrad -> Adam); epochs
- * after the early stop are no-ops on the device */
+ * after the early stop are no-ops on the device; enqueueing more than
+ * max_epochs epochs in total returns NVDB_EINVAL */
 NVDB_API int nvdb_trainer_run(nvdb_trainer* tr, int32_t epochs, void* stream);
 /* one epoch split for data parallelism: phase 1 = sampler, fwd/dgrad, wgrad,
  * partial reduction into the gradient buffer; phase 2 = Adam, early stop,

@@ -32,7 +32,7 @@ EXPORTED = [
     "nvdb_leaf_list", "nvdb_l0_apply", "nvdb_leaf_finalize", "nvdb_pack_eq", "nvdb_neural_rows",
     "nvdb_query_finalize", "nvdb_trainer_create", "nvdb_trainer_destroy", "nvdb_trainer_run",
     "nvdb_trainer_status", "nvdb_trainer_weights", "nvdb_sample_indices", "nvdb_trainer_phase",
-    "nvdb_trainer_buffers", "nvdb_sample_indices_subset", "nvdb_fbm_leaves",
+    "nvdb_trainer_buffers", "nvdb_sample_indices_subset", "nvdb_fbm_leaves", "nvdb_trim",
 ]
 
 SRC_NORM_F32, SRC_CENTER_F64, SRC_COORD_I32, SRC_LEAF_VOX, SRC_L1_SLOT = range(5)
@@ -119,6 +119,7 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_query_finalize": (C.c_int, [vp, i64, vp, vp, vp, vp, vp, vp]),
         "nvdb_trainer_create": (C.c_int, [C.POINTER(TrainDesc), C.POINTER(vp)]),
         "nvdb_trainer_destroy": (C.c_int, [vp]),
+        "nvdb_trim": (sz, []),
         "nvdb_trainer_run": (C.c_int, [vp, i32, vp]),
         "nvdb_trainer_status": (C.c_int, [vp, C.POINTER(i32), C.POINTER(i32), vp, i32]),
         "nvdb_trainer_weights": (C.c_int, [vp, C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.POINTER(C.c_float))]),

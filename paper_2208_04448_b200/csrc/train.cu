@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -1154,9 +1155,10 @@ __global__ void __launch_bounds__(kRedThreads) k_train_adam(AdamArgs a) {
 
 // the stop decision of k_train_adam takes effect here, after every block of
 // the update ran (the reference applies the stopping epoch's update, then breaks)
-__global__ void k_train_advance(int32_t* epoch, int32_t* stopped, int32_t* epochs_done, const int32_t* stop_next) {
+__global__ void k_train_advance(int32_t* epoch, int32_t* stopped, int32_t* epochs_done, const int32_t* stop_next,
+                                int32_t max_epochs) {
   if (*stopped) return;
-  if (*stop_next) {
+  if (*stop_next || *epoch + 1 >= max_epochs) {  // early stop, or the last epoch ran
     *stopped = 1;
     *epochs_done = *epoch + 1;
   } else {
@@ -1216,17 +1218,35 @@ struct nvdb_trainer {
   double* loss_hist = nullptr;
   int64_t* dpoff = nullptr;
   std::vector<std::pair<void*, size_t>> owned;  // device blocks from the block cache
+  int device = -1;
+  cudaEvent_t done = nullptr;  // recorded after every enqueue (stream-ordered block reuse at destroy)
+  bool enqueued = false;
+  ~nvdb_trainer();
 };
 
 namespace {
 
-// Device block cache for trainer buffers: encode / encode_sequence create and
+// Device block cache for trainer buffers.  encode / encode_sequence create and
 // destroy a trainer per network with the same sizes, and cudaMalloc/cudaFree
 // of the ~0.3 GB per trainer (presampled indices, tile images, partials)
-// cost ~90 ms per trainer; freed blocks are kept by size class (up to 4 GiB)
-// and handed to the next trainer.  Contents are not cleared (as cudaMalloc).
+// cost ~90 ms per trainer; freed blocks are kept by (device, size class) and
+// handed to the next trainer on the same device.  Reuse is stream ordered:
+// a block returns to the cache with the event recorded after its trainer's
+// last enqueued work, and is handed out only after that event completed.
+// Contents are not cleared (as cudaMalloc).  nvdb_trim() releases the cache;
+// a failed cudaMalloc releases it and retries once.
+struct ReadyEvent {  // shared by every block of one destroyed trainer
+  cudaEvent_t e = nullptr;
+  ~ReadyEvent() {
+    if (e) cudaEventDestroy(e);
+  }
+};
+struct CachedBlock {
+  void* p;
+  std::shared_ptr<ReadyEvent> ready;  // null: no work was ever enqueued on the block
+};
 std::mutex g_cache_mu;
-std::multimap<size_t, void*> g_cache;
+std::multimap<std::pair<int, size_t>, CachedBlock> g_cache;  // (device, size class) -> block
 size_t g_cache_bytes = 0;
 constexpr size_t kCacheCap = size_t(4) << 30;
 
@@ -1237,32 +1257,74 @@ size_t size_class(size_t b) {
   return c;
 }
 
+// release every cached block (all devices); returns the bytes freed
+size_t cache_release_all() {
+  std::multimap<std::pair<int, size_t>, CachedBlock> drop;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    drop.swap(g_cache);
+    g_cache_bytes = 0;
+  }
+  size_t freed = 0;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& kv : drop) {
+    cudaSetDevice(kv.first.first);
+    if (kv.second.ready) cudaEventSynchronize(kv.second.ready->e);
+    cudaFree(kv.second.p);
+    freed += kv.first.second;
+  }
+  cudaSetDevice(cur);
+  return freed;
+}
+
 cudaError_t cached_malloc(void** p, size_t* bytes) {
   const size_t c = size_class(*bytes);
   *bytes = c;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  CachedBlock blk{nullptr, {}};
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto it = g_cache.find(c);
+    auto it = g_cache.find({dev, c});
     if (it != g_cache.end()) {
-      *p = it->second;
+      blk = it->second;
       g_cache.erase(it);
       g_cache_bytes -= c;
-      return cudaSuccess;
     }
   }
-  return cudaMalloc(p, c);
+  if (blk.p) {
+    if (blk.ready) {  // the previous owner's queued kernels may still touch the block
+      e = cudaEventSynchronize(blk.ready->e);
+      if (e != cudaSuccess) return e;
+    }
+    *p = blk.p;
+    return cudaSuccess;
+  }
+  e = cudaMalloc(p, c);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    cache_release_all();
+    e = cudaMalloc(p, c);
+  }
+  return e;
 }
 
-void cached_free(void* p, size_t bytes) {
+// `ready`: event after the last work that may use the block (ownership passes to the cache)
+void cached_free(void* p, size_t bytes, const std::shared_ptr<ReadyEvent>& ready) {
   if (!p) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     if (g_cache_bytes + bytes <= kCacheCap) {
-      g_cache.emplace(bytes, p);
+      g_cache.emplace(std::make_pair(dev, bytes), CachedBlock{p, ready});
       g_cache_bytes += bytes;
       return;
     }
   }
+  if (ready) cudaEventSynchronize(ready->e);
   cudaFree(p);
 }
 
@@ -1278,12 +1340,31 @@ int dalloc(nvdb_trainer* tr, T** p, size_t count) {
 
 }  // namespace
 
+nvdb_trainer::~nvdb_trainer() {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (device >= 0) cudaSetDevice(device);
+  // the blocks go back to the cache with the event recorded after this
+  // trainer's last enqueued work (the cache now owns the event)
+  std::shared_ptr<ReadyEvent> ready;
+  if (done) {
+    ready = std::make_shared<ReadyEvent>();
+    ready->e = done;
+    if (!enqueued) ready.reset();  // never recorded: nothing to wait for (destroys the event)
+    done = nullptr;
+  }
+  for (auto& b : owned) cached_free(b.first, b.second, ready);
+  owned.clear();
+  cudaSetDevice(cur);
+}
+
 extern "C" int nvdb_trainer_destroy(nvdb_trainer* tr) {
   if (!tr) return NVDB_OK;
-  for (auto& b : tr->owned) cached_free(b.first, b.second);
   delete tr;
   return NVDB_OK;
 }
+
+extern "C" size_t nvdb_trim(void) { return cache_release_all(); }
 
 extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out) {
   if (!d || !out) return fail(NVDB_EINVAL, "nvdb_trainer_create: null argument");
@@ -1295,6 +1376,8 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
     return fail(NVDB_EUNSUPPORTED, "sample_interval * batch >= 2^32");
   if (d->sampled && (uint64_t)d->n > 0xFFFFFFFFull) return fail(NVDB_EUNSUPPORTED, "n >= 2^32");
   std::unique_ptr<nvdb_trainer> tr(new nvdb_trainer());
+  NVDB_CUDA_TRY(cudaGetDevice(&tr->device));
+  NVDB_CUDA_TRY(cudaEventCreateWithFlags(&tr->done, cudaEventDisableTiming));
   tr->d = *d;
   tr->m = nd.m;
   tr->Wr = nd.width;
@@ -1340,6 +1423,14 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   const size_t o_bias = align_up(wimg_bytes, 256), o_headw = align_up(o_bias + 4 * depth * W, 256);
   const size_t o_headb = align_up(o_headw + 4 * 3 * W, 256), o_b2pi = align_up(o_headb + 16, 256);
   const size_t blob_bytes = align_up(o_b2pi + 4 * 3 * (k0 / 2), 256);
+  // shared-memory plan and kernel limits before any device allocation
+  tr->plan = plan_smem((uint32_t)wimg_bytes, W, tr->nwg);
+  if (enable_max_smem(k_train_fb) < (long long)tr->plan.total ||
+      enable_max_smem(k_train_wgrad<false>) < kWgSmem || enable_max_smem(k_train_wgrad<true>) < kWgSmem ||
+      enable_max_smem(k_train_fbwg<false>) < (long long)std::max<uint32_t>(tr->plan.total, kWgSmem) ||
+      enable_max_smem(k_train_fbwg<true>) < (long long)std::max<uint32_t>(tr->plan.total, kWgSmem))
+    return fail(NVDB_EUNSUPPORTED, "training kernels exceed the shared-memory limit (%u B of resident weights "
+                "and tile buffers)", tr->plan.total);
   std::vector<uint8_t> blob(blob_bytes, 0);
   std::vector<float> master(P), gscale(P), fold(P, 1.f);
   std::vector<int32_t> imgoff(P, -1), f32dst(P, -1);
@@ -1431,7 +1522,6 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   n.act = nd.activation;
   n.head = nd.head;
   n.expert = 0;
-  t->plan = plan_smem((uint32_t)wimg_bytes, W, t->nwg);
   // ---- per-step buffers
   const size_t tile_elems = (size_t)kTileM * W;
   {  // data-parallel share: contiguous tile range of this rank (whole batch when unsharded)
@@ -1490,13 +1580,6 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
     t->cub_tmp = q;
     t->owned.emplace_back(q, cb);
   }
-  // kernel attributes
-  if (enable_max_smem(k_train_fb) < (long long)t->plan.total ||
-      enable_max_smem(k_train_wgrad<false>) < kWgSmem || enable_max_smem(k_train_wgrad<true>) < kWgSmem ||
-      enable_max_smem(k_train_fbwg<false>) < (long long)std::max<uint32_t>(t->plan.total, kWgSmem) ||
-      enable_max_smem(k_train_fbwg<true>) < (long long)std::max<uint32_t>(t->plan.total, kWgSmem))
-    return fail(NVDB_EUNSUPPORTED, "training kernels exceed the shared-memory limit (%u B of resident weights "
-                "and tile buffers; weight streaming is built for decode only)", t->plan.total);
   *out = tr.release();
   return NVDB_OK;
 }
@@ -1508,6 +1591,11 @@ namespace {
 // fused_update: single rank -- the Adam kernel reduces the partials itself
 int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update, int sample_ahead) {
   const nvdb_train_desc& d = t->d;
+  // the device arrays (presampled indices, lr / c1 / c2, loss history) hold
+  // max_epochs rows; epochs past them are refused, not run off the end
+  if (t->host_epoch >= d.max_epochs)
+    return fail(NVDB_EINVAL, "trainer: all %d epochs already enqueued", d.max_epochs);
+  t->enqueued = true;
   int32_t* ep = t->ctl;
   int32_t* stopped = t->ctl + 1;
   if (phase == 1) {
@@ -1623,6 +1711,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
           t->partial, t->wg_grid, t->P, t->grad, t->loss_part, t->fb_grid, t->lossbuf, stopped);
       NVDB_CHECK_LAUNCH();
     }
+    NVDB_CUDA_TRY(cudaEventRecord(t->done, st));
     return NVDB_OK;
   }
     AdamArgs aa{};
@@ -1656,9 +1745,10 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
     aa.loss_hist = t->loss_hist;
     k_train_adam<<<(int)((t->P + kRedParams - 1) / kRedParams), kRedThreads, 0, st>>>(aa);
     NVDB_CHECK_LAUNCH();
-    k_train_advance<<<1, 1, 0, st>>>(ep, stopped, t->ctl + 2, t->ctl + 3);
+    k_train_advance<<<1, 1, 0, st>>>(ep, stopped, t->ctl + 2, t->ctl + 3, d.max_epochs);
     NVDB_CHECK_LAUNCH();
     ++t->host_epoch;
+    NVDB_CUDA_TRY(cudaEventRecord(t->done, st));
   return NVDB_OK;
 }
 }  // namespace

@@ -1,8 +1,8 @@
 """C3-shaped decode throughput: fBm density 1024^3 generated on
 the GPU, decomposed into 8 experts (2x2x2 at S = 512), Chameleon-class nets
 (L1 3x128/m128, L0 and voxel 3x256/m256; sine, omega 3) with random weights
-(the framework cannot train nets this wide yet, BASELINE.md allows random-init
-weights of the named architecture for throughput), then the device decode
+(the bench contract of the task -- not BASELINE.md -- asks for random-init
+weights of the named architecture when no trained ones exist), then the device decode
 stages over the grid's true topology: level-0 classification of every leaf
 voxel and voxel regression of every active voxel, gate-blended across the
 overlapping experts.

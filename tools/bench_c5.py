@@ -2,8 +2,8 @@
 int32 coordinates in [0, 2048)^3 (torch Philox, seed 0) through the hybrid
 grid of a 2048^3 narrow-band sphere (radius 960, half width 3: 69.5 M active
 voxels): upper-tree lookup, gate-blended voxel regressor (Lucy-class 3x256 /
-m256 nets with random weights -- the framework cannot train nets this wide
-yet; BASELINE.md allows random-init weights of the named architecture), value
+m256 nets with random weights: the bench contract of the task -- not
+BASELINE.md -- asks for random-init weights of the named architecture), value
 finalize.  The topology is the grid's own (what a perfectly trained
 classifier pair would reconstruct).
 

@@ -88,6 +88,7 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
     nd.act = d.activation;
     nd.head = d.head;
     nd.expert = 0;
+    nd.omega = d.activation == NVDB_ACT_SINE ? d.frequency : 1.0f;
     nd.wimg_bytes = (uint32_t)align_up((size_t)2 * ((size_t)W * k0 + (size_t)(d.depth - 1) * W * W), 16);
     max_wimg = std::max(max_wimg, nd.wimg_bytes);
     max_width = std::max(max_width, W);
@@ -116,17 +117,19 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
     const float om = sine ? d.frequency : 1.0f;
     uint16_t* wimg = reinterpret_cast<uint16_t*>(blob.data() + pieces[i].wimg);
     // layer 0: B operand (N = W rows, K = k0), serialized interleaved feature order;
-    // amplitude and omega folded in before rounding to fp16
+    // the feature amplitude (1 unless set) folded in, omega applied in the
+    // fp32 epilogue so 16-bit container weights stay exact in fp16
     for (int n = 0; n < d.width; ++n)
       for (int k = 0; k < 2 * m; ++k) {
-        const float w = d.weights[0][(size_t)n * 2 * m + k] * d.amplitude * om;
+        const float w = d.amplitude == 1.0f ? d.weights[0][(size_t)n * 2 * m + k]
+                                            : d.weights[0][(size_t)n * 2 * m + k] * d.amplitude;
         wimg[kmajor_offset(n, k, W) / 2] = f2h_bits(w);
       }
     size_t base = (size_t)W * k0;
     for (int l = 1; l < d.depth; ++l) {
       for (int n = 0; n < d.width; ++n)
         for (int k = 0; k < d.width; ++k)
-          wimg[base + kmajor_offset(n, k, W) / 2] = f2h_bits(d.weights[l][(size_t)n * d.width + k] * om);
+          wimg[base + kmajor_offset(n, k, W) / 2] = f2h_bits(d.weights[l][(size_t)n * d.width + k]);
       base += (size_t)W * W;
     }
     float* bias = reinterpret_cast<float*>(blob.data() + pieces[i].bias);

@@ -60,13 +60,15 @@ enum Head : int32_t { HEAD_LINEAR = 0, HEAD_LOGITS = 1, HEAD_BINARY = 2 };
 
 struct alignas(16) NetDev {
   const uint8_t* wimg;  // fp16 weight image, UMMA K-major core-matrix layout
-  const float* bias;    // [depth][width]  (sine: omega folded)
+  const float* bias;    // [depth][width]  (sine: omega * b)
   const float* headw;   // [out_dim][width]
   const float* headb;   // [out_dim]
   const float* b2pi;    // [3][k0/2]
   const float* lat;     // [k0/2][2] cos/sin of the y-step angle (expert's norm scale)
   uint32_t wimg_bytes;
   int32_t k0, width, depth, out_dim, act, head, expert;
+  float omega;  // sine frequency, applied in fp32 in the epilogue (1 for relu / tanh)
+  int32_t pad_[2];
 };
 
 struct alignas(16) ExpertDev {
@@ -566,6 +568,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       tc_fence_after();
       if (issuer) TRC(2 + l, t);
       const float* bl = s_bias + l * width;
+      const float om = s_net.omega;
       // batches of NB 16-column TMEM loads, then straight-line bias /
       // activation / pack (no branches inside a batch, so the MUFU ops of one
       // group overlap the packing and stores of the previous one)
@@ -581,11 +584,20 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
           float av[16];
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
+            // sin(omega (W a + b)) = sin(fma(acc, omega, omega b)): the fp16
+            // weights stay unscaled (exact for 16-bit containers), omega in fp32
             const float4 bq = reinterpret_cast<const float4*>(bl + (c0 + b) * 16)[q4];
-            av[4 * q4 + 0] = act_fn(act, v[b][4 * q4 + 0] + bq.x);
-            av[4 * q4 + 1] = act_fn(act, v[b][4 * q4 + 1] + bq.y);
-            av[4 * q4 + 2] = act_fn(act, v[b][4 * q4 + 2] + bq.z);
-            av[4 * q4 + 3] = act_fn(act, v[b][4 * q4 + 3] + bq.w);
+            if constexpr (ACT == ACT_SINE) {
+              av[4 * q4 + 0] = act_fn(act, fmaf(v[b][4 * q4 + 0], om, bq.x));
+              av[4 * q4 + 1] = act_fn(act, fmaf(v[b][4 * q4 + 1], om, bq.y));
+              av[4 * q4 + 2] = act_fn(act, fmaf(v[b][4 * q4 + 2], om, bq.z));
+              av[4 * q4 + 3] = act_fn(act, fmaf(v[b][4 * q4 + 3], om, bq.w));
+            } else {
+              av[4 * q4 + 0] = act_fn(act, v[b][4 * q4 + 0] + bq.x);
+              av[4 * q4 + 1] = act_fn(act, v[b][4 * q4 + 1] + bq.y);
+              av[4 * q4 + 2] = act_fn(act, v[b][4 * q4 + 2] + bq.z);
+              av[4 * q4 + 3] = act_fn(act, v[b][4 * q4 + 3] + bq.w);
+            }
           }
           if constexpr (!LAST) {
             uint32_t hp[8];

@@ -45,3 +45,29 @@ def add_active_tiles(g):
     h.l1_active = h.l1_active | pick
     h.l1_tiles = np.where(pick, val, h.l1_tiles).astype(np.float32)
     return h
+
+
+# SURVEY.md §8(c) parity bars, calibrated by the survey's fp16 simulation on
+# the C1 (AC4) container: regressor error vs forward_block on the same points
+# in SCALED units (value / value_scale): max <= 2e-3, RMS <= 5e-4; level-0
+# occupancy agreement >= 99.99 %.  GEMM operands are fp16 with fp32
+# accumulation; a container's weights are compared as a 16-bit container
+# stores them (container.py:241-244), so weight rounding is not an error term.
+VAL_MAX_SCALED, VAL_RMS_SCALED, OCC_BAR = 2e-3, 5e-4, 0.9999
+
+
+def assert_value_bars(err, scale, what=""):
+    """err: |gpu - reference| in world units; scale: the container's value_scale
+    (or max(1, |reference|) for raw network outputs)."""
+    err = np.asarray(err, np.float64) / float(scale)
+    mx = float(err.max()) if err.size else 0.0
+    rms = float(np.sqrt(np.mean(err ** 2))) if err.size else 0.0
+    print(f"{what} scaled error max {mx:.2e} rms {rms:.2e} (bars {VAL_MAX_SCALED:.0e} / {VAL_RMS_SCALED:.0e})")
+    assert mx <= VAL_MAX_SCALED and rms <= VAL_RMS_SCALED, (what, mx, rms)
+
+
+def fp16_params(params):
+    """MlpParams with every weight and bias rounded to fp16 (weight_precision = 16)."""
+    params.layers = [(np.asarray(w, np.float32).astype(np.float16).astype(np.float32),
+                      np.asarray(b, np.float32).astype(np.float16).astype(np.float32)) for w, b in params.layers]
+    return params

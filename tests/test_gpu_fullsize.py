@@ -26,12 +26,7 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
-VAL_MAX, VAL_RMS = 2e-2, 2e-3
-# on the self-trained C2 nets the fp16-operand error of the regressor is larger
-# than on the reference-trained AC4 container (C1: RMS 1.3e-3 world units,
-# test_gpu_decode.py): measured 2.4e-3 world = 7.9e-4 in scaled units
-# (value_scale 3), max 8.5e-3; the C2 sample bar is RMS 3e-3, max 2e-2
-VAL_RMS_C2 = 3e-3
+from helpers import OCC_BAR, assert_value_bars, fp16_params  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -150,6 +145,9 @@ def test_c2_oracle_sample_parity(c2):
     cen0 = (lo[:, None, :] + (LEAF_LOCAL + 0.5)[None]).reshape(-1, 3)
     p0, cov0 = O.blended(c.layout, c.experts, cen0, "l0")
     act_ref = cov0 & (p0[:, 0] > 0.5)
+    # the stated precision model (fp16 GEMM operands, fp32 accumulation) of the same computation
+    p0h, cov0h = O.blended(c.layout, c.experts, cen0, "l0", operands="f16")
+    act_f16 = cov0h & (p0h[:, 0] > 0.5)
     gl = d.leaf_origins[:d.leaf_count].cpu().numpy()
     index = {tuple(o): i for i, o in enumerate(gl)}
     li = np.array([index[tuple(o)] for o in lo])
@@ -163,9 +161,13 @@ def test_c2_oracle_sample_parity(c2):
     near0 = np.abs(p0[fl0, 0] - 0.5)
     print(f"l1 class agreement {agree1:.6f}; l0 occupancy agreement {agree0:.6f} on {unpatched.sum()} voxels, "
           f"max |p_ref - 0.5| at a flip {near0.max() if fl0.size else 0.0:.2e}")
-    # occupancy: >= 99.95 % on this 48 K-voxel sample (99.99 % over the C1 decode, test_gpu_decode.py),
-    # and every flip is a near tie of the fp32 reference's probability
-    assert agree0 >= 0.9995 and (near0 < 2e-2).all(), (agree0, near0)
+    agree16 = (ga[unpatched] == act_f16[unpatched]).mean()
+    print(f"l0 occupancy agreement with the fp16-operand model of the reference computation {agree16:.6f}")
+    # occupancy >= 99.99 % against the fp16-operand model; against the fp32
+    # reference (measured 99.98 % on this self-trained container, 99.9987 % on
+    # the reference-trained C1 container) every flip is a near tie
+    assert agree16 >= OCC_BAR, agree16
+    assert agree0 >= 0.9995 and (near0 < 1e-2).all(), (agree0, near0)
     both = ga & act_ref & unpatched
     vref, _ = O.blended(c.layout, c.experts, cen0[both], "voxel")
     scale = float(c.grid_meta.value_scale)
@@ -174,7 +176,7 @@ def test_c2_oracle_sample_parity(c2):
     err = np.abs(gv - vref)
     print(f"values: max {err.max():.2e} rms {np.sqrt(np.mean(err ** 2)):.2e} on {both.sum()} voxels")
     m.close()
-    assert err.max() < VAL_MAX and np.sqrt(np.mean(err ** 2)) < VAL_RMS_C2
+    assert_value_bars(err, scale, "C2 sample voxel values")
 
 
 def test_c5_shaped_query_sample_parity():
@@ -202,7 +204,7 @@ def test_c5_shaped_query_sample_parity():
         p = init_mlp(512, [256] * 3, 1, Activation("sine", 3.0), "linear", 100 + sub.id)
         w, b = p.layers[-1]
         p.layers[-1] = (rng.normal(0, 0.05, size=w.shape).astype(np.float32), b)
-        e.voxel_regressor = NetRecord(p, FourierFeatures(256, 10.0, 200 + sub.id))
+        e.voxel_regressor = NetRecord(fp16_params(p), FourierFeatures(256, 10.0, 200 + sub.id))
         experts.append(e)
     experts.sort(key=lambda e: e.id)
     ev = NetEvaluator(experts, layout.size, layout.halo, float(g.background), dev)
@@ -223,7 +225,12 @@ def test_c5_shaped_query_sample_parity():
     err = np.abs(val[reg] - ref)
     print(f"C5-shaped sample: {coords.shape[0]} queries, {nr} regressed, max {err.max():.2e} "
           f"rms {np.sqrt(np.mean(err ** 2)):.2e}")
-    assert err.max() < 2e-2 * 3.0 and np.sqrt(np.mean(err ** 2)) < 3e-3 * 3.0
+    bh, covh = O.blended(layout, experts, coords[reg].astype(np.float64) + 0.5, "voxel", operands="f16")
+    ref16 = np.where(covh, np.clip(bh[:, 0], -1.0, 1.0) * 3.0, g.background).astype(np.float32)
+    # the survey's bars against the fp16-operand model of the reference computation;
+    # random (untrained) 3x256 nets sit just outside them against fp32 (2.3e-3 / 5.7e-4)
+    assert_value_bars(np.abs(val[reg] - ref16), 3.0, "C5-shaped regressed rows vs fp16-operand model")
+    assert (err / 3.0).max() < 4e-3 and np.sqrt(np.mean((err / 3.0) ** 2)) < 1e-3
     ev.close()
 
 
@@ -252,7 +259,7 @@ def test_c3_shaped_decode_sample_parity():
         p = init_mlp(2 * m, [width] * 3, out, Activation("sine", 3.0), head, seed)
         w, b = p.layers[-1]
         p.layers[-1] = (rng.normal(0, 0.05, size=w.shape).astype(np.float32), b)
-        return NetRecord(p, FourierFeatures(m, 10.0, seed + 1))
+        return NetRecord(fp16_params(p), FourierFeatures(m, 10.0, seed + 1))
     experts = []
     for sub in layout.subdomains:
         no, ns = expert_norm(sub, g)
@@ -295,5 +302,5 @@ def test_c3_shaped_decode_sample_parity():
     assert vcov.all()
     err = np.abs(vals[gi] - vref[:, 0])
     print(f"values on {ci.size} active voxels: max {err.max():.2e} rms {np.sqrt(np.mean(err ** 2)):.2e}")
-    assert err.max() < 2e-2 * max(1.0, np.abs(vref).max()) and np.sqrt(np.mean(err ** 2)) < 3e-3
+    assert_value_bars(err, max(1.0, float(np.abs(vref).max())), "C3-shaped voxel values")
     ev.close()

@@ -1,15 +1,16 @@
 """GPU parity tests for the C-ABI kernels (need a B200 + built library).
 
-Tolerances (fp16 tensor-core operands, fp32 accumulate, fp32 head):
-forward outputs within 2e-2 absolute and 3e-3 RMS of the oracle for
-O(1)-scale random nets; classifier decisions within the 99.99 % bar;
-lookups bit-exact.
+Tolerances (fp16 tensor-core operands, fp32 accumulate, fp32 head;
+SURVEY.md §8(c), tests/helpers.py): forward outputs within 2e-3 max and
+5e-4 RMS of the oracle (relative to max(1, |output|) for random nets, whose
+weights both sides read as a 16-bit container stores them); classifier
+decisions within the 99.99 % bar; lookups bit-exact.
 """
 import numpy as np
 import pytest
 
 import oracle as O
-from helpers import net_from_fixture
+from helpers import OCC_BAR, assert_value_bars, fp16_params, net_from_fixture
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -107,17 +108,16 @@ def test_forward_matches_oracle(golden):
     for ci in range(int(z["ncases"][0])):
         q = f"n{ci}_"
         params, ff = net_from_fixture(z, q)
+        # the oracle is pinned to these fixtures (tests/test_oracle_golden.py); both
+        # sides see the weights as a 16-bit container stores them
+        fp16_params(params)
         tag = "l1" if params.head == "logits" else "voxel"
         ns = DeviceNetSet([_Expert(tag, NetRecord(params, ff))], 512)
         pts = torch.from_numpy(z[q + "pts"]).to(DEV)
         got = ns.forward(0, pts).cpu().numpy()
         ref = O.forward_block(params, ff, z[q + "pts"])
-        err = np.abs(got - ref)
-        rms = float(np.sqrt(np.mean(err ** 2)))
-        print(f"case {ci} ({params.activation.kind}) max {err.max():.2e} rms {rms:.2e} "
-              f"scale {np.abs(ref).max():.2f}")
-        assert err.max() < 2e-2 * max(1.0, np.abs(ref).max())
-        assert rms < 3e-3 * max(1.0, np.abs(ref).max())
+        assert_value_bars(np.abs(got - ref), max(1.0, float(np.abs(ref).max())),
+                          f"case {ci} ({params.activation.kind})")
         ns.close()
 
 
@@ -146,13 +146,17 @@ def test_blended_matches_reference(golden, name):
         np.testing.assert_array_equal(cov, z[ck])
         err = np.abs(out - z[pk])
         print(name, tag, "max err", err.max())
-        assert err.max() < 2e-2
+        # against the reference's own outputs (fp32 weights rounded to fp16 on the device)
+        if tag == "voxel":
+            assert_value_bars(err, 1.0, f"{name} blended voxel")
+        else:
+            assert err.max() < 2e-3
         if tag == "l1":
             agree = (out.argmax(1) == z[pk].argmax(1))[cov].mean()
-            assert agree >= 0.999
+            assert agree >= OCC_BAR
         if tag == "l0":
             agree = ((out > 0.5) == (z[pk] > 0.5))[cov].mean()
-            assert agree >= 0.999
+            assert agree >= OCC_BAR
     ns.close()
 
 
@@ -169,15 +173,12 @@ def test_wide_nets_stream_weights(width, m, depth):
     # the init zeroes the output layer; give it weights so the check is not trivial
     w, b = params.layers[-1]
     params.layers[-1] = (rng.normal(0, 0.2, size=w.shape).astype(np.float32), b)
+    fp16_params(params)
     ns = DeviceNetSet([_Expert("voxel", NetRecord(params, ff))], 512)
     pts_np = rng.uniform(0.0, 1.0, size=(20000, 3)).astype(np.float32)
     got = ns.forward(0, torch.from_numpy(pts_np).to(DEV)).cpu().numpy()
     ref = O.forward_block(params, ff, pts_np)
-    err = np.abs(got - ref)
-    rms = float(np.sqrt(np.mean(err ** 2)))
-    scale = max(1.0, float(np.abs(ref).max()))
-    print(f"W={width} m={m} depth={depth}: max {err.max():.2e} rms {rms:.2e} scale {scale:.2f}")
-    assert err.max() < 2e-2 * scale and rms < 3e-3 * scale
+    assert_value_bars(np.abs(got - ref), max(1.0, float(np.abs(ref).max())), f"W={width} m={m} depth={depth}")
     ns.close()
 
 
@@ -201,6 +202,7 @@ def test_forward_ragged_shapes(hidden, m, kind, head, n):
     params = init_mlp(2 * m, hidden, od, Activation(kind, 3.0 if kind == "sine" else 1.0), head, 7)
     w, b = params.layers[-1]
     params.layers[-1] = (rng.normal(0, 0.2, size=w.shape).astype(np.float32), b)
+    fp16_params(params)
     tag = "l1" if head == "logits" else "voxel"
     ns = DeviceNetSet([_Expert(tag, NetRecord(params, ff))], 512)
     pts_np = rng.uniform(0.0, 1.0, size=(n, 3)).astype(np.float32)
@@ -208,10 +210,7 @@ def test_forward_ragged_shapes(hidden, m, kind, head, n):
     assert got.shape == (n, od)
     if n:
         ref = O.forward_block(params, ff, pts_np)
-        err = np.abs(got - ref)
-        scale = max(1.0, float(np.abs(ref).max()))
-        print(f"{hidden} m={m} {kind}/{head} n={n}: max {err.max():.2e} scale {scale:.2f}")
-        assert err.max() < 2e-2 * scale and float(np.sqrt(np.mean(err ** 2))) < 3e-3 * scale
+        assert_value_bars(np.abs(got - ref), max(1.0, float(np.abs(ref).max())), f"{hidden} m={m} {kind}/{head} n={n}")
     ns.close()
 
 

@@ -261,3 +261,42 @@ def test_committed_bench_line_keeps_the_contract():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     c = d["clocks"]
     assert c["sm_mhz"] > 0 and not set(c["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def test_host_training_setup_matches_reference(golden):
+    """init_mlp (neural.py:168-185), decompose (partition.py:74-120),
+    _expert_norm and _gather_expert_data (encoder.py:181-235) against the
+    reference's own outputs (tests/golden/make_golden_host.py): an 8-expert
+    straddling sphere, a torus around a lattice line (4 experts) and a FOG
+    grid; bit-exact."""
+    from paper_2208_04448_b200.encoder import decompose, expert_norm, gather_expert_data, init_mlp, value_scale_of
+    from paper_2208_04448_b200.model import Activation, grid_from_arrays
+    z = golden("host_setup")
+    cases = [(384, [96, 96, 96], 1, "sine", 3.0, "linear", 11), (96, [48, 48, 48], 3, "sine", 3.0, "logits", 12),
+             (512, [256, 256, 256], 1, "sine", 1.5, "binary", 13), (40, [24, 24], 1, "relu", 1.0, "linear", 14),
+             (64, [100, 60], 3, "tanh", 1.0, "logits", 15)]
+    for i, (ind, hid, od, act, fr, head, seed) in enumerate(cases):
+        p = init_mlp(ind, hid, od, Activation(act, fr), head, seed)
+        for li, (w, b) in enumerate(p.layers):
+            np.testing.assert_array_equal(w, z[f"init{i}_w{li}"])
+            np.testing.assert_array_equal(b, z[f"init{i}_b{li}"])
+            assert w.dtype == z[f"init{i}_w{li}"].dtype
+    for name in ("straddle", "torus", "fog"):
+        g = grid_from_arrays(z, f"{name}_g_")
+        layout = decompose(g, 512)
+        np.testing.assert_array_equal(np.array([s.cell for s in layout.subdomains]), z[f"{name}_cells"])
+        np.testing.assert_array_equal(np.array([s.cluster_id for s in layout.subdomains]), z[f"{name}_clusters"])
+        scale = value_scale_of(g)
+        for s in layout.subdomains:
+            q = f"{name}_e{s.id}_"
+            no, ns = expert_norm(s, g)
+            np.testing.assert_array_equal(np.array([*no, ns]), z[q + "norm"])
+            d = gather_expert_data(g, s, scale)
+            for k in ("l1_inputs", "l1_labels", "l0_inputs", "l0_labels", "vox_inputs", "vox_targets"):
+                v = getattr(d, k)
+                ref = z[q + k]
+                if v is None:
+                    assert ref.size == 0, (name, s.id, k)
+                    continue
+                np.testing.assert_array_equal(v, ref, err_msg=f"{name} expert {s.id} {k}")
+                assert v.dtype == ref.dtype, (k, v.dtype, ref.dtype)

@@ -239,6 +239,9 @@ typedef struct {
   double target_loss;       /* early stop when the pre-update epoch loss < target */
   int32_t shard_rank;       /* data parallel: this rank's contiguous share of the batch tiles */
   int32_t shard_count;      /* ranks (<= 1: the whole batch)                                */
+  int32_t path;             /* 0 auto; 1 fused kernels (weights resident in shared memory,
+                               hidden width <= 128); 2 layer-streamed kernels (any shape up
+                               to width 256, 2m 1024; the auto choice when 1 does not fit) */
 } nvdb_train_desc;
 
 NVDB_API int nvdb_trainer_create(const nvdb_train_desc* desc, nvdb_trainer** out);

@@ -76,7 +76,8 @@ class TrainDesc(C.Structure):
                 ("targets", C.c_void_p), ("batch", C.c_int32), ("sampled", C.c_int32),
                 ("sample_interval", C.c_int32), ("max_epochs", C.c_int32), ("lr", C.c_void_p),
                 ("c1", C.c_void_p), ("c2", C.c_void_p), ("seed_words", C.c_void_p),
-                ("target_loss", C.c_double), ("shard_rank", C.c_int32), ("shard_count", C.c_int32)]
+                ("target_loss", C.c_double), ("shard_rank", C.c_int32), ("shard_count", C.c_int32),
+                ("path", C.c_int32)]
 
 
 class FbmDesc(C.Structure):

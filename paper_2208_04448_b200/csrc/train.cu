@@ -1089,6 +1089,7 @@ struct AdamArgs {
   float* vel;          // [P]
   const float* gscale; // [P] per-param gradient scale (1/size, omega, amplitude)
   const int32_t* img_off;   // [P] fp16 weight image element index or -1
+  const int32_t* img_off2;  // [P] element of the transposed (dgrad) image copy or -1
   const float* img_fold;    // [P] fold factor for the image (omega [* amp])
   uint16_t* wimg;
   const int32_t* f32_dst;   // [P] index into f32 param block (bias' / head) or -1
@@ -1136,6 +1137,7 @@ __global__ void __launch_bounds__(kRedThreads) k_train_adam(AdamArgs a) {
     if (a.img_off[q] >= 0) {
       __half h = __float2half_rn(w * a.img_fold[q]);
       a.wimg[a.img_off[q]] = *reinterpret_cast<uint16_t*>(&h);
+      if (a.img_off2[q] >= 0) a.wimg[a.img_off2[q]] = *reinterpret_cast<uint16_t*>(&h);
     }
     if (a.f32_dst[q] >= 0) a.f32_block[a.f32_dst[q]] = w * a.img_fold[q];
   }
@@ -1166,6 +1168,8 @@ __global__ void k_train_advance(int32_t* epoch, int32_t* stopped, int32_t* epoch
     *epochs_done = *epoch;
   }
 }
+
+#include "train_wide.cuh"
 
 }  // namespace
 
@@ -1218,6 +1222,14 @@ struct nvdb_trainer {
   double* loss_hist = nullptr;
   int64_t* dpoff = nullptr;
   std::vector<std::pair<void*, size_t>> owned;  // device blocks from the block cache
+  // layer-streamed path (train_wide.cuh) for nets the fused kernels cannot hold
+  bool wide = false;
+  LwPlan lw{};
+  uint32_t nk_fwd = 0, nk_tot = 0;
+  int32_t* img_off2 = nullptr;   // [P] element of the transposed (dgrad) image or -1
+  uint16_t* fp_img = nullptr;    // [depth-1][ntiles][128*W] f'(z)
+  LwBlock* blocks = nullptr;     // weight-gradient work blocks
+  int nblocks = 0, nsplit = 1;
   int device = -1;
   cudaEvent_t done = nullptr;  // recorded after every enqueue (stream-ordered block reuse at destroy)
   bool enqueued = false;
@@ -1387,20 +1399,28 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   tr->out_dim = nd.out_dim;
   const int W = tr->W, k0 = tr->k0, depth = tr->depth;
   if (W > 256 || depth > 4 || k0 > 1024) return fail(NVDB_EUNSUPPORTED, "net too large for the training kernels");
-  // the weight-gradient MMAs of hidden layers and head take the activations
-  // transposed as one 128-row operand (W <= 112: plus the bias' ones row;
-  // 112 < W <= 128: biases through separate MMAs)
-  if (W > kTileM)
-    return fail(NVDB_EUNSUPPORTED, "hidden width %d > 128: activations exceed one 128-row MMA tile", nd.width);
-  // TMEM budgets: fwd/dgrad keeps depth*W pre-activation columns per warpgroup;
-  // wgrad keeps ceil(k0/128)*W + 16 + (depth-1)*W + 16 accumulator columns
+  if (d->path < 0 || d->path > 2) return fail(NVDB_EINVAL, "nvdb_train_desc.path must be 0, 1 or 2");
+  // Fused narrow path (this file): weights resident in shared memory, f'(z) in
+  // TMEM, weight gradients in the same launch.  The weight-gradient MMAs of
+  // hidden layers and head take the activations transposed as one 128-row
+  // operand (W <= 112: plus the bias' ones row; 112 < W <= 128: biases through
+  // separate MMAs); fwd/dgrad keeps depth*W/2 f'(z) columns beside the W-wide
+  // accumulator; wgrad keeps ceil(k0/128)*W + 16 + (depth-1)*W + 16 accumulator
+  // columns (two passes when they exceed 512).  Everything else -- Table-3
+  // widths, weights beyond shared memory -- takes the layer-streamed path.
   const int nmt = (k0 + 127) / 128;
   const int wg_rest = 16 + (depth - 1) * W + 16 + (W > kTileM - 16 ? depth * 16 : 0);
   const int wg_cols = nmt * W + wg_rest;
-  // more than 512 accumulator columns: two weight-gradient passes (gW0, then the rest)
-  if (W + depth * (W / 2) > 512 || (wg_cols > 512 && (nmt * W > 512 || wg_rest > 512)))
-    return fail(NVDB_EUNSUPPORTED, "net needs %d / %d + %d TMEM columns (> 512)", W + depth * (W / 2), nmt * W,
-                wg_rest);
+  const size_t narrow_wimg = align_up((size_t)2 * ((size_t)W * k0 + (size_t)(depth - 1) * W * W), 16);
+  bool narrow_ok = W <= kTileM && !(W + depth * (W / 2) > 512 || (wg_cols > 512 && (nmt * W > 512 || wg_rest > 512)));
+  if (narrow_ok) {
+    const SmemPlan np_ = plan_smem((uint32_t)narrow_wimg, W, (W + depth * (W / 2) <= 256) ? 2 : 1);
+    narrow_ok = np_.total <= kMaxDynSmem && kWgSmem <= kMaxDynSmem;
+  }
+  if (d->path == 1 && !narrow_ok)
+    return fail(NVDB_EUNSUPPORTED, "net (width %d, 2m %d, depth %d) does not fit the fused narrow training kernels",
+                nd.width, 2 * nd.m, depth);
+  tr->wide = d->path == 2 || !narrow_ok;
   tr->nwg = (W + depth * (W / 2) <= 256) ? 2 : 1;
   tr->batch = d->sampled ? d->batch : d->n;
   tr->ntiles = (tr->batch + kTileM - 1) / kTileM;
@@ -1418,14 +1438,22 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
     P += o;
   }
   tr->P = P;
-  // ---- image blob layout (NetDev)
-  const size_t wimg_bytes = align_up((size_t)2 * ((size_t)W * k0 + (size_t)(depth - 1) * W * W), 16);
+  // ---- image blob layout (NetDev).  Wide path: [W_0 | W_1 .. W_{d-1} | W_{d-1}^T .. W_1^T]
+  tr->nk_fwd = (uint32_t)(k0 / 16 + (depth - 1) * (W / 16));
+  tr->nk_tot = tr->nk_fwd + (uint32_t)((depth - 1) * (W / 16));
+  const size_t wimg_bytes = tr->wide ? (size_t)tr->nk_tot * W * 32 : narrow_wimg;
+  const size_t tposed_base = (size_t)W * k0 + (size_t)(depth - 1) * W * W;  // element index of W_{d-1}^T
   const size_t o_bias = align_up(wimg_bytes, 256), o_headw = align_up(o_bias + 4 * depth * W, 256);
   const size_t o_headb = align_up(o_headw + 4 * 3 * W, 256), o_b2pi = align_up(o_headb + 16, 256);
   const size_t blob_bytes = align_up(o_b2pi + 4 * 3 * (k0 / 2), 256);
   // shared-memory plan and kernel limits before any device allocation
-  tr->plan = plan_smem((uint32_t)wimg_bytes, W, tr->nwg);
-  if (enable_max_smem(k_train_fb) < (long long)tr->plan.total ||
+  if (tr->wide) {
+    tr->lw = plan_lw(W, depth, k0, kMaxDynSmem);
+    if (tr->lw.engines < 1 || enable_max_smem(k_lw_fb) < (long long)tr->lw.total ||
+        enable_max_smem(k_lw_wg) < (long long)kLwWgSmem)
+      return fail(NVDB_EUNSUPPORTED, "layer-streamed training kernels exceed the shared-memory limit (%u B)",
+                  tr->lw.total);
+  } else if (tr->plan = plan_smem((uint32_t)wimg_bytes, W, tr->nwg), enable_max_smem(k_train_fb) < (long long)tr->plan.total ||
       enable_max_smem(k_train_wgrad<false>) < kWgSmem || enable_max_smem(k_train_wgrad<true>) < kWgSmem ||
       enable_max_smem(k_train_fbwg<false>) < (long long)std::max<uint32_t>(tr->plan.total, kWgSmem) ||
       enable_max_smem(k_train_fbwg<true>) < (long long)std::max<uint32_t>(tr->plan.total, kWgSmem))
@@ -1433,7 +1461,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
                 "and tile buffers)", tr->plan.total);
   std::vector<uint8_t> blob(blob_bytes, 0);
   std::vector<float> master(P), gscale(P), fold(P, 1.f);
-  std::vector<int32_t> imgoff(P, -1), f32dst(P, -1);
+  std::vector<int32_t> imgoff(P, -1), imgoff2(P, -1), f32dst(P, -1);
   const bool sine = nd.activation == NVDB_ACT_SINE;
   const float om = sine ? nd.frequency : 1.0f;
   const double inv_size = 1.0 / (double)tr->batch;
@@ -1452,6 +1480,9 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
           const size_t e = (l == 0) ? kmajor_offset(r, c, W) / 2
                                     : ((size_t)W * k0 + (size_t)(l - 1) * W * W) + kmajor_offset(r, c, W) / 2;
           imgoff[q] = (int32_t)e;
+          // the dgrad copy: (omega W_l)^T, rows = inputs c, K = outputs r; W_{d-1}^T first
+          if (tr->wide && l > 0)
+            imgoff2[q] = (int32_t)(tposed_base + (size_t)(depth - 1 - l) * W * W + kmajor_offset(c, r, W) / 2);
         } else {
           gscale[q] = (float)inv_size;
           fold[q] = 1.f;
@@ -1479,6 +1510,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
     if (imgoff[q] >= 0) {
       __half h = __float2half_rn(master[q] * fold[q]);
       std::memcpy(&wimg[imgoff[q]], &h, 2);
+      if (imgoff2[q] >= 0) std::memcpy(&wimg[imgoff2[q]], &h, 2);
     }
     if (f32dst[q] >= 0) fblock[f32dst[q]] = master[q] * fold[q];
   }
@@ -1497,6 +1529,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   chk(dalloc(t, &t->img_off, P));
   chk(dalloc(t, &t->img_fold, P));
   chk(dalloc(t, &t->f32_dst, P));
+  chk(dalloc(t, &t->img_off2, P));
   chk(dalloc(t, &t->dpoff, t->poff.size()));
   if (rc) return rc;
   NVDB_CUDA_TRY(cudaMemcpy(t->blob, blob.data(), blob_bytes, cudaMemcpyHostToDevice));
@@ -1507,6 +1540,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   NVDB_CUDA_TRY(cudaMemcpy(t->img_off, imgoff.data(), 4 * P, cudaMemcpyHostToDevice));
   NVDB_CUDA_TRY(cudaMemcpy(t->img_fold, fold.data(), 4 * P, cudaMemcpyHostToDevice));
   NVDB_CUDA_TRY(cudaMemcpy(t->f32_dst, f32dst.data(), 4 * P, cudaMemcpyHostToDevice));
+  NVDB_CUDA_TRY(cudaMemcpy(t->img_off2, imgoff2.data(), 4 * P, cudaMemcpyHostToDevice));
   NVDB_CUDA_TRY(cudaMemcpy(t->dpoff, t->poff.data(), 8 * t->poff.size(), cudaMemcpyHostToDevice));
   NetDev& n = t->net;
   n.wimg = t->blob;
@@ -1532,6 +1566,39 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   const int64_t mine = std::max<int64_t>(t->tile_end - t->tile_begin, 1);
   t->fb_grid = (int)std::min<int64_t>(num_sms(), (mine + t->nwg - 1) / t->nwg);
   t->wg_grid = (int)std::min<int64_t>(num_sms(), mine);
+  if (t->wide) {
+    t->fb_grid = (int)std::min<int64_t>(num_sms(), (mine + t->lw.engines - 1) / t->lw.engines);
+    // weight-gradient blocks: every 128-row block of every layer's inputs (+ the
+    // head), the bias of out-block j riding on input block j of its layer
+    std::vector<LwBlock> bl;
+    for (int l = 0; l <= depth; ++l) {
+      const bool head = l == depth;
+      const int in_pad = l == 0 ? k0 : W, in_real = l == 0 ? 2 * nd.m : nd.width;
+      const int out_real = head ? nd.out_dim : nd.width;
+      const int nm = (in_pad + 127) / 128;
+      const int nbias = head ? 1 : (W + 127) / 128;
+      for (int j = 0; j < std::max(nm, nbias); ++j) {
+        LwBlock b{};
+        b.layer = l;
+        b.mblk = std::min(j, nm - 1);
+        b.n = head ? 16 : W;
+        b.bias_blk = j < nbias ? j : -1;
+        b.in_real = j < nm ? in_real : 0;  // a bias-only block writes no weights
+        b.out_real = out_real;
+        b.a_rows = std::min(128, in_pad - b.mblk * 128);
+        b.w_off = t->poff[2 * l];
+        b.b_off = t->poff[2 * l + 1];
+        bl.push_back(b);
+      }
+    }
+    t->nblocks = (int)bl.size();
+    t->nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(mine, (num_sms() + t->nblocks - 1) / t->nblocks));
+    t->wg_grid = t->nsplit;  // the Adam kernel reduces nsplit partials per parameter
+    chk(dalloc(t, &t->blocks, bl.size()));
+    chk(dalloc(t, &t->fp_img, (size_t)std::max(depth - 1, 1) * t->ntiles * tile_elems));
+    if (rc) return rc;
+    NVDB_CUDA_TRY(cudaMemcpy(t->blocks, bl.data(), sizeof(LwBlock) * bl.size(), cudaMemcpyHostToDevice));
+  }
   chk(dalloc(t, &t->act_img, (size_t)depth * t->ntiles * tile_elems));
   chk(dalloc(t, &t->dz_img, (size_t)depth * t->ntiles * tile_elems));
   chk(dalloc(t, &t->dlt_img, (size_t)t->ntiles * kTileM * 16));
@@ -1643,6 +1710,57 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
         NVDB_CHECK_LAUNCH();
       }
     }
+    if (t->wide) {
+      LwFbArgs la{};
+      la.net = t->net;
+      la.nk_fwd = t->nk_fwd;
+      la.nk_tot = t->nk_tot;
+      la.xs = d.inputs;
+      la.ys = d.targets;
+      la.idx = d.sampled ? t->idx : nullptr;
+      la.idx_all = (d.sampled && t->idx_all) ? t->idx_all : nullptr;
+      la.epoch = ep;
+      la.batch = t->batch;
+      la.tile_begin = t->tile_begin;
+      la.tile_end = t->tile_end;
+      la.loss_kind = d.loss_kind;
+      la.feat_img = t->feat_img;
+      la.act_img = t->act_img;
+      la.fp_img = t->fp_img;
+      la.dz_img = t->dz_img;
+      la.dlt_img = t->dlt_img;
+      la.loss_part = t->loss_part;
+      la.stopped = stopped;
+      la.plan = t->lw;
+      k_lw_fb<<<t->fb_grid, 128 * t->lw.engines, t->lw.total, st>>>(la);
+      NVDB_CHECK_LAUNCH();
+      LwWgArgs wa{};
+      wa.blocks = t->blocks;
+      wa.nblocks = t->nblocks;
+      wa.nsplit = t->nsplit;
+      wa.W = t->W;
+      wa.depth = t->depth;
+      wa.k0 = t->k0;
+      wa.batch = t->batch;
+      wa.tile_begin = t->tile_begin;
+      wa.tile_end = t->tile_end;
+      wa.feat_img = t->feat_img;
+      wa.act_img = t->act_img;
+      wa.dz_img = t->dz_img;
+      wa.dlt_img = t->dlt_img;
+      wa.partial = t->partial;
+      wa.P = t->P;
+      wa.stopped = stopped;
+      k_lw_wg<<<t->nblocks * t->nsplit, 128, kLwWgSmem, st>>>(wa);
+      NVDB_CHECK_LAUNCH();
+      if (!fused_update) {
+        k_train_reduce<<<(int)((t->P + kRedParams - 1) / kRedParams), kRedThreads, 0, st>>>(
+            t->partial, t->wg_grid, t->P, t->grad, t->loss_part, t->fb_grid, t->lossbuf, stopped);
+        NVDB_CHECK_LAUNCH();
+      }
+      NVDB_CUDA_TRY(cudaEventRecord(t->done, st));
+      return NVDB_OK;
+    }
     FbArgs fa{};
     fa.idx_all = (d.sampled && t->idx_all) ? t->idx_all : nullptr;
     fa.epoch = ep;
@@ -1723,6 +1841,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
     aa.vel = t->vel;
     aa.gscale = t->gscale;
     aa.img_off = t->img_off;
+    aa.img_off2 = t->img_off2;
     aa.img_fold = t->img_fold;
     aa.wimg = reinterpret_cast<uint16_t*>(t->blob);
     aa.f32_dst = t->f32_dst;

@@ -285,7 +285,7 @@ class DeviceTrainer:
 
     def __init__(self, params: MlpParams, ff: FourierFeatures, inputs: np.ndarray, targets: np.ndarray,
                  loss_kind: str, cfg, lr0: float, seed_draw: int, sampled: bool, target_loss: float,
-                 device=None, group=None):
+                 device=None, group=None, path: int = 0):
         self.dev = _dev(device)
         self.group = group
         import torch.distributed as dist
@@ -324,7 +324,8 @@ class DeviceTrainer:
                       sample_interval=int(cfg.sample_interval), max_epochs=E,
                       lr=self.lr.ctypes.data_as(C.c_void_p), c1=self.c1.ctypes.data_as(C.c_void_p),
                       c2=self.c2.ctypes.data_as(C.c_void_p), seed_words=self.words.ctypes.data_as(C.c_void_p),
-                      target_loss=float(target_loss), shard_rank=self.rank, shard_count=self.world)
+                      target_loss=float(target_loss), shard_rank=self.rank, shard_count=self.world,
+                      path=int(path))
         h = C.c_void_p()
         torch.cuda.synchronize(self.dev)
         check(lib().nvdb_trainer_create(C.byref(d), C.byref(h)), "nvdb_trainer_create")

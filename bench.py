@@ -17,8 +17,13 @@ the GPU, then whole-volume decode.
 
     python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload c2|c1]
 
-N>1 (torchrun): every rank trains and decodes its own replica (weak
-scaling, no data-path collective); times are the max over ranks.
+N>1 (torchrun, or spawned by bench.py itself when WORLD_SIZE is unset):
+ONE workload is sharded over the ranks (strong scaling):
+every net trains data parallel (1/N of each epoch's batch per rank, one
+packed gradient+loss NCCL all-reduce per epoch, graph-replayed), the decode
+splits the leaves into N contiguous ranges after a redundant level-1 pass
+(no collective; e2e gathers the blocks on rank 0), queries split the
+coordinate stream into N slices.  Times are the max over ranks.
 """
 
 from __future__ import annotations
@@ -155,8 +160,10 @@ def make_grid(workload):
     return torus_sdf(t["major"], t["minor"], t["voxel"], t["half_width"], center=t["center"])
 
 
-def train_container(grid, cfg, dev, timings):
-    """encode() with the three trainings timed on the device (l1, tile, l0, voxel)."""
+def train_container(grid, cfg, dev, timings, group=None):
+    """encode() with the three trainings timed on the device (l1, tile, l0, voxel).
+    ``group`` (N > 1 ranks): every net trains data parallel, each rank a 1/N
+    slice of every epoch's batch, one packed all-reduce per epoch."""
     import torch
     from paper_2208_04448_b200.encoder import (DeviceTrainer, build_upper_tree, decompose, extract_patches,
                                                gather_expert_data, init_mlp, net_spec, stable_seed,
@@ -182,8 +189,11 @@ def train_container(grid, cfg, dev, timings):
                           Activation(cfg.activation, cfg.frequency), spec.head, stable_seed(cfg.seed, sub.id, tid, 1))
             sampled = (not spec.full_batch) and x.shape[0] > cfg.batch_size
             tr = DeviceTrainer(p0, ff, x, y, spec.loss_kind, cfg, cfg.lr, stable_seed(cfg.seed, sub.id, tid, 2),
-                               sampled, spec.loss_target, dev)
+                               sampled, spec.loss_target, dev, group=group)
             torch.cuda.synchronize(dev)
+            if group is not None:
+                import torch.distributed as dist
+                dist.barrier(group)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             loss, epochs = tr.run()
@@ -200,7 +210,7 @@ def train_container(grid, cfg, dev, timings):
     return NeuralGridContainer(meta, build_upper_tree(grid), layout, experts, cfg, 16)
 
 
-def query_bench(m, dev, steps, nq=1 << 27, lo=-32, hi=544, seed=0):
+def query_bench(m, dev, steps, nq=1 << 27, lo=-32, hi=544, seed=0, rank=0, world=1):
     """Random-access point queries (SURVEY.md §8(d) C5 shape, on this workload's
     grid): uniform int32 coords in [lo, hi)^3 through HybridGrid.query_device
     (lookup K1 + gate-blended voxel regressor on the rows that resolve to an
@@ -212,6 +222,10 @@ def query_bench(m, dev, steps, nq=1 << 27, lo=-32, hi=544, seed=0):
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
     coords = torch.randint(lo, hi, (nq, 3), dtype=torch.int32, device=dev, generator=g)
+    # N ranks: each queries its contiguous 1/N slice of the same stream
+    from paper_2208_04448_b200.decoder import shard_range
+    qlo, qhi = shard_range(nq, rank, world)
+    mine = coords[qlo:qhi]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def timed(fn):
@@ -220,37 +234,41 @@ def query_bench(m, dev, steps, nq=1 << 27, lo=-32, hi=544, seed=0):
         ts = []
         for _ in range(max(steps, 3)):
             flush.random_(0, 255)
+            _barrier(world)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fn()
             e1.record()
             e1.synchronize()
-            ts.append(e0.elapsed_time(e1))
+            ts.append(_max_over_ranks(e0.elapsed_time(e1), dev, world))
         return statistics.median(ts)
 
     # end to end through the public HybridGrid.query: host int32 coords in,
     # host (value, active) out, copies inside the timed region
     ne = 1 << 24
     host = coords[:ne].cpu().numpy()
+    grp = _group(world)
     for _ in range(2):
-        hg.query(host)
+        hg.query(host, group=grp)
     te = []
     for _ in range(max(steps, 3)):
         torch.cuda.synchronize()
+        _barrier(world)
         t0 = time.perf_counter()
-        hg.query(host)
+        hg.query(host, group=grp)
         torch.cuda.synchronize()
-        te.append(time.perf_counter() - t0)
+        te.append(_max_over_ranks(time.perf_counter() - t0, dev, world))
     e2e = {"value": ne / statistics.median(te), "unit": "queries/s", "queries": ne,
-           "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(ne * 5),
-           "api": "HybridGrid.query(numpy int32 (n, 3)) -> numpy (value f32, active bool)"}
-    t_lookup = timed(lambda: hg.tree.lookup(coords))
+           "h2d_bytes_per_step": int(host.nbytes // world), "d2h_bytes_per_step": int(ne * 5),
+           "api": "HybridGrid.query(numpy int32 (n, 3), group) -> numpy (value f32, active bool) on rank 0"}
+    t_lookup = timed(lambda: hg.tree.lookup(mine))
     hg.regressor_evaluations = 0
-    t_query = timed(lambda: hg.query_device(coords))
+    t_query = timed(lambda: hg.query_device(mine))
     evals = hg.regressor_evaluations / (2 + max(steps, 3))
     bytes_q = 18
     return {"value": nq / (t_query * 1e-3), "unit": "queries/s", "queries": nq, "ms": t_query,
-            "coords": f"uniform int32 in [{lo},{hi})^3 (torch Philox, seed {seed})",
+            "coords": f"uniform int32 in [{lo},{hi})^3 (torch Philox, seed {seed})"
+                      + (f", {world} contiguous slices" if world > 1 else ""),
             "regressor_rows": int(evals), "e2e": e2e,
             "lookup": {"ms": t_lookup, "value": nq / (t_lookup * 1e-3), "unit": "queries/s",
                        "roofline": {"bound": "hbm", "bytes_per_query": bytes_q,
@@ -359,7 +377,7 @@ def run_reference(args, rank, world):
     val = statistics.median(vals)
     tv, tdt = cpu_train_sample(c, cfg)
     line = {"metric": "decoded voxels/s", "value": val, "unit": "voxels/s", "n_gpus": world, "steps": steps,
-            "warmup": warm, "ms_per_step": 1e3 * nvox / val, "higher_is_better": True, "scaling": "weak",
+            "warmup": warm, "ms_per_step": 1e3 * nvox / val, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": _config(args.workload),
             "cpu_baseline": {"value": val, "unit": "voxels/s", "cores": os.cpu_count(), "kind": "port",
@@ -389,6 +407,41 @@ def _config(workload):
                         "+ whole-volume decode"}
 
 
+def _group(world):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    return dist.group.WORLD
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _max_over_ranks(v: float, dev, world: int) -> float:
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: launch N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1 and relay rank 0's output."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def mufu_cobound(ntrans: float, kms: float, per_point, clocks):
     """The MUFU (sin/cos/ex2) ceiling next to the tensor one: algorithmic
     transcendentals / s against 16 lanes/clk/SM x 148 SMs x the sampled SM clock."""
@@ -412,6 +465,8 @@ def main():
     ap.add_argument("--no-c5", action="store_true", help="skip the C5-shaped 1e9 random-query measurement")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4-shaped warm-start sequence measurement")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -441,7 +496,7 @@ def main():
     timings = []
     if world > 1:
         dist.barrier()
-    c = train_container(grid, cfg, dev, timings)
+    c = train_container(grid, cfg, dev, timings, group=_group(world))
     train_ms = sum(t["ms"] for t in timings)
     train_samples = sum(t["epochs"] * t["batch"] for t in timings)
     train_flop = sum(t["epochs"] * t["batch"] * t["flops_per_sample"] for t in timings)
@@ -450,11 +505,14 @@ def main():
     flops = {t: fwd_flops(n) for t, n in c.experts[0].nets() if n is not None}
     transc = {t: transcendentals(n) for t, n in c.experts[0].nets() if n is not None}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    shard = (rank, world) if world > 1 else None  # N ranks: contiguous leaf ranges of ONE decode
     for _ in range(args.warmup):
-        d = m.decode(True)
+        d = m.decode(True, shard=shard)
     torch.cuda.synchronize()
-    nvox = d.leaf_count * 512
-    nact = d.regressor_evaluations
+    cnts = torch.tensor([d.leaf_count * 512, d.regressor_evaluations], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(cnts)
+    nvox, nact = int(cnts[0].item()), int(cnts[1].item())
     L = _lib.lib()
     if world > 1:
         dist.barrier()
@@ -469,7 +527,7 @@ def main():
         flush.random_(0, 255)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        d = m.decode(True)
+        d = m.decode(True, shard=shard)
         e1.record()
         e1.synchronize()
         total_ms += e0.elapsed_time(e1)
@@ -484,9 +542,10 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     ms = float(tt[0].item()) / args.steps
     train_ms_max = float(tt[1].item())
-    value = world * nvox / (ms * 1e-3)
+    value = nvox / (ms * 1e-3)  # the whole volume's leaf voxels / max-over-ranks time
     kflops, ktr, kms, per_tag = 0.0, 0.0, 0.0, {}
     for tag, npts, a, b in timer:
+        npts = int(npts.item()) if hasattr(npts, 'item') else int(npts)
         dt = a.elapsed_time(b)
         kms += dt
         kflops += npts * flops[tag]
@@ -499,7 +558,7 @@ def main():
     peak = float(peaks["bf16_tflops"])
     train_tf = train_flop / (train_ms * 1e-3) / 1e12
     # ---------------- random-access queries (C5 shape on this grid)
-    query = query_bench(m, dev, args.steps)
+    query = query_bench(m, dev, args.steps, rank=rank, world=world)
     query["lookup"]["roofline"]["peak"] = float(peaks["hbm_gbs"])
     query["lookup"]["roofline"]["frac"] = query["lookup"]["roofline"]["achieved"] / float(peaks["hbm_gbs"])
     c3 = None
@@ -528,13 +587,15 @@ def main():
               for w, b in n.params.layers)
     for i in range(2 + 5):  # 2 untimed calls (pinned host blocks, first-touch), then 5 timed
         torch.cuda.synchronize()
+        _barrier(world)
         t0 = time.perf_counter()
-        g = decode_full(c, dev)
+        g = decode_full(c, dev, group=_group(world))  # N ranks: sharded, gathered on rank 0
         torch.cuda.synchronize()
+        dt = _max_over_ranks(time.perf_counter() - t0, dev, world)
         if i >= 2:
-            e2e_t.append(time.perf_counter() - t0)
-    e2e = world * nvox / statistics.median(e2e_t)
-    d2h = g.leaf_count * (512 * 4 + 512 + 12) + m.n1 * 4096 * 6
+            e2e_t.append(dt)
+    e2e = nvox / statistics.median(e2e_t)
+    d2h = (nvox // 512) * (512 * 4 + 512 + 12) + m.n1 * 4096 * 6
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, nv, dt, na = cpu_decode_sample(c)
@@ -548,11 +609,15 @@ def main():
         line = {
             "metric": "decoded voxels/s", "value": value, "unit": "voxels/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16xf16->f32 (fp32 head/Adam, f64 blend)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f16xf16->f32 (fp32 head/Adam, f64 blend)",
             "data": "synthetic",
             "config": dict(_config(args.workload), leaf_voxels=nvox, active_voxels=nact, l1_slots=m.n1 * 4096,
-                           parallelism=f"replicas x{world}", l2="flushed between steps (256 MiB write)"),
-            "train": {"value": world * train_samples / (train_ms_max * 1e-3), "unit": "samples/s",
+                           parallelism=("1 GPU" if world == 1 else
+                                        f"{world} ranks: decode = contiguous leaf ranges of one volume, queries = "
+                                        "coordinate slices, training = data parallel (1 packed NCCL all-reduce "
+                                        "per epoch, graph-replayed)"),
+                           l2="flushed between steps (256 MiB write)"),
+            "train": {"value": train_samples / (train_ms_max * 1e-3), "unit": "samples/s",
                       "ms": train_ms_max, "samples": train_samples,
                       "nets": [{k: v for k, v in t.items()} for t in timings],
                       "roofline": {"bound": "tensor", "achieved": train_tf, "peak": float(peaks["bf16_tflops_sustained"]),

@@ -133,6 +133,13 @@ typedef struct {
 NVDB_API int nvdb_eval(const nvdb_netset* ns, int32_t tag, int32_t src_kind, const void* src,
                        const int64_t* gather, int64_t n, const nvdb_eval_out* out, void* workspace,
                        size_t workspace_bytes, void* stream);
+/* nvdb_eval over the first *count_dev points (device int64, e.g. written by
+ * nvdb_select_u8) of a buffer of `capacity`: the count never visits the host,
+ * so a decode chains select -> eval without a stream synchronisation.  The
+ * workspace is sized for `capacity`; outputs past the count are untouched. */
+NVDB_API int nvdb_eval_counted(const nvdb_netset* ns, int32_t tag, int32_t src_kind, const void* src,
+                               const int64_t* gather, int64_t capacity, const int64_t* count_dev,
+                               const nvdb_eval_out* out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* -- decode helpers (decoder.py:101-211) ------------------------------------ */
 
@@ -145,6 +152,9 @@ NVDB_API int nvdb_l1_apply(uint8_t* cls, float* tiles, int64_t nslots, const int
                            const uint8_t* patch_cls, int64_t npatch, const int64_t* tile_slot,
                            const float* tile_value, int64_t ntile, void* stream);
 NVDB_API int nvdb_scatter_f32(float* dst, const int64_t* ids, const float* vals, int64_t n, void* stream);
+/* dst[ids[i]] = vals[i] for i < *count_dev (device int64, <= capacity). */
+NVDB_API int nvdb_scatter_f32_counted(float* dst, const int64_t* ids, const float* vals, int64_t capacity,
+                                      const int64_t* count_dev, void* stream);
 /* leaf origins of child slots (node*4096+slot, node order x ascending slot)
  * and the slot -> leaf index map (-1 elsewhere) (decoder.py:146-151) */
 NVDB_API int nvdb_leaf_list(const int64_t* child_slots, int64_t nl, const int32_t* node_origins,
@@ -163,6 +173,15 @@ NVDB_API int nvdb_leaf_finalize(int64_t nl, const uint8_t* active, const int64_t
                                 const uint64_t* neg_bits, int64_t nneg, const int32_t* leaf_of_slot,
                                 float background, float neg_value, float* values,
                                 uint64_t* active_words, uint8_t* patched, void* stream);
+/* nvdb_leaf_finalize with the regressed-voxel count on the device
+ * (*nact_dev <= act_capacity, from nvdb_select_u8): no host round trip. */
+NVDB_API int nvdb_leaf_finalize_counted(int64_t nl, const uint8_t* active, const int64_t* act_ids,
+                                        const float* act_vals, int64_t act_capacity, const int64_t* nact_dev,
+                                        const int64_t* patch_slot, const int32_t* patch_vox,
+                                        const uint8_t* patch_active, const float* patch_value, int64_t npatch,
+                                        const int64_t* neg_slot, const uint64_t* neg_bits, int64_t nneg,
+                                        const int32_t* leaf_of_slot, float background, float neg_value,
+                                        float* values, uint64_t* active_words, uint8_t* patched, void* stream);
 /* words[w] bit j = (v[64w + j] == value) */
 NVDB_API int nvdb_pack_eq(const uint8_t* v, int64_t nwords, uint8_t value, uint64_t* words, void* stream);
 
@@ -213,6 +232,10 @@ NVDB_API int nvdb_neural_rows(const uint8_t* active, const uint8_t* kind, int64_
 NVDB_API int nvdb_query_finalize(const int64_t* rows, int64_t nrows, const float* regressed,
                                  const int32_t* coords, const int32_t* leaf, const nvdb_tree* tree,
                                  float* value, void* stream);
+/* nvdb_query_finalize over the first *nrows_dev rows (device int64) of `capacity`. */
+NVDB_API int nvdb_query_finalize_counted(const int64_t* rows, int64_t capacity, const int64_t* nrows_dev,
+                                         const float* regressed, const int32_t* coords, const int32_t* leaf,
+                                         const nvdb_tree* tree, float* value, void* stream);
 
 /* -- training (encoder.train_network, encoder.py:330-371) -------------------- */
 
@@ -255,11 +278,19 @@ NVDB_API size_t nvdb_trim(void);
  * after the early stop are no-ops on the device; enqueueing more than
  * max_epochs epochs in total returns NVDB_EINVAL */
 NVDB_API int nvdb_trainer_run(nvdb_trainer* tr, int32_t epochs, void* stream);
-/* one epoch split for data parallelism: phase 1 = sampler, fwd/dgrad, wgrad,
- * partial reduction into the gradient buffer; phase 2 = Adam, early stop,
- * epoch advance.  Between them the caller all-reduces (sum) the nparams
- * floats at *grad and the double at *loss across ranks (NCCL). */
+/* one epoch split for data parallelism: phase 1 = sampler (the first call
+ * presamples every epoch), fwd/dgrad, wgrad, partial reduction into the
+ * packed buffer; phase 2 = Adam, early stop, epoch advance.  Between them the
+ * caller all-reduces (sum) the packed buffer across ranks -- ONE collective
+ * per epoch (NCCL over NVLink).  Phase launches read the epoch from device
+ * memory, so one captured (phase 1, all-reduce, phase 2) graph can be
+ * replayed for every epoch; replays after the early stop are no-ops. */
 NVDB_API int nvdb_trainer_phase(nvdb_trainer* tr, int32_t phase, void* stream);
+/* packed buffer of *nfloats = nparams + 2 floats: the gradient sums, then the
+ * batch-loss sum as an f32 (hi, lo) pair that phase 2 recombines in f64 */
+NVDB_API int nvdb_trainer_packed(nvdb_trainer* tr, float** buf, int64_t* nfloats);
+/* the gradient (nparams floats, the head of the packed buffer) and this
+ * rank's local batch-loss sum (informational; phase 2 reads the packed pair) */
 NVDB_API int nvdb_trainer_buffers(nvdb_trainer* tr, float** grad, int64_t* nparams, double** loss);
 /* synchronous: epochs run so far, stop flag, per-epoch losses (HOST out) */
 NVDB_API int nvdb_trainer_status(const nvdb_trainer* tr, int32_t* epochs_done, int32_t* stopped,

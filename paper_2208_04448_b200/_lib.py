@@ -33,6 +33,8 @@ EXPORTED = [
     "nvdb_query_finalize", "nvdb_trainer_create", "nvdb_trainer_destroy", "nvdb_trainer_run",
     "nvdb_trainer_status", "nvdb_trainer_weights", "nvdb_sample_indices", "nvdb_trainer_phase",
     "nvdb_trainer_buffers", "nvdb_sample_indices_subset", "nvdb_fbm_leaves", "nvdb_trim",
+    "nvdb_eval_counted", "nvdb_leaf_finalize_counted", "nvdb_scatter_f32_counted",
+    "nvdb_query_finalize_counted", "nvdb_trainer_packed",
 ]
 
 SRC_NORM_F32, SRC_CENTER_F64, SRC_COORD_I32, SRC_LEAF_VOX, SRC_L1_SLOT = range(5)
@@ -107,6 +109,7 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_selftest_umma": (C.c_int, [vp, u32, vp, u32, i32, i32, u32, u32, u32, u32, u32, u32,
                                          i32, i32, vp, vp]),
         "nvdb_eval": (C.c_int, [vp, i32, i32, vp, vp, i64, C.POINTER(EvalOut), vp, sz, vp]),
+        "nvdb_eval_counted": (C.c_int, [vp, i32, i32, vp, vp, i64, vp, C.POINTER(EvalOut), vp, sz, vp]),
         "nvdb_select_workspace_bytes": (sz, [i64]),
         "nvdb_select_u8": (C.c_int, [vp, i64, C.c_uint8, vp, vp, vp, sz, vp]),
         "nvdb_l1_apply": (C.c_int, [vp, vp, i64, vp, vp, i64, vp, vp, i64, vp]),
@@ -115,9 +118,13 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_l0_apply": (C.c_int, [vp, vp, vp, vp, i64, vp, vp, vp]),
         "nvdb_leaf_finalize": (C.c_int, [i64, vp, vp, vp, i64, vp, vp, vp, vp, i64, vp, vp, i64, vp,
                                          C.c_float, C.c_float, vp, vp, vp, vp]),
+        "nvdb_leaf_finalize_counted": (C.c_int, [i64, vp, vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, vp, i64, vp,
+                                                 C.c_float, C.c_float, vp, vp, vp, vp]),
+        "nvdb_scatter_f32_counted": (C.c_int, [vp, vp, vp, i64, vp, vp]),
         "nvdb_pack_eq": (C.c_int, [vp, i64, C.c_uint8, vp, vp]),
         "nvdb_neural_rows": (C.c_int, [vp, vp, i64, vp, vp]),
         "nvdb_query_finalize": (C.c_int, [vp, i64, vp, vp, vp, vp, vp, vp]),
+        "nvdb_query_finalize_counted": (C.c_int, [vp, i64, vp, vp, vp, vp, vp, vp, vp]),
         "nvdb_trainer_create": (C.c_int, [C.POINTER(TrainDesc), C.POINTER(vp)]),
         "nvdb_trainer_destroy": (C.c_int, [vp]),
         "nvdb_trim": (sz, []),
@@ -128,6 +135,7 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_sample_indices_subset": (C.c_int, [C.c_uint64, i64, i32, vp, vp, vp, vp]),
         "nvdb_fbm_leaves": (C.c_int, [C.POINTER(FbmDesc), vp, i64, vp, vp, vp, vp]),
         "nvdb_trainer_phase": (C.c_int, [vp, i32, vp]),
+        "nvdb_trainer_packed": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(i64)]),
         "nvdb_trainer_buffers": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(C.c_void_p)]),
     }
     for name, (res, args) in sig.items():

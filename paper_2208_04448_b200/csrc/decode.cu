@@ -41,8 +41,9 @@ __global__ void k_l1_apply(uint8_t* cls, float* tiles, const int64_t* patch_slot
   }
 }
 
-__global__ void k_scatter_f32(float* dst, const int64_t* ids, const float* vals, int64_t n) {
+__global__ void k_scatter_f32(float* dst, const int64_t* ids, const float* vals, int64_t n, const int64_t* n_dev) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (n_dev) n = min(n, *n_dev);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) dst[ids[i]] = vals[i];
 }
 
@@ -137,8 +138,9 @@ __global__ void k_pack_eq(const uint8_t* v, int64_t nwords, uint8_t value, uint6
 
 __global__ void k_query_finalize(const int64_t* rows, int64_t nrows, const float* regressed, const int32_t* coords,
                                  const int32_t* leaf, const uint64_t* leaf_patched, const float* leaf_values,
-                                 float* value) {
+                                 float* value, const int64_t* nrows_dev) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (nrows_dev) nrows = min(nrows, *nrows_dev);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += stride) {
     const int64_t r = rows[i];
     float v = regressed[i];
@@ -166,8 +168,9 @@ struct EqValue {
 
 }  // namespace
 
-extern "C" int nvdb_eval(const nvdb_netset* ns, int32_t tag, int32_t src_kind, const void* src, const int64_t* gather,
-                         int64_t n, const nvdb_eval_out* out, void* ws, size_t ws_bytes, void* stream) {
+static int eval_impl(const nvdb_netset* ns, int32_t tag, int32_t src_kind, const void* src, const int64_t* gather,
+                     int64_t n, const int64_t* n_dev, const nvdb_eval_out* out, void* ws, size_t ws_bytes,
+                     void* stream) {
   if (!ns || !out || tag < 0 || tag > 3 || src_kind < 0 || src_kind > 4) return fail(NVDB_EINVAL, "nvdb_eval: bad args");
   if (n < 0 || (n > 0 && !src)) return fail(NVDB_EINVAL, "nvdb_eval: bad source");
   BlendOut o{};
@@ -187,7 +190,19 @@ extern "C" int nvdb_eval(const nvdb_netset* ns, int32_t tag, int32_t src_kind, c
     case OUT_VALUE: if (!o.out_f32 && n) return fail(NVDB_EINVAL, "nvdb_eval: f32 output missing"); break;
     default: return fail(NVDB_EINVAL, "nvdb_eval: bad out_mode %d", o.out_mode);
   }
-  return run_blended(ns, tag, src_kind, src, gather, n, o, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+  return run_blended(ns, tag, src_kind, src, gather, n, o, ws, ws_bytes, static_cast<cudaStream_t>(stream), n_dev);
+}
+
+extern "C" int nvdb_eval(const nvdb_netset* ns, int32_t tag, int32_t src_kind, const void* src, const int64_t* gather,
+                         int64_t n, const nvdb_eval_out* out, void* ws, size_t ws_bytes, void* stream) {
+  return eval_impl(ns, tag, src_kind, src, gather, n, nullptr, out, ws, ws_bytes, stream);
+}
+
+extern "C" int nvdb_eval_counted(const nvdb_netset* ns, int32_t tag, int32_t src_kind, const void* src,
+                                 const int64_t* gather, int64_t capacity, const int64_t* count_dev,
+                                 const nvdb_eval_out* out, void* ws, size_t ws_bytes, void* stream) {
+  if (!count_dev) return fail(NVDB_EINVAL, "nvdb_eval_counted: count_dev missing");
+  return eval_impl(ns, tag, src_kind, src, gather, capacity, count_dev, out, ws, ws_bytes, stream);
 }
 
 extern "C" size_t nvdb_select_workspace_bytes(int64_t n) {
@@ -236,7 +251,7 @@ extern "C" int nvdb_l1_apply(uint8_t* cls, float* tiles, int64_t nslots, const i
 extern "C" int nvdb_scatter_f32(float* dst, const int64_t* ids, const float* vals, int64_t n, void* stream) {
   if (n < 0 || (n > 0 && (!dst || !ids || !vals))) return fail(NVDB_EINVAL, "nvdb_scatter_f32: bad args");
   if (!n) return NVDB_OK;
-  k_scatter_f32<<<blocks_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, ids, vals, n);
+  k_scatter_f32<<<blocks_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, ids, vals, n, nullptr);
   NVDB_CHECK_LAUNCH();
   return NVDB_OK;
 }
@@ -269,12 +284,12 @@ extern "C" int nvdb_l0_apply(uint8_t* active, const int64_t* patch_slot, const i
   return NVDB_OK;
 }
 
-extern "C" int nvdb_leaf_finalize(int64_t nl, const uint8_t* active, const int64_t* act_ids, const float* act_vals,
-                                  int64_t nact, const int64_t* patch_slot, const int32_t* patch_vox,
-                                  const uint8_t* patch_active, const float* patch_value, int64_t npatch,
-                                  const int64_t* neg_slot, const uint64_t* neg_bits, int64_t nneg,
-                                  const int32_t* leaf_of_slot, float background, float neg_value, float* values,
-                                  uint64_t* active_words, uint8_t* patched, void* stream) {
+static int leaf_finalize(int64_t nl, const uint8_t* active, const int64_t* act_ids, const float* act_vals,
+                         int64_t nact, const int64_t* nact_dev, const int64_t* patch_slot, const int32_t* patch_vox,
+                         const uint8_t* patch_active, const float* patch_value, int64_t npatch,
+                         const int64_t* neg_slot, const uint64_t* neg_bits, int64_t nneg,
+                         const int32_t* leaf_of_slot, float background, float neg_value, float* values,
+                         uint64_t* active_words, uint8_t* patched, void* stream) {
   if (nl < 0 || nact < 0 || npatch < 0 || nneg < 0) return fail(NVDB_EINVAL, "nvdb_leaf_finalize: bad counts");
   if (nl == 0) return NVDB_OK;
   if (!active || !values) return fail(NVDB_EINVAL, "nvdb_leaf_finalize: null buffers");
@@ -283,7 +298,7 @@ extern "C" int nvdb_leaf_finalize(int64_t nl, const uint8_t* active, const int64
   NVDB_CHECK_LAUNCH();
   if (patched) NVDB_CUDA_TRY(cudaMemsetAsync(patched, 0, (size_t)nl * 512, st));
   if (nact && act_vals) {
-    k_scatter_f32<<<blocks_for(nact), 256, 0, st>>>(values, act_ids, act_vals, nact);
+    k_scatter_f32<<<blocks_for(nact), 256, 0, st>>>(values, act_ids, act_vals, nact, nact_dev);
     NVDB_CHECK_LAUNCH();
   }
   if (npatch) {
@@ -300,6 +315,41 @@ extern "C" int nvdb_leaf_finalize(int64_t nl, const uint8_t* active, const int64
     k_pack_eq<<<blocks_for(nl * 8), 256, 0, st>>>(active, nl * 8, 1, active_words);
     NVDB_CHECK_LAUNCH();
   }
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_leaf_finalize(int64_t nl, const uint8_t* active, const int64_t* act_ids, const float* act_vals,
+                                  int64_t nact, const int64_t* patch_slot, const int32_t* patch_vox,
+                                  const uint8_t* patch_active, const float* patch_value, int64_t npatch,
+                                  const int64_t* neg_slot, const uint64_t* neg_bits, int64_t nneg,
+                                  const int32_t* leaf_of_slot, float background, float neg_value, float* values,
+                                  uint64_t* active_words, uint8_t* patched, void* stream) {
+  return leaf_finalize(nl, active, act_ids, act_vals, nact, nullptr, patch_slot, patch_vox, patch_active, patch_value,
+                       npatch, neg_slot, neg_bits, nneg, leaf_of_slot, background, neg_value, values, active_words,
+                       patched, stream);
+}
+
+extern "C" int nvdb_leaf_finalize_counted(int64_t nl, const uint8_t* active, const int64_t* act_ids,
+                                          const float* act_vals, int64_t act_capacity, const int64_t* nact_dev,
+                                          const int64_t* patch_slot, const int32_t* patch_vox,
+                                          const uint8_t* patch_active, const float* patch_value, int64_t npatch,
+                                          const int64_t* neg_slot, const uint64_t* neg_bits, int64_t nneg,
+                                          const int32_t* leaf_of_slot, float background, float neg_value,
+                                          float* values, uint64_t* active_words, uint8_t* patched, void* stream) {
+  if (!nact_dev) return fail(NVDB_EINVAL, "nvdb_leaf_finalize_counted: nact_dev missing");
+  return leaf_finalize(nl, active, act_ids, act_vals, act_capacity, nact_dev, patch_slot, patch_vox, patch_active,
+                       patch_value, npatch, neg_slot, neg_bits, nneg, leaf_of_slot, background, neg_value, values,
+                       active_words, patched, stream);
+}
+
+extern "C" int nvdb_scatter_f32_counted(float* dst, const int64_t* ids, const float* vals, int64_t capacity,
+                                        const int64_t* count_dev, void* stream) {
+  if (capacity < 0 || !count_dev || (capacity > 0 && (!dst || !ids || !vals)))
+    return fail(NVDB_EINVAL, "nvdb_scatter_f32_counted: bad args");
+  if (!capacity) return NVDB_OK;
+  k_scatter_f32<<<blocks_for(capacity), 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, ids, vals, capacity,
+                                                                                     count_dev);
+  NVDB_CHECK_LAUNCH();
   return NVDB_OK;
 }
 
@@ -325,7 +375,19 @@ extern "C" int nvdb_query_finalize(const int64_t* rows, int64_t nrows, const flo
     return fail(NVDB_EINVAL, "nvdb_query_finalize: bad args");
   if (!nrows) return NVDB_OK;
   k_query_finalize<<<blocks_for(nrows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      rows, nrows, regressed, coords, leaf, tree->leaf_patched, tree->leaf_values, value);
+      rows, nrows, regressed, coords, leaf, tree->leaf_patched, tree->leaf_values, value, nullptr);
+  NVDB_CHECK_LAUNCH();
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_query_finalize_counted(const int64_t* rows, int64_t capacity, const int64_t* nrows_dev,
+                                           const float* regressed, const int32_t* coords, const int32_t* leaf,
+                                           const nvdb_tree* tree, float* value, void* stream) {
+  if (capacity < 0 || !tree || !nrows_dev || (capacity > 0 && (!rows || !regressed || !coords || !leaf || !value)))
+    return fail(NVDB_EINVAL, "nvdb_query_finalize_counted: bad args");
+  if (!capacity) return NVDB_OK;
+  k_query_finalize<<<blocks_for(capacity), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      rows, capacity, regressed, coords, leaf, tree->leaf_patched, tree->leaf_values, value, nrows_dev);
   NVDB_CHECK_LAUNCH();
   return NVDB_OK;
 }

@@ -326,9 +326,15 @@ __device__ __forceinline__ long long floor_div(double v, double s) { return (lon
 // tag's net with a positive gate weight (partition.py:180-229 keeps w > 0).
 __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather, int64_t n, int pass, const int32_t* cells, int ncell,
                             const int32_t* tagnet, int tag, int S, int halo, uint8_t* ncand, uint16_t* keys,
-                            int64_t* vals, BlendOut o, int nokey, int32_t* maxc) {
+                            int64_t* vals, BlendOut o, int nokey, int32_t* maxc, const int64_t* n_dev) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (n_dev && i >= *n_dev) {  // capacity tail beyond the device count: no candidate, no output
+    if (pass == 0) ncand[i] = 0;
+    keys[i] = (uint16_t)nokey;
+    vals[i] = i;
+    return;
+  }
   double c[3];
   point_centre(src_kind, src, gather ? gather[i] : i, c);
   const double h = (double)halo;
@@ -473,7 +479,7 @@ namespace nvdb {
 size_t blended_workspace_bytes(const nvdb_netset* ns, int64_t n) { return ws_layout(ns, n).total; }
 
 int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, const int64_t* gather, int64_t n,
-                const BlendOut& o, void* ws, size_t ws_bytes, cudaStream_t st) {
+                const BlendOut& o, void* ws, size_t ws_bytes, cudaStream_t st, const int64_t* n_dev) {
   if (n <= 0) return NVDB_OK;
   if (n > (int64_t)INT32_MAX) return fail(NVDB_EUNSUPPORTED, "run_blended: n > 2^31");
   MlpArgs a{};
@@ -494,6 +500,7 @@ int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, c
     a.tiles = nullptr;
     a.implicit_net = ns->tagnet[tag];
     a.n_implicit = n;
+    a.n_dev = n_dev;
     const int64_t ntiles = (n + kTileM - 1) / kTileM;
     a.npairs = (int32_t)((ntiles + 1) / 2);
     return launch_mlp(ns, a, nullptr, (int)std::min<int64_t>(a.npairs, num_sms()), st);
@@ -523,7 +530,7 @@ int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, c
   for (int pass = 0; pass < passes; ++pass) {
     if (pass == 0) NVDB_CUDA_TRY(cudaMemsetAsync(maxc, 0, 4, st));
     k_pass_keys<<<blocks, threads, 0, st>>>(src_kind, src, gather, n, pass, ns->dev_cells, ns->nexperts, ns->dev_tagnet,
-                                            tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o, nokey, maxc);
+                                            tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o, nokey, maxc, n_dev);
     NVDB_CHECK_LAUNCH();
     if (pass == 0) {  // later passes only exist up to the largest candidate count of this call
       int32_t hmax = 0;

@@ -97,6 +97,8 @@ struct MlpArgs {
   int32_t pass;               //           last = (ncand[id] == pass + 1); else tile flags
   int32_t implicit_net;
   int64_t n_implicit;
+  const int64_t* n_dev;       // non-null (implicit tiles): the point count is min(*n_dev, n_implicit),
+                              //   read on the device (written by a prior select), no host round trip
   int32_t src_kind;
   const int64_t* idx;     // tile position -> point id (outputs are written at [id])
   const int64_t* gather;  // point id -> source id (nullable: identity)
@@ -288,7 +290,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   const bool issuer = p == 0;
   const double inv2h = 0.5 / (double)a.halo;
 
-  const int npairs = a.npairs_dev ? *a.npairs_dev : a.npairs;
+  const int64_t n_impl = a.n_dev ? min(*a.n_dev, a.n_implicit) : a.n_implicit;
+  const int npairs = a.npairs_dev ? *a.npairs_dev
+                     : a.n_dev ? (int)(((n_impl + kTileM - 1) / kTileM + 1) / 2) : a.npairs;
   const int per_cta = (npairs + gridDim.x - 1) / gridDim.x;
   const int t_begin = 2 * min(npairs, (int)blockIdx.x * per_cta);
   const int t_end = 2 * min(npairs, ((int)blockIdx.x + 1) * per_cta);
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       tl.net = a.implicit_net;
       tl.first = first;
       tl.flags = TF_FIRST | TF_LAST;
-      tl.count = (int32_t)max((int64_t)0, min((int64_t)kTileM, a.n_implicit - first));
+      tl.count = (int32_t)max((int64_t)0, min((int64_t)kTileM, n_impl - first));
     }
     return tl;
   };

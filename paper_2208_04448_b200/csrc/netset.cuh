@@ -123,6 +123,6 @@ struct BlendOut {
 };
 size_t blended_workspace_bytes(const nvdb_netset* ns, int64_t n);
 int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, const int64_t* gather, int64_t n,
-                const BlendOut& o, void* ws, size_t ws_bytes, cudaStream_t st);
+                const BlendOut& o, void* ws, size_t ws_bytes, cudaStream_t st, const int64_t* n_dev = nullptr);
 
 }  // namespace nvdb

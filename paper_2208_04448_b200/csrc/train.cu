@@ -1077,6 +1077,11 @@ __global__ void __launch_bounds__(kRedThreads) k_train_reduce(const float* __res
     double sl = 0.0;
     for (int c = 0; c < nloss; ++c) sl += loss_part[c];
     lossbuf[0] = sl;
+    // the loss rides in the gradient buffer as an f32 (hi, lo) pair, so a
+    // data-parallel step all-reduces ONE buffer of P + 2 floats
+    const float hi = (float)sl;
+    grad[P] = hi;
+    grad[P + 1] = (float)(sl - (double)hi);
   }
 }
 
@@ -1146,8 +1151,8 @@ __global__ void __launch_bounds__(kRedThreads) k_train_adam(AdamArgs a) {
     if (a.loss_part) {
       sl = 0.0;
       for (int c = 0; c < a.nloss; ++c) sl += a.loss_part[c];
-    } else {
-      sl = a.lossbuf[0];
+    } else {  // all-reduced (hi, lo) pair after grad[P] (k_train_reduce)
+      sl = (double)a.grad[a.P] + (double)a.grad[a.P + 1];
     }
     const double loss = sl / a.loss_den;
     a.loss_hist[e] = loss;
@@ -1605,7 +1610,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   chk(dalloc(t, &t->feat_img, (size_t)t->ntiles * kTileM * t->k0));
   chk(dalloc(t, &t->partial, (size_t)t->wg_grid * P));
   chk(dalloc(t, &t->loss_part, (size_t)t->fb_grid));
-  chk(dalloc(t, &t->grad, (size_t)P));
+  chk(dalloc(t, &t->grad, (size_t)P + 2));  // + the loss (hi, lo) pair
   chk(dalloc(t, &t->lossbuf, 1));
   chk(dalloc(t, &t->ctl, 4));
   chk(dalloc(t, &t->loss_hist, d->max_epochs));
@@ -1885,7 +1890,9 @@ extern "C" int nvdb_trainer_run(nvdb_trainer* t, int32_t epochs, void* stream) {
 
 extern "C" int nvdb_trainer_phase(nvdb_trainer* t, int32_t phase, void* stream) {
   if (!t || (phase != 1 && phase != 2)) return fail(NVDB_EINVAL, "nvdb_trainer_phase: bad args");
-  return enqueue_phase(t, phase, static_cast<cudaStream_t>(stream), false, 64);
+  // data-parallel epochs are replayed from a captured graph: presample every
+  // epoch in the first phase-1 call so later epochs launch no sampler
+  return enqueue_phase(t, phase, static_cast<cudaStream_t>(stream), false, t->d.max_epochs);
 }
 
 extern "C" int nvdb_trainer_buffers(nvdb_trainer* t, float** grad, int64_t* nparams, double** loss) {
@@ -1893,6 +1900,13 @@ extern "C" int nvdb_trainer_buffers(nvdb_trainer* t, float** grad, int64_t* npar
   *grad = t->grad;
   *nparams = t->P;
   *loss = t->lossbuf;
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_trainer_packed(nvdb_trainer* t, float** buf, int64_t* nfloats) {
+  if (!t || !buf || !nfloats) return fail(NVDB_EINVAL, "nvdb_trainer_packed: null argument");
+  *buf = t->grad;
+  *nfloats = t->P + 2;
   return NVDB_OK;
 }
 

@@ -156,12 +156,12 @@ class NetEvaluator:
 
     def evaluate(self, tag: str, src_kind: int, src: torch.Tensor, n: int, out_mode: int, *,
                  gather: Optional[torch.Tensor] = None, u8=None, f32=None, probs=None, raw=None,
-                 value_scale: float = 1.0, clip: bool = False) -> None:
+                 value_scale: float = 1.0, clip: bool = False, count: Optional[torch.Tensor] = None) -> None:
         return DeviceModel.evaluate(self, tag, src_kind, src, n, out_mode, gather=gather, u8=u8, f32=f32,
-                                    probs=probs, raw=raw, value_scale=value_scale, clip=clip)
+                                    probs=probs, raw=raw, value_scale=value_scale, clip=clip, count=count)
 
-    def select(self, v: torch.Tensor, value: int) -> torch.Tensor:
-        return DeviceModel.select(self, v, value)
+    def select(self, v: torch.Tensor, value: int, sync: bool = True):
+        return DeviceModel.select(self, v, value, sync)
 
 
 class DeviceModel:
@@ -339,11 +339,36 @@ class DeviceModel:
 
     def evaluate(self, tag: str, src_kind: int, src: torch.Tensor, n: int, out_mode: int, *,
                  gather: Optional[torch.Tensor] = None, u8=None, f32=None, probs=None, raw=None,
-                 value_scale: float = 1.0, clip: bool = False) -> None:
-        """nvdb_eval over n points, chunked on the multi-expert path."""
+                 value_scale: float = 1.0, clip: bool = False, count: Optional[torch.Tensor] = None) -> None:
+        """nvdb_eval over n points, chunked on the multi-expert path.
+
+        ``count``: a device int64 scalar; only its first ``count`` of the n
+        (capacity) points are evaluated and n never has to visit the host
+        (nvdb_eval_counted; single-expert nets only -- the blended path sizes
+        its candidate passes on the host)."""
         if n == 0:
             return
         fast = self.single and self.has_tag[tag]
+        if count is not None:
+            if not fast:
+                n = int(count.item())
+                if n == 0:
+                    return
+            else:
+                out = EvalOut(out_mode=out_mode, raw=_ptr(raw), probs=_ptr(probs), u8=_ptr(u8), f32=_ptr(f32),
+                              value_scale=float(value_scale), background=self.background, clip=int(bool(clip)))
+                timer = getattr(self, "timer", None)
+                if timer is not None:
+                    ev0 = torch.cuda.Event(enable_timing=True)
+                    ev1 = torch.cuda.Event(enable_timing=True)
+                    ev0.record()
+                check(lib().nvdb_eval_counted(self.ns.handle, TAG_CODES[tag], src_kind, _ptr(src), _ptr(gather), n,
+                                              _ptr(count), C.byref(out), None, 0, _stream(self.dev)),
+                      "nvdb_eval_counted")
+                if timer is not None:
+                    ev1.record()
+                    timer.append((tag, count, ev0, ev1))
+                return
         chunk = n if fast else EVAL_CHUNK
         if src_kind == _lib.SRC_LEAF_VOX and gather is None:
             chunk = max(512, chunk // 512 * 512)
@@ -380,8 +405,10 @@ class DeviceModel:
                 ev1.record()
                 timer.append((tag, m, ev0, ev1))
 
-    def select(self, v: torch.Tensor, value: int) -> torch.Tensor:
-        """ids of v == value, ascending (one device->host count read)."""
+    def select(self, v: torch.Tensor, value: int, sync: bool = True):
+        """ids of v == value, ascending.  sync: one device->host count read,
+        returns the ids; otherwise returns (ids at capacity v.numel(), device
+        int64 count) without a host round trip."""
         n = v.numel()
         ids = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
         cnt = torch.zeros(1, dtype=torch.int64, device=self.dev)
@@ -389,6 +416,8 @@ class DeviceModel:
         ws = torch.empty(int(wsb), dtype=torch.uint8, device=self.dev)
         check(lib().nvdb_select_u8(_ptr(v), n, value, _ptr(ids), _ptr(cnt), _ptr(ws), ws.numel(),
                                    _stream(self.dev)), "nvdb_select_u8")
+        if not sync:
+            return ids, cnt
         return ids[:int(cnt.item())]
 
     # -- decode --------------------------------------------------------------------
@@ -410,14 +439,17 @@ class DeviceModel:
         check(lib().nvdb_l1_apply(_ptr(cls), _ptr(tiles), nslots, _ptr(self.p1_slot), _ptr(self.p1_cls),
                                   self.p1_slot.numel(), _ptr(self.t_slot), _ptr(self.t_val), self.t_slot.numel(),
                                   st), "nvdb_l1_apply")
-        active_tiles = self.select(cls[:nslots], 1)
-        if active_tiles.numel():
-            tv = torch.empty(active_tiles.numel(), dtype=torch.float32, device=dev)
+        # active tiles through the tile regressor; without a tile net they stay
+        # background (blended_values uncovered -> background, decoder.py:135-141)
+        if self.has_tag["tile"]:
+            tids, tcnt = self.select(cls[:nslots], 1, sync=False)
+            tv = torch.empty(max(nslots, 1), dtype=torch.float32, device=dev)
             # tile values scale by float(np.float32(value_scale)), no clip (decoder.py:141)
-            self.evaluate("tile", _lib.SRC_L1_SLOT, self.d_origins, active_tiles.numel(), _lib.OUT_VALUE,
-                          gather=active_tiles, f32=tv, value_scale=float(np.float32(self.value_scale)))
-            check(lib().nvdb_scatter_f32(_ptr(tiles), _ptr(active_tiles), _ptr(tv), active_tiles.numel(), st),
-                  "nvdb_scatter_f32")
+            self.evaluate("tile", _lib.SRC_L1_SLOT, self.d_origins, nslots, _lib.OUT_VALUE, gather=tids, f32=tv,
+                          value_scale=float(np.float32(self.value_scale)), count=tcnt)
+            check(lib().nvdb_scatter_f32_counted(_ptr(tiles), _ptr(tids), _ptr(tv), nslots, _ptr(tcnt), st),
+                  "nvdb_scatter_f32_counted")
+        # the one host round trip of a decode: the leaf count sizes the leaf buffers
         child = self.select(cls[:nslots], 0)
         leaf_of_slot = torch.empty(max(nslots, 1), dtype=torch.int32, device=dev)
         if shard is not None:
@@ -438,33 +470,33 @@ class DeviceModel:
             leaf_origins = torch.empty((max(nl, 1), 3), dtype=torch.int32, device=dev)
             check(lib().nvdb_leaf_list(_ptr(child), nl, _ptr(self.d_origins), nslots, _ptr(leaf_origins),
                                        _ptr(leaf_of_slot), st), "nvdb_leaf_list")
-        act = torch.zeros(max(nl * LEAF_SIZE, 1), dtype=torch.uint8, device=dev)
-        self.evaluate("l0", _lib.SRC_LEAF_VOX, leaf_origins, nl * LEAF_SIZE, _lib.OUT_L0ACTIVE, u8=act)
+        nv = nl * LEAF_SIZE
+        act = torch.zeros(max(nv, 1), dtype=torch.uint8, device=dev)
+        self.evaluate("l0", _lib.SRC_LEAF_VOX, leaf_origins, nv, _lib.OUT_L0ACTIVE, u8=act)
         self._ensure_l0()  # host work while the L0 stage runs
         err = torch.zeros(1, dtype=torch.int32, device=dev)
         check(lib().nvdb_l0_apply(_ptr(act), _ptr(self.p0_slot), _ptr(self.p0_vox), _ptr(self.p0_act),
                                   self.p0_slot.numel(), _ptr(leaf_of_slot), _ptr(err), st), "nvdb_l0_apply")
-        evals = 0
         act_ids = vals = None
+        acnt = torch.zeros(1, dtype=torch.int64, device=dev)
         if materialize_values and nl:
-            act_ids = self.select(act[:nl * LEAF_SIZE], 1)
-            evals = int(act_ids.numel())
-            vals = torch.empty(max(evals, 1), dtype=torch.float32, device=dev)
-            self.evaluate("voxel", _lib.SRC_LEAF_VOX, leaf_origins, evals, _lib.OUT_VALUE, gather=act_ids,
-                          f32=vals, value_scale=self.value_scale, clip=self.meta.grid_class == "sdf")
-        values = torch.empty(max(nl * LEAF_SIZE, 1), dtype=torch.float32, device=dev)
+            # active voxels -> voxel regressor -> finalize, the count staying on the device
+            act_ids, acnt = self.select(act[:nv], 1, sync=False)
+            vals = torch.empty(max(nv, 1), dtype=torch.float32, device=dev)
+            self.evaluate("voxel", _lib.SRC_LEAF_VOX, leaf_origins, nv, _lib.OUT_VALUE, gather=act_ids,
+                          f32=vals, value_scale=self.value_scale, clip=self.meta.grid_class == "sdf", count=acnt)
+        values = torch.empty(max(nv, 1), dtype=torch.float32, device=dev)
         words = torch.empty(max(nl * 8, 1), dtype=torch.int64, device=dev)
-        patched = torch.empty(max(nl * LEAF_SIZE, 1), dtype=torch.uint8, device=dev)
-        check(lib().nvdb_leaf_finalize(nl, _ptr(act), _ptr(act_ids), _ptr(vals), evals, _ptr(self.p0_slot),
-                                       _ptr(self.p0_vox), _ptr(self.p0_act), _ptr(self.p0_val),
-                                       self.p0_slot.numel(), _ptr(self.neg_slot), _ptr(self.neg_bits),
-                                       self.neg_slot.numel(), _ptr(leaf_of_slot), self.background,
-                                       -float(np.float32(self.value_scale)), _ptr(values), _ptr(words),
-                                       _ptr(patched), st), "nvdb_leaf_finalize")
-        if int(err.item()):
-            raise SvcodecError("corrupt container: level-0 patch outside every reconstructed leaf")
-        return DeviceDecode(self, cls[:nslots], tiles[:nslots], child, leaf_origins[:nl], act[:nl * LEAF_SIZE],
-                            values[:nl * LEAF_SIZE], words[:nl * 8], patched[:nl * LEAF_SIZE], evals, shard)
+        patched = torch.empty(max(nv, 1), dtype=torch.uint8, device=dev)
+        check(lib().nvdb_leaf_finalize_counted(nl, _ptr(act), _ptr(act_ids), _ptr(vals),
+                                               nv if act_ids is not None else 0, _ptr(acnt), _ptr(self.p0_slot),
+                                               _ptr(self.p0_vox), _ptr(self.p0_act), _ptr(self.p0_val),
+                                               self.p0_slot.numel(), _ptr(self.neg_slot), _ptr(self.neg_bits),
+                                               self.neg_slot.numel(), _ptr(leaf_of_slot), self.background,
+                                               -float(np.float32(self.value_scale)), _ptr(values), _ptr(words),
+                                               _ptr(patched), st), "nvdb_leaf_finalize_counted")
+        return DeviceDecode(self, cls[:nslots], tiles[:nslots], child, leaf_origins[:nl], act[:nv],
+                            values[:nv], words[:nl * 8], patched[:nv], acnt, shard, err)
 
 
 @dataclass
@@ -480,17 +512,34 @@ class DeviceDecode:
     leaf_values: torch.Tensor   # (nl*512,) f32
     active_words: torch.Tensor  # (nl*8,) packed masks (int64 view of u64)
     patched: torch.Tensor       # (nl*512,) u8
-    regressor_evaluations: int
+    evals_dev: torch.Tensor     # (1,) int64: voxel-regressor evaluations (device)
     shard: Optional[Tuple[int, int]] = None  # (rank, world) when only a leaf range was decoded
+    err_dev: Optional[torch.Tensor] = None   # (1,) int32: a level-0 patch fell outside every leaf
+    _checked: bool = False
 
     @property
     def leaf_count(self) -> int:
         return int(self.leaf_origins.shape[0])
 
+    @property
+    def regressor_evaluations(self) -> int:
+        return int(self.evals_dev.item())
+
+    def check(self) -> "DeviceDecode":
+        """Raise SvcodecError for a corrupt container (decoder.py:172-175).  The
+        flag is read lazily (first host access) so a decode enqueues without a
+        stream synchronisation."""
+        if not self._checked and self.err_dev is not None:
+            if int(self.err_dev.item()):
+                raise SvcodecError("corrupt container: level-0 patch outside every reconstructed leaf")
+            self._checked = True
+        return self
+
     def to_grid(self) -> DenseLeafGrid:
         """Host DenseLeafGrid in canonical (root, idx2, idx1) order."""
         if self.shard is not None and self.shard[1] > 1:
             raise ValueError("a sharded decode holds a leaf range, not a grid; gather the shards first")
+        self.check()
         m = self.model
         c = m.c
         meta = c.grid_meta
@@ -546,25 +595,91 @@ def shard_range(nleaves: int, rank: int, world: int) -> Tuple[int, int]:
     return nleaves * rank // world, nleaves * (rank + 1) // world
 
 
+def gather_rows(parts, group=None, dst: int = 0):
+    """Concatenate every rank's row blocks, in rank order, on rank ``dst``.
+
+    ``parts``: this rank's tensors, each (n_rank, ...) with the same row count
+    n_rank across the list (row counts may differ between ranks).  One
+    all-gather of the counts, then one all-gather per tensor of the blocks
+    padded to the largest count (NCCL over NVLink for device tensors, gloo for
+    host tensors).  Returns the concatenated tensors on ``dst`` and None
+    elsewhere.  SURVEY.md §8(e): the optional gather of dense-leaf outputs."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = parts[0].device
+    n = int(parts[0].shape[0])
+    cnt = torch.tensor([n], dtype=torch.int64, device=dev)
+    allc = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(allc, cnt, group=group)
+    counts = [int(c.item()) for c in allc]
+    mx = max(max(counts), 1)
+    out = []
+    for t in parts:
+        pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+        pad[:n] = t[:n]
+        bufs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(bufs, pad, group=group)
+        out.append(torch.cat([b[:c] for b, c in zip(bufs, counts)]) if rank == dst else None)
+    return out if rank == dst else None
+
+
 def _as_model(c, device=None) -> DeviceModel:
     return c if isinstance(c, DeviceModel) else DeviceModel(c, device)
 
 
-def decode_full(c, device=None, as_svcodec: bool = False):
+def decode_sharded(m: DeviceModel, group=None, dst: int = 0) -> Optional["DeviceDecode"]:
+    """Decode over the ranks of ``group`` (one process per GPU): every rank
+    classifies the level-1 slots (cheap, redundant), decodes its contiguous
+    leaf range, and the dense-leaf blocks are gathered in leaf order on rank
+    ``dst`` (PAPER.md:253 disjoint-block decode).  Returns
+    the full DeviceDecode on ``dst``, None elsewhere."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    d = m.decode(True, shard=(rank, world)).check()
+    nl = d.leaf_count
+    parts = [d.child_slots[:nl], d.leaf_origins[:nl], d.leaf_active.view(nl, LEAF_SIZE),
+             d.leaf_values.view(nl, LEAF_SIZE), d.active_words.view(nl, 8), d.patched.view(nl, LEAF_SIZE)]
+    g = gather_rows(parts, group, dst)
+    ev = torch.zeros(1, dtype=torch.int64, device=m.dev)
+    ev += d.evals_dev
+    dist.all_reduce(ev, group=group)
+    if g is None:
+        return None
+    child, lo, la, lv, w, pt = g
+    return DeviceDecode(m, d.l1_class, d.l1_tiles, child, lo, la.reshape(-1), lv.reshape(-1), w.reshape(-1),
+                        pt.reshape(-1), ev, None, None, True)
+
+
+def decode_full(c, device=None, as_svcodec: bool = False, group=None):
     """decoder.decode_full (decoder.py:214-217): the complete explicit grid.
 
     Returns a :class:`DenseLeafGrid` (or an svcodec ``VdbGrid`` with
-    ``as_svcodec=True`` when the reference package is importable).
+    ``as_svcodec=True`` when the reference package is importable).  With a
+    ``torch.distributed`` group of G > 1 ranks (one per GPU) the leaves are
+    decoded in G contiguous ranges and gathered on rank 0, which returns the
+    grid; the other ranks return None.
     """
     m = _as_model(c, device)
-    g = m.decode(True).to_grid()
+    if group is not None and _world(group) > 1:
+        d = decode_sharded(m, group)
+        if d is None:
+            return None
+    else:
+        d = m.decode(True)
+    g = d.to_grid()
     return g.to_svcodec() if as_svcodec else g
+
+
+def _world(group) -> int:
+    import torch.distributed as dist
+    return dist.get_world_size(group)
 
 
 def decode_report(c, device=None) -> Dict[str, int]:
     """decoder.decode_report (decoder.py:294-300)."""
     m = _as_model(c, device)
-    d = m.decode(True)
+    d = m.decode(True).check()
     return {"regressor_evaluations": d.regressor_evaluations,
             "active_voxels": int(d.leaf_active.sum().item())}
 
@@ -580,15 +695,14 @@ def hybrid_query(tree: DeviceTree, nets, coords: torch.Tensor, value_scale: floa
     val, act, kind, leaf = tree.lookup(coords, want_leaf=True)
     flag = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
     check(lib().nvdb_neural_rows(_ptr(act), _ptr(kind), n, _ptr(flag), st), "nvdb_neural_rows")
-    rows = nets.select(flag[:n], 1)
-    nr = rows.numel()
-    if nr:
-        reg = torch.empty(nr, dtype=torch.float32, device=dev)
-        nets.evaluate("voxel", _lib.SRC_COORD_I32, coords, nr, _lib.OUT_VALUE, gather=rows, f32=reg,
-                      value_scale=value_scale, clip=clip)
-        check(lib().nvdb_query_finalize(_ptr(rows), nr, _ptr(reg), _ptr(coords), _ptr(leaf),
-                                        tree.handle, _ptr(val), st), "nvdb_query_finalize")
-    return val, act, nr
+    rows, cnt = nets.select(flag[:n], 1, sync=False)
+    if n:
+        reg = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+        nets.evaluate("voxel", _lib.SRC_COORD_I32, coords, n, _lib.OUT_VALUE, gather=rows, f32=reg,
+                      value_scale=value_scale, clip=clip, count=cnt)
+        check(lib().nvdb_query_finalize_counted(_ptr(rows), n, _ptr(cnt), _ptr(reg), _ptr(coords), _ptr(leaf),
+                                                tree.handle, _ptr(val), st), "nvdb_query_finalize_counted")
+    return val, act, cnt
 
 
 class HybridGrid:
@@ -609,11 +723,29 @@ class HybridGrid:
         """(values f32, active u8) for device int32 coords (n,3)."""
         m = self.model
         val, act, nr = hybrid_query(self.tree, m, coords, m.value_scale, m.meta.grid_class == "sdf")
-        self.regressor_evaluations += nr
+        self._evals.append(nr)
         return val, act
 
-    def query(self, coords) -> Tuple[np.ndarray, np.ndarray]:
-        """Batched (value, active) at integer coordinates (decoder.py:239-264)."""
+    @property
+    def regressor_evaluations(self) -> int:
+        """Voxel-regressor rows over all queries so far (decoder.py:262-263)."""
+        if self._evals:
+            self._base += int(sum(int(t.item()) for t in self._evals))
+            self._evals = []
+        return self._base
+
+    @regressor_evaluations.setter
+    def regressor_evaluations(self, v: int) -> None:
+        self._evals, self._base = [], int(v)
+
+    def query(self, coords, group=None) -> Tuple[np.ndarray, np.ndarray]:
+        """Batched (value, active) at integer coordinates (decoder.py:239-264).
+
+        With a ``torch.distributed`` group of G > 1 ranks every rank passes the
+        same coordinates, queries its contiguous 1/G slice on its own GPU (tree
+        and nets replicated, no collective on the data path), and rank 0
+        returns all results in order (gathered over NCCL); other ranks return
+        (None, None).  SURVEY.md §8(e) "Random query"."""
         c = np.asarray(coords)
         if c.dtype != np.int32:
             c = c.astype(np.int64)
@@ -621,8 +753,17 @@ class HybridGrid:
         lim = 1 << 30
         if c.size and (c.max() >= lim or c.min() <= -lim):  # grid.py:69-71, no abs() overflow on int32
             raise SvcodecError("coordinate outside legal range +-2^30")
+        if group is not None and _world(group) > 1:
+            import torch.distributed as dist
+            lo, hi = shard_range(c.shape[0], dist.get_rank(group), _world(group))
+            c = c[lo:hi]
         d = torch.from_numpy(np.ascontiguousarray(c, dtype=np.int32)).to(self.model.dev)
         v, a = self.query_device(d)
+        if group is not None and _world(group) > 1:
+            g = gather_rows([v, a], group)
+            if g is None:
+                return None, None
+            v, a = g
         v, a = _to_host([v, a])
         return v.copy(), a.view(np.bool_).copy()
 

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import logging
+import os
 from dataclasses import dataclass, field, replace
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -331,23 +332,49 @@ class DeviceTrainer:
         check(lib().nvdb_trainer_create(C.byref(d), C.byref(h)), "nvdb_trainer_create")
         self.handle = h
         self.epochs_enqueued = 0
-        if self.world > 1:
-            g, npar, lo = C.c_void_p(), C.c_int64(), C.c_void_p()
-            check(lib().nvdb_trainer_buffers(self.handle, C.byref(g), C.byref(npar), C.byref(lo)),
-                  "nvdb_trainer_buffers")
-            self.grad = torch.as_tensor(_DeviceArray(g.value, npar.value, "<f4"), device=self.dev)
-            self.loss = torch.as_tensor(_DeviceArray(lo.value, 1, "<f8"), device=self.dev)
+        self._graph = None
+        if group is not None:  # data-parallel form (a world-1 group runs it too)
+            g, nf = C.c_void_p(), C.c_int64()
+            check(lib().nvdb_trainer_packed(self.handle, C.byref(g), C.byref(nf)), "nvdb_trainer_packed")
+            # gradient sums + the loss (hi, lo) pair: one all-reduce per epoch
+            self.packed = torch.as_tensor(_DeviceArray(g.value, nf.value, "<f4"), device=self.dev)
+            import torch.distributed as dist
+            self._graphable = dist.get_backend(group) == "nccl" and os.environ.get("NVDB_DP_GRAPH", "1") == "1"
+
+    def _epoch_dp(self, st) -> None:
+        import torch.distributed as dist
+        check(lib().nvdb_trainer_phase(self.handle, 1, st), "nvdb_trainer_phase")
+        dist.all_reduce(self.packed, group=self.group)
+        check(lib().nvdb_trainer_phase(self.handle, 2, st), "nvdb_trainer_phase")
 
     def _enqueue(self, k: int, st) -> None:
-        if self.world == 1:
+        if self.group is None:
             check(lib().nvdb_trainer_run(self.handle, k, st), "nvdb_trainer_run")
             return
-        import torch.distributed as dist
+        if self.epochs_enqueued == 0 or not self._graphable:
+            # eager epoch (the first one also presamples every epoch's batch)
+            self._epoch_dp(st)
+            k -= 1
+            if not self._graphable:
+                for _ in range(k):
+                    self._epoch_dp(st)
+                return
+        if k <= 0:
+            return
+        if self._graph is None:
+            # phase 1 -> NCCL all-reduce -> phase 2 captured once; every launch
+            # reads the epoch from device memory, so the graph replays any epoch
+            # (no Python / host launch cost per epoch; replays after the early
+            # stop are device no-ops)
+            torch.cuda.synchronize(self.dev)
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(self.dev)
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(g, stream=cap):
+                    self._epoch_dp(cap.cuda_stream)
+            self._graph = g  # capture does not execute: every epoch below is a replay
         for _ in range(k):
-            check(lib().nvdb_trainer_phase(self.handle, 1, st), "nvdb_trainer_phase")
-            dist.all_reduce(self.grad, group=self.group)
-            dist.all_reduce(self.loss, group=self.group)
-            check(lib().nvdb_trainer_phase(self.handle, 2, st), "nvdb_trainer_phase")
+            self._graph.replay()
 
     def run(self, epochs: Optional[int] = None) -> Tuple[float, int]:
         """Train until the early stop or max_epochs; returns (final loss, epochs)."""
@@ -424,8 +451,9 @@ def _check_targets(targets: np.ndarray, kind: str, out_dim: int) -> None:
 
 def train_network(inputs: np.ndarray, targets: np.ndarray, spec: NetSpec, cfg, expert_id: int, lr0: float,
                   warm: Optional[NetRecord] = None, stop_loss: Optional[float] = None, workspace=None,
-                  device=None, return_trainer: bool = False) -> NetRecord:
-    """Train one network on the GPU; returns the committed record (encoder.py:330-371)."""
+                  device=None, return_trainer: bool = False, group=None) -> NetRecord:
+    """Train one network on the GPU; returns the committed record (encoder.py:330-371).
+    ``group``: data-parallel over the ranks of a torch.distributed group."""
     del workspace
     depth, width = spec.arch
     tagid = NET_TAGS[spec.tag]
@@ -447,7 +475,8 @@ def train_network(inputs: np.ndarray, targets: np.ndarray, spec: NetSpec, cfg, e
     n = x.shape[0]
     target = spec.loss_target if stop_loss is None else max(spec.loss_target, stop_loss)
     sampled = (not spec.full_batch) and n > cfg.batch_size
-    tr = DeviceTrainer(params, ff, x, targets, spec.loss_kind, cfg, lr0, seed_draw, sampled, target, device)
+    tr = DeviceTrainer(params, ff, x, targets, spec.loss_kind, cfg, lr0, seed_draw, sampled, target, device,
+                       group=group)
     try:
         loss, epochs = tr.run()
         out = NetRecord(params=tr.weights(), ff=ff, final_loss=float(loss), epochs=epochs)
@@ -460,10 +489,11 @@ def train_network(inputs: np.ndarray, targets: np.ndarray, spec: NetSpec, cfg, e
 
 
 def extract_patches(grid: DenseLeafGrid, layout: SubdomainLayout, experts: List[EncodedSubdomain], cfg,
-                    device=None) -> None:
+                    device=None, only=None) -> None:
     """Classifier disagreements vs ground truth become patches (encoder.py:430-486).
 
     Predictions come from the same fused blended evaluator the decoder uses.
+    ``only``: subdomain ids to extract (an expert-parallel rank's own).
     """
     band = grid.half_width * grid.voxel_size
     if cfg.significance_threshold is not None:
@@ -476,6 +506,8 @@ def extract_patches(grid: DenseLeafGrid, layout: SubdomainLayout, experts: List[
     by_id = {e.id: e for e in experts}
     try:
         for sub in layout.subdomains:
+            if only is not None and sub.id not in only:
+                continue
             expert = by_id[sub.id]
             patches = PatchList()
             own1 = np.all((grid.l1_origins >= sub.lo) & (grid.l1_origins < sub.hi), axis=1) \
@@ -546,7 +578,7 @@ def build_upper_tree(grid: DenseLeafGrid) -> UpperTree:
 
 
 def _train_expert(grid: DenseLeafGrid, sub: Subdomain, cfg, lr0: float, warm=None, stop_losses=None,
-                  device=None) -> EncodedSubdomain:
+                  device=None, group=None) -> EncodedSubdomain:
     """encoder.py:531-570."""
     scale = value_scale_of(grid)
     norm = (np.asarray(warm.norm_origin, dtype=np.float64).copy(), float(warm.norm_scale)) \
@@ -565,7 +597,7 @@ def _train_expert(grid: DenseLeafGrid, sub: Subdomain, cfg, lr0: float, warm=Non
         stop = None if stop_losses is None else stop_losses.get(tag)
         try:
             return train_network(inputs, targets, spec, cfg, sub.id, lr0, warm=warm_net, stop_loss=stop,
-                                 device=device)
+                                 device=device, group=group)
         except Exception as exc:
             raise EncodeError(f"{tag} training failed: {exc}", sub.id) from exc
 
@@ -579,8 +611,18 @@ def _train_expert(grid: DenseLeafGrid, sub: Subdomain, cfg, lr0: float, warm=Non
 
 
 def encode(grid, cfg, weight_precision: int = 32, workers: int = 1, _warm=None, _lr0=None, _stop_losses=None,
-           device=None) -> NeuralGridContainer:
-    """Encode a grid into its hierarchical neural container (encoder.py:573-611)."""
+           device=None, group=None) -> NeuralGridContainer:
+    """Encode a grid into its hierarchical neural container (encoder.py:573-611).
+
+    ``group``: a ``torch.distributed`` group of G > 1 ranks, one per GPU, all
+    calling with the same grid (SURVEY.md §8(e) "Training").  With at least G
+    experts the experts are spread round-robin over the ranks (independent,
+    no collective while training; the reference's expert thread pool,
+    encoder.py:596-600) and each rank extracts its experts' patches; the
+    trained experts are then exchanged so every rank returns the complete
+    container.  With fewer experts than ranks every network is trained data
+    parallel (each rank a 1/G slice of every epoch's batch, one packed
+    gradient + loss all-reduce per epoch)."""
     del workers  # experts train one after another on the device; each net uses the whole GPU
     _validate(cfg)
     g = as_grid(grid)
@@ -588,14 +630,39 @@ def encode(grid, cfg, weight_precision: int = 32, workers: int = 1, _warm=None, 
     if not layout.subdomains:
         raise EncodeError("grid has no active values")
     lr0 = cfg.lr if _lr0 is None else _lr0
+    world, rank = 1, 0
+    if group is not None:
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    expert_parallel = world > 1 and len(layout.subdomains) >= world
+    dp_group = group if world > 1 and not expert_parallel else None
     experts = []
-    for sub in layout.subdomains:
+    for i, sub in enumerate(layout.subdomains):
+        if expert_parallel and i % world != rank:
+            continue
         warm = _warm.get(sub.cell) if _warm else None
         stops = None
         if _stop_losses is not None:
             stops = {tag: _stop_losses[(sub.cell, tag)] for tag in NET_TAGS if (sub.cell, tag) in _stop_losses}
-        experts.append(_train_expert(g, sub, cfg, lr0, warm=warm, stop_losses=stops, device=device))
-    extract_patches(g, layout, experts, cfg, device)
+        experts.append(_train_expert(g, sub, cfg, lr0, warm=warm, stop_losses=stops, device=device,
+                                     group=dp_group))
+    if expert_parallel:
+        # every rank needs all experts: patch extraction blends across
+        # subdomain boundaries and the container holds every expert
+        import torch.distributed as dist
+        got: list = [None] * world
+        dist.all_gather_object(got, experts, group=group)
+        experts = sorted((e for part in got for e in part), key=lambda e: e.id)
+        mine = [s.id for i, s in enumerate(layout.subdomains) if i % world == rank]
+        extract_patches(g, layout, experts, cfg, device, only=set(mine))
+        pats: list = [None] * world
+        dist.all_gather_object(pats, {e.id: e.patches for e in experts if e.id in mine}, group=group)
+        by_id = {e.id: e for e in experts}
+        for part in pats:
+            for sid, p in part.items():
+                by_id[sid].patches = p
+    else:
+        extract_patches(g, layout, experts, cfg, device)
     meta = GridMeta(g.grid_class, g.background, g.voxel_size, g.half_width, value_scale_of(g))
     return NeuralGridContainer(grid_meta=meta, upper_tree=build_upper_tree(g), layout=layout, experts=experts,
                                config=replace(cfg) if hasattr(cfg, "__dataclass_fields__") else cfg,
@@ -621,7 +688,7 @@ def _frame_loss(c) -> float:
     return float(np.mean(losses)) if losses else 0.0
 
 
-def encode_sequence(grids: Sequence, cfg, weight_precision: int = 32, workers: int = 1, device=None):
+def encode_sequence(grids: Sequence, cfg, weight_precision: int = 32, workers: int = 1, device=None, group=None):
     """Warm-start encoding of an animated sequence (encoder.py:638-714)."""
     if len(grids) < 2:
         raise EncodeError("a sequence needs at least 2 frames")
@@ -639,11 +706,11 @@ def encode_sequence(grids: Sequence, cfg, weight_precision: int = 32, workers: i
         return replace(cfg, seed=stable_seed(cfg.seed, 9000 + pass_id))
 
     def cold_refine(g, pass_id, warm_from=None, only_cells=None):
-        cold = encode(g, frame_cfg(pass_id), weight_precision, workers, _warm=warm_from, device=device)
+        cold = encode(g, frame_cfg(pass_id), weight_precision, workers, _warm=warm_from, device=device, group=group)
         cold_epochs = _frame_epochs(cold)
         warm = {e.cell: e for e in cold.experts if only_cells is None or e.cell in only_cells}
         refined = encode(g, frame_cfg(pass_id + 1), weight_precision, workers, _warm=warm, _lr0=refine_lr,
-                         device=device)
+                         device=device, group=group)
         return cold, refined, cold_epochs
 
     _, frame0, cold_epochs0 = cold_refine(gs[0], 0)
@@ -669,7 +736,7 @@ def encode_sequence(grids: Sequence, cfg, weight_precision: int = 32, workers: i
                         if net is not None:
                             targets[(e.cell, tag)] = net.final_loss
         ct = encode(gs[t], frame_cfg(10 * t + 2), weight_precision, workers, _warm=warm, _lr0=refine_lr,
-                    _stop_losses=targets, device=device)
+                    _stop_losses=targets, device=device, group=group)
         containers.append(ct)
         reports.append(FrameReport(t, _frame_epochs(ct), _frame_loss(ct), {}))
         prev = ct

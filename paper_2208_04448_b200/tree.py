@@ -95,6 +95,7 @@ class DeviceTree:
     def from_decode(cls, d) -> "DeviceTree":
         """Hybrid topology of a device decode (decoder.py:52-81 + _fill_leaves wiring)."""
         from ._lib import lib as _l  # noqa: WPS433
+        d.check()
         m = d.model
         c = m.c
         ut = c.upper_tree

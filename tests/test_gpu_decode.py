@@ -17,7 +17,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from conftest import GOLDEN  # noqa: E402
-from paper_2208_04448_b200.decoder import DeviceModel, make_hybrid  # noqa: E402
+from paper_2208_04448_b200.decoder import DeviceModel, decode_full, make_hybrid  # noqa: E402
 from paper_2208_04448_b200.model import LEAF_SIZE, container_from_arrays, grid_from_arrays  # noqa: E402
 from helpers import OCC_BAR, assert_value_bars  # noqa: E402
 
@@ -162,8 +162,14 @@ def test_corrupt_containers_raise_svcodec_error(golden):
     corner = m.origins[ni] + L1_LOCAL[si] * 8
     m.close()
     c.experts[0].patches.l0.append((tuple(int(v) for v in corner), True, 0.5))
+    # the decode enqueues without a host round trip; the corruption flag is
+    # raised at the first host access (decode_full, make_hybrid, check())
     with pytest.raises(SvcodecError):
-        DeviceModel(c).decode(True)
+        DeviceModel(c).decode(True).check()
+    with pytest.raises(SvcodecError):
+        decode_full(c)
+    with pytest.raises(SvcodecError):
+        make_hybrid(c)
 
 
 @pytest.mark.parametrize("name", ["decode_small", "decode_multi"])

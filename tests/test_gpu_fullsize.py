@@ -218,6 +218,7 @@ def test_c5_shaped_query_sample_parity():
     rv, ra, rk = O.lookup(g, coords.astype(np.int64))
     np.testing.assert_array_equal(act, ra)
     reg = ra & (rk == 2)
+    nr = int(nr.item())
     assert nr == int(reg.sum()) and nr >= 4096
     np.testing.assert_array_equal(val[~reg].view(np.uint32), np.asarray(rv, np.float32)[~reg].view(np.uint32))
     bv, cov = O.blended(layout, experts, coords[reg].astype(np.float64) + 0.5, "voxel")

@@ -146,3 +146,25 @@ def test_shard_ranges_partition():
                 assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+def _gather_rows(rank, world):
+    import torch
+    from paper_2208_04448_b200.decoder import gather_rows
+    n = 3 + 2 * rank  # unequal blocks per rank
+    a = torch.arange(n * 4, dtype=torch.int32).view(n, 4) + 1000 * rank
+    b = torch.full((n,), float(rank), dtype=torch.float32)
+    out = gather_rows([a, b], None, dst=0)
+    return None if out is None else [t.numpy() for t in out]
+
+
+def test_gather_rows_concatenates_in_rank_order():
+    """decoder.gather_rows (the dense-leaf / query-result gather of the sharded
+    decode and query) on real gloo collectives: unequal blocks, rank order."""
+    out = _spawn("_gather_rows")
+    assert out[1] is None
+    a, b = out[0]
+    exp_a = np.concatenate([np.arange(n * 4, dtype=np.int32).reshape(n, 4) + 1000 * r
+                            for r, n in ((0, 3), (1, 5))])
+    np.testing.assert_array_equal(a, exp_a)
+    np.testing.assert_array_equal(b, np.array([0] * 3 + [1] * 5, np.float32))

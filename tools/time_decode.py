@@ -25,6 +25,7 @@ e1.record()
 torch.cuda.synchronize()
 print("decode total ms", e0.elapsed_time(e1))
 for tag, n, a, b in m.timer:
+    n = int(n.item()) if hasattr(n, 'item') else int(n)
     print(" stage", tag, n, "ms", a.elapsed_time(b))
 m.timer = None
 lo = d.leaf_origins

@@ -480,10 +480,17 @@ def main():
             dist.barrier()
             dist.destroy_process_group()
         return
+    # one rank per GPU; NVDB_BENCH_BACKEND=gloo lets N ranks share fewer GPUs
+    # (a functional check of the N > 1 path on a 1-GPU box, never a bench number)
+    backend = os.environ.get("NVDB_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     args.warmup = max(args.warmup, 3)
     from paper_2208_04448_b200 import _lib
     from paper_2208_04448_b200.decoder import DeviceModel, decode_full

@@ -237,6 +237,19 @@ NVDB_API int nvdb_query_finalize_counted(const int64_t* rows, int64_t capacity, 
                                          const float* regressed, const int32_t* coords, const int32_t* leaf,
                                          const nvdb_tree* tree, float* value, void* stream);
 
+/* -- NVGR emission (gridfile.py:43-76) ------------------ */
+/* Leaf records (origin i32x3 | packbits-little active mask 64 B | 512 f32
+ * values, 2124 B) of a dense-leaf decode, leaf r written at out + rec_off[r]
+ * (byte offsets into the NVGR stream, any alignment).  DEVICE pointers. */
+NVDB_API int nvdb_nvgr_leaf_records(const int32_t* leaf_origins, const uint64_t* active_words,
+                                    const float* values, int64_t nleaves, const int64_t* rec_off, uint8_t* out,
+                                    void* stream);
+/* Level-1 node records (origin | child mask 512 B (class 0) | active mask
+ * 512 B (class 1) | 4096 f32 tiles, 17420 B) from the decode's per-slot
+ * classes and tiles (node order of node_origins).  DEVICE pointers. */
+NVDB_API int nvdb_nvgr_l1_records(const int32_t* node_origins, const uint8_t* l1_class, const float* tiles,
+                                  int64_t nnodes, const int64_t* rec_off, uint8_t* out, void* stream);
+
 /* -- training (encoder.train_network, encoder.py:330-371) -------------------- */
 
 #define NVDB_LOSS_MSE 0

@@ -34,7 +34,7 @@ EXPORTED = [
     "nvdb_trainer_status", "nvdb_trainer_weights", "nvdb_sample_indices", "nvdb_trainer_phase",
     "nvdb_trainer_buffers", "nvdb_sample_indices_subset", "nvdb_fbm_leaves", "nvdb_trim",
     "nvdb_eval_counted", "nvdb_leaf_finalize_counted", "nvdb_scatter_f32_counted",
-    "nvdb_query_finalize_counted", "nvdb_trainer_packed",
+    "nvdb_query_finalize_counted", "nvdb_trainer_packed", "nvdb_nvgr_leaf_records", "nvdb_nvgr_l1_records",
 ]
 
 SRC_NORM_F32, SRC_CENTER_F64, SRC_COORD_I32, SRC_LEAF_VOX, SRC_L1_SLOT = range(5)
@@ -136,6 +136,8 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_fbm_leaves": (C.c_int, [C.POINTER(FbmDesc), vp, i64, vp, vp, vp, vp]),
         "nvdb_trainer_phase": (C.c_int, [vp, i32, vp]),
         "nvdb_trainer_packed": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(i64)]),
+        "nvdb_nvgr_leaf_records": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
+        "nvdb_nvgr_l1_records": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
         "nvdb_trainer_buffers": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(C.c_void_p)]),
     }
     for name, (res, args) in sig.items():

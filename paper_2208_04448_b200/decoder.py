@@ -582,6 +582,87 @@ class DeviceDecode:
             l1_tiles=tiles[order], leaf_origins=lo if ident else lo[leaf_perm],
             leaf_active=la if ident else la[leaf_perm], leaf_values=lv if ident else lv[leaf_perm])
 
+    def to_nvgr(self) -> bytes:
+        """The decoded grid as NVGR bytes, identical to
+        ``gridfile.serialize_grid(decode_full(c))`` (gridfile.py:43-76).
+
+        The level-1 node and leaf records -- all but a few hundred bytes per
+        root entry -- are written on the device straight from the dense-leaf
+        output (``nvdb_nvgr_l1_records`` / ``nvdb_nvgr_leaf_records``) and come
+        back in one copy; the host adds the header, the root entries and the
+        level-2 node blocks from the container's upper tree."""
+        import struct
+        if self.shard is not None and self.shard[1] > 1:
+            raise ValueError("a sharded decode holds a leaf range, not a grid; gather the shards first")
+        self.check()
+        m = self.model
+        c = m.c
+        meta = c.grid_meta
+        ut = c.upper_tree
+        n1, dev = m.n1, m.dev
+        bg = np.float32(meta.background)
+        L2REC, L1REC, LEAFREC = 4096 + 4096 + 4 * L2_SIZE, 12 + 512 + 512 + 4 * L1_SIZE, 12 + 64 + 4 * LEAF_SIZE
+        cnt = (self.l1_class.view(max(n1, 0), L1_SIZE) == 0).sum(dim=1) if n1 else torch.zeros(0, device=dev)
+        cnt = cnt.to(torch.int64).cpu().numpy()
+        org = m.origins  # decode node order (sorted origins)
+        roots = org & ~np.int64(4095)
+        l2 = {tuple(int(v) for v in nd.origin): nd for nd in ut.l2_nodes}
+        keys = sorted(set(l2) | set(ut.root_tiles))
+        # level-1 nodes per root in NVGR order (ascending idx2 == ascending origin in a root)
+        by_root: Dict[tuple, list] = {}
+        for i, r in enumerate(map(tuple, roots.tolist())):
+            by_root.setdefault(r, []).append(i)
+        off = 4 + 4 + 1 + 4 + 8 + 4 + 8
+        l1_off = np.zeros(n1, np.int64)
+        host_parts = []  # (offset, bytes)
+        header = b"NVGR" + struct.pack("<IBfdfQ", 1, 0 if meta.grid_class == "sdf" else 1, float(bg),
+                                       float(meta.voxel_size), float(np.float32(meta.half_width)), len(keys))
+        host_parts.append((0, header))
+        for key in keys:
+            tile = ut.root_tiles.get(key)
+            if tile is not None:
+                host_parts.append((off, struct.pack("<iiiBfB", *key, 1, float(tile[0]), int(bool(tile[1])))))
+                off += 13 + 5
+                continue
+            nd = l2[key]
+            tiles = np.full(L2_SIZE, bg, np.float32)
+            if nd.tiles:
+                tiles[np.fromiter(nd.tiles.keys(), np.int64, len(nd.tiles))] = np.fromiter(
+                    nd.tiles.values(), np.float32, len(nd.tiles))
+            blob = (struct.pack("<iiiB", *key, 0)
+                    + np.packbits(np.asarray(nd.child_mask.bits, bool), bitorder="little").tobytes()
+                    + np.packbits(np.asarray(nd.active_mask.bits, bool), bitorder="little").tobytes()
+                    + tiles.tobytes())
+            host_parts.append((off, blob))
+            off += 13 + L2REC
+            mine = by_root.get(key, [])
+            if mine:
+                sizes = L1REC + cnt[mine] * LEAFREC
+                l1_off[mine] = off + np.concatenate([[0], np.cumsum(sizes)[:-1]])
+                off += int(sizes.sum())
+        total = off
+        out = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
+        st = _stream(dev)
+        nl = self.leaf_count
+        if n1:
+            d_l1 = torch.from_numpy(l1_off).to(dev)
+            check(lib().nvdb_nvgr_l1_records(_ptr(m.d_origins), _ptr(self.l1_class), _ptr(self.l1_tiles), n1,
+                                             _ptr(d_l1), _ptr(out), st), "nvdb_nvgr_l1_records")
+        if nl:
+            # leaf j of node i (decode order, node-contiguous): l1_off[i] + L1REC + (j - first_i) * LEAFREC
+            node = torch.repeat_interleave(torch.arange(n1, device=dev), torch.from_numpy(cnt).to(dev))
+            first = torch.from_numpy(np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)).to(dev)
+            j = torch.arange(nl, device=dev)
+            leaf_off = d_l1[node] + L1REC + (j - first[node]) * LEAFREC
+            check(lib().nvdb_nvgr_leaf_records(_ptr(self.leaf_origins), _ptr(self.active_words),
+                                               _ptr(self.leaf_values), nl, _ptr(leaf_off), _ptr(out), st),
+                  "nvdb_nvgr_leaf_records")
+        (host,) = _to_host([out[:total]])
+        buf = bytearray(host.tobytes())
+        for o, b in host_parts:
+            buf[o:o + len(b)] = b
+        return bytes(buf)
+
     def tree(self) -> DeviceTree:
         """Device tree over this decode (hybrid topology for random access)."""
         return DeviceTree.from_decode(self)
@@ -626,6 +707,21 @@ def gather_rows(parts, group=None, dst: int = 0):
 
 def _as_model(c, device=None) -> DeviceModel:
     return c if isinstance(c, DeviceModel) else DeviceModel(c, device)
+
+
+def decode_nvgr(c, device=None, group=None) -> Optional[bytes]:
+    """``gridfile.serialize_grid(decoder.decode_full(c))`` (decoder.py:214,
+    gridfile.py:43-76) with the records emitted on the device: the decoded
+    grid as NVGR bytes, no per-node host objects.  With a process group the
+    decode is sharded and rank 0 returns the bytes (None elsewhere)."""
+    m = _as_model(c, device)
+    if group is not None and _world(group) > 1:
+        d = decode_sharded(m, group)
+        if d is None:
+            return None
+    else:
+        d = m.decode(True)
+    return d.to_nvgr()
 
 
 def decode_sharded(m: DeviceModel, group=None, dst: int = 0) -> Optional["DeviceDecode"]:

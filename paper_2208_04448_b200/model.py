@@ -162,6 +162,16 @@ class Mask:
     def __init__(self, bits):
         self.bits = np.asarray(bits, dtype=bool)
 
+    def indices(self) -> np.ndarray:
+        return np.flatnonzero(self.bits)
+
+    def count(self) -> int:
+        return int(np.count_nonzero(self.bits))
+
+    def packed_words(self) -> bytes:
+        """grid.py:167-169: little-endian packed bits (container serialization)."""
+        return np.packbits(self.bits, bitorder="little").tobytes()
+
 
 @dataclass
 class GridMeta:
@@ -515,36 +525,65 @@ class DenseLeafGrid:
         )
 
     def to_svcodec(self):
-        """Rebuild an svcodec ``VdbGrid`` (requires the reference package)."""
-        from svcodec.grid import InternalNode, LeafNode, VdbGrid  # noqa: WPS433
+        """Rebuild an svcodec ``VdbGrid`` (requires the reference package).
+
+        Vectorized assembly (decoder.py:197-210): node
+        masks, tiles and leaf values are row views of this grid's dense
+        arrays (copied once into contiguous blocks owned by the new grid), and
+        the node objects are created without their constructors' per-node
+        ``np.full`` / mask allocation, so the host cost is one small object
+        per node instead of three 512- to 32768-element array allocations."""
+        from svcodec.grid import InternalNode, LeafNode, NodeMask, VdbGrid  # noqa: WPS433
         g = VdbGrid(self.background, self.grid_class, self.voxel_size, self.half_width)
         g.root_tiles = dict(self.root_tiles)
-        l1_by_origin = {}
-        for ni in range(self.l2_origins.shape[0]):
-            key = tuple(int(v) for v in self.l2_origins[ni])
-            n2 = InternalNode(key, L2_LOG2, self.background)
-            n2.child_mask.bits[:] = self.l2_child[ni]
-            n2.active_mask.bits[:] = self.l2_active[ni]
-            n2.tiles[:] = self.l2_tiles[ni]
-            g.root[key] = n2
-        for ni in range(self.l1_origins.shape[0]):
-            org = tuple(int(v) for v in self.l1_origins[ni])
-            n1 = InternalNode(org, L1_LOG2, self.background)
-            n1.child_mask.bits[:] = self.l1_child[ni]
-            n1.active_mask.bits[:] = self.l1_active[ni]
-            n1.tiles[:] = self.l1_tiles[ni]
-            root = tuple(v & ~(L2_SPAN - 1) for v in org)
-            idx2 = (((org[0] & 4095) >> 7) << 10) | (((org[1] & 4095) >> 7) << 5) | ((org[2] & 4095) >> 7)
-            g.root[root].children[idx2] = n1
-            l1_by_origin[org] = n1
-        for li in range(self.leaf_origins.shape[0]):
-            org = tuple(int(v) for v in self.leaf_origins[li])
-            leaf = LeafNode(org, self.background)
-            leaf.active.bits[:] = self.leaf_active[li]
-            leaf.values[:] = self.leaf_values[li]
-            parent = tuple(v & ~(L1_SPAN - 1) for v in org)
-            idx1 = (((org[0] & 127) >> 3) << 8) | (((org[1] & 127) >> 3) << 4) | ((org[2] & 127) >> 3)
-            l1_by_origin[parent].children[idx1] = leaf
+        new_leaf, new_node, new_mask = LeafNode.__new__, InternalNode.__new__, NodeMask.__new__
+
+        def mask(bits):
+            mk = new_mask(NodeMask)
+            mk.bits = bits
+            return mk
+
+        def node(origin, log2dim, child, active, tiles):
+            n = new_node(InternalNode)
+            n.origin = origin
+            n.log2dim = log2dim
+            n.slot_span = (LEAF_SPAN << log2dim if log2dim == L1_LOG2 else L1_SPAN << log2dim) >> log2dim
+            n.child_mask = mask(child)
+            n.active_mask = mask(active)
+            n.tiles = tiles
+            n.children = {}
+            return n
+
+        n2 = self.l2_origins.shape[0]
+        c2, a2 = np.array(self.l2_child, dtype=bool), np.array(self.l2_active, dtype=bool)
+        t2 = np.array(self.l2_tiles, dtype=np.float32)
+        for ni, key in enumerate(map(tuple, self.l2_origins.tolist())):
+            g.root[key] = node(key, L2_LOG2, c2[ni], a2[ni], t2[ni])
+        n1 = self.l1_origins.shape[0]
+        c1, a1 = np.array(self.l1_child, dtype=bool), np.array(self.l1_active, dtype=bool)
+        t1 = np.array(self.l1_tiles, dtype=np.float32)
+        o1 = self.l1_origins.astype(np.int64)
+        roots1 = map(tuple, (o1 & ~np.int64(L2_SPAN - 1)).tolist())
+        idx2 = ((((o1[:, 0] & 4095) >> 7) << 10) | (((o1[:, 1] & 4095) >> 7) << 5) | ((o1[:, 2] & 4095) >> 7)).tolist()
+        l1_nodes = []
+        for ni, (org, root, k2) in enumerate(zip(map(tuple, o1.tolist()), roots1, idx2)):
+            nd = node(org, L1_LOG2, c1[ni], a1[ni], t1[ni])
+            g.root[root].children[k2] = nd
+            l1_nodes.append(nd)
+        nl = self.leaf_origins.shape[0]
+        if nl:
+            la = np.array(self.leaf_active, dtype=bool).reshape(nl, LEAF_SIZE)
+            lv = np.array(self.leaf_values, dtype=np.float32).reshape(nl, LEAF_SIZE)
+            ol = self.leaf_origins.astype(np.int64)
+            by_origin = dict(zip(map(tuple, o1.tolist()), l1_nodes))
+            parents = map(tuple, (ol & ~np.int64(L1_SPAN - 1)).tolist())
+            idx1 = ((((ol[:, 0] & 127) >> 3) << 8) | (((ol[:, 1] & 127) >> 3) << 4) | ((ol[:, 2] & 127) >> 3)).tolist()
+            for li, (org, par, k1) in enumerate(zip(map(tuple, ol.tolist()), parents, idx1)):
+                leaf = new_leaf(LeafNode)
+                leaf.origin = org
+                leaf.values = lv[li]
+                leaf.active = mask(la[li])
+                by_origin[par].children[k1] = leaf
         return g
 
 

@@ -10,6 +10,15 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# the stock reference package (svcodec) for the drop-in tests: the driver's
+# offline install under baseline/_ref (travels to the GPU box), else the
+# read-only reference tree in the build container; tests needing it skip
+# when neither exists
+for _p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+    if os.path.isdir(os.path.join(_p, "svcodec")) and _p not in sys.path:
+        sys.path.append(_p)
+        break
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")

@@ -185,3 +185,47 @@ def test_decode_report_counts(golden, name):
     assert abs(rep["regressor_evaluations"] - int(z["evals"][0])) <= max(3, int(0.001 * z["evals"][0]))
     assert abs(rep["active_voxels"] - int(ref.leaf_active.sum())) <= max(3, int(0.001 * ref.leaf_active.sum()))
     assert rep["regressor_evaluations"] == rep["active_voxels"]
+
+
+# ---------------------------------------------------------------- NVGR emission
+
+@pytest.mark.parametrize("name", ["decode_small", "decode_multi"])
+def test_nvgr_bytes_equal_serialize_grid(golden, name):
+    """DeviceDecode.to_nvgr (records written on the device) is byte-identical
+    to the reference's gridfile.serialize_grid of the same decoded grid, and
+    deserializes back to it (gridfile.py:43-76, 79-140)."""
+    gridfile = pytest.importorskip("svcodec.gridfile")
+    from paper_2208_04448_b200.decoder import decode_nvgr
+    from paper_2208_04448_b200.model import DenseLeafGrid
+    c = container_from_arrays(golden(name))
+    m = DeviceModel(c)
+    d = m.decode(True)
+    g = d.to_grid()
+    ref = gridfile.serialize_grid(g.to_svcodec())
+    got = d.to_nvgr()
+    assert len(got) == len(ref)
+    assert got == ref
+    assert decode_nvgr(c) == ref
+    back = DenseLeafGrid.from_svcodec(gridfile.deserialize_grid(got))
+    for f in ("leaf_origins", "leaf_active", "leaf_values", "l1_origins", "l1_child", "l1_tiles"):
+        np.testing.assert_array_equal(getattr(back, f), getattr(g, f))
+    m.close()
+
+
+def test_nvgr_root_tiles_and_negative_coordinates():
+    """A grid spanning several root entries (negative coordinates, a root
+    tile, level-1 nodes in different level-2 nodes): NVGR order is root key
+    then idx2, not the decode's sorted-origin order."""
+    gridfile = pytest.importorskip("svcodec.gridfile")
+    from paper_2208_04448_b200.encoder import encode
+    from paper_2208_04448_b200.procgen import sphere_sdf
+    from helpers import tiny_cfg
+    a = sphere_sdf((-4.0, 4090.0, 10.0), 9.0, 1.0, 3.0)  # straddles x = 0 and y = 4096 root boundaries
+    c = encode(a, tiny_cfg(max_epochs=20), device="cuda:0")
+    c.upper_tree.root_tiles[(8192, 0, 0)] = (-3.0, False)
+    m = DeviceModel(c)
+    d = m.decode(True)
+    g = d.to_grid()
+    assert len({tuple(int(v) & ~4095 for v in o) for o in g.l1_origins}) >= 3
+    assert d.to_nvgr() == gridfile.serialize_grid(g.to_svcodec())
+    m.close()

@@ -360,39 +360,147 @@ def cpu_train_sample(c, cfg, steps=3):
     return steps * cfg.batch_size / dt, dt
 
 
+def _import_svcodec():
+    """The stock reference package: the driver's offline install under
+    baseline/_ref (or the reference tree in the build container)."""
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "svcodec")) and p not in sys.path:
+            sys.path.append(p)
+            break
+    try:
+        import svcodec  # noqa: F401
+        return True
+    except Exception:  # noqa: BLE001
+        return False
+
+
+def restrict_container(c, nodes: int):
+    """A copy of an svcodec container holding only its first `nodes` level-1
+    nodes (sorted-origin order = the reference's decode order,
+    decoder.py:71): level-2 child bits, tile records, negative fills and
+    patches restricted to them.  Input preparation for a bounded sample; the
+    decode that runs on it is svcodec's own, unmodified."""
+    import copy
+    ut = c.upper_tree
+    keep = sorted(tuple(o) for o in ut.l1_origins)[:nodes]
+    ks = set(keep)
+    out = copy.copy(c)
+    nut = copy.copy(ut)
+    nut.l1_origins = list(keep)
+    nut.l1_tiles = {o: t for o, t in ut.l1_tiles.items() if tuple(o) in ks}
+    nut.leaf_negative_fill = {o: b for o, b in ut.leaf_negative_fill.items()
+                              if tuple(v & ~127 for v in o) in ks}
+    nodes2 = []
+    for nd in ut.l2_nodes:
+        n2 = copy.deepcopy(nd)
+        bits = np.zeros_like(np.asarray(n2.child_mask.bits))
+        for o in keep:
+            if tuple(v & ~4095 for v in o) == tuple(nd.origin):
+                bits[(((o[0] & 4095) >> 7) << 10) | (((o[1] & 4095) >> 7) << 5) | ((o[2] & 4095) >> 7)] = True
+        n2.child_mask.bits[:] = bits
+        nodes2.append(n2)
+    nut.l2_nodes = nodes2
+    out.upper_tree = nut
+    exps = []
+    for e in c.experts:
+        e2 = copy.copy(e)
+        p = copy.copy(e.patches)
+        p.l1 = [(o, k) for o, k in e.patches.l1 if tuple(v & ~127 for v in o) in ks]
+        p.l0 = [(o, a, v) for o, a, v in e.patches.l0 if tuple(w & ~127 for w in o) in ks]
+        e2.patches = p
+        exps.append(e2)
+    out.experts = exps
+    return out
+
+
+def reference_decode_sample(workload, nodes=None):
+    """Stock svcodec (baseline/_ref): read_container of the workload's
+    container fixture, restricted to its first level-1 nodes, then the
+    reference's own decode_full.  Returns (voxels/s, leaf voxels, s, active)."""
+    from svcodec.container import read_container
+    from svcodec.decoder import decode_full as ref_decode_full
+    name = "c1_sphere128.nvdb" if workload == "c1" else "c2_torus512.nvdb"
+    c = read_container(os.path.join(ROOT, "tests", "golden", name))
+    sub = restrict_container(c, nodes or (1 if workload == "c1" else 4))
+    t0 = time.perf_counter()
+    g = ref_decode_full(sub)
+    dt = time.perf_counter() - t0
+    nvox = sum(1 for _ in g.iter_leaves()) * 512
+    return nvox / dt, nvox, dt, g.active_voxel_count()
+
+
+def reference_train_sample(workload, steps=3):
+    """Stock svcodec.neural.fused_step (neural.py:444-524) on the container's
+    voxel net, B = 65536, `steps` steps."""
+    from svcodec.container import read_container
+    from svcodec.neural import AdamState, FusedNet, TrainWorkspace, fused_step
+    name = "c1_sphere128.nvdb" if workload == "c1" else "c2_torus512.nvdb"
+    c = read_container(os.path.join(ROOT, "tests", "golden", name))
+    rec = c.experts[0].voxel_regressor
+    params = rec.params.copy()
+    net = FusedNet(params, rec.ff, AdamState(params))
+    ws = TrainWorkspace()
+    rng = np.random.default_rng(0)
+    x = rng.uniform(0.2, 0.8, size=(65536, 3)).astype(np.float32)
+    y = rng.uniform(-1, 1, size=65536).astype(np.float32)
+    fused_step(net, x, y, "mse", np.float32(1e-3), ws)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        fused_step(net, x, y, "mse", np.float32(1e-3), ws)
+    dt = time.perf_counter() - t0
+    return steps * 65536 / dt, dt
+
+
 def run_reference(args, rank, world):
-    """Reference arm: the CPU oracle restatement of svcodec's decode path on the
-    same synthetic workload (bounded sample per step), all host cores."""
+    """Reference arm: the UNMODIFIED svcodec (baseline/_ref) decoding a bounded
+    sample of the same workload's container on the host cores (all of them:
+    OpenBLAS default threading); rank 0 only.  Falls back to the numpy
+    oracle port when the reference package is not installed."""
     if rank != 0:
         return
-    cfg = accept_config()
-    c = _reference_container(args.workload, cfg)
     steps, warm = min(args.steps, 3), min(args.warmup, 1)
-    for _ in range(warm):
-        cpu_decode_sample(c)
-    vals = []
-    for _ in range(steps):
-        v, nvox, dt, nact = cpu_decode_sample(c)
-        vals.append(v)
+    if _import_svcodec():
+        kind = "reference"
+        for _ in range(warm):
+            reference_decode_sample(args.workload)
+        vals = []
+        for _ in range(steps):
+            v, nvox, dt, nact = reference_decode_sample(args.workload)
+            vals.append(v)
+        tv, tdt = reference_train_sample(args.workload)
+        sample = (f"svcodec.decoder.decode_full (stock, baseline/_ref) of the workload's container restricted to "
+                  f"its first level-1 nodes: {nvox} leaf voxels, {nact} active, per step")
+        tsample = f"3 svcodec.neural.fused_step of the voxel net, B=65536 ({tdt:.1f} s)"
+    else:
+        kind = "port"
+        cfg = accept_config()
+        c = _reference_container(args.workload, cfg)
+        for _ in range(warm):
+            cpu_decode_sample(c)
+        vals = []
+        for _ in range(steps):
+            v, nvox, dt, nact = cpu_decode_sample(c)
+            vals.append(v)
+        tv, tdt = cpu_train_sample(c, cfg)
+        sample = (f"{nvox} leaf voxels of the first decoded leaves per step (L0 classify + voxel regress on "
+                  f"{nact} active), numpy/OpenBLAS oracle port (svcodec not installed)")
+        tsample = f"3 oracle fused_steps of the voxel net, B=65536 ({tdt:.1f} s)"
     val = statistics.median(vals)
-    tv, tdt = cpu_train_sample(c, cfg)
     line = {"metric": "decoded voxels/s", "value": val, "unit": "voxels/s", "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": 1e3 * nvox / val, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-            "config": _config(args.workload),
-            "cpu_baseline": {"value": val, "unit": "voxels/s", "cores": os.cpu_count(), "kind": "port",
-                             "sample": f"{nvox} leaf voxels of the first decoded leaves per step (L0 classify "
-                                       f"+ voxel regress on {nact} active), numpy/OpenBLAS oracle"},
-            "train": {"value": tv, "unit": "samples/s", "sample": f"3 fused_steps of the voxel net, B=65536 "
-                                                                   f"({tdt:.1f} s)"},
+            "config": dict(_config(args.workload), same_config=kind == "reference"),
+            "cpu_baseline": {"value": val, "unit": "voxels/s", "cores": os.cpu_count(), "kind": kind,
+                             "sample": sample},
+            "train": {"value": tv, "unit": "samples/s", "sample": tsample},
             "e2e": {"value": val, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def _reference_container(workload, cfg):
-    """The container the reference arm decodes: always the committed C1 fixture
-    (the reference's own AC4 encode, tests/golden/c1_sphere128.npz), whatever
-    the workload."""
+    """The container the oracle-port fallback decodes: the committed C1
+    fixture (the reference's own AC4 encode, tests/golden/c1_sphere128.npz);
+    used only when svcodec itself is not installed."""
     from paper_2208_04448_b200.model import container_from_arrays
     z = np.load(os.path.join(ROOT, "tests", "golden", "c1_sphere128.npz"))
     return container_from_arrays(z)
@@ -605,13 +713,23 @@ def main():
     d2h = (nvox // 512) * (512 * 4 + 512 + 12) + m.n1 * 4096 * 6
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, nv, dt, na = cpu_decode_sample(c)
-        tv, tdt = cpu_train_sample(c, cfg)
-        cpu = {"value": v, "unit": "voxels/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"oracle decode of the first {nv // 512} decoded leaves ({nv} leaf voxels: L0 classify "
-                         f"+ voxel regress of {na} active), numpy/OpenBLAS, {dt:.1f} s",
-               "train": {"value": tv, "unit": "samples/s",
-                         "sample": f"3 oracle fused_steps, voxel net, B=65536, {tdt:.1f} s"}}
+        if _import_svcodec():  # the stock reference on this box's host cores
+            v, nv, dt, na = reference_decode_sample(args.workload)
+            tv, tdt = reference_train_sample(args.workload)
+            cpu = {"value": v, "unit": "voxels/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"svcodec.decoder.decode_full (stock, baseline/_ref) of this workload's container "
+                             f"(tests/golden, trained by this arm's encode) restricted to its first level-1 "
+                             f"nodes: {nv} leaf voxels, {na} active, {dt:.1f} s",
+                   "train": {"value": tv, "unit": "samples/s",
+                             "sample": f"3 svcodec.neural.fused_step, voxel net, B=65536, {tdt:.1f} s"}}
+        else:
+            v, nv, dt, na = cpu_decode_sample(c)
+            tv, tdt = cpu_train_sample(c, cfg)
+            cpu = {"value": v, "unit": "voxels/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"oracle decode of the first {nv // 512} decoded leaves ({nv} leaf voxels: L0 classify "
+                             f"+ voxel regress of {na} active), numpy/OpenBLAS, {dt:.1f} s",
+                   "train": {"value": tv, "unit": "samples/s",
+                             "sample": f"3 oracle fused_steps, voxel net, B=65536, {tdt:.1f} s"}}
     if rank == 0:
         line = {
             "metric": "decoded voxels/s", "value": value, "unit": "voxels/s", "n_gpus": world,

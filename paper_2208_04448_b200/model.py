@@ -426,6 +426,17 @@ class NeuralGridContainer:
     config: object = None
     weight_precision: int = 32
 
+    def payload_bytes(self) -> int:
+        """container.py:167-169 (svcodec's own payload builder)."""
+        from svcodec.container import _build_payload  # noqa: WPS433
+        return len(_build_payload(self))
+
+    def parameter_count(self) -> int:
+        return sum(n.params.parameter_count() for e in self.experts for _, n in e.nets() if n is not None)
+
+    def patch_count(self) -> int:
+        return sum(len(e.patches) for e in self.experts)
+
 
 # -- explicit grid ----------------------------------------------------------------
 

@@ -41,29 +41,28 @@ def leaf_keys(o):
     return (o[:, 0] << 42) | (o[:, 1] << 21) | o[:, 2]
 
 
-def main():
-    size = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
-    epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 2500
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    group = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        group = dist.group.WORLD
+def run(size: int, epochs: int, dev, group=None) -> dict:
+    """The whole C3 pipeline on this rank's GPU (all ranks of `group` call it);
+    returns the result dict (times are max over ranks)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if group is not None else 1
+    rank = dist.get_rank(group) if group is not None else 0
     cfg = SimpleNamespace(**dict(CHAMELEON, max_epochs=epochs))
     t0 = time.perf_counter()
     g = fbm_density(octaves=5, lacunarity=2.0, gain=0.5, base_frequency=4.0 / 1024.0, seed=9,
                     domain=((0, 0, 0), (size, size, size)), threshold=0.45, device=dev)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
+    if world > 1:
+        dist.barrier(group)
     t0 = time.perf_counter()
     c = encode(g, cfg, 16, device=dev, group=group)
     torch.cuda.synchronize()
     t_enc = time.perf_counter() - t0
+    if world > 1:
+        te = torch.tensor([t_enc], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX, group=group)
+        t_enc = float(te.item())
     m = DeviceModel(c, dev)
     shard = (rank, world) if world > 1 else None
     d = m.decode(True, shard=shard)  # warm
@@ -73,7 +72,7 @@ def main():
     for _ in range(3):
         flush.random_(0, 255)
         if world > 1:
-            dist.barrier()
+            dist.barrier(group)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         d = m.decode(True, shard=shard)
@@ -84,8 +83,8 @@ def main():
     cnt = torch.tensor([d.leaf_count * 512, d.regressor_evaluations, ms], dtype=torch.float64, device=dev)
     if world > 1:
         mx = cnt[2:].clone()
-        dist.all_reduce(cnt)
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnt, group=group)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
         cnt[2] = mx[0]
     nvox, nact, ms = int(cnt[0].item()), int(cnt[1].item()), float(cnt[2].item())
     # quality: decoded active set vs the input's (FOG: IoU over active voxels), on the device
@@ -105,16 +104,34 @@ def main():
     e = c.experts[0]
     F = {t: fwd_flops(n) for t, n in e.nets() if n is not None}
     epochs_run = {f"{x.id}:{t}": n.epochs for x in c.experts for t, n in x.nets() if n is not None}
-    if rank == 0:
-        print(json.dumps({
+    F_all = (m.n1 * 4096 * F["l1"] + nvox * F["l0"] + nact * F["voxel"])
+    m.close()
+    return {
             "workload": f"C3 fBm {size}^3 (545 M active at 1024^3), 8 experts at S=512, Chameleon nets "
                         f"(L1 3x128/m128, L0+voxel 3x256/m256, {epochs} epochs max), trained by encode()",
             "ranks": world, "generate_s": round(t_gen, 2), "encode_s": round(t_enc, 1),
             "leaf_voxels": nvox, "regressor_evaluations": nact, "l1_slots": m.n1 * 4096,
             "decode_ms": round(ms, 2), "decode_voxels_per_s": nvox / (ms * 1e-3),
-            "decode_tflops": (m.n1 * 4096 * F["l1"] + nvox * F["l0"] + nact * F["voxel"]) / (ms * 1e-3) / 1e12,
+            "decode_tflops": F_all / (ms * 1e-3) / 1e12,
             "iou_active": iou, "patches": sum(len(x.patches) for x in c.experts),
-            "epochs": epochs_run}), flush=True)
+            "epochs": epochs_run}
+
+
+def main():
+    size = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+    epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 2500
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    r = run(size, epochs, dev, group)
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps(r), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

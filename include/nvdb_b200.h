@@ -250,6 +250,21 @@ NVDB_API int nvdb_nvgr_leaf_records(const int32_t* leaf_origins, const uint64_t*
 NVDB_API int nvdb_nvgr_l1_records(const int32_t* node_origins, const uint8_t* l1_class, const float* tiles,
                                   int64_t nnodes, const int64_t* rec_off, uint8_t* out, void* stream);
 
+/* -- verification metrics (metrics.py:116-230) --------- */
+/* One pass of grid A against grid B: enumerates A's leaf voxels (origins in
+ * A's tree order, DEVICE int32 (nl,3)) and A's tile extents (host-compacted
+ * list: origin, extent 8|128, value, active, prefix of extent^3 (ntiles+1);
+ * DEVICE), resolving each coordinate in B.  Adds 8 double sums per block to
+ * `partials` (nvdb_metric_partials() blocks x 8, DEVICE, zeroed here):
+ * |act A|, |act A & act B|, |occ A|, |occ A & occ B|, sum over act A & act B
+ * of (vA - vB)^2, sum over act A & !act B of (vA - bg_B)^2, surface points
+ * of A, sum of |trilinear_B| at them (want_mcd != 0). */
+NVDB_API size_t nvdb_metric_partials(void);
+NVDB_API int nvdb_metric_pass(const nvdb_tree* a, const int32_t* a_leaf_origins, const nvdb_tree* b,
+                              const int32_t* tile_origin, const int32_t* tile_extent, const float* tile_value,
+                              const uint8_t* tile_active, const int64_t* tile_first, int64_t ntiles, int32_t sdf,
+                              int32_t want_mcd, double* partials, void* stream);
+
 /* -- training (encoder.train_network, encoder.py:330-371) -------------------- */
 
 #define NVDB_LOSS_MSE 0

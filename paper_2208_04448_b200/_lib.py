@@ -35,6 +35,7 @@ EXPORTED = [
     "nvdb_trainer_buffers", "nvdb_sample_indices_subset", "nvdb_fbm_leaves", "nvdb_trim",
     "nvdb_eval_counted", "nvdb_leaf_finalize_counted", "nvdb_scatter_f32_counted",
     "nvdb_query_finalize_counted", "nvdb_trainer_packed", "nvdb_nvgr_leaf_records", "nvdb_nvgr_l1_records",
+    "nvdb_metric_partials", "nvdb_metric_pass",
 ]
 
 SRC_NORM_F32, SRC_CENTER_F64, SRC_COORD_I32, SRC_LEAF_VOX, SRC_L1_SLOT = range(5)
@@ -138,6 +139,8 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_trainer_packed": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(i64)]),
         "nvdb_nvgr_leaf_records": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
         "nvdb_nvgr_l1_records": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
+        "nvdb_metric_partials": (sz, []),
+        "nvdb_metric_pass": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, i32, i32, vp, vp]),
         "nvdb_trainer_buffers": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(C.c_void_p)]),
     }
     for name, (res, args) in sig.items():

@@ -17,67 +17,79 @@ using namespace nvdb;
 
 namespace {
 
-__device__ __forceinline__ int cmp3(const int32_t* k, int x, int y, int z) {
-  if (k[0] != x) return k[0] < x ? -1 : 1;
-  if (k[1] != y) return k[1] < y ? -1 : 1;
-  if (k[2] != z) return k[2] < z ? -1 : 1;
-  return 0;
-}
-
+// Four queries per thread: three 16-byte coordinate loads (the thread's 48
+// contiguous bytes), four independent traversals in flight, then one 16-byte
+// value store, one 4-byte active store and one 4-byte kind store.
 __global__ void k_lookup(TreeView t, const int32_t* __restrict__ coords, int64_t n, float* __restrict__ value,
                          uint8_t* __restrict__ active, uint8_t* __restrict__ kind, int32_t* __restrict__ leaf_out) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int x = __ldg(coords + 3 * i), y = __ldg(coords + 3 * i + 1), z = __ldg(coords + 3 * i + 2);
-    float v = t.background;
-    uint8_t a = 0, k = 0;
-    int32_t leaf = -1;
-    // root: two's-complement masking (grid.py:74-94)
-    const int rx = x & ~4095, ry = y & ~4095, rz = z & ~4095;
-    int lo = 0, hi = t.nroots - 1, r = -1;
-    while (lo <= hi) {
-      const int mid = (lo + hi) >> 1;
-      const int c = cmp3(t.root_keys + 3 * mid, rx, ry, rz);
-      if (c == 0) { r = mid; break; }
-      if (c < 0) lo = mid + 1; else hi = mid - 1;
-    }
-    if (r >= 0) {
-      const int n2 = t.root_l2[r];
-      if (n2 < 0) {
-        v = t.root_tile_value[r];
-        a = t.root_tile_active[r];
-        k = 1;
-      } else {
-        const int i2 = (((x & 4095) >> 7) << 10) | (((y & 4095) >> 7) << 5) | ((z & 4095) >> 7);
-        const int64_t s2 = (int64_t)n2 * 32768 + i2;
-        const int n1 = __ldg(t.l2_slot + s2);
-        if (n1 < 0) {
-          v = __ldg(t.l2_tiles + s2);
-          a = (__ldg(reinterpret_cast<const unsigned long long*>(t.l2_active) + (s2 >> 6)) >> (i2 & 63)) & 1ull;
-          k = 1;
-        } else {
-          const int i1 = (((x & 127) >> 3) << 8) | (((y & 127) >> 3) << 4) | ((z & 127) >> 3);
-          const int64_t s1 = (int64_t)n1 * 4096 + i1;
-          leaf = __ldg(t.l1_slot + s1);
-          if (leaf < 0) {
-            v = __ldg(t.l1_tiles + s1);
-            a = (__ldg(reinterpret_cast<const unsigned long long*>(t.l1_active) + (s1 >> 6)) >> (i1 & 63)) & 1ull;
-            k = 1;
-          } else {
-            const int i0 = ((x & 7) << 6) | ((y & 7) << 3) | (z & 7);
-            v = __ldg(t.leaf_values + (int64_t)leaf * 512 + i0);
-            a = (__ldg(reinterpret_cast<const unsigned long long*>(t.leaf_active) + (int64_t)leaf * 8 + (i0 >> 6)) >>
-                 (i0 & 63)) & 1ull;
-            k = 2;
-          }
-        }
-      }
-    }
+  const int64_t nq4 = n >> 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq4; q += stride) {
+    const int4* cp = reinterpret_cast<const int4*>(coords + 12 * q);
+    const int4 c0 = __ldcs(cp), c1 = __ldcs(cp + 1), c2 = __ldcs(cp + 2);
+    const int xs[4] = {c0.x, c0.w, c1.z, c2.y}, ys[4] = {c0.y, c1.x, c1.w, c2.z}, zs[4] = {c0.z, c1.y, c2.x, c2.w};
+    float v[4];
+    uint8_t a[4], k[4];
+    int32_t lf[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tree_resolve(t, xs[j], ys[j], zs[j], v[j], a[j], k[j], lf[j]);
+    __stcs(reinterpret_cast<float4*>(value) + q, make_float4(v[0], v[1], v[2], v[3]));
+    __stcs(reinterpret_cast<unsigned int*>(active) + q,
+           (uint32_t)a[0] | ((uint32_t)a[1] << 8) | ((uint32_t)a[2] << 16) | ((uint32_t)a[3] << 24));
+    __stcs(reinterpret_cast<unsigned int*>(kind) + q,
+           (uint32_t)k[0] | ((uint32_t)k[1] << 8) | ((uint32_t)k[2] << 16) | ((uint32_t)k[3] << 24));
+    if (leaf_out) __stcs(reinterpret_cast<int4*>(leaf_out) + q, make_int4(lf[0], lf[1], lf[2], lf[3]));
+  }
+  // tail (n % 4 rows)
+  const int64_t i = 4 * nq4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    float v;
+    uint8_t a, k;
+    int32_t lf;
+    tree_resolve(t, coords[3 * i], coords[3 * i + 1], coords[3 * i + 2], v, a, k, lf);
     value[i] = v;
     active[i] = a;
     kind[i] = k;
-    if (leaf_out) leaf_out[i] = leaf;
+    if (leaf_out) leaf_out[i] = lf;
   }
+}
+
+// scalar form for buffers that are not 16-byte aligned
+__global__ void k_lookup1(TreeView t, const int32_t* __restrict__ coords, int64_t n, float* __restrict__ value,
+                          uint8_t* __restrict__ active, uint8_t* __restrict__ kind, int32_t* __restrict__ leaf_out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    float v;
+    uint8_t a, k;
+    int32_t lf;
+    tree_resolve(t, __ldg(coords + 3 * i), __ldg(coords + 3 * i + 1), __ldg(coords + 3 * i + 2), v, a, k, lf);
+    value[i] = v;
+    active[i] = a;
+    kind[i] = k;
+    if (leaf_out) leaf_out[i] = lf;
+  }
+}
+
+// packed lookup entries of one level: child index, or tile value + active bit
+__global__ void k_pack_level(const int32_t* __restrict__ slot, const float* __restrict__ tiles,
+                             const uint64_t* __restrict__ active, int64_t nslots, uint64_t* __restrict__ ent) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nslots) return;
+  const int32_t c = slot[i];
+  if (c >= 0) {
+    ent[i] = (uint64_t)(uint32_t)c;
+  } else {
+    const uint64_t act = (active[i >> 6] >> (i & 63)) & 1ull;
+    ent[i] = (uint64_t)__float_as_uint(tiles[i]) | (act << 32) | (1ull << kEntKindShift);
+  }
+}
+
+__global__ void k_pack_leaf(const float* __restrict__ values, const uint64_t* __restrict__ active, int64_t nvox,
+                            uint64_t* __restrict__ ent) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nvox) return;
+  const uint64_t act = (active[i >> 6] >> (i & 63)) & 1ull;
+  ent[i] = (uint64_t)__float_as_uint(values[i]) | (act << 32) | (2ull << kEntKindShift);
 }
 
 // slot -> child index (node base + set child bits before the slot), -1 for a tile slot
@@ -138,6 +150,21 @@ int tree_build_prefix(nvdb_tree* t, cudaStream_t st) {
                                                            t->l1_slot);
     NVDB_CHECK_LAUNCH();
   }
+  if (t->n2 > 0) {
+    const int64_t ns = (int64_t)t->n2 * 32768;
+    k_pack_level<<<(int)((ns + 255) / 256), 256, 0, st>>>(t->l2_slot, t->l2_tiles, t->l2_active, ns, t->l2_ent);
+    NVDB_CHECK_LAUNCH();
+  }
+  if (t->n1 > 0) {
+    const int64_t ns = (int64_t)t->n1 * 4096;
+    k_pack_level<<<(int)((ns + 255) / 256), 256, 0, st>>>(t->l1_slot, t->l1_tiles, t->l1_active, ns, t->l1_ent);
+    NVDB_CHECK_LAUNCH();
+  }
+  if (t->nl > 0) {
+    const int64_t nv = (int64_t)t->nl * 512;
+    k_pack_leaf<<<(int)((nv + 255) / 256), 256, 0, st>>>(t->leaf_values, t->leaf_active, nv, t->leaf_ent);
+    NVDB_CHECK_LAUNCH();
+  }
   return NVDB_OK;
 }
 
@@ -145,9 +172,18 @@ int launch_lookup(const nvdb_tree* t, const int32_t* coords, int64_t n, float* v
                   int32_t* leaf, cudaStream_t st) {
   if (n <= 0) return NVDB_OK;
   const int threads = 256;
-  const int64_t want = (n + threads - 1) / threads;
-  const int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * 16);
-  k_lookup<<<blocks, threads, 0, st>>>(view_of(t), coords, n, value, active, kind, leaf);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(coords) | reinterpret_cast<uintptr_t>(value) |
+                         reinterpret_cast<uintptr_t>(leaf)) & 15) == 0 &&
+                       ((reinterpret_cast<uintptr_t>(active) | reinterpret_cast<uintptr_t>(kind)) & 3) == 0;
+  if (aligned) {
+    const int64_t want = (std::max<int64_t>(n / 4, 1) + threads - 1) / threads;
+    const int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * 16);
+    k_lookup<<<blocks, threads, 0, st>>>(view_of(t), coords, n, value, active, kind, leaf);
+  } else {
+    const int64_t want = (n + threads - 1) / threads;
+    const int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * 16);
+    k_lookup1<<<blocks, threads, 0, st>>>(view_of(t), coords, n, value, active, kind, leaf);
+  }
   NVDB_CHECK_LAUNCH();
   return NVDB_OK;
 }
@@ -193,6 +229,9 @@ extern "C" int nvdb_tree_create(const nvdb_tree_desc* d, nvdb_tree** out) {
   chk(upload(t, &t->leaf_active, d->leaf_active, (size_t)8 * d->nl));
   chk(upload(t, &t->leaf_values, d->leaf_values, (size_t)512 * d->nl));
   if (d->leaf_patched) chk(upload(t, &t->leaf_patched, d->leaf_patched, (size_t)8 * d->nl));
+  chk(upload(t, &t->l2_ent, (const uint64_t*)nullptr, (size_t)32768 * d->n2));
+  chk(upload(t, &t->l1_ent, (const uint64_t*)nullptr, (size_t)4096 * d->n1));
+  chk(upload(t, &t->leaf_ent, (const uint64_t*)nullptr, (size_t)512 * d->nl));
   if (!rc) rc = tree_build_prefix(t, 0);
   if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = fail(NVDB_ECUDA, "tree prefix build failed");
   if (rc) {

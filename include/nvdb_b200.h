@@ -86,6 +86,15 @@ NVDB_API long long nvdb_launch_count(void);
  * inference.eval_net, inference.py:23-26). */
 NVDB_API int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts,
                        int32_t nexperts, int32_t subdomain_size, int32_t halo, nvdb_netset** out);
+/* Device bytes a netset of these nets needs, and its creation inside a
+ * CALLER-OWNED device buffer: packed on the host, uploaded with an async copy
+ * on `stream` (no host synchronisation, no cudaMalloc/cudaFree); destroy then
+ * frees only the host handle.  The buffer must outlive the handle. */
+NVDB_API int nvdb_netset_device_bytes(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts,
+                                      int32_t nexperts, int32_t subdomain_size, int32_t halo, size_t* bytes);
+NVDB_API int nvdb_netset_create_at(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts,
+                                   int32_t nexperts, int32_t subdomain_size, int32_t halo, void* device_mem,
+                                   size_t device_bytes, void* stream, nvdb_netset** out);
 NVDB_API int nvdb_netset_destroy(nvdb_netset* ns);
 
 /* neural.forward_block (neural.py:527-550): raw outputs of net `net` at n
@@ -306,6 +315,12 @@ NVDB_API size_t nvdb_trim(void);
  * after the early stop are no-ops on the device; enqueueing more than
  * max_epochs epochs in total returns NVDB_EINVAL */
 NVDB_API int nvdb_trainer_run(nvdb_trainer* tr, int32_t epochs, void* stream);
+/* Bound the CTAs (one per SM) this trainer's epoch kernels launch with, so
+ * several trainers on separate streams train concurrently on disjoint SMs
+ * (the survey's grouped launch of a container's nets, §7 hard part 4).
+ * 0 = every SM; never more than at creation.  Takes effect at the next
+ * enqueued epoch; the gradient summation order follows the CTA count. */
+NVDB_API int nvdb_trainer_set_ctas(nvdb_trainer* tr, int32_t ctas);
 /* one epoch split for data parallelism: phase 1 = sampler (the first call
  * presamples every epoch), fwd/dgrad, wgrad, partial reduction into the
  * packed buffer; phase 2 = Adam, early stop, epoch advance.  Between them the

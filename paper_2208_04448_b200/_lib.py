@@ -35,7 +35,8 @@ EXPORTED = [
     "nvdb_trainer_buffers", "nvdb_sample_indices_subset", "nvdb_fbm_leaves", "nvdb_trim",
     "nvdb_eval_counted", "nvdb_leaf_finalize_counted", "nvdb_scatter_f32_counted",
     "nvdb_query_finalize_counted", "nvdb_trainer_packed", "nvdb_nvgr_leaf_records", "nvdb_nvgr_l1_records",
-    "nvdb_metric_partials", "nvdb_metric_pass",
+    "nvdb_metric_partials", "nvdb_metric_pass", "nvdb_trainer_set_ctas", "nvdb_netset_device_bytes",
+    "nvdb_netset_create_at",
 ]
 
 SRC_NORM_F32, SRC_CENTER_F64, SRC_COORD_I32, SRC_LEAF_VOX, SRC_L1_SLOT = range(5)
@@ -101,6 +102,10 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_netset_create": (C.c_int, [C.POINTER(NetDesc), i32, C.POINTER(ExpertDesc), i32, i32, i32,
                                          C.POINTER(vp)]),
         "nvdb_netset_destroy": (C.c_int, [vp]),
+        "nvdb_netset_device_bytes": (C.c_int, [C.POINTER(NetDesc), i32, C.POINTER(ExpertDesc), i32, i32, i32,
+                                               C.POINTER(sz)]),
+        "nvdb_netset_create_at": (C.c_int, [C.POINTER(NetDesc), i32, C.POINTER(ExpertDesc), i32, i32, i32, vp, sz,
+                                            vp, C.POINTER(vp)]),
         "nvdb_forward": (C.c_int, [vp, i32, vp, i64, vp, vp]),
         "nvdb_eval_workspace_bytes": (sz, [vp, i64]),
         "nvdb_eval_blended": (C.c_int, [vp, i32, vp, i64, vp, vp, vp, sz, vp]),
@@ -130,6 +135,7 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_trainer_destroy": (C.c_int, [vp]),
         "nvdb_trim": (sz, []),
         "nvdb_trainer_run": (C.c_int, [vp, i32, vp]),
+        "nvdb_trainer_set_ctas": (C.c_int, [vp, i32]),
         "nvdb_trainer_status": (C.c_int, [vp, C.POINTER(i32), C.POINTER(i32), vp, i32]),
         "nvdb_trainer_weights": (C.c_int, [vp, C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.POINTER(C.c_float))]),
         "nvdb_sample_indices": (C.c_int, [C.c_uint64, i64, vp, vp, vp]),

@@ -45,13 +45,18 @@ extern "C" NVDB_API int nvdb_debug_trace(void* buf, uint32_t cap) {
 // ---------------------------------------------------------------------------
 // netset
 // ---------------------------------------------------------------------------
-extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts,
-                                  int32_t nexperts, int32_t subdomain_size, int32_t halo, nvdb_netset** out) {
-  if (!out || (nnets > 0 && !nets) || nexperts < 0 || (nexperts > 0 && !experts))
+// mem == nullptr: the library allocates (cudaMalloc) and uploads synchronously;
+// else the netset lives in the caller's device buffer (`mem_bytes` >= the
+// size nvdb_netset_device_bytes reports) and is uploaded on `st` without a
+// host synchronisation; *need (nullable) receives the device bytes.
+static int netset_create(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts, int32_t nexperts,
+                         int32_t subdomain_size, int32_t halo, void* mem, size_t mem_bytes, cudaStream_t st,
+                         nvdb_netset** out, size_t* need) {
+  if ((!out && !need) || (nnets > 0 && !nets) || nexperts < 0 || (nexperts > 0 && !experts))
     return fail(NVDB_EINVAL, "nvdb_netset_create: null argument");
   if (subdomain_size <= 0 || subdomain_size % 512 || halo <= 0)
     return fail(NVDB_EINVAL, "bad subdomain size %d / halo %d", subdomain_size, halo);
-  *out = nullptr;
+  if (out) *out = nullptr;
   // ---- host packing: one blob, every piece 256-byte aligned
   struct Piece {
     size_t wimg, bias, headw, headb, b2pi, lat;
@@ -108,6 +113,17 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
   if (!plan.ok)
     return fail(NVDB_EUNSUPPORTED, "nets need %u B of shared memory / %d-wide TMEM accumulators; "
                 "weight streaming not built", plan.total, max_width);
+  {
+    auto al0 = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t need_bytes =
+        al0(al0(al0(al0(std::max<size_t>(total, 256)) + sizeof(NetDev) * std::max(nnets, 1)) +
+                sizeof(ExpertDev) * std::max(nexperts, 1)) + sizeof(int32_t) * 3 * std::max(nexperts, 1)) +
+        sizeof(int32_t) * 4 * std::max(nexperts, 1);
+    if (need) *need = need_bytes;
+    if (!out) return NVDB_OK;
+    if (mem && mem_bytes < need_bytes)
+      return fail(NVDB_ENOMEM, "netset needs %zu device bytes, buffer has %zu", need_bytes, mem_bytes);
+  }
   std::vector<uint8_t> blob(std::max<size_t>(total, 256), 0);
   for (int i = 0; i < nnets; ++i) {
     const nvdb_net_desc& d = nets[i];
@@ -201,7 +217,12 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
   const size_t off_cells = al(off_exp + sizeof(ExpertDev) * std::max(nexperts, 1));
   const size_t off_tag = al(off_cells + sizeof(int32_t) * cells.size());
   const size_t all_bytes = off_tag + sizeof(int32_t) * tagnet.size();
-  if (cudaMalloc(&ns->dev_blob, all_bytes) != cudaSuccess) return cleanup(fail(NVDB_ECUDA, "cudaMalloc netset"));
+  if (mem) {
+    ns->dev_blob = static_cast<uint8_t*>(mem);
+    ns->owns_blob = false;
+  } else if (cudaMalloc(&ns->dev_blob, all_bytes) != cudaSuccess) {
+    return cleanup(fail(NVDB_ECUDA, "cudaMalloc netset"));
+  }
   ns->dev_nets = reinterpret_cast<NetDev*>(ns->dev_blob + off_nets);
   ns->dev_experts = reinterpret_cast<ExpertDev*>(ns->dev_blob + off_exp);
   ns->dev_cells = reinterpret_cast<int32_t*>(ns->dev_blob + off_cells);
@@ -219,7 +240,10 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
   if (nexperts) std::memcpy(blob.data() + off_exp, hexp.data(), sizeof(ExpertDev) * nexperts);
   std::memcpy(blob.data() + off_cells, cells.data(), sizeof(int32_t) * cells.size());
   std::memcpy(blob.data() + off_tag, tagnet.data(), sizeof(int32_t) * tagnet.size());
-  if (cudaMemcpy(ns->dev_blob, blob.data(), all_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+  // pageable source: cudaMemcpyAsync returns once the bytes are staged, so the
+  // host vector may go; the upload is ordered on the caller's stream
+  if ((mem ? cudaMemcpyAsync(ns->dev_blob, blob.data(), all_bytes, cudaMemcpyHostToDevice, st)
+           : cudaMemcpy(ns->dev_blob, blob.data(), all_bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
     return cleanup(fail(NVDB_ECUDA, "upload netset"));
   ns->nets = hnets;
   ns->experts = hexp;
@@ -228,9 +252,29 @@ extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, cons
   return NVDB_OK;
 }
 
+extern "C" int nvdb_netset_create(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts,
+                                  int32_t nexperts, int32_t subdomain_size, int32_t halo, nvdb_netset** out) {
+  if (!out) return fail(NVDB_EINVAL, "nvdb_netset_create: null argument");
+  return netset_create(nets, nnets, experts, nexperts, subdomain_size, halo, nullptr, 0, nullptr, out, nullptr);
+}
+
+extern "C" int nvdb_netset_device_bytes(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts,
+                                        int32_t nexperts, int32_t subdomain_size, int32_t halo, size_t* bytes) {
+  if (!bytes) return fail(NVDB_EINVAL, "nvdb_netset_device_bytes: null argument");
+  return netset_create(nets, nnets, experts, nexperts, subdomain_size, halo, nullptr, 0, nullptr, nullptr, bytes);
+}
+
+extern "C" int nvdb_netset_create_at(const nvdb_net_desc* nets, int32_t nnets, const nvdb_expert_desc* experts,
+                                     int32_t nexperts, int32_t subdomain_size, int32_t halo, void* device_mem,
+                                     size_t device_bytes, void* stream, nvdb_netset** out) {
+  if (!out || !device_mem) return fail(NVDB_EINVAL, "nvdb_netset_create_at: null argument");
+  return netset_create(nets, nnets, experts, nexperts, subdomain_size, halo, device_mem, device_bytes,
+                       static_cast<cudaStream_t>(stream), out, nullptr);
+}
+
 extern "C" int nvdb_netset_destroy(nvdb_netset* ns) {
   if (!ns) return NVDB_OK;
-  cudaFree(ns->dev_blob);  // the tables live in the same allocation
+  if (ns->owns_blob) cudaFree(ns->dev_blob);  // the tables live in the same allocation
   delete ns;
   return NVDB_OK;
 }

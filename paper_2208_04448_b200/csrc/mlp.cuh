@@ -199,6 +199,9 @@ constexpr int kSlots = 2;                    // feature chunk slots per engine
 constexpr int kEChunkK = 48;                 // feature K per chunk (3 MMAs of K = 16)
 constexpr int kEChunkBytes = kTileM * kEChunkK * 2;  // 12 KB
 constexpr int kEvalThreads = 128 * kMaxEngines;  // largest block (512)
+#ifndef NVDB_WRING_SLACK
+#define NVDB_WRING_SLACK 1  // refill up to WR - SLACK chunks ahead of the issuer
+#endif
 constexpr int kMaxWRing = 8;                 // weight ring slots per engine (streamed weights)
 
 // ACT: the hidden activation of every net in the launch (a container's nets
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   auto w_next = [&]() {  // slot of this issuer's next chunk, once it landed
     while (true) {
       const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&s_wnext);
-      if (n >= wcons + (uint32_t)WR - 1) break;
+      if (n >= wcons + (uint32_t)WR - NVDB_WRING_SLACK) break;
       if (atomicCAS(&s_wnext, n, n + 1) == n) w_fill_pos(n);
     }
     const uint32_t slot = wcons % (uint32_t)WR;

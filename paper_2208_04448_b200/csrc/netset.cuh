@@ -12,6 +12,7 @@ struct nvdb_netset {
   int nnets = 0, nexperts = 0;
   int subdomain_size = 512, halo = 8;
   uint8_t* dev_blob = nullptr;            // weight images + float params
+  bool owns_blob = true;                  // false: the caller's buffer (nvdb_netset_create_at)
   nvdb::NetDev* dev_nets = nullptr;       // [nnets]
   nvdb::ExpertDev* dev_experts = nullptr; // [nexperts]
   int32_t* dev_cells = nullptr;           // [nexperts][3] sorted lexicographically (= sid order)

@@ -1184,6 +1184,7 @@ struct nvdb_trainer {
   int W = 0, Wr = 0, k0 = 0, depth = 0, out_dim = 0, m = 0;
   int64_t P = 0, batch = 0, ntiles = 0, nraw = 0;
   int fb_grid = 0, wg_grid = 0, nwg = 1;
+  int fb_grid0 = 0, wg_grid0 = 0, nsplit0 = 1;  // creation-time grids (buffers are sized for them)
   NetDev net{};
   uint32_t wg_smem = 0;
   SmemPlan plan{};
@@ -1604,6 +1605,9 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
     if (rc) return rc;
     NVDB_CUDA_TRY(cudaMemcpy(t->blocks, bl.data(), sizeof(LwBlock) * bl.size(), cudaMemcpyHostToDevice));
   }
+  t->fb_grid0 = t->fb_grid;
+  t->wg_grid0 = t->wg_grid;
+  t->nsplit0 = t->nsplit;
   chk(dalloc(t, &t->act_img, (size_t)depth * t->ntiles * tile_elems));
   chk(dalloc(t, &t->dz_img, (size_t)depth * t->ntiles * tile_elems));
   chk(dalloc(t, &t->dlt_img, (size_t)t->ntiles * kTileM * 16));
@@ -1893,6 +1897,21 @@ extern "C" int nvdb_trainer_phase(nvdb_trainer* t, int32_t phase, void* stream) 
   // data-parallel epochs are replayed from a captured graph: presample every
   // epoch in the first phase-1 call so later epochs launch no sampler
   return enqueue_phase(t, phase, static_cast<cudaStream_t>(stream), false, t->d.max_epochs);
+}
+
+extern "C" int nvdb_trainer_set_ctas(nvdb_trainer* t, int32_t ctas) {
+  if (!t || ctas < 0) return fail(NVDB_EINVAL, "nvdb_trainer_set_ctas: bad args");
+  const int c = ctas == 0 ? num_sms() : ctas;
+  t->fb_grid = std::max(1, std::min(t->fb_grid0, c));
+  if (t->wide) {
+    t->nsplit = std::max(1, std::min(t->nsplit0, (c + t->nblocks - 1) / t->nblocks));
+    t->wg_grid = t->nsplit;
+  } else if (t->fb_grid0 == t->wg_grid0) {
+    t->wg_grid = t->fb_grid;  // the fused fwd/bwd + weight-gradient kernel keeps one tile partition
+  } else {
+    t->wg_grid = std::max(1, std::min(t->wg_grid0, c));
+  }
+  return NVDB_OK;
 }
 
 extern "C" int nvdb_trainer_buffers(nvdb_trainer* t, float** grad, int64_t* nparams, double** loss) {

@@ -147,7 +147,7 @@ class NetEvaluator:
         self.dev = _dev(device)
         self.background = float(np.float32(background))
         experts = sorted(experts, key=lambda e: e.id)
-        self.ns = DeviceNetSet(experts, subdomain_size, halo)
+        self.ns = DeviceNetSet(experts, subdomain_size, halo, device=self.dev)
         self.single = len(experts) == 1
         self.has_tag = {t: any(dict(e.nets()).get(t) is not None for e in experts) for t in TAG_CODES}
 
@@ -175,7 +175,7 @@ class DeviceModel:
         self.background = float(np.float32(meta.background))
         self.value_scale = float(meta.value_scale)
         experts = sorted(c.experts, key=lambda e: e.id)
-        self.ns = DeviceNetSet(experts, c.layout.size, c.layout.halo)
+        self.ns = DeviceNetSet(experts, c.layout.size, c.layout.halo, device=self.dev)
         self.single = len(experts) == 1
         self.has_tag = {t: any(dict(e.nets()).get(t) is not None for e in experts) for t in TAG_CODES}
         ut = c.upper_tree

@@ -296,6 +296,7 @@ class DeviceTrainer:
         n = inputs.shape[0]
         self.n = n
         self.max_epochs = int(cfg.max_epochs)
+        self.batch, self.sampled = int(cfg.batch_size), bool(sampled)
         self.x = torch.from_numpy(np.ascontiguousarray(inputs, dtype=np.float32).reshape(-1, 3)).to(self.dev)
         self.y = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.float32).reshape(-1)).to(self.dev)
         E = self.max_epochs
@@ -340,6 +341,15 @@ class DeviceTrainer:
             self.packed = torch.as_tensor(_DeviceArray(g.value, nf.value, "<f4"), device=self.dev)
             import torch.distributed as dist
             self._graphable = dist.get_backend(group) == "nccl" and os.environ.get("NVDB_DP_GRAPH", "1") == "1"
+
+    def set_ctas(self, ctas: int) -> None:
+        """Bound the SMs this trainer's epoch kernels use (0 = all; nvdb_trainer_set_ctas)."""
+        check(lib().nvdb_trainer_set_ctas(self.handle, int(ctas)), "nvdb_trainer_set_ctas")
+
+    def epoch_work(self) -> float:
+        """Relative per-epoch work: samples x training flops per sample."""
+        batch = min(self.n, self.batch) if self.sampled else self.n
+        return float(batch) * float(_train_flops(self.params.layers))
 
     def _epoch_dp(self, st) -> None:
         import torch.distributed as dist
@@ -436,6 +446,64 @@ class DeviceTrainer:
             pass
 
 
+def _train_flops(layers) -> int:
+    """2*(3*sum MAC - MAC_0) per sample."""
+    macs = [np.asarray(w).shape[0] * np.asarray(w).shape[1] for w, _ in layers]
+    return int(2 * (3 * sum(macs) - macs[0]))
+
+
+def run_concurrent(trainers: Sequence[DeviceTrainer], sms: Optional[int] = None) -> List[Tuple[float, int]]:
+    """Train independent networks CONCURRENTLY (SURVEY.md §7 hard part 4: the
+    nets x experts of a container as one grouped workload): each trainer gets
+    its own stream and a share of the SMs proportional to its per-epoch work
+    (nvdb_trainer_set_ctas), chunks of epochs are enqueued on every stream,
+    and the shares are re-planned whenever a net stops.  Results equal
+    training each net alone up to the gradient summation order (it follows
+    the CTA count; repeated runs are bit-identical).  Returns (final loss,
+    epochs) per trainer."""
+    if not trainers:
+        return []
+    if any(t.group is not None for t in trainers) or len(trainers) == 1:
+        return [t.run() for t in trainers]
+    dev = trainers[0].dev
+    sms = sms or torch.cuda.get_device_properties(dev).multi_processor_count
+    cur = torch.cuda.current_stream(dev)
+    streams = [torch.cuda.Stream(dev) for _ in trainers]
+    for s in streams:
+        s.wait_stream(cur)
+    active = list(range(len(trainers)))
+
+    def plan():
+        w = np.asarray([trainers[i].epoch_work() for i in active], dtype=np.float64)
+        share = np.maximum(1, np.floor(sms * w / w.sum())).astype(int)
+        for i, c in zip(active, share):
+            trainers[i].set_ctas(int(c))
+
+    plan()
+    while active:
+        for i in active:
+            t = trainers[i]
+            k = min(DeviceTrainer.CHUNK, t.max_epochs - t.epochs_enqueued)
+            with torch.cuda.stream(streams[i]):
+                t._enqueue(k, streams[i].cuda_stream)
+            t.epochs_enqueued += k
+        before = len(active)
+        keep = []
+        for i in active:
+            t = trainers[i]
+            done, stopped = t.status()[:2]  # synchronous (waits for this trainer's work)
+            if not stopped and t.epochs_enqueued < t.max_epochs:
+                keep.append(i)
+        active = keep
+        if active and len(active) != before:
+            plan()
+    for s in streams:
+        cur.wait_stream(s)
+    for t in trainers:
+        t.set_ctas(0)
+    return [t.final() for t in trainers]
+
+
 def _check_targets(targets: np.ndarray, kind: str, out_dim: int) -> None:
     """Label / target validation of neural.py:282-283, 295-296 (ValueError)."""
     t = np.asarray(targets)
@@ -449,12 +517,11 @@ def _check_targets(targets: np.ndarray, kind: str, out_dim: int) -> None:
         raise ValueError("NaN in targets")
 
 
-def train_network(inputs: np.ndarray, targets: np.ndarray, spec: NetSpec, cfg, expert_id: int, lr0: float,
-                  warm: Optional[NetRecord] = None, stop_loss: Optional[float] = None, workspace=None,
-                  device=None, return_trainer: bool = False, group=None) -> NetRecord:
-    """Train one network on the GPU; returns the committed record (encoder.py:330-371).
-    ``group``: data-parallel over the ranks of a torch.distributed group."""
-    del workspace
+def make_trainer(inputs: np.ndarray, targets: np.ndarray, spec: NetSpec, cfg, expert_id: int, lr0: float,
+                 warm: Optional[NetRecord] = None, stop_loss: Optional[float] = None, device=None,
+                 group=None) -> Tuple[DeviceTrainer, FourierFeatures]:
+    """The trainer train_network runs (encoder.py:330-360: seeds, warm start,
+    init, sampler choice, stop target), not yet started."""
     depth, width = spec.arch
     tagid = NET_TAGS[spec.tag]
     seed_ff = stable_seed(cfg.seed, expert_id, tagid, 0)
@@ -477,6 +544,16 @@ def train_network(inputs: np.ndarray, targets: np.ndarray, spec: NetSpec, cfg, e
     sampled = (not spec.full_batch) and n > cfg.batch_size
     tr = DeviceTrainer(params, ff, x, targets, spec.loss_kind, cfg, lr0, seed_draw, sampled, target, device,
                        group=group)
+    return tr, ff
+
+
+def train_network(inputs: np.ndarray, targets: np.ndarray, spec: NetSpec, cfg, expert_id: int, lr0: float,
+                  warm: Optional[NetRecord] = None, stop_loss: Optional[float] = None, workspace=None,
+                  device=None, return_trainer: bool = False, group=None) -> NetRecord:
+    """Train one network on the GPU; returns the committed record (encoder.py:330-371).
+    ``group``: data-parallel over the ranks of a torch.distributed group."""
+    del workspace
+    tr, ff = make_trainer(inputs, targets, spec, cfg, expert_id, lr0, warm, stop_loss, device, group)
     try:
         loss, epochs = tr.run()
         out = NetRecord(params=tr.weights(), ff=ff, final_loss=float(loss), epochs=epochs)
@@ -577,37 +654,61 @@ def build_upper_tree(grid: DenseLeafGrid) -> UpperTree:
     return tree
 
 
-def _train_expert(grid: DenseLeafGrid, sub: Subdomain, cfg, lr0: float, warm=None, stop_losses=None,
-                  device=None, group=None) -> EncodedSubdomain:
-    """encoder.py:531-570."""
+_EXPERT_NETS = (("l1", "l1_classifier"), ("tile", "tile_regressor"), ("l0", "l0_classifier"),
+                ("voxel", "voxel_regressor"))
+
+
+def _prepare_expert(grid: DenseLeafGrid, sub: Subdomain, cfg, lr0: float, warm=None, stop_losses=None,
+                    device=None, group=None):
+    """encoder.py:531-570 up to training: the expert's data and one trainer per
+    net (l1, tile, l0, voxel), not yet run."""
     scale = value_scale_of(grid)
     norm = (np.asarray(warm.norm_origin, dtype=np.float64).copy(), float(warm.norm_scale)) \
         if warm is not None else None
     data = gather_expert_data(grid, sub, scale, norm=norm)
     expert = EncodedSubdomain(id=sub.id, cell=sub.cell, cluster_id=sub.cluster_id, norm_origin=data.norm_origin,
                               norm_scale=data.norm_scale, value_scale=scale)
-
-    def run(tag, inputs, targets):
+    inputs = {"l1": (data.l1_inputs, data.l1_labels), "tile": (data.tile_inputs, data.tile_targets),
+              "l0": (data.l0_inputs, data.l0_labels), "voxel": (data.vox_inputs, data.vox_targets)}
+    jobs = []
+    for tag, attr in _EXPERT_NETS:
+        x, y = inputs[tag]
         spec = net_spec(tag, cfg)
-        if spec is None or inputs is None:
-            if inputs is not None and spec is None and tag == "tile":
+        if spec is None or x is None:
+            if x is not None and spec is None and tag == "tile":
                 logger.warning("expert %d: active tiles present but config has no tile network", sub.id)
-            return None
+            continue
         warm_net = dict(warm.nets()).get(tag) if warm is not None else None
         stop = None if stop_losses is None else stop_losses.get(tag)
         try:
-            return train_network(inputs, targets, spec, cfg, sub.id, lr0, warm=warm_net, stop_loss=stop,
-                                 device=device, group=group)
+            tr, ff = make_trainer(x, y, spec, cfg, sub.id, lr0, warm=warm_net, stop_loss=stop, device=device,
+                                  group=group)
         except Exception as exc:
             raise EncodeError(f"{tag} training failed: {exc}", sub.id) from exc
+        jobs.append((attr, tr, ff))
+    return expert, jobs
 
-    expert.l1_classifier = run("l1", data.l1_inputs, data.l1_labels)
-    expert.tile_regressor = run("tile", data.tile_inputs, data.tile_targets)
-    expert.l0_classifier = run("l0", data.l0_inputs, data.l0_labels)
-    expert.voxel_regressor = run("voxel", data.vox_inputs, data.vox_targets)
-    if expert.voxel_regressor is None:
-        logger.warning("expert %d: no active voxels, value regressor skipped", sub.id)
-    return expert
+
+def _train_experts(grid: DenseLeafGrid, subs, cfg, lr0: float, warm_of, stops_of, device=None, group=None):
+    """Train every net of every given expert; with no data-parallel group all of
+    them train CONCURRENTLY (run_concurrent), else one after another."""
+    prepared = [_prepare_expert(grid, sub, cfg, lr0, warm=warm_of(sub), stop_losses=stops_of(sub), device=device,
+                                group=group) for sub in subs]
+    trainers = [tr for _, jobs in prepared for _, tr, _ in jobs]
+    try:
+        results = iter(run_concurrent(trainers))
+        experts = []
+        for expert, jobs in prepared:
+            for attr, tr, ff in jobs:
+                loss, epochs = next(results)
+                setattr(expert, attr, NetRecord(params=tr.weights(), ff=ff, final_loss=float(loss), epochs=epochs))
+            if expert.voxel_regressor is None:
+                logger.warning("expert %d: no active voxels, value regressor skipped", expert.id)
+            experts.append(expert)
+        return experts
+    finally:
+        for tr in trainers:
+            tr.close()
 
 
 def encode(grid, cfg, weight_precision: int = 32, workers: int = 1, _warm=None, _lr0=None, _stop_losses=None,
@@ -636,16 +737,17 @@ def encode(grid, cfg, weight_precision: int = 32, workers: int = 1, _warm=None, 
         world, rank = dist.get_world_size(group), dist.get_rank(group)
     expert_parallel = world > 1 and len(layout.subdomains) >= world
     dp_group = group if world > 1 and not expert_parallel else None
-    experts = []
-    for i, sub in enumerate(layout.subdomains):
-        if expert_parallel and i % world != rank:
-            continue
-        warm = _warm.get(sub.cell) if _warm else None
-        stops = None
-        if _stop_losses is not None:
-            stops = {tag: _stop_losses[(sub.cell, tag)] for tag in NET_TAGS if (sub.cell, tag) in _stop_losses}
-        experts.append(_train_expert(g, sub, cfg, lr0, warm=warm, stop_losses=stops, device=device,
-                                     group=dp_group))
+    mine_subs = [sub for i, sub in enumerate(layout.subdomains) if not expert_parallel or i % world == rank]
+
+    def warm_of(sub):
+        return _warm.get(sub.cell) if _warm else None
+
+    def stops_of(sub):
+        if _stop_losses is None:
+            return None
+        return {tag: _stop_losses[(sub.cell, tag)] for tag in NET_TAGS if (sub.cell, tag) in _stop_losses}
+
+    experts = _train_experts(g, mine_subs, cfg, lr0, warm_of, stops_of, device=device, group=dp_group)
     if expert_parallel:
         # every rank needs all experts: patch extraction blends across
         # subdomain boundaries and the container holds every expert

@@ -65,7 +65,7 @@ class DeviceNetSet:
     by ``decompose`` (partition.py:90-94).
     """
 
-    def __init__(self, experts: Sequence, subdomain_size: int, halo: int = 8):
+    def __init__(self, experts: Sequence, subdomain_size: int, halo: int = 8, device=None):
         descs: List[NetDesc] = []
         exps: List[ExpertDesc] = []
         keep: list = []
@@ -88,8 +88,18 @@ class DeviceNetSet:
         darr = (NetDesc * max(len(descs), 1))(*descs)
         earr = (ExpertDesc * max(len(exps), 1))(*exps)
         handle = C.c_void_p()
-        check(lib().nvdb_netset_create(darr, len(descs), earr, len(exps), int(subdomain_size), int(halo),
-                                       C.byref(handle)), "nvdb_netset_create")
+        # device memory from the caller (torch's caching allocator) and an
+        # upload ordered on the current stream: no cudaMalloc / cudaFree and no
+        # host synchronisation per net set (nvdb_netset_create_at)
+        need = C.c_size_t()
+        check(lib().nvdb_netset_device_bytes(darr, len(descs), earr, len(exps), int(subdomain_size), int(halo),
+                                             C.byref(need)), "nvdb_netset_device_bytes")
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.mem = torch.empty(int(need.value), dtype=torch.uint8, device=dev)
+        check(lib().nvdb_netset_create_at(darr, len(descs), earr, len(exps), int(subdomain_size), int(halo),
+                                          self.mem.data_ptr(), self.mem.numel(),
+                                          torch.cuda.current_stream(dev).cuda_stream, C.byref(handle)),
+              "nvdb_netset_create_at")
         self.handle = handle
         self.nexperts = len(exps)
 

@@ -166,12 +166,12 @@ def train_container(grid, cfg, dev, timings, group=None):
     slice of every epoch's batch, one packed all-reduce per epoch."""
     import torch
     from paper_2208_04448_b200.encoder import (DeviceTrainer, build_upper_tree, decompose, extract_patches,
-                                               gather_expert_data, init_mlp, net_spec, run_concurrent, stable_seed,
+                                               gather_expert_data, init_mlp, net_spec, stable_seed,
                                                value_scale_of, NET_TAGS)
     from paper_2208_04448_b200.model import (Activation, EncodedSubdomain, FourierFeatures, GridMeta,
                                              NetRecord, NeuralGridContainer)
     layout = decompose(grid, cfg.subdomain_size)
-    experts, jobs = [], []
+    experts = []
     for sub in layout.subdomains:
         scale = value_scale_of(grid)
         data = gather_expert_data(grid, sub, scale)
@@ -190,26 +190,21 @@ def train_container(grid, cfg, dev, timings, group=None):
             sampled = (not spec.full_batch) and x.shape[0] > cfg.batch_size
             tr = DeviceTrainer(p0, ff, x, y, spec.loss_kind, cfg, cfg.lr, stable_seed(cfg.seed, sub.id, tid, 2),
                                sampled, spec.loss_target, dev, group=group)
+            torch.cuda.synchronize(dev)
+            if group is not None:
+                import torch.distributed as dist
+                dist.barrier(group)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            loss, epochs = tr.run()
+            e1.record()
+            e1.synchronize()
             batch = cfg.batch_size if sampled else x.shape[0]
-            jobs.append((ex, attr, tag, tr, ff, int(batch), train_flops(p0.layers)))
+            timings.append({"tag": tag, "epochs": epochs, "batch": int(batch), "ms": e0.elapsed_time(e1),
+                            "loss": loss, "flops_per_sample": train_flops(p0.layers)})
+            setattr(ex, attr, NetRecord(tr.weights(), ff, loss, epochs))
+            tr.close()
         experts.append(ex)
-    # every net of the container trains at once (one stream and an SM share
-    # each; encoder.run_concurrent), one device-timed region for all of them
-    torch.cuda.synchronize(dev)
-    if group is not None:
-        import torch.distributed as dist
-        dist.barrier(group)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    res = run_concurrent([j[3] for j in jobs])
-    e1.record()
-    e1.synchronize()
-    total_ms = e0.elapsed_time(e1)
-    for (ex, attr, tag, tr, ff, batch, fl), (loss, epochs) in zip(jobs, res):
-        timings.append({"tag": tag, "epochs": epochs, "batch": batch, "loss": loss, "flops_per_sample": fl})
-        setattr(ex, attr, NetRecord(tr.weights(), ff, loss, epochs))
-        tr.close()
-    timings.append({"tag": "all", "ms": total_ms, "concurrent": group is None})
     extract_patches(grid, layout, experts, cfg, dev)
     meta = GridMeta(grid.grid_class, grid.background, grid.voxel_size, grid.half_width, value_scale_of(grid))
     return NeuralGridContainer(meta, build_upper_tree(grid), layout, experts, cfg, 16)
@@ -617,10 +612,9 @@ def main():
     if world > 1:
         dist.barrier()
     c = train_container(grid, cfg, dev, timings, group=_group(world))
-    train_ms = sum(t["ms"] for t in timings if "ms" in t)
-    nets_t = [t for t in timings if "epochs" in t]
-    train_samples = sum(t["epochs"] * t["batch"] for t in nets_t)
-    train_flop = sum(t["epochs"] * t["batch"] * t["flops_per_sample"] for t in nets_t)
+    train_ms = sum(t["ms"] for t in timings)
+    train_samples = sum(t["epochs"] * t["batch"] for t in timings)
+    train_flop = sum(t["epochs"] * t["batch"] * t["flops_per_sample"] for t in timings)
     # ---------------- decode steps
     m = DeviceModel(c, dev)
     flops = {t: fwd_flops(n) for t, n in c.experts[0].nets() if n is not None}

@@ -166,6 +166,15 @@ NVDB_API int nvdb_scatter_f32_counted(float* dst, const int64_t* ids, const floa
                                       const int64_t* count_dev, void* stream);
 /* leaf origins of child slots (node*4096+slot, node order x ascending slot)
  * and the slot -> leaf index map (-1 elsewhere) (decoder.py:146-151) */
+/* Level-1 slot (node * 4096 + idx1, -1 outside every node) and idx0 of
+ * int32 coordinates (n,3), the node found through a dense int32 table over
+ * the bounding box [lut_lo, lut_lo + lut_span) of the level-1 origins >> 7
+ * (node index in sorted-origin order or -1); lut_lo / lut_span are HOST
+ * int32[3].  err (nullable, DEVICE) is set to 1 when a coordinate lies in no
+ * node.  vox nullable. */
+NVDB_API int nvdb_node_slots(const int32_t* lut, const int32_t* lut_lo, const int32_t* lut_span,
+                             const int32_t* coords, int64_t n, int64_t* slot, int32_t* vox, int32_t* err,
+                             void* stream);
 NVDB_API int nvdb_leaf_list(const int64_t* child_slots, int64_t nl, const int32_t* node_origins,
                             int64_t nslots, int32_t* leaf_origins, int32_t* leaf_of_slot, void* stream);
 /* level-0 patches on the active mask; *err = 1 if a patch has no leaf (decoder.py:168-179) */

@@ -36,7 +36,7 @@ EXPORTED = [
     "nvdb_eval_counted", "nvdb_leaf_finalize_counted", "nvdb_scatter_f32_counted",
     "nvdb_query_finalize_counted", "nvdb_trainer_packed", "nvdb_nvgr_leaf_records", "nvdb_nvgr_l1_records",
     "nvdb_metric_partials", "nvdb_metric_pass", "nvdb_trainer_set_ctas", "nvdb_netset_device_bytes",
-    "nvdb_netset_create_at",
+    "nvdb_netset_create_at", "nvdb_node_slots",
 ]
 
 SRC_NORM_F32, SRC_CENTER_F64, SRC_COORD_I32, SRC_LEAF_VOX, SRC_L1_SLOT = range(5)
@@ -121,6 +121,7 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_l1_apply": (C.c_int, [vp, vp, i64, vp, vp, i64, vp, vp, i64, vp]),
         "nvdb_scatter_f32": (C.c_int, [vp, vp, vp, i64, vp]),
         "nvdb_leaf_list": (C.c_int, [vp, i64, vp, i64, vp, vp, vp]),
+        "nvdb_node_slots": (C.c_int, [vp, C.POINTER(i32), C.POINTER(i32), vp, i64, vp, vp, vp, vp]),
         "nvdb_l0_apply": (C.c_int, [vp, vp, vp, vp, i64, vp, vp, vp]),
         "nvdb_leaf_finalize": (C.c_int, [i64, vp, vp, vp, i64, vp, vp, vp, vp, i64, vp, vp, i64, vp,
                                          C.c_float, C.c_float, vp, vp, vp, vp]),

@@ -32,11 +32,12 @@ __global__ void k_l1_apply(uint8_t* cls, float* tiles, const int64_t* patch_slot
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (phase == 0) {
-    for (int64_t i = i0; i < npatch; i += stride) cls[patch_slot[i]] = patch_cls[i];
+    for (int64_t i = i0; i < npatch; i += stride)
+      if (patch_slot[i] >= 0) cls[patch_slot[i]] = patch_cls[i];  // < 0: outside every node (flagged)
   } else {
     for (int64_t i = i0; i < ntile; i += stride) {
       const int64_t s = tile_slot[i];
-      if (cls[s] == 2) tiles[s] = tile_value[i];
+      if (s >= 0 && cls[s] == 2) tiles[s] = tile_value[i];
     }
   }
 }
@@ -252,6 +253,37 @@ extern "C" int nvdb_scatter_f32(float* dst, const int64_t* ids, const float* val
   if (n < 0 || (n > 0 && (!dst || !ids || !vals))) return fail(NVDB_EINVAL, "nvdb_scatter_f32: bad args");
   if (!n) return NVDB_OK;
   k_scatter_f32<<<blocks_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, ids, vals, n, nullptr);
+  NVDB_CHECK_LAUNCH();
+  return NVDB_OK;
+}
+
+// node index of a coordinate through a dense table over the bounding box of
+// the level-1 origins (>> 7), then node * 4096 + idx1 and idx0 (grid.py:74-94)
+__global__ void k_node_slots(const int32_t* __restrict__ lut, int lx, int ly, int lz, int sx, int sy, int sz,
+                             const int32_t* __restrict__ coords, int64_t n, int64_t* __restrict__ slot,
+                             int32_t* __restrict__ vox, int32_t* __restrict__ err) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int x = coords[3 * i], y = coords[3 * i + 1], z = coords[3 * i + 2];
+    const int cx = (x >> 7) - lx, cy = (y >> 7) - ly, cz = (z >> 7) - lz;
+    int node = -1;
+    if ((unsigned)cx < (unsigned)sx && (unsigned)cy < (unsigned)sy && (unsigned)cz < (unsigned)sz)
+      node = lut[((int64_t)cx * sy + cy) * sz + cz];
+    const int i1 = (((x & 127) >> 3) << 8) | (((y & 127) >> 3) << 4) | ((z & 127) >> 3);
+    slot[i] = node < 0 ? -1 : (int64_t)node * 4096 + i1;
+    if (vox) vox[i] = ((x & 7) << 6) | ((y & 7) << 3) | (z & 7);
+    if (node < 0 && err) atomicExch(err, 1);
+  }
+}
+
+extern "C" int nvdb_node_slots(const int32_t* lut, const int32_t* lut_lo, const int32_t* lut_span,
+                               const int32_t* coords, int64_t n, int64_t* slot, int32_t* vox, int32_t* err,
+                               void* stream) {
+  if (n < 0 || !lut_lo || !lut_span || (n > 0 && (!lut || !coords || !slot)))
+    return fail(NVDB_EINVAL, "nvdb_node_slots: bad args");
+  if (!n) return NVDB_OK;
+  k_node_slots<<<blocks_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      lut, lut_lo[0], lut_lo[1], lut_lo[2], lut_span[0], lut_span[1], lut_span[2], coords, n, slot, vox, err);
   NVDB_CHECK_LAUNCH();
   return NVDB_OK;
 }

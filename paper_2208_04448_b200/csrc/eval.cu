@@ -1,6 +1,7 @@
 // Netset upload, the forward_block seam and the generic gate-blended
 // evaluation driver (inference.py:39-84, partition.py:160-256).
 #define NVDB_MLP_KERNEL_TU
+#include <immintrin.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -23,6 +24,37 @@ uint16_t f2h_bits(float f) {
 }
 
 int round_up_i(int v, int a) { return (v + a - 1) / a * a; }
+
+// one weight matrix (rows x cols, row-major fp32, times `scale`) into the fp16
+// K-major core-matrix image of R padded rows: 8 consecutive k of a row are 16
+// contiguous bytes of the image, converted 8 at a time with F16C when the
+// host has it (round to nearest even, as __float2half_rn)
+__attribute__((target("avx,f16c"))) void pack_rows_f16c(uint16_t* img, const float* w, int rows, int cols, int R,
+                                                        float scale) {
+  const __m256 sc = _mm256_set1_ps(scale);
+  for (int n = 0; n < rows; ++n) {
+    const float* src = w + (size_t)n * cols;
+    int k = 0;
+    for (; k + 8 <= cols; k += 8) {
+      __m256 v = _mm256_loadu_ps(src + k);
+      if (scale != 1.0f) v = _mm256_mul_ps(v, sc);
+      const __m128i h = _mm256_cvtps_ph(v, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+      _mm_storeu_si128(reinterpret_cast<__m128i*>(img + kmajor_offset(n, k, R) / 2), h);
+    }
+    for (; k < cols; ++k) img[kmajor_offset(n, k, R) / 2] = f2h_bits(scale == 1.0f ? src[k] : src[k] * scale);
+  }
+}
+
+void pack_rows(uint16_t* img, const float* w, int rows, int cols, int R, float scale) {
+  static const bool f16c = __builtin_cpu_supports("f16c") && __builtin_cpu_supports("avx");
+  if (f16c) {
+    pack_rows_f16c(img, w, rows, cols, R, scale);
+    return;
+  }
+  for (int n = 0; n < rows; ++n)
+    for (int k = 0; k < cols; ++k)
+      img[kmajor_offset(n, k, R) / 2] = f2h_bits(scale == 1.0f ? w[(size_t)n * cols + k] : w[(size_t)n * cols + k] * scale);
+}
 
 }  // namespace
 
@@ -135,17 +167,10 @@ static int netset_create(const nvdb_net_desc* nets, int32_t nnets, const nvdb_ex
     // layer 0: B operand (N = W rows, K = k0), serialized interleaved feature order;
     // the feature amplitude (1 unless set) folded in, omega applied in the
     // fp32 epilogue so 16-bit container weights stay exact in fp16
-    for (int n = 0; n < d.width; ++n)
-      for (int k = 0; k < 2 * m; ++k) {
-        const float w = d.amplitude == 1.0f ? d.weights[0][(size_t)n * 2 * m + k]
-                                            : d.weights[0][(size_t)n * 2 * m + k] * d.amplitude;
-        wimg[kmajor_offset(n, k, W) / 2] = f2h_bits(w);
-      }
+    pack_rows(wimg, d.weights[0], d.width, 2 * m, W, d.amplitude);
     size_t base = (size_t)W * k0;
     for (int l = 1; l < d.depth; ++l) {
-      for (int n = 0; n < d.width; ++n)
-        for (int k = 0; k < d.width; ++k)
-          wimg[base + kmajor_offset(n, k, W) / 2] = f2h_bits(d.weights[l][(size_t)n * d.width + k]);
+      pack_rows(wimg + base, d.weights[l], d.width, d.width, W, 1.0f);
       base += (size_t)W * W;
     }
     float* bias = reinterpret_cast<float*>(blob.data() + pieces[i].bias);

@@ -1661,6 +1661,17 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
 }
 
 namespace {
+// the completion event of the trainer's last enqueued work; not recorded while
+// the stream is being captured into a graph (an event recorded in a capture
+// cannot be waited on) -- the caller of graph replays orders the host itself
+cudaError_t record_done(nvdb_trainer* t, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(st, &cs);
+  if (e != cudaSuccess) return e;
+  if (cs != cudaStreamCaptureStatusNone) return cudaSuccess;
+  return cudaEventRecord(t->done, st);
+}
+
 // phase 1: sampler -> fwd/dgrad -> wgrad -> partial reduction (grad, loss);
 // phase 2: Adam + early stop + epoch advance.  A data-parallel caller
 // all-reduces grad[P] and the loss between the two phases.
@@ -1767,7 +1778,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
             t->partial, t->wg_grid, t->P, t->grad, t->loss_part, t->fb_grid, t->lossbuf, stopped);
         NVDB_CHECK_LAUNCH();
       }
-      NVDB_CUDA_TRY(cudaEventRecord(t->done, st));
+      NVDB_CUDA_TRY(record_done(t, st));
       return NVDB_OK;
     }
     FbArgs fa{};
@@ -1838,7 +1849,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
           t->partial, t->wg_grid, t->P, t->grad, t->loss_part, t->fb_grid, t->lossbuf, stopped);
       NVDB_CHECK_LAUNCH();
     }
-    NVDB_CUDA_TRY(cudaEventRecord(t->done, st));
+    NVDB_CUDA_TRY(record_done(t, st));
     return NVDB_OK;
   }
     AdamArgs aa{};
@@ -1876,7 +1887,7 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
     k_train_advance<<<1, 1, 0, st>>>(ep, stopped, t->ctl + 2, t->ctl + 3, d.max_epochs);
     NVDB_CHECK_LAUNCH();
     ++t->host_epoch;
-    NVDB_CUDA_TRY(cudaEventRecord(t->done, st));
+    NVDB_CUDA_TRY(record_done(t, st));
   return NVDB_OK;
 }
 }  // namespace
@@ -1932,6 +1943,9 @@ extern "C" int nvdb_trainer_packed(nvdb_trainer* t, float** buf, int64_t* nfloat
 extern "C" int nvdb_trainer_status(const nvdb_trainer* t, int32_t* epochs_done, int32_t* stopped, double* losses,
                                    int32_t nlosses) {
   if (!t) return fail(NVDB_EINVAL, "nvdb_trainer_status: null trainer");
+  // the trainer's work may be on any (non-blocking) stream: wait for the event
+  // recorded after its last enqueued phase before reading its state
+  if (t->enqueued) NVDB_CUDA_TRY(cudaEventSynchronize(t->done));
   int32_t ctl[3];
   NVDB_CUDA_TRY(cudaMemcpy(ctl, t->ctl, sizeof(ctl), cudaMemcpyDeviceToHost));
   if (epochs_done) *epochs_done = ctl[2];
@@ -2019,6 +2033,7 @@ extern "C" int nvdb_sample_indices(uint64_t n, int64_t batch, const uint64_t* wo
 extern "C" int nvdb_trainer_weights(const nvdb_trainer* t, float* const* weights, float* const* biases) {
   if (!t || !weights || !biases) return fail(NVDB_EINVAL, "nvdb_trainer_weights: null argument");
   std::vector<float> host(t->P);
+  if (t->enqueued) NVDB_CUDA_TRY(cudaEventSynchronize(t->done));  // work on any stream
   NVDB_CUDA_TRY(cudaMemcpy(host.data(), t->wmaster, 4 * t->P, cudaMemcpyDeviceToHost));
   for (int l = 0; l <= t->depth; ++l) {
     const int64_t nw = t->poff[2 * l + 1] - t->poff[2 * l];

@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from ._lib import EvalOut, check, lib
 from .errors import SvcodecError
-from .model import (L1_SIZE, L2_SIZE, LEAF_SIZE, DenseLeafGrid, LeafBitsMap, PatchRecords)
+from .model import (L1_SIZE, L2_SIZE, LEAF_SIZE, DenseLeafGrid, L1TileMap, LeafBitsMap, PatchRecords)
 from .netset import TAG_CODES, DeviceNetSet
 from .tree import DeviceTree
 
@@ -195,47 +195,83 @@ class DeviceModel:
         self.origins = np.asarray(origins, dtype=np.int64).reshape(-1, 3)
         self.n1 = len(origins)
         host = {"d_origins": self.origins.astype(np.int32)}  # device tables, uploaded together below
+        # dense node table over the origins' bounding box: patch / fill / tile
+        # coordinates become node * 4096 + idx1 on the device (nvdb_node_slots)
+        self._lut_lo = self._lut_span = None
+        if self.n1:
+            o = self.origins >> 7
+            lo, span = o.min(axis=0), o.max(axis=0) - o.min(axis=0) + 1
+            if float(span[0]) * float(span[1]) * float(span[2]) <= float(1 << 24) and (np.abs(self.origins) < (1 << 30)).all():
+                code = ((o[:, 0] - lo[0]) * span[1] + (o[:, 1] - lo[1])) * span[2] + (o[:, 2] - lo[2])
+                lut = np.full(int(span.prod()), -1, np.int32)
+                lut[code[::-1]] = np.arange(self.n1, dtype=np.int32)[::-1]
+                host["lut"] = lut
+                self._lut_lo = (C.c_int32 * 3)(*[int(v) for v in lo])
+                self._lut_span = (C.c_int32 * 3)(*[int(v) for v in span])
         # patch maps (decoder.py:84-92): later experts override earlier keys
         l1k, l1c = _patch_arrays([e.patches.l1 for e in c.experts], 1)
-        ni1 = self._node_index(l1k & ~np.int64(127))
-        if (ni1 < 0).any():
-            bad = tuple(int(v) for v in l1k[np.flatnonzero(ni1 < 0)[0]])
-            raise SvcodecError(f"corrupt container: level-1 patch {bad} outside every level-1 node")
-        host["p1_slot"] = (ni1 * L1_SIZE + _slot1_arr(l1k)).astype(np.int64)
+        host["p1_key"] = l1k.astype(np.int32).reshape(-1, 3)
         host["p1_cls"] = np.asarray(l1c).astype(np.uint8)
         # tile records per level-1 node
-        ts, tv = [np.zeros(0, np.int64)], [np.zeros(0, np.float32)]
-        torg = list(ut.l1_tiles.keys())
-        if torg:
-            tni = self._node_index(np.asarray(torg, dtype=np.int64).reshape(-1, 3))
-            if (tni < 0).any():
-                bad = tuple(int(v) for v in torg[int(np.flatnonzero(tni < 0)[0])])
-                raise SvcodecError(f"corrupt container: tile record for unknown level-1 node {bad}")
-            for ni, d in zip(tni, ut.l1_tiles.values()):
-                if d:
-                    ts.append(ni * L1_SIZE + np.fromiter(d.keys(), dtype=np.int64, count=len(d)))
-                    tv.append(np.fromiter(d.values(), dtype=np.float32, count=len(d)))
-        host["t_slot"] = np.concatenate(ts).astype(np.int64)
-        host["t_val"] = np.concatenate(tv).astype(np.float32)
+        t_slot, t_val = self._tile_records(ut.l1_tiles)
+        host["t_slot"], host["t_val"] = t_slot, t_val
+        host["err"] = np.zeros(2, np.int32)  # [0] level-1 patch outside every node
         self._tables = []
         self._upload(host)
+        self.p1_slot = torch.empty(max(l1k.shape[0], 1), dtype=torch.int64, device=self.dev)[:l1k.shape[0]]
+        self._slots(self.p1_key, self.p1_slot, None, self.err[:1], "level-1 patch")
         self._l0_ready = False  # level-0 tables: built by _ensure_l0 (decode overlaps them with the L0 stage)
 
+    def _slots(self, keys: torch.Tensor, slot: torch.Tensor, vox, err, what: str) -> None:
+        """node * 4096 + idx1 (and idx0) of int32 coordinate rows, on the device."""
+        n = keys.shape[0]
+        if n == 0:
+            return
+        if self._lut_lo is not None:
+            check(lib().nvdb_node_slots(_ptr(self.lut), self._lut_lo, self._lut_span, _ptr(keys), n, _ptr(slot),
+                                        _ptr(vox), _ptr(err), _stream(self.dev)), "nvdb_node_slots")
+            return
+        # very sparse node sets (bounding box > 2^24 cells): host lookup
+        k = keys.cpu().numpy().astype(np.int64)
+        ni = self._node_index(k & ~np.int64(127))
+        if err is not None and (ni < 0).any():
+            err.fill_(1)
+        slot.copy_(torch.from_numpy(np.where(ni < 0, -1, ni * L1_SIZE + _slot1_arr(k)).astype(np.int64)))
+        if vox is not None:
+            vox.copy_(torch.from_numpy(_slot0_arr(k).astype(np.int32)))
+
+    def _tile_records(self, tiles_map):
+        """(slot, value) of the inactive-tile records (decoder.py:126-134); an
+        unknown node raises SvcodecError (decoder.py:128-130)."""
+        if isinstance(tiles_map, L1TileMap):  # columns already (model.L1TileMap)
+            torg, counts, slots, vals = tiles_map.arrays()
+        else:
+            torg = np.asarray(list(tiles_map.keys()), dtype=np.int64).reshape(-1, 3)
+            ds = list(tiles_map.values())
+            counts = np.fromiter((len(d) for d in ds), dtype=np.int64, count=len(ds))
+            slots = np.fromiter(itertools.chain.from_iterable(d.keys() for d in ds), dtype=np.int64,
+                                count=int(counts.sum()))
+            vals = np.fromiter(itertools.chain.from_iterable(d.values() for d in ds), dtype=np.float32,
+                               count=int(counts.sum()))
+        if torg.shape[0] == 0:
+            return np.zeros(0, np.int64), np.zeros(0, np.float32)
+        tni = self._node_index(torg)
+        if (tni < 0).any():
+            bad = tuple(int(v) for v in torg[int(np.flatnonzero(tni < 0)[0])])
+            raise SvcodecError(f"corrupt container: tile record for unknown level-1 node {bad}")
+        return (np.repeat(tni, counts) * L1_SIZE + slots).astype(np.int64), vals.astype(np.float32)
+
     def _ensure_l0(self) -> None:
-        """Level-0 patch and negative-fill tables (host conversion + upload)."""
+        """Level-0 patch and negative-fill tables (one upload; slots on the device)."""
         if self._l0_ready:
             return
         c, ut = self.c, self.c.upper_tree
         host = {}
         l0k, l0a, l0v = _patch_arrays([e.patches.l0 for e in c.experts], 2)
-        # level-0 patches: slot -1 when outside every level-1 node (checked in the decode)
-        ni0 = self._node_index(l0k & ~np.int64(127))
-        host["p0_slot"] = np.where(ni0 < 0, -1, ni0 * L1_SIZE + _slot1_arr(l0k)).astype(np.int64)
-        host["p0_vox"] = _slot0_arr(l0k).astype(np.int32)
+        host["p0_key"] = l0k.astype(np.int32).reshape(-1, 3)
         host["p0_act"] = np.asarray(l0a).astype(np.uint8)
         host["p0_val"] = l0v.astype(np.float32)
         self._l0_keys = l0k
-        # negative-fill bits of leaves inside a level-1 node
         nf = ut.leaf_negative_fill
         if len(nf):
             if isinstance(nf, LeafBitsMap):  # columns already (model.LeafBitsMap)
@@ -247,16 +283,22 @@ class DeviceModel:
                 if bits.size != LEAF_SIZE * len(nf):
                     raise SvcodecError("corrupt container: negative-fill entry of the wrong size")
                 bits = bits.astype(bool, copy=False).reshape(-1, LEAF_SIZE)
-            nni = self._node_index(norg & ~np.int64(127))
-            keep = nni >= 0
-            bits = bits[keep]
-            host["neg_slot"] = (nni[keep] * L1_SIZE + _slot1_arr(norg[keep])).astype(np.int64)
-            packed = np.packbits(bits, axis=1, bitorder="little")  # (n, 64) bytes = 8 x u64 per leaf
-            host["neg_bits"] = np.ascontiguousarray(packed).view(np.int64).reshape(-1, 8)
+            host["neg_key"] = norg.astype(np.int32).reshape(-1, 3)
+            host["neg_u8"] = np.ascontiguousarray(bits).view(np.uint8).reshape(-1, LEAF_SIZE)
         else:
-            host["neg_slot"] = np.zeros(0, np.int64)
-            host["neg_bits"] = np.zeros((0, 8), np.int64)
+            host["neg_key"] = np.zeros((0, 3), np.int32)
+            host["neg_u8"] = np.zeros((0, LEAF_SIZE), np.uint8)
         self._upload(host)
+        n0, nn = l0k.shape[0], self.neg_key.shape[0]
+        self.p0_slot = torch.empty(max(n0, 1), dtype=torch.int64, device=self.dev)[:n0]
+        self.p0_vox = torch.empty(max(n0, 1), dtype=torch.int32, device=self.dev)[:n0]
+        self._slots(self.p0_key, self.p0_slot, self.p0_vox, None, "level-0 patch")  # -1: flagged by l0_apply
+        self.neg_slot = torch.empty(max(nn, 1), dtype=torch.int64, device=self.dev)[:nn]
+        self._slots(self.neg_key, self.neg_slot, None, None, "negative fill")  # -1: skipped (not a leaf)
+        self.neg_bits = torch.empty((max(nn, 1), 8), dtype=torch.int64, device=self.dev)[:nn]
+        if nn:
+            check(lib().nvdb_pack_eq(_ptr(self.neg_u8), nn * 8, 1, _ptr(self.neg_bits), _stream(self.dev)),
+                  "nvdb_pack_eq")
         self._l0_ready = True
 
     @property
@@ -272,10 +314,13 @@ class DeviceModel:
         for k, a in host.items():
             offs[k] = n
             n += (a.nbytes + 255) & ~255
-        buf = np.zeros(max(n, 256), np.uint8)
+        # pinned staging from torch's caching host allocator (blocks are reused
+        # once their copy completed): an asynchronous copy, no host wait
+        pin = torch.empty(max(n, 256), dtype=torch.uint8, pin_memory=True)
+        buf = pin.numpy()
         for k, a in host.items():
             buf[offs[k]:offs[k] + a.nbytes] = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
-        dbuf = torch.from_numpy(buf).to(self.dev)
+        dbuf = pin.to(self.dev, non_blocking=True)
         self._tables.append(dbuf)
         for k, a in host.items():
             t = dbuf[offs[k]:offs[k] + a.nbytes].view(_TORCH_DTYPE[a.dtype.type]).view(a.shape)
@@ -530,6 +575,8 @@ class DeviceDecode:
         flag is read lazily (first host access) so a decode enqueues without a
         stream synchronisation."""
         if not self._checked and self.err_dev is not None:
+            if int(self.model.err[0].item()):  # decoder.py:121-124
+                raise SvcodecError("corrupt container: level-1 patch outside every level-1 node")
             if int(self.err_dev.item()):
                 raise SvcodecError("corrupt container: level-0 patch outside every reconstructed leaf")
             self._checked = True

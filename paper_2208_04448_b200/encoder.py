@@ -26,7 +26,8 @@ from .errors import EncodeError, SvcodecError
 from .model import (GRID_CLASS_SDF, L1_CLASS_ACTIVE_TILE, L1_CLASS_CHILD, L1_CLASS_INACTIVE_TILE,
                     L1_LOCAL, L1_SIZE, L2_SIZE, LEAF_LOCAL, LEAF_SIZE, Activation, DenseLeafGrid,
                     EncodedSubdomain, FourierFeatures, GridMeta, L2NodeRecord, Mask, MlpParams,
-                    LeafBitsMap, NetRecord, NeuralGridContainer, PatchList, Subdomain, SubdomainLayout, UpperTree)
+                    L1TileMap, LeafBitsMap, NetRecord, NeuralGridContainer, PatchList, Subdomain, SubdomainLayout,
+                    UpperTree)
 from .netset import _net_desc
 
 logger = logging.getLogger(__name__)
@@ -347,9 +348,12 @@ class DeviceTrainer:
         check(lib().nvdb_trainer_set_ctas(self.handle, int(ctas)), "nvdb_trainer_set_ctas")
 
     def epoch_work(self) -> float:
-        """Relative per-epoch work: samples x training flops per sample."""
+        """Relative per-epoch time: 128-sample tiles per epoch (the epoch kernels
+        are latency-bound per tile, so their time follows the tile count more
+        than the flops), weighted by the layer width's share of the work."""
         batch = min(self.n, self.batch) if self.sampled else self.n
-        return float(batch) * float(_train_flops(self.params.layers))
+        width = max(np.asarray(w).shape[0] for w, _ in self.params.layers[:-1])
+        return float((batch + 127) // 128) * (1.0 + width / 256.0)
 
     def _epoch_dp(self, st) -> None:
         import torch.distributed as dist
@@ -400,6 +404,8 @@ class DeviceTrainer:
         return self.final()
 
     def status(self):
+        if self._graph is not None:  # graph replays record no completion event: order the host here
+            torch.cuda.current_stream(self.dev).synchronize()
         done, stopped = C.c_int32(), C.c_int32()
         losses = np.zeros(self.max_epochs, dtype=np.float64)
         check(lib().nvdb_trainer_status(self.handle, C.byref(done), C.byref(stopped),
@@ -423,6 +429,8 @@ class DeviceTrainer:
             rows = np.asarray(w).shape[0] if li == depth else width
             cols = np.asarray(w).shape[1] if li == 0 else width
             shapes.append((rows, cols))
+        if self._graph is not None:
+            torch.cuda.current_stream(self.dev).synchronize()
         ws = [np.zeros(sh, dtype=np.float32) for sh in shapes]
         bs = [np.zeros(sh[0], dtype=np.float32) for sh in shapes]
         wp = (C.POINTER(C.c_float) * len(ws))(*[w.ctypes.data_as(C.POINTER(C.c_float)) for w in ws])
@@ -436,6 +444,9 @@ class DeviceTrainer:
 
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:
+            if getattr(self, "_graph", None) is not None:  # replays record no completion event
+                torch.cuda.current_stream(self.dev).synchronize()
+                self._graph = None
             lib().nvdb_trainer_destroy(self.handle)
             self.handle = None
 
@@ -450,58 +461,6 @@ def _train_flops(layers) -> int:
     """2*(3*sum MAC - MAC_0) per sample."""
     macs = [np.asarray(w).shape[0] * np.asarray(w).shape[1] for w, _ in layers]
     return int(2 * (3 * sum(macs) - macs[0]))
-
-
-def run_concurrent(trainers: Sequence[DeviceTrainer], sms: Optional[int] = None) -> List[Tuple[float, int]]:
-    """Train independent networks CONCURRENTLY (SURVEY.md §7 hard part 4: the
-    nets x experts of a container as one grouped workload): each trainer gets
-    its own stream and a share of the SMs proportional to its per-epoch work
-    (nvdb_trainer_set_ctas), chunks of epochs are enqueued on every stream,
-    and the shares are re-planned whenever a net stops.  Results equal
-    training each net alone up to the gradient summation order (it follows
-    the CTA count; repeated runs are bit-identical).  Returns (final loss,
-    epochs) per trainer."""
-    if not trainers:
-        return []
-    if any(t.group is not None for t in trainers) or len(trainers) == 1:
-        return [t.run() for t in trainers]
-    dev = trainers[0].dev
-    sms = sms or torch.cuda.get_device_properties(dev).multi_processor_count
-    cur = torch.cuda.current_stream(dev)
-    streams = [torch.cuda.Stream(dev) for _ in trainers]
-    for s in streams:
-        s.wait_stream(cur)
-    active = list(range(len(trainers)))
-
-    def plan():
-        w = np.asarray([trainers[i].epoch_work() for i in active], dtype=np.float64)
-        share = np.maximum(1, np.floor(sms * w / w.sum())).astype(int)
-        for i, c in zip(active, share):
-            trainers[i].set_ctas(int(c))
-
-    plan()
-    while active:
-        for i in active:
-            t = trainers[i]
-            k = min(DeviceTrainer.CHUNK, t.max_epochs - t.epochs_enqueued)
-            with torch.cuda.stream(streams[i]):
-                t._enqueue(k, streams[i].cuda_stream)
-            t.epochs_enqueued += k
-        before = len(active)
-        keep = []
-        for i in active:
-            t = trainers[i]
-            done, stopped = t.status()[:2]  # synchronous (waits for this trainer's work)
-            if not stopped and t.epochs_enqueued < t.max_epochs:
-                keep.append(i)
-        active = keep
-        if active and len(active) != before:
-            plan()
-    for s in streams:
-        cur.wait_stream(s)
-    for t in trainers:
-        t.set_ctas(0)
-    return [t.final() for t in trainers]
 
 
 def _check_targets(targets: np.ndarray, kind: str, out_dim: int) -> None:
@@ -641,12 +600,12 @@ def build_upper_tree(grid: DenseLeafGrid) -> UpperTree:
         tiles = {int(i): float(grid.l2_tiles[ni, i]) for i in np.flatnonzero(keep)}
         tree.l2_nodes.append(L2NodeRecord(tuple(int(v) for v in grid.l2_origins[ni]),
                                           Mask(grid.l2_child[ni].copy()), Mask(grid.l2_active[ni].copy()), tiles))
-    for ni in range(grid.l1_origins.shape[0]):
-        org = tuple(int(v) for v in grid.l1_origins[ni])
-        tree.l1_origins.append(org)
-        inactive = ~grid.l1_child[ni] & ~grid.l1_active[ni] & (grid.l1_tiles[ni] != bg)
-        if inactive.any():
-            tree.l1_tiles[org] = {int(i): float(grid.l1_tiles[ni, i]) for i in np.flatnonzero(inactive)}
+    tree.l1_origins = [tuple(o) for o in grid.l1_origins.astype(np.int64).tolist()]
+    # inactive tiles with a stored value, as columns (model.L1TileMap; encoder.py:512-517)
+    inactive = ~grid.l1_child & ~grid.l1_active & (grid.l1_tiles != bg)
+    rows, cols = np.nonzero(inactive)
+    nodes, counts = np.unique(rows, return_counts=True)
+    tree.l1_tiles = L1TileMap.from_arrays(grid.l1_origins[nodes], counts, cols, grid.l1_tiles[rows, cols])
     neg = ~grid.leaf_active & (grid.leaf_values < 0)
     sel = np.flatnonzero(neg.any(axis=1))
     tree.leaf_negative_fill = LeafBitsMap.from_arrays(grid.leaf_origins[sel], neg[sel])
@@ -690,25 +649,26 @@ def _prepare_expert(grid: DenseLeafGrid, sub: Subdomain, cfg, lr0: float, warm=N
 
 
 def _train_experts(grid: DenseLeafGrid, subs, cfg, lr0: float, warm_of, stops_of, device=None, group=None):
-    """Train every net of every given expert; with no data-parallel group all of
-    them train CONCURRENTLY (run_concurrent), else one after another."""
-    prepared = [_prepare_expert(grid, sub, cfg, lr0, warm=warm_of(sub), stop_losses=stops_of(sub), device=device,
-                                group=group) for sub in subs]
-    trainers = [tr for _, jobs in prepared for _, tr, _ in jobs]
-    try:
-        results = iter(run_concurrent(trainers))
-        experts = []
-        for expert, jobs in prepared:
+    """Train every net of every given expert, one after another, each net on
+    the whole GPU.  (Running a container's nets concurrently on SM shares was
+    measured: +16 % at best for two ACCEPT nets, because the epoch kernels are
+    latency-bound per tile and a smaller share lengthens each CTA's tile
+    chain; DESIGN.md "Training".)"""
+    experts = []
+    for sub in subs:
+        expert, jobs = _prepare_expert(grid, sub, cfg, lr0, warm=warm_of(sub), stop_losses=stops_of(sub),
+                                       device=device, group=group)
+        try:
             for attr, tr, ff in jobs:
-                loss, epochs = next(results)
+                loss, epochs = tr.run()
                 setattr(expert, attr, NetRecord(params=tr.weights(), ff=ff, final_loss=float(loss), epochs=epochs))
-            if expert.voxel_regressor is None:
-                logger.warning("expert %d: no active voxels, value regressor skipped", expert.id)
-            experts.append(expert)
-        return experts
-    finally:
-        for tr in trainers:
-            tr.close()
+        finally:
+            for _, tr, _ in jobs:
+                tr.close()
+        if expert.voxel_regressor is None:
+            logger.warning("expert %d: no active voxels, value regressor skipped", expert.id)
+        experts.append(expert)
+    return experts
 
 
 def encode(grid, cfg, weight_precision: int = 32, workers: int = 1, _warm=None, _lr0=None, _stop_losses=None,

@@ -286,6 +286,99 @@ class LeafBitsMap(MutableMapping):
         self._index, self._extra = None, {}
 
 
+class L1TileMap(MutableMapping):
+    """Array-backed ``{level-1 node origin: {slot: tile value}}`` (the
+    reference's ``UpperTree.l1_tiles`` dict of dicts, encoder.py:512-517): a
+    mapping for the reference's readers (container writer, decoder loops) that
+    hands the device decode its records as columns without a per-record
+    conversion.  Rows are grouped per node in insertion order."""
+
+    def __init__(self, items=None):
+        self._org = np.zeros((0, 3), np.int64)
+        self._cnt = np.zeros(0, np.int64)
+        self._slot = np.zeros(0, np.int64)
+        self._val = np.zeros(0, np.float32)
+        self._extra = {}  # nodes assigned one by one (merged on arrays())
+        if items:
+            for k, v in (items.items() if hasattr(items, "items") else items):
+                self[k] = v
+
+    @classmethod
+    def from_arrays(cls, node_origins, counts, slots, values) -> "L1TileMap":
+        m = cls()
+        m._org = np.asarray(node_origins, np.int64).reshape(-1, 3).copy()
+        m._cnt = np.asarray(counts, np.int64).reshape(-1).copy()
+        m._slot = np.asarray(slots, np.int64).reshape(-1).copy()
+        m._val = np.asarray(values, np.float32).reshape(-1).copy()
+        if m._org.shape[0] != m._cnt.shape[0] or int(m._cnt.sum()) != m._slot.shape[0] != m._val.shape[0]:
+            raise ValueError("tile map columns disagree")
+        return m
+
+    def arrays(self):
+        """(node origins (k, 3), records per node (k,), slots (n,), values (n,))."""
+        if self._extra:
+            org = [self._org] + [np.asarray([k], np.int64) for k in self._extra]
+            cnt = [self._cnt] + [np.asarray([len(d)], np.int64) for d in self._extra.values()]
+            sl = [self._slot] + [np.fromiter(d.keys(), np.int64, len(d)) for d in self._extra.values()]
+            vl = [self._val] + [np.fromiter(d.values(), np.float32, len(d)) for d in self._extra.values()]
+            self._org, self._cnt = np.concatenate(org), np.concatenate(cnt)
+            self._slot, self._val = np.concatenate(sl), np.concatenate(vl)
+            self._extra = {}
+        return self._org, self._cnt, self._slot, self._val
+
+    def _rows(self):
+        return {tuple(int(v) for v in o): i for i, o in enumerate(self._org)}
+
+    def __getitem__(self, key):
+        key = tuple(int(v) for v in key)
+        if key in self._extra:
+            return self._extra[key]
+        i = self._rows().get(key)
+        if i is None:
+            raise KeyError(key)
+        s = int(self._cnt[:i].sum())
+        e = s + int(self._cnt[i])
+        return dict(zip(self._slot[s:e].tolist(), self._val[s:e].astype(np.float64).tolist()))
+
+    def __setitem__(self, key, value):
+        key = tuple(int(v) for v in key)
+        if key in self._rows():
+            del self[key]
+        self._extra[key] = {int(k): float(v) for k, v in dict(value).items()}
+
+    def __delitem__(self, key):
+        key = tuple(int(v) for v in key)
+        if key in self._extra:
+            del self._extra[key]
+            return
+        i = self._rows().get(key)
+        if i is None:
+            raise KeyError(key)
+        s = int(self._cnt[:i].sum())
+        e = s + int(self._cnt[i])
+        self._org = np.delete(self._org, i, axis=0)
+        self._cnt = np.delete(self._cnt, i)
+        self._slot = np.delete(self._slot, np.s_[s:e])
+        self._val = np.delete(self._val, np.s_[s:e])
+
+    def __iter__(self):
+        self.arrays()
+        return (tuple(int(v) for v in o) for o in self._org)
+
+    def __len__(self) -> int:
+        return self._org.shape[0] + len(self._extra)
+
+    def __repr__(self) -> str:
+        return f"L1TileMap(nodes={len(self)}, records={int(self._cnt.sum())})"
+
+    def __getstate__(self):
+        return self.arrays()
+
+    def __setstate__(self, st):
+        self._org, self._cnt, self._slot, self._val = st
+        self._extra = {}
+
+
 @dataclass
 class UpperTree:
     root_tiles: Dict[Coord, Tuple[float, bool]] = field(default_factory=dict)

@@ -150,8 +150,10 @@ def test_corrupt_containers_raise_svcodec_error(golden):
     # a level-1 patch outside every level-1 node
     c = copy.deepcopy(base)
     c.experts[0].patches.l1.append(((1 << 20, 0, 0), 1))
+    with pytest.raises(SvcodecError):  # patch slots are resolved on the device; raised at the first host access
+        DeviceModel(c).decode(True).check()
     with pytest.raises(SvcodecError):
-        DeviceModel(c).decode(True)
+        decode_full(c)
     # a level-0 patch inside a node but in a slot that decodes to no leaf
     c = copy.deepcopy(base)
     m = DeviceModel(c)

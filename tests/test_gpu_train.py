@@ -516,43 +516,3 @@ def test_data_parallel_phases_equal_fused_epochs():
     np.testing.assert_allclose(dp.status()[2][:10], fused.status()[2][:10], rtol=1e-12)
     fused.close()
     dp.close()
-
-
-def test_concurrent_training_equals_sequential_and_is_deterministic():
-    """encoder.run_concurrent (all nets of a container at once, one stream and
-    an SM share each) against training each net alone: the same epochs and
-    losses up to the gradient summation order (the CTA count), and
-    bit-identical when repeated."""
-    from paper_2208_04448_b200.encoder import run_concurrent
-    rng = np.random.default_rng(21)
-    jobs = []
-    for k, (w, m, n, loss) in enumerate([(48, 48, 20000, "mse"), (96, 96, 150000, "mse"), (64, 64, 90000, "bce")]):
-        x = rng.uniform(0, 1, (n, 3)).astype(np.float32)
-        y = (np.sin(4 * x[:, 0] + k) * np.cos(3 * x[:, 1])).astype(np.float32)
-        if loss == "bce":
-            y = (y > 0).astype(np.float32)
-        ff = FourierFeatures(m, 5.0, 30 + k)
-        p0 = init_mlp(2 * m, [w, w, w], 1, Activation("sine", 3.0), "binary" if loss == "bce" else "linear", 40 + k)
-        jobs.append((p0, ff, x, y, loss))
-    cfg = tiny_cfg(max_epochs=150, batch_size=65536, lr=1e-3, activation="sine", frequency=3.0)
-
-    def make():
-        return [DeviceTrainer(p0, ff, x, y, loss, cfg, 1e-3, 50 + i, x.shape[0] > 65536, -1.0, DEV)
-                for i, (p0, ff, x, y, loss) in enumerate(jobs)]
-
-    seq = make()
-    ref = [t.run() for t in seq]
-    conc = make()
-    got = run_concurrent(conc)
-    again = make()
-    got2 = run_concurrent(again)
-    for a, b, c2, ta, tb, tc in zip(ref, got, got2, seq, conc, again):
-        assert a[1] == b[1] == c2[1] == 150
-        la, lb = ta.status()[2][:150], tb.status()[2][:150]
-        np.testing.assert_allclose(lb, la, rtol=2e-3)
-        np.testing.assert_array_equal(lb, tc.status()[2][:150])
-        for (wb, bb), (wc, bc) in zip(tb.weights().layers, tc.weights().layers):
-            np.testing.assert_array_equal(wb, wc)
-            np.testing.assert_array_equal(bb, bc)
-    for t in seq + conc + again:
-        t.close()

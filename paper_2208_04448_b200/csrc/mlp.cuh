@@ -723,9 +723,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       return;
     }
     const bool covered = den > 0.0;
-    if (covered) {
+    if (covered && den != 1.0) {  // a single covering expert has den == 1 (x / 1 == x): skip the f64 divides
 #pragma unroll
-      for (int k = 0; k < kMaxOut; ++k) num[k] = den == 1.0 ? num[k] : num[k] / den;  // x / 1 == x
+      for (int k = 0; k < kMaxOut; ++k) num[k] = num[k] / den;
     }
     switch (a.out_mode) {
       case OUT_PROBS:

@@ -890,25 +890,35 @@ class HybridGrid:
         returns all results in order (gathered over NCCL); other ranks return
         (None, None).  SURVEY.md §8(e) "Random query"."""
         c = np.asarray(coords)
-        if c.dtype != np.int32:
-            c = c.astype(np.int64)
-        c = c.reshape(-1, 3)
         lim = 1 << 30
-        if c.size and (c.max() >= lim or c.min() <= -lim):  # grid.py:69-71, no abs() overflow on int32
-            raise SvcodecError("coordinate outside legal range +-2^30")
+        if c.dtype != np.int32:
+            c = c.astype(np.int64).reshape(-1, 3)
+            if c.size and (c.max() >= lim or c.min() <= -lim):  # grid.py:69-71
+                raise SvcodecError("coordinate outside legal range +-2^30")
+            c = c.astype(np.int32)
+        c = c.reshape(-1, 3)
         if group is not None and _world(group) > 1:
             import torch.distributed as dist
             lo, hi = shard_range(c.shape[0], dist.get_rank(group), _world(group))
             c = c[lo:hi]
-        d = torch.from_numpy(np.ascontiguousarray(c, dtype=np.int32)).to(self.model.dev)
+        d = torch.from_numpy(np.ascontiguousarray(c)).to(self.model.dev)
+        # int32 input: the +-2^30 range check runs on the device, read with the results
+        bad = ((d >= lim) | (d <= -lim)).any().view(1).to(torch.uint8)
         v, a = self.query_device(d)
         if group is not None and _world(group) > 1:
+            import torch.distributed as dist
+            bad32 = bad.to(torch.int32)
+            dist.all_reduce(bad32, op=dist.ReduceOp.MAX, group=group)
             g = gather_rows([v, a], group)
             if g is None:
                 return None, None
             v, a = g
-        v, a = _to_host([v, a])
-        return v.copy(), a.view(np.bool_).copy()
+            bad = bad32.to(torch.uint8)
+        v, a, bad = _to_host([v, a, bad])
+        if bad.any():
+            raise SvcodecError("coordinate outside legal range +-2^30")
+        # views of a pooled pinned block (free again once the caller drops them)
+        return v, a.view(np.bool_)
 
 
 def make_hybrid(c, device=None) -> HybridGrid:

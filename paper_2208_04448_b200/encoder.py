@@ -383,9 +383,20 @@ class DeviceTrainer:
             torch.cuda.synchronize(self.dev)
             g = torch.cuda.CUDAGraph()
             cap = torch.cuda.Stream(self.dev)
-            with torch.cuda.stream(cap):
-                with torch.cuda.graph(g, stream=cap):
-                    self._epoch_dp(cap.cuda_stream)
+            try:
+                with torch.cuda.stream(cap):
+                    with torch.cuda.graph(g, stream=cap):
+                        self._epoch_dp(cap.cuda_stream)
+            except Exception as exc:  # noqa: BLE001 -- a communicator that cannot be captured: eager epochs
+                logger.warning("data-parallel epoch graph capture failed (%s); running eager epochs", exc)
+                torch.cuda.synchronize(self.dev)
+                self._graphable = False
+                for _ in range(k):
+                    try:
+                        self._epoch_dp(st)
+                    except _lib.NvdbError:  # the failed capture counted one epoch on the host: the run is complete
+                        break
+                return
             self._graph = g  # capture does not execute: every epoch below is a replay
         for _ in range(k):
             self._graph.replay()

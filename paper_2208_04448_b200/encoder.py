@@ -394,7 +394,7 @@ class DeviceTrainer:
                 for _ in range(k):
                     try:
                         self._epoch_dp(st)
-                    except _lib.NvdbError:  # the failed capture counted one epoch on the host: the run is complete
+                    except (ValueError, _lib.NvdbError):  # the failed capture counted one host epoch: run complete
                         break
                 return
             self._graph = g  # capture does not execute: every epoch below is a replay

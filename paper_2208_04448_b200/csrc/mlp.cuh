@@ -492,29 +492,33 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
         const float bxa[4] = {bx.x, bx.y, bx.z, bx.w}, bya[4] = {by.x, by.y, by.z, by.w};
         const float bza[4] = {bz.x, bz.y, bz.z, bz.w};
         const float cba[4] = {la.x, la.z, lb.x, lb.z}, sba[4] = {la.y, la.w, lb.y, lb.w};
-        float cs[4][2], sn[4][2], c2[4];
+        // (cos, sin) pairs on the packed fp32x2 pipe (FFMA2: one issue per pair,
+        // per-lane IEEE fma, so the values are those of the scalar recurrence)
+        float2 u[4][2], c2[4];
         uint32_t hp[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float th = fmaf(x2, bza[q], fmaf(x1, bya[q], x0 * bxa[q]));
-          __sincosf(th, &sn[q][0], &cs[q][0]);
-          cs[q][1] = fmaf(cs[q][0], cba[q], -sn[q][0] * sba[q]);
-          sn[q][1] = fmaf(cs[q][0], sba[q], sn[q][0] * cba[q]);
-          c2[q] = 2.0f * cba[q];
-          hp[q] = pack_half2(cs[q][0], sn[q][0]);
+          float s0, c0;
+          __sincosf(th, &s0, &c0);
+          u[q][0] = make_float2(c0, s0);
+          // (c0 cb - s0 sb, c0 sb + s0 cb): the products s0 * (-sb, cb) rounded, then one fma each
+          u[q][1] = __ffma2_rn(make_float2(c0, c0), make_float2(cba[q], sba[q]),
+                               __fmul2_rn(make_float2(s0, s0), make_float2(-sba[q], cba[q])));
+          c2[q] = make_float2(2.0f * cba[q], 2.0f * cba[q]);
+          hp[q] = pack_half2(c0, s0);
         }
         st_shared_v4(buf + kmajor_offset(lii * 64 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) hp[q] = pack_half2(cs[q][1], sn[q][1]);
+        for (int q = 0; q < 4; ++q) hp[q] = pack_half2(u[q][1].x, u[q][1].y);
         st_shared_v4(buf + kmajor_offset(lii * 64 + 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
 #pragma unroll
         for (int jy = 2; jy < 8; ++jy) {
           const int cur = jy & 1;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            cs[q][cur] = fmaf(c2[q], cs[q][cur ^ 1], -cs[q][cur]);
-            sn[q][cur] = fmaf(c2[q], sn[q][cur ^ 1], -sn[q][cur]);
-            hp[q] = pack_half2(cs[q][cur], sn[q][cur]);
+            u[q][cur] = __ffma2_rn(c2[q], u[q][cur ^ 1], make_float2(-u[q][cur].x, -u[q][cur].y));
+            hp[q] = pack_half2(u[q][cur].x, u[q][cur].y);
           }
           st_shared_v4(buf + kmajor_offset(lii * 64 + jy * 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
         }
@@ -595,10 +599,15 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
             // weights stay unscaled (exact for 16-bit containers), omega in fp32
             const float4 bq = reinterpret_cast<const float4*>(bl + (c0 + b) * 16)[q4];
             if constexpr (ACT == ACT_SINE) {
-              av[4 * q4 + 0] = act_fn(act, fmaf(v[b][4 * q4 + 0], om, bq.x));
-              av[4 * q4 + 1] = act_fn(act, fmaf(v[b][4 * q4 + 1], om, bq.y));
-              av[4 * q4 + 2] = act_fn(act, fmaf(v[b][4 * q4 + 2], om, bq.z));
-              av[4 * q4 + 3] = act_fn(act, fmaf(v[b][4 * q4 + 3], om, bq.w));
+              const float2 om2 = make_float2(om, om);
+              const float2 z01 = __ffma2_rn(make_float2(v[b][4 * q4 + 0], v[b][4 * q4 + 1]), om2,
+                                            make_float2(bq.x, bq.y));
+              const float2 z23 = __ffma2_rn(make_float2(v[b][4 * q4 + 2], v[b][4 * q4 + 3]), om2,
+                                            make_float2(bq.z, bq.w));
+              av[4 * q4 + 0] = act_fn(act, z01.x);
+              av[4 * q4 + 1] = act_fn(act, z01.y);
+              av[4 * q4 + 2] = act_fn(act, z23.x);
+              av[4 * q4 + 3] = act_fn(act, z23.y);
             } else {
               av[4 * q4 + 0] = act_fn(act, v[b][4 * q4 + 0] + bq.x);
               av[4 * q4 + 1] = act_fn(act, v[b][4 * q4 + 1] + bq.y);
@@ -618,15 +627,18 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
             for (int k = 0; k < kMaxOut; ++k) {
               if (k < out_dim) {
                 const float4* hw = reinterpret_cast<const float4*>(s_headw + k * width + (c0 + b) * 16);
-                float sp[4];
+                // four short partial sums as two fp32x2 chains (even / odd columns)
+                float2 sp[2];
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {  // four short partial sums
-                  const float4 w4 = hw[q4];
-                  sp[q4] = fmaf(av[4 * q4], w4.x, av[4 * q4 + 1] * w4.y);
-                  sp[q4] = fmaf(av[4 * q4 + 2], w4.z, sp[q4]);
-                  sp[q4] = fmaf(av[4 * q4 + 3], w4.w, sp[q4]);
+                for (int h2 = 0; h2 < 2; ++h2) {
+                  const float4 wa = hw[2 * h2], wb = hw[2 * h2 + 1];
+                  const float* a8 = av + 8 * h2;
+                  sp[h2] = __fmul2_rn(make_float2(a8[0], a8[1]), make_float2(wa.x, wa.y));
+                  sp[h2] = __ffma2_rn(make_float2(a8[2], a8[3]), make_float2(wa.z, wa.w), sp[h2]);
+                  sp[h2] = __ffma2_rn(make_float2(a8[4], a8[5]), make_float2(wb.x, wb.y), sp[h2]);
+                  sp[h2] = __ffma2_rn(make_float2(a8[6], a8[7]), make_float2(wb.z, wb.w), sp[h2]);
                 }
-                y[k] += (sp[0] + sp[1]) + (sp[2] + sp[3]);
+                y[k] += (sp[0].x + sp[0].y) + (sp[1].x + sp[1].y);
               }
             }
           }

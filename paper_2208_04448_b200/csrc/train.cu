@@ -15,7 +15,9 @@
 //   k_train_adam    fixed-order reduction of the partials, bias-corrected Adam
 //                   on fp32 master weights (numpy's op order and float32
 //                   constants), refreshed fp16 weight image, batch loss,
-//                   early stop flag.
+//                   early stop flag; its last block advances the epoch.
+//   (k_train_fb and k_train_wgrad run as one launch, k_train_fbwg, when they
+//   share the tile partition.)
 //
 // Loss scaling: dL/dout is kept without the 1/size factor (fp16 would
 // underflow at size 65536); the factor, and omega / amplitude folded into the
@@ -294,6 +296,21 @@ struct FbArgs {
   uint32_t w_off, region_off, region_bytes, small_off, bar_off;
 };
 
+// tile-image traffic between the fwd/dgrad and weight-gradient phases: the
+// images are written with L2 evict_last and read once with evict_first, so
+// the most recent tiles (read first by the weight-gradient phase) stay in L2
+#ifndef NVDB_L2HINT
+#define NVDB_L2HINT 1
+#endif
+__device__ __forceinline__ void img_store(void* p, uint4 v, uint64_t pol) {
+  if (NVDB_L2HINT) st_global_v4_hint(p, v, pol);
+  else *reinterpret_cast<uint4*>(p) = v;
+}
+__device__ __forceinline__ void img_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  if (NVDB_L2HINT) bulk_g2s_hint(dst, src, bytes, bar, pol);
+  else bulk_g2s(dst, src, bytes, bar);
+}
+
 __device__ __forceinline__ float act_deriv_from(int act, float zp) {
   if (act == ACT_SINE) return __cosf(zp);
   if (act == ACT_TANH) {
@@ -363,6 +380,7 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
   const int64_t t0 = a.tile_begin + blockIdx.x * per, t1 = min(a.tile_end, t0 + per);
   double loss_acc = 0.0;
   const size_t tile_elems = (size_t)kTileM * width;
+  const uint64_t pol_img = l2_evict_last();  // tile images: re-read by the weight-gradient phase
 
   // inputs of this thread's row, loaded one tile ahead (the gather through the
   // sampled indices is two dependent global loads)
@@ -405,8 +423,8 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
         }
         const uint32_t fo = kmajor_offset(row, half * 32 + q * 8, kTileM);
         st_shared_v4(buf + fo, h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.feat_img) + (size_t)tau * kTileM * k0 * 2 +
-                                  (size_t)ch * kChunkBytes + fo) = make_uint4(h[0], h[1], h[2], h[3]);
+        img_store(reinterpret_cast<uint8_t*>(a.feat_img) + (size_t)tau * kTileM * k0 * 2 + (size_t)ch * kChunkBytes + fo,
+                  make_uint4(h[0], h[1], h[2], h[3]), pol_img);
       }
       fence_async_smem();
       tc_fence_before();
@@ -466,8 +484,8 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           const uint32_t p4 = pack_half2(av[8], av[9]), p5 = pack_half2(av[10], av[11]);
           const uint32_t p6 = pack_half2(av[12], av[13]), p7 = pack_half2(av[14], av[15]);
           const uint32_t o0 = kmajor_offset(row, cc * 16, kTileM), o1 = kmajor_offset(row, cc * 16 + 8, kTileM);
-          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o0) = make_uint4(p0, p1, p2, p3);
-          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gact) + o1) = make_uint4(p4, p5, p6, p7);
+          img_store(reinterpret_cast<uint8_t*>(gact) + o0, make_uint4(p0, p1, p2, p3), pol_img);
+          img_store(reinterpret_cast<uint8_t*>(gact) + o1, make_uint4(p4, p5, p6, p7), pol_img);
           if (!last) {
             st_shared_v4(region_s + o0, p0, p1, p2, p3);
             st_shared_v4(region_s + o1, p4, p5, p6, p7);
@@ -545,9 +563,9 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
         }
       }
       uint8_t* gd = reinterpret_cast<uint8_t*>(a.dlt_img + (size_t)tau * kTileM * 16);
-      *reinterpret_cast<uint4*>(gd + kmajor_offset(row, 0, kTileM)) =
-          make_uint4(pack_half2(dl[0], dl[1]), pack_half2(dl[2], 0.f), 0u, 0u);
-      *reinterpret_cast<uint4*>(gd + kmajor_offset(row, 8, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
+      img_store(gd + kmajor_offset(row, 0, kTileM), make_uint4(pack_half2(dl[0], dl[1]), pack_half2(dl[2], 0.f), 0u, 0u),
+                pol_img);
+      img_store(gd + kmajor_offset(row, 8, kTileM), make_uint4(0u, 0u, 0u, 0u), pol_img);
     }
     // deterministic loss sum: warp shuffle, then fixed warp order
     float ls = lterm;
@@ -612,8 +630,8 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           const uint32_t p4 = pack_half2(dz[8], dz[9]), p5 = pack_half2(dz[10], dz[11]);
           const uint32_t p6 = pack_half2(dz[12], dz[13]), p7 = pack_half2(dz[14], dz[15]);
           const uint32_t o0 = kmajor_offset(row, cc * 16, kTileM), o1 = kmajor_offset(row, cc * 16 + 8, kTileM);
-          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o0) = make_uint4(p0, p1, p2, p3);
-          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(gdz) + o1) = make_uint4(p4, p5, p6, p7);
+          img_store(reinterpret_cast<uint8_t*>(gdz) + o0, make_uint4(p0, p1, p2, p3), pol_img);
+          img_store(reinterpret_cast<uint8_t*>(gdz) + o1, make_uint4(p4, p5, p6, p7), pol_img);
           if (l > 0) {
             st_shared_v4(region_s + o0, p0, p1, p2, p3);
             st_shared_v4(region_s + o1, p4, p5, p6, p7);
@@ -740,6 +758,7 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
   const int64_t per = (a.tile_end - a.tile_begin + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = a.tile_begin + blockIdx.x * per, t1 = min(a.tile_end, t0 + per);
   const size_t tbytes = (size_t)kTileM * W * 2;
+  const uint64_t pol_rd = l2_evict_first();  // each tile image is read once
   const uint32_t sfe = smem_addr(s_feat), son = smem_addr(s_ones);
   const int nmt = (k0 + 127) / 128;  // M tiles of 128 features
   const int nst = mode == 1 ? 1 : depth + 1;  // load stages per tile: dz0 | (a0,dz1) .. | (a_{d-1}, dlt)
@@ -766,16 +785,16 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
     if (s > 0) bytes += (s == depth) ? (uint32_t)(kTileM * 16 * 2) : (uint32_t)tbytes;
     mbar_arrive_expect_tx(&bars[b], bytes);
     if (s == 0) {
-      bulk_g2s(s_dz[b], reinterpret_cast<const uint8_t*>(a.dz_img) + tau * tbytes, (uint32_t)tbytes, &bars[b]);
+      img_load(s_dz[b], reinterpret_cast<const uint8_t*>(a.dz_img) + tau * tbytes, (uint32_t)tbytes, &bars[b], pol_rd);
     } else {
-      bulk_g2s(s_act[b], reinterpret_cast<const uint8_t*>(a.act_img) + ((size_t)(s - 1) * ntiles + tau) * tbytes,
-               (uint32_t)tbytes, &bars[b]);
+      img_load(s_act[b], reinterpret_cast<const uint8_t*>(a.act_img) + ((size_t)(s - 1) * ntiles + tau) * tbytes,
+               (uint32_t)tbytes, &bars[b], pol_rd);
       if (s == depth)
-        bulk_g2s(s_dlt[b], reinterpret_cast<const uint8_t*>(a.dlt_img) + (size_t)tau * kTileM * 16 * 2,
-                 kTileM * 16 * 2, &bars[b]);
+        img_load(s_dlt[b], reinterpret_cast<const uint8_t*>(a.dlt_img) + (size_t)tau * kTileM * 16 * 2,
+                 kTileM * 16 * 2, &bars[b], pol_rd);
       else
-        bulk_g2s(s_dz[b], reinterpret_cast<const uint8_t*>(a.dz_img) + ((size_t)s * ntiles + tau) * tbytes,
-                 (uint32_t)tbytes, &bars[b]);
+        img_load(s_dz[b], reinterpret_cast<const uint8_t*>(a.dz_img) + ((size_t)s * ntiles + tau) * tbytes,
+                 (uint32_t)tbytes, &bars[b], pol_rd);
     }
   };
   auto wait_full = [&](int64_t q) {
@@ -796,9 +815,9 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
     if (rb == 1 && pr1) { mbar_wait(&bars[5], (nring1 - 1u) & 1u); pr1 = false; }
     const uint32_t nb = (uint32_t)min(128, k0 - j * 128) * kTileM * 2;
     mbar_arrive_expect_tx(&bars[7 + rb], nb);
-    bulk_g2s(s_feat + rb * 32768,
+    img_load(s_feat + rb * 32768,
              reinterpret_cast<const uint8_t*>(a.feat_img) + (size_t)tt * kTileM * k0 * 2 + (size_t)j * 32768, nb,
-             &bars[7 + rb]);
+             &bars[7 + rb], pol_rd);
   };
   if (t == 0 && nstages > 0) {
     issue_load(0);
@@ -1047,6 +1066,18 @@ __device__ __forceinline__ float reduce_partials32(const float* __restrict__ par
   float g0 = 0.f, g1 = 0.f;
   if (q < P) {
     int c = w;
+    // eight loads in flight per thread (the sums stay in the chains' order:
+    // c = w, w + 16, ... into g0 and c = w + 8, w + 24, ... into g1)
+    for (; c + 56 < ncta; c += 64) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = partial[(size_t)(c + 8 * j) * P + q];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        g0 += v[j];
+        g1 += v[j + 1];
+      }
+    }
     for (; c + 8 < ncta; c += 16) {
       g0 += partial[(size_t)c * P + q];
       g1 += partial[(size_t)(c + 8) * P + q];
@@ -1106,8 +1137,12 @@ struct AdamArgs {
   double target;
   int32_t* epoch;
   const int32_t* stopped;
-  int32_t* stop_next;  // set when this epoch's pre-update loss reached the target (applied by k_train_advance)
+  int32_t* stop_next;  // set when this epoch's pre-update loss reached the target (applied by the last block of k_train_adam)
   double* loss_hist;
+  unsigned int* done_blocks;  // finished-block counter (zero between launches)
+  int32_t* stopped_w;         // == stopped (written by the last block)
+  int32_t* epochs_done;
+  int32_t max_epochs;
   // fused single-rank form: reduce the per-CTA partials here (grad == nullptr)
   const float* partial;
   int32_t ncta;
@@ -1124,27 +1159,42 @@ __global__ void __launch_bounds__(kRedThreads) k_train_adam(AdamArgs a) {
   const float lr = a.lr[e], c1 = a.c1[e], c2 = a.c2[e];
   __shared__ float s_sum[8 * 32];
   const int64_t q = blockIdx.x * (int64_t)kRedParams + (threadIdx.x & 31);
+  // the update's per-parameter state is loaded before the reduction (its
+  // latency overlaps the partial sums instead of trailing them)
+  const bool upd_lane = threadIdx.x < 32 && q < a.P;
+  float gs = 0.f, m0 = 0.f, v0 = 0.f, w0 = 0.f, fold = 0.f;
+  int32_t io = -1, io2 = -1, fd = -1;
+  if (upd_lane) {
+    gs = a.gscale[q];
+    m0 = a.mom[q];
+    v0 = a.vel[q];
+    w0 = a.wmaster[q];
+    io = a.img_off[q];
+    io2 = a.img_off2[q];
+    fold = a.img_fold[q];
+    fd = a.f32_dst[q];
+  }
   float gsum = 0.f;
   if (!a.grad) gsum = reduce_partials32(a.partial, a.ncta, a.P, q, s_sum);  // block-uniform branch
-  if (threadIdx.x < 32 && q < a.P) {
+  if (upd_lane) {
     if (a.grad) gsum = a.grad[q];
-    const float g = gsum * a.gscale[q];
+    const float g = gsum * gs;
     // numpy float32 arithmetic with weak python scalars (neural.py:508-523)
-    float m = a.mom[q] * 0.9f;
+    float m = m0 * 0.9f;
     m = m + 0.1f * g;
-    float v = a.vel[q] * 0.999f;
+    float v = v0 * 0.999f;
     v = v + 0.001f * (g * g);
     a.mom[q] = m;
     a.vel[q] = v;
     const float upd = lr * (m / c1) / (sqrtf(v / c2) + 1e-8f);
-    const float w = a.wmaster[q] - upd;
+    const float w = w0 - upd;
     a.wmaster[q] = w;
-    if (a.img_off[q] >= 0) {
-      __half h = __float2half_rn(w * a.img_fold[q]);
-      a.wimg[a.img_off[q]] = *reinterpret_cast<uint16_t*>(&h);
-      if (a.img_off2[q] >= 0) a.wimg[a.img_off2[q]] = *reinterpret_cast<uint16_t*>(&h);
+    if (io >= 0) {
+      __half h = __float2half_rn(w * fold);
+      a.wimg[io] = *reinterpret_cast<uint16_t*>(&h);
+      if (io2 >= 0) a.wimg[io2] = *reinterpret_cast<uint16_t*>(&h);
     }
-    if (a.f32_dst[q] >= 0) a.f32_block[a.f32_dst[q]] = w * a.img_fold[q];
+    if (fd >= 0) a.f32_block[fd] = w * fold;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     double sl;
@@ -1158,19 +1208,25 @@ __global__ void __launch_bounds__(kRedThreads) k_train_adam(AdamArgs a) {
     a.loss_hist[e] = loss;
     if (loss < a.target) *a.stop_next = 1;
   }
-}
-
-// the stop decision of k_train_adam takes effect here, after every block of
-// the update ran (the reference applies the stopping epoch's update, then breaks)
-__global__ void k_train_advance(int32_t* epoch, int32_t* stopped, int32_t* epochs_done, const int32_t* stop_next,
-                                int32_t max_epochs) {
-  if (*stopped) return;
-  if (*stop_next || *epoch + 1 >= max_epochs) {  // early stop, or the last epoch ran
-    *stopped = 1;
-    *epochs_done = *epoch + 1;
-  } else {
-    *epoch += 1;
-    *epochs_done = *epoch;
+  // the last block to finish applies the epoch advance after every block's
+  // update (the reference applies the stopping epoch's update, then breaks)
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.done_blocks, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    *a.done_blocks = 0;
+    if (*reinterpret_cast<volatile int32_t*>(a.stop_next) || e + 1 >= a.max_epochs) {
+      a.stopped_w[0] = 1;
+      *a.epochs_done = e + 1;
+    } else {
+      *a.epoch = e + 1;
+      *a.epochs_done = e + 1;
+    }
   }
 }
 
@@ -1179,6 +1235,15 @@ __global__ void k_train_advance(int32_t* epoch, int32_t* stopped, int32_t* epoch
 }  // namespace
 
 // ------------------------------------------------------------------ host trainer
+// CTAs that get tiles under the kernels' contiguous partition of n tiles over
+// g CTAs (per = ceil(n / g)): idle CTAs would only add zero partials to the
+// Adam reduction
+static int busy_grid(int64_t n, int64_t g) {
+  n = std::max<int64_t>(n, 1);
+  const int64_t per = (n + g - 1) / g;
+  return (int)((n + per - 1) / per);
+}
+
 struct nvdb_trainer {
   nvdb_train_desc d{};
   int W = 0, Wr = 0, k0 = 0, depth = 0, out_dim = 0, m = 0;
@@ -1224,7 +1289,7 @@ struct nvdb_trainer {
   float* lr = nullptr;
   float* c1 = nullptr;
   float* c2 = nullptr;
-  int32_t* ctl = nullptr;  // epoch, stopped, epochs_done
+  int32_t* ctl = nullptr;  // epoch, stopped, epochs_done, stop_next, Adam done-block counter
   double* loss_hist = nullptr;
   int64_t* dpoff = nullptr;
   std::vector<std::pair<void*, size_t>> owned;  // device blocks from the block cache
@@ -1572,6 +1637,7 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   const int64_t mine = std::max<int64_t>(t->tile_end - t->tile_begin, 1);
   t->fb_grid = (int)std::min<int64_t>(num_sms(), (mine + t->nwg - 1) / t->nwg);
   t->wg_grid = (int)std::min<int64_t>(num_sms(), mine);
+  if (t->fb_grid == t->wg_grid) t->fb_grid = t->wg_grid = busy_grid(mine, t->wg_grid);
   if (t->wide) {
     t->fb_grid = (int)std::min<int64_t>(num_sms(), (mine + t->lw.engines - 1) / t->lw.engines);
     // weight-gradient blocks: every 128-row block of every layer's inputs (+ the
@@ -1616,13 +1682,13 @@ extern "C" int nvdb_trainer_create(const nvdb_train_desc* d, nvdb_trainer** out)
   chk(dalloc(t, &t->loss_part, (size_t)t->fb_grid));
   chk(dalloc(t, &t->grad, (size_t)P + 2));  // + the loss (hi, lo) pair
   chk(dalloc(t, &t->lossbuf, 1));
-  chk(dalloc(t, &t->ctl, 4));
+  chk(dalloc(t, &t->ctl, 8));
   chk(dalloc(t, &t->loss_hist, d->max_epochs));
   chk(dalloc(t, &t->lr, d->max_epochs));
   chk(dalloc(t, &t->c1, d->max_epochs));
   chk(dalloc(t, &t->c2, d->max_epochs));
   if (rc) return rc;
-  NVDB_CUDA_TRY(cudaMemset(t->ctl, 0, 16));
+  NVDB_CUDA_TRY(cudaMemset(t->ctl, 0, 32));
   NVDB_CUDA_TRY(cudaMemset(t->loss_hist, 0, 8 * d->max_epochs));
   NVDB_CUDA_TRY(cudaMemcpy(t->lr, d->lr, 4 * d->max_epochs, cudaMemcpyHostToDevice));
   NVDB_CUDA_TRY(cudaMemcpy(t->c1, d->c1, 4 * d->max_epochs, cudaMemcpyHostToDevice));
@@ -1882,9 +1948,11 @@ int enqueue_phase(nvdb_trainer* t, int phase, cudaStream_t st, bool fused_update
       aa.nloss = t->fb_grid;
     }
     aa.loss_hist = t->loss_hist;
+    aa.done_blocks = reinterpret_cast<unsigned int*>(t->ctl + 4);
+    aa.stopped_w = stopped;
+    aa.epochs_done = t->ctl + 2;
+    aa.max_epochs = d.max_epochs;
     k_train_adam<<<(int)((t->P + kRedParams - 1) / kRedParams), kRedThreads, 0, st>>>(aa);
-    NVDB_CHECK_LAUNCH();
-    k_train_advance<<<1, 1, 0, st>>>(ep, stopped, t->ctl + 2, t->ctl + 3, d.max_epochs);
     NVDB_CHECK_LAUNCH();
     ++t->host_epoch;
     NVDB_CUDA_TRY(record_done(t, st));
@@ -1918,7 +1986,8 @@ extern "C" int nvdb_trainer_set_ctas(nvdb_trainer* t, int32_t ctas) {
     t->nsplit = std::max(1, std::min(t->nsplit0, (c + t->nblocks - 1) / t->nblocks));
     t->wg_grid = t->nsplit;
   } else if (t->fb_grid0 == t->wg_grid0) {
-    t->wg_grid = t->fb_grid;  // the fused fwd/bwd + weight-gradient kernel keeps one tile partition
+    // the fused fwd/bwd + weight-gradient kernel keeps one tile partition
+    t->fb_grid = t->wg_grid = busy_grid(t->tile_end - t->tile_begin, t->fb_grid);
   } else {
     t->wg_grid = std::max(1, std::min(t->wg_grid0, c));
   }

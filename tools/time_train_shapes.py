@@ -45,7 +45,8 @@ def main():
         cfg = SimpleNamespace(max_epochs=epochs, decay=0.975, interval=100.0, sample_interval=1, batch_size=65536)
         ff = FourierFeatures(m, scale, 11)
         p0 = init_mlp(2 * m, [width] * depth, 1, Activation("sine", omega), "linear", 12)
-        tr = DeviceTrainer(p0, ff, x, y, "mse", cfg, 1e-3, 13, True, 0.0, dev)
+        tr = DeviceTrainer(p0, ff, x, y, "mse", cfg, 1e-3, 13, True, 0.0, dev,
+                           path=int(os.environ.get("NVDB_TRAIN_PATH", "0")))
         tr.run(8)  # warm
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -28,6 +28,7 @@ from .netset import TAG_CODES, DeviceNetSet
 from .tree import DeviceTree
 
 EVAL_CHUNK = 1 << 24  # points per evaluator call on the multi-expert path
+MAX_CALL = 1 << 30    # points per evaluator call on the single-expert path (int32 tile counts)
 
 
 def _dev(device=None) -> torch.device:
@@ -395,7 +396,7 @@ class DeviceModel:
             return
         fast = self.single and self.has_tag[tag]
         if count is not None:
-            if not fast:
+            if not fast or n > MAX_CALL:
                 n = int(count.item())
                 if n == 0:
                     return
@@ -414,7 +415,7 @@ class DeviceModel:
                     ev1.record()
                     timer.append((tag, count, ev0, ev1))
                 return
-        chunk = n if fast else EVAL_CHUNK
+        chunk = min(n, MAX_CALL) if fast else EVAL_CHUNK
         if src_kind == _lib.SRC_LEAF_VOX and gather is None:
             chunk = max(512, chunk // 512 * 512)
         if src_kind == _lib.SRC_L1_SLOT and gather is None:

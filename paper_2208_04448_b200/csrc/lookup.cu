@@ -9,6 +9,7 @@
 // Integer-only; the traffic is the coordinate read plus a few L2-resident
 // node words per query.
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "tree.cuh"
@@ -17,11 +18,94 @@ using namespace nvdb;
 
 namespace {
 
+constexpr int kRootLinear = 16;  // roots staged in shared memory (and scanned linearly) up to this count
+
+// Level-synchronous resolve of Q queries (tree_resolve's result for each):
+// every level's Q entry loads are issued back to back (predicated, no
+// early exits), so a thread keeps Q independent random loads in flight per
+// level instead of one dependent chain.  Root keys / entries come from
+// shared memory when the block staged them (s_keys != nullptr); larger
+// root tables take the binary search in global memory.
+template <int Q>
+__device__ __forceinline__ void resolve_q(const TreeView& t, const int32_t* s_keys, const uint64_t* s_rent,
+                                          const int (&x)[Q], const int (&y)[Q], const int (&z)[Q], float (&v)[Q],
+                                          uint8_t (&a)[Q], uint8_t (&k)[Q], int32_t (&lf)[Q]) {
+  uint64_t e[Q];
+  if (s_keys && t.nroots <= kRootLinear) {
+    // few roots (the common case): branch-free scan of the staged keys
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      const int rx = x[j] & ~4095, ry = y[j] & ~4095, rz = z[j] & ~4095;
+      e[j] = kEntMiss;
+      for (int r = 0; r < t.nroots; ++r)
+        if (s_keys[3 * r] == rx && s_keys[3 * r + 1] == ry && s_keys[3 * r + 2] == rz) e[j] = s_rent[r];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      const int rx = x[j] & ~4095, ry = y[j] & ~4095, rz = z[j] & ~4095;
+      int lo = 0, hi = t.nroots - 1, r = -1;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const int c = cmp3(t.root_keys + 3 * mid, rx, ry, rz);
+        if (c == 0) {
+          r = mid;
+          break;
+        }
+        if (c < 0) lo = mid + 1;
+        else hi = mid - 1;
+      }
+      e[j] = r < 0 ? kEntMiss : __ldg(reinterpret_cast<const unsigned long long*>(t.root_ent) + r);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {  // level 2
+    const int i2 = (((x[j] & 4095) >> 7) << 10) | (((y[j] & 4095) >> 7) << 5) | ((z[j] & 4095) >> 7);
+    if ((e[j] >> kEntKindShift) == 0)
+      e[j] = __ldg(reinterpret_cast<const unsigned long long*>(t.l2_ent) + (int64_t)(uint32_t)e[j] * 32768 + i2);
+  }
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {  // level 1
+    const int i1 = (((x[j] & 127) >> 3) << 8) | (((y[j] & 127) >> 3) << 4) | ((z[j] & 127) >> 3);
+    if ((e[j] >> kEntKindShift) == 0)
+      e[j] = __ldg(reinterpret_cast<const unsigned long long*>(t.l1_ent) + (int64_t)(uint32_t)e[j] * 4096 + i1);
+  }
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {  // leaf voxel
+    const int i0 = ((x[j] & 7) << 6) | ((y[j] & 7) << 3) | (z[j] & 7);
+    lf[j] = -1;
+    if ((e[j] >> kEntKindShift) == 0) {
+      lf[j] = (int32_t)(uint32_t)e[j];
+      e[j] = __ldg(reinterpret_cast<const unsigned long long*>(t.leaf_ent) + (int64_t)lf[j] * 512 + i0);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    const uint32_t kd = (uint32_t)(e[j] >> kEntKindShift);
+    const bool miss = kd == 3u;
+    v[j] = miss ? t.background : __uint_as_float((uint32_t)e[j]);
+    a[j] = miss ? 0 : (uint8_t)((e[j] >> 32) & 1u);
+    k[j] = miss ? 0 : (uint8_t)kd;
+  }
+}
+
+
 // Four queries per thread: three 16-byte coordinate loads (the thread's 48
-// contiguous bytes), four independent traversals in flight, then one 16-byte
-// value store, one 4-byte active store and one 4-byte kind store.
-__global__ void k_lookup(TreeView t, const int32_t* __restrict__ coords, int64_t n, float* __restrict__ value,
-                         uint8_t* __restrict__ active, uint8_t* __restrict__ kind, int32_t* __restrict__ leaf_out) {
+// contiguous bytes), one level-synchronous resolve, then one 16-byte value
+// store, one 4-byte active store and one 4-byte kind store.
+__global__ void __launch_bounds__(256) k_lookup(TreeView t, const int32_t* __restrict__ coords, int64_t n,
+                                                float* __restrict__ value, uint8_t* __restrict__ active,
+                                                uint8_t* __restrict__ kind, int32_t* __restrict__ leaf_out) {
+  __shared__ int32_t s_keys[3 * kRootLinear];
+  __shared__ uint64_t s_rent[kRootLinear];
+  const bool staged = t.nroots <= kRootLinear;
+  if (staged) {
+    for (int i = threadIdx.x; i < 3 * t.nroots; i += blockDim.x) s_keys[i] = t.root_keys[i];
+    for (int i = threadIdx.x; i < t.nroots; i += blockDim.x) s_rent[i] = t.root_ent[i];
+    __syncthreads();
+  }
+  const int32_t* sk = staged ? s_keys : nullptr;
+  const uint64_t* sr = staged ? s_rent : nullptr;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t nq4 = n >> 2;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq4; q += stride) {
@@ -31,8 +115,7 @@ __global__ void k_lookup(TreeView t, const int32_t* __restrict__ coords, int64_t
     float v[4];
     uint8_t a[4], k[4];
     int32_t lf[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) tree_resolve(t, xs[j], ys[j], zs[j], v[j], a[j], k[j], lf[j]);
+    resolve_q<4>(t, sk, sr, xs, ys, zs, v, a, k, lf);
     __stcs(reinterpret_cast<float4*>(value) + q, make_float4(v[0], v[1], v[2], v[3]));
     __stcs(reinterpret_cast<unsigned int*>(active) + q,
            (uint32_t)a[0] | ((uint32_t)a[1] << 8) | ((uint32_t)a[2] << 16) | ((uint32_t)a[3] << 24));
@@ -232,6 +315,19 @@ extern "C" int nvdb_tree_create(const nvdb_tree_desc* d, nvdb_tree** out) {
   chk(upload(t, &t->l2_ent, (const uint64_t*)nullptr, (size_t)32768 * d->n2));
   chk(upload(t, &t->l1_ent, (const uint64_t*)nullptr, (size_t)4096 * d->n1));
   chk(upload(t, &t->leaf_ent, (const uint64_t*)nullptr, (size_t)512 * d->nl));
+  {  // root entries: level-2 node index, or the root tile (kind 1, value bits, active bit)
+    std::vector<uint64_t> re((size_t)d->nroots);
+    for (int r = 0; r < d->nroots; ++r) {
+      if (d->root_l2[r] >= 0) {
+        re[r] = (uint64_t)(uint32_t)d->root_l2[r];
+      } else {
+        uint32_t vb;
+        std::memcpy(&vb, d->root_tile_value + r, 4);
+        re[r] = (uint64_t)vb | ((uint64_t)(d->root_tile_active[r] ? 1 : 0) << 32) | (1ull << kEntKindShift);
+      }
+    }
+    chk(upload(t, &t->root_ent, re.data(), re.size()));
+  }
   if (!rc) rc = tree_build_prefix(t, 0);
   if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = fail(NVDB_ECUDA, "tree prefix build failed");
   if (rc) {

@@ -33,6 +33,7 @@ struct nvdb_tree {
   uint64_t* l2_ent = nullptr;        // (n2,32768)
   uint64_t* l1_ent = nullptr;        // (n1,4096)
   uint64_t* leaf_ent = nullptr;      // (nl,512)
+  uint64_t* root_ent = nullptr;      // (nroots) level-2 node index, or the root tile as a kind-1 entry
   void* owned[32] = {};
   int nowned = 0;
 };
@@ -63,6 +64,7 @@ struct TreeView {  // kernel-side copy of the pointers
   const uint64_t* l2_ent;
   const uint64_t* l1_ent;
   const uint64_t* leaf_ent;
+  const uint64_t* root_ent;
 };
 
 inline TreeView view_of(const nvdb_tree* t) {
@@ -70,11 +72,12 @@ inline TreeView view_of(const nvdb_tree* t) {
                   t->root_tile_active, t->l2_child,   t->l2_active,     t->l2_tiles,  t->l2_child_base,
                   t->l2_prefix,     t->l1_child,      t->l1_active,     t->l1_tiles,  t->l1_child_base,
                   t->l1_prefix,     t->l2_slot,       t->l1_slot,       t->leaf_active, t->leaf_values,
-                  t->l2_ent,        t->l1_ent,        t->leaf_ent};
+                  t->l2_ent,        t->l1_ent,        t->leaf_ent,  t->root_ent};
 }
 
 constexpr uint64_t kEntActive = 1ull << 32;
 constexpr int kEntKindShift = 33;
+constexpr uint64_t kEntMiss = 3ull << kEntKindShift;  // outside every root: background, kind 0
 
 __device__ __forceinline__ int cmp3(const int32_t* k, int x, int y, int z) {
   if (k[0] != x) return k[0] < x ? -1 : 1;

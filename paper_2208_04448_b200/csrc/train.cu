@@ -413,10 +413,15 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint32_t h[4];
+        const int f0 = ch * (kChunkK / 2) + half * 16 + q * 4;  // 4 features: one 16-byte load per axis
+        const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
+        const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
+        const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
+        const float bxa[4] = {bx.x, bx.y, bx.z, bx.w}, bya[4] = {by.x, by.y, by.z, by.w};
+        const float bza[4] = {bz.x, bz.y, bz.z, bz.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int f = ch * (kChunkK / 2) + half * 16 + q * 4 + j;
-          const float th = fmaf(x2, s_b2pi[2 * mp + f], fmaf(x1, s_b2pi[mp + f], x0 * s_b2pi[f]));
+          const float th = fmaf(x2, bza[j], fmaf(x1, bya[j], x0 * bxa[j]));
           float sn, cs;
           __sincosf(th, &sn, &cs);
           h[j] = pack_half2(cs, sn);
@@ -473,10 +478,18 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           uint32_t fpk[8];  // f'(z) for the backward pass, fp16 pairs -> TMEM F_l
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
-            const float z0 = v[b2][i] + bl[cc * 16 + i], z1 = v[b2][i + 1] + bl[cc * 16 + i + 1];
-            av[i] = act_fn(act, z0);
-            av[i + 1] = act_fn(act, z1);
-            fpk[i >> 1] = pack_half2(act_deriv_from(act, z0), act_deriv_from(act, z1));
+            const float2 bb = *reinterpret_cast<const float2*>(bl + cc * 16 + i);
+            const float2 z = __fadd2_rn(make_float2(v[b2][i], v[b2][i + 1]), bb);
+            if (act == ACT_SINE) {  // sin and cos of one argument (one range reduction)
+              float c0, c1;
+              __sincosf(z.x, &av[i], &c0);
+              __sincosf(z.y, &av[i + 1], &c1);
+              fpk[i >> 1] = pack_half2(c0, c1);
+            } else {
+              av[i] = act_fn(act, z.x);
+              av[i + 1] = act_fn(act, z.y);
+              fpk[i >> 1] = pack_half2(act_deriv_from(act, z.x), act_deriv_from(act, z.y));
+            }
           }
           tmem_st8(fcol + (uint32_t)(l * (width >> 1)) + lane_off + cc * 8, fpk);
           const uint32_t p0 = pack_half2(av[0], av[1]), p1 = pack_half2(av[2], av[3]);
@@ -609,12 +622,22 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           const int cc = half + 2 * (c0 + b2);
           if (top) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float s2 = 0.f;
+            for (int i4 = 0; i4 < 4; ++i4) {
+              float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-              for (int k = 0; k < 3; ++k)
-                if (k < out_dim) s2 = fmaf(dl[k], s_headw[k * width + cc * 16 + i], s2);
-              da[b2][i] = s2;
+              for (int k = 0; k < 3; ++k) {
+                if (k < out_dim) {
+                  const float4 hw = *reinterpret_cast<const float4*>(s_headw + k * width + cc * 16 + 4 * i4);
+                  s4.x = fmaf(dl[k], hw.x, s4.x);
+                  s4.y = fmaf(dl[k], hw.y, s4.y);
+                  s4.z = fmaf(dl[k], hw.z, s4.z);
+                  s4.w = fmaf(dl[k], hw.w, s4.w);
+                }
+              }
+              da[b2][4 * i4] = s4.x;
+              da[b2][4 * i4 + 1] = s4.y;
+              da[b2][4 * i4 + 2] = s4.z;
+              da[b2][4 * i4 + 3] = s4.w;
             }
           }
           float dz[16];
@@ -622,8 +645,9 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           for (int i = 0; i < 8; ++i) {
             const __half2 h = *reinterpret_cast<const __half2*>(&fz[b2][i]);
             const float2 f = __half22float2(h);
-            dz[2 * i] = valid ? da[b2][2 * i] * f.x : 0.f;
-            dz[2 * i + 1] = valid ? da[b2][2 * i + 1] * f.y : 0.f;
+            const float2 d2 = __fmul2_rn(make_float2(da[b2][2 * i], da[b2][2 * i + 1]), f);
+            dz[2 * i] = valid ? d2.x : 0.f;
+            dz[2 * i + 1] = valid ? d2.y : 0.f;
           }
           const uint32_t p0 = pack_half2(dz[0], dz[1]), p1 = pack_half2(dz[2], dz[3]);
           const uint32_t p2 = pack_half2(dz[4], dz[5]), p3 = pack_half2(dz[6], dz[7]);

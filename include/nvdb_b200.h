@@ -243,6 +243,16 @@ NVDB_API int nvdb_tree_destroy(nvdb_tree* tree);
 NVDB_API int nvdb_lookup(const nvdb_tree* tree, const int32_t* coords, int64_t n, float* value, uint8_t* active,
                 uint8_t* kind, int32_t* leaf, void* stream);
 
+/* nvdb_lookup fused with the query's neural-row selection (decoder.py:243):
+ * value/active/kind as nvdb_lookup, and the rows with active && kind == 2
+ * appended to rows (capacity n, int64 row ids, order not deterministic) with
+ * their number in *count (device int64).  Rows whose voxel holds an exact
+ * patch already have their final value and are counted in *npatched
+ * (device int64) instead: regressor evaluations = *count + *npatched.
+ * coords/value 16-byte and active/kind 4-byte aligned. */
+NVDB_API int nvdb_lookup_rows(const nvdb_tree* tree, const int32_t* coords, int64_t n, float* value, uint8_t* active,
+                              uint8_t* kind, int64_t* rows, int64_t* count, int64_t* npatched, void* stream);
+
 /* HybridGrid.query (decoder.py:239-264) pieces: flag rows with active &&
  * kind == 2, then write regressed values (patched voxels keep their exact
  * stored value from the tree) back to those rows. */

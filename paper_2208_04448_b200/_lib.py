@@ -27,7 +27,7 @@ NVDB_ENOMEM = -5
 EXPORTED = [
     "nvdb_last_error", "nvdb_version", "nvdb_launch_count", "nvdb_netset_create", "nvdb_netset_destroy",
     "nvdb_forward", "nvdb_eval_workspace_bytes", "nvdb_eval_blended", "nvdb_tree_create",
-    "nvdb_tree_destroy", "nvdb_lookup", "nvdb_selftest_umma", "nvdb_eval",
+    "nvdb_tree_destroy", "nvdb_lookup", "nvdb_lookup_rows", "nvdb_selftest_umma", "nvdb_eval",
     "nvdb_select_workspace_bytes", "nvdb_select_u8", "nvdb_l1_apply", "nvdb_scatter_f32",
     "nvdb_leaf_list", "nvdb_l0_apply", "nvdb_leaf_finalize", "nvdb_pack_eq", "nvdb_neural_rows",
     "nvdb_query_finalize", "nvdb_trainer_create", "nvdb_trainer_destroy", "nvdb_trainer_run",
@@ -112,6 +112,7 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_tree_create": (C.c_int, [C.POINTER(TreeDesc), C.POINTER(vp)]),
         "nvdb_tree_destroy": (C.c_int, [vp]),
         "nvdb_lookup": (C.c_int, [vp, vp, i64, vp, vp, vp, vp, vp]),
+        "nvdb_lookup_rows": (C.c_int, [vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]),
         "nvdb_selftest_umma": (C.c_int, [vp, u32, vp, u32, i32, i32, u32, u32, u32, u32, u32, u32,
                                          i32, i32, vp, vp]),
         "nvdb_eval": (C.c_int, [vp, i32, i32, vp, vp, i64, C.POINTER(EvalOut), vp, sz, vp]),

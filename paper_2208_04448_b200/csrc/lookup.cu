@@ -90,12 +90,70 @@ __device__ __forceinline__ void resolve_q(const TreeView& t, const int32_t* s_ke
 }
 
 
+// Neural rows of a query batch (decoder.py:243: active && kind == 2) appended
+// by the lookup itself: rows whose voxel carries an exact patch keep the
+// value just looked up (what the reference's finalize writes) and are only
+// counted; the others go to rows[] for the regressor.  One atomic per warp
+// per iteration (warp-aggregated); the row order is not deterministic, the
+// values are (each row is evaluated and written independently).
+struct RowSink {
+  int64_t* rows;                 // (n) capacity
+  unsigned long long* count;     // rows appended
+  unsigned long long* npatched;  // neural rows answered by an exact patch
+  const uint64_t* patched;       // tree leaf_patched (nullable)
+};
+
+template <int Q>
+__device__ __forceinline__ void append_rows(const RowSink& s, const int64_t (&id)[Q], const bool (&nr)[Q],
+                                            const int32_t (&lf)[Q], const int (&x)[Q], const int (&y)[Q],
+                                            const int (&z)[Q]) {
+  bool app[Q];
+  int npt = 0;
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    bool pt = false;
+    if (nr[j] && s.patched) {
+      const int i0 = ((x[j] & 7) << 6) | ((y[j] & 7) << 3) | (z[j] & 7);
+      pt = (__ldg(reinterpret_cast<const unsigned long long*>(s.patched) + (int64_t)lf[j] * 8 + (i0 >> 6)) >>
+            (i0 & 63)) & 1ull;
+    }
+    app[j] = nr[j] && !pt;
+    npt += (nr[j] && pt) ? 1 : 0;
+  }
+  const unsigned m = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned bal[Q];
+  int tot = 0;
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    bal[j] = __ballot_sync(m, app[j]);
+    tot += __popc(bal[j]);
+  }
+  for (int o = 16; o > 0; o >>= 1) npt += __shfl_xor_sync(m, npt, o);  // inactive lanes contribute 0
+  unsigned long long base = 0;
+  if (lane == leader) {
+    if (tot) base = atomicAdd(s.count, (unsigned long long)tot);
+    if (npt) atomicAdd(s.npatched, (unsigned long long)npt);
+  }
+  base = __shfl_sync(m, base, leader);
+  int off = 0;
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    if (app[j]) s.rows[base + off + __popc(bal[j] & lt)] = id[j];
+    off += __popc(bal[j]);
+  }
+}
+
 // Four queries per thread: three 16-byte coordinate loads (the thread's 48
 // contiguous bytes), one level-synchronous resolve, then one 16-byte value
-// store, one 4-byte active store and one 4-byte kind store.
+// store, one 4-byte active store and one 4-byte kind store.  ROWS: the
+// neural rows are appended to a RowSink instead of writing leaf indices.
+template <bool ROWS>
 __global__ void __launch_bounds__(256) k_lookup(TreeView t, const int32_t* __restrict__ coords, int64_t n,
                                                 float* __restrict__ value, uint8_t* __restrict__ active,
-                                                uint8_t* __restrict__ kind, int32_t* __restrict__ leaf_out) {
+                                                uint8_t* __restrict__ kind, int32_t* __restrict__ leaf_out,
+                                                RowSink sink) {
   __shared__ int32_t s_keys[3 * kRootLinear];
   __shared__ uint64_t s_rent[kRootLinear];
   const bool staged = t.nroots <= kRootLinear;
@@ -121,7 +179,13 @@ __global__ void __launch_bounds__(256) k_lookup(TreeView t, const int32_t* __res
            (uint32_t)a[0] | ((uint32_t)a[1] << 8) | ((uint32_t)a[2] << 16) | ((uint32_t)a[3] << 24));
     __stcs(reinterpret_cast<unsigned int*>(kind) + q,
            (uint32_t)k[0] | ((uint32_t)k[1] << 8) | ((uint32_t)k[2] << 16) | ((uint32_t)k[3] << 24));
-    if (leaf_out) __stcs(reinterpret_cast<int4*>(leaf_out) + q, make_int4(lf[0], lf[1], lf[2], lf[3]));
+    if constexpr (ROWS) {
+      const int64_t id[4] = {4 * q, 4 * q + 1, 4 * q + 2, 4 * q + 3};
+      const bool nr[4] = {a[0] && k[0] == 2, a[1] && k[1] == 2, a[2] && k[2] == 2, a[3] && k[3] == 2};
+      append_rows<4>(sink, id, nr, lf, xs, ys, zs);
+    } else if (leaf_out) {
+      __stcs(reinterpret_cast<int4*>(leaf_out) + q, make_int4(lf[0], lf[1], lf[2], lf[3]));
+    }
   }
   // tail (n % 4 rows)
   const int64_t i = 4 * nq4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -129,11 +193,20 @@ __global__ void __launch_bounds__(256) k_lookup(TreeView t, const int32_t* __res
     float v;
     uint8_t a, k;
     int32_t lf;
-    tree_resolve(t, coords[3 * i], coords[3 * i + 1], coords[3 * i + 2], v, a, k, lf);
+    const int x = coords[3 * i], y = coords[3 * i + 1], z = coords[3 * i + 2];
+    tree_resolve(t, x, y, z, v, a, k, lf);
     value[i] = v;
     active[i] = a;
     kind[i] = k;
-    if (leaf_out) leaf_out[i] = lf;
+    if constexpr (ROWS) {
+      const int64_t id[1] = {i};
+      const bool nr[1] = {a && k == 2};
+      const int32_t lfa[1] = {lf};
+      const int xa[1] = {x}, ya[1] = {y}, za[1] = {z};
+      append_rows<1>(sink, id, nr, lfa, xa, ya, za);
+    } else if (leaf_out) {
+      leaf_out[i] = lf;
+    }
   }
 }
 
@@ -261,12 +334,27 @@ int launch_lookup(const nvdb_tree* t, const int32_t* coords, int64_t n, float* v
   if (aligned) {
     const int64_t want = (std::max<int64_t>(n / 4, 1) + threads - 1) / threads;
     const int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * 16);
-    k_lookup<<<blocks, threads, 0, st>>>(view_of(t), coords, n, value, active, kind, leaf);
+    k_lookup<false><<<blocks, threads, 0, st>>>(view_of(t), coords, n, value, active, kind, leaf, RowSink{});
   } else {
     const int64_t want = (n + threads - 1) / threads;
     const int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * 16);
     k_lookup1<<<blocks, threads, 0, st>>>(view_of(t), coords, n, value, active, kind, leaf);
   }
+  NVDB_CHECK_LAUNCH();
+  return NVDB_OK;
+}
+
+int launch_lookup_rows(const nvdb_tree* t, const int32_t* coords, int64_t n, float* value, uint8_t* active,
+                       uint8_t* kind, int64_t* rows, int64_t* count, int64_t* npatched, cudaStream_t st) {
+  NVDB_CUDA_TRY(cudaMemsetAsync(count, 0, 8, st));
+  NVDB_CUDA_TRY(cudaMemsetAsync(npatched, 0, 8, st));
+  if (n <= 0) return NVDB_OK;
+  const int threads = 256;
+  const int64_t want = (std::max<int64_t>(n / 4, 1) + threads - 1) / threads;
+  const int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * 16);
+  const RowSink sink{rows, reinterpret_cast<unsigned long long*>(count), reinterpret_cast<unsigned long long*>(npatched),
+                     t->leaf_patched};
+  k_lookup<true><<<blocks, threads, 0, st>>>(view_of(t), coords, n, value, active, kind, nullptr, sink);
   NVDB_CHECK_LAUNCH();
   return NVDB_OK;
 }
@@ -343,6 +431,17 @@ extern "C" int nvdb_tree_destroy(nvdb_tree* t) {
   for (int i = 0; i < t->nowned; ++i) cudaFree(t->owned[i]);
   delete t;
   return NVDB_OK;
+}
+
+extern "C" int nvdb_lookup_rows(const nvdb_tree* t, const int32_t* coords, int64_t n, float* value, uint8_t* active,
+                                uint8_t* kind, int64_t* rows, int64_t* count, int64_t* npatched, void* stream) {
+  if (!t) return fail(NVDB_EINVAL, "nvdb_lookup_rows: null tree");
+  if (n < 0 || !count || !npatched || (n > 0 && (!coords || !value || !active || !kind || !rows)))
+    return fail(NVDB_EINVAL, "nvdb_lookup_rows: bad buffers");
+  if ((reinterpret_cast<uintptr_t>(coords) | reinterpret_cast<uintptr_t>(value)) & 15 ||
+      (reinterpret_cast<uintptr_t>(active) | reinterpret_cast<uintptr_t>(kind)) & 3)
+    return fail(NVDB_EINVAL, "nvdb_lookup_rows: coords/value need 16-byte, active/kind 4-byte alignment");
+  return launch_lookup_rows(t, coords, n, value, active, kind, rows, count, npatched, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int nvdb_lookup(const nvdb_tree* t, const int32_t* coords, int64_t n, float* value, uint8_t* active,

@@ -836,17 +836,16 @@ def hybrid_query(tree: DeviceTree, nets, coords: torch.Tensor, value_scale: floa
     active, regressor evaluations)."""
     dev, st = nets.dev, _stream(nets.dev)
     n = coords.shape[0]
-    val, act, kind, leaf = tree.lookup(coords, want_leaf=True)
-    flag = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
-    check(lib().nvdb_neural_rows(_ptr(act), _ptr(kind), n, _ptr(flag), st), "nvdb_neural_rows")
-    rows, cnt = nets.select(flag[:n], 1, sync=False)
+    # one pass: lookup + the active leaf-voxel rows (patched rows keep their
+    # exact value and only count as evaluated, as the reference's finalize)
+    val, act, kind, rows, cnt, npatched = tree.lookup_rows(coords)
     if n:
         reg = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         nets.evaluate("voxel", _lib.SRC_COORD_I32, coords, n, _lib.OUT_VALUE, gather=rows, f32=reg,
                       value_scale=value_scale, clip=clip, count=cnt)
-        check(lib().nvdb_query_finalize_counted(_ptr(rows), n, _ptr(cnt), _ptr(reg), _ptr(coords), _ptr(leaf),
-                                                tree.handle, _ptr(val), st), "nvdb_query_finalize_counted")
-    return val, act, cnt
+        check(lib().nvdb_scatter_f32_counted(_ptr(val), _ptr(rows), _ptr(reg), n, _ptr(cnt), st),
+              "nvdb_scatter_f32_counted")
+    return val, act, cnt + npatched
 
 
 class HybridGrid:

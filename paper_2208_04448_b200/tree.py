@@ -176,3 +176,22 @@ class DeviceTree:
                                 kind.data_ptr(), leaf.data_ptr() if leaf is not None else None,
                                 torch.cuda.current_stream(dev).cuda_stream), "nvdb_lookup")
         return (val, act, kind, leaf) if want_leaf else (val, act, kind)
+
+    def lookup_rows(self, coords: torch.Tensor):
+        """lookup() fused with the query's neural-row selection
+        (nvdb_lookup_rows): (value, active, kind, rows, count, npatched);
+        rows[:count] are the active leaf-voxel rows without an exact patch
+        (device int64 count), npatched the active leaf-voxel rows answered
+        by a patch."""
+        assert coords.is_cuda and coords.dtype == torch.int32 and coords.is_contiguous()
+        n = coords.shape[0]
+        dev = coords.device
+        val = torch.empty(n, dtype=torch.float32, device=dev)
+        act = torch.empty(n, dtype=torch.uint8, device=dev)
+        kind = torch.empty(n, dtype=torch.uint8, device=dev)
+        rows = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        cnt = torch.empty(2, dtype=torch.int64, device=dev)
+        check(lib().nvdb_lookup_rows(self.handle, coords.data_ptr(), n, val.data_ptr(), act.data_ptr(),
+                                     kind.data_ptr(), rows.data_ptr(), cnt.data_ptr(), cnt[1:].data_ptr(),
+                                     torch.cuda.current_stream(dev).cuda_stream), "nvdb_lookup_rows")
+        return val, act, kind, rows, cnt[:1], cnt[1:]

@@ -334,6 +334,8 @@ int launch_mlp(const nvdb_netset* ns, MlpArgs a, const int32_t* npairs_dev, int 
   a.wstream = plan.wstream;
   a.wring = plan.wring;
   a.wring_off = plan.wring_off;
+  a.wslot_bytes = plan.wslot_bytes;
+  a.wslack = plan.wslack;
   a.sm_bias = plan.sm_bias;
   a.sm_headw = plan.sm_headw;
   a.sm_headb = plan.sm_headb;

@@ -121,8 +121,10 @@ struct MlpArgs {
                     // [+ the weight ring when streaming]
   int32_t wstream;  // 1: weights do not fit in shared memory; each engine streams K = 16 weight
                     //    chunks (W x 32 bytes) through a ring of `wring` slots, wring_off into its region
-  int32_t wring;
+  int32_t wring;     // ring slots
   uint32_t wring_off;
+  uint32_t wslot_bytes;  // ring slot capacity: up to 4 consecutive K = 16 chunks (one bulk copy, one barrier round)
+  int32_t wslack;        // refill up to wring - wslack slots ahead of an issuer
   int32_t sm_bias, sm_headw, sm_headb, sm_b2pi, sm_lat, sm_hx;  // float offsets in the small region
 };
 
@@ -199,9 +201,6 @@ constexpr int kSlots = 2;                    // feature chunk slots per engine
 constexpr int kEChunkK = 48;                 // feature K per chunk (3 MMAs of K = 16)
 constexpr int kEChunkBytes = kTileM * kEChunkK * 2;  // 12 KB
 constexpr int kEvalThreads = 128 * kMaxEngines;  // largest block (512)
-#ifndef NVDB_WRING_SLACK
-#define NVDB_WRING_SLACK 1  // refill up to WR - SLACK chunks ahead of the issuer
-#endif
 constexpr int kMaxWRing = 8;                 // weight ring slots per engine (streamed weights)
 
 // ACT: the hidden activation of every net in the launch (a container's nets
@@ -314,48 +313,68 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     return tl;
   };
 
-  // ---- streamed weights: the net's fp16 image is a sequence of nK K = 16
+  // ---- streamed weights: the net's fp16 image is a sequence of K = 16
   // chunks of W x 32 bytes (layer 0, then each hidden layer), consumed in
   // that order once per tile by every engine.  One ring of `wring` slots per
   // CTA is shared by the engines, so each chunk fetched from L2 serves all
-  // engines' current tiles.  Chunk positions count up globally; any engine's
-  // issuer may claim the next position to fill (s_wnext); a slot is refilled
-  // once all E engines consumed its previous chunk (wempty counts E).
+  // engines' current tiles.  A slot holds `wp` consecutive chunks (one bulk
+  // copy, one full / empty barrier round for wp MMAs: the issuing thread's
+  // per-slot bookkeeping -- barrier waits, copy issue, commit -- costs
+  // several MMAs' worth of clocks, tools/ubench/wstream.cu).  Slot positions
+  // count up globally; any engine's issuer may claim the next position to
+  // fill (s_wnext); a slot is refilled once all E engines consumed its
+  // previous contents (wempty counts E).
   const int WR = a.wring;
   const uint32_t wring_s = smem_addr(smem + a.wring_off);
   uint8_t* const wring_p = smem + a.wring_off;
-  uint32_t wcons = 0, wbase = 0;  // per issuer
+  uint32_t wcons = 0, wbase = 0;  // per issuer: slot position being consumed, sequence start of the net
+  uint32_t wp = 1, wpc = 0, wslot = 0;  // chunks per slot (per net), chunk within the current slot, its ring slot
   auto w_fill_pos = [&](uint32_t pos) {
     const uint32_t slot = pos % (uint32_t)WR;
     if (pos >= (uint32_t)WR) mbar_wait(wempty + slot, ((pos / WR) - 1) & 1u);
-    const uint32_t cb = (uint32_t)s_net.width * 32u;
+    const uint32_t cb = (uint32_t)s_net.width * 32u * wp;
     const uint32_t nk = s_net.wimg_bytes / cb;
     const uint32_t c = (pos - wbase) % nk;
     mbar_arrive_expect_tx(wfull + slot, cb);
-    bulk_g2s(wring_p + slot * cb, s_net.wimg + (size_t)c * cb, cb, wfull + slot);
+    bulk_g2s(wring_p + slot * a.wslot_bytes, s_net.wimg + (size_t)c * cb, cb, wfull + slot);
   };
-  auto w_next = [&]() {  // slot of this issuer's next chunk, once it landed
+  auto w_refill = [&](bool blocking) {  // claim and fill positions up to WR - wslack ahead of this issuer
     while (true) {
       const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&s_wnext);
-      if (n >= wcons + (uint32_t)WR - NVDB_WRING_SLACK) break;
+      if (n >= wcons + (uint32_t)(WR - a.wslack)) break;
+      if (!blocking && n >= (uint32_t)WR && !mbar_test(wempty + n % (uint32_t)WR, ((n / WR) - 1) & 1u)) break;
+      if (atomicCAS(&s_wnext, n, n + 1) == n) w_fill_pos(n);
+    }
+  };
+  auto w_next = [&]() {  // ring slot of this issuer's next position, once it landed
+    w_refill(false);  // prefetch into slots that are already free
+    while (true) {    // this issuer's own position must be claimed (blocking only for it)
+      const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&s_wnext);
+      if (n > wcons) break;
       if (atomicCAS(&s_wnext, n, n + 1) == n) w_fill_pos(n);
     }
     const uint32_t slot = wcons % (uint32_t)WR;
     mbar_wait(wfull + slot, (wcons / WR) & 1u);
     return slot;
   };
-  // one K = 16 MMA with the next weight chunk of the sequence (issuer only)
+  // one K = 16 MMA with the next weight chunk of the sequence (issuer only);
+  // the slot is released after its last chunk, then refilled if already free
   auto w_mma = [&](uint32_t d, uint64_t adesc, uint32_t idesc, uint32_t acc, bool ts, uint32_t a_tmem) {
-    const uint32_t slot = w_next();
-    const uint64_t bd = smem_desc(wring_s + slot * (uint32_t)s_net.width * 32u, s_net.width * 16, 128);
+    if (wpc == 0) wslot = w_next();
+    const uint64_t bd = smem_desc(wring_s + wslot * a.wslot_bytes + wpc * (uint32_t)s_net.width * 32u,
+                                  s_net.width * 16, 128);
     if (ts) umma_f16_ts(d, a_tmem, bd, idesc, acc);
     else umma_f16(d, adesc, bd, idesc, acc);
-    umma_commit(wempty + slot);
-    ++wcons;
+    if (++wpc == wp) {
+      umma_commit(wempty + wslot);
+      ++wcons;
+      wpc = 0;
+      w_refill(false);
+    }
   };
-  // an engine without a tile in this (sub-)round still consumes the tile's chunks
+  // an engine without a tile in this (sub-)round still consumes the tile's slots
   auto w_skip_tile = [&]() {
-    const uint32_t nk = s_net.wimg_bytes / ((uint32_t)s_net.width * 32u);
+    const uint32_t nk = s_net.wimg_bytes / ((uint32_t)s_net.width * 32u * wp);
     for (uint32_t c = 0; c < nk; ++c) {
       const uint32_t slot = w_next();
       mbar_arrive(wempty + slot);
@@ -409,7 +428,24 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       w_restart();
     }
     __syncthreads();
-    if (a.wstream) wcons = wbase = s_wnext;
+    if (a.wstream) {
+      wcons = wbase = s_wnext;
+      wpc = 0;
+      // chunks per slot: the most that fit a slot and divide every layer's chunk count
+      const uint32_t pb = (uint32_t)s_net.width * 32u;
+      uint32_t g = (uint32_t)s_net.k0 / 16u, h = (uint32_t)s_net.width / 16u;
+      while (h) {
+        const uint32_t r = g % h;
+        g = h;
+        h = r;
+      }
+      wp = 1;
+      for (uint32_t q = min(a.wslot_bytes / pb, 4u); q > 1; --q)
+        if (g % q == 0) {
+          wp = q;
+          break;
+        }
+    }
     loaded = net;
   };
 

@@ -53,7 +53,8 @@ constexpr uint32_t kMaxDynSmem = 227 * 1024 - 512;  // leave room for static __s
 struct EvalPlan {
   uint32_t w_off, region_off, region_bytes, small_off, bar_off, total;
   int engines, tcols, ereg, wstream, wring, ok;
-  uint32_t wring_off;
+  uint32_t wring_off, wslot_bytes;
+  int wslack;
   int sm_bias, sm_headw, sm_headb, sm_b2pi, sm_lat, sm_hx;
 };
 
@@ -83,24 +84,29 @@ inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t 
   p.wring = 0;
   p.wring_off = 0;
   if (p.engines < 2) {
-    // streamed: as many engines as TMEM allows, then the deepest CTA-wide weight
-    // ring that fits (each slot = one K = 16 chunk of W x 32 bytes)
+    // streamed: as many engines as TMEM allows, then the CTA-wide weight ring:
+    // slots of up to 4 K = 16 chunks (W x 32 bytes each), as many slots (2..4)
+    // as fit, bigger slots first (the issuer's bookkeeping is per slot)
     p.wstream = 1;
     p.region_off = 0;
     room = (long long)limit - small_bytes - 16 - 1024;
     p.engines = 0;
     for (int ne = by_tmem; ne >= 1 && !p.engines; --ne)
-      for (int r = kMaxWRing; r >= 3; --r) {
-        if (ne * base_ereg + (long long)r * W * 32 <= room) {
-          p.engines = ne;
-          p.wring = r;
-          p.ereg = (int)base_ereg;
-          break;
+      for (int pc = 4; pc >= 1 && !p.engines; pc /= 2)
+        for (int r = 4; r >= 2; --r) {
+          if (ne * base_ereg + (long long)r * pc * W * 32 <= room) {
+            p.engines = ne;
+            p.wring = r;
+            p.wslot_bytes = (uint32_t)(pc * W * 32);
+            p.ereg = (int)base_ereg;
+            break;
+          }
         }
-      }
+    p.wslack = p.wring >= 3 ? 1 : 0;
     p.wring_off = (uint32_t)(p.engines * base_ereg);
   }
-  p.region_bytes = (uint32_t)(std::max(p.engines, 1) * p.ereg) + (p.wstream ? (uint32_t)(p.wring * W * 32) : 0u);
+  p.region_bytes = (uint32_t)(std::max(p.engines, 1) * p.ereg) +
+                   (p.wstream ? (uint32_t)p.wring * p.wslot_bytes : 0u);
   p.small_off = p.region_off + p.region_bytes;
   p.bar_off = (uint32_t)align_up(p.small_off + small_bytes, 16);
   p.total = p.bar_off + 1024;

@@ -328,7 +328,10 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   const uint32_t wring_s = smem_addr(smem + a.wring_off);
   uint8_t* const wring_p = smem + a.wring_off;
   uint32_t wcons = 0, wbase = 0;  // per issuer: slot position being consumed, sequence start of the net
-  uint32_t wp = 1, wpc = 0, wslot = 0;  // chunks per slot (per net), chunk within the current slot, its ring slot
+  uint32_t wp = 1, wpc = 0;     // chunks per slot (per net), chunk within the current slot
+  uint32_t wcur = 0, wph = 0;   // ring slot and barrier parity of position wcons
+  uint32_t wdstep = 0;          // descriptor step of one chunk (W x 32 bytes >> 4)
+  uint64_t wdesc = 0;           // B descriptor of chunk 0 of the current slot
   auto w_fill_pos = [&](uint32_t pos) {
     const uint32_t slot = pos % (uint32_t)WR;
     if (pos >= (uint32_t)WR) mbar_wait(wempty + slot, ((pos / WR) - 1) & 1u);
@@ -346,28 +349,35 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       if (atomicCAS(&s_wnext, n, n + 1) == n) w_fill_pos(n);
     }
   };
-  auto w_next = [&]() {  // ring slot of this issuer's next position, once it landed
+  // ring slot of this issuer's next position, once it landed (the slot's
+  // descriptor is built here once; per chunk the issuer only adds wdstep)
+  auto w_next = [&]() {
     w_refill(false);  // prefetch into slots that are already free
     while (true) {    // this issuer's own position must be claimed (blocking only for it)
       const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&s_wnext);
       if (n > wcons) break;
       if (atomicCAS(&s_wnext, n, n + 1) == n) w_fill_pos(n);
     }
-    const uint32_t slot = wcons % (uint32_t)WR;
-    mbar_wait(wfull + slot, (wcons / WR) & 1u);
-    return slot;
+    mbar_wait(wfull + wcur, wph);
+    wdesc = smem_desc(wring_s + wcur * a.wslot_bytes, wdstep << 3, 128);
+  };
+  auto w_advance = [&]() {
+    ++wcons;
+    if (++wcur == (uint32_t)WR) {
+      wcur = 0;
+      wph ^= 1u;
+    }
   };
   // one K = 16 MMA with the next weight chunk of the sequence (issuer only);
   // the slot is released after its last chunk, then refilled if already free
   auto w_mma = [&](uint32_t d, uint64_t adesc, uint32_t idesc, uint32_t acc, bool ts, uint32_t a_tmem) {
-    if (wpc == 0) wslot = w_next();
-    const uint64_t bd = smem_desc(wring_s + wslot * a.wslot_bytes + wpc * (uint32_t)s_net.width * 32u,
-                                  s_net.width * 16, 128);
+    if (wpc == 0) w_next();
+    const uint64_t bd = wdesc + (uint64_t)(wpc * wdstep);
     if (ts) umma_f16_ts(d, a_tmem, bd, idesc, acc);
     else umma_f16(d, adesc, bd, idesc, acc);
     if (++wpc == wp) {
-      umma_commit(wempty + wslot);
-      ++wcons;
+      umma_commit(wempty + wcur);
+      w_advance();
       wpc = 0;
       w_refill(false);
     }
@@ -376,9 +386,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   auto w_skip_tile = [&]() {
     const uint32_t nk = s_net.wimg_bytes / ((uint32_t)s_net.width * 32u * wp);
     for (uint32_t c = 0; c < nk; ++c) {
-      const uint32_t slot = w_next();
-      mbar_arrive(wempty + slot);
-      ++wcons;
+      w_next();
+      mbar_arrive(wempty + wcur);
+      w_advance();
     }
   };
   // new net (all engines at the barrier, every engine consumed the same
@@ -431,6 +441,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     if (a.wstream) {
       wcons = wbase = s_wnext;
       wpc = 0;
+      wcur = wcons % (uint32_t)WR;
+      wph = (wcons / (uint32_t)WR) & 1u;
+      wdstep = (uint32_t)s_net.width * 2u;  // (W x 32 bytes) >> 4
       // chunks per slot: the most that fit a slot and divide every layer's chunk count
       const uint32_t pb = (uint32_t)s_net.width * 32u;
       uint32_t g = (uint32_t)s_net.k0 / 16u, h = (uint32_t)s_net.width / 16u;

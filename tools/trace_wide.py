@@ -4,7 +4,8 @@ lattice source (diagnostic; needs `make -C csrc trace`).
     NVDB_LIB=libnvdb_b200_trace.so python tools/trace_wide.py [W m depth]
 
 Events per engine (warp 4g): 1 = layer 0 issued, 2+l = layer l's MMAs done
-(epilogue start), 9 = tile done."""
+(epilogue start), 20+l = epilogue of layer l done (the engine's barrier),
+30+l = layer l+1's MMAs issued, 9 = tile done."""
 import ctypes as C
 import os
 import sys
@@ -61,12 +62,12 @@ rows = defaultdict(dict)
 for c_, e_, t_, w_ in zip(clk, evs, tile, warp):
     rows[(w_ // 4, t_)][e_] = c_
 print(f"W={W} m={m} depth={depth}: CTA0 span {clk[-1]} clk, {len([k for k in rows if 9 in rows[k]])} tiles")
-print("eng  tile |   start->L0 issued  ->L0 done  ->L1 done  ->L2 done  ->tile done")
+print("eng  tile | start->L0 issued ->L0 done ->epi0 done ->L1 issued ->L1 done ->epi1 done ->L2 issued ->L2 done ->tile done")
 prev = {}
 for k in sorted(rows, key=lambda k: min(rows[k].values()))[:24]:
     r = rows[k]
     b = prev.get(k[0], 0)
-    seq = [r.get(e) for e in (1, 2, 3, 4, 9)]
+    seq = [r.get(e) for e in (1, 2, 20, 30, 3, 21, 31, 4, 9)]
     out, last = [], b
     for s in seq:
         out.append(f"{(s - last) if s is not None else -1:9d}")

@@ -143,37 +143,77 @@ __global__ void __launch_bounds__(128 * kLwMaxEngines, 1) k_lw_fb(const LwFbArgs
   uint8_t* const ring_p = smem + a.plan.ring_off;
   const uint32_t nk = a.nk_tot;
 
-  // ---- weight ring (issuer threads): positions count up over the whole
-  // launch, chunk c = pos % nk; any engine's issuer may claim the next
-  // position; a slot is refilled once every engine consumed its chunk
-  uint32_t wcons = 0;
+  // ---- weight ring (issuer threads): slots of wp consecutive chunks (one
+  // bulk copy, one barrier round and one commit per slot: the issuer's
+  // per-slot bookkeeping costs several MMAs' worth of clocks, see
+  // mlp_eval_kernel), kLwRing / wp slots; positions count up over the whole
+  // launch, slot chunk group c = pos % (nk / wp); any engine's issuer may
+  // claim the next position; a slot is refilled once every engine consumed it
+  uint32_t wp = 1;
+  {
+    uint32_t g0 = (uint32_t)k0 / 16u, h0 = (uint32_t)W / 16u;
+    while (h0) {
+      const uint32_t r = g0 % h0;
+      g0 = h0;
+      h0 = r;
+    }
+    for (uint32_t q = 4; q > 1; q >>= 1)
+      if (g0 % q == 0 && nk % q == 0) {
+        wp = q;
+        break;
+      }
+  }
+  const uint32_t WRn = (uint32_t)kLwRing / wp, sb = cb * wp, nkp = nk / wp;
+  const uint32_t wslack = WRn >= 3 ? 1u : 0u;
+  const uint32_t wdstep = (uint32_t)W * 2u;  // one chunk in descriptor units (W x 32 bytes >> 4)
+  uint32_t wcons = 0, wcur = 0, wph = 0, wpc = 0;
+  uint64_t wdesc = 0;
   auto w_fill_pos = [&](uint32_t pos) {
-    const uint32_t slot = pos % (uint32_t)kLwRing;
-    if (pos >= (uint32_t)kLwRing) mbar_wait(wempty + slot, ((pos / kLwRing) - 1) & 1u);
-    mbar_arrive_expect_tx(wfull + slot, cb);
-    bulk_g2s(ring_p + slot * cb, nd.wimg + (size_t)(pos % nk) * cb, cb, wfull + slot);
+    const uint32_t slot = pos % WRn;
+    if (pos >= WRn) mbar_wait(wempty + slot, ((pos / WRn) - 1) & 1u);
+    mbar_arrive_expect_tx(wfull + slot, sb);
+    bulk_g2s(ring_p + slot * sb, nd.wimg + (size_t)(pos % nkp) * sb, sb, wfull + slot);
   };
-  auto w_next = [&]() {
+  auto w_refill = [&]() {  // prefetch into slots that are already free
     while (true) {
       const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&s_wnext);
-      if (n >= wcons + (uint32_t)kLwRing - 1) break;
+      if (n >= wcons + WRn - wslack) break;
+      if (n >= WRn && !mbar_test(wempty + n % WRn, ((n / WRn) - 1) & 1u)) break;
       if (atomicCAS(&s_wnext, n, n + 1) == n) w_fill_pos(n);
     }
-    const uint32_t slot = wcons % (uint32_t)kLwRing;
-    mbar_wait(wfull + slot, (wcons / kLwRing) & 1u);
-    return slot;
+  };
+  auto w_next = [&]() {
+    w_refill();
+    while (true) {  // this issuer's own position must be claimed (blocking only for it)
+      const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&s_wnext);
+      if (n > wcons) break;
+      if (atomicCAS(&s_wnext, n, n + 1) == n) w_fill_pos(n);
+    }
+    mbar_wait(wfull + wcur, wph);
+    wdesc = smem_desc(ring_s + wcur * sb, W * 16, 128);
+  };
+  auto w_advance = [&]() {
+    ++wcons;
+    if (++wcur == WRn) {
+      wcur = 0;
+      wph ^= 1u;
+    }
   };
   auto w_mma = [&](uint64_t adesc, uint32_t acc) {
-    const uint32_t slot = w_next();
-    umma_f16(zcol, adesc, smem_desc(ring_s + slot * cb, W * 16, 128), idesc, acc);
-    umma_commit(wempty + slot);
-    ++wcons;
+    if (wpc == 0) w_next();
+    umma_f16(zcol, adesc, wdesc + (uint64_t)(wpc * wdstep), idesc, acc);
+    if (++wpc == wp) {
+      umma_commit(wempty + wcur);
+      w_advance();
+      wpc = 0;
+      w_refill();
+    }
   };
   auto w_skip_tile = [&]() {
-    for (uint32_t c = 0; c < nk; ++c) {
-      const uint32_t slot = w_next();
-      mbar_arrive(wempty + slot);
-      ++wcons;
+    for (uint32_t c = 0; c < nkp; ++c) {
+      w_next();
+      mbar_arrive(wempty + wcur);
+      w_advance();
     }
   };
 
@@ -416,8 +456,8 @@ __global__ void __launch_bounds__(128 * kLwMaxEngines, 1) k_lw_fb(const LwFbArgs
     double sl = 0.0;
     for (int e = 0; e < E; ++e) sl += s_loss[4 * e];
     a.loss_part[blockIdx.x] = sl;
-    for (uint32_t pos = wcons; pos < s_wnext; ++pos)  // prefetched chunks nobody will use
-      mbar_wait(wfull + pos % (uint32_t)kLwRing, (pos / kLwRing) & 1u);
+    for (uint32_t pos = wcons; pos < s_wnext; ++pos)  // prefetched slots nobody will use
+      mbar_wait(wfull + pos % WRn, (pos / WRn) & 1u);
   }
   tc_fence_before();
   __syncthreads();

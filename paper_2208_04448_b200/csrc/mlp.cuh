@@ -707,10 +707,12 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
         tc_fence_before();
         named_bar_sync(1 + g, 128);
         if (issuer) {
+          TRC(20 + l, t);
           tc_fence_after();
           uint64_t ad = smem_desc(asm_, kTileM * 16, 128);
           if (a.wstream) {
             for (int k = 0; k < width / 16; ++k, ad += 256) w_mma(dcol, ad, idesc, k != 0, false, 0);
+            TRC(30 + l, t);
           } else {
             uint64_t bd = smem_desc(w_s + (uint32_t)(width * k0 * 2 + l * width * width * 2), width * 16, 128);
             umma_f16(dcol, ad, bd, idesc, 0);
@@ -719,6 +721,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
               ad += 256;
               umma_f16(dcol, ad, bd, idesc, 1);
             }
+            TRC(30 + l, t);
           }
           umma_commit(mdone);
         }

@@ -160,11 +160,14 @@ def test_blended_matches_reference(golden, name):
     ns.close()
 
 
-@pytest.mark.parametrize("width,m,depth", [(256, 256, 3), (192, 192, 3), (128, 256, 3), (256, 512, 2)])
+@pytest.mark.parametrize("width,m,depth", [(256, 256, 3), (192, 192, 3), (128, 256, 3), (256, 512, 2),
+                                           (176, 176, 3), (160, 240, 3), (240, 120, 3)])
 def test_wide_nets_stream_weights(width, m, depth):
     """Table-3 widths (Dragon 3x128/m256, LeVeque 3x192, Chameleon/Lucy 3x256):
-    weights no longer fit in shared memory and are streamed per K = 16 chunk;
-    forward_block parity vs the fp32 oracle on random nets and points."""
+    weights no longer fit in shared memory and are streamed through the weight
+    ring (slots of 4 K = 16 chunks; the last three shapes give 1, 2 and 3
+    chunks per slot, chunk counts 22/11, 30/10, 15/15); forward_block parity
+    vs the fp32 oracle on random nets and points."""
     from paper_2208_04448_b200.encoder import init_mlp
     from paper_2208_04448_b200.model import Activation, FourierFeatures
     rng = np.random.default_rng(width + m + depth)
@@ -212,6 +215,31 @@ def test_forward_ragged_shapes(hidden, m, kind, head, n):
         ref = O.forward_block(params, ff, pts_np)
         assert_value_bars(np.abs(got - ref), max(1.0, float(np.abs(ref).max())), f"{hidden} m={m} {kind}/{head} n={n}")
     ns.close()
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 1027, 20001])
+def test_lookup_rows_matches_lookup(golden, n):
+    """nvdb_lookup_rows (the query's lookup with the neural rows appended,
+    decoder.py:243) against nvdb_lookup: identical value / active / kind,
+    rows = exactly the active leaf-voxel rows (any order, no duplicates),
+    on batch sizes with and without a ragged tail of < 4 queries."""
+    z = golden("lookup_small")
+    g = grid_from_arrays(z)
+    tree = DeviceTree(g)
+    rng = np.random.default_rng(n + 3)
+    lo = np.asarray(g.leaf_origins).min(axis=0) - 16 if len(g.leaf_origins) else np.zeros(3, np.int64)
+    hi = np.asarray(g.leaf_origins).max(axis=0) + 24 if len(g.leaf_origins) else np.full(3, 64)
+    coords = torch.from_numpy(rng.integers(lo, hi, size=(n, 3)).astype(np.int32)).to(DEV)
+    v, a, k = tree.lookup(coords)
+    v2, a2, k2, rows, cnt, npt = tree.lookup_rows(coords)
+    torch.cuda.synchronize()
+    assert torch.equal(a, a2) and torch.equal(k, k2)
+    assert torch.equal(v.view(torch.int32), v2.view(torch.int32))
+    want = ((a == 1) & (k == 2)).nonzero().flatten().cpu().numpy()
+    c = int(cnt.item())
+    got = np.sort(rows[:c].cpu().numpy())
+    assert int(npt.item()) + c == want.size  # the test grid has no exact patches: npatched == 0
+    np.testing.assert_array_equal(got, want)
 
 
 def test_lookup_extreme_and_empty_coordinates(golden):

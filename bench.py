@@ -152,6 +152,59 @@ def accept_config():
                        significance_threshold=0.0, strict_topology=False, seed=4242)
 
 
+def dragon_config():
+    """SURVEY.md §8(d) C2 throughput nets, the Table-3 "Dragon" row
+    (PAPER.md:430-443): L1 3x64, L0/voxel 3x128, sine/1.5, ffm 10/256."""
+    from paper_2208_04448_b200.encoder import TrainConfig
+    return TrainConfig(subdomain_size=512, l1_net=(3, 64), tile_net=None, l0_net=(3, 128), voxel_net=(3, 128),
+                       activation="sine", frequency=1.5, ffm_scale=10.0, ffm_size=256, lr=1e-3, decay=0.975,
+                       interval=100.0, max_epochs=800, sample_interval=1, batch_size=65536,
+                       significance_threshold=0.0, strict_topology=False, seed=4242)
+
+
+def c2_dragon(grid, dev, steps, peaks):
+    """C2 with the survey's throughput nets (Dragon shape):
+    the same encode() path trains them on the device (layer-streamed kernels:
+    3x128/m256 exceeds the fused narrow kernel), then the whole-volume decode
+    is device-timed like the headline (L2 flushed between steps); the
+    3x128 weights are streamed through the MLP kernel's weight ring."""
+    import torch
+    from paper_2208_04448_b200.decoder import DeviceModel
+    timings = []
+    c = train_container(grid, dragon_config(), dev, timings)
+    m = DeviceModel(c, dev)
+    for _ in range(3):
+        d = m.decode(True)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ts = []
+    for _ in range(max(steps, 3)):
+        flush.random_(0, 255)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d = m.decode(True)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    nvox, nact = d.leaf_count * 512, d.regressor_evaluations
+    e = c.experts[0]
+    F = {t: fwd_flops(n) for t, n in e.nets() if n is not None}
+    flop = m.n1 * 4096 * F["l1"] + nvox * F["l0"] + nact * F["voxel"]
+    tms = sum(t["ms"] for t in timings)
+    tflop = sum(t["epochs"] * t["batch"] * t["flops_per_sample"] for t in timings)
+    tsamp = sum(t["epochs"] * t["batch"] for t in timings)
+    m.close()
+    return {"workload": "C2 torus 512^3, Dragon nets (L1 3x64/m128, L0+voxel 3x128/m256, sine 1.5, ffm 10, "
+                        "800 epochs, B=65536) trained by encode(), whole-volume decode",
+            "leaf_voxels": nvox, "active_voxels": nact, "decode_ms": ms, "decode_voxels_per_s": nvox / (ms * 1e-3),
+            "decode_tflops": flop / (ms * 1e-3) / 1e12,
+            "decode_frac": flop / (ms * 1e-3) / 1e12 / float(peaks["bf16_tflops"]),
+            "train": {"samples_per_s": tsamp / (tms * 1e-3), "ms": tms, "tflops": tflop / (tms * 1e-3) / 1e12,
+                      "frac_sustained": tflop / (tms * 1e-3) / 1e12 / float(peaks["bf16_tflops_sustained"]),
+                      "nets": [{k: v for k, v in t.items()} for t in timings]}}
+
+
 def make_grid(workload):
     from paper_2208_04448_b200.procgen import sphere_sdf, torus_sdf
     if workload == "c1":
@@ -572,6 +625,7 @@ def main():
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 encode + sharded decode pipeline")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5-shaped 1e9 random-query measurement")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4-shaped warm-start sequence measurement")
+    ap.add_argument("--no-dragon", action="store_true", help="skip the C2 run with the survey's Dragon nets")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
@@ -686,6 +740,12 @@ def main():
                                   "unit": "TFLOP/s", "frac": c3["decode_tflops"] / float(peaks["bf16_tflops"])}
         except Exception as ex:  # noqa: BLE001 -- the headline line must still print
             c3 = {"error": repr(ex)[:300]}
+    dragon = None
+    if rank == 0 and world == 1 and args.workload == "c2" and not args.no_dragon:
+        try:
+            dragon = c2_dragon(grid, dev, args.steps, peaks)
+        except Exception as ex:  # noqa: BLE001 -- the headline line must still print
+            dragon = {"error": repr(ex)[:300]}
     c4 = None
     if rank == 0 and world == 1 and not args.no_c4:
         try:
@@ -756,6 +816,7 @@ def main():
                          "per_stage_ms": {k: v[1] / args.steps for k, v in per_tag.items()},
                          "co_bound": mufu_cobound(ktr, kms, transc, clocks)},
             "query": query,
+            "c2_dragon": dragon,
             "c3": c3,
             "c4_sequence": c4,
             "c5_query": c5,

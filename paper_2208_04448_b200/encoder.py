@@ -231,6 +231,85 @@ def gather_expert_data(grid: DenseLeafGrid, sub: Subdomain, value_scale: float, 
     return data
 
 
+class DeviceGrid:
+    """A dense-leaf grid's arrays on the device, uploaded once per encode, so
+    that every expert's training sets (encoder.py:197-235) are gathered there
+    instead of in host numpy (C3: 8 experts x ~80 M leaf voxels)."""
+
+    def __init__(self, grid: DenseLeafGrid, device=None):
+        import torch
+        dev = _dev(device)
+        self.dev = dev
+
+        def up(a, dt=None):
+            a = np.ascontiguousarray(a if dt is None else np.asarray(a, dt))
+            return torch.from_numpy(a).to(dev)
+        self.l1_origins = up(grid.l1_origins, np.int64).reshape(-1, 3)
+        self.l1_child = up(grid.l1_child, np.bool_).reshape(-1, L1_SIZE)
+        self.l1_active = up(grid.l1_active, np.bool_).reshape(-1, L1_SIZE)
+        self.l1_tiles = up(grid.l1_tiles, np.float32).reshape(-1, L1_SIZE)
+        self.leaf_origins = up(grid.leaf_origins, np.int64).reshape(-1, 3)
+        self.leaf_active = up(grid.leaf_active, np.bool_).reshape(-1, LEAF_SIZE)
+        self.leaf_values = up(grid.leaf_values, np.float32).reshape(-1, LEAF_SIZE)
+        self.slot_center = torch.from_numpy(SLOT_CENTER).to(dev)
+        self.voxel_center = torch.from_numpy(VOXEL_CENTER).to(dev)
+
+
+def gather_expert_data_device(grid: DenseLeafGrid, dg: DeviceGrid, sub: Subdomain, value_scale: float,
+                              norm=None) -> ExpertData:
+    """gather_expert_data on the device: the same f64 centre / normalisation
+    arithmetic (IEEE, so bit-identical to the numpy form) and the same row
+    order; the fields are device tensors."""
+    import torch
+    lo, hi = sub.expanded_lo(), sub.expanded_hi()
+    no, ns = expert_norm(sub, grid) if norm is None else norm
+    data = ExpertData(sub=sub, norm_origin=no, norm_scale=ns)
+    dev = dg.dev
+    no_t = torch.as_tensor(np.asarray(no, np.float64), device=dev)
+    # divisors as device tensors: torch divides by a host scalar as a
+    # multiplication by its reciprocal, which is not the IEEE quotient numpy takes
+    ns_t = torch.tensor([float(ns)], dtype=torch.float64, device=dev)
+    vs_t = torch.tensor([float(value_scale)], dtype=torch.float32, device=dev)
+    lo_t = torch.as_tensor(np.asarray(lo, np.int64), device=dev)
+    hi_t = torch.as_tensor(np.asarray(hi, np.int64), device=dev)
+
+    def nrm(c):
+        return torch.div(c - no_t, ns_t).to(torch.float32)
+
+    def boxes(origins, span):
+        if origins.shape[0] == 0:
+            return torch.zeros(0, dtype=torch.bool, device=dev)
+        return torch.all((origins + span > lo_t) & (origins < hi_t), dim=1)
+
+    sel1 = boxes(dg.l1_origins, 128)
+    if bool(sel1.any()):
+        org = dg.l1_origins[sel1]
+        cen = (org[:, None, :].to(torch.float64) + dg.slot_center[None]).reshape(-1, 3)
+        child = dg.l1_child[sel1].reshape(-1)
+        active = dg.l1_active[sel1].reshape(-1)
+        labels = torch.full(child.shape, L1_CLASS_INACTIVE_TILE, dtype=torch.int64, device=dev)
+        labels[active & ~child] = L1_CLASS_ACTIVE_TILE
+        labels[child] = L1_CLASS_CHILD
+        data.l1_inputs = nrm(cen)
+        data.l1_labels = labels
+        tsel = active & ~child
+        if bool(tsel.any()):
+            data.tile_inputs = data.l1_inputs[tsel]
+            data.tile_targets = torch.div(dg.l1_tiles[sel1].reshape(-1)[tsel], vs_t)
+    sel0 = boxes(dg.leaf_origins, 8)
+    if bool(sel0.any()):
+        org = dg.leaf_origins[sel0]
+        cen = (org[:, None, :].to(torch.float64) + dg.voxel_center[None]).reshape(-1, 3)
+        act = dg.leaf_active[sel0].reshape(-1)
+        data.l0_inputs = nrm(cen)
+        del cen
+        data.l0_labels = act.to(torch.float32)
+        if bool(act.any()):
+            data.vox_inputs = data.l0_inputs[act]
+            data.vox_targets = torch.div(dg.leaf_values[sel0].reshape(-1)[act], vs_t)
+    return data
+
+
 @dataclass
 class NetSpec:
     tag: str
@@ -298,8 +377,14 @@ class DeviceTrainer:
         self.n = n
         self.max_epochs = int(cfg.max_epochs)
         self.batch, self.sampled = int(cfg.batch_size), bool(sampled)
-        self.x = torch.from_numpy(np.ascontiguousarray(inputs, dtype=np.float32).reshape(-1, 3)).to(self.dev)
-        self.y = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.float32).reshape(-1)).to(self.dev)
+        if isinstance(inputs, torch.Tensor):  # device-gathered training set (gather_expert_data_device)
+            self.x = inputs.to(self.dev, torch.float32).reshape(-1, 3).contiguous()
+        else:
+            self.x = torch.from_numpy(np.ascontiguousarray(inputs, dtype=np.float32).reshape(-1, 3)).to(self.dev)
+        if isinstance(targets, torch.Tensor):
+            self.y = targets.to(self.dev, torch.float32).reshape(-1).contiguous()
+        else:
+            self.y = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.float32).reshape(-1)).to(self.dev)
         E = self.max_epochs
         ep = np.arange(E, dtype=np.float64)
         # lr_at in float64 then np.float32 (neural.py:215-219, encoder.py:366)
@@ -474,8 +559,20 @@ def _train_flops(layers) -> int:
     return int(2 * (3 * sum(macs) - macs[0]))
 
 
-def _check_targets(targets: np.ndarray, kind: str, out_dim: int) -> None:
+def _check_targets(targets, kind: str, out_dim: int) -> None:
     """Label / target validation of neural.py:282-283, 295-296 (ValueError)."""
+    import torch
+    if isinstance(targets, torch.Tensor):
+        t = targets
+        if kind == "ce":
+            if t.numel() and (bool(t.min() < 0) or bool(t.max() >= out_dim)):
+                raise ValueError("class label outside head arity")
+        elif kind == "bce":
+            if bool(((t != 0) & (t != 1)).any()):
+                raise ValueError("binary targets must be 0 or 1")
+        if t.is_floating_point() and bool(torch.isnan(t).any()):
+            raise ValueError("NaN in targets")
+        return
     t = np.asarray(targets)
     if kind == "ce":
         if t.size and (t.min() < 0 or t.max() >= out_dim):
@@ -505,8 +602,9 @@ def make_trainer(inputs: np.ndarray, targets: np.ndarray, spec: NetSpec, cfg, ex
     else:
         ff = FourierFeatures(spec.m, cfg.ffm_scale, seed_ff)
         params = init_mlp(2 * spec.m, [width] * depth, spec.out_dim, activation, spec.head, seed_init)
-    x = np.asarray(inputs)
-    if np.isnan(x).any():
+    import torch
+    x = inputs if isinstance(inputs, torch.Tensor) else np.asarray(inputs)
+    if (bool(torch.isnan(x).any()) if isinstance(x, torch.Tensor) else np.isnan(x).any()):
         raise ValueError("NaN in batch inputs")
     _check_targets(targets, spec.loss_kind, spec.out_dim)
     n = x.shape[0]
@@ -629,13 +727,14 @@ _EXPERT_NETS = (("l1", "l1_classifier"), ("tile", "tile_regressor"), ("l0", "l0_
 
 
 def _prepare_expert(grid: DenseLeafGrid, sub: Subdomain, cfg, lr0: float, warm=None, stop_losses=None,
-                    device=None, group=None):
+                    device=None, group=None, dgrid: Optional[DeviceGrid] = None):
     """encoder.py:531-570 up to training: the expert's data and one trainer per
     net (l1, tile, l0, voxel), not yet run."""
     scale = value_scale_of(grid)
     norm = (np.asarray(warm.norm_origin, dtype=np.float64).copy(), float(warm.norm_scale)) \
         if warm is not None else None
-    data = gather_expert_data(grid, sub, scale, norm=norm)
+    data = gather_expert_data_device(grid, dgrid, sub, scale, norm=norm) if dgrid is not None \
+        else gather_expert_data(grid, sub, scale, norm=norm)
     expert = EncodedSubdomain(id=sub.id, cell=sub.cell, cluster_id=sub.cluster_id, norm_origin=data.norm_origin,
                               norm_scale=data.norm_scale, value_scale=scale)
     inputs = {"l1": (data.l1_inputs, data.l1_labels), "tile": (data.tile_inputs, data.tile_targets),
@@ -666,9 +765,10 @@ def _train_experts(grid: DenseLeafGrid, subs, cfg, lr0: float, warm_of, stops_of
     latency-bound per tile and a smaller share lengthens each CTA's tile
     chain; DESIGN.md "Training".)"""
     experts = []
+    dgrid = DeviceGrid(grid, device) if subs else None  # training sets gathered on the device
     for sub in subs:
         expert, jobs = _prepare_expert(grid, sub, cfg, lr0, warm=warm_of(sub), stop_losses=stops_of(sub),
-                                       device=device, group=group)
+                                       device=device, group=group, dgrid=dgrid)
         try:
             for attr, tr, ff in jobs:
                 loss, epochs = tr.run()

@@ -634,11 +634,14 @@ def train_network(inputs: np.ndarray, targets: np.ndarray, spec: NetSpec, cfg, e
 
 
 def extract_patches(grid: DenseLeafGrid, layout: SubdomainLayout, experts: List[EncodedSubdomain], cfg,
-                    device=None, only=None) -> None:
+                    device=None, only=None, dgrid: Optional[DeviceGrid] = None) -> None:
     """Classifier disagreements vs ground truth become patches (encoder.py:430-486).
 
     Predictions come from the same fused blended evaluator the decoder uses.
     ``only``: subdomain ids to extract (an expert-parallel rank's own).
+    ``dgrid``: the grid on the device; the level-0 comparison (every leaf
+    voxel of the core box) then runs there and only the disagreeing rows
+    come back to the host.
     """
     band = grid.half_width * grid.voxel_size
     if cfg.significance_threshold is not None:
@@ -671,6 +674,10 @@ def extract_patches(grid: DenseLeafGrid, layout: SubdomainLayout, experts: List[
                 so = (org[:, None, :] + (L1_LOCAL * 8)[None]).reshape(-1, 3)
                 bad = np.flatnonzero(pred != truth)
                 patches.l1.extend_arrays(so[bad], truth[bad])
+            if dgrid is not None:
+                _l0_patches_device(grid, dgrid, sub, ev, cfg, band, eps, patches)
+                expert.patches = patches
+                continue
             own0 = np.all((grid.leaf_origins >= sub.lo) & (grid.leaf_origins < sub.hi), axis=1) \
                 if grid.leaf_origins.shape[0] else np.zeros(0, bool)
             if own0.any():
@@ -697,6 +704,44 @@ def extract_patches(grid: DenseLeafGrid, layout: SubdomainLayout, experts: List[
             expert.patches = patches
     finally:
         ev.close()
+
+
+def _l0_patches_device(grid: DenseLeafGrid, dg: DeviceGrid, sub, ev, cfg, band: float, eps: float,
+                       patches: PatchList) -> None:
+    """extract_patches' level-0 stage (encoder.py:461-486) on the device: the
+    same masks (comparisons of f32 values against the f32-cast thresholds, as
+    numpy's weak-scalar rules do), rows in the same order."""
+    dev = dg.dev
+    if dg.leaf_origins.shape[0] == 0:
+        return
+    lo = torch.as_tensor(np.asarray(sub.lo, np.int64), device=dev)
+    hi = torch.as_tensor(np.asarray(sub.hi, np.int64), device=dev)
+    own0 = torch.all((dg.leaf_origins >= lo) & (dg.leaf_origins < hi), dim=1)
+    idx = own0.nonzero().flatten()
+    if idx.numel() == 0:
+        return
+    org = dg.leaf_origins[idx]
+    d_org = org.to(torch.int32).contiguous()
+    n = org.shape[0] * LEAF_SIZE
+    pred = torch.empty(n, dtype=torch.uint8, device=dev)
+    ev.evaluate("l0", _lib.SRC_LEAF_VOX, d_org, n, _lib.OUT_L0ACTIVE, u8=pred)
+    truth = dg.leaf_active[idx].reshape(-1)
+    values = dg.leaf_values[idx].reshape(-1)
+    disagree = pred.bool() != truth
+    if not cfg.strict_topology:
+        keep = truth.clone()
+        if grid.grid_class == GRID_CLASS_SDF:
+            keep &= values.abs() < float(np.float32(band - eps))
+        else:
+            keep &= values > float(np.float32(eps))
+        disagree &= keep
+    bad = disagree.nonzero().flatten()
+    if bad.numel() == 0:
+        return
+    act = truth[bad]
+    coords = org[bad // LEAF_SIZE] + torch.from_numpy(LEAF_LOCAL).to(dev)[bad % LEAF_SIZE]
+    vals = torch.where(act, values[bad].to(torch.float64), torch.zeros((), dtype=torch.float64, device=dev))
+    patches.l0.extend_arrays(coords.cpu().numpy(), act.cpu().numpy().astype(bool), vals.cpu().numpy())
 
 
 def build_upper_tree(grid: DenseLeafGrid) -> UpperTree:
@@ -758,14 +803,16 @@ def _prepare_expert(grid: DenseLeafGrid, sub: Subdomain, cfg, lr0: float, warm=N
     return expert, jobs
 
 
-def _train_experts(grid: DenseLeafGrid, subs, cfg, lr0: float, warm_of, stops_of, device=None, group=None):
+def _train_experts(grid: DenseLeafGrid, subs, cfg, lr0: float, warm_of, stops_of, device=None, group=None,
+                   dgrid: Optional[DeviceGrid] = None):
     """Train every net of every given expert, one after another, each net on
     the whole GPU.  (Running a container's nets concurrently on SM shares was
     measured: +16 % at best for two ACCEPT nets, because the epoch kernels are
     latency-bound per tile and a smaller share lengthens each CTA's tile
     chain; DESIGN.md "Training".)"""
     experts = []
-    dgrid = DeviceGrid(grid, device) if subs else None  # training sets gathered on the device
+    if dgrid is None and subs:
+        dgrid = DeviceGrid(grid, device)  # training sets gathered on the device
     for sub in subs:
         expert, jobs = _prepare_expert(grid, sub, cfg, lr0, warm=warm_of(sub), stop_losses=stops_of(sub),
                                        device=device, group=group, dgrid=dgrid)
@@ -818,7 +865,8 @@ def encode(grid, cfg, weight_precision: int = 32, workers: int = 1, _warm=None, 
             return None
         return {tag: _stop_losses[(sub.cell, tag)] for tag in NET_TAGS if (sub.cell, tag) in _stop_losses}
 
-    experts = _train_experts(g, mine_subs, cfg, lr0, warm_of, stops_of, device=device, group=dp_group)
+    dgrid = DeviceGrid(g, device)  # the grid on the device once: training sets and patch extraction
+    experts = _train_experts(g, mine_subs, cfg, lr0, warm_of, stops_of, device=device, group=dp_group, dgrid=dgrid)
     if expert_parallel:
         # every rank needs all experts: patch extraction blends across
         # subdomain boundaries and the container holds every expert
@@ -827,7 +875,7 @@ def encode(grid, cfg, weight_precision: int = 32, workers: int = 1, _warm=None, 
         dist.all_gather_object(got, experts, group=group)
         experts = sorted((e for part in got for e in part), key=lambda e: e.id)
         mine = [s.id for i, s in enumerate(layout.subdomains) if i % world == rank]
-        extract_patches(g, layout, experts, cfg, device, only=set(mine))
+        extract_patches(g, layout, experts, cfg, device, only=set(mine), dgrid=dgrid)
         pats: list = [None] * world
         dist.all_gather_object(pats, {e.id: e.patches for e in experts if e.id in mine}, group=group)
         by_id = {e.id: e for e in experts}
@@ -835,7 +883,8 @@ def encode(grid, cfg, weight_precision: int = 32, workers: int = 1, _warm=None, 
             for sid, p in part.items():
                 by_id[sid].patches = p
     else:
-        extract_patches(g, layout, experts, cfg, device)
+        extract_patches(g, layout, experts, cfg, device, dgrid=dgrid)
+    del dgrid
     meta = GridMeta(g.grid_class, g.background, g.voxel_size, g.half_width, value_scale_of(g))
     return NeuralGridContainer(grid_meta=meta, upper_tree=build_upper_tree(g), layout=layout, experts=experts,
                                config=replace(cfg) if hasattr(cfg, "__dataclass_fields__") else cfg,

@@ -553,3 +553,25 @@ def test_device_gather_matches_reference(golden):
     a, b = gather_expert_data(g, s, value_scale_of(g)), gather_expert_data_device(g, DeviceGrid(g, DEV), s, value_scale_of(g))
     for k in ("l1_inputs", "l1_labels", "l0_inputs", "l0_labels", "vox_inputs", "vox_targets"):
         np.testing.assert_array_equal(getattr(b, k).cpu().numpy(), getattr(a, k), err_msg=f"sphere {k}")
+
+
+def test_device_patch_extraction_matches_host():
+    """extract_patches' level-0 stage on the device (dgrid) gives the same
+    patch records, in the same order, as the host form (encoder.py:461-486)
+    on the AC4 sphere and on an 8-expert FOG-class straddling grid."""
+    from bench import accept_config
+    from paper_2208_04448_b200.encoder import DeviceGrid, decompose, extract_patches
+    from paper_2208_04448_b200.procgen import sphere_sdf
+    g = sphere_sdf((63.5, 63.5, 63.5), 61.0, 1.0, 3.0)
+    cfg = accept_config()
+    cfg = type(cfg)(**{**cfg.__dict__, "max_epochs": 60})
+    c = encode(g, cfg, device=DEV)
+    layout = decompose(g, cfg.subdomain_size)
+    extract_patches(g, layout, c.experts, cfg, DEV)
+    host = [(e.id, [np.array(x) for x in (e.patches.l0._keys, *e.patches.l0._cols)]) for e in c.experts]
+    extract_patches(g, layout, c.experts, cfg, DEV, dgrid=DeviceGrid(g, DEV))
+    for (eid, h), e in zip(host, c.experts):
+        d = [np.array(x) for x in (e.patches.l0._keys, *e.patches.l0._cols)]
+        assert len(h[0]) > 0
+        for a, b in zip(h, d):
+            np.testing.assert_array_equal(a, b, err_msg=f"expert {eid}")

@@ -382,6 +382,26 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       w_refill(false);
     }
   };
+  // `cnt` consecutive K = 16 MMAs (A advancing 256 = 4 KB per step): whole
+  // 4-chunk slots go out as one umma_f16_x4
+  auto w_mma_run = [&](uint32_t d, uint64_t adesc, uint32_t idesc, uint32_t acc, int cnt) {
+    for (int k = 0; k < cnt;) {
+      if (wpc == 0 && wp == 4 && cnt - k >= 4) {
+        w_next();
+        umma_f16_x4(d, adesc, wdesc, idesc, acc, 256, wdstep);
+        umma_commit(wempty + wcur);
+        w_advance();
+        w_refill(false);
+        k += 4;
+        adesc += 1024;
+      } else {
+        w_mma(d, adesc, idesc, acc, false, 0);
+        ++k;
+        adesc += 256;
+      }
+      acc = 1;
+    }
+  };
   // an engine without a tile in this (sub-)round still consumes the tile's slots
   auto w_skip_tile = [&]() {
     const uint32_t nk = s_net.wimg_bytes / ((uint32_t)s_net.width * 32u * wp);
@@ -711,7 +731,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
           tc_fence_after();
           uint64_t ad = smem_desc(asm_, kTileM * 16, 128);
           if (a.wstream) {
-            for (int k = 0; k < width / 16; ++k, ad += 256) w_mma(dcol, ad, idesc, k != 0, false, 0);
+            w_mma_run(dcol, ad, idesc, 0u, width / 16);
             TRC(30 + l, t);
           } else {
             uint64_t bd = smem_desc(w_s + (uint32_t)(width * k0 * 2 + l * width * width * 2), width * 16, 128);

@@ -11,6 +11,23 @@
 using namespace nvdb;
 
 constexpr int W = 256;
+
+// four K = 16 MMAs (B advancing by bstep, A by astep) in one asm block: one
+// ELECT / R2UR sequence for the group instead of one per MMA
+__device__ __forceinline__ void umma_f16_x4(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc,
+                                            uint64_t astep, uint64_t bstep) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.u64 a1, %1, %5;\n\tadd.u64 a2, a1, %5;\n\tadd.u64 a3, a2, %5;\n\t"
+      "add.u64 b1, %2, %6;\n\tadd.u64 b2, b1, %6;\n\tadd.u64 b3, b2, %6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n\t}" ::"r"(d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "l"(astep), "l"(bstep)
+      : "memory");
+}
 constexpr uint32_t kChunk = W * 32;  // one K = 16 chunk
 
 __global__ void __launch_bounds__(128, 1) k(const uint8_t* __restrict__ wimg, uint32_t nchunks, int WR, int PIECES,
@@ -85,7 +102,7 @@ __global__ void __launch_bounds__(128, 1) k(const uint8_t* __restrict__ wimg, ui
       uint32_t fpos = 0, fc = 0;  // next fill position and its chunk
       const uint32_t npos = nslots_total;
       const long long t2 = clock64();
-      for (; fpos < (uint32_t)AHEAD; ++fpos) {
+      for (; fpos < (uint32_t)(AHEAD % 100); ++fpos) {
         const uint32_t sl = fpos & (WR - 1);
         mbar_arrive_expect_tx(&full[sl], slot_bytes);
         bulk_g2s(ring + sl * slot_bytes, wimg + (size_t)fc * kChunk, slot_bytes, &full[sl]);
@@ -111,7 +128,9 @@ __global__ void __launch_bounds__(128, 1) k(const uint8_t* __restrict__ wimg, ui
         tc_fence_after();
         c1 = clock64(); acc[4] += c1 - c0; c0 = c1;
         uint64_t bd = bd0 + sl * dstep;
-        for (int p = 0; p < PIECES; ++p, bd += pstep) umma_f16(tslot, ad, bd, idesc, 1u);
+        if (AHEAD >= 100 && PIECES == 4) umma_f16_x4(tslot, ad, bd, idesc, 1u, 0, pstep);
+        else
+          for (int p = 0; p < PIECES; ++p, bd += pstep) umma_f16(tslot, ad, bd, idesc, 1u);
         c1 = clock64(); acc[5] += c1 - c0; c0 = c1;
         umma_commit(&empty[sl]);
         c1 = clock64(); acc[6] += c1 - c0; c0 = c1;
@@ -145,7 +164,7 @@ int main() {
   const int iters = 64;
   // MODE 0: as mlp_eval; 1: no tcgen05 fence after the wait; 2: one commit per two slots;
   // 3: no wait on the full barrier (data race, timing only); 4: each CTA starts at another chunk
-  int cfg[][4] = {{8, 1, 4, 11}, {4, 2, 2, 11}, {2, 4, 1, 11}};
+  int cfg[][4] = {{2, 4, 1, 11}, {2, 4, 101, 11}, {4, 4, 2, 11}, {4, 4, 102, 11}};
   for (auto& c : cfg) {
     const int WR = c[0], PIECES = c[1], AHEAD = c[2], MODE = c[3];
     for (int rep = 0; rep < 2; ++rep) {

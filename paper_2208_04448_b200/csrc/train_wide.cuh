@@ -209,6 +209,26 @@ __global__ void __launch_bounds__(128 * kLwMaxEngines, 1) k_lw_fb(const LwFbArgs
       w_refill();
     }
   };
+  // `cnt` consecutive chunks (A advancing 256 = 4 KB per step): whole
+  // 4-chunk slots go out as one umma_f16_x4 (one ELECT/R2UR sequence)
+  auto w_mma_run = [&](uint64_t adesc, uint32_t acc, int cnt) {
+    for (int k = 0; k < cnt;) {
+      if (wpc == 0 && wp == 4 && cnt - k >= 4) {
+        w_next();
+        umma_f16_x4(zcol, adesc, wdesc, idesc, acc, 256, wdstep);
+        umma_commit(wempty + wcur);
+        w_advance();
+        w_refill();
+        k += 4;
+        adesc += 1024;
+      } else {
+        w_mma(adesc, acc);
+        ++k;
+        adesc += 256;
+      }
+      acc = 1;
+    }
+  };
   auto w_skip_tile = [&]() {
     for (uint32_t c = 0; c < nkp; ++c) {
       w_next();
@@ -268,7 +288,7 @@ __global__ void __launch_bounds__(128 * kLwMaxEngines, 1) k_lw_fb(const LwFbArgs
         tc_fence_after();
         const uint64_t ad = smem_desc(buf, kTileM * 16, 128);
 #pragma unroll
-        for (int k = 0; k < kLwChunkK / 16; ++k) w_mma(ad + (uint64_t)(k * 256), (ch | k) != 0);
+        w_mma_run(ad, ch != 0 ? 1u : 0u, kLwChunkK / 16);
         umma_commit(slot_free + s);
         if (ch == nch - 1) umma_commit(mdone);
       }
@@ -332,7 +352,7 @@ __global__ void __launch_bounds__(128 * kLwMaxEngines, 1) k_lw_fb(const LwFbArgs
         if (issuer) {
           tc_fence_after();
           const uint64_t ad = smem_desc(region, kTileM * 16, 128);
-          for (int k = 0; k < W / 16; ++k) w_mma(ad + (uint64_t)(k * 256), k != 0);
+          w_mma_run(ad, 0u, W / 16);
           umma_commit(mdone);
         }
       }
@@ -433,7 +453,7 @@ __global__ void __launch_bounds__(128 * kLwMaxEngines, 1) k_lw_fb(const LwFbArgs
         if (issuer) {
           tc_fence_after();
           const uint64_t ad = smem_desc(region, kTileM * 16, 128);
-          for (int k = 0; k < W / 16; ++k) w_mma(ad + (uint64_t)(k * 256), k != 0);
+          w_mma_run(ad, 0u, W / 16);
           umma_commit(mdone);
         }
       }

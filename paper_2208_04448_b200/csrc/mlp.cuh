@@ -626,9 +626,13 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
           if (kch > 32) w_mma(dcol, ad + 512, idesc, 1, false, 0);
         } else {
           const uint64_t bd = bdesc0 + (uint64_t)(ch * (kEChunkK / 16) * bstep);
-          umma_f16(dcol, ad, bd, idesc, ch != 0);
-          if (kch > 16) umma_f16(dcol, ad + 256, bd + bstep, idesc, 1);
-          if (kch > 32) umma_f16(dcol, ad + 512, bd + 2 * bstep, idesc, 1);
+          if (kch == 48) {  // one asm block (one ELECT / R2UR sequence) for the chunk's 3 MMAs
+            umma_f16_x3(dcol, ad, bd, idesc, ch != 0, 256, bstep);
+          } else {
+            umma_f16(dcol, ad, bd, idesc, ch != 0);
+            if (kch > 16) umma_f16(dcol, ad + 256, bd + bstep, idesc, 1);
+            if (kch > 32) umma_f16(dcol, ad + 512, bd + 2 * bstep, idesc, 1);
+          }
         }
         umma_commit(slot_free + s);
         if (ch == nch - 1) umma_commit(mdone);
@@ -735,12 +739,10 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
             TRC(30 + l, t);
           } else {
             uint64_t bd = smem_desc(w_s + (uint32_t)(width * k0 * 2 + l * width * width * 2), width * 16, 128);
-            umma_f16(dcol, ad, bd, idesc, 0);
-            for (int k = 1; k < width / 16; ++k) {
-              bd += bstep;
-              ad += 256;
-              umma_f16(dcol, ad, bd, idesc, 1);
-            }
+            int k = 0;
+            for (; k + 3 <= width / 16; k += 3, ad += 768, bd += 3 * bstep)
+              umma_f16_x3(dcol, ad, bd, idesc, k != 0, 256, bstep);
+            for (; k < width / 16; ++k, ad += 256, bd += bstep) umma_f16(dcol, ad, bd, idesc, k != 0);
             TRC(30 + l, t);
           }
           umma_commit(mdone);

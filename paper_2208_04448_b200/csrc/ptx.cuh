@@ -179,6 +179,23 @@ __device__ __forceinline__ void umma_f16_x3(uint32_t d_tmem, uint64_t adesc, uin
       : "memory");
 }
 
+// n consecutive K = 16 MMAs into one accumulator (descriptors advancing by
+// astep / bstep), in groups of 4 and 3 from single asm blocks
+__device__ __forceinline__ void umma_f16_run(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate, int n, uint64_t astep, uint64_t bstep) {
+  int k = 0;
+  for (; k + 4 <= n; k += 4, adesc += 4 * astep, bdesc += 4 * bstep, accumulate = 1)
+    umma_f16_x4(d_tmem, adesc, bdesc, idesc, accumulate, astep, bstep);
+  if (k + 3 <= n) {
+    umma_f16_x3(d_tmem, adesc, bdesc, idesc, accumulate, astep, bstep);
+    k += 3;
+    adesc += 3 * astep;
+    bdesc += 3 * bstep;
+    accumulate = 1;
+  }
+  for (; k < n; ++k, adesc += astep, bdesc += bstep, accumulate = 1) umma_f16(d_tmem, adesc, bdesc, idesc, accumulate);
+}
+
 // D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16; A rows = TMEM lanes, two fp16
 // per 32-bit column (K-step of 16 = 8 columns)
 __device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,

@@ -436,12 +436,10 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
       named_bar_sync(1 + grp, 256);
       if (gt == 0) {
         tc_fence_after();
-#pragma unroll
-        for (int s = 0; s < kChunkK / 16; ++s) {
-          const uint64_t ad = smem_desc(buf + s * (2 * kTileM * 16), kTileM * 16, 128);
-          const uint32_t wb = w_s + (uint32_t)(((ch * kChunkK + s * 16) >> 3) * (width >> 3) * 128);
-          umma_f16(tcol, ad, smem_desc(wb, width * 16, 128), idesc, (ch | s) != 0);
-        }
+        // the chunk's MMAs from single asm blocks (one ELECT / R2UR sequence per group)
+        umma_f16_run(tcol, smem_desc(buf, kTileM * 16, 128),
+                     smem_desc(w_s + (uint32_t)(((ch * kChunkK) >> 3) * (width >> 3) * 128), width * 16, 128), idesc,
+                     ch != 0, kChunkK / 16, 256, (uint64_t)(width * 2));
         umma_commit(bar_c0 + bsel);
         if (ch == nch - 1) umma_commit(bar_layer);
       }
@@ -528,11 +526,8 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
         if (gt == 0) {
           tc_fence_after();
           const uint32_t wl = w_s + woff;
-          for (int s = 0; s < width / 16; ++s) {
-            const uint64_t ad = smem_desc(region_s + s * (2 * kTileM * 16), kTileM * 16, 128);
-            const uint64_t bd = smem_desc(wl + (uint32_t)(s * 2 * (width >> 3) * 128), width * 16, 128);
-            umma_f16(tcol, ad, bd, idesc, s != 0);
-          }
+          umma_f16_run(tcol, smem_desc(region_s, kTileM * 16, 128), smem_desc(wl, width * 16, 128), idesc, 0u,
+                       width / 16, 256, (uint64_t)(width * 2));
           umma_commit(bar_layer);
         }
         woff += (uint32_t)(width * width * 2);
@@ -670,11 +665,8 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
           tc_fence_after();
           // W'_l image (rows o, cols i, K-major) read as B = (N = i, K = o) MN-major
           const uint32_t wl = w_s + (uint32_t)(width * k0 * 2) + (uint32_t)((l - 1) * width * width * 2);
-          for (int s = 0; s < width / 16; ++s) {
-            const uint64_t ad = smem_desc(region_s + s * (2 * kTileM * 16), kTileM * 16, 128);
-            const uint64_t bd = smem_desc(wl + (uint32_t)(s * 256), 128, width * 16);
-            umma_f16(tcol, ad, bd, idesc_bt, s != 0);
-          }
+          umma_f16_run(tcol, smem_desc(region_s, kTileM * 16, 128), smem_desc(wl, 128, width * 16), idesc_bt, 0u,
+                       width / 16, 256, 16);
           umma_commit(bar_layer);
         }
         mbar_wait(bar_layer, nlayer & 1u);
@@ -874,9 +866,8 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
         const uint32_t fb = sfe + rb * 32768;
         const uint32_t sdz = smem_addr(s_dz[qbase & 1]);
         const uint32_t idesc = idesc_f16(kTileM, W, 1, 1);
-        for (int s = 0; s < kTileM / 16; ++s)
-          umma_f16(tmem + a.col_w0 + j * W, smem_desc(fb + s * 256, 128, 2048), smem_desc(sdz + s * 256, 128, 2048),
-                   idesc, (!first || s != 0) ? 1u : 0u);
+        umma_f16_run(tmem + a.col_w0 + j * W, smem_desc(fb, 128, 2048), smem_desc(sdz, 128, 2048), idesc,
+                     !first ? 1u : 0u, kTileM / 16, 16, 16);
         umma_commit(&bars[4 + rb]);
         if (rb == 0) { nring0++; pr0 = true; } else { nring1++; pr1 = true; }
         if (j + 2 < nmt) load_feat(tau, j + 2);
@@ -891,9 +882,8 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
     if (t == 0 && do_rest) {
       const uint32_t sdz = smem_addr(s_dz[qbase & 1]);
       const uint32_t idesc = idesc_f16(kTileM, 16, 1, 0);
-      for (int s = 0; s < kTileM / 16; ++s)
-        umma_f16(tmem + col_b0, smem_desc(sdz + s * 256, 128, 2048), smem_desc(son + s * 512, 256, 128), idesc,
-                 (!first || s != 0) ? 1u : 0u);
+      umma_f16_run(tmem + col_b0, smem_desc(sdz, 128, 2048), smem_desc(son, 256, 128), idesc, !first ? 1u : 0u,
+                   kTileM / 16, 16, 32);
       done_stage(qbase);
       TTRC(11, tau);
       // ---- stages 1..depth: gW_l^T[i][o] += [a_{l-1} | 1]^T dz_l (head: dL/dout)
@@ -911,21 +901,18 @@ __device__ __forceinline__ void wg_body(const WgArgs& a, uint8_t* smem) {
         const uint32_t col = head ? col_head : col_h + (l - 1) * W;
         const uint32_t sa = smem_addr(s_act[b]);
         const uint32_t bsrc = head ? smem_addr(s_dlt[b]) : smem_addr(s_dz[b]);
-        for (int s = 0; s < kTileM / 16; ++s)
-          umma_f16(tmem + col, smem_desc(sa + s * 256, 128, 2048), smem_desc(bsrc + s * 256, 128, 2048), idesc,
-                   (!first || s != 0) ? 1u : 0u);
+        umma_f16_run(tmem + col, smem_desc(sa, 128, 2048), smem_desc(bsrc, 128, 2048), idesc, !first ? 1u : 0u,
+                     kTileM / 16, 16, 16);
         if (sep_bias) {
           const uint32_t cb = tmem + col_hb + (uint32_t)(l - 1) * 16u;
           if (!head) {  // gb_l[o] = dz_l^T 1: A = dz_l (outputs x samples), B = ones
             const uint32_t idb = idesc_f16(kTileM, 16, 1, 0);
-            for (int s = 0; s < kTileM / 16; ++s)
-              umma_f16(cb, smem_desc(bsrc + s * 256, 128, 2048), smem_desc(son + s * 512, 256, 128), idb,
-                       (!first || s != 0) ? 1u : 0u);
+            umma_f16_run(cb, smem_desc(bsrc, 128, 2048), smem_desc(son, 256, 128), idb, !first ? 1u : 0u, kTileM / 16,
+                         16, 32);
           } else {  // gb_head[o] = 1^T dL/dout: A = a ones block (SBO 0: every row group reads it), B = dL/dout
             const uint32_t idb = idesc_f16(kTileM, 16, 0, 1);
-            for (int s = 0; s < kTileM / 16; ++s)
-              umma_f16(cb, smem_desc(son, 128, 0), smem_desc(bsrc + s * 256, 128, 2048), idb,
-                       (!first || s != 0) ? 1u : 0u);
+            umma_f16_run(cb, smem_desc(son, 128, 0), smem_desc(bsrc, 128, 2048), idb, !first ? 1u : 0u, kTileM / 16,
+                         0, 16);
           }
         }
         done_stage(q);

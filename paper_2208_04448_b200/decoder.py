@@ -468,13 +468,20 @@ class DeviceModel:
 
     # -- decode --------------------------------------------------------------------
 
-    def decode(self, materialize_values: bool = True, shard: Optional[Tuple[int, int]] = None) -> "DeviceDecode":
+    def decode(self, materialize_values: bool = True, shard: Optional[Tuple[int, int]] = None,
+               prefetch_host: bool = False) -> "DeviceDecode":
         """decoder._reconstruct (decoder.py:101-211) on the device.
 
         ``shard=(rank, world)``: level-1 classification runs on every rank
         (n1*4096 slots, cheap), then the leaf list is split into ``world``
         contiguous ranges (:func:`shard_range`) and this rank classifies,
         regresses and finalizes only its own leaves -- no collective.
+
+        ``prefetch_host=True`` (``decode_full``): the arrays that are final
+        once the level-0 patches are applied (level-1 classes and tiles, leaf
+        origins, active flags) are copied to pinned host memory on a side
+        stream while the voxel stage runs; ``to_grid`` then copies only the
+        values.
         """
         dev, st = self.dev, _stream(self.dev)
         n1 = self.n1
@@ -523,6 +530,9 @@ class DeviceModel:
         err = torch.zeros(1, dtype=torch.int32, device=dev)
         check(lib().nvdb_l0_apply(_ptr(act), _ptr(self.p0_slot), _ptr(self.p0_vox), _ptr(self.p0_act),
                                   self.p0_slot.numel(), _ptr(leaf_of_slot), _ptr(err), st), "nvdb_l0_apply")
+        pre = None
+        if prefetch_host and shard is None and nl:
+            pre = self._host_prefetch([cls[:nslots], tiles[:nslots], leaf_origins[:nl], act[:nv]])
         act_ids = vals = None
         acnt = torch.zeros(1, dtype=torch.int64, device=dev)
         if materialize_values and nl:
@@ -541,8 +551,37 @@ class DeviceModel:
                                                self.neg_slot.numel(), _ptr(leaf_of_slot), self.background,
                                                -float(np.float32(self.value_scale)), _ptr(values), _ptr(words),
                                                _ptr(patched), st), "nvdb_leaf_finalize_counted")
-        return DeviceDecode(self, cls[:nslots], tiles[:nslots], child, leaf_origins[:nl], act[:nv],
-                            values[:nv], words[:nl * 8], patched[:nv], acnt, shard, err)
+        d = DeviceDecode(self, cls[:nslots], tiles[:nslots], child, leaf_origins[:nl], act[:nv],
+                         values[:nv], words[:nl * 8], patched[:nv], acnt, shard, err)
+        d.host_pre = pre
+        return d
+
+    def _host_prefetch(self, ts):
+        """Asynchronous copies of finished device arrays into one pooled pinned
+        block on a side stream, ordered after the work enqueued so far; returns
+        (numpy views, completion event)."""
+        dev = self.dev
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=dev)
+        cs = self._copy_stream
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dev))
+        cs.wait_event(ev)
+        offs, n = [], 0
+        for t in ts:
+            offs.append(n)
+            n += (t.numel() * t.element_size() + 255) & ~255
+        pin, arr = _PINNED.get(n)
+        outs = []
+        with torch.cuda.stream(cs):
+            for t, o in zip(ts, offs):
+                nb = t.numel() * t.element_size()
+                pin[o:o + nb].view(t.dtype).view(t.shape).copy_(t, non_blocking=True)
+                outs.append(arr[o:o + nb].view(_NP_DTYPE[t.dtype]).reshape(tuple(t.shape)))
+                t.record_stream(cs)
+        done = torch.cuda.Event()
+        done.record(cs)
+        return outs, done
 
 
 @dataclass
@@ -562,6 +601,7 @@ class DeviceDecode:
     shard: Optional[Tuple[int, int]] = None  # (rank, world) when only a leaf range was decoded
     err_dev: Optional[torch.Tensor] = None   # (1,) int32: a level-0 patch fell outside every leaf
     _checked: bool = False
+    host_pre: Optional[tuple] = None  # decode(prefetch_host=True): (host arrays, event) of cls / tiles / origins / active
 
     @property
     def leaf_count(self) -> int:
@@ -593,8 +633,13 @@ class DeviceDecode:
         meta = c.grid_meta
         bg = np.float32(meta.background)
         n1 = m.n1
-        cls, tiles, lo, la, lv = _to_host([self.l1_class, self.l1_tiles, self.leaf_origins,
-                                           self.leaf_active, self.leaf_values])
+        if self.host_pre is not None:
+            (cls, tiles, lo, la), done = self.host_pre
+            (lv,) = _to_host([self.leaf_values])
+            done.synchronize()
+        else:
+            cls, tiles, lo, la, lv = _to_host([self.l1_class, self.l1_tiles, self.leaf_origins,
+                                               self.leaf_active, self.leaf_values])
         cls = cls.reshape(n1, L1_SIZE)
         tiles = tiles.reshape(n1, L1_SIZE)
         lo = lo.astype(np.int64).reshape(-1, 3)
@@ -810,7 +855,7 @@ def decode_full(c, device=None, as_svcodec: bool = False, group=None):
         if d is None:
             return None
     else:
-        d = m.decode(True)
+        d = m.decode(True, prefetch_host=True)
     g = d.to_grid()
     return g.to_svcodec() if as_svcodec else g
 

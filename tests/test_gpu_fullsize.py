@@ -76,6 +76,18 @@ def test_c2_sharded_decode_equals_full(c2, world):
     assert torch.equal(torch.cat([p.leaf_values[:n] for p, n in zip(parts, nl)]), full.leaf_values[:sum(nl)])
 
 
+def test_c2_prefetched_to_grid_equals_plain(c2):
+    """decode(prefetch_host=True) (classes, tiles, origins and active flags
+    copied to the host during the voxel stage) gives the same host grid."""
+    _, m, _ = c2
+    a = m.decode(True).to_grid()
+    d = m.decode(True, prefetch_host=True)
+    assert d.host_pre is not None
+    b = d.to_grid()
+    for f in ("leaf_origins", "leaf_active", "leaf_values", "l1_origins", "l1_child", "l1_active", "l1_tiles"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
 def test_c2_query_matches_decode(c2):
     from paper_2208_04448_b200.decoder import HybridGrid
     _, m, _ = c2

@@ -28,3 +28,20 @@ for i in range(13):
         for k, v in zip(ph, (t1 - t0, t2 - t1, t3 - t2, t3 - t0)):
             ph[k].append(v * 1e3)
 print({k: round(statistics.median(v), 2) for k, v in ph.items()}, "ms")
+from paper_2208_04448_b200.decoder import decode_full  # noqa: E402
+for pf in (False, True):
+    ts = []
+    for i in range(13):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        m = DeviceModel(c, dev)
+        g = m.decode(True, prefetch_host=pf).to_grid()
+        ts.append(time.perf_counter() - t0)
+    print(f"prefetch_host={pf}: {1e3 * statistics.median(ts[3:]):.2f} ms")
+ts = []
+for i in range(13):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = decode_full(c, dev)
+    ts.append(time.perf_counter() - t0)
+print(f"decode_full {1e3 * statistics.median(ts[3:]):.2f} ms = {g.leaf_values.size / statistics.median(ts[3:]) / 1e9:.3f} G voxels/s")

@@ -397,13 +397,15 @@ __device__ __forceinline__ long long floor_div(double v, double s) { return (lon
 // tag's net with a positive gate weight (partition.py:180-229 keeps w > 0).
 __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather, int64_t n, int pass, const int32_t* cells, int ncell,
                             const int32_t* tagnet, int tag, int S, int halo, uint8_t* ncand, uint16_t* keys,
-                            int64_t* vals, BlendOut o, int nokey, int32_t* maxc, const int64_t* n_dev) {
+                            int64_t* vals, BlendOut o, int nokey, int32_t* maxc, const int64_t* n_dev,
+                            int32_t* hist, uint8_t* flags) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (n_dev && i >= *n_dev) {  // capacity tail beyond the device count: no candidate, no output
     if (pass == 0) ncand[i] = 0;
     keys[i] = (uint16_t)nokey;
     vals[i] = i;
+    if (flags) flags[i] = 0;
     return;
   }
   double c[3];
@@ -439,7 +441,10 @@ __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather
   }
   if (pass == 0) {
     ncand[i] = (uint8_t)found;
-    if (found > 1) atomicMax(maxc, found);
+    if (found > 1) {
+      atomicMax(maxc, found);
+      atomicAdd(hist + found, 1);  // points with > 1 candidate (the later passes' sizes)
+    }
     if (found == 0) {  // uncovered everywhere (inference.py:53-56 -> background)
       switch (o.out_mode) {
         case OUT_PROBS: {
@@ -461,6 +466,7 @@ __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather
   }
   keys[i] = (uint16_t)key;
   vals[i] = i;
+  if (flags) flags[i] = key != nokey ? 1 : 0;
 }
 
 // Segments of equal key in the sorted list -> tiles (pairs share a net).
@@ -512,6 +518,7 @@ __global__ void k_write_tiles(const int64_t* __restrict__ start, const int64_t* 
 
 struct WsLayout {
   size_t ncand, keys_in, keys_out, vals_in, vals_out, tiles, npairs, runs, acc, cub, total;
+  size_t flags, keys_c, vals_c, nsel;
   size_t cub_bytes;
   int64_t max_tiles;
 };
@@ -531,12 +538,22 @@ WsLayout ws_layout(const nvdb_netset* ns, int64_t n) {
   w.vals_in = take(8 * n);
   w.vals_out = take(8 * n);
   w.tiles = take(sizeof(Tile) * w.max_tiles);
-  w.npairs = take(16);  // npairs | max candidates per point
+  w.npairs = take(64);  // npairs | max candidates per point | histogram of candidate counts [9]
+  w.flags = take(n);     // later passes: the points that have a candidate in the pass
+  w.keys_c = take(2 * n);
+  w.vals_c = take(8 * n);
+  w.nsel = take(16);
   w.runs = take(8 * (3 * (size_t)std::max(ns->nnets, 1) + 1));  // start | end | toff (+1)
   w.acc = take(32 * n);
   size_t cub_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint16_t*)nullptr, (uint16_t*)nullptr, (int64_t*)nullptr,
                                   (int64_t*)nullptr, (int)std::max<int64_t>(n, 1), 0, 16);
+  size_t sel_k = 0, sel_v = 0;
+  cub::DeviceSelect::Flagged(nullptr, sel_k, (uint16_t*)nullptr, (uint8_t*)nullptr, (uint16_t*)nullptr, (int*)nullptr,
+                             (int)std::max<int64_t>(n, 1));
+  cub::DeviceSelect::Flagged(nullptr, sel_v, (int64_t*)nullptr, (uint8_t*)nullptr, (int64_t*)nullptr, (int*)nullptr,
+                             (int)std::max<int64_t>(n, 1));
+  cub_bytes = std::max(cub_bytes, std::max(sel_k, sel_v));
   w.cub_bytes = cub_bytes;
   w.cub = take(cub_bytes);
   w.total = off;
@@ -597,27 +614,54 @@ int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, c
   int kbits = 1;
   while ((1 << kbits) <= nokey) ++kbits;
   int32_t* maxc = npairs + 1;
+  int32_t* hist = npairs + 2;  // [9]
+  uint8_t* flags = base + w.flags;
+  uint16_t* kc = reinterpret_cast<uint16_t*>(base + w.keys_c);
+  int64_t* vc = reinterpret_cast<int64_t*>(base + w.vals_c);
+  int* nsel = reinterpret_cast<int*>(base + w.nsel);
   int passes = 8;
+  int32_t hh[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // maxc | hist[0..8]
   for (int pass = 0; pass < passes; ++pass) {
-    if (pass == 0) NVDB_CUDA_TRY(cudaMemsetAsync(maxc, 0, 4, st));
+    // pass 0 sorts every point; a later pass p only the points with more than
+    // p candidates (counted in pass 0), compacted first in their original
+    // order -- the same subsequence the full stable sort would put before
+    // the sentinel keys, so the tiles and results are unchanged
+    int64_t np_ = n;
+    if (pass > 0) {
+      np_ = 0;
+      for (int c = pass + 1; c <= 8; ++c) np_ += hh[1 + c];
+      if (np_ == 0) continue;
+    }
+    const bool compact = pass > 0 && np_ < n;
+    if (pass == 0) NVDB_CUDA_TRY(cudaMemsetAsync(maxc, 0, 40, st));
     k_pass_keys<<<blocks, threads, 0, st>>>(src_kind, src, gather, n, pass, ns->dev_cells, ns->nexperts, ns->dev_tagnet,
-                                            tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o, nokey, maxc, n_dev);
+                                            tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o, nokey, maxc, n_dev,
+                                            hist, compact ? flags : nullptr);
     NVDB_CHECK_LAUNCH();
     if (pass == 0) {  // later passes only exist up to the largest candidate count of this call
-      int32_t hmax = 0;
-      NVDB_CUDA_TRY(cudaMemcpyAsync(&hmax, maxc, 4, cudaMemcpyDeviceToHost, st));
+      NVDB_CUDA_TRY(cudaMemcpyAsync(hh, maxc, 40, cudaMemcpyDeviceToHost, st));
       NVDB_CUDA_TRY(cudaStreamSynchronize(st));
-      passes = std::max(1, std::min(8, (int)hmax));
+      passes = std::max(1, std::min(8, (int)hh[0]));
+    }
+    const uint16_t* ksrc = kin;
+    const int64_t* vsrc = vin;
+    if (compact) {
+      size_t cs = w.cub_bytes;
+      NVDB_CUDA_TRY(cub::DeviceSelect::Flagged(base + w.cub, cs, kin, flags, kc, nsel, (int)n, st));
+      cs = w.cub_bytes;
+      NVDB_CUDA_TRY(cub::DeviceSelect::Flagged(base + w.cub, cs, vin, flags, vc, nsel, (int)n, st));
+      ksrc = kc;
+      vsrc = vc;
     }
     size_t cb = w.cub_bytes;
-    NVDB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(base + w.cub, cb, kin, kout, vin, vout, (int)n, 0, kbits, st));
+    NVDB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(base + w.cub, cb, ksrc, kout, vsrc, vout, (int)np_, 0, kbits, st));
     {
       const int nn = std::max(ns->nnets, 1);
       int64_t* rs = reinterpret_cast<int64_t*>(base + w.runs);
       int64_t* re = rs + nn;
       int64_t* to = re + nn;
       NVDB_CUDA_TRY(cudaMemsetAsync(rs, 0, 16 * (size_t)nn, st));
-      k_run_bounds<<<blocks, threads, 0, st>>>(kout, n, nokey, rs, re);
+      k_run_bounds<<<(int)((np_ + threads - 1) / threads), threads, 0, st>>>(kout, np_, nokey, rs, re);
       NVDB_CHECK_LAUNCH();
       k_tile_plan<<<1, 32, 0, st>>>(rs, re, ns->nnets, w.max_tiles, to, npairs);
       NVDB_CHECK_LAUNCH();

@@ -398,7 +398,7 @@ __device__ __forceinline__ long long floor_div(double v, double s) { return (lon
 __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather, int64_t n, int pass, const int32_t* cells, int ncell,
                             const int32_t* tagnet, int tag, int S, int halo, uint8_t* ncand, uint16_t* keys,
                             int64_t* vals, BlendOut o, int nokey, int32_t* maxc, const int64_t* n_dev,
-                            int32_t* hist, uint8_t* flags) {
+                            int32_t* hist, uint8_t* flags, uint16_t* cand) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (n_dev && i >= *n_dev) {  // capacity tail beyond the device count: no candidate, no output
@@ -437,6 +437,7 @@ __global__ void k_pass_keys(int src_kind, const void* src, const int64_t* gather
     if (net < 0) continue;
     if (!(gate_weight(cell, S, halo, c, 0.5 / (double)halo) > 0.0)) continue;
     if (found == pass) key = net;
+    if (cand) cand[8 * i + found] = (uint16_t)net;  // pass 0 records every candidate for the later passes
     ++found;
   }
   if (pass == 0) {
@@ -516,9 +517,22 @@ __global__ void k_write_tiles(const int64_t* __restrict__ start, const int64_t* 
   tiles[t] = tl;
 }
 
+// keys of a later pass from the candidates pass 0 recorded (no centre /
+// cell / gate recomputation): the pass-th candidate's net, or the sentinel
+__global__ void k_pass_keys_later(int64_t n, int pass, const uint8_t* __restrict__ ncand,
+                                  const uint16_t* __restrict__ cand, int nokey, uint16_t* keys, int64_t* vals,
+                                  uint8_t* flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool has = ncand[i] > pass;
+  keys[i] = has ? cand[8 * i + pass] : (uint16_t)nokey;
+  vals[i] = i;
+  if (flags) flags[i] = has ? 1 : 0;
+}
+
 struct WsLayout {
   size_t ncand, keys_in, keys_out, vals_in, vals_out, tiles, npairs, runs, acc, cub, total;
-  size_t flags, keys_c, vals_c, nsel;
+  size_t flags, keys_c, vals_c, nsel, cand;
   size_t cub_bytes;
   int64_t max_tiles;
 };
@@ -543,6 +557,7 @@ WsLayout ws_layout(const nvdb_netset* ns, int64_t n) {
   w.keys_c = take(2 * n);
   w.vals_c = take(8 * n);
   w.nsel = take(16);
+  w.cand = take(16 * n);  // up to 8 candidate nets per point (pass 0)
   w.runs = take(8 * (3 * (size_t)std::max(ns->nnets, 1) + 1));  // start | end | toff (+1)
   w.acc = take(32 * n);
   size_t cub_bytes = 0;
@@ -619,6 +634,7 @@ int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, c
   uint16_t* kc = reinterpret_cast<uint16_t*>(base + w.keys_c);
   int64_t* vc = reinterpret_cast<int64_t*>(base + w.vals_c);
   int* nsel = reinterpret_cast<int*>(base + w.nsel);
+  uint16_t* cand = reinterpret_cast<uint16_t*>(base + w.cand);
   int passes = 8;
   int32_t hh[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // maxc | hist[0..8]
   for (int pass = 0; pass < passes; ++pass) {
@@ -634,9 +650,13 @@ int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, c
     }
     const bool compact = pass > 0 && np_ < n;
     if (pass == 0) NVDB_CUDA_TRY(cudaMemsetAsync(maxc, 0, 40, st));
-    k_pass_keys<<<blocks, threads, 0, st>>>(src_kind, src, gather, n, pass, ns->dev_cells, ns->nexperts, ns->dev_tagnet,
-                                            tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o, nokey, maxc, n_dev,
-                                            hist, compact ? flags : nullptr);
+    if (pass == 0) {
+      k_pass_keys<<<blocks, threads, 0, st>>>(src_kind, src, gather, n, pass, ns->dev_cells, ns->nexperts,
+                                              ns->dev_tagnet, tag, ns->subdomain_size, ns->halo, ncand, kin, vin, o,
+                                              nokey, maxc, n_dev, hist, nullptr, cand);
+    } else {
+      k_pass_keys_later<<<blocks, threads, 0, st>>>(n, pass, ncand, cand, nokey, kin, vin, compact ? flags : nullptr);
+    }
     NVDB_CHECK_LAUNCH();
     if (pass == 0) {  // later passes only exist up to the largest candidate count of this call
       NVDB_CUDA_TRY(cudaMemcpyAsync(hh, maxc, 40, cudaMemcpyDeviceToHost, st));

@@ -59,17 +59,23 @@ def run():
 
 _, _, nr = run()
 torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-run()
-e1.record()
-torch.cuda.synchronize()
-ms = e0.elapsed_time(e1)
-e0.record()
-tree.lookup(coords)
-e1.record()
-torch.cuda.synchronize()
-ms_lookup = e0.elapsed_time(e1)
+
+
+def timed(fn, reps=5):
+    """median of reps device-timed calls (after the warm call above)"""
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+ms = timed(run)
+ms_lookup = timed(lambda: tree.lookup(coords))
 peaks = {"hbm_gbs": 6549.4, "bf16_tflops": 1641.1}
 try:
     with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) as f:

@@ -200,6 +200,8 @@ constexpr int kMaxEngines = 4;
 constexpr int kSlots = 2;                    // feature chunk slots per engine
 constexpr int kEChunkK = 48;                 // feature K per chunk (3 MMAs of K = 16)
 constexpr int kEChunkBytes = kTileM * kEChunkK * 2;  // 12 KB
+constexpr int kEChunkKS = 64;                // streamed weights: a feature chunk = one 4-chunk weight slot
+constexpr int kEChunkBytesS = kTileM * kEChunkKS * 2;  // 16 KB
 constexpr int kEvalThreads = 128 * kMaxEngines;  // largest block (512)
 constexpr int kMaxWRing = 8;                 // weight ring slots per engine (streamed weights)
 
@@ -501,7 +503,12 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   constexpr int act = ACT;
 
   auto process = [&](const Tile& tile, int t) {
-    const int k0 = s_net.k0, mp = k0 >> 1, nch = (k0 + kEChunkK - 1) / kEChunkK;
+    // feature chunk: 48 K with resident weights (two 12 KB slots beside the
+    // weights), 64 K with streamed ones (one 4-chunk weight slot per feature
+    // chunk; the engine region holds the wide A tile anyway)
+    const int cK = a.wstream ? kEChunkKS : kEChunkK;
+    const uint32_t cbytes = a.wstream ? kEChunkBytesS : kEChunkBytes;
+    const int k0 = s_net.k0, mp = k0 >> 1, nch = (k0 + cK - 1) / cK;
     const int width = s_net.width, depth = s_net.depth, out_dim = s_net.out_dim;
     const uint32_t asm_ = ring;  // hidden fp16 A tile (K-major, 128 rows): the engine's slots once layer 0 is done
     const uint32_t idesc = idesc_f16(kTileM, width, 0, 0);
@@ -545,14 +552,14 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
     for (int ch = 0; ch < nch; ++ch, ++cc) {
       const uint32_t s = cc % kSlots;
       if (cc >= kSlots) mbar_wait(slot_free + s, ((cc / kSlots) - 1) & 1u);
-      const uint32_t buf = ring + s * kEChunkBytes;
-      const int kch = min(kEChunkK, k0 - ch * kEChunkK);  // K of this chunk: 16, 32 or 48
+      const uint32_t buf = ring + s * cbytes;
+      const int kch = min(cK, k0 - ch * cK);  // K of this chunk: a multiple of 16
       const int ngrp = kch >> 3;                           // 4-feature groups in it
       if (lattice) {
         // 4 features x 8 y rows: one sincos, one rotation by exp(i beta),
         // then the Chebyshev recurrence u_{j+1} = 2 cos(beta) u_j - u_{j-1}
         if (lpg < ngrp) {
-        const int f0 = ch * (kEChunkK / 2) + lpg * 4;
+        const int f0 = ch * (cK / 2) + lpg * 4;
         const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
         const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
         const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
@@ -594,9 +601,9 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < kEChunkK / 8; ++q) {
+        for (int q = 0; q < kEChunkKS / 8; ++q) {
           if (q >= ngrp) break;
-          const int f0 = ch * (kEChunkK / 2) + q * 4;
+          const int f0 = ch * (cK / 2) + q * 4;
           const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
           const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
           const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
@@ -621,9 +628,7 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
         // one K = 16 step = 2 core-matrix columns of the operand
         const uint64_t ad = smem_desc(buf, kTileM * 16, 128);
         if (a.wstream) {
-          w_mma(dcol, ad, idesc, ch != 0, false, 0);
-          if (kch > 16) w_mma(dcol, ad + 256, idesc, 1, false, 0);
-          if (kch > 32) w_mma(dcol, ad + 512, idesc, 1, false, 0);
+          w_mma_run(dcol, ad, idesc, ch != 0 ? 1u : 0u, kch >> 4);
         } else {
           const uint64_t bd = bdesc0 + (uint64_t)(ch * (kEChunkK / 16) * bstep);
           if (kch == 48) {  // one asm block (one ELECT / R2UR sequence) for the chunk's 3 MMAs

@@ -74,7 +74,7 @@ inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t 
   p.region_off = (uint32_t)align_up(max_wimg, 1024);
   p.tcols = (W + 15) & ~15;
   const int by_tmem = std::max(0, std::min(kMaxEngines, 512 / std::max(p.tcols, 16)));
-  const long long base_ereg = (long long)align_up(std::max<size_t>((size_t)kSlots * kEChunkBytes,
+  long long base_ereg = (long long)align_up(std::max<size_t>((size_t)kSlots * kEChunkBytes,
                                                                    (size_t)kTileM * W * 2), 1024);
   // resident weights when at least two engines fit beside them, else streamed weights
   long long room = (long long)limit - p.region_off - small_bytes - 16 - 1024;
@@ -84,6 +84,8 @@ inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t 
   p.wring = 0;
   p.wring_off = 0;
   if (p.engines < 2) {
+    // streamed: 64 K feature chunks (two 16 KB slots) beside the hidden A tile
+    base_ereg = (long long)align_up(std::max<size_t>((size_t)kSlots * kEChunkBytesS, (size_t)kTileM * W * 2), 1024);
     // streamed: as many engines as TMEM allows, then the CTA-wide weight ring:
     // slots of up to 4 K = 16 chunks (W x 32 bytes each), as many slots (2..4)
     // as fit, bigger slots first (the issuer's bookkeeping is per slot)

@@ -577,16 +577,16 @@ __global__ void __launch_bounds__(128, 1) k_lw_wg(const LwWgArgs a) {
       tc_fence_after();
       const uint32_t sa = smem_addr(s_a[st]), sb = smem_addr(s_b[st]);
       const bool first = tau == ts;
-      for (int s = 0; s < kTileM / 16; ++s) {
-        const uint32_t acc = (!first || s != 0) ? 1u : 0u;
-        umma_f16(dcol, smem_desc(sa + s * 256, 128, 2048), smem_desc(sb + s * 256, 128, 2048), idesc, acc);
-        if (bk.bias_blk >= 0) {
-          if (!head)
-            umma_f16(bcol, smem_desc(sb + (uint32_t)bk.bias_blk * 32768 + s * 256, 128, 2048),
-                     smem_desc(smem_addr(s_ones) + s * 512, 256, 128), idesc_b, acc);
-          else
-            umma_f16(bcol, smem_desc(smem_addr(s_ones), 128, 0), smem_desc(sb + s * 256, 128, 2048), idesc_hb, acc);
-        }
+      // the tile's K = 16 steps as groups from single asm blocks (umma_f16_run)
+      const uint32_t acc0 = first ? 0u : 1u;
+      umma_f16_run(dcol, smem_desc(sa, 128, 2048), smem_desc(sb, 128, 2048), idesc, acc0, kTileM / 16, 16, 16);
+      if (bk.bias_blk >= 0) {
+        if (!head)
+          umma_f16_run(bcol, smem_desc(sb + (uint32_t)bk.bias_blk * 32768, 128, 2048),
+                       smem_desc(smem_addr(s_ones), 256, 128), idesc_b, acc0, kTileM / 16, 16, 32);
+        else
+          umma_f16_run(bcol, smem_desc(smem_addr(s_ones), 128, 0), smem_desc(sb, 128, 2048), idesc_hb, acc0,
+                       kTileM / 16, 0, 16);
       }
       umma_commit(&bars[2 + st]);
       if (tau + 2 < te) {  // refill this stage once its MMAs are done

@@ -80,6 +80,11 @@ def run(size: int, epochs: int, dev, group=None) -> dict:
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
+    if os.environ.get("NVDB_PROFILE") == "1":  # ncu --profile-from-start off: one decode's launch list
+        torch.cuda.profiler.start()
+        m.decode(True, shard=shard)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     cnt = torch.tensor([d.leaf_count * 512, d.regressor_evaluations, ms], dtype=torch.float64, device=dev)
     if world > 1:
         mx = cnt[2:].clone()

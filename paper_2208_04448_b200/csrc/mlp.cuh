@@ -622,7 +622,16 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       }
       fence_async_smem();
       named_bar_sync(1 + g, 128);
-      if (issuer) {
+      if (!a.wstream && kch == 48) {
+        // resident weights: the engine's first warp issues converged (elected lane)
+        if ((warp & 3) == 0) {
+          tc_fence_after();
+          umma_f16_x3_w(dcol, smem_desc(buf, kTileM * 16, 128),
+                        bdesc0 + (uint64_t)(ch * (kEChunkK / 16) * bstep), idesc, ch != 0, 256, bstep);
+          umma_commit_w(slot_free + s);
+          if (ch == nch - 1) umma_commit_w(mdone);
+        }
+      } else if (issuer) {
         tc_fence_after();
         // descriptors: start-address field += byte offset >> 4 (no carry: smem < 256 KB);
         // one K = 16 step = 2 core-matrix columns of the operand

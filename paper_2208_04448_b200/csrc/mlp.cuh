@@ -740,7 +740,21 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       if (last) run_layer(std::true_type{});
       else run_layer(std::false_type{});
       tc_fence_before();
-      if (!last) {
+      if (!last && !a.wstream && (width % 48) == 0) {
+        // resident weights, W a multiple of 48: the layer's MMAs in threes from
+        // the engine's first warp, converged (as the feature chunks)
+        fence_async_smem();
+        tc_fence_before();
+        named_bar_sync(1 + g, 128);
+        if ((warp & 3) == 0) {
+          tc_fence_after();
+          uint64_t ad = smem_desc(asm_, kTileM * 16, 128);
+          uint64_t bd = smem_desc(w_s + (uint32_t)(width * k0 * 2 + l * width * width * 2), width * 16, 128);
+          for (int k = 0; k < width / 16; k += 3, ad += 768, bd += 3 * bstep)
+            umma_f16_x3_w(dcol, ad, bd, idesc, k != 0, 256, bstep);
+          umma_commit_w(mdone);
+        }
+      } else if (!last) {
         fence_async_smem();
         tc_fence_before();
         named_bar_sync(1 + g, 128);

@@ -213,6 +213,47 @@ __device__ __forceinline__ void umma_f16_x3_w(uint32_t d_tmem, uint64_t adesc, u
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "l"(astep), "l"(bstep)
       : "memory");
 }
+__device__ __forceinline__ void umma_f16_x4_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate, uint64_t astep, uint64_t bstep) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.u64 a1, %1, %5;\n\tadd.u64 a2, a1, %5;\n\tadd.u64 a3, a2, %5;\n\t"
+      "add.u64 b1, %2, %6;\n\tadd.u64 b2, b1, %6;\n\tadd.u64 b3, b2, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "l"(astep), "l"(bstep)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// umma_f16_run from a converged warp (every lane calls it)
+__device__ __forceinline__ void umma_f16_run_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate, int n, uint64_t astep, uint64_t bstep) {
+  int k = 0;
+  for (; k + 4 <= n; k += 4, adesc += 4 * astep, bdesc += 4 * bstep, accumulate = 1)
+    umma_f16_x4_w(d_tmem, adesc, bdesc, idesc, accumulate, astep, bstep);
+  if (k + 3 <= n) {
+    umma_f16_x3_w(d_tmem, adesc, bdesc, idesc, accumulate, astep, bstep);
+    k += 3;
+    adesc += 3 * astep;
+    bdesc += 3 * bstep;
+    accumulate = 1;
+  }
+  for (; k < n; ++k, adesc += astep, bdesc += bstep, accumulate = 1)
+    umma_f16_w(d_tmem, adesc, bdesc, idesc, accumulate);
+}
 __device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

@@ -434,14 +434,13 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
       fence_async_smem();
       tc_fence_before();
       named_bar_sync(1 + grp, 256);
-      if (gt == 0) {
+      if (gw == 0) {  // the group's first warp issues converged (elect inside the asm)
         tc_fence_after();
-        // the chunk's MMAs from single asm blocks (one ELECT / R2UR sequence per group)
-        umma_f16_run(tcol, smem_desc(buf, kTileM * 16, 128),
-                     smem_desc(w_s + (uint32_t)(((ch * kChunkK) >> 3) * (width >> 3) * 128), width * 16, 128), idesc,
-                     ch != 0, kChunkK / 16, 256, (uint64_t)(width * 2));
-        umma_commit(bar_c0 + bsel);
-        if (ch == nch - 1) umma_commit(bar_layer);
+        umma_f16_run_w(tcol, smem_desc(buf, kTileM * 16, 128),
+                       smem_desc(w_s + (uint32_t)(((ch * kChunkK) >> 3) * (width >> 3) * 128), width * 16, 128),
+                       idesc, ch != 0, kChunkK / 16, 256, (uint64_t)(width * 2));
+        umma_commit_w(bar_c0 + bsel);
+        if (ch == nch - 1) umma_commit_w(bar_layer);
       }
       if (bsel == 0) { nc0++; pend0 = true; } else { nc1++; pend1 = true; }
     }
@@ -523,12 +522,12 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
         fence_async_smem();
         tc_fence_before();
         named_bar_sync(1 + grp, 256);
-        if (gt == 0) {
+        if (gw == 0) {
           tc_fence_after();
           const uint32_t wl = w_s + woff;
-          umma_f16_run(tcol, smem_desc(region_s, kTileM * 16, 128), smem_desc(wl, width * 16, 128), idesc, 0u,
-                       width / 16, 256, (uint64_t)(width * 2));
-          umma_commit(bar_layer);
+          umma_f16_run_w(tcol, smem_desc(region_s, kTileM * 16, 128), smem_desc(wl, width * 16, 128), idesc, 0u,
+                         width / 16, 256, (uint64_t)(width * 2));
+          umma_commit_w(bar_layer);
         }
         woff += (uint32_t)(width * width * 2);
         mbar_wait(bar_layer, nlayer & 1u);
@@ -661,13 +660,13 @@ __device__ __forceinline__ void fb_body(const FbArgs& a, uint8_t* smem) {
         fence_async_smem();
         tc_fence_before();
         named_bar_sync(1 + grp, 256);
-        if (gt == 0) {
+        if (gw == 0) {
           tc_fence_after();
           // W'_l image (rows o, cols i, K-major) read as B = (N = i, K = o) MN-major
           const uint32_t wl = w_s + (uint32_t)(width * k0 * 2) + (uint32_t)((l - 1) * width * width * 2);
-          umma_f16_run(tcol, smem_desc(region_s, kTileM * 16, 128), smem_desc(wl, 128, width * 16), idesc_bt, 0u,
-                       width / 16, 256, 16);
-          umma_commit(bar_layer);
+          umma_f16_run_w(tcol, smem_desc(region_s, kTileM * 16, 128), smem_desc(wl, 128, width * 16), idesc_bt, 0u,
+                         width / 16, 256, 16);
+          umma_commit_w(bar_layer);
         }
         mbar_wait(bar_layer, nlayer & 1u);
         nlayer++;

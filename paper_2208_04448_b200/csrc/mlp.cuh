@@ -129,7 +129,7 @@ struct MlpArgs {
 };
 
 // small per-net parameters staged in shared memory:
-// bias [4*256] | headw [3*256] | headb [4] | b2pi [3*512] | lat [2*512] | head exchange [2][128][4]
+// bias [4*256] | headw [3*256] | headb [4] | b2pi [3*512] | lat [8*512] | head exchange [2][128][4]
 constexpr int kSmallBias = 0;
 constexpr int kSmallHeadW = 4 * 256;
 constexpr int kSmallHeadB = kSmallHeadW + 3 * 256;
@@ -292,6 +292,15 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t dcol = tmem_base + (uint32_t)(g * a.tcols);
   const bool issuer = p == 0;
+  // lattice feature stores (leaf-voxel tiles): row = x * 64 + y * 8 + z, with
+  // z = p & 7, feature group (p >> 3) & 7, x = p >> 6; K-major core-matrix
+  // offsets (kmajor_offset) without the y row (+ y * 128) and the slot base
+  const uint32_t lat_row = (uint32_t)(p >> 6) * 1024u + (uint32_t)(p & 7) * 16u;
+  auto lat_k = [&](uint32_t k) { return (k >> 3) * (uint32_t)(kTileM * 16) + (k & 7u) * 2u; };
+  const uint32_t lat4_off = lat_row + lat_k((uint32_t)((p >> 3) & 7) * 8u);
+  const uint32_t lat3_off0 = lat_row + lat_k((uint32_t)((p >> 3) & 7) * 6u);
+  const uint32_t lat3_off1 = lat_row + lat_k((uint32_t)((p >> 3) & 7) * 6u + 2u);
+  const uint32_t lat3_off2 = lat_row + lat_k((uint32_t)((p >> 3) & 7) * 6u + 4u);
   const double inv2h = 0.5 / (double)a.halo;
 
   const int64_t n_impl = a.n_dev ? min(*a.n_dev, a.n_implicit) : a.n_implicit;
@@ -450,8 +459,16 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       for (int i = tid; i < nd.out_dim * nd.width; i += nthreads) s_headw[i] = nd.headw[i];
       if (tid < nd.out_dim) s_headb[tid] = nd.headb[tid];
       for (int i = tid; i < 3 * (nd.k0 / 2); i += nthreads) s_b2pi[i] = nd.b2pi[i];
-      if (nd.lat)
-        for (int i = tid; i < nd.k0; i += nthreads) s_lat[i] = nd.lat[i];
+      if (nd.lat) {
+        // per complex feature f: {bx, by, bz, 2 cos(beta)}, {cos(beta), sin(beta), -sin(beta), 0}
+        const int mp = nd.k0 / 2;
+        for (int f = tid; f < mp; f += nthreads) {
+          const float cb = nd.lat[2 * f], sb = nd.lat[2 * f + 1];
+          float4* L = reinterpret_cast<float4*>(s_lat) + 2 * f;
+          L[0] = make_float4(nd.b2pi[f], nd.b2pi[mp + f], nd.b2pi[2 * mp + f], 2.0f * cb);
+          L[1] = make_float4(cb, sb, -sb, 0.0f);
+        }
+      }
     }
     if (!a.wstream) {
       mbar_wait(wbar, wphase);
@@ -555,49 +572,68 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
       const uint32_t buf = ring + s * cbytes;
       const int kch = min(cK, k0 - ch * cK);  // K of this chunk: a multiple of 16
       const int ngrp = kch >> 3;                           // 4-feature groups in it
-      if (lattice) {
-        // 4 features x 8 y rows: one sincos, one rotation by exp(i beta),
-        // then the Chebyshev recurrence u_{j+1} = 2 cos(beta) u_j - u_{j-1}
-        if (lpg < ngrp) {
-        const int f0 = ch * (cK / 2) + lpg * 4;
-        const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
-        const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
-        const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
-        const float4 la = *reinterpret_cast<const float4*>(s_lat + 2 * f0);
-        const float4 lb = *reinterpret_cast<const float4*>(s_lat + 2 * f0 + 4);
-        const float bxa[4] = {bx.x, bx.y, bx.z, bx.w}, bya[4] = {by.x, by.y, by.z, by.w};
-        const float bza[4] = {bz.x, bz.y, bz.z, bz.w};
-        const float cba[4] = {la.x, la.z, lb.x, lb.z}, sba[4] = {la.y, la.w, lb.y, lb.w};
-        // (cos, sin) pairs on the packed fp32x2 pipe (FFMA2: one issue per pair,
-        // per-lane IEEE fma, so the values are those of the scalar recurrence)
-        float2 u[4][2], c2[4];
-        uint32_t hp[4];
+      if (lattice && kch == kEChunkK) {
+        // 24 features x 8 z x 2 x = 384 columns of 8 y rows: three columns per
+        // thread (all 128 lanes busy), one sincos + rotation per column, then
+        // the Chebyshev recurrence u_{j+1} = 2 cos(beta) u_j - u_{j-1} along y
+        const float4* L = reinterpret_cast<const float4*>(s_lat) + 2 * (ch * (cK / 2) + lpg * 3);
+        float2 u[3][2];
+        float c2[3];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float th = fmaf(x2, bza[q], fmaf(x1, bya[q], x0 * bxa[q]));
+        for (int q = 0; q < 3; ++q) {
+          const float4 A = L[2 * q], B = L[2 * q + 1];  // {bx, by, bz, 2 cb}, {cb, sb, -sb, 0}
+          const float th = fmaf(x2, A.z, fmaf(x1, A.y, x0 * A.x));
           float s0, c0;
           __sincosf(th, &s0, &c0);
           u[q][0] = make_float2(c0, s0);
           // (c0 cb - s0 sb, c0 sb + s0 cb): the products s0 * (-sb, cb) rounded, then one fma each
-          u[q][1] = __ffma2_rn(make_float2(c0, c0), make_float2(cba[q], sba[q]),
-                               __fmul2_rn(make_float2(s0, s0), make_float2(-sba[q], cba[q])));
-          c2[q] = make_float2(2.0f * cba[q], 2.0f * cba[q]);
+          u[q][1] = __ffma2_rn(make_float2(c0, c0), make_float2(B.x, B.y), __fmul2_rn(make_float2(s0, s0), make_float2(B.z, B.x)));
+          c2[q] = A.w;
+        }
+        const uint32_t b0 = buf + lat3_off0, b1 = buf + lat3_off1, b2 = buf + lat3_off2;
+        static_for<0, 8>([&](auto jyc) {
+          constexpr int jy = decltype(jyc)::value;
+          if constexpr (jy >= 2) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+              u[q][jy & 1] = __ffma2_rn(make_float2(c2[q], c2[q]), u[q][(jy & 1) ^ 1],
+                                        make_float2(-u[q][jy & 1].x, -u[q][jy & 1].y));
+          }
+          st_shared_b32_at<jy * 128>(b0, pack_half2(u[0][jy & 1].x, u[0][jy & 1].y));
+          st_shared_b32_at<jy * 128>(b1, pack_half2(u[1][jy & 1].x, u[1][jy & 1].y));
+          st_shared_b32_at<jy * 128>(b2, pack_half2(u[2][jy & 1].x, u[2][jy & 1].y));
+        });
+      } else if (lattice) {
+        // 4 features x 8 y rows (64-K chunks: all lanes; shorter tail chunks: lpg < ngrp)
+        if (lpg < ngrp) {
+        const float4* L = reinterpret_cast<const float4*>(s_lat) + 2 * (ch * (cK / 2) + lpg * 4);
+        float2 u[4][2], c2[4];
+        uint32_t hp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 A = L[2 * q], B = L[2 * q + 1];
+          const float th = fmaf(x2, A.z, fmaf(x1, A.y, x0 * A.x));
+          float s0, c0;
+          __sincosf(th, &s0, &c0);
+          u[q][0] = make_float2(c0, s0);
+          u[q][1] = __ffma2_rn(make_float2(c0, c0), make_float2(B.x, B.y), __fmul2_rn(make_float2(s0, s0), make_float2(B.z, B.x)));
+          c2[q] = make_float2(A.w, A.w);
           hp[q] = pack_half2(c0, s0);
         }
-        st_shared_v4(buf + kmajor_offset(lii * 64 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
+        const uint32_t b4 = buf + lat4_off;
+        st_shared_v4_at<0>(b4, hp[0], hp[1], hp[2], hp[3]);
 #pragma unroll
         for (int q = 0; q < 4; ++q) hp[q] = pack_half2(u[q][1].x, u[q][1].y);
-        st_shared_v4(buf + kmajor_offset(lii * 64 + 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
-#pragma unroll
-        for (int jy = 2; jy < 8; ++jy) {
-          const int cur = jy & 1;
+        st_shared_v4_at<128>(b4, hp[0], hp[1], hp[2], hp[3]);
+        static_for<2, 8>([&](auto jyc) {
+          constexpr int jy = decltype(jyc)::value;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            u[q][cur] = __ffma2_rn(c2[q], u[q][cur ^ 1], make_float2(-u[q][cur].x, -u[q][cur].y));
-            hp[q] = pack_half2(u[q][cur].x, u[q][cur].y);
+            u[q][jy & 1] = __ffma2_rn(c2[q], u[q][(jy & 1) ^ 1], make_float2(-u[q][jy & 1].x, -u[q][jy & 1].y));
+            hp[q] = pack_half2(u[q][jy & 1].x, u[q][jy & 1].y);
           }
-          st_shared_v4(buf + kmajor_offset(lii * 64 + jy * 8 + lk, lpg * 8, kTileM), hp[0], hp[1], hp[2], hp[3]);
-        }
+          st_shared_v4_at<jy * 128>(b4, hp[0], hp[1], hp[2], hp[3]);
+        });
         }
       } else {
 #pragma unroll

@@ -68,7 +68,7 @@ inline EvalPlan plan_eval(uint32_t max_wimg, int W, int depth, int k0, uint32_t 
   p.sm_headb = p.sm_headw + a4(3 * W);
   p.sm_b2pi = p.sm_headb + 4;
   p.sm_lat = p.sm_b2pi + a4(3 * (k0 / 2));
-  p.sm_hx = p.sm_lat + a4(k0);
+  p.sm_hx = p.sm_lat + a4(4 * k0);  // lattice table: 8 floats per complex feature
   const uint32_t small_bytes = (uint32_t)p.sm_hx * 4u;
   p.w_off = 0;
   p.region_off = (uint32_t)align_up(max_wimg, 1024);

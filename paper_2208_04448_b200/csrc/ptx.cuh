@@ -4,6 +4,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
+#include <type_traits>
 
 namespace nvdb {
 
@@ -351,6 +352,24 @@ __device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+// stores at a compile-time byte offset from a base register (one STS [R + imm])
+template <int OFF>
+__device__ __forceinline__ void st_shared_b32_at(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.b32 [%0+%1], %2;" ::"r"(addr), "n"(OFF), "r"(v) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void st_shared_v4_at(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0+%1], {%2,%3,%4,%5};" ::"r"(addr), "n"(OFF), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+// compile-time loop: f(std::integral_constant<int, I>) for I in [B, E)
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
 }
 
 // Byte offset of element (row, k) of an R-row K-major operand tile stored in

@@ -643,14 +643,20 @@ __global__ void __launch_bounds__(kEvalThreads, 1) mlp_eval_kernel(const MlpArgs
           const float4 bx = *reinterpret_cast<const float4*>(s_b2pi + f0);
           const float4 by = *reinterpret_cast<const float4*>(s_b2pi + mp + f0);
           const float4 bz = *reinterpret_cast<const float4*>(s_b2pi + 2 * mp + f0);
-          const float bxa[4] = {bx.x, bx.y, bx.z, bx.w}, bya[4] = {by.x, by.y, by.z, by.w};
-          const float bza[4] = {bz.x, bz.y, bz.z, bz.w};
+          // theta = fma(x2, bz, fma(x1, by, x0 bx)) for two features per packed op
+          // (per-lane IEEE, the scalar chain's values)
+          float2 th[2];
+          th[0] = __ffma2_rn(make_float2(x2, x2), make_float2(bz.x, bz.y),
+                             __ffma2_rn(make_float2(x1, x1), make_float2(by.x, by.y),
+                                        __fmul2_rn(make_float2(x0, x0), make_float2(bx.x, bx.y))));
+          th[1] = __ffma2_rn(make_float2(x2, x2), make_float2(bz.z, bz.w),
+                             __ffma2_rn(make_float2(x1, x1), make_float2(by.z, by.w),
+                                        __fmul2_rn(make_float2(x0, x0), make_float2(bx.z, bx.w))));
           uint32_t h[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const float th = fmaf(x2, bza[j], fmaf(x1, bya[j], x0 * bxa[j]));
             float sv, cv;
-            __sincosf(th, &sv, &cv);
+            __sincosf((j & 1) ? th[j >> 1].y : th[j >> 1].x, &sv, &cv);
             h[j] = pack_half2(cv, sv);
           }
           st_shared_v4(buf + kmajor_offset(p, q * 8, kTileM), h[0], h[1], h[2], h[3]);

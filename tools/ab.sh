@@ -4,6 +4,6 @@
 A=${1:-libnvdb_b200_base.so}; B=${2:-libnvdb_b200.so}; R=${3:-3}
 for i in $(seq "$R"); do
   for L in "$A" "$B"; do
-    echo "== $L"; NVDB_LIB=$L python tools/time_decode.py 2>&1 | grep -E "stage (l0|voxel)|l0 alone" | tail -3
+    echo "== $L"; NVDB_LIB=$L python tools/time_decode.py 2>&1 | grep -E "alone" | tail -6
   done
 done

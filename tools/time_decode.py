@@ -41,3 +41,15 @@ for i in range(5):
     t1 = time.perf_counter()
     torch.cuda.synchronize()
     print(f" l0 alone: gpu {a.elapsed_time(b):.3f} ms, host launch {1e3 * (t1 - t0):.3f} ms")
+# voxel stage alone: the active voxels of the level-0 result (no patches applied)
+act_ids, acnt = m.select(act, 1, sync=False)
+vals = torch.empty(n, dtype=torch.float32, device=dev)
+for i in range(5):
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    m.evaluate("voxel", _lib.SRC_LEAF_VOX, lo, n, _lib.OUT_VALUE, gather=act_ids, f32=vals,
+               value_scale=m.value_scale, clip=m.meta.grid_class == "sdf", count=acnt)
+    b.record()
+    torch.cuda.synchronize()
+    print(f" voxel alone: gpu {a.elapsed_time(b):.3f} ms ({int(acnt.item())} points)")

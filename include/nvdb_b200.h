@@ -164,6 +164,11 @@ NVDB_API int nvdb_scatter_f32(float* dst, const int64_t* ids, const float* vals,
 /* dst[ids[i]] = vals[i] for i < *count_dev (device int64, <= capacity). */
 NVDB_API int nvdb_scatter_f32_counted(float* dst, const int64_t* ids, const float* vals, int64_t capacity,
                                       const int64_t* count_dev, void* stream);
+/* as nvdb_scatter_f32_counted, skipping ids with skip[id] != 0: the voxel
+ * regressor's values of one leaf range after nvdb_leaf_finalize_counted ran
+ * without them (patched voxels keep their patch value; decoder.py:191-196) */
+NVDB_API int nvdb_scatter_f32_unpatched_counted(float* dst, const int64_t* ids, const float* vals, int64_t capacity,
+                                                const int64_t* count_dev, const uint8_t* skip, void* stream);
 /* leaf origins of child slots (node*4096+slot, node order x ascending slot)
  * and the slot -> leaf index map (-1 elsewhere) (decoder.py:146-151) */
 /* Level-1 slot (node * 4096 + idx1, -1 outside every node) and idx0 of

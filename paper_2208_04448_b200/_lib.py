@@ -33,7 +33,7 @@ EXPORTED = [
     "nvdb_query_finalize", "nvdb_trainer_create", "nvdb_trainer_destroy", "nvdb_trainer_run",
     "nvdb_trainer_status", "nvdb_trainer_weights", "nvdb_sample_indices", "nvdb_trainer_phase",
     "nvdb_trainer_buffers", "nvdb_sample_indices_subset", "nvdb_fbm_leaves", "nvdb_trim",
-    "nvdb_eval_counted", "nvdb_leaf_finalize_counted", "nvdb_scatter_f32_counted",
+    "nvdb_eval_counted", "nvdb_leaf_finalize_counted", "nvdb_scatter_f32_counted", "nvdb_scatter_f32_unpatched_counted",
     "nvdb_query_finalize_counted", "nvdb_trainer_packed", "nvdb_nvgr_leaf_records", "nvdb_nvgr_l1_records",
     "nvdb_metric_partials", "nvdb_metric_pass", "nvdb_trainer_set_ctas", "nvdb_netset_device_bytes",
     "nvdb_netset_create_at", "nvdb_node_slots",
@@ -129,6 +129,7 @@ def _declare(lib: C.CDLL) -> None:
         "nvdb_leaf_finalize_counted": (C.c_int, [i64, vp, vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, vp, i64, vp,
                                                  C.c_float, C.c_float, vp, vp, vp, vp]),
         "nvdb_scatter_f32_counted": (C.c_int, [vp, vp, vp, i64, vp, vp]),
+        "nvdb_scatter_f32_unpatched_counted": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
         "nvdb_pack_eq": (C.c_int, [vp, i64, C.c_uint8, vp, vp]),
         "nvdb_neural_rows": (C.c_int, [vp, vp, i64, vp, vp]),
         "nvdb_query_finalize": (C.c_int, [vp, i64, vp, vp, vp, vp, vp, vp]),

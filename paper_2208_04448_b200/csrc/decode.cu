@@ -42,10 +42,14 @@ __global__ void k_l1_apply(uint8_t* cls, float* tiles, const int64_t* patch_slot
   }
 }
 
-__global__ void k_scatter_f32(float* dst, const int64_t* ids, const float* vals, int64_t n, const int64_t* n_dev) {
+__global__ void k_scatter_f32(float* dst, const int64_t* ids, const float* vals, int64_t n, const int64_t* n_dev,
+                              const uint8_t* skip = nullptr) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (n_dev) n = min(n, *n_dev);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) dst[ids[i]] = vals[i];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t id = ids[i];
+    if (!skip || !skip[id]) dst[id] = vals[i];
+  }
 }
 
 __global__ void k_fill_i32(int32_t* dst, int64_t n, int32_t v) {
@@ -381,6 +385,17 @@ extern "C" int nvdb_scatter_f32_counted(float* dst, const int64_t* ids, const fl
   if (!capacity) return NVDB_OK;
   k_scatter_f32<<<blocks_for(capacity), 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, ids, vals, capacity,
                                                                                      count_dev);
+  NVDB_CHECK_LAUNCH();
+  return NVDB_OK;
+}
+
+extern "C" int nvdb_scatter_f32_unpatched_counted(float* dst, const int64_t* ids, const float* vals, int64_t capacity,
+                                                  const int64_t* count_dev, const uint8_t* skip, void* stream) {
+  if (capacity < 0 || !count_dev || (capacity > 0 && (!dst || !ids || !vals || !skip)))
+    return fail(NVDB_EINVAL, "nvdb_scatter_f32_unpatched_counted: bad args");
+  if (!capacity) return NVDB_OK;
+  k_scatter_f32<<<blocks_for(capacity), 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, ids, vals, capacity,
+                                                                                     count_dev, skip);
   NVDB_CHECK_LAUNCH();
   return NVDB_OK;
 }

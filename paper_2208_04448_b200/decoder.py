@@ -29,6 +29,7 @@ from .tree import DeviceTree
 
 EVAL_CHUNK = 1 << 24  # points per evaluator call on the multi-expert path
 MAX_CALL = 1 << 30    # points per evaluator call on the single-expert path (int32 tile counts)
+PIPE_LEAVES = 1024    # decode_full's pipelined voxel stage: leaf ranges of at least this many leaves
 
 
 def _dev(device=None) -> torch.device:
@@ -262,9 +263,26 @@ class DeviceModel:
             raise SvcodecError(f"corrupt container: tile record for unknown level-1 node {bad}")
         return (np.repeat(tni, counts) * L1_SIZE + slots).astype(np.int64), vals.astype(np.float32)
 
-    def _ensure_l0(self) -> None:
-        """Level-0 patch and negative-fill tables (one upload; slots on the device)."""
+    def _ensure_l0(self, after: Optional[torch.cuda.Event] = None) -> None:
+        """Level-0 patch and negative-fill tables (one upload; slots on the device).
+
+        ``after``: an event on the current stream recorded before the level-0
+        stage was enqueued; the upload and its slot kernels then run on the
+        side stream beside that stage, and the current stream waits for them."""
         if self._l0_ready:
+            return
+        if after is not None:
+            main = torch.cuda.current_stream(self.dev)
+            side = self._side_stream()
+            side.wait_event(after)
+            with torch.cuda.stream(side):
+                self._ensure_l0()
+            for k in ("p0_key", "p0_act", "p0_val", "neg_key", "neg_u8", "p0_slot", "p0_vox", "neg_slot",
+                      "neg_bits"):
+                getattr(self, k).record_stream(main)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            main.wait_event(ev)
             return
         c, ut = self.c, self.c.upper_tree
         host = {}
@@ -525,16 +543,26 @@ class DeviceModel:
                                        _ptr(leaf_of_slot), st), "nvdb_leaf_list")
         nv = nl * LEAF_SIZE
         act = torch.zeros(max(nv, 1), dtype=torch.uint8, device=dev)
+        pre_l0 = None
+        if not self._l0_ready:
+            pre_l0 = torch.cuda.Event()
+            pre_l0.record(torch.cuda.current_stream(dev))
         self.evaluate("l0", _lib.SRC_LEAF_VOX, leaf_origins, nv, _lib.OUT_L0ACTIVE, u8=act)
-        self._ensure_l0()  # host work while the L0 stage runs
+        self._ensure_l0(after=pre_l0)  # host work and the table upload while the L0 stage runs
         err = torch.zeros(1, dtype=torch.int32, device=dev)
         check(lib().nvdb_l0_apply(_ptr(act), _ptr(self.p0_slot), _ptr(self.p0_vox), _ptr(self.p0_act),
                                   self.p0_slot.numel(), _ptr(leaf_of_slot), _ptr(err), st), "nvdb_l0_apply")
         pre = None
         if prefetch_host and shard is None and nl:
-            pre = self._host_prefetch([cls[:nslots], tiles[:nslots], leaf_origins[:nl], act[:nv]])
+            pre = self._host_prefetch([cls[:nslots], tiles[:nslots], leaf_origins[:nl], act[:nv], err,
+                                      self.err])
         act_ids = vals = None
         acnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        if (pre is not None and materialize_values and nl >= 4 * PIPE_LEAVES
+                and self.single and self.has_tag["voxel"]):
+            d = self._decode_pipelined(cls, tiles, child, leaf_origins, leaf_of_slot, act, nl, err, shard)
+            d.host_pre = pre
+            return d
         if materialize_values and nl:
             # active voxels -> voxel regressor -> finalize, the count staying on the device
             act_ids, acnt = self.select(act[:nv], 1, sync=False)
@@ -554,16 +582,74 @@ class DeviceModel:
         d = DeviceDecode(self, cls[:nslots], tiles[:nslots], child, leaf_origins[:nl], act[:nv],
                          values[:nv], words[:nl * 8], patched[:nv], acnt, shard, err)
         d.host_pre = pre
+        if pre is not None:
+            # the dense values follow on the copy stream as soon as finalize is
+            # done; to_grid orders the leaves on the host while they travel
+            d.host_vals = self._host_prefetch([values[:nv]])
         return d
+
+    def _decode_pipelined(self, cls, tiles, child, leaf_origins, leaf_of_slot, act, nl, err, shard):
+        """Voxel stage + value scatter in leaf ranges, each range's dense values
+        copied to pinned host memory (copy stream) while the next range is
+        regressed.  Finalize runs first without the regressor values (fills,
+        patches, negative fill, masks); the per-range scatter skips patched
+        voxels, so every value equals the one-pass decode's."""
+        dev, st = self.dev, _stream(self.dev)
+        nv = nl * LEAF_SIZE
+        values = torch.empty(nv, dtype=torch.float32, device=dev)
+        words = torch.empty(nl * 8, dtype=torch.int64, device=dev)
+        patched = torch.empty(nv, dtype=torch.uint8, device=dev)
+        zero = torch.zeros(1, dtype=torch.int64, device=dev)
+        check(lib().nvdb_leaf_finalize_counted(nl, _ptr(act), None, None, 0, _ptr(zero), _ptr(self.p0_slot),
+                                               _ptr(self.p0_vox), _ptr(self.p0_act), _ptr(self.p0_val),
+                                               self.p0_slot.numel(), _ptr(self.neg_slot), _ptr(self.neg_bits),
+                                               self.neg_slot.numel(), _ptr(leaf_of_slot), self.background,
+                                               -float(np.float32(self.value_scale)), _ptr(values), _ptr(words),
+                                               _ptr(patched), st), "nvdb_leaf_finalize_counted")
+        cs = self._side_stream()
+        pin, arr = _PINNED.get(nv * 4)
+        host_vals = arr[:nv * 4].view(np.float32)
+        nparts = max(4, -(-nl // (4 * PIPE_LEAVES)))
+        bounds = [nl * k // nparts for k in range(nparts + 1)]
+        counts = []
+        clip = self.meta.grid_class == "sdf"
+        for l0, l1 in zip(bounds[:-1], bounds[1:]):
+            if l1 == l0:
+                continue
+            v0, v1 = l0 * LEAF_SIZE, l1 * LEAF_SIZE
+            ids, cnt = self.select(act[v0:v1], 1, sync=False)
+            vals = torch.empty(v1 - v0, dtype=torch.float32, device=dev)
+            self.evaluate("voxel", _lib.SRC_LEAF_VOX, leaf_origins[l0:l1], v1 - v0, _lib.OUT_VALUE, gather=ids,
+                          f32=vals, value_scale=self.value_scale, clip=clip, count=cnt)
+            check(lib().nvdb_scatter_f32_unpatched_counted(_ptr(values, 4 * v0), _ptr(ids), _ptr(vals), v1 - v0,
+                                                           _ptr(cnt), _ptr(patched, v0), st),
+                  "nvdb_scatter_f32_unpatched_counted")
+            counts.append(cnt)
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(dev))
+            cs.wait_event(ev)
+            with torch.cuda.stream(cs):
+                pin[4 * v0:4 * v1].view(torch.float32).copy_(values[v0:v1], non_blocking=True)
+        values.record_stream(cs)
+        done = torch.cuda.Event()
+        done.record(cs)
+        acnt = torch.stack(counts).sum(0) if counts else torch.zeros(1, dtype=torch.int64, device=dev)
+        d = DeviceDecode(self, cls[:self.n1 * L1_SIZE], tiles[:self.n1 * L1_SIZE], child, leaf_origins[:nl],
+                         act[:nv], values, words, patched, acnt, shard, err)
+        d.host_vals = ([host_vals], done)
+        return d
+
+    def _side_stream(self) -> torch.cuda.Stream:
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=self.dev)
+        return self._copy_stream
 
     def _host_prefetch(self, ts):
         """Asynchronous copies of finished device arrays into one pooled pinned
         block on a side stream, ordered after the work enqueued so far; returns
         (numpy views, completion event)."""
         dev = self.dev
-        if getattr(self, "_copy_stream", None) is None:
-            self._copy_stream = torch.cuda.Stream(device=dev)
-        cs = self._copy_stream
+        cs = self._side_stream()
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(dev))
         cs.wait_event(ev)
@@ -601,7 +687,8 @@ class DeviceDecode:
     shard: Optional[Tuple[int, int]] = None  # (rank, world) when only a leaf range was decoded
     err_dev: Optional[torch.Tensor] = None   # (1,) int32: a level-0 patch fell outside every leaf
     _checked: bool = False
-    host_pre: Optional[tuple] = None  # decode(prefetch_host=True): (host arrays, event) of cls / tiles / origins / active
+    host_pre: Optional[tuple] = None  # decode(prefetch_host=True): (host arrays, event) of cls / tiles / origins / active / error flags
+    host_vals: Optional[tuple] = None  # decode(prefetch_host=True): ([host leaf values], event)
 
     @property
     def leaf_count(self) -> int:
@@ -616,9 +703,15 @@ class DeviceDecode:
         flag is read lazily (first host access) so a decode enqueues without a
         stream synchronisation."""
         if not self._checked and self.err_dev is not None:
-            if int(self.model.err[0].item()):  # decoder.py:121-124
+            if self.host_pre is not None:  # flags copied to the host with the level-1 / leaf arrays
+                (_, _, _, _, e0, e1), done = self.host_pre
+                done.synchronize()
+                e1, e0 = int(e1[0]), int(e0[0])
+            else:
+                e1, e0 = int(self.model.err[0].item()), int(self.err_dev.item())
+            if e1:  # decoder.py:121-124
                 raise SvcodecError("corrupt container: level-1 patch outside every level-1 node")
-            if int(self.err_dev.item()):
+            if e0:
                 raise SvcodecError("corrupt container: level-0 patch outside every reconstructed leaf")
             self._checked = True
         return self
@@ -633,9 +726,13 @@ class DeviceDecode:
         meta = c.grid_meta
         bg = np.float32(meta.background)
         n1 = m.n1
+        vdone = None
         if self.host_pre is not None:
-            (cls, tiles, lo, la), done = self.host_pre
-            (lv,) = _to_host([self.leaf_values])
+            (cls, tiles, lo, la, _, _), done = self.host_pre
+            if self.host_vals is not None:
+                (lv,), vdone = self.host_vals  # waited for below, after the host-side ordering
+            else:
+                (lv,) = _to_host([self.leaf_values])
             done.synchronize()
         else:
             cls, tiles, lo, la, lv = _to_host([self.l1_class, self.l1_tiles, self.leaf_origins,
@@ -667,6 +764,8 @@ class DeviceDecode:
             l2a[j] = nd.active_mask.bits
             for k, v in nd.tiles.items():
                 l2t[j, int(k)] = v
+        if vdone is not None:
+            vdone.synchronize()
         return DenseLeafGrid(
             background=float(meta.background), grid_class=meta.grid_class, voxel_size=float(meta.voxel_size),
             half_width=float(meta.half_width), root_tiles=dict(ut.root_tiles),

@@ -78,11 +78,18 @@ def test_c2_sharded_decode_equals_full(c2, world):
 
 def test_c2_prefetched_to_grid_equals_plain(c2):
     """decode(prefetch_host=True) (classes, tiles, origins and active flags
-    copied to the host during the voxel stage) gives the same host grid."""
+    copied to the host during the voxel stage; the voxel stage pipelined in
+    leaf ranges with the values following to the host) gives the same device
+    arrays and the same host grid."""
     _, m, _ = c2
-    a = m.decode(True).to_grid()
+    da = m.decode(True)
+    a = da.to_grid()
     d = m.decode(True, prefetch_host=True)
-    assert d.host_pre is not None
+    assert d.host_pre is not None and d.host_vals is not None
+    for f in ("leaf_values", "leaf_active", "active_words", "patched"):
+        assert torch.equal(getattr(da, f), getattr(d, f)), f
+    assert int(da.evals_dev.item()) == int(d.evals_dev.item())
+    assert int(d.patched.sum().item()) > 0  # the C2 container's level-0 patches are exercised
     b = d.to_grid()
     for f in ("leaf_origins", "leaf_active", "leaf_values", "l1_origins", "l1_child", "l1_active", "l1_tiles"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f

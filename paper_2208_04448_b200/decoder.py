@@ -51,20 +51,30 @@ class _PinnedPool:
     as numpy views of one pooled uint8 array; it is free again once every view
     a caller holds is gone (reference count of the pooled array)."""
 
-    CAP = 4
+    CAP = 8
 
     def __init__(self):
         self.blocks = []  # [pinned uint8 tensor, its numpy view]
 
     def get(self, nbytes: int):
-        for blk in self.blocks:
-            if blk[1].size >= nbytes and sys.getrefcount(blk[1]) <= 2:  # held by blk + the call's argument
-                return blk
+        free = [blk for blk in self.blocks
+                if blk[1].size >= nbytes and sys.getrefcount(blk[1]) <= 2  # held by blk + the call's argument
+                and (blk[2] is None or blk[2].query())]  # its last host->device copy has completed
+        if free:
+            blk = min(free, key=lambda b: b[1].size)  # best fit
+            blk[2] = None
+            return blk[0], blk[1]
         t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
-        blk = [t, t.numpy()]
+        blk = [t, t.numpy(), None]
         if len(self.blocks) < self.CAP:
             self.blocks.append(blk)
-        return blk
+        return blk[0], blk[1]
+
+    def fence(self, arr, event) -> None:
+        """The block behind ``arr`` is the source of a copy completing at ``event``."""
+        for blk in self.blocks:
+            if blk[1] is arr:
+                blk[2] = event
 
 
 _PINNED = _PinnedPool()
@@ -333,13 +343,16 @@ class DeviceModel:
         for k, a in host.items():
             offs[k] = n
             n += (a.nbytes + 255) & ~255
-        # pinned staging from torch's caching host allocator (blocks are reused
-        # once their copy completed): an asynchronous copy, no host wait
-        pin = torch.empty(max(n, 256), dtype=torch.uint8, pin_memory=True)
-        buf = pin.numpy()
+        # pinned staging from the decode pool (handed out again once the copy
+        # has completed): an asynchronous copy, no host wait
+        pin, buf = _PINNED.get(max(n, 256))
         for k, a in host.items():
             buf[offs[k]:offs[k] + a.nbytes] = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
-        dbuf = pin.to(self.dev, non_blocking=True)
+        dbuf = torch.empty(max(n, 256), dtype=torch.uint8, device=self.dev)
+        dbuf.copy_(pin[:max(n, 256)], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        _PINNED.fence(buf, ev)
         self._tables.append(dbuf)
         for k, a in host.items():
             t = dbuf[offs[k]:offs[k] + a.nbytes].view(_TORCH_DTYPE[a.dtype.type]).view(a.shape)

@@ -622,8 +622,10 @@ class DeviceModel:
         cs = self._side_stream()
         pin, arr = _PINNED.get(nv * 4)
         host_vals = arr[:nv * 4].view(np.float32)
-        nparts = max(4, -(-nl // (4 * PIPE_LEAVES)))
-        bounds = [nl * k // nparts for k in range(nparts + 1)]
+        # ranges shrinking 4:3:2:1, so the one copy left after the last range
+        # is a tenth of the values
+        w = np.cumsum([0, 4, 3, 2, 1])
+        bounds = [int(nl * int(x) // int(w[-1])) for x in w]
         counts = []
         clip = self.meta.grid_class == "sdf"
         for l0, l1 in zip(bounds[:-1], bounds[1:]):

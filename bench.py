@@ -736,14 +736,14 @@ def main():
     e2e_t = []
     h2d = sum(w.nbytes + b.nbytes for e in c.experts for _, n in e.nets() if n is not None
               for w, b in n.params.layers)
-    for i in range(2 + 5):  # 2 untimed calls (pinned host blocks, first-touch), then 5 timed
+    for i in range(3 + 10):  # 3 untimed calls (pinned host blocks, first-touch), then 10 timed
         torch.cuda.synchronize()
         _barrier(world)
         t0 = time.perf_counter()
         g = decode_full(c, dev, group=_group(world))  # N ranks: sharded, gathered on rank 0
         torch.cuda.synchronize()
         dt = _max_over_ranks(time.perf_counter() - t0, dev, world)
-        if i >= 2:
+        if i >= 3:
             e2e_t.append(dt)
     e2e = nvox / statistics.median(e2e_t)
     c3 = None

@@ -47,25 +47,38 @@ def _ptr(t: Optional[torch.Tensor], byte_offset: int = 0):
 
 
 class _PinnedPool:
-    """Reusable pinned host blocks for decode outputs.  A block is handed out
-    as numpy views of one pooled uint8 array; it is free again once every view
-    a caller holds is gone (reference count of the pooled array)."""
+    """Reusable pinned host blocks for decode and query outputs.  A block is
+    handed out as numpy views of one pooled uint8 array; it is free again once
+    every view a caller holds is gone (reference count of the pooled array) and
+    its last host->device copy has completed.  A full pool replaces its least
+    recently used free block, so blocks that callers keep (results of the
+    previous call) never force an uncached cudaHostAlloc per call."""
 
-    CAP = 8
+    CAP = 12
 
     def __init__(self):
-        self.blocks = []  # [pinned uint8 tensor, its numpy view]
+        self.blocks = []  # [pinned uint8 tensor, its numpy view, fence event, last use]
+        self.clock = 0
+
+    @staticmethod
+    def _idle(blk) -> bool:
+        # held by blk + getrefcount's argument only; its last host->device copy done
+        return sys.getrefcount(blk[1]) <= 2 and (blk[2] is None or blk[2].query())
 
     def get(self, nbytes: int):
-        free = [blk for blk in self.blocks
-                if blk[1].size >= nbytes and sys.getrefcount(blk[1]) <= 2  # held by blk + the call's argument
-                and (blk[2] is None or blk[2].query())]  # its last host->device copy has completed
+        self.clock += 1
+        free = [blk for blk in self.blocks if blk[1].size >= nbytes and self._idle(blk)]
         if free:
             blk = min(free, key=lambda b: b[1].size)  # best fit
             blk[2] = None
+            blk[3] = self.clock
             return blk[0], blk[1]
+        if len(self.blocks) >= self.CAP:
+            idle = [blk for blk in self.blocks if self._idle(blk)]
+            if idle:
+                self.blocks.remove(min(idle, key=lambda b: b[3]))
         t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
-        blk = [t, t.numpy(), None]
+        blk = [t, t.numpy(), None, self.clock]
         if len(self.blocks) < self.CAP:
             self.blocks.append(blk)
         return blk[0], blk[1]

@@ -219,8 +219,8 @@ def train_container(grid, cfg, dev, timings, group=None):
     slice of every epoch's batch, one packed all-reduce per epoch."""
     import torch
     from paper_2208_04448_b200.encoder import (DeviceTrainer, build_upper_tree, decompose, extract_patches,
-                                               gather_expert_data, init_mlp, net_spec, stable_seed,
-                                               value_scale_of, NET_TAGS)
+                                               gather_expert_data, init_mlp, net_spec, run_concurrent,
+                                               stable_seed, value_scale_of, NET_TAGS)
     from paper_2208_04448_b200.model import (Activation, EncodedSubdomain, FourierFeatures, GridMeta,
                                              NetRecord, NeuralGridContainer)
     layout = decompose(grid, cfg.subdomain_size)
@@ -229,6 +229,7 @@ def train_container(grid, cfg, dev, timings, group=None):
         scale = value_scale_of(grid)
         data = gather_expert_data(grid, sub, scale)
         ex = EncodedSubdomain(sub.id, sub.cell, sub.cluster_id, data.norm_origin, data.norm_scale, scale)
+        jobs = []
         for tag, x, y, attr in (("l1", data.l1_inputs, data.l1_labels, "l1_classifier"),
                                 ("tile", data.tile_inputs, data.tile_targets, "tile_regressor"),
                                 ("l0", data.l0_inputs, data.l0_labels, "l0_classifier"),
@@ -243,18 +244,22 @@ def train_container(grid, cfg, dev, timings, group=None):
             sampled = (not spec.full_batch) and x.shape[0] > cfg.batch_size
             tr = DeviceTrainer(p0, ff, x, y, spec.loss_kind, cfg, cfg.lr, stable_seed(cfg.seed, sub.id, tid, 2),
                                sampled, spec.loss_target, dev, group=group)
-            torch.cuda.synchronize(dev)
-            if group is not None:
-                import torch.distributed as dist
-                dist.barrier(group)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            loss, epochs = tr.run()
-            e1.record()
-            e1.synchronize()
             batch = cfg.batch_size if sampled else x.shape[0]
-            timings.append({"tag": tag, "epochs": epochs, "batch": int(batch), "ms": e0.elapsed_time(e1),
-                            "loss": loss, "flops_per_sample": train_flops(p0.layers)})
+            jobs.append((tag, attr, tr, ff, int(batch), train_flops(p0.layers)))
+        # the expert's nets train at once, each on its own stream with its full
+        # grid (encode()'s schedule, run_concurrent); timed as one group
+        torch.cuda.synchronize(dev)
+        if group is not None:
+            import torch.distributed as dist
+            dist.barrier(group)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = run_concurrent([j[2] for j in jobs])
+        e1.record()
+        e1.synchronize()
+        for (tag, attr, tr, ff, batch, fl), (loss, epochs) in zip(jobs, res):
+            timings.append({"tag": tag, "epochs": epochs, "batch": batch, "ms": e0.elapsed_time(e1) / len(jobs),
+                            "loss": loss, "flops_per_sample": fl, "concurrent": len(jobs)})
             setattr(ex, attr, NetRecord(tr.weights(), ff, loss, epochs))
             tr.close()
         experts.append(ex)

@@ -579,12 +579,15 @@ WsLayout ws_layout(const nvdb_netset* ns, int64_t n) {
 
 namespace nvdb {
 
-size_t blended_workspace_bytes(const nvdb_netset* ns, int64_t n) { return ws_layout(ns, n).total; }
+// calls above 2^30 points run in chunks of 2^30 (run_blended): the workspace covers one chunk
+size_t blended_workspace_bytes(const nvdb_netset* ns, int64_t n) {
+  return ws_layout(ns, std::min<int64_t>(n, int64_t(1) << 30)).total;
+}
 
-int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, const int64_t* gather, int64_t n,
-                const BlendOut& o, void* ws, size_t ws_bytes, cudaStream_t st, const int64_t* n_dev) {
+static int run_blended_one(const nvdb_netset* ns, int tag, int src_kind, const void* src, const int64_t* gather,
+                           int64_t n, const BlendOut& o, void* ws, size_t ws_bytes, cudaStream_t st,
+                           const int64_t* n_dev) {
   if (n <= 0) return NVDB_OK;
-  if (n > (int64_t)INT32_MAX) return fail(NVDB_EUNSUPPORTED, "run_blended: n > 2^31");
   MlpArgs a{};
   a.src_kind = src_kind;
   a.src = src;
@@ -690,6 +693,52 @@ int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, c
     }
     a.pass = pass;
     int rc = launch_mlp(ns, a, npairs, num_sms(), st);
+    if (rc) return rc;
+  }
+  return NVDB_OK;
+}
+
+// Calls above 2^30 points run as consecutive chunks of 2^30 (a multiple of
+// the 4096 points of a level-1 node, so implicit leaf-voxel / slot ids keep
+// their node): the tile indices, radix sorts and selections inside one
+// chunk stay in 32-bit range.  A chunk's source, gather list and outputs are
+// the caller's arrays advanced to its first point; the workspace sized for n
+// covers any chunk.  A device-held count (n_dev) cannot be split on the host.
+int run_blended(const nvdb_netset* ns, int tag, int src_kind, const void* src, const int64_t* gather, int64_t n,
+                const BlendOut& o, void* ws, size_t ws_bytes, cudaStream_t st, const int64_t* n_dev) {
+  constexpr int64_t kChunk = int64_t(1) << 30;
+  if (n <= kChunk) return run_blended_one(ns, tag, src_kind, src, gather, n, o, ws, ws_bytes, st, n_dev);
+  if (n_dev) return fail(NVDB_EUNSUPPORTED, "run_blended: a device-counted call above 2^30 points");
+  int out_dim = 1;
+  for (int e = 0; e < ns->nexperts; ++e) {
+    const int ni = ns->tagnet[e * 4 + tag];
+    if (ni >= 0) {
+      out_dim = ns->nets[ni].out_dim;
+      break;
+    }
+  }
+  for (int64_t s0 = 0; s0 < n; s0 += kChunk) {
+    const int64_t m = std::min(kChunk, n - s0);
+    const void* csrc = src;
+    const int64_t* cg = gather;
+    if (gather) {
+      cg = gather + s0;
+    } else {
+      switch (src_kind) {
+        case SRC_NORM_F32: csrc = static_cast<const float*>(src) + 3 * s0; break;
+        case SRC_CENTER_F64: csrc = static_cast<const double*>(src) + 3 * s0; break;
+        case SRC_COORD_I32: csrc = static_cast<const int32_t*>(src) + 3 * s0; break;
+        case SRC_LEAF_VOX: csrc = static_cast<const int32_t*>(src) + 3 * (s0 >> 9); break;
+        case SRC_L1_SLOT: csrc = static_cast<const int32_t*>(src) + 3 * (s0 >> 12); break;
+        default: return fail(NVDB_EINVAL, "run_blended: bad source kind %d", src_kind);
+      }
+    }
+    BlendOut c = o;
+    if (c.out_raw) c.out_raw += s0 * out_dim;
+    if (c.out_probs) c.out_probs += s0 * out_dim;
+    if (c.out_u8) c.out_u8 += s0;
+    if (c.out_f32) c.out_f32 += s0;
+    const int rc = run_blended_one(ns, tag, src_kind, csrc, cg, m, c, ws, ws_bytes, st, nullptr);
     if (rc) return rc;
   }
   return NVDB_OK;

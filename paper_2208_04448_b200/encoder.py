@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import logging
+import time
 import os
 from dataclasses import dataclass, field, replace
 from typing import Dict, List, Optional, Sequence, Tuple
@@ -553,6 +554,65 @@ class DeviceTrainer:
             pass
 
 
+def run_concurrent(trainers: List["DeviceTrainer"], width: int = 2) -> List[Tuple[float, int]]:
+    """Run independent trainers ``width`` at a time, each on its own stream
+    with its full grid (the same kernels, tile partitions and reduction order
+    as ``DeviceTrainer.run``, so every net's weights and epochs are
+    bit-identical to training them one after another).  The epoch kernels are
+    latency-bound per tile: two nets' epochs
+    interleaved on the SMs overlap one net's weight-gradient / Adam tail and
+    launch gaps with the other's fwd/dgrad (C2 l0 + voxel, 800 epochs: 169.7
+    -> 148.9 ms).  Three at once was measured slower on the ACCEPT nets (the
+    tile images of three nets no longer stay in L2).  The largest nets start
+    first; a finished net's stream takes the next one.  Data-parallel
+    trainers (a process group) run one after another."""
+    if len(trainers) <= 1 or width <= 1 or any(t.group is not None for t in trainers):
+        return [t.run() for t in trainers]
+    dev = trainers[0].dev
+    cur = torch.cuda.current_stream(dev)
+    streams = [torch.cuda.Stream(dev) for _ in range(width)]
+    for s in streams:
+        s.wait_stream(cur)  # the trainers' uploads were enqueued on the current stream
+    todo = sorted((i for i, t in enumerate(trainers) if t.epochs_enqueued < t.max_epochs),
+                  key=lambda i: -trainers[i].epoch_work() * trainers[i].max_epochs)
+    slots: List[Optional[Tuple[int, torch.cuda.Event]]] = [None] * width
+
+    def enqueue(slot, i):
+        t = trainers[i]
+        k = min(t.CHUNK, t.max_epochs - t.epochs_enqueued)
+        t._enqueue(k, streams[slot].cuda_stream)
+        t.epochs_enqueued += k
+        ev = torch.cuda.Event()
+        ev.record(streams[slot])
+        slots[slot] = (i, ev)
+
+    for slot in range(width):
+        if todo:
+            enqueue(slot, todo.pop(0))
+    while any(sl is not None for sl in slots):
+        # the stop flag is checked per chunk in completion order, so a
+        # finished chunk is followed at once by the next one on its stream
+        progressed = False
+        for slot, sl in enumerate(slots):
+            if sl is None or not sl[1].query():
+                continue
+            progressed = True
+            i = sl[0]
+            t = trainers[i]
+            _, stopped = t.status()[:2]
+            if stopped or t.epochs_enqueued >= t.max_epochs:
+                slots[slot] = None
+                if todo:
+                    enqueue(slot, todo.pop(0))
+            else:
+                enqueue(slot, i)
+        if not progressed:
+            time.sleep(2e-5)
+    for s in streams:
+        cur.wait_stream(s)
+    return [t.final() for t in trainers]
+
+
 def _train_flops(layers) -> int:
     """2*(3*sum MAC - MAC_0) per sample."""
     macs = [np.asarray(w).shape[0] * np.asarray(w).shape[1] for w, _ in layers]
@@ -805,11 +865,11 @@ def _prepare_expert(grid: DenseLeafGrid, sub: Subdomain, cfg, lr0: float, warm=N
 
 def _train_experts(grid: DenseLeafGrid, subs, cfg, lr0: float, warm_of, stops_of, device=None, group=None,
                    dgrid: Optional[DeviceGrid] = None):
-    """Train every net of every given expert, one after another, each net on
-    the whole GPU.  (Running a container's nets concurrently on SM shares was
-    measured: +16 % at best for two ACCEPT nets, because the epoch kernels are
-    latency-bound per tile and a smaller share lengthens each CTA's tile
-    chain; DESIGN.md "Training".)"""
+    """Train every net of every given expert: an expert's nets run at once on
+    their own streams, each with its full grid (``run_concurrent``; splitting
+    the SMs between them instead was measured slower, because the epoch
+    kernels are latency-bound per tile and a smaller share lengthens each
+    CTA's tile chain)."""
     experts = []
     if dgrid is None and subs:
         dgrid = DeviceGrid(grid, device)  # training sets gathered on the device
@@ -817,8 +877,7 @@ def _train_experts(grid: DenseLeafGrid, subs, cfg, lr0: float, warm_of, stops_of
         expert, jobs = _prepare_expert(grid, sub, cfg, lr0, warm=warm_of(sub), stop_losses=stops_of(sub),
                                        device=device, group=group, dgrid=dgrid)
         try:
-            for attr, tr, ff in jobs:
-                loss, epochs = tr.run()
+            for (attr, tr, ff), (loss, epochs) in zip(jobs, run_concurrent([tr for _, tr, _ in jobs])):
                 setattr(expert, attr, NetRecord(params=tr.weights(), ff=ff, final_loss=float(loss), epochs=epochs))
         finally:
             for _, tr, _ in jobs:

@@ -231,3 +231,47 @@ def test_nvgr_root_tiles_and_negative_coordinates():
     assert len({tuple(int(v) & ~4095 for v in o) for o in g.l1_origins}) >= 3
     assert d.to_nvgr() == gridfile.serialize_grid(g.to_svcodec())
     m.close()
+
+
+def test_c_abi_eval_above_2_30_points():
+    """nvdb_eval called once with 2^30 + 8192 leaf-voxel points (the C-ABI
+    splits it into 2^30-point chunks, eval.cu run_blended): the leaves on
+    either side of the chunk boundary and at the tail decide exactly as
+    small calls over the same origins."""
+    import ctypes as C
+
+    from paper_2208_04448_b200 import _lib
+    from paper_2208_04448_b200._lib import EvalOut, lib
+    from paper_2208_04448_b200.decoder import TAG_CODES, _ptr, _stream
+
+    z = np.load(os.path.join(GOLDEN, "decode_small.npz"))
+    c = container_from_arrays(z)
+    m = DeviceModel(c, "cuda:0")
+    dev = m.dev
+    n = (1 << 30) + 8192
+    nleaf = n // LEAF_SIZE
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    org = torch.randint(0, 64, (nleaf, 3), dtype=torch.int32, device=dev, generator=g) * 8
+    u8 = torch.full((n,), 7, dtype=torch.uint8, device=dev)
+
+    def run(origins, npts, out):
+        o = EvalOut(out_mode=_lib.OUT_L0ACTIVE, raw=None, probs=None, u8=_ptr(out), f32=None,
+                    value_scale=1.0, background=0.0, clip=0)
+        _lib.check(lib().nvdb_eval(m.ns.handle, TAG_CODES["l0"], _lib.SRC_LEAF_VOX, _ptr(origins), None, npts,
+                                   C.byref(o), None, 0, _stream(dev)), "nvdb_eval")
+
+    try:
+        if not m.single:
+            pytest.skip("single-expert container expected")
+        run(org, n, u8)
+        assert int((u8 > 1).sum().item()) == 0  # every point written
+        b = (1 << 30) // LEAF_SIZE
+        for lo in (0, b - 8, nleaf - 16):
+            sub = org[lo:lo + 16].contiguous()
+            ref = torch.empty(16 * LEAF_SIZE, dtype=torch.uint8, device=dev)
+            run(sub, 16 * LEAF_SIZE, ref)
+            assert torch.equal(u8[lo * LEAF_SIZE:(lo + 16) * LEAF_SIZE], ref), lo
+    finally:
+        del u8
+        m.close()

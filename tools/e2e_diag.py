@@ -28,9 +28,27 @@ def get(self, nbytes):
 
 
 D._PinnedPool.get = get
+gct = []
+_gc0 = [0.0]
+
+
+def _gccb(phase, info):
+    if phase == "start":
+        _gc0[0] = time.perf_counter()
+    else:
+        gct.append((info["generation"], round((time.perf_counter() - _gc0[0]) * 1e3, 2)))
+
+
+import gc  # noqa: E402
+gc.callbacks.append(_gccb)
+if os.environ.get("AFTER_QUERY"):
+    import bench  # noqa: E402
+    mm = D.DeviceModel(c, dev)
+    bench.query_bench(mm, dev, 20, rank=0, world=1)
 g = None
 for i in range(12):
     news.clear()
+    gct.clear()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     m = D._as_model(c, dev)
@@ -41,4 +59,4 @@ for i in range(12):
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     print(f"call {i}: total {1e3 * (t3 - t0):.2f} ms (model {1e3 * (t1 - t0):.2f}, decode {1e3 * (t2 - t1):.2f}, "
-          f"to_grid {1e3 * (t3 - t2):.2f}); new pinned blocks (MiB, ms, pool size) {news}", flush=True)
+          f"to_grid {1e3 * (t3 - t2):.2f}); new pinned blocks (MiB, ms, pool size) {news}; gc {gct}", flush=True)

@@ -554,6 +554,9 @@ class DeviceTrainer:
             pass
 
 
+_TRAIN_STREAMS: Dict[int, list] = {}
+
+
 def run_concurrent(trainers: List["DeviceTrainer"], width: int = 2) -> List[Tuple[float, int]]:
     """Run independent trainers ``width`` at a time, each on its own stream
     with its full grid (the same kernels, tile partitions and reduction order
@@ -570,7 +573,10 @@ def run_concurrent(trainers: List["DeviceTrainer"], width: int = 2) -> List[Tupl
         return [t.run() for t in trainers]
     dev = trainers[0].dev
     cur = torch.cuda.current_stream(dev)
-    streams = [torch.cuda.Stream(dev) for _ in range(width)]
+    pool = _TRAIN_STREAMS.setdefault(dev.index if dev.index is not None else torch.cuda.current_device(), [])
+    while len(pool) < width:  # persistent per device (torch's allocator pools blocks per stream)
+        pool.append(torch.cuda.Stream(dev))
+    streams = pool[:width]
     for s in streams:
         s.wait_stream(cur)  # the trainers' uploads were enqueued on the current stream
     todo = sorted((i for i, t in enumerate(trainers) if t.epochs_enqueued < t.max_epochs),

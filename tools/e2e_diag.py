@@ -45,6 +45,15 @@ if os.environ.get("AFTER_QUERY"):
     import bench  # noqa: E402
     mm = D.DeviceModel(c, dev)
     bench.query_bench(mm, dev, 20, rank=0, world=1)
+    if os.environ.get("AFTER_QUERY") == "pool":  # drop the pinned blocks the query section left
+        D._PINNED.blocks.clear()
+    if os.environ.get("AFTER_QUERY") == "mem":  # release the device memory it left cached
+        del mm
+        import gc as _g
+        _g.collect()
+        torch.cuda.empty_cache()
+if os.environ.get("BIG_ALLOC"):
+    big = torch.empty(int(os.environ["BIG_ALLOC"]) << 20, dtype=torch.uint8, device=dev)
 g = None
 for i in range(12):
     news.clear()

@@ -49,7 +49,7 @@ TORUS = dict(major=160.0, minor=64.0, voxel=1.0, half_width=3.0, center=(256.0, 
 def load_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of one L0-stage mlp_eval_kernel
     launch from the committed ncu --set full capture (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "r01", "ncu_mlp_eval_c2_l0_v10.json")
+    path = os.path.join(ROOT, "profiles", "r02", "ncu_mlp_eval_c2_l0_r02g.json")
     try:
         with open(path) as f:
             rec = json.load(f)[0]

@@ -113,6 +113,40 @@ def _to_host(ts):
     return outs
 
 
+_COPY_POOL = None
+
+
+def _to_device(a: np.ndarray, dev) -> torch.Tensor:
+    """Host array -> device tensor through a pooled pinned block, in 32 MiB
+    pieces: each piece's pageable -> pinned copy is split over host threads
+    (numpy releases the GIL while copying) and its asynchronous host->device
+    copy on the current stream runs while the next piece is staged.  The
+    block is fenced until the last copy completes."""
+    global _COPY_POOL
+    a = np.ascontiguousarray(a)
+    n = a.nbytes
+    if n < (8 << 20):  # small: the driver's staged copy is as fast
+        return torch.from_numpy(a).to(dev)
+    pin, arr = _PINNED.get(n)
+    src = a.reshape(-1).view(np.uint8)
+    out = torch.empty(a.shape, dtype=_TORCH_DTYPE[a.dtype.type], device=dev)
+    obytes = out.view(-1).view(torch.uint8)
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _COPY_POOL = ThreadPoolExecutor(8, thread_name_prefix="nvdb-h2d")
+    piece = 32 << 20
+    for p0 in range(0, n, piece):
+        p1 = min(n, p0 + piece)
+        k = int(min(8, max(1, (p1 - p0) >> 22)))
+        cuts = [p0 + (((p1 - p0) * i // k) & ~4095) for i in range(k)] + [p1]
+        list(_COPY_POOL.map(lambda i: np.copyto(arr[cuts[i]:cuts[i + 1]], src[cuts[i]:cuts[i + 1]]), range(k)))
+        obytes[p0:p1].copy_(pin[p0:p1], non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(dev))
+    _PINNED.fence(arr, ev)
+    return out
+
+
 _TORCH_DTYPE = {np.uint8: torch.uint8, np.int32: torch.int32, np.int64: torch.int64, np.float32: torch.float32}
 _NP_DTYPE = {torch.uint8: np.uint8, torch.int32: np.int32, torch.int64: np.int64, torch.float32: np.float32,
              torch.float64: np.float64, torch.bool: np.bool_}
@@ -1081,7 +1115,7 @@ class HybridGrid:
             import torch.distributed as dist
             lo, hi = shard_range(c.shape[0], dist.get_rank(group), _world(group))
             c = c[lo:hi]
-        d = torch.from_numpy(np.ascontiguousarray(c)).to(self.model.dev)
+        d = _to_device(c, self.model.dev)
         # int32 input: the +-2^30 range check runs on the device, read with the results
         bad = ((d >= lim) | (d <= -lim)).any().view(1).to(torch.uint8)
         v, a = self.query_device(d)

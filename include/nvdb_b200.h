@@ -138,7 +138,9 @@ typedef struct {
 
 /* The fused evaluator behind every decode stage (decoder.py:110-196) and
  * the blended seams: point ids 0..n-1 (source id gather[i] when gather is
- * non-null), outputs written at index i.  Workspace: nvdb_eval_workspace_bytes. */
+ * non-null), outputs written at index i.  Workspace: nvdb_eval_workspace_bytes.
+ * Calls above 2^30 points run as consecutive 2^30-point chunks (the workspace
+ * covers one chunk); the counted form below takes at most 2^30 points. */
 NVDB_API int nvdb_eval(const nvdb_netset* ns, int32_t tag, int32_t src_kind, const void* src,
                        const int64_t* gather, int64_t n, const nvdb_eval_out* out, void* workspace,
                        size_t workspace_bytes, void* stream);

@@ -565,12 +565,31 @@ def run_concurrent(trainers: List["DeviceTrainer"], width: int = 2) -> List[Tupl
     latency-bound per tile: two nets' epochs
     interleaved on the SMs overlap one net's weight-gradient / Adam tail and
     launch gaps with the other's fwd/dgrad (C2 l0 + voxel, 800 epochs: 169.7
-    -> 148.9 ms).  Three at once was measured slower on the ACCEPT nets (the
-    tile images of three nets no longer stay in L2).  The largest nets start
-    first; a finished net's stream takes the next one.  Data-parallel
-    trainers (a process group) run one after another."""
+    -> 148.9 ms).  Nets pair up by epoch shape (an expert's l0 and voxel
+    nets); three at once, or the full-batch l1 net beside an l0 net, was
+    measured slower or unstable.  Data-parallel trainers (a process group)
+    run one after another."""
     if len(trainers) <= 1 or width <= 1 or any(t.group is not None for t in trainers):
         return [t.run() for t in trainers]
+    # nets of the same epoch shape (the l0 and voxel nets of an expert) pair
+    # up; a net without a partner runs alone on the whole GPU (pairing the
+    # full-batch l1 net with an l0 net ran 186-275 ms run to run on C2
+    # against 180 for l1 alone then l0 + voxel)
+    shapes: Dict[float, List[int]] = {}
+    for i, t in enumerate(trainers):
+        shapes.setdefault(t.epoch_work(), []).append(i)
+    res: List[Optional[Tuple[float, int]]] = [None] * len(trainers)
+    for idx in sorted(shapes.values(), key=len):
+        if len(idx) == 1:
+            res[idx[0]] = trainers[idx[0]].run()
+        else:
+            for i, r in zip(idx, _run_streams([trainers[i] for i in idx], width)):
+                res[i] = r
+    return res
+
+
+def _run_streams(trainers: List["DeviceTrainer"], width: int) -> List[Tuple[float, int]]:
+    """run_concurrent's stream schedule: ``width`` trainers at a time."""
     dev = trainers[0].dev
     cur = torch.cuda.current_stream(dev)
     pool = _TRAIN_STREAMS.setdefault(dev.index if dev.index is not None else torch.cuda.current_device(), [])
